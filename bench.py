@@ -1,0 +1,385 @@
+"""Benchmark: image pairs/s of the B200 generator (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = one batch of synthetic PIV image pairs generated on the GPU by the
+fused kernel (Philox seeding, bilinear advection, distributed binning, splat,
+finalize) -- workload C2 (256x256, B=256 per GPU, Lamb-Oseen vortex flow,
+reference defaults: ppp 0.06, d in [0.8, 1.2], I0 = 1, rho = 0). Multi-GPU:
+one process per GPU (torchrun), each rank renders B=256 pairs of a global
+batch of 256*N (weak scaling), no data-path collective; time = max over ranks.
+
+`value` is device-timed (CUDA events around each step on the launching
+stream, L2 flushed between steps), `e2e` goes through the C ABI with HOST
+buffers (flow uploaded, images copied back each step). `--impl reference`
+times the reference CPU implementation (oracle/_ref = /root/reference/pkg
+compiled here) on the host cores with all threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "image pairs/sec at 256x256, B=256 on 1/2/4/8 B200; % of HBM/SFU roofline"
+
+CONFIGS = {
+    # name: (H, W, B per GPU, ppp, d_range, flow, extra)
+    "c1": (256, 256, 1, (0.06, 0.06), (0.8, 1.2), "uniform", {}),
+    "c2": (256, 256, 256, (0.06, 0.06), (0.8, 1.2), "vortex", {}),
+    "c3": (1024, 1024, 64, (0.1, 0.1), (1.0, 4.0), "vortex", {}),
+    "c4": (512, 512, 256, (0.06, 0.06), (0.8, 1.2), "vortex",
+           dict(noise=(0.05, 0.02), hide_probability=0.05,
+                laser_sheet=dict(thickness=1.0, shape=2.0, efficiency=1.0, out_of_plane=0.1))),
+    "c5": (256, 256, 8192, (0.06, 0.06), (0.8, 1.2), "vortex", {}),
+}
+
+
+def vortex(h, w, scale=2.0):
+    def fn(x, y):
+        cx, cy = (w - 1) / 2.0, (h - 1) / 2.0
+        rc = 0.1 * w
+        dx, dy = x - cx, y - cy
+        r = np.sqrt(dx * dx + dy * dy) + 1e-12
+        vt = 1.398 * scale * (rc / r) * (1.0 - np.exp(-(r / rc) ** 2))
+        return -vt * dy / r, vt * dx / r
+    return fn
+
+
+def uniform(x, y):
+    return 2.0 + 0.0 * x, -1.0 + 0.0 * y
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_cfg(pg, name, per_gpu_batch):
+    H, W, B, ppp, dr, flow, extra = CONFIGS[name]
+    kw = dict(image_height=H, image_width=W, batch_size=per_gpu_batch, seeding_density_range=ppp,
+              diameter_range=dr, seed=0, flow_sources=(pg.FlowSource(function=f"bench_{flow}"),))
+    if "noise" in extra:
+        kw["noise"] = pg.NoiseConfig(*extra["noise"])
+    if "hide_probability" in extra:
+        kw["hide_probability"] = extra["hide_probability"]
+    if "laser_sheet" in extra:
+        kw["laser_sheet"] = pg.LaserSheetConfig(**extra["laser_sheet"])
+    return pg.GeneratorConfig(**kw)
+
+
+def ref_cfg(name, batch, threads):
+    from oracle import reference
+
+    pv = reference.load()
+    H, W, B, ppp, dr, flow, extra = CONFIGS[name]
+    pv.register_flow_function(f"bench_{flow}", vortex(H, W) if flow == "vortex" else uniform)
+    kw = dict(image_height=H, image_width=W, batch_size=batch, seeding_density_range=ppp,
+              diameter_range=dr, seed=0, threads=threads,
+              flow_sources=(pv.FlowSource(function=f"bench_{flow}"),))
+    if "noise" in extra:
+        kw["noise"] = pv.NoiseConfig(*extra["noise"])
+    if "hide_probability" in extra:
+        kw["hide_probability"] = extra["hide_probability"]
+        kw["frame2_intensity_std"] = 0.05    # stand-in for the laser sheet (no z in the reference)
+    return pv, pv.GeneratorConfig(**kw)
+
+
+def cpu_baseline(name: str, budget_s: float = 15.0):
+    """Reference CPU path (oracle/_ref, native Cython kernel) on the host cores."""
+    threads = os.cpu_count() or 1
+    pv, cfg = ref_cfg(name, min(CONFIGS[name][2], 256), threads)
+    from pivgen.pipeline import Sampler
+
+    pairs = 0
+    t_total = 0.0
+    with Sampler(cfg) as s:
+        s.next_batch()                         # warm-up (thread pool, page-in)
+        while t_total < budget_s:
+            t0 = time.perf_counter()
+            s.next_batch()
+            t_total += time.perf_counter() - t0
+            pairs += cfg.batch_size
+    return {"value": pairs / t_total, "unit": "pairs/s", "cores": threads, "kind": "reference",
+            "sample": f"{pairs} pairs of {name} ({cfg.image_height}x{cfg.image_width}, "
+                      f"B={cfg.batch_size}) via pivgen Sampler.next_batch, threads={threads}, "
+                      f"backend={pv.active_backend()}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    name = args.config
+    threads = os.cpu_count() or 1
+    pv, cfg = ref_cfg(name, min(CONFIGS[name][2], 256), threads)
+    from pivgen.pipeline import Sampler
+
+    times = []
+    with Sampler(cfg) as s:
+        for _ in range(args.warmup):
+            s.next_batch()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            s.next_batch()
+            times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = cfg.batch_size * len(times) / total
+    H, W = cfg.image_height, cfg.image_width
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64/f32 (CPU)", "data": "synthetic (Lamb-Oseen vortex flow)",
+        "config": {"workload": f"{name}: {H}x{W}, B={cfg.batch_size} per step (CPU reference)",
+                   "global_batch": cfg.batch_size, "image": [H, W], "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} steps x {cfg.batch_size} pairs, pivgen "
+                                   f"{pv.__version__} backend={pv.active_backend()}"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2512_09664_b200 as pg
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    name = args.config
+    H, W, Bcfg, *_ = CONFIGS[name]
+    per_gpu = Bcfg if name != "c5" else Bcfg // world
+    global_batch = per_gpu * world if name != "c5" else Bcfg
+    pg.register_flow_function("bench_vortex", vortex(H, W))
+    pg.register_flow_function("bench_uniform", uniform)
+    cfg = make_cfg(pg, name, global_batch)
+    lib = _lib.load()
+    ncfg = native_config(cfg)
+    field = pg.from_function(vortex(H, W) if CONFIGS[name][5] == "vortex" else uniform, H, W)
+    flows = field.to_device(dev).unsqueeze(0).contiguous()
+    u16 = False
+    img1 = torch.empty((per_gpu, H, W), dtype=torch.float32, device=dev)
+    img2 = torch.empty_like(img1)
+    stats = {"seeding_density": torch.empty(per_gpu, dtype=torch.float64, device=dev),
+             "active_count": torch.empty(per_gpu, dtype=torch.int32, device=dev),
+             "side": torch.empty(per_gpu, dtype=torch.int32, device=dev),
+             "d_max": torch.empty(per_gpu, dtype=torch.float32, device=dev)}
+    st = _lib.PgbPairStats(**{k: v.data_ptr() for k, v in stats.items()})
+    pair_base = rank * per_gpu
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(batch_index):
+        _lib.check(lib.pgb_generate_batch_dev(ncfg, batch_index, pair_base, per_gpu, flows.data_ptr(),
+                                              1, global_batch, _lib.OUT_U16 if u16 else _lib.OUT_F32,
+                                              img1.data_ptr(), img2.data_ptr(), st, None,
+                                              stream.cuda_stream))
+
+    for w in range(args.warmup):
+        step(w)
+    torch.cuda.synchronize()
+    lib.pgb_overflow_reset()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = lib.pgb_launch_count()
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()                          # L2 flush between timed steps (not timed)
+            starts[k].record(stream)
+            step(args.warmup + k)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t_wall = time.perf_counter() - t_wall
+    launches = lib.pgb_launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ovf = lib.pgb_overflow_count()
+    value = global_batch * args.steps / (total_ms / 1000.0)
+
+    # ---- end to end through the C ABI with HOST buffers (rank-local) ----------
+    host_flow = torch.from_numpy(field.interleaved()).pin_memory()
+    h1 = torch.empty((per_gpu, H, W), dtype=torch.float32).pin_memory()
+    h2 = torch.empty_like(h1).pin_memory()
+    hst = {"seeding_density": np.empty(per_gpu, np.float64), "active_count": np.empty(per_gpu, np.int32),
+           "side": np.empty(per_gpu, np.int32), "d_max": np.empty(per_gpu, np.float32)}
+    hs = _lib.PgbPairStats(**{k: v.ctypes.data for k, v in hst.items()})
+
+    def e2e_step(b):
+        _lib.check(lib.pgb_generate_batch(ncfg, b, pair_base, per_gpu, host_flow.data_ptr(), 1,
+                                          global_batch, _lib.OUT_F32, h1.data_ptr(), h2.data_ptr(), hs))
+
+    e2e_steps = max(2, min(args.steps, 10))
+    e2e_step(0)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        e2e_step(1 + k)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = global_batch * e2e_steps / e2e_s
+    h2d = host_flow.numel() * 4
+    d2h = 2 * per_gpu * H * W * 4 + per_gpu * (8 + 4 + 4 + 4)
+
+    if rank == 0:
+        peak, peak_kind = load_peaks()
+        bytes_per_launch = 2 * per_gpu * H * W * 4
+        kernel_s = (total_ms / 1000.0) / args.steps
+        achieved = bytes_per_launch / kernel_s / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                with open(tp) as fh:
+                    tj = json.load(fh)
+                traffic = tj.get(name)
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Lamb-Oseen vortex flow; Philox-seeded particles)",
+            "config": {"workload": f"{name}: {H}x{W}, B={per_gpu} pairs per GPU, ppp 0.06, d in [0.8,1.2]",
+                       "global_batch": global_batch, "seq_len": None, "image": [H, W],
+                       "parallelism": f"dp{world} (pairs sharded, no collective)",
+                       "l2": "flushed between steps (256 MiB write, untimed); per-step CUDA events summed",
+                       "output": "float32 images1+images2 in HBM"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "kernel": "pgb::fused_generate_kernel", "peak_source": peak_kind},
+            "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "pgb_generate_batch (C ABI, host buffers: flow H2D + images D2H, pinned)"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "wall_s_timed_region": t_wall,
+            "overflow_events": int(ovf),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(name if name != "c5" else "c2")
+            except Exception as exc:  # pragma: no cover - reference missing on the box
+                line["cpu_baseline"] = {"value": None, "unavailable": str(exc)}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,789 @@
+// pivgen_b200.cu -- kernels + C ABI of libpivgen_b200.so (see include/pivgen_b200.h).
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -cudart static
+//        -shared -Xcompiler -fPIC (driven by paper_2512_09664_b200/build.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/pivgen_b200.h"
+#include "common.cuh"
+#include "fused.cuh"
+
+namespace pgb {
+
+// ----------------------------------------------------------------------------
+// Small standalone kernels (oracle-mode helpers; the generator itself is the
+// fused cluster kernel in fused.cuh).
+// ----------------------------------------------------------------------------
+
+// advect (particles.py:129-136) / sample_flow (flowfield.py:207-232), float64.
+__global__ void advect_kernel(const double* __restrict__ pos, long long n,
+                              const float2* __restrict__ flow, int H, int W,
+                              double* __restrict__ out, int add_position) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double x = pos[2 * i], y = pos[2 * i + 1];
+    double u, v;
+    sample_flow_exact(flow, H, W, x, y, &u, &v);
+    out[2 * i] = add_position ? dadd(x, u) : u;
+    out[2 * i + 1] = add_position ? dadd(y, v) : v;
+  }
+}
+
+// finalize (raster.py:154-161) with the same Philox noise as the fused epilogue.
+__global__ void finalize_kernel(const float* __restrict__ raw, int pairs, long long hw,
+                                float bg, float sd, uint32_t k0, uint32_t k1, uint32_t batch,
+                                long long pair_base, int frame, int mode, void* out) {
+  const long long quads = (hw + 3) >> 2;
+  const long long total = quads * pairs;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long pl = e / quads;
+    const long long q = e - pl * quads;
+    float4 nz = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sd > 0.f) nz = noise4(k0, k1, (uint32_t)(pair_base + pl), batch, (uint32_t)frame, (uint32_t)q);
+    const float nzs[4] = {nz.x, nz.y, nz.z, nz.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long long p = q * 4 + j;
+      if (p >= hw) break;
+      const float v = finalize_px(raw[pl * hw + p], bg, sd, nzs[j]);
+      if (mode == kOutU16) static_cast<uint16_t*>(out)[pl * hw + p] = quant_u16(v);
+      else static_cast<float*>(out)[pl * hw + p] = v;
+    }
+  }
+}
+
+__global__ void quantize_kernel(const float* __restrict__ img, long long n, uint16_t* out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = quant_u16(img[i]);
+}
+
+// Particle arrays of the generator (one block per pair). Same make_particle as
+// the fused kernel, so these arrays are exactly what the fused kernel renders.
+__global__ void sample_particles_kernel(FusedParams P, pgb_particle_out O) {
+  const int pl = blockIdx.x;
+  __shared__ int sM;
+  __shared__ unsigned sdmax;
+  __shared__ double sppp;
+  if (threadIdx.x == 0) {
+    const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
+    const uint4 w = draw(key, 0u, kTagPair);
+    const double ppp = lerp_exact(P.g.ppp_lo, P.g.ppp_hi, u53_to_unit(w.x, w.y));
+    double m = rint(dmul(dmul(ppp, (double)P.g.H), (double)P.g.W));
+    m = fmin(fmax(m, 0.0), (double)P.n);
+    sM = (int)m;
+    sppp = ppp;
+    sdmax = 0u;
+  }
+  __syncthreads();
+  const int M = sM;
+  unsigned dm = 0u;
+  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
+    Particle pt;
+    make_particle<0>(P, pl, i, M, pt);
+    const size_t o = (size_t)pl * P.n + i;
+    // recompute the frame-independent draws the Particle struct does not carry
+    const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
+    bool vis1 = true, vis2 = true;
+    double z1 = 0.0;
+    if (P.g.need_b) {
+      const uint4 b = draw(key, (uint32_t)i, kTagParticleB);
+      vis1 = u32_to_unit(b.y) >= P.g.hide_p;
+      vis2 = u32_to_unit(b.z) >= P.g.hide_p;
+      z1 = lerp_exact(P.g.z_lo, P.g.z_hi, u32_to_unit(b.w));
+    }
+    if (O.pos1) { O.pos1[2 * o] = pt.x[0]; O.pos1[2 * o + 1] = pt.y[0]; }
+    if (O.pos2) { O.pos2[2 * o] = pt.x[1]; O.pos2[2 * o + 1] = pt.y[1]; }
+    if (O.i0_1) O.i0_1[o] = pt.amp[0];
+    if (O.sx_1) O.sx_1[o] = pt.sx[0];
+    if (O.sy_1) O.sy_1[o] = pt.sy[0];
+    if (O.rho_1) O.rho_1[o] = pt.rho[0];
+    if (O.i0_2) O.i0_2[o] = pt.amp[1];
+    if (O.sx_2) O.sx_2[o] = pt.sx[1];
+    if (O.sy_2) O.sy_2[o] = pt.sy[1];
+    if (O.rho_2) O.rho_2[o] = pt.rho[1];
+    if (O.diameter) O.diameter[o] = pt.diam;
+    if (O.z1) O.z1[o] = (float)z1;
+    if (O.active) O.active[o] = pt.active ? 1 : 0;
+    if (O.visible1) O.visible1[o] = (vis1 && pt.active) ? 1 : 0;
+    if (O.visible2) O.visible2[o] = (vis2 && pt.active) ? 1 : 0;
+    if (pt.active) dm = max(dm, __float_as_uint(pt.diam));
+  }
+  atomicMax(&sdmax, dm);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float dmax = M > 0 ? __uint_as_float(sdmax) : (float)P.g.d_hi;
+    if (P.st_ppp) P.st_ppp[pl] = sppp;
+    if (P.st_M) P.st_M[pl] = M;
+    if (P.st_dmax) P.st_dmax[pl] = dmax;
+    if (P.st_side) P.st_side[pl] = patch_side_exact((double)dmax, P.g.patch_mult);
+  }
+}
+
+// perturb_frame2 (particles.py:104-126) on caller arrays, same draws as the
+// fused kernel (stream kTagPerturb, particle index i).
+__global__ void perturb_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, uint32_t batch,
+                               float sd_sigma, float sd_i0, float sd_rho, const float* i0_1,
+                               const float* sx_1, const float* sy_1, const float* rho_1,
+                               float* i0_2, float* sx_2, float* sy_2, float* rho_2) {
+  const RngKey key{k0, k1, gpair, batch};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint4 c = draw(key, (uint32_t)i, kTagPerturb);
+    const float2 n01 = box_muller(c.x, c.y);
+    const float2 n23 = box_muller(c.z, c.w);
+    float sx = sx_1[i], sy = sy_1[i], a = i0_1[i], r = rho_1[i];
+    if (sd_sigma > 0.f) {
+      sx = (float)fmax((double)sx + (double)sd_sigma * (double)n01.x, 1e-3);
+      sy = (float)fmax((double)sy + (double)sd_sigma * (double)n01.y, 1e-3);
+    }
+    if (sd_i0 > 0.f) {
+      const double t = fmin(fmax((double)a + (double)sd_i0 * (double)n23.x, 0.0), 1.0);
+      a = a == 0.f ? 0.f : (float)t;
+    }
+    if (sd_rho > 0.f) {
+      const double lim = 1.0 - 1e-3;
+      r = (float)fmin(fmax((double)r + (double)sd_rho * (double)n23.y, -lim), lim);
+    }
+    sx_2[i] = sx; sy_2[i] = sy; i0_2[i] = a; rho_2[i] = r;
+  }
+}
+
+// apply_hiding (particles.py:139-147): visible_k = U_k >= p & active.
+__global__ void hiding_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, uint32_t batch,
+                              double p_hide, const uint8_t* active, uint8_t* vis1, uint8_t* vis2) {
+  const RngKey key{k0, k1, gpair, batch};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint4 b = draw(key, (uint32_t)i, kTagParticleB);
+    const bool a = active[i] != 0;
+    vis1[i] = (a && u32_to_unit(b.y) >= p_hide) ? 1 : 0;
+    vis2[i] = (a && u32_to_unit(b.z) >= p_hide) ? 1 : 0;
+  }
+}
+
+template __global__ void fused_generate_kernel<0, kPsfPoint>(const FusedParams);
+template __global__ void fused_generate_kernel<0, kPsfErf>(const FusedParams);
+template __global__ void fused_generate_kernel<1, kPsfPoint>(const FusedParams);
+template __global__ void fused_generate_kernel<1, kPsfErf>(const FusedParams);
+
+// ----------------------------------------------------------------------------
+// Host side: errors, workspace, plan, launch
+// ----------------------------------------------------------------------------
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+struct Error {
+  std::string msg;
+};
+
+#define PGB_CK(call)                                                                  \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw Error{std::string(#call) + " failed: " + cudaGetErrorString(e_)};        \
+  } while (0)
+
+#define PGB_REQUIRE(cond, msg)         \
+  do {                                 \
+    if (!(cond)) throw Error{(msg)};   \
+  } while (0)
+
+struct Plan {
+  int TH, TW, tiles_y, tiles_x, tiles, CL, passes, cap, spill_cap, halo, cells_cap;
+  size_t smem;
+};
+
+constexpr size_t kSmemTarget = 110 * 1024;  // two CTAs per SM
+constexpr size_t kSmemMax = 220 * 1024;
+
+Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, int cl_max) {
+  Plan p{};
+  p.halo = halo;
+  p.TW = W <= 256 ? W : 256;
+  p.TH = std::max(1, std::min(rows, 8192 / std::max(1, p.TW)));
+  for (;;) {
+    const double ext = (double)std::min(p.TH + 2 * halo, rows + 2 * halo) *
+                       (double)std::min(p.TW + 2 * halo, W + 2 * halo);
+    const double lam = std::min((double)n, (double)n * ext / ((double)H_full * (double)W));
+    long long cap = (long long)std::ceil(lam + 6.0 * std::sqrt(lam) + 32.0);
+    cap = std::min<long long>(cap, std::max<long long>(n, 1));
+    cap = (cap + 7) / 8 * 8;
+    p.cap = (int)cap;
+    p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
+                  ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
+    p.smem = (size_t)p.TH * p.TW * 4 + (size_t)nframes * p.cap * sizeof(Cand) +
+             sizeof(SharedHdr) + (size_t)p.cells_cap * 4;
+    if (p.smem <= kSmemTarget) break;
+    if (p.TH > 1) p.TH = (p.TH + 1) / 2;
+    else if (p.TW > 4) p.TW = ((p.TW / 2) + 3) / 4 * 4;
+    else break;
+  }
+  PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
+  p.tiles_y = (rows + p.TH - 1) / p.TH;
+  p.tiles_x = (W + p.TW - 1) / p.TW;
+  p.tiles = p.tiles_y * p.tiles_x;
+  p.CL = std::max(1, std::min(p.tiles, cl_max));
+  p.passes = (p.tiles + p.CL - 1) / p.CL;
+  p.spill_cap = std::max(256, 2 * p.cap);
+  return p;
+}
+
+struct DevWork {
+  void* spill = nullptr;
+  size_t spill_bytes = 0;
+  int* overflow = nullptr;
+  // host-API staging
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+std::recursive_mutex g_mu;
+std::map<int, DevWork> g_work;
+
+DevWork& work_for_current() {
+  int dev = 0;
+  PGB_CK(cudaGetDevice(&dev));
+  DevWork& w = g_work[dev];
+  if (!w.overflow) {
+    PGB_CK(cudaMalloc(&w.overflow, sizeof(int)));
+    PGB_CK(cudaMemset(w.overflow, 0, sizeof(int)));
+  }
+  return w;
+}
+
+void* ensure(void*& buf, size_t& have, size_t need) {
+  if (need > have) {
+    if (buf) PGB_CK(cudaFree(buf));
+    buf = nullptr;
+    PGB_CK(cudaMalloc(&buf, need));
+    have = need;
+  }
+  return buf;
+}
+
+using KernelFn = void (*)(const FusedParams);
+
+KernelFn pick_kernel(int mode, int psf) {
+  if (mode == 0) return psf == kPsfErf ? fused_generate_kernel<0, kPsfErf> : fused_generate_kernel<0, kPsfPoint>;
+  return psf == kPsfErf ? fused_generate_kernel<1, kPsfErf> : fused_generate_kernel<1, kPsfPoint>;
+}
+
+int max_active_clusters(KernelFn fn, int CL, size_t smem) {
+  static std::map<std::tuple<void*, int, size_t, int>, int> cache;
+  int dev = 0;
+  PGB_CK(cudaGetDevice(&dev));
+  auto key = std::make_tuple((void*)fn, CL, smem, dev);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (CL > 8) PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CL * 64);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int num = 0;
+  PGB_CK(cudaOccupancyMaxActiveClusters(&num, (const void*)fn, &cfg));
+  PGB_REQUIRE(num > 0, "cluster configuration cannot be scheduled");
+  cache[key] = num;
+  return num;
+}
+
+void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
+  KernelFn fn = pick_kernel(P.mode, P.psf);
+  P.TH = pl.TH; P.TW = pl.TW; P.tiles_y = pl.tiles_y; P.tiles_x = pl.tiles_x; P.tiles = pl.tiles;
+  P.CL = pl.CL; P.passes = pl.passes; P.cap = pl.cap; P.spill_cap = pl.spill_cap;
+  P.halo = pl.halo; P.cells_cap = pl.cells_cap;
+  const int items = P.pairs * P.passes;
+  if (items <= 0) return;
+  const int maxc = max_active_clusters(fn, pl.CL, pl.smem);
+  const int nclusters = std::min(items, maxc);
+  DevWork& w = work_for_current();
+  const size_t spill_need = (size_t)nclusters * pl.CL * 2 * pl.spill_cap * sizeof(Cand);
+  P.spill = static_cast<Cand*>(ensure(w.spill, w.spill_bytes, spill_need));
+  P.overflow = w.overflow;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nclusters * pl.CL);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pl.CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PGB_CK(cudaLaunchKernelEx(&cfg, fn, P));
+  g_launches.fetch_add(1);
+}
+
+int grid_for(long long n, int block) {
+  long long g = (n + block - 1) / block;
+  return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 16));
+}
+
+GenCfg gen_cfg_from(const pgb_config* c) {
+  GenCfg g{};
+  g.H = c->height;
+  g.W = c->width;
+  g.n = c->n_capacity;
+  g.k0 = (uint32_t)(c->seed & 0xffffffffu);
+  g.k1 = (uint32_t)(c->seed >> 32);
+  g.ppp_lo = c->ppp_lo; g.ppp_hi = c->ppp_hi;
+  g.d_lo = c->d_lo; g.d_hi = c->d_hi;
+  g.i0_lo = c->i0_lo; g.i0_hi = c->i0_hi;
+  g.rho_lo = c->rho_lo; g.rho_hi = c->rho_hi;
+  g.sigma_ratio = c->sigma_ratio;
+  g.patch_mult = c->patch_multiplier;
+  g.hide_p = c->hide_probability;
+  g.z_lo = c->laser_z_lo; g.z_hi = c->laser_z_hi;
+  g.f2_sigma_std = (float)c->f2_sigma_std;
+  g.f2_rho_std = (float)c->f2_rho_std;
+  g.f2_i0_std = (float)c->f2_i0_std;
+  g.dz0 = (float)c->laser_dz0;
+  g.shape = (float)c->laser_shape;
+  g.q = (float)c->laser_q;
+  g.w = (float)c->laser_w;
+  g.laser = c->laser_enabled ? 1 : 0;
+  g.need_b = (c->rho_hi != c->rho_lo) || (c->hide_probability > 0.0) || g.laser;
+  g.need_perturb = (c->f2_sigma_std > 0.0) || (c->f2_rho_std > 0.0) || (c->f2_i0_std > 0.0);
+  return g;
+}
+
+void validate_cfg(const pgb_config* c) {
+  PGB_REQUIRE(c != nullptr, "config is NULL");
+  PGB_REQUIRE(c->height > 0 && c->width > 0, "image size must be positive");
+  PGB_REQUIRE(c->height < 30000 && c->width < 30000, "image side must be < 30000");
+  PGB_REQUIRE(c->n_capacity >= 1, "n_capacity must be >= 1");
+  PGB_REQUIRE(c->psf == PGB_PSF_POINT || c->psf == PGB_PSF_ERF, "unknown psf");
+  PGB_REQUIRE(c->sigma_ratio > 0 && c->patch_multiplier > 0, "ratio/multiplier must be > 0");
+  PGB_REQUIRE(c->i0_hi <= 1.0 && c->i0_lo >= 0.0, "peak intensity range must lie in [0, 1]");
+  PGB_REQUIRE(!c->laser_enabled || (c->laser_q > 0 && c->laser_q <= 1.0 && c->laser_dz0 > 0),
+              "laser sheet: need 0 < q <= 1 and dz0 > 0");
+}
+
+FusedParams base_params(int H, int W) {
+  FusedParams P{};
+  P.H = H;
+  P.W = W;
+  P.row_lo = 0;
+  P.row_hi = H;
+  P.out_pair_elems = (long long)H * W;
+  P.pairs_per_field = 1;
+  return P;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  std::lock_guard<std::recursive_mutex> lock(g_mu);
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.msg;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  } catch (...) {
+    g_err = "unknown error";
+  }
+  return 1;
+}
+
+void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
+                       const float* flows, int num_fields, int pairs_per_field, int out_mode,
+                       void* img1, void* img2, const pgb_pair_stats* stats, int32_t* bin_counts,
+                       cudaStream_t stream) {
+  validate_cfg(cfg);
+  PGB_REQUIRE(pairs >= 0, "pairs must be >= 0");
+  PGB_REQUIRE(flows != nullptr && num_fields >= 1 && pairs_per_field >= 1, "flows required");
+  PGB_REQUIRE(out_mode == PGB_OUT_RAW || out_mode == PGB_OUT_FINAL_F32 || out_mode == PGB_OUT_FINAL_U16,
+              "out_mode must be RAW, FINAL_F32 or FINAL_U16");
+  PGB_REQUIRE(img1 && img2, "output buffers required");
+  PGB_REQUIRE(batch < (1ull << 32), "batch index must be < 2^32");
+  PGB_REQUIRE((int64_t)(pair_base + pairs) <= (int64_t)num_fields * pairs_per_field,
+              "pair range exceeds the flow window (num_fields * pairs_per_field)");
+  const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
+  FusedParams P = base_params(cfg->height, cfg->width);
+  P.n = cfg->n_capacity;
+  P.pairs = pairs;
+  P.pair_base = pair_base;
+  P.batch_lo = (uint32_t)batch;
+  P.psf = cfg->psf;
+  P.out_mode = out_mode;
+  P.bg_offset = (float)cfg->bg_offset;
+  P.noise_std = (float)cfg->noise_std;
+  P.mode = 0;
+  P.nframes = 2;
+  P.g = gen_cfg_from(cfg);
+  P.flows = reinterpret_cast<const float2*>(flows);
+  P.num_fields = num_fields;
+  P.pairs_per_field = pairs_per_field;
+  P.field_elems = (long long)cfg->height * cfg->width;
+  P.out[0] = img1;
+  P.out[1] = img2;
+  if (stats) {
+    P.st_ppp = stats->seeding_density;
+    P.st_M = stats->active_count;
+    P.st_side = stats->side;
+    P.st_dmax = stats->d_max;
+  }
+  P.bin_counts = bin_counts;
+  const Plan pl = make_plan(cfg->height, cfg->height, cfg->width, cfg->n_capacity, halo, 2, 8);
+  launch_fused(P, pl, stream);
+}
+
+}  // namespace pgb
+
+using namespace pgb;
+
+extern "C" {
+
+int pgb_abi_version(void) { return PGB_ABI_VERSION; }
+
+const char* pgb_last_error(void) { return g_err.c_str(); }
+
+int pgb_patch_side(double max_diameter, double multiplier) {
+  return patch_side_exact(max_diameter, multiplier);
+}
+
+int64_t pgb_launch_count(void) { return g_launches.load(); }
+
+int pgb_plan(int height, int width, int64_t n_per_pair, double ppp_hi, int halo, int frames,
+             pgb_plan_info* info) {
+  (void)ppp_hi;
+  return guarded([&] {
+    PGB_REQUIRE(info != nullptr, "info is NULL");
+    const Plan p = make_plan(height, height, width, n_per_pair, halo, frames, 8);
+    info->tile_h = p.TH; info->tile_w = p.TW; info->tiles_y = p.tiles_y; info->tiles_x = p.tiles_x;
+    info->cluster = p.CL; info->passes = p.passes; info->capacity = p.cap; info->halo = p.halo;
+    info->smem_bytes = (int)p.smem; info->threads = kThreads;
+  });
+}
+
+int pgb_splat_accumulate_dev(const double* pos, const float* i0, const float* sigma_x,
+                             const float* sigma_y, const float* rho, const unsigned char* mask,
+                             int64_t n, int side, float* out, int height, int width,
+                             int row_start, int row_stop, int psf, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(height > 0 && width > 0 && height < 30000 && width < 30000, "bad image size");
+    PGB_REQUIRE(side >= 1, "side must be >= 1");
+    PGB_REQUIRE(n >= 0 && n < (1LL << 31), "bad particle count");
+    row_start = std::max(0, row_start);
+    row_stop = std::min(height, row_stop);
+    if (n == 0 || row_stop <= row_start) return;
+    FusedParams P = base_params(height, width);
+    P.row_lo = row_start;
+    P.row_hi = row_stop;
+    P.n = (int)n;
+    P.pairs = 1;
+    P.psf = psf;
+    P.out_mode = kOutAccum;
+    P.mode = 1;
+    P.nframes = 1;
+    P.inj[0] = InjFrame{pos, i0, sigma_x, sigma_y, rho, mask};
+    int* side_dev = nullptr;
+    DevWork& w = work_for_current();
+    // side lives in the staging buffer head (4 bytes)
+    ensure(w.stage, w.stage_bytes, 256);
+    side_dev = static_cast<int*>(w.stage);
+    PGB_CK(cudaMemcpyAsync(side_dev, &side, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    P.side_in = side_dev;
+    P.out[0] = out;
+    const Plan pl = make_plan(height, row_stop - row_start, width, n, side / 2, 1, 8);
+    launch_fused(P, pl, (cudaStream_t)stream);
+    PGB_CK(cudaGetLastError());
+    // the side staging slot is reused: keep the host value alive until the copy ran
+    PGB_CK(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int pgb_splat_accumulate(const double* pos, const float* i0, const float* sigma_x,
+                         const float* sigma_y, const float* rho, const unsigned char* mask,
+                         int64_t n, int side, float* out, int height, int width, int row_start,
+                         int row_stop) {
+  return guarded([&] {
+    PGB_REQUIRE(height > 0 && width > 0, "bad image size");
+    const size_t np = (size_t)n;
+    const size_t hw = (size_t)height * width;
+    const size_t bytes = np * 16 + np * 4 * 4 + np + hw * 4 + 1024;
+    std::vector<char> dummy;
+    void* buf = nullptr;
+    PGB_CK(cudaMalloc(&buf, bytes));
+    char* b = static_cast<char*>(buf);
+    double* d_pos = reinterpret_cast<double*>(b); b += np * 16;
+    float* d_i0 = reinterpret_cast<float*>(b); b += np * 4;
+    float* d_sx = reinterpret_cast<float*>(b); b += np * 4;
+    float* d_sy = reinterpret_cast<float*>(b); b += np * 4;
+    float* d_rho = reinterpret_cast<float*>(b); b += np * 4;
+    float* d_out = reinterpret_cast<float*>(b); b += hw * 4;
+    unsigned char* d_mask = reinterpret_cast<unsigned char*>(b);
+    auto fail = [&](const std::string& m) { cudaFree(buf); throw Error{m}; };
+    if (cudaMemcpy(d_pos, pos, np * 16, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_i0, i0, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_sx, sigma_x, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_sy, sigma_y, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_rho, rho, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_mask, mask, np, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_out, out, hw * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      fail("host->device copy failed");
+    if (pgb_splat_accumulate_dev(d_pos, d_i0, d_sx, d_sy, d_rho, d_mask, n, side, d_out, height,
+                                 width, row_start, row_stop, PGB_PSF_POINT, nullptr) != 0)
+      fail(g_err);
+    if (cudaMemcpy(out, d_out, hw * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+      fail("device->host copy failed");
+    cudaFree(buf);
+  });
+}
+
+int pgb_render_pairs_dev(const pgb_particles* frame1, const pgb_particles* frame2,
+                         int64_t n_per_pair, int pairs, const int* side_per_pair, int height,
+                         int width, int psf, int out_mode, double bg_offset, double noise_std,
+                         uint64_t seed, uint64_t batch, int64_t pair_base, void* out1, void* out2,
+                         int32_t* bin_counts, int* tiles_out, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(frame1 && frame2 && side_per_pair, "frame1/frame2/side_per_pair required");
+    PGB_REQUIRE(height > 0 && width > 0 && height < 30000 && width < 30000, "bad image size");
+    PGB_REQUIRE(out_mode == PGB_OUT_RAW || out_mode == PGB_OUT_FINAL_F32 || out_mode == PGB_OUT_FINAL_U16,
+                "out_mode must be RAW, FINAL_F32 or FINAL_U16");
+    PGB_REQUIRE(n_per_pair >= 1 && n_per_pair < (1LL << 31), "bad particle count");
+    PGB_REQUIRE(pairs >= 0, "pairs must be >= 0");
+    if (pairs == 0) return;
+    int smax = 1;
+    for (int i = 0; i < pairs; ++i) {
+      PGB_REQUIRE(side_per_pair[i] >= 1, "side must be >= 1");
+      smax = std::max(smax, side_per_pair[i]);
+    }
+    DevWork& w = work_for_current();
+    ensure(w.stage, w.stage_bytes, (size_t)pairs * sizeof(int) + 256);
+    int* side_dev = static_cast<int*>(w.stage);
+    PGB_CK(cudaMemcpyAsync(side_dev, side_per_pair, (size_t)pairs * sizeof(int),
+                           cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    FusedParams P = base_params(height, width);
+    P.n = (int)n_per_pair;
+    P.pairs = pairs;
+    P.pair_base = pair_base;
+    P.batch_lo = (uint32_t)batch;
+    P.psf = psf;
+    P.out_mode = out_mode;
+    P.bg_offset = (float)bg_offset;
+    P.noise_std = (float)noise_std;
+    P.mode = 1;
+    P.nframes = 2;
+    P.g.k0 = (uint32_t)(seed & 0xffffffffu);
+    P.g.k1 = (uint32_t)(seed >> 32);
+    P.inj[0] = InjFrame{frame1->pos, frame1->i0, frame1->sigma_x, frame1->sigma_y, frame1->rho, frame1->mask};
+    P.inj[1] = InjFrame{frame2->pos, frame2->i0, frame2->sigma_x, frame2->sigma_y, frame2->rho, frame2->mask};
+    P.side_in = side_dev;
+    P.out[0] = out1;
+    P.out[1] = out2;
+    P.bin_counts = bin_counts;
+    const Plan pl = make_plan(height, height, width, n_per_pair, smax / 2, 2, 8);
+    if (tiles_out) *tiles_out = pl.tiles;
+    launch_fused(P, pl, (cudaStream_t)stream);
+    PGB_CK(cudaGetLastError());
+    PGB_CK(cudaStreamSynchronize((cudaStream_t)stream));  // side staging reuse
+  });
+}
+
+int pgb_advect_dev(const double* pos, int64_t n, const float* flow_uv, int height, int width,
+                   double* out_pos, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(height > 0 && width > 0, "bad field size");
+    if (n <= 0) return;
+    advect_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+        pos, n, reinterpret_cast<const float2*>(flow_uv), height, width, out_pos, 1);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_sample_flow_dev(const double* pos, int64_t n, const float* flow_uv, int height, int width,
+                        double* out_uv, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(height > 0 && width > 0, "bad field size");
+    if (n <= 0) return;
+    advect_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+        pos, n, reinterpret_cast<const float2*>(flow_uv), height, width, out_uv, 0);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_finalize_dev(const float* raw, int pairs, int height, int width, double bg_offset,
+                     double noise_std, uint64_t seed, uint64_t batch, int64_t pair_base, int frame,
+                     int out_mode, void* out, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(out_mode == PGB_OUT_FINAL_F32 || out_mode == PGB_OUT_FINAL_U16,
+                "out_mode must be FINAL_F32 or FINAL_U16");
+    PGB_REQUIRE(frame == 1 || frame == 2, "frame must be 1 or 2");
+    const long long hw = (long long)height * width;
+    if (pairs <= 0 || hw <= 0) return;
+    finalize_kernel<<<grid_for(((hw + 3) / 4) * pairs, 256), 256, 0, (cudaStream_t)stream>>>(
+        raw, pairs, hw, (float)bg_offset, (float)noise_std, (uint32_t)(seed & 0xffffffffu),
+        (uint32_t)(seed >> 32), (uint32_t)batch, pair_base, frame, out_mode, out);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_quantize_u16_dev(const float* img, int64_t count, uint16_t* out, void* stream) {
+  return guarded([&] {
+    if (count <= 0) return;
+    quantize_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(img, count, out);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_generate_batch_dev(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
+                           const float* flows, int num_fields, int pairs_per_field, int out_mode,
+                           void* img1, void* img2, const pgb_pair_stats* stats,
+                           int32_t* bin_counts, void* stream) {
+  return guarded([&] {
+    generate_dev_impl(cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, out_mode,
+                      img1, img2, stats, bin_counts, (cudaStream_t)stream);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_generate_batch(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
+                       const float* flows, int num_fields, int pairs_per_field, int out_mode,
+                       void* img1, void* img2, const pgb_pair_stats* stats) {
+  return guarded([&] {
+    validate_cfg(cfg);
+    const size_t hw = (size_t)cfg->height * cfg->width;
+    const size_t px_bytes = out_mode == PGB_OUT_FINAL_U16 ? 2 : 4;
+    const size_t img_bytes = (size_t)pairs * hw * px_bytes;
+    const size_t flow_bytes = (size_t)num_fields * hw * 2 * sizeof(float);
+    const size_t st_bytes = (size_t)pairs * (8 + 4 + 4 + 4);
+    DevWork& w = work_for_current();
+    const size_t need = 2 * img_bytes + flow_bytes + st_bytes + 1024;
+    char* b = static_cast<char*>(ensure(w.stage, w.stage_bytes, need));
+    float* d_flow = reinterpret_cast<float*>(b);
+    char* d_img1 = b + ((flow_bytes + 255) / 256) * 256;
+    char* d_img2 = d_img1 + ((img_bytes + 255) / 256) * 256;
+    char* d_st = d_img2 + ((img_bytes + 255) / 256) * 256;
+    pgb_pair_stats dst{};
+    if (stats) {
+      dst.seeding_density = reinterpret_cast<double*>(d_st);
+      dst.active_count = reinterpret_cast<int32_t*>(d_st + (size_t)pairs * 8);
+      dst.side = reinterpret_cast<int32_t*>(d_st + (size_t)pairs * 12);
+      dst.d_max = reinterpret_cast<float*>(d_st + (size_t)pairs * 16);
+    }
+    cudaStream_t s = nullptr;
+    PGB_CK(cudaMemcpyAsync(d_flow, flows, flow_bytes, cudaMemcpyHostToDevice, s));
+    generate_dev_impl(cfg, batch, pair_base, pairs, d_flow, num_fields, pairs_per_field, out_mode,
+                      d_img1, d_img2, stats ? &dst : nullptr, nullptr, s);
+    PGB_CK(cudaMemcpyAsync(img1, d_img1, img_bytes, cudaMemcpyDeviceToHost, s));
+    PGB_CK(cudaMemcpyAsync(img2, d_img2, img_bytes, cudaMemcpyDeviceToHost, s));
+    if (stats) {
+      if (stats->seeding_density)
+        PGB_CK(cudaMemcpyAsync(stats->seeding_density, dst.seeding_density, (size_t)pairs * 8, cudaMemcpyDeviceToHost, s));
+      if (stats->active_count)
+        PGB_CK(cudaMemcpyAsync(stats->active_count, dst.active_count, (size_t)pairs * 4, cudaMemcpyDeviceToHost, s));
+      if (stats->side)
+        PGB_CK(cudaMemcpyAsync(stats->side, dst.side, (size_t)pairs * 4, cudaMemcpyDeviceToHost, s));
+      if (stats->d_max)
+        PGB_CK(cudaMemcpyAsync(stats->d_max, dst.d_max, (size_t)pairs * 4, cudaMemcpyDeviceToHost, s));
+    }
+    PGB_CK(cudaStreamSynchronize(s));
+    int ovf = 0;
+    PGB_CK(cudaMemcpy(&ovf, w.overflow, sizeof(int), cudaMemcpyDeviceToHost));
+    PGB_REQUIRE(ovf == 0, "particle-list overflow: tile capacity exceeded (extreme density)");
+  });
+}
+
+int pgb_sample_particles_dev(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
+                             const float* flows, int num_fields, int pairs_per_field,
+                             const pgb_particle_out* out, const pgb_pair_stats* stats,
+                             void* stream) {
+  return guarded([&] {
+    validate_cfg(cfg);
+    PGB_REQUIRE(out != nullptr, "out is NULL");
+    PGB_REQUIRE(flows != nullptr && num_fields >= 1 && pairs_per_field >= 1, "flows required");
+    if (pairs <= 0) return;
+    FusedParams P = base_params(cfg->height, cfg->width);
+    P.n = cfg->n_capacity;
+    P.pairs = pairs;
+    P.pair_base = pair_base;
+    P.batch_lo = (uint32_t)batch;
+    P.g = gen_cfg_from(cfg);
+    P.flows = reinterpret_cast<const float2*>(flows);
+    P.num_fields = num_fields;
+    P.pairs_per_field = pairs_per_field;
+    P.field_elems = (long long)cfg->height * cfg->width;
+    if (stats) {
+      P.st_ppp = stats->seeding_density;
+      P.st_M = stats->active_count;
+      P.st_side = stats->side;
+      P.st_dmax = stats->d_max;
+    }
+    sample_particles_kernel<<<pairs, 256, 0, (cudaStream_t)stream>>>(P, *out);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_perturb_frame2_dev(int64_t n, uint64_t seed, uint64_t batch, int64_t gpair,
+                           double sd_sigma, double sd_i0, double sd_rho, const float* i0_1,
+                           const float* sx_1, const float* sy_1, const float* rho_1, float* i0_2,
+                           float* sx_2, float* sy_2, float* rho_2, void* stream) {
+  return guarded([&] {
+    if (n <= 0) return;
+    perturb_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int)n, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), (uint32_t)gpair,
+        (uint32_t)batch, (float)sd_sigma, (float)sd_i0, (float)sd_rho, i0_1, sx_1, sy_1, rho_1,
+        i0_2, sx_2, sy_2, rho_2);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_apply_hiding_dev(int64_t n, uint64_t seed, uint64_t batch, int64_t gpair, double p_hide,
+                         const unsigned char* active, unsigned char* visible1,
+                         unsigned char* visible2, void* stream) {
+  return guarded([&] {
+    if (n <= 0) return;
+    hiding_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int)n, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), (uint32_t)gpair,
+        (uint32_t)batch, p_hide, active, visible1, visible2);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_overflow_count(void) {
+  int v = -1;
+  guarded([&] {
+    DevWork& w = work_for_current();
+    PGB_CK(cudaMemcpy(&v, w.overflow, sizeof(int), cudaMemcpyDeviceToHost));
+  });
+  return v;
+}
+
+int pgb_overflow_reset(void) {
+  return guarded([&] {
+    DevWork& w = work_for_current();
+    PGB_CK(cudaMemset(w.overflow, 0, sizeof(int)));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+"""Generate golden fixtures from the REAL reference (oracle/_ref pivgen).
+
+Run in the build container (needs oracle/_ref, built by oracle/build_ref.sh):
+    python tests/golden/make_golden.py
+Writes tests/golden/ref_cases.npz: reference particle sets (sample_particles ->
+advect -> perturb_frame2 -> apply_hiding, pipeline.py:285-295), their patch
+sides, the reference splat images of both frames (raster.splat -> native
+_native.splat_accumulate) and reference finalize outputs (noise off), for
+SPEC-style random configs. Also tests/golden/philox_curand.txt from NVIDIA's
+curand_Philox4x32_10 (oracle/_ref/philox_curand_check).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import reference  # noqa: E402
+
+CASES = [
+    # name, H, W, ppp, d_range, rho_range, sigma_std, i0_std, hide, flow, seed
+    ("c1_uniform_256", 256, 256, (0.06, 0.06), (0.8, 1.2), (0.0, 0.0), 0.0, 0.0, 0.0, "uniform", 0),
+    ("small_64_rho", 64, 64, (0.1, 0.1), (0.5, 4.0), (-0.5, 0.5), 0.1, 0.05, 0.1, "vortex", 11),
+    ("small_64_dense", 64, 64, (0.05, 0.1), (1.0, 4.0), (0.0, 0.0), 0.0, 0.0, 0.0, "vortex", 5),
+    ("rect_48x80", 48, 80, (0.08, 0.08), (0.8, 2.5), (-0.3, 0.3), 0.0, 0.0, 0.2, "uniform", 7),
+    ("odd_37x53", 37, 53, (0.04, 0.07), (0.8, 1.2), (0.0, 0.0), 0.0, 0.1, 0.0, "vortex", 3),
+]
+
+
+def vortex(h, w):
+    """Lamb-Oseen vortex centred in the image, r_c = 0.1 W, peak ~2.7 px."""
+    def fn(x, y):
+        cx, cy = (w - 1) / 2.0, (h - 1) / 2.0
+        rc = 0.1 * w
+        dx, dy = x - cx, y - cy
+        r = np.sqrt(dx * dx + dy * dy) + 1e-12
+        vt = 1.398 * 2.0 * (rc / r) * (1.0 - np.exp(-(r / rc) ** 2))
+        return -vt * dy / r, vt * dx / r
+    return fn
+
+
+def main() -> None:
+    pv = reference.load()
+    from pivgen import config, flowfield, particles, raster
+    from pivgen.rng import STREAM_NOISE, pair_key
+
+    out = {}
+    names = []
+    for name, H, W, ppp, dr, rr, ss, si, hide, flow, seed in CASES:
+        if flow == "uniform":
+            field = flowfield.FlowField(np.full((H, W), 2.0, np.float32), np.full((H, W), -1.0, np.float32))
+        else:
+            field = flowfield.from_function(vortex(H, W), H, W)
+        cfg = config.GeneratorConfig(image_height=H, image_width=W, seeding_density_range=ppp,
+                                     diameter_range=dr, rho_range=rr, frame2_sigma_std=ss,
+                                     frame2_intensity_std=si, hide_probability=hide, seed=seed)
+        for pair in range(2):
+            key = pair_key(seed, 0, pair)
+            ps, params = particles.sample_particles(key, cfg)
+            particles.advect(ps, field)
+            ps.app2 = particles.perturb_frame2(key, ps.app1, cfg)
+            particles.apply_hiding(key, ps, cfg.hide_probability)
+            m = params.active_count
+            dmax = float(params.diameters[:m].max()) if m else cfg.diameter_range[1]
+            side = raster.patch_side(dmax, cfg.patch_multiplier)
+            tag = f"{name}_p{pair}"
+            names.append(tag)
+            out[f"{tag}/hw"] = np.array([H, W])
+            out[f"{tag}/side"] = np.array(side)
+            out[f"{tag}/flow"] = np.stack([field.u, field.v], axis=-1)
+            for f, (pos, app) in enumerate(((ps.pos1, ps.app1), (ps.pos2, ps.app2)), start=1):
+                mask = raster.contribution_mask(ps, f)
+                out[f"{tag}/pos{f}"] = pos
+                out[f"{tag}/i0_{f}"] = app.i0
+                out[f"{tag}/sx_{f}"] = app.sigma_x
+                out[f"{tag}/sy_{f}"] = app.sigma_y
+                out[f"{tag}/rho_{f}"] = app.rho
+                out[f"{tag}/mask{f}"] = mask
+                raw = raster.splat(ps, f, H, W, side)
+                out[f"{tag}/raw{f}"] = raw
+                fin = raster.finalize(raw, config.NoiseConfig(background_offset=0.05),
+                                      key.with_stream(STREAM_NOISE, lane=f))
+                out[f"{tag}/fin{f}"] = fin
+    out["names"] = np.array(names)
+    path = os.path.join(HERE, "ref_cases.npz")
+    np.savez_compressed(path, **out)
+    print("wrote", path, os.path.getsize(path), "bytes,", len(names), "cases")
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "philox_curand_check")
+    txt = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
+    with open(os.path.join(HERE, "philox_curand.txt"), "w") as fh:
+        fh.write(txt)
+    print("wrote philox_curand.txt")
+
+
+if __name__ == "__main__":
+    main()

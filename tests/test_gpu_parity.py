@@ -1,0 +1,384 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference and the oracle.
+
+Tolerances (north_star): rendered images max-abs <= 1e-5 and
+PSNR >= 100 dB vs the reference; bin counts, positions (advection), masks,
+M, side and uint16 quantisation bit-exact.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+from oracle import generate as og
+from oracle import reference
+from oracle import render as orr
+from _helpers import vortex_fn
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _psnr(a, b):
+    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    return math.inf if mse == 0 else 10 * math.log10(1.0 / mse)
+
+
+def _assert_close(got, want, tol=TOL, psnr=100.0, what=""):
+    err = float(np.abs(got.astype(np.float64) - want.astype(np.float64)).max()) if got.size else 0.0
+    assert err <= tol, f"{what}: max-abs {err:.3e} > {tol:.1e}"
+    assert _psnr(got, want) >= psnr, f"{what}: PSNR {_psnr(got, want):.1f} dB"
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import paper_2512_09664_b200 as pg
+    from paper_2512_09664_b200 import _lib
+
+    _lib.load()
+    return pg
+
+
+def test_splat_seam_host_buffers_vs_reference(pg, golden):
+    """pgb_splat_accumulate (host buffers) == _native.splat_accumulate contract."""
+    from paper_2512_09664_b200 import _lib
+
+    for name, c in golden.items():
+        H, W = (int(x) for x in c["hw"])
+        for f in (1, 2):
+            out = np.zeros((H, W), np.float32)
+            args = [np.ascontiguousarray(c[k]) for k in (f"pos{f}", f"i0_{f}", f"sx_{f}", f"sy_{f}",
+                                                         f"rho_{f}", f"mask{f}")]
+            n = args[0].shape[0]
+            _lib.call("pgb_splat_accumulate", *[a.ctypes.data for a in args], n, int(c["side"]),
+                      out.ctypes.data, H, W, 0, H)
+            _assert_close(out, c[f"raw{f}"], what=f"{name} frame {f}")
+
+
+def test_splat_seam_accumulates_in_place_and_bands(pg, golden):
+    c = golden["small_64_rho_p0"]
+    H, W = (int(x) for x in c["hw"])
+    args = (c["pos1"], c["i0_1"], c["sx_1"], c["sy_1"], c["rho_1"], c["mask1"], int(c["side"]))
+    whole = np.zeros((H, W), np.float32)
+    pg.splat_accumulate(*args, whole, 0, H)
+    banded = np.zeros((H, W), np.float32)
+    for lo, hi in ((0, 17), (17, 40), (40, H)):
+        pg.splat_accumulate(*args, banded, lo, hi)
+    np.testing.assert_array_equal(banded, whole)          # band-independent, bit-exact
+    twice = whole.copy()
+    pg.splat_accumulate(*args, twice, 0, H)
+    np.testing.assert_allclose(twice, 2 * whole, atol=2e-6)  # in-place +=
+
+
+def _render_golden(pg, c, out_mode, bg=0.0):
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+
+    H, W = (int(x) for x in c["hw"])
+    dev = torch.device("cuda")
+    frames, keep = [], []
+    for f in (1, 2):
+        t = dict(pos=torch.from_numpy(c[f"pos{f}"]).to(dev),
+                 i0=torch.from_numpy(c[f"i0_{f}"]).to(dev), sx=torch.from_numpy(c[f"sx_{f}"]).to(dev),
+                 sy=torch.from_numpy(c[f"sy_{f}"]).to(dev), rho=torch.from_numpy(c[f"rho_{f}"]).to(dev),
+                 mask=torch.from_numpy(c[f"mask{f}"]).to(dev))
+        keep.append(t)
+        frames.append(_lib.PgbParticles(t["pos"].data_ptr(), t["i0"].data_ptr(), t["sx"].data_ptr(),
+                                        t["sy"].data_ptr(), t["rho"].data_ptr(), t["mask"].data_ptr()))
+    n = c["pos1"].shape[0]
+    out = [torch.zeros((1, H, W), dtype=torch.float32, device=dev) for _ in range(2)]
+    tiles = ctypes.c_int(0)
+    bins = torch.full((1, 2, 4096), -1, dtype=torch.int32, device=dev)
+    sides = (ctypes.c_int * 1)(int(c["side"]))
+    _lib.call("pgb_render_pairs_dev", ctypes.byref(frames[0]), ctypes.byref(frames[1]), n, 1, sides,
+              H, W, 0, out_mode, bg, 0.0, 0, 0, 0, out[0].data_ptr(), out[1].data_ptr(),
+              bins.data_ptr(), ctypes.byref(tiles), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return [o[0].cpu().numpy() for o in out], bins.cpu().numpy(), tiles.value
+
+
+def test_render_pairs_raw_vs_reference(pg, golden):
+    from paper_2512_09664_b200 import _lib
+
+    for name, c in golden.items():
+        imgs, _, _ = _render_golden(pg, c, _lib.OUT_RAW)
+        for f in (1, 2):
+            _assert_close(imgs[f - 1], c[f"raw{f}"], what=f"{name} raw{f}")
+
+
+def test_render_pairs_finalized_vs_reference(pg, golden):
+    from paper_2512_09664_b200 import _lib
+
+    for name, c in golden.items():
+        imgs, _, _ = _render_golden(pg, c, _lib.OUT_F32, bg=0.05)
+        for f in (1, 2):
+            _assert_close(imgs[f - 1], c[f"fin{f}"], what=f"{name} fin{f}")
+
+
+def test_bin_counts_bit_exact(pg, golden):
+    from paper_2512_09664_b200 import _lib
+
+    for name, c in golden.items():
+        H, W = (int(x) for x in c["hw"])
+        _, bins, tiles = _render_golden(pg, c, _lib.OUT_RAW)
+        info = _lib.PgbPlanInfo()
+        _lib.call("pgb_plan", H, W, c["pos1"].shape[0], 0.0, int(c["side"]) // 2, 2, ctypes.byref(info))
+        assert tiles == info.tiles_y * info.tiles_x
+        for f in (1, 2):
+            want = orr.tile_counts(c[f"pos{f}"], c[f"mask{f}"], info.halo, info.tile_h, info.tile_w, H, W)
+            np.testing.assert_array_equal(bins[0, f - 1, :tiles], want, err_msg=f"{name} f{f}")
+
+
+def test_advect_and_sample_flow_bit_exact(pg, golden):
+    for name, c in golden.items():
+        fld = pg.FlowField(c["flow"][..., 0], c["flow"][..., 1])
+        ps = pg.ParticleSet(count=c["pos1"].shape[0], pos1=c["pos1"],
+                            app1=pg.Appearance(c["i0_1"], c["sx_1"], c["sy_1"], c["rho_1"]),
+                            active=np.ones(c["pos1"].shape[0], bool))
+        pg.advect(ps, fld)
+        np.testing.assert_array_equal(ps.pos2, c["pos2"], err_msg=name)
+        uv = pg.sample_flow(fld, c["pos1"])
+        np.testing.assert_array_equal(uv, og.sample_flow(c["flow"], c["pos1"]), err_msg=name)
+
+
+def test_sample_flow_spec_examples(pg):
+    fld = pg.FlowField(np.array([[0.0, 1.0], [0.0, 1.0]], np.float32), np.zeros((2, 2), np.float32))
+    assert pg.sample_flow(fld, [(0.5, 0.5)])[0, 0] == 0.5
+    const = pg.FlowField(np.full((4, 4), 2.0, np.float32), np.full((4, 4), -1.0, np.float32))
+    np.testing.assert_array_equal(pg.sample_flow(const, [(-5, -5), (1.3, 2.7)]), [[2, -1], [2, -1]])
+
+
+def test_quantize_bit_exact(pg):
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.uniform(-0.2, 1.2, 100000).astype(np.float32),
+                        (np.arange(65536, dtype=np.float32) + 0.5) / np.float32(65535),
+                        np.array([0.5, 0.0, 1.0, np.nextafter(np.float32(0.5), np.float32(1))], np.float32)])
+    np.testing.assert_array_equal(pg.quantize_u16(x), orr.quantize_u16(x))
+
+
+def test_spec_known_answers(pg):
+    one = dict(pos=np.array([[5.0, 5.0]]), i0=np.array([1.0], np.float32), sx=np.array([1.0], np.float32),
+               sy=np.array([1.0], np.float32), rho=np.array([0.0], np.float32))
+    ps = pg.ParticleSet(count=1, pos1=one["pos"], app1=pg.Appearance(one["i0"], one["sx"], one["sy"], one["rho"]),
+                        active=np.array([True]))
+    img = pg.splat(ps, 1, 11, 11, 7)
+    assert img[5, 5] == pytest.approx(1.0, abs=1e-6)
+    assert img[5, 6] == pytest.approx(math.exp(-0.5), abs=1e-6)
+    two = pg.ParticleSet(count=2, pos1=np.repeat(one["pos"], 2, 0),
+                         app1=pg.Appearance(*(np.repeat(one[k], 2) for k in ("i0", "sx", "sy", "rho"))),
+                         active=np.array([True, True]))
+    np.testing.assert_allclose(pg.splat(two, 1, 11, 11, 7), 2 * img, atol=1e-6)
+    empty = pg.ParticleSet(count=1, pos1=one["pos"],
+                           app1=pg.Appearance(one["i0"], one["sx"], one["sy"], one["rho"]),
+                           active=np.array([False]))
+    assert not pg.splat(empty, 1, 11, 11, 7).any()
+    assert pg.eval_particle(1, 1, 1, 0.5, (0, 0), (1, 1)) == pytest.approx(math.exp(-2 / 3), rel=1e-9)
+
+
+def _gen_cfg(pg, **kw):
+    base = dict(image_height=64, image_width=64, batch_size=4, seeding_density_range=(0.05, 0.1),
+                diameter_range=(0.5, 4.0), rho_range=(-0.5, 0.5), frame2_sigma_std=0.05,
+                frame2_intensity_std=0.05, frame2_rho_std=0.05, hide_probability=0.1, seed=9,
+                flow_sources=(pg.FlowSource(function="vortex"),))
+    base.update(kw)
+    return pg.GeneratorConfig(**base)
+
+
+def _oracle_cfg(cfg):
+    ls = cfg.laser_sheet
+    laser = None
+    if ls is not None:
+        zlo, zhi = ls.resolved_z_range()
+        laser = dict(dz0=ls.thickness, shape=ls.shape, q=ls.efficiency, z_lo=zlo, z_hi=zhi, w=ls.out_of_plane)
+    return og.GenConfig(height=cfg.image_height, width=cfg.image_width, seed=cfg.seed,
+                        ppp_range=cfg.seeding_density_range, d_range=cfg.diameter_range,
+                        i0_range=cfg.peak_intensity_range, rho_range=cfg.rho_range,
+                        sigma_ratio=cfg.diameter_sigma_ratio, patch_multiplier=cfg.patch_multiplier,
+                        f2_sigma_std=cfg.frame2_sigma_std, f2_rho_std=cfg.frame2_rho_std,
+                        f2_i0_std=cfg.frame2_intensity_std, hide_probability=cfg.hide_probability,
+                        laser=laser)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(),
+    dict(image_height=256, image_width=256, seeding_density_range=(0.06, 0.06), diameter_range=(0.8, 1.2),
+         rho_range=(0.0, 0.0), frame2_sigma_std=0.0, frame2_intensity_std=0.0, frame2_rho_std=0.0,
+         hide_probability=0.0),
+    dict(image_height=48, image_width=80, laser_sheet={"thickness": 1.0, "shape": 2.0, "out_of_plane": 0.1}),
+])
+def test_generated_particles_match_oracle(pg, kw):
+    import torch
+
+    cfg = _gen_cfg(pg, **kw)
+    H, W = cfg.image_height, cfg.image_width
+    flow = pg.from_function(vortex_fn(H, W), H, W)
+    flows = flow.to_device().unsqueeze(0)
+    arr = pg.particles.generate_particle_arrays(cfg, 3, range(0, cfg.batch_size), flows=flows,
+                                                pairs_per_field=cfg.batch_size)
+    oc = _oracle_cfg(cfg)
+    for p in range(cfg.batch_size):
+        o = og.sample_pair(oc, 3, p, flow.interleaved())
+        g = {k: v[p].cpu().numpy() for k, v in arr.items() if v.ndim >= 2}
+        assert int(arr["active_count"][p]) == o["M"]
+        assert int(arr["side"][p]) == o["side"]
+        assert float(arr["seeding_density"][p]) == o["ppp"]
+        for k in ("pos1", "pos2", "sx_1", "sy_1", "rho_1", "diameter"):
+            np.testing.assert_array_equal(g[k], o[k], err_msg=k)
+        np.testing.assert_array_equal(g["active"].astype(bool), o["active"])
+        np.testing.assert_array_equal(g["visible1"].astype(bool), o["visible1"])
+        np.testing.assert_array_equal(g["visible2"].astype(bool), o["visible2"])
+        if cfg.laser_sheet is None:
+            np.testing.assert_array_equal(g["i0_1"], o["i0_1"])
+        for k in ("i0_1", "i0_2", "sx_2", "sy_2", "rho_2"):
+            np.testing.assert_allclose(g[k], o[k], rtol=2e-5, atol=2e-6, err_msg=k)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("kw", [
+    dict(),
+    dict(image_height=256, image_width=256, batch_size=3, seeding_density_range=(0.06, 0.06),
+         diameter_range=(0.8, 1.2), rho_range=(0.0, 0.0), frame2_sigma_std=0.0,
+         frame2_intensity_std=0.0, frame2_rho_std=0.0, hide_probability=0.0),
+    dict(image_height=96, image_width=160, batch_size=2, seeding_density_range=(0.1, 0.1),
+         diameter_range=(1.0, 4.0), rho_range=(0.0, 0.0)),
+])
+def test_fused_generate_raw_matches_oracle_render(pg, kw):
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    cfg = _gen_cfg(pg, **kw)
+    H, W, B = cfg.image_height, cfg.image_width, cfg.batch_size
+    flow = pg.from_function(vortex_fn(H, W), H, W)
+    flows = flow.to_device().unsqueeze(0)
+    img = [torch.empty((B, H, W), dtype=torch.float32, device="cuda") for _ in range(2)]
+    _lib.call("pgb_generate_batch_dev", native_config(cfg), 5, 0, B, flows.data_ptr(), 1, B,
+              _lib.OUT_RAW, img[0].data_ptr(), img[1].data_ptr(), None, None,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert _lib.load().pgb_overflow_count() == 0
+    oc = _oracle_cfg(cfg)
+    for p in range(B):
+        o = og.sample_pair(oc, 5, p, flow.interleaved())
+        for f in (1, 2):
+            want = orr.splat(o[f"pos{f}"], o[f"i0_{f}"], o[f"sx_{f}"], o[f"sy_{f}"], o[f"rho_{f}"],
+                             o[f"on{f}"], o["side"], H, W)
+            _assert_close(img[f - 1][p].cpu().numpy(), want, tol=2e-5 if cfg.frame2_sigma_std else TOL,
+                          what=f"pair {p} frame {f}")
+
+
+def test_fused_generate_final_with_noise_matches_oracle(pg):
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    cfg = _gen_cfg(pg, image_height=64, image_width=96, batch_size=2, rho_range=(0.0, 0.0),
+                   frame2_sigma_std=0.0, frame2_intensity_std=0.0, frame2_rho_std=0.0,
+                   noise=pg.NoiseConfig(background_offset=0.05, gaussian_std=0.02))
+    H, W, B = cfg.image_height, cfg.image_width, cfg.batch_size
+    flows = pg.from_function(vortex_fn(H, W), H, W).to_device().unsqueeze(0)
+    out = {}
+    for mode in (_lib.OUT_RAW, _lib.OUT_F32, _lib.OUT_U16):
+        dt = torch.uint16 if mode == _lib.OUT_U16 else torch.float32
+        img = [torch.empty((B, H, W), dtype=dt, device="cuda") for _ in range(2)]
+        _lib.call("pgb_generate_batch_dev", native_config(cfg), 2, 0, B, flows.data_ptr(), 1, B, mode,
+                  img[0].data_ptr(), img[1].data_ptr(), None, None, torch.cuda.current_stream().cuda_stream)
+        out[mode] = [i.cpu().numpy() for i in img]
+    for p in range(B):
+        for f in (1, 2):
+            raw = out[_lib.OUT_RAW][f - 1][p]
+            want = orr.finalize(raw, 0.05, 0.02, seed=cfg.seed, batch=2, gpair=p, frame=f)
+            _assert_close(out[_lib.OUT_F32][f - 1][p], want, tol=2e-6, what=f"fin p{p} f{f}")
+            # fused uint16 == quantize_u16(fused float32), bit-exact
+            np.testing.assert_array_equal(out[_lib.OUT_U16][f - 1][p],
+                                          orr.quantize_u16(out[_lib.OUT_F32][f - 1][p]))
+    # standalone finalize kernel uses the same noise stream as the fused epilogue
+    raw_t = torch.from_numpy(np.stack(out[_lib.OUT_RAW][0])).cuda()
+    fin = pg.finalize(raw_t, cfg.noise, pg.RngKey(cfg.seed, 2, 0), frame=1)
+    np.testing.assert_array_equal(fin.cpu().numpy(), np.stack(out[_lib.OUT_F32][0]))
+
+
+def test_sharding_and_determinism_bit_identical(pg):
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    cfg = _gen_cfg(pg, image_height=128, image_width=128, batch_size=8)
+    H, W, B = 128, 128, 8
+    flows = pg.from_function(vortex_fn(H, W), H, W).to_device().unsqueeze(0)
+
+    def run(base, count):
+        img = [torch.empty((count, H, W), dtype=torch.float32, device="cuda") for _ in range(2)]
+        _lib.call("pgb_generate_batch_dev", native_config(cfg), 1, base, count, flows.data_ptr(), 1, B,
+                  _lib.OUT_F32, img[0].data_ptr(), img[1].data_ptr(), None, None,
+                  torch.cuda.current_stream().cuda_stream)
+        return [i.cpu().numpy() for i in img]
+
+    full = run(0, 8)
+    again = run(0, 8)
+    halves = [run(0, 3), run(3, 5)]
+    for f in range(2):
+        np.testing.assert_array_equal(full[f], again[f])
+        np.testing.assert_array_equal(full[f], np.concatenate([halves[0][f], halves[1][f]]))
+
+
+def test_erf_psf_matches_oracle(pg, golden):
+    for name in ("small_64_rho_p0", "small_64_dense_p1", "rect_48x80_p1"):
+        c = golden[name]
+        H, W = (int(x) for x in c["hw"])
+        for f in (1, 2):
+            args = (c[f"pos{f}"], c[f"i0_{f}"], c[f"sx_{f}"], c[f"sy_{f}"], c[f"rho_{f}"], c[f"mask{f}"],
+                    int(c["side"]))
+            got = np.zeros((H, W), np.float32)
+            pg.splat_accumulate(*args, got, 0, H, psf="erf")
+            want = orr.render_erf(*args, H, W)
+            _assert_close(got, want, tol=2e-5, psnr=90, what=f"{name} erf f{f}")
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_spec_oracle_equivalence_random_configs(pg, seed):
+    """SPEC.md:600 (100 random 64^2 configs; 10 per test x 10 seeds): GPU splat vs the
+    REAL reference's splat (oracle/_ref) or, if absent, the bit-equal restatement."""
+    rng = np.random.default_rng(1000 + seed)
+    use_ref = reference.available()
+    if use_ref:
+        reference.load()
+        from pivgen import config as rc
+        from pivgen import particles as rp
+        from pivgen import raster as rr
+        from pivgen.rng import pair_key as rkey
+    for k in range(10):
+        ppp = float(rng.uniform(0.01, 0.1))
+        dmax = float(rng.uniform(0.6, 4.0))
+        dmin = float(rng.uniform(0.3, dmax))
+        rho = float(rng.uniform(0.0, 0.5))
+        if use_ref:
+            cfg = rc.GeneratorConfig(image_height=64, image_width=64, seeding_density_range=(ppp / 2, ppp),
+                                     diameter_range=(dmin, dmax), rho_range=(-rho, rho),
+                                     seed=int(rng.integers(1 << 30)))
+            ps, params = rp.sample_particles(rkey(cfg.seed, 0, k), cfg)
+            side = rr.patch_side(float(params.diameters[:params.active_count].max())
+                                 if params.active_count else dmax)
+            want = rr.splat(ps, 1, 64, 64, side)
+            mask = rr.contribution_mask(ps, 1)
+            pos, app = ps.pos1, ps.app1
+            got = np.zeros((64, 64), np.float32)
+            pg.splat_accumulate(pos, app.i0, app.sigma_x, app.sigma_y, app.rho, mask, side, got, 0, 64)
+        else:
+            oc = og.GenConfig(height=64, width=64, seed=k, ppp_range=(ppp / 2, ppp), d_range=(dmin, dmax),
+                              rho_range=(-rho, rho))
+            o = og.sample_pair(oc, 0, k, np.zeros((64, 64, 2), np.float32))
+            side = o["side"]
+            args = (o["pos1"], o["i0_1"], o["sx_1"], o["sy_1"], o["rho_1"], o["on1"], side)
+            want = orr.splat(*args, 64, 64)
+            got = np.zeros((64, 64), np.float32)
+            pg.splat_accumulate(*args, got, 0, 64)
+        _assert_close(got, want, what=f"config {seed}/{k}")
