@@ -11,9 +11,10 @@ draw layout of the B200 kernels, and the reference semantics it implements:
   apply_hiding        particles.py:139-147
   patch_side          raster.py:30-38 (+ pipeline.py:291-294 for d_max)
 
-Every float64 step is a separately rounded numpy op (no FMA), so positions,
-diameters, sigma, i0, rho, masks, M and side are bit-identical to the GPU;
-Box-Muller normals (frame-2 jitter) and the laser-sheet profile use float32
+Positions are fixed point (x = (2w + 1) W / 2^33, anchor + float32 fraction);
+every float32 step is a separately rounded numpy float32 op (no FMA), so
+positions, diameters, sigma, i0, rho, masks, M and side are bit-identical to
+the GPU; Box-Muller normals (frame-2 jitter) and the laser-sheet profile use
 fast intrinsics on the GPU and agree to ~1e-6.
 """
 
@@ -85,14 +86,68 @@ class GenConfig:
         return particle_capacity(self.ppp_range[1], self.height, self.width)
 
 
-def laser_profile(z: np.ndarray, dz0: float, shape: float, q: float) -> np.ndarray:
-    """I0(z) = q exp(-(1/sqrt(2 pi)) |2 z^2 / dZ0^2|^s)."""
+def laser_profile(z, dz0: float, shape: float, q: float):
+    """I0(z) = q exp(-(1/sqrt(2 pi)) |2 z^2 / dZ0^2|^s), float64."""
     t = 2.0 * np.asarray(z, np.float64) ** 2 / (dz0 * dz0)
     return q * np.exp(-(1.0 / math.sqrt(2.0 * math.pi)) * np.abs(t) ** shape)
 
 
+F32 = np.float32
+
+
+def unit23(w) -> np.ndarray:
+    """((w >> 9) + 0.5) * 2^-23 in float32: exact, strictly inside (0, 1)."""
+    w = np.asarray(w, dtype=np.uint32)
+    return ((w >> np.uint32(9)).astype(F32) + F32(0.5)) * F32(2.0 ** -23)
+
+
+def lerp32(lo: float, hi: float, u: np.ndarray) -> np.ndarray:
+    """f32(lo) + (f32(hi) - f32(lo)) * u, each op rounded to float32."""
+    lo32, hi32 = F32(lo), F32(hi)
+    span = F32(hi32 - lo32)
+    return (lo32 + span * u).astype(F32)
+
+
+def fixed_anchor(F: np.ndarray):
+    """Fixed-point coordinate F / 2^33 -> (anchor floor(v + 1/2), float32 fraction)."""
+    F = F.astype(np.uint64)
+    an = (F + np.uint64(1 << 32)) >> np.uint64(33)
+    diff = (F - (an << np.uint64(33))).astype(np.int64)
+    return an.astype(np.int64), (diff.astype(np.float64) * 2.0 ** -33).astype(F32)
+
+
+def fixed_cell(F: np.ndarray, n: int):
+    lim = np.uint64((n - 1) << 33)
+    xc = np.minimum(F.astype(np.uint64), lim)
+    c = np.minimum((xc >> np.uint64(33)).astype(np.int64), max(n - 2, 0))
+    t = ((xc - (c.astype(np.uint64) << np.uint64(33))).astype(np.int64).astype(np.float64)
+         * 2.0 ** -33).astype(F32)
+    return c, t
+
+
+def bilerp32(g00, g01, g10, g11, tx, ty):
+    one = F32(1.0)
+    sx, sy = (one - tx).astype(F32), (one - ty).astype(F32)
+    top = (sx * g00).astype(F32) + (tx * g01).astype(F32)
+    bot = (sx * g10).astype(F32) + (tx * g11).astype(F32)
+    return ((sy * top).astype(F32) + (ty * bot).astype(F32)).astype(F32)
+
+
+def shift_anchor(a, f, d):
+    t = (f + d).astype(F32)
+    k = np.floor((t + F32(0.5)).astype(F32)).astype(F32)
+    return a + k.astype(np.int64), (t - k).astype(F32)
+
+
+def hide_threshold(p: float) -> int:
+    """visible iff (w + 1/2) 2^-32 >= p  <=>  w >= ceil(p 2^32 - 1/2)."""
+    t = math.ceil(p * 4294967296.0 - 0.5)
+    return int(min(max(t, 0), 4294967296))
+
+
 def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> dict:
-    """All per-particle arrays of one pair, as the B200 kernel generates them."""
+    """All per-particle arrays of one pair, exactly as csrc/fused.cuh gen_particle()
+    produces them: fixed-point positions, float32 attributes and advection."""
     n = cfg.n
     H, W = cfg.height, cfg.width
     idx = np.arange(n, dtype=np.uint64)
@@ -102,60 +157,70 @@ def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> 
     m = min(max(m, 0), n)
 
     a = px.draw(cfg.seed, gpair, batch, idx, px.TAG_PARTICLE_A)
-    x1 = px.u32_to_unit(a[0]) * W
-    y1 = px.u32_to_unit(a[1]) * H
-    d = cfg.d_range[0] + (cfg.d_range[1] - cfg.d_range[0]) * px.u32_to_unit(a[2])
-    i0 = cfg.i0_range[0] + (cfg.i0_range[1] - cfg.i0_range[0]) * px.u32_to_unit(a[3])
+    X = (2 * a[0].astype(np.uint64) + np.uint64(1)) * np.uint64(W)
+    Y = (2 * a[1].astype(np.uint64) + np.uint64(1)) * np.uint64(H)
+    d = lerp32(cfg.d_range[0], cfg.d_range[1], unit23(a[2]))
+    i0 = lerp32(cfg.i0_range[0], cfg.i0_range[1], unit23(a[3]))
     active = np.arange(n) < m
 
     need_b = (cfg.rho_range[0] != cfg.rho_range[1]) or cfg.hide_probability > 0 or cfg.laser is not None
     if need_b:
         b = px.draw(cfg.seed, gpair, batch, idx, px.TAG_PARTICLE_B)
-        rho = cfg.rho_range[0] + (cfg.rho_range[1] - cfg.rho_range[0]) * px.u32_to_unit(b[0])
-        vis1 = px.u32_to_unit(b[1]) >= cfg.hide_probability
-        vis2 = px.u32_to_unit(b[2]) >= cfg.hide_probability
+        rho = lerp32(cfg.rho_range[0], cfg.rho_range[1], unit23(b[0]))
+        thr = hide_threshold(cfg.hide_probability)
+        vis1 = b[1].astype(np.uint64) >= np.uint64(thr)
+        vis2 = b[2].astype(np.uint64) >= np.uint64(thr)
         z_lo, z_hi = (cfg.laser["z_lo"], cfg.laser["z_hi"]) if cfg.laser else (0.0, 0.0)
-        z1 = z_lo + (z_hi - z_lo) * px.u32_to_unit(b[3])
+        z1 = lerp32(z_lo, z_hi, unit23(b[3]))
     else:
-        rho = np.full(n, cfg.rho_range[0])
+        rho = np.full(n, F32(cfg.rho_range[0]), dtype=F32)
         vis1 = vis2 = np.ones(n, dtype=bool)
-        z1 = np.zeros(n)
+        z1 = np.zeros(n, dtype=F32)
 
-    i0f = np.where(active, i0, 0.0).astype(np.float32)
-    sig = (d / cfg.sigma_ratio).astype(np.float32)
-    rhof = rho.astype(np.float32)
-    sx2, sy2, i02, rho2 = sig.copy(), sig.copy(), i0f.copy(), rhof.copy()
+    i0f = np.where(active, i0, F32(0.0)).astype(F32)
+    sig = (d * F32(1.0 / cfg.sigma_ratio)).astype(F32)
+    sx2, sy2, i02, rho2 = sig.copy(), sig.copy(), i0f.copy(), rho.copy()
     if cfg.f2_sigma_std > 0 or cfg.f2_rho_std > 0 or cfg.f2_i0_std > 0:
         c = px.draw(cfg.seed, gpair, batch, idx, px.TAG_PERTURB)
         n0, n1 = px.box_muller64(c[0], c[1])
         n2, n3 = px.box_muller64(c[2], c[3])
-        sd = np.float64(np.float32(cfg.f2_sigma_std))
         if cfg.f2_sigma_std > 0:
-            sx2 = np.maximum(sig.astype(np.float64) + sd * n0, SIGMA_FLOOR).astype(np.float32)
-            sy2 = np.maximum(sig.astype(np.float64) + sd * n1, SIGMA_FLOOR).astype(np.float32)
+            sd = F32(cfg.f2_sigma_std)
+            sx2 = np.maximum(sig + (sd * n0.astype(F32)).astype(F32), F32(1e-3)).astype(F32)
+            sy2 = np.maximum(sig + (sd * n1.astype(F32)).astype(F32), F32(1e-3)).astype(F32)
         if cfg.f2_i0_std > 0:
-            t = np.clip(i0f.astype(np.float64) + np.float64(np.float32(cfg.f2_i0_std)) * n2, 0.0, 1.0)
-            i02 = np.where(i0f == 0.0, 0.0, t).astype(np.float32)
+            t = np.clip(i0f + (F32(cfg.f2_i0_std) * n2.astype(F32)).astype(F32), F32(0), F32(1))
+            i02 = np.where(i0f == 0.0, F32(0.0), t).astype(F32)
         if cfg.f2_rho_std > 0:
-            t = np.clip(rhof.astype(np.float64) + np.float64(np.float32(cfg.f2_rho_std)) * n3,
-                        -RHO_CLAMP, RHO_CLAMP)
-            rho2 = t.astype(np.float32)
-    amp1, amp2 = i0f.astype(np.float64), i02.astype(np.float64)
+            rho2 = np.clip(rho + (F32(cfg.f2_rho_std) * n3.astype(F32)).astype(F32),
+                           F32(-0.999), F32(0.999)).astype(F32)
+    amp1, amp2 = i0f, i02
     if cfg.laser is not None:
         L = cfg.laser
-        amp1 = amp1 * laser_profile(z1.astype(np.float32), L["dz0"], L["shape"], L["q"])
-        amp2 = amp2 * laser_profile(z1.astype(np.float32) + np.float32(L["w"]), L["dz0"], L["shape"], L["q"])
-    amp1 = amp1.astype(np.float32)
-    amp2 = amp2.astype(np.float32)
+        amp1 = (i0f * laser_profile(z1, L["dz0"], L["shape"], L["q"])).astype(F32)
+        amp2 = (i02 * laser_profile((z1 + F32(L["w"])).astype(F32), L["dz0"], L["shape"],
+                                     L["q"])).astype(F32)
 
-    pos1 = np.stack([x1, y1], axis=1)
-    pos2 = pos1 + sample_flow(flow_uv, pos1)
+    ax1, fx1 = fixed_anchor(X)
+    ay1, fy1 = fixed_anchor(Y)
+    cx, tx = fixed_cell(X, W)
+    cy, ty = fixed_cell(Y, H)
+    cx1 = np.minimum(cx + 1, W - 1)
+    cy1 = np.minimum(cy + 1, H - 1)
+    g = flow_uv.astype(F32)
+    u = bilerp32(g[cy, cx, 0], g[cy, cx1, 0], g[cy1, cx, 0], g[cy1, cx1, 0], tx, ty)
+    v = bilerp32(g[cy, cx, 1], g[cy, cx1, 1], g[cy1, cx, 1], g[cy1, cx1, 1], tx, ty)
+    ax2, fx2 = shift_anchor(ax1, fx1, u)
+    ay2, fy2 = shift_anchor(ay1, fy1, v)
+
+    pos1 = np.stack([ax1 + fx1.astype(np.float64), ay1 + fy1.astype(np.float64)], axis=1)
+    pos2 = np.stack([ax2 + fx2.astype(np.float64), ay2 + fy2.astype(np.float64)], axis=1)
     on1 = active & vis1 & (amp1 > 0)
     on2 = active & vis2 & (amp2 > 0)
-    diam = d.astype(np.float32)
-    dmax = float(diam[:m].max()) if m else float(np.float32(cfg.d_range[1]))
+    dmax = float(d[:m].max()) if m else float(cfg.d_range[1])
     side = patch_side(dmax, cfg.patch_multiplier)
     return dict(ppp=ppp, M=m, pos1=pos1, pos2=pos2, i0_1=amp1, sx_1=sig, sy_1=sig.copy(),
-                rho_1=rhof, i0_2=amp2, sx_2=sx2, sy_2=sy2, rho_2=rho2, diameter=diam,
-                z1=z1.astype(np.float32), active=active, visible1=vis1 & active,
-                visible2=vis2 & active, on1=on1, on2=on2, side=side, d_max=dmax)
+                rho_1=rho, i0_2=amp2, sx_2=sx2, sy_2=sy2, rho_2=rho2, diameter=d,
+                z1=z1, active=active, visible1=vis1 & active, visible2=vis2 & active,
+                on1=on1, on2=on2, side=side, d_max=dmax,
+                anchors=(ax1, ay1, ax2, ay2), fracs=(fx1, fy1, fx2, fy2))

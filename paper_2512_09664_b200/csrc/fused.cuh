@@ -1,4 +1,4 @@
-// fused.cuh -- the batched image-pair generator as ONE cluster kernel.
+// fused.cuh -- the batched image-pair generator as ONE persistent cluster kernel.
 //
 // Replaces the body of Sampler._render_batch (reference pipeline.py:278-329):
 // per pair, sample_particles / perturb_frame2 / advect / apply_hiding
@@ -7,23 +7,24 @@
 // (raster.py:154-161) + quantize_u16 (export.py:19-20).
 //
 // Decomposition (B200-first):
-//   * one thread-block CLUSTER per (pair, pass); CTA r of the cluster owns
-//     screen tile (pass * CL + r) of the image for BOTH frames;
-//   * seeding: CTA r generates the particle slice [r*N/CL, (r+1)*N/CL) with
-//     Philox (or reads injected oracle arrays), advects it (bilinear, float64)
-//     and bins it by destination tile -- a distributed counting sort:
-//       count pass -> per-(frame, tile) counts in smem,
-//       one remote atomicAdd per (frame, tile) on the owner's fill counter
-//       reserves a contiguous slot range in the owner's shared memory,
-//       write pass -> records are stored straight into the owner CTA's
-//       shared memory through DSMEM (st.shared::cluster), overflow spills to
-//       a per-CTA global region;
-//   * render: each CTA splats its tile's particle list into a shared-memory
-//     fixed-point (int32, 2^-s units) accumulator; contributions are integers,
-//     so the per-pixel sum is exact and ORDER-INDEPENDENT -> the output bits
-//     do not depend on scheduling, tiling, cluster size or GPU count;
+//   * a persistent grid of thread-block CLUSTERS; each cluster loops over
+//     (pair, pass) work items; CTA r of the cluster owns screen tile
+//     (pass * CL + r) of the image for both frames;
+//   * seeding (one pass): CTA r generates the particle slice
+//     [r*N/CL, (r+1)*N/CL) with Philox4x32-10 in fixed point + float32 (or
+//     reads injected oracle arrays), advects it through the bilinear flow,
+//     and bins every particle by destination tile -- a distributed counting
+//     sort: lanes with the same destination are grouped with match.any, the
+//     group leader reserves a contiguous slot range with ONE remote atomicAdd
+//     on the owner's fill counter, and the render-ready 32-byte records are
+//     stored straight into the owner CTA's shared memory through DSMEM;
+//   * render: each CTA splats its tile's records into a padded shared-memory
+//     fixed-point accumulator (int32, 2^-s units); integer addition is
+//     associative, so the per-pixel sum is exact and ORDER-INDEPENDENT: the
+//     output bits do not depend on scheduling, tiling, cluster size or GPU
+//     count (bit-identical shards);
 //   * fused epilogue: offset + Philox noise + clamp (+ uint16 quantisation),
-//     128-bit coalesced stores of the tile for each frame.
+//     128-bit coalesced streaming stores of each frame of the tile.
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -34,33 +35,35 @@ namespace cg = cooperative_groups;
 
 namespace pgb {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCluster = 16;
-constexpr int kAccShift = 22;     // default fixed-point fraction bits
+constexpr int kAccShift = 22;     // max fixed-point fraction bits
 constexpr int kCellMin = 8;       // coverage-guard cell size floor
 constexpr float kLog2e = 1.4426950408889634f;
 
 enum OutMode { kOutRaw = 0, kOutF32 = 1, kOutU16 = 2, kOutAccum = 3 };
 enum Psf { kPsfPoint = 0, kPsfErf = 1 };
 
-// 32-byte particle record exchanged between CTAs.
-// After setup (point PSF) the fields (amp, sx, sy, rho) hold (L, A, B, C):
-//   value * 2^s = exp2(L - (A dx^2 + B dx dy + C dy^2)),  L = log2(amp) + s.
-// After setup (erf PSF): (amp', isx, isy, slope) -- see setup_erf().
-struct __align__(16) Cand {
+// 32-byte render-ready particle record exchanged between CTAs.
+//   point PSF:  value * 2^s = exp2(L + s - (A dx^2 + B dx dy + C dy^2))
+//   erf PSF:    L = amp', A = 1/(sc sqrt2), B = 1/(sy sqrt2), C = slope, aux = separable
+struct __align__(16) Rec {
   int axy;      // anchor: ax in low 16 bits, ay in high 16 bits (both signed)
   float fx, fy; // sub-pixel offset from the anchor: x - ax, y - ay
-  float amp;
-  float sx, sy, rho;
+  float L;
+  float A, B, C;
   float aux;
 };
 
 struct GenCfg {
   int H, W, n;
   uint32_t k0, k1;
-  double ppp_lo, ppp_hi, d_lo, d_hi, i0_lo, i0_hi, rho_lo, rho_hi;
-  double sigma_ratio, patch_mult, hide_p;
-  double z_lo, z_hi;
+  double ppp_lo, ppp_hi;
+  float d_lo, d_span, i0_lo, i0_span, rho_lo, rho_span, inv_ratio;
+  double patch_mult, d_hi;
+  uint64_t hide_thr;         // visible iff word >= hide_thr  (exactly U >= p)
+  float z_lo, z_span;
   float f2_sigma_std, f2_rho_std, f2_i0_std;
   float dz0, shape, q, w;
   int laser;
@@ -78,8 +81,9 @@ struct InjFrame {
 
 struct FusedParams {
   int H, W, row_lo, row_hi;
-  int TH, TW, tiles_y, tiles_x, tiles, CL, passes;
+  int TH, TW, tiles_y, tiles_x, tiles, CL, passes, th_shift, tw_shift;
   int cap, spill_cap, halo, nframes, cells_cap;
+  int pad, AH, AS;   // accumulator: AH rows x AS ints (tile + pad on each side)
   int n, pairs;
   long long pair_base;
   uint32_t batch_lo;
@@ -99,15 +103,12 @@ struct FusedParams {
   int* st_side;
   float* st_dmax;
   int* bin_counts;
-  Cand* spill;
+  Rec* spill;
   int* overflow;
 };
 
 struct SharedHdr {
   int fill[2];
-  int cnt[2][kMaxCluster];
-  int base[2][kMaxCluster];
-  int cursor[2][kMaxCluster];
   unsigned dmax_bits;
   unsigned amp_bits;
   int cov_max;
@@ -115,13 +116,67 @@ struct SharedHdr {
   double ppp;
 };
 
-struct Particle {
-  double x[2], y[2];
-  float amp[2], sx[2], sy[2], rho[2];
-  bool on[2];
-  float diam;
-  bool active;
+// ----------------------------------------------------------------------------
+// Seeding (generate mode): fixed-point positions, float32 attributes.
+//   x1 = (2 w + 1) W / 2^33 exactly; anchor = floor(x1 + 1/2); the fraction is
+//   rounded once to float32. Advection and all attribute arithmetic are
+//   separately rounded float32 ops (no contraction), restated bit-exactly by
+//   oracle/generate.py.
+// ----------------------------------------------------------------------------
+struct Frame {
+  int ax, ay;
+  float fx, fy;
+  float amp, sx, sy, rho;
+  bool on;
 };
+
+struct Particle {
+  Frame fr[2];
+  float diam, z1;
+  bool active, vis1, vis2;
+};
+
+// Open-interval float32 uniform ((w >> 9) + 1/2) 2^-23: exact, strictly inside (0, 1).
+PGB_HD float unit23(uint32_t w) { return ((float)(w >> 9) + 0.5f) * 0x1p-23f; }
+
+__device__ __forceinline__ float lerpf_exact(float lo, float span, float u) {
+  return __fadd_rn(lo, __fmul_rn(span, u));
+}
+
+// Fixed-point coordinate -> (anchor, fraction), value = F / 2^33.
+__device__ __forceinline__ void fixed_anchor(uint64_t F, int& a, float& f) {
+  const uint64_t an = (F + (1ull << 32)) >> 33;
+  a = (int)an;
+  const long long diff = (long long)(F - (an << 33));
+  f = __double2float_rn((double)diff * 0x1p-33);
+}
+
+// Clamped bilinear cell: x = min(v, N-1), c = min(floor x, N-2), t = x - c.
+__device__ __forceinline__ void fixed_cell(uint64_t F, int N, int& c, float& t) {
+  const uint64_t lim = (uint64_t)(N - 1) << 33;
+  const uint64_t xc = F < lim ? F : lim;
+  int cc = (int)(xc >> 33);
+  const int cmax = N - 2 > 0 ? N - 2 : 0;
+  cc = cc < cmax ? cc : cmax;
+  c = cc;
+  t = __double2float_rn((double)(long long)(xc - ((uint64_t)cc << 33)) * 0x1p-33);
+}
+
+__device__ __forceinline__ float bilerp(float g00, float g01, float g10, float g11, float tx,
+                                        float ty) {
+  const float sx = __fsub_rn(1.0f, tx), sy = __fsub_rn(1.0f, ty);
+  const float top = __fadd_rn(__fmul_rn(sx, g00), __fmul_rn(tx, g01));
+  const float bot = __fadd_rn(__fmul_rn(sx, g10), __fmul_rn(tx, g11));
+  return __fadd_rn(__fmul_rn(sy, top), __fmul_rn(ty, bot));
+}
+
+// Anchor after a displacement d of the point (a, f): t = f + d, k = floor(t + 1/2).
+__device__ __forceinline__ void shift_anchor(int a, float f, float d, int& a2, float& f2) {
+  const float t = __fadd_rn(f, d);
+  const float k = floorf(__fadd_rn(t, 0.5f));
+  a2 = a + (int)k;
+  f2 = __fsub_rn(t, k);
+}
 
 __device__ __forceinline__ float laser_profile(const GenCfg& g, float z) {
   // I0(z) = q exp(-(1/sqrt(2 pi)) |2 z^2 / dZ0^2|^s)
@@ -130,279 +185,264 @@ __device__ __forceinline__ float laser_profile(const GenCfg& g, float z) {
   return g.q * expf(-0.3989422804014327f * p);
 }
 
-// Per-particle seeding (generate mode) or injection (oracle mode).
-template <int MODE>
-__device__ __forceinline__ void make_particle(const FusedParams& P, int pl, int i, int M,
-                                              Particle& pt) {
-  if (MODE == 1) {
-#pragma unroll
-    for (int f = 0; f < 2; ++f) {
-      if (f >= P.nframes) { pt.on[f] = false; continue; }
-      const InjFrame& F = P.inj[f];
-      const size_t o = (size_t)pl * P.n + i;
-      pt.x[f] = F.pos[2 * o];
-      pt.y[f] = F.pos[2 * o + 1];
-      pt.amp[f] = F.i0[o];
-      pt.sx[f] = F.sx[o];
-      pt.sy[f] = F.sy[o];
-      pt.rho[f] = F.rho[o];
-      pt.on[f] = F.mask[o] != 0;
-    }
-    pt.diam = 0.f;
-    pt.active = false;
-    return;
-  }
+__device__ __forceinline__ void gen_particle(const FusedParams& P, int pl, int i, int M,
+                                             Particle& pt) {
   const GenCfg& g = P.g;
-  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
-  const RngKey key{g.k0, g.k1, gpair, P.batch_lo};
-  // sample_particles (particles.py:61-101): positions, diameter, intensity.
+  const RngKey key{g.k0, g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
+  // sample_particles (particles.py:61-101)
   const uint4 a = draw(key, (uint32_t)i, kTagParticleA);
-  const double x1 = dmul(u32_to_unit(a.x), (double)g.W);
-  const double y1 = dmul(u32_to_unit(a.y), (double)g.H);
-  const double d = lerp_exact(g.d_lo, g.d_hi, u32_to_unit(a.z));
-  const double i0 = lerp_exact(g.i0_lo, g.i0_hi, u32_to_unit(a.w));
+  const uint64_t X = (2ull * a.x + 1ull) * (uint64_t)g.W;
+  const uint64_t Y = (2ull * a.y + 1ull) * (uint64_t)g.H;
+  const float d = lerpf_exact(g.d_lo, g.d_span, unit23(a.z));
+  const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
   const bool active = i < M;
-  double rho = g.rho_lo, z1 = 0.0;
+  float rho = g.rho_lo, z1 = 0.f;
   bool vis1 = true, vis2 = true;
   if (g.need_b) {
     const uint4 b = draw(key, (uint32_t)i, kTagParticleB);
-    rho = lerp_exact(g.rho_lo, g.rho_hi, u32_to_unit(b.x));
-    // apply_hiding (particles.py:139-147): visible iff U >= p_hide.
-    vis1 = u32_to_unit(b.y) >= g.hide_p;
-    vis2 = u32_to_unit(b.z) >= g.hide_p;
-    z1 = lerp_exact(g.z_lo, g.z_hi, u32_to_unit(b.w));
+    rho = lerpf_exact(g.rho_lo, g.rho_span, unit23(b.x));
+    vis1 = (uint64_t)b.y >= g.hide_thr;   // apply_hiding (particles.py:139-147)
+    vis2 = (uint64_t)b.z >= g.hide_thr;
+    z1 = lerpf_exact(g.z_lo, g.z_span, unit23(b.w));
   }
-  const float i0f = active ? (float)i0 : 0.f;
-  const float sig = (float)ddiv(d, g.sigma_ratio);
-  const float rhof = (float)rho;
-  float sx2 = sig, sy2 = sig, i02 = i0f, rho2 = rhof;
+  const float i0f = active ? i0 : 0.f;
+  const float sig = __fmul_rn(d, g.inv_ratio);
+  float sx2 = sig, sy2 = sig, i02 = i0f, rho2 = rho;
   if (g.need_perturb) {
-    // perturb_frame2 (particles.py:104-126): zero-mean Gaussian jitter, floors/clamps.
+    // perturb_frame2 (particles.py:104-126)
     const uint4 c = draw(key, (uint32_t)i, kTagPerturb);
     const float2 n01 = box_muller(c.x, c.y);
     const float2 n23 = box_muller(c.z, c.w);
     if (g.f2_sigma_std > 0.f) {
-      sx2 = (float)fmax((double)sig + (double)g.f2_sigma_std * (double)n01.x, 1e-3);
-      sy2 = (float)fmax((double)sig + (double)g.f2_sigma_std * (double)n01.y, 1e-3);
+      sx2 = fmaxf(__fadd_rn(sig, __fmul_rn(g.f2_sigma_std, n01.x)), 1e-3f);
+      sy2 = fmaxf(__fadd_rn(sig, __fmul_rn(g.f2_sigma_std, n01.y)), 1e-3f);
     }
     if (g.f2_i0_std > 0.f) {
-      const double t = fmin(fmax((double)i0f + (double)g.f2_i0_std * (double)n23.x, 0.0), 1.0);
-      i02 = i0f == 0.f ? 0.f : (float)t;
+      const float t = fminf(fmaxf(__fadd_rn(i0f, __fmul_rn(g.f2_i0_std, n23.x)), 0.f), 1.f);
+      i02 = i0f == 0.f ? 0.f : t;
     }
     if (g.f2_rho_std > 0.f) {
-      const double lim = 1.0 - 1e-3;
-      rho2 = (float)fmin(fmax((double)rhof + (double)g.f2_rho_std * (double)n23.y, -lim), lim);
+      const float lim = 0.999f;
+      rho2 = fminf(fmaxf(__fadd_rn(rho, __fmul_rn(g.f2_rho_std, n23.y)), -lim), lim);
     }
   }
   float amp1 = i0f, amp2 = i02;
   if (g.laser) {
-    amp1 *= laser_profile(g, (float)z1);
-    amp2 *= laser_profile(g, (float)z1 + g.w);
+    amp1 *= laser_profile(g, z1);
+    amp2 *= laser_profile(g, z1 + g.w);
   }
-  // advect (particles.py:129-136): one forward-Euler step through the
-  // bilinear field, float64 exactly as the reference.
+  Frame& f1 = pt.fr[0];
+  Frame& f2 = pt.fr[1];
+  fixed_anchor(X, f1.ax, f1.fx);
+  fixed_anchor(Y, f1.ay, f1.fy);
+  // advect (particles.py:129-136): bilinear, edge-clamped (flowfield.py:207-232)
+  int cx, cy;
+  float tx, ty;
+  fixed_cell(X, g.W, cx, tx);
+  fixed_cell(Y, g.H, cy, ty);
   const long long field = (P.pair_base + pl) / P.pairs_per_field;
   const float2* flow = P.flows + (size_t)field * P.field_elems;
-  double u, v;
-  sample_flow_exact(flow, g.H, g.W, x1, y1, &u, &v);
-  pt.x[0] = x1;
-  pt.y[0] = y1;
-  pt.x[1] = dadd(x1, u);
-  pt.y[1] = dadd(y1, v);
-  pt.amp[0] = amp1;
-  pt.amp[1] = amp2;
-  pt.sx[0] = sig;
-  pt.sy[0] = sig;
-  pt.rho[0] = rhof;
-  pt.sx[1] = sx2;
-  pt.sy[1] = sy2;
-  pt.rho[1] = rho2;
-  // contribution_mask (raster.py:86-88): active & visible & i0 > 0.
-  pt.on[0] = active && vis1 && amp1 > 0.f;
-  pt.on[1] = active && vis2 && amp2 > 0.f;
-  pt.diam = (float)d;
+  const int cx1 = cx + 1 < g.W ? cx + 1 : g.W - 1;
+  const int cy1 = cy + 1 < g.H ? cy + 1 : g.H - 1;
+  const float2 q00 = __ldg(flow + (size_t)cy * g.W + cx);
+  const float2 q01 = __ldg(flow + (size_t)cy * g.W + cx1);
+  const float2 q10 = __ldg(flow + (size_t)cy1 * g.W + cx);
+  const float2 q11 = __ldg(flow + (size_t)cy1 * g.W + cx1);
+  const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
+  const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
+  shift_anchor(f1.ax, f1.fx, u, f2.ax, f2.fx);
+  shift_anchor(f1.ay, f1.fy, v, f2.ay, f2.fy);
+  f1.amp = amp1; f1.sx = sig; f1.sy = sig; f1.rho = rho;
+  f2.amp = amp2; f2.sx = sx2; f2.sy = sy2; f2.rho = rho2;
+  // contribution_mask (raster.py:86-88): active & visible & i0 > 0
+  f1.on = active && vis1 && amp1 > 0.f;
+  f2.on = active && vis2 && amp2 > 0.f;
+  pt.diam = d;
+  pt.z1 = z1;
   pt.active = active;
+  pt.vis1 = vis1 && active;
+  pt.vis2 = vis2 && active;
 }
 
-// Anchor = nearest pixel floor(x + 0.5) (_native.pyx:31-32); returns false
-// when the (2*halo+1)^2 window misses the covered region entirely.
-__device__ __forceinline__ bool anchor_of(const FusedParams& P, double x, double y, int& ax,
-                                          int& ay) {
-  const double fxa = floor(dadd(x, 0.5));
-  const double fya = floor(dadd(y, 0.5));
-  const int hx = P.halo;
-  if (!(fxa >= (double)(-hx) && fxa <= (double)(P.W - 1 + hx))) return false;
-  if (!(fya >= (double)(P.row_lo - hx) && fya <= (double)(P.row_hi - 1 + hx))) return false;
-  ax = (int)fxa;
-  ay = (int)fya;
-  return true;
+// Oracle mode: float64 positions from the reference; anchor = floor(x + 1/2)
+// (_native.pyx:31-32), fraction rounded once to float32.
+__device__ __forceinline__ void inject_particle(const FusedParams& P, int pl, int i,
+                                                Particle& pt) {
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    Frame& fr = pt.fr[f];
+    fr.on = false;
+    if (f >= P.nframes) continue;
+    const InjFrame& F = P.inj[f];
+    const size_t o = (size_t)pl * P.n + i;
+    if (!F.mask[o]) continue;
+    const double x = F.pos[2 * o], y = F.pos[2 * o + 1];
+    const double fxa = floor(dadd(x, 0.5)), fya = floor(dadd(y, 0.5));
+    // far-away particles are rejected by the window test; keep int conversion safe
+    if (!(fabs(fxa) < 1e8 && fabs(fya) < 1e8)) continue;
+    fr.ax = (int)fxa;
+    fr.ay = (int)fya;
+    fr.fx = (float)dsub(x, fxa);
+    fr.fy = (float)dsub(y, fya);
+    fr.amp = F.i0[o];
+    fr.sx = F.sx[o];
+    fr.sy = F.sy[o];
+    fr.rho = F.rho[o];
+    fr.on = true;
+  }
+  pt.diam = 0.f;
+  pt.active = false;
 }
 
-// Destination tiles of a window, restricted to this pass. Calls fn(rank).
-template <typename Fn>
-__device__ __forceinline__ void for_each_dest(const FusedParams& P, int pass, int ax, int ay,
-                                              Fn&& fn) {
-  const int hx = P.halo;
-  const int rlo = max(ay - hx, P.row_lo) - P.row_lo;
-  const int rhi = min(ay + hx, P.row_hi - 1) - P.row_lo;
-  const int clo = max(ax - hx, 0);
-  const int chi = min(ax + hx, P.W - 1);
-  const int ty0 = rlo / P.TH, ty1 = rhi / P.TH;
-  const int tx0 = clo / P.TW, tx1 = chi / P.TW;
-  const int t_lo = pass * P.CL;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      const int d = ty * P.tiles_x + tx - t_lo;
-      if (d >= 0 && d < P.CL) fn(d);
-    }
+__device__ __forceinline__ Rec make_rec(const Frame& fr, int psf) {
+  Rec r;
+  r.axy = (fr.ay << 16) | (fr.ax & 0xffff);
+  r.fx = fr.fx;
+  r.fy = fr.fy;
+  const float sx = fr.sx, sy = fr.sy, rho = fr.rho;
+  if (psf == kPsfPoint) {
+    const float q = 1.0f - rho * rho;
+    r.A = 0.5f * kLog2e / (q * sx * sx);
+    r.C = 0.5f * kLog2e / (q * sy * sy);
+    r.B = -kLog2e * rho / (q * sx * sy);
+    r.L = __log2f(fr.amp);
+    r.aux = fr.amp;
+  } else {
+    const float k = 1.2533141373155001f;  // sqrt(pi/2)
+    const float sc = sx * sqrtf(fmaxf(1.0f - rho * rho, 0.f));
+    const bool sep = rho == 0.f;
+    r.L = sep ? fr.amp * (k * sx) * (k * sy) : fr.amp * (k * sc);
+    r.A = 0.70710678118654752f / sc;
+    r.B = 0.70710678118654752f / sy;
+    r.C = rho * sx / sy;
+    r.aux = sep ? 1.f : 0.f;
+  }
+  return r;
 }
 
+// ----------------------------------------------------------------------------
+// Render: lanes = (candidate slot, patch column); each lane walks the rows.
+// ----------------------------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-// Round a non-negative value < 2^22 (+ a few ulp) to the nearest integer
-// with two full-rate ALU ops (magic-number add), avoiding the F2I pipe.
+// Round a non-negative value <= 2^22 (+ a few ulp) to the nearest integer with
+// two full-rate ALU ops (magic-number add), avoiding the conversion pipe.
 __device__ __forceinline__ int round_small(float v) {
   return __float_as_int(v + 12582912.0f) - 0x4B400000;
 }
 
-__device__ __forceinline__ void setup_point(Cand& c, float s_scale_log2) {
-  const float sx = c.sx, sy = c.sy, r = c.rho;
-  const float q = 1.0f - r * r;
-  const float a = 0.5f / (q * sx * sx);
-  const float b = r / (q * sx * sy);
-  const float cc = 0.5f / (q * sy * sy);
-  c.sx = a * kLog2e;
-  c.sy = -b * kLog2e;
-  c.rho = cc * kLog2e;
-  c.amp = (c.amp > 0.f ? __log2f(c.amp) : -INFINITY) + s_scale_log2;
-}
-
-// erf PSF: pixel-area mean of Eq. (1) over [c-1/2, c+1/2] x [r-1/2, r+1/2].
-//   x | y is Gaussian with mean x0 + slope (y - y0), std sc = sx sqrt(1 - rho^2):
-//   value = amp * int_dy exp(-dy^2 / (2 sy^2)) * sc sqrt(pi/2) [erf(.)-erf(.)] dy
-// rho == 0: closed form in y as well.
 constexpr int kGLPoints = 8;
-__constant__ float kGLx[kGLPoints] = {-0.4801449282487681f, -0.3983332387068134f,
-                                       -0.2627662050032837f, -0.0916173212478249f,
-                                       0.0916173212478249f,  0.2627662050032837f,
-                                       0.3983332387068134f,  0.4801449282487681f};
-__constant__ float kGLw[kGLPoints] = {0.0506142681451881f, 0.1111905172266872f,
-                                       0.1568533229389436f, 0.1813418916891810f,
-                                       0.1813418916891810f, 0.1568533229389436f,
-                                       0.1111905172266872f, 0.0506142681451881f};
+__constant__ float kGLx[kGLPoints] = {-0.48014492824876809f, -0.39833323870681336f, -0.2627662049581645f, -0.09171732124782489f, 0.091717321247824893f, 0.2627662049581645f, 0.39833323870681336f, 0.48014492824876809f};
+__constant__ float kGLw[kGLPoints] = {0.050614268145188532f, 0.11119051722668721f, 0.15685332293894344f, 0.18134189168918083f, 0.18134189168918083f, 0.15685332293894344f, 0.11119051722668721f, 0.050614268145188532f};
 
-__device__ __forceinline__ void setup_erf(Cand& c, float scale) {
-  const float sx = c.sx, sy = c.sy, r = c.rho;
-  const float sc = sx * sqrtf(fmaxf(1.0f - r * r, 0.f));
-  const float k = 1.2533141373155001f;  // sqrt(pi/2)
-  c.aux = (r == 0.f) ? 1.f : 0.f;
-  if (r == 0.f) c.amp = c.amp * scale * (k * sx) * (k * sy);
-  else c.amp = c.amp * scale * (k * sc);
-  c.sx = 0.70710678118654752f / sc;        // 1 / (sc sqrt 2)
-  c.rho = r * sx / sy;                       // slope of the conditional mean
-  c.sy = 0.70710678118654752f / sy;        // 1 / (sy sqrt 2)
-}
-
-__device__ __forceinline__ const Cand* cand_at(const Cand* local, const Cand* spill, int cap,
-                                               int k) {
-  return k < cap ? local + k : spill + (k - cap);
-}
-
-// Accumulate one (candidate, patch row) work item.
-template <int SIDE, int PSF>
-__device__ __forceinline__ void splat_row(int* __restrict__ acc, const Cand& c, int side_rt,
-                                          int i, int r0, int nr, int c0, int nc, int TW) {
-  const int side = SIDE > 0 ? SIDE : side_rt;
-  const int h = side >> 1;
-  const int ay = c.axy >> 16;
-  const int ax = (int)(short)(c.axy & 0xffff);
-  const int row = ay - h + i - r0;
-  if ((unsigned)row >= (unsigned)nr) return;
-  const int col0 = ax - h - c0;
-  int* base = acc + row * TW + col0;
-  const float dy = (float)(i - h) - c.fy;
+template <int S, int PSF>
+__device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, int side, int j,
+                                           int r0p, int c0p, int AS, float s_log2, float scale) {
+  const int side_ = S > 0 ? S : side;
+  const int h = side_ >> 1;
+  const int ay = r.axy >> 16;
+  const int ax = (int)(short)(r.axy & 0xffff);
+  int* p = acc + (ay - h - r0p) * AS + (ax - h + j - c0p);
+  const float dx = (float)(j - h) - r.fx;
   if (PSF == kPsfPoint) {
-    const float Ly = fmaf(-c.rho * dy, dy, c.amp);
-    const float By = c.sy * dy;
+    const float Lx = fmaf(-r.A * dx, dx, r.L + s_log2);
+    const float Bdx = r.B * dx;
 #pragma unroll
-    for (int j = 0; j < (SIDE > 0 ? SIDE : 64); ++j) {
-      if (SIDE == 0 && j >= side) break;
-      const float dx = (float)(j - h) - c.fx;
-      const float t = fmaf(c.sx, dx, By);
-      const float e = fmaf(-t, dx, Ly);
-      const int q = round_small(ex2_approx(e));
-      if ((unsigned)(col0 + j) < (unsigned)nc) atomicAdd(base + j, q);
+    for (int i = 0; i < (S > 0 ? S : 64); ++i) {
+      if (S == 0 && i >= side_) break;
+      const float dy = (float)(i - h) - r.fy;
+      const float t = fmaf(r.C, dy, Bdx);
+      const float e = fmaf(-t, dy, Lx);
+      atomicAdd(p + i * AS, round_small(ex2_approx(e)));
     }
   } else {
-    // erf PSF
-    float wrow = 1.f;
-    const bool sep = c.aux != 0.f;
-    if (sep) wrow = erff((dy + 0.5f) * c.sy) - erff((dy - 0.5f) * c.sy);
-    float eprev = 0.f;
-    for (int j = 0; j <= side; ++j) {
-      const float dxl = (float)(j - h) - c.fx - 0.5f;  // left edge of column j
-      float val = 0.f;
+    const bool sep = r.aux != 0.f;
+    float ex = 0.f;
+    if (sep) ex = erff((dx + 0.5f) * r.A) - erff((dx - 0.5f) * r.A);
+    for (int i = 0; i < side_; ++i) {
+      const float dy = (float)(i - h) - r.fy;
+      float val;
       if (sep) {
-        const float e = erff(dxl * c.sx);
-        if (j > 0) val = (e - eprev) * wrow;
-        eprev = e;
-      } else if (j > 0) {
-        const float dxc = dxl - 0.5f;  // centre of column j-1 relative to x0
+        val = ex * (erff((dy + 0.5f) * r.B) - erff((dy - 0.5f) * r.B));
+      } else {
         float s = 0.f;
 #pragma unroll
-        for (int g = 0; g < kGLPoints; ++g) {
-          const float yy = dy + kGLx[g];
-          const float mu = c.rho * yy;               // conditional mean offset
-          const float gy = __expf(-yy * yy * (c.sy * c.sy));  // exp(-yy^2/(2 sy^2))
-          const float hi = erff((dxc + 0.5f - mu) * c.sx);
-          const float lo = erff((dxc - 0.5f - mu) * c.sx);
-          s = fmaf(kGLw[g] * gy, hi - lo, s);
+        for (int gq = 0; gq < kGLPoints; ++gq) {
+          const float yy = dy + kGLx[gq];
+          const float mu = r.C * yy;
+          const float gy = __expf(-yy * yy * (r.B * r.B));
+          const float hi = erff((dx + 0.5f - mu) * r.A);
+          const float lo = erff((dx - 0.5f - mu) * r.A);
+          s = fmaf(kGLw[gq] * gy, hi - lo, s);
         }
         val = s;
       }
-      if (j > 0) {
-        const int jj = j - 1;
-        const int q = __float2int_rn(val * c.amp);
-        if ((unsigned)(col0 + jj) < (unsigned)nc && q != 0) atomicAdd(base + jj, q);
-      }
+      const int q = __float2int_rn(val * r.L * scale);
+      if (q) atomicAdd(p + i * AS, q);
     }
   }
 }
 
-template <int SIDE, int PSF>
-__device__ void splat_items(int* __restrict__ acc, const Cand* __restrict__ local,
-                            const Cand* __restrict__ spill, int cap, int K, int side, int r0,
-                            int nr, int c0, int nc, int TW) {
-  const int total = K * side;
-  const float inv = 1.0f / (float)side;
-  for (int w = threadIdx.x; w < total; w += kThreads) {
-    int k = (int)(((float)w + 0.5f) * inv);  // exact for w < 2^22
-    int i = w - k * side;
-    const Cand c = *cand_at(local, spill, cap, k);
-    splat_row<SIDE, PSF>(acc, c, side, i, r0, nr, c0, nc, TW);
+template <int S, int PSF>
+__device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ local,
+                           const Rec* __restrict__ spill, int cap, int K, int side, int r0p,
+                           int c0p, int AS, float s_log2, float scale) {
+  const int side_ = S > 0 ? S : side;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (side_ <= 32) {
+    const int cpw = 32 / side_;                       // candidates per warp-step
+    const int slot = lane / side_;
+    const int j = lane - slot * side_;
+    if (slot >= cpw) return;
+    for (int kb = warp * cpw; kb < K; kb += kWarps * cpw) {
+      const int k = kb + slot;
+      if (k >= K) break;
+      const Rec r = k < cap ? local[k] : spill[k - cap];
+      splat_lane<S, PSF>(acc, r, side_, j, r0p, c0p, AS, s_log2, scale);
+    }
+  } else {
+    // very large patches: the warp walks one candidate, lanes stride the columns
+    for (int k = warp; k < K; k += kWarps) {
+      const Rec r = k < cap ? local[k] : spill[k - cap];
+      for (int jj = lane; jj < side_; jj += 32)
+        splat_lane<0, PSF>(acc, r, side_, jj, r0p, c0p, AS, s_log2, scale);
+    }
   }
 }
 
 template <int PSF>
-__device__ void splat_dispatch(int* acc, const Cand* local, const Cand* spill, int cap, int K,
-                               int side, int r0, int nr, int c0, int nc, int TW) {
+__device__ void splat_dispatch(int* acc, const Rec* local, const Rec* spill, int cap, int K,
+                               int side, int r0p, int c0p, int AS, float s_log2, float scale) {
   if (PSF == kPsfPoint) {
     switch (side) {
-      case 3: splat_items<3, PSF>(acc, local, spill, cap, K, side, r0, nr, c0, nc, TW); return;
-      case 5: splat_items<5, PSF>(acc, local, spill, cap, K, side, r0, nr, c0, nc, TW); return;
-      case 7: splat_items<7, PSF>(acc, local, spill, cap, K, side, r0, nr, c0, nc, TW); return;
-      case 9: splat_items<9, PSF>(acc, local, spill, cap, K, side, r0, nr, c0, nc, TW); return;
-      case 13: splat_items<13, PSF>(acc, local, spill, cap, K, side, r0, nr, c0, nc, TW); return;
+      case 3: splat_tile<3, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
+      case 5: splat_tile<5, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
+      case 7: splat_tile<7, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
+      case 9: splat_tile<9, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
+      case 11: splat_tile<11, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
+      case 13: splat_tile<13, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
       default: break;
     }
   }
-  splat_items<0, PSF>(acc, local, spill, cap, K, side, r0, nr, c0, nc, TW);
+  splat_tile<0, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale);
 }
 
+// Largest fixed-point shift s <= kAccShift with cnt * (amp_max * 2^s + 1/2) < 2^31.
+__device__ __forceinline__ int shift_for(int cnt, float amp_max) {
+  const double per = (2147483648.0 / (double)cnt - 0.5) / (double)amp_max;
+  if (!(per >= 1.0)) return 0;
+  int e = ilogb(per);                      // floor(log2(per)), exact
+  return e < kAccShift ? e : kAccShift;
+}
+
+// ----------------------------------------------------------------------------
+// Epilogue
+// ----------------------------------------------------------------------------
 // Pixel noise: Philox(quad = p >> 2, pair, batch, kTagNoise + frame) ->
 // two Box-Muller pairs -> normals for pixels 4q .. 4q+3.
 __device__ __forceinline__ float4 noise4(uint32_t k0, uint32_t k1, uint32_t gpair,
@@ -425,46 +465,77 @@ __device__ __forceinline__ uint16_t quant_u16(float x) {
   return (uint16_t)__float2int_rn(y);
 }
 
-// Epilogue for one frame of one tile: convert, finalize, store, re-zero acc.
-__device__ void store_tile(const FusedParams& P, int* __restrict__ acc, int pl, int f, int r0,
-                           int nr, int c0, int nc, float inv_scale) {
+// int accumulator (>= 0, < 2^23) -> float with two ALU ops.
+__device__ __forceinline__ float acc_to_float(int a) {
+  return __int_as_float(a | 0x4B000000) - 8388608.0f;
+}
+
+__device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, int pl, int f,
+                           int r0, int nr, int c0, int nc, float inv_scale) {
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
-  const int TW = P.TW;
+  const int AS = P.AS, pad = P.pad;
   const size_t pair_off = (size_t)pl * (size_t)P.out_pair_elems;
-  const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0) && ((TW & 3) == 0);
+  const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
   const int mode = P.out_mode;
   const float bg = P.bg_offset, sd = P.noise_std;
   if (vec) {
-    const int qpr = nc >> 2;  // quads per row
+    const int qpr = nc >> 2;
+    // Fast path: a power-of-two number of quads per row that divides the block:
+    // every thread owns one fixed column quad and walks rows with pointer steps.
+    const bool fast = (qpr & (qpr - 1)) == 0 && qpr <= kThreads;
+    const int cq = fast ? (threadIdx.x & (qpr - 1)) : 0;
+    const int row0 = fast ? (threadIdx.x >> __ffs(qpr) - 1) : 0;
+    const int rstep = fast ? kThreads / qpr : 0;
+    const uint32_t magic = fast ? 0u : (uint32_t)((0x100000000ull + qpr - 1) / qpr);
     const int total = nr * qpr;
-    for (int e = threadIdx.x; e < total; e += kThreads) {
-      const int row = e / qpr;
-      const int cq = e - row * qpr;
-      int4* ap = reinterpret_cast<int4*>(acc + row * TW + cq * 4);
-      const int4 a = *ap;
-      *ap = make_int4(0, 0, 0, 0);
-      float4 v = make_float4((float)a.x * inv_scale, (float)a.y * inv_scale,
-                             (float)a.z * inv_scale, (float)a.w * inv_scale);
-      const size_t p = (size_t)(r0 + row) * P.W + (size_t)(c0 + cq * 4);
+    const char* outb = static_cast<const char*>(P.out[f]);
+    const size_t esz = mode == kOutU16 ? 2 : 4;
+    for (int e = threadIdx.x, rowf = row0; e < total; e += kThreads, rowf += rstep) {
+      int row, c;
+      if (fast) {
+        if (rowf >= nr) break;
+        row = rowf;
+        c = cq;
+      } else {
+        row = (int)__umulhi((uint32_t)e, magic);
+        c = e - row * qpr;
+      }
+      const int4 a = *reinterpret_cast<const int4*>(acc + (row + pad) * AS + pad + c * 4);
+      float4 v;
+      if ((a.x | a.y | a.z | a.w) >= (1 << 23)) {
+        v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
+      } else {
+        v = make_float4(acc_to_float(a.x), acc_to_float(a.y), acc_to_float(a.z), acc_to_float(a.w));
+      }
+      const size_t p = (size_t)(r0 + row) * P.W + (size_t)(c0 + c * 4);
+      char* dst = const_cast<char*>(outb) + (pair_off + p) * esz;
       if (mode == kOutRaw) {
-        reinterpret_cast<float4*>(static_cast<float*>(P.out[f]) + pair_off + p)[0] = v;
+        v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
+        __stcs(reinterpret_cast<float4*>(dst), v);
       } else if (mode == kOutAccum) {
-        float4* o = reinterpret_cast<float4*>(static_cast<float*>(P.out[f]) + pair_off + p);
+        float4* o = reinterpret_cast<float4*>(dst);
         float4 old = *o;
-        old.x += v.x; old.y += v.y; old.z += v.z; old.w += v.w;
+        old.x = fmaf(v.x, inv_scale, old.x); old.y = fmaf(v.y, inv_scale, old.y);
+        old.z = fmaf(v.z, inv_scale, old.z); old.w = fmaf(v.w, inv_scale, old.w);
         *o = old;
       } else {
-        float4 nz = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (sd > 0.f) nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
-        v.x = finalize_px(v.x, bg, sd, nz.x);
-        v.y = finalize_px(v.y, bg, sd, nz.y);
-        v.z = finalize_px(v.z, bg, sd, nz.z);
-        v.w = finalize_px(v.w, bg, sd, nz.w);
+        if (sd > 0.f) {
+          const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
+          v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
+          v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
+          v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
+          v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
+        } else {
+          v.x = fminf(fmaxf(fmaf(v.x, inv_scale, bg), 0.f), 1.f);
+          v.y = fminf(fmaxf(fmaf(v.y, inv_scale, bg), 0.f), 1.f);
+          v.z = fminf(fmaxf(fmaf(v.z, inv_scale, bg), 0.f), 1.f);
+          v.w = fminf(fmaxf(fmaf(v.w, inv_scale, bg), 0.f), 1.f);
+        }
         if (mode == kOutF32) {
-          reinterpret_cast<float4*>(static_cast<float*>(P.out[f]) + pair_off + p)[0] = v;
+          __stcs(reinterpret_cast<float4*>(dst), v);
         } else {
           ushort4 u = make_ushort4(quant_u16(v.x), quant_u16(v.y), quant_u16(v.z), quant_u16(v.w));
-          reinterpret_cast<ushort4*>(static_cast<uint16_t*>(P.out[f]) + pair_off + p)[0] = u;
+          __stcs(reinterpret_cast<ushort4*>(dst), u);
         }
       }
     }
@@ -473,9 +544,7 @@ __device__ void store_tile(const FusedParams& P, int* __restrict__ acc, int pl, 
     for (int e = threadIdx.x; e < total; e += kThreads) {
       const int row = e / nc;
       const int col = e - row * nc;
-      int* ap = acc + row * TW + col;
-      float v = (float)(*ap) * inv_scale;
-      *ap = 0;
+      float v = (float)acc[(row + pad) * AS + pad + col] * inv_scale;
       const size_t p = (size_t)(r0 + row) * P.W + (size_t)(c0 + col);
       if (mode == kOutRaw) {
         static_cast<float*>(P.out[f])[pair_off + p] = v;
@@ -485,8 +554,8 @@ __device__ void store_tile(const FusedParams& P, int* __restrict__ acc, int pl, 
         float nzv = 0.f;
         if (sd > 0.f) {
           const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
-          const int j = (int)(p & 3);
-          nzv = j == 0 ? nz.x : (j == 1 ? nz.y : (j == 2 ? nz.z : nz.w));
+          const int jn = (int)(p & 3);
+          nzv = jn == 0 ? nz.x : (jn == 1 ? nz.y : (jn == 2 ? nz.z : nz.w));
         }
         v = finalize_px(v, bg, sd, nzv);
         if (mode == kOutF32) static_cast<float*>(P.out[f])[pair_off + p] = v;
@@ -494,6 +563,38 @@ __device__ void store_tile(const FusedParams& P, int* __restrict__ acc, int pl, 
       }
     }
   }
+}
+
+// ----------------------------------------------------------------------------
+// Exchange: lanes with the same destination are grouped with match.any; the
+// leader reserves a slot range with ONE remote atomicAdd; records go straight
+// to the owner's shared memory through DSMEM.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void exchange(cg::cluster_group& cluster, const FusedParams& P,
+                                         SharedHdr* sh, Rec* rec_base, int cluster_first, int f,
+                                         int dest, const Rec& r) {
+  const int lane = threadIdx.x & 31;
+  const unsigned peers = __match_any_sync(~0u, dest);
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (dest >= 0 && lane == leader)
+    base = atomicAdd(cluster.map_shared_rank(&sh->fill[f], dest), __popc(peers));
+  base = __shfl_sync(~0u, base, leader);
+  if (dest < 0) return;
+  const int slot = base + __popc(peers & ((1u << lane) - 1u));
+  Rec* dst;
+  if (slot < P.cap) {
+    dst = cluster.map_shared_rank(rec_base, dest) + (size_t)f * P.cap + slot;
+  } else if (slot - P.cap < P.spill_cap) {
+    dst = P.spill + ((size_t)(cluster_first + dest) * 2 + f) * P.spill_cap + (slot - P.cap);
+  } else {
+    atomicAdd(P.overflow, 1);
+    return;
+  }
+  const float4* s4 = reinterpret_cast<const float4*>(&r);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  d4[0] = s4[0];
+  d4[1] = s4[1];
 }
 
 template <int MODE, int PSF>
@@ -508,17 +609,18 @@ __global__ void __launch_bounds__(kThreads, 2) fused_generate_kernel(const Fused
 
   extern __shared__ __align__(16) unsigned char smem[];
   int* acc = reinterpret_cast<int*>(smem);
-  Cand* cand = reinterpret_cast<Cand*>(smem + (size_t)P.TH * P.TW * sizeof(int));
-  SharedHdr* sh = reinterpret_cast<SharedHdr*>(cand + (size_t)P.nframes * P.cap);
+  const int acc_ints = P.AH * P.AS;
+  Rec* rec = reinterpret_cast<Rec*>(smem + (size_t)acc_ints * sizeof(int));
+  SharedHdr* sh = reinterpret_cast<SharedHdr*>(rec + (size_t)P.nframes * P.cap);
   int* cells = reinterpret_cast<int*>(sh + 1);
-  // this CTA's private spill region (persistent grid => bounded footprint)
-  Cand* my_spill = P.spill + (size_t)blockIdx.x * 2 * P.spill_cap;
+  Rec* my_spill = P.spill + (size_t)blockIdx.x * 2 * P.spill_cap;
 
-  {
-    int4* a4 = reinterpret_cast<int4*>(acc);
-    const int n4 = (P.TH * P.TW) >> 2;
-    for (int e = tid; e < n4; e += kThreads) a4[e] = make_int4(0, 0, 0, 0);
-  }
+  for (int e = tid; e < (acc_ints >> 2); e += kThreads)
+    reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
+
+  // this CTA's particle slice (fixed for every item)
+  const int i_lo = (int)((long long)rank * P.n / CL);
+  const int i_hi = (int)((long long)(rank + 1) * P.n / CL);
 
   const int items = P.pairs * P.passes;
   for (int item = cid; item < items; item += nclusters) {
@@ -526,10 +628,6 @@ __global__ void __launch_bounds__(kThreads, 2) fused_generate_kernel(const Fused
     const int pass = item - pl * P.passes;
 
     // ---- init (local state only; remote traffic starts after the sync) -----
-    if (tid < 2 * kMaxCluster) {
-      (&sh->cnt[0][0])[tid] = 0;
-      (&sh->cursor[0][0])[tid] = 0;
-    }
     if (tid == 0) {
       sh->fill[0] = sh->fill[1] = 0;
       sh->dmax_bits = 0u;
@@ -552,76 +650,69 @@ __global__ void __launch_bounds__(kThreads, 2) fused_generate_kernel(const Fused
     cluster.sync();
     const int M = sh->M;
 
-    const long long n = P.n;
-    const int i_lo = (int)((long long)rank * n / CL);
-    const int i_hi = (int)((long long)(rank + 1) * n / CL);
-
-    // ---- count pass: bin this slice by destination tile --------------------
-    unsigned dmax_local = 0u;
-    for (int i = i_lo + tid; i < i_hi; i += kThreads) {
+    // ---- seeding + distributed binning (one pass) ----------------------------
+    const int hx = P.halo;
+    const int t_lo = pass * CL;
+    unsigned dmax_local = 0u, amp_local = 0u;
+    for (int base = i_lo; base < i_hi; base += kThreads) {
+      const int i = base + tid;
       Particle pt;
-      make_particle<MODE>(P, pl, i, M, pt);
+      if (i < i_hi) {
+        if (MODE == 0) gen_particle(P, pl, i, M, pt);
+        else inject_particle(P, pl, i, pt);
+      } else {
+        pt.fr[0].on = pt.fr[1].on = false;
+        pt.active = false;
+      }
       if (MODE == 0 && pt.active) dmax_local = max(dmax_local, __float_as_uint(pt.diam));
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
-        if (f >= P.nframes || !pt.on[f]) continue;
-        int ax, ay;
-        if (!anchor_of(P, pt.x[f], pt.y[f], ax, ay)) continue;
-        for_each_dest(P, pass, ax, ay, [&](int d) { atomicAdd(&sh->cnt[f][d], 1); });
-      }
-    }
-    if (MODE == 0) {
-      for (int o = 16; o > 0; o >>= 1)
-        dmax_local = max(dmax_local, __shfl_xor_sync(~0u, dmax_local, o));
-      if ((tid & 31) == 0 && dmax_local) atomicMax(&sh->dmax_bits, dmax_local);
-    }
-    __syncthreads();
-    // ---- reserve contiguous slot ranges in the owners' shared memory -------
-    if (tid < P.nframes * CL) {
-      const int f = tid / CL, d = tid - (tid / CL) * CL;
-      const int c = sh->cnt[f][d];
-      if (c > 0) sh->base[f][d] = atomicAdd(cluster.map_shared_rank(&sh->fill[f], d), c);
-    } else if (MODE == 0 && tid >= 64 && tid < 64 + CL) {
-      const unsigned m = sh->dmax_bits;
-      if (m) atomicMax(cluster.map_shared_rank(&sh->dmax_bits, tid - 64), m);
-    }
-    __syncthreads();
-
-    // ---- write pass: regenerate, store records into the owners' smem -------
-    for (int i = i_lo + tid; i < i_hi; i += kThreads) {
-      Particle pt;
-      make_particle<MODE>(P, pl, i, M, pt);
-#pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        if (f >= P.nframes || !pt.on[f]) continue;
-        int ax, ay;
-        if (!anchor_of(P, pt.x[f], pt.y[f], ax, ay)) continue;
-        Cand rec;
-        rec.axy = (ay << 16) | (ax & 0xffff);
-        rec.fx = (float)dsub(pt.x[f], (double)ax);
-        rec.fy = (float)dsub(pt.y[f], (double)ay);
-        rec.amp = pt.amp[f];
-        rec.sx = pt.sx[f];
-        rec.sy = pt.sy[f];
-        rec.rho = pt.rho[f];
-        rec.aux = 0.f;
-        for_each_dest(P, pass, ax, ay, [&](int d) {
-          const int slot = sh->base[f][d] + atomicAdd(&sh->cursor[f][d], 1);
-          Cand* dst;
-          if (slot < P.cap) {
-            dst = cluster.map_shared_rank(cand, d) + (size_t)f * P.cap + slot;
-          } else if (slot - P.cap < P.spill_cap) {
-            dst = P.spill + ((size_t)(cluster_first + d) * 2 + f) * P.spill_cap + (slot - P.cap);
-          } else {
-            atomicAdd(P.overflow, 1);
-            return;
+        if (f >= P.nframes) break;
+        const Frame& fr = pt.fr[f];
+        // destination tiles of the (2 hx + 1)^2 window within this pass
+        int ty0 = 1, ty1 = 0, tx0 = 1, tx1 = 0;
+        if (fr.on) {
+          const int rlo = max(fr.ay - hx, P.row_lo), rhi = min(fr.ay + hx, P.row_hi - 1);
+          const int clo = max(fr.ax - hx, 0), chi = min(fr.ax + hx, P.W - 1);
+          if (rlo <= rhi && clo <= chi) {
+            ty0 = (rlo - P.row_lo) >> P.th_shift;
+            ty1 = (rhi - P.row_lo) >> P.th_shift;
+            tx0 = clo >> P.tw_shift;
+            tx1 = chi >> P.tw_shift;
           }
-          const float4* s4 = reinterpret_cast<const float4*>(&rec);
-          float4* d4 = reinterpret_cast<float4*>(dst);
-          d4[0] = s4[0];
-          d4[1] = s4[1];
-        });
+        }
+        const int nty = ty1 - ty0 + 1, ntx = tx1 - tx0 + 1;
+        const int ndest = (nty > 0 && ntx > 0) ? nty * ntx : 0;
+        Rec r;
+        if (ndest) {
+          r = make_rec(fr, P.psf);
+          amp_local = max(amp_local, __float_as_uint(fr.amp));
+        }
+        for (int e = 0; __any_sync(~0u, e < ndest); ++e) {
+          int dest = -1;
+          if (e < ndest) {
+            const int q = ntx == 1 ? e : e / ntx;
+            const int ty = ty0 + q, tx = tx0 + (e - q * ntx);
+            const int d = ty * P.tiles_x + tx - t_lo;
+            if (d >= 0 && d < CL) dest = d;
+          }
+          exchange(cluster, P, sh, rec, cluster_first, f, dest, r);
+        }
       }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      dmax_local = max(dmax_local, __shfl_xor_sync(~0u, dmax_local, o));
+      amp_local = max(amp_local, __shfl_xor_sync(~0u, amp_local, o));
+    }
+    if ((tid & 31) == 0) {
+      if (dmax_local) atomicMax(&sh->dmax_bits, dmax_local);
+      if (amp_local) atomicMax(&sh->amp_bits, amp_local);
+    }
+    __syncthreads();
+    if (tid < CL) {
+      const unsigned m = sh->dmax_bits, am = sh->amp_bits;
+      if (m) atomicMax(cluster.map_shared_rank(&sh->dmax_bits, tid), m);
+      if (am) atomicMax(cluster.map_shared_rank(&sh->amp_bits, tid), am);
     }
     cluster.sync();
 
@@ -631,8 +722,9 @@ __global__ void __launch_bounds__(kThreads, 2) fused_generate_kernel(const Fused
     float dmax = 0.f;
     if (MODE == 0) {
       dmax = __uint_as_float(sh->dmax_bits);
+      // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
+      side = patch_side_exact(M == 0 ? P.g.d_hi : (double)dmax, P.g.patch_mult);
       if (M == 0) dmax = (float)P.g.d_hi;
-      side = patch_side_exact((double)dmax, P.g.patch_mult);
     } else {
       side = P.side_in[pl];
     }
@@ -649,79 +741,61 @@ __global__ void __launch_bounds__(kThreads, 2) fused_generate_kernel(const Fused
     const int c0 = tx * P.TW;
     const int nc = min(P.TW, P.W - c0);
     const int h = side >> 1;
+    const float amp_max = fmaxf(__uint_as_float(sh->amp_bits), 1e-30f);
 
     for (int f = 0; f < P.nframes; ++f) {
       int K = sh->fill[f];
       if (P.bin_counts && tid == 0) P.bin_counts[((size_t)pl * 2 + f) * P.tiles + t] = K;
       if (K > P.cap + P.spill_cap) K = P.cap + P.spill_cap;
-      Cand* local = cand + (size_t)f * P.cap;
-      Cand* spill = my_spill + (size_t)f * P.spill_cap;
-      // -- coverage guard: per-pixel particle count bound from a cell
+      const Rec* local = rec + (size_t)f * P.cap;
+      const Rec* spill = my_spill + (size_t)f * P.spill_cap;
+      // -- fixed-point shift: the per-pixel sum of rounded contributions must
+      //    stay below 2^31. Cheap bound from K first (one thread); if it would
+      //    cost precision (shift < 21) bound the per-pixel coverage with a cell
       //    histogram (cells >= 2h+1 wide: a pixel's anchor window lies in a
-      //    2x2 block); picks the fixed-point shift so int32 cannot overflow.
-      const int S = max(2 * h + 1, kCellMin);
-      const int ncy = (nr + 2 * h + S - 1) / S, ncx = (nc + 2 * h + S - 1) / S;
-      const bool cells_ok = ncy * ncx <= P.cells_cap;
-      if (cells_ok)
-        for (int e = tid; e < ncy * ncx; e += kThreads) cells[e] = 0;
+      //    2x2 block of cells).
+      if (tid == 0) sh->cov_max = shift_for(K, amp_max);
       __syncthreads();
-      unsigned amp_local = 0u;
-      for (int k = tid; k < K; k += kThreads) {
-        const Cand* c = cand_at(local, spill, P.cap, k);
-        amp_local = max(amp_local, __float_as_uint(fmaxf(c->amp, 0.f)));
-        if (cells_ok) {
-          const int ay = c->axy >> 16, ax = (int)(short)(c->axy & 0xffff);
-          const int cy = ay - (r0 - h), cx = ax - (c0 - h);
-          if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
-            atomicAdd(&cells[(cy / S) * ncx + cx / S], 1);
+      int shift = sh->cov_max;
+      if (shift < kAccShift - 1) {
+        const int S = max(2 * h + 1, kCellMin);
+        const int ncy = (nr + 2 * h + S - 1) / S, ncx = (nc + 2 * h + S - 1) / S;
+        if (ncy * ncx <= P.cells_cap) {
+          __syncthreads();
+          if (tid == 0) sh->cov_max = 0;
+          for (int e = tid; e < ncy * ncx; e += kThreads) cells[e] = 0;
+          __syncthreads();
+          for (int k = tid; k < K; k += kThreads) {
+            const Rec& c = k < P.cap ? local[k] : spill[k - P.cap];
+            const int cy = (c.axy >> 16) - (r0 - h), cx = (int)(short)(c.axy & 0xffff) - (c0 - h);
+            if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
+              atomicAdd(&cells[(cy / S) * ncx + cx / S], 1);
+          }
+          __syncthreads();
+          int cm = 0;
+          for (int e = tid; e < ncy * ncx; e += kThreads) {
+            const int cy = e / ncx, cx = e - (e / ncx) * ncx;
+            int sm = cells[e];
+            if (cx + 1 < ncx) sm += cells[e + 1];
+            if (cy + 1 < ncy) sm += cells[e + ncx];
+            if (cx + 1 < ncx && cy + 1 < ncy) sm += cells[e + ncx + 1];
+            cm = max(cm, sm);
+          }
+          for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
+          if ((tid & 31) == 0) atomicMax(&sh->cov_max, cm);
+          __syncthreads();
+          if (tid == 0) sh->cov_max = shift_for(max(sh->cov_max, 1), amp_max);
+          __syncthreads();
+          shift = sh->cov_max;
         }
       }
-      for (int o = 16; o > 0; o >>= 1)
-        amp_local = max(amp_local, __shfl_xor_sync(~0u, amp_local, o));
-      if ((tid & 31) == 0) atomicMax(&sh->amp_bits, amp_local);
+      splat_dispatch<PSF>(acc, local, spill, P.cap, K, side, r0 - P.pad, c0 - P.pad, P.AS,
+                          (float)shift, exp2f((float)shift));
       __syncthreads();
-      if (cells_ok) {
-        int cm = 0;
-        for (int e = tid; e < ncy * ncx; e += kThreads) {
-          const int cy = e / ncx, cx = e - (e / ncx) * ncx;
-          int s = cells[e];
-          if (cx + 1 < ncx) s += cells[e + 1];
-          if (cy + 1 < ncy) s += cells[e + ncx];
-          if (cx + 1 < ncx && cy + 1 < ncy) s += cells[e + ncx + 1];
-          cm = max(cm, s);
-        }
-        for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
-        if ((tid & 31) == 0) atomicMax(&sh->cov_max, cm);
-      }
-      __syncthreads();
-      const float amp_max = __uint_as_float(sh->amp_bits);
-      int shift = kAccShift;
-      if (amp_max > 1.0f) shift -= (int)ceilf(log2f(amp_max));
-      {
-        const float cov = cells_ok ? (float)sh->cov_max : (float)K;
-        const float units = cov * fmaxf(amp_max, 1e-30f);
-        if (units > 0.f) {
-          // keep cov * amp_max * 2^shift + cov < 2^31
-          const int lim = 30 - (int)ceilf(log2f(units + 1.0f));
-          if (shift > lim) shift = lim;
-        }
-      }
-      // -- per-candidate coefficients, in place
-      for (int k = tid; k < K; k += kThreads) {
-        Cand* c = const_cast<Cand*>(cand_at(local, spill, P.cap, k));
-        if (PSF == kPsfPoint) setup_point(*c, (float)shift);
-        else setup_erf(*c, exp2f((float)shift));
-      }
-      __syncthreads();
-      if (tid == 0) {
-        sh->amp_bits = 0u;
-        sh->cov_max = 0;
-      }
-      // -- splat: integer accumulation in shared memory
-      splat_dispatch<PSF>(acc, local, spill, P.cap, K, side, r0, nr, c0, nc, P.TW);
-      __syncthreads();
-      // -- fused epilogue
       store_tile(P, acc, pl, f, r0, nr, c0, nc, exp2f(-(float)shift));
+      __syncthreads();
+      for (int e = tid; e < (acc_ints >> 2); e += kThreads)
+        reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
       __syncthreads();
     }
   }

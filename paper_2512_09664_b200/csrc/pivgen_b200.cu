@@ -70,8 +70,8 @@ __global__ void quantize_kernel(const float* __restrict__ img, long long n, uint
     out[i] = quant_u16(img[i]);
 }
 
-// Particle arrays of the generator (one block per pair). Same make_particle as
-// the fused kernel, so these arrays are exactly what the fused kernel renders.
+// Particle arrays of the generator (one block per pair): exactly the particles
+// gen_particle() feeds to the fused kernel (positions = anchor + fraction).
 __global__ void sample_particles_kernel(FusedParams P, pgb_particle_out O) {
   const int pl = blockIdx.x;
   __shared__ int sM;
@@ -92,43 +92,35 @@ __global__ void sample_particles_kernel(FusedParams P, pgb_particle_out O) {
   unsigned dm = 0u;
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     Particle pt;
-    make_particle<0>(P, pl, i, M, pt);
+    gen_particle(P, pl, i, M, pt);
     const size_t o = (size_t)pl * P.n + i;
-    // recompute the frame-independent draws the Particle struct does not carry
-    const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
-    bool vis1 = true, vis2 = true;
-    double z1 = 0.0;
-    if (P.g.need_b) {
-      const uint4 b = draw(key, (uint32_t)i, kTagParticleB);
-      vis1 = u32_to_unit(b.y) >= P.g.hide_p;
-      vis2 = u32_to_unit(b.z) >= P.g.hide_p;
-      z1 = lerp_exact(P.g.z_lo, P.g.z_hi, u32_to_unit(b.w));
-    }
-    if (O.pos1) { O.pos1[2 * o] = pt.x[0]; O.pos1[2 * o + 1] = pt.y[0]; }
-    if (O.pos2) { O.pos2[2 * o] = pt.x[1]; O.pos2[2 * o + 1] = pt.y[1]; }
-    if (O.i0_1) O.i0_1[o] = pt.amp[0];
-    if (O.sx_1) O.sx_1[o] = pt.sx[0];
-    if (O.sy_1) O.sy_1[o] = pt.sy[0];
-    if (O.rho_1) O.rho_1[o] = pt.rho[0];
-    if (O.i0_2) O.i0_2[o] = pt.amp[1];
-    if (O.sx_2) O.sx_2[o] = pt.sx[1];
-    if (O.sy_2) O.sy_2[o] = pt.sy[1];
-    if (O.rho_2) O.rho_2[o] = pt.rho[1];
+    const Frame& a = pt.fr[0];
+    const Frame& b = pt.fr[1];
+    if (O.pos1) { O.pos1[2 * o] = (double)a.ax + (double)a.fx; O.pos1[2 * o + 1] = (double)a.ay + (double)a.fy; }
+    if (O.pos2) { O.pos2[2 * o] = (double)b.ax + (double)b.fx; O.pos2[2 * o + 1] = (double)b.ay + (double)b.fy; }
+    if (O.i0_1) O.i0_1[o] = a.amp;
+    if (O.sx_1) O.sx_1[o] = a.sx;
+    if (O.sy_1) O.sy_1[o] = a.sy;
+    if (O.rho_1) O.rho_1[o] = a.rho;
+    if (O.i0_2) O.i0_2[o] = b.amp;
+    if (O.sx_2) O.sx_2[o] = b.sx;
+    if (O.sy_2) O.sy_2[o] = b.sy;
+    if (O.rho_2) O.rho_2[o] = b.rho;
     if (O.diameter) O.diameter[o] = pt.diam;
-    if (O.z1) O.z1[o] = (float)z1;
+    if (O.z1) O.z1[o] = pt.z1;
     if (O.active) O.active[o] = pt.active ? 1 : 0;
-    if (O.visible1) O.visible1[o] = (vis1 && pt.active) ? 1 : 0;
-    if (O.visible2) O.visible2[o] = (vis2 && pt.active) ? 1 : 0;
+    if (O.visible1) O.visible1[o] = pt.vis1 ? 1 : 0;
+    if (O.visible2) O.visible2[o] = pt.vis2 ? 1 : 0;
     if (pt.active) dm = max(dm, __float_as_uint(pt.diam));
   }
   atomicMax(&sdmax, dm);
   __syncthreads();
   if (threadIdx.x == 0) {
-    float dmax = M > 0 ? __uint_as_float(sdmax) : (float)P.g.d_hi;
+    const float dmax = M > 0 ? __uint_as_float(sdmax) : (float)P.g.d_hi;
     if (P.st_ppp) P.st_ppp[pl] = sppp;
     if (P.st_M) P.st_M[pl] = M;
     if (P.st_dmax) P.st_dmax[pl] = dmax;
-    if (P.st_side) P.st_side[pl] = patch_side_exact((double)dmax, P.g.patch_mult);
+    if (P.st_side) P.st_side[pl] = patch_side_exact(M > 0 ? (double)dmax : P.g.d_hi, P.g.patch_mult);
   }
 }
 
@@ -145,16 +137,15 @@ __global__ void perturb_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, 
     const float2 n23 = box_muller(c.z, c.w);
     float sx = sx_1[i], sy = sy_1[i], a = i0_1[i], r = rho_1[i];
     if (sd_sigma > 0.f) {
-      sx = (float)fmax((double)sx + (double)sd_sigma * (double)n01.x, 1e-3);
-      sy = (float)fmax((double)sy + (double)sd_sigma * (double)n01.y, 1e-3);
+      sx = fmaxf(__fadd_rn(sx, __fmul_rn(sd_sigma, n01.x)), 1e-3f);
+      sy = fmaxf(__fadd_rn(sy, __fmul_rn(sd_sigma, n01.y)), 1e-3f);
     }
     if (sd_i0 > 0.f) {
-      const double t = fmin(fmax((double)a + (double)sd_i0 * (double)n23.x, 0.0), 1.0);
-      a = a == 0.f ? 0.f : (float)t;
+      const float t = fminf(fmaxf(__fadd_rn(a, __fmul_rn(sd_i0, n23.x)), 0.f), 1.f);
+      a = a == 0.f ? 0.f : t;
     }
     if (sd_rho > 0.f) {
-      const double lim = 1.0 - 1e-3;
-      r = (float)fmin(fmax((double)r + (double)sd_rho * (double)n23.y, -lim), lim);
+      r = fminf(fmaxf(__fadd_rn(r, __fmul_rn(sd_rho, n23.y)), -0.999f), 0.999f);
     }
     sx_2[i] = sx; sy_2[i] = sy; i0_2[i] = a; rho_2[i] = r;
   }
@@ -162,13 +153,13 @@ __global__ void perturb_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, 
 
 // apply_hiding (particles.py:139-147): visible_k = U_k >= p & active.
 __global__ void hiding_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, uint32_t batch,
-                              double p_hide, const uint8_t* active, uint8_t* vis1, uint8_t* vis2) {
+                              uint64_t thr, const uint8_t* active, uint8_t* vis1, uint8_t* vis2) {
   const RngKey key{k0, k1, gpair, batch};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint4 b = draw(key, (uint32_t)i, kTagParticleB);
     const bool a = active[i] != 0;
-    vis1[i] = (a && u32_to_unit(b.y) >= p_hide) ? 1 : 0;
-    vis2[i] = (a && u32_to_unit(b.z) >= p_hide) ? 1 : 0;
+    vis1[i] = (a && (uint64_t)b.y >= thr) ? 1 : 0;
+    vis2[i] = (a && (uint64_t)b.z >= thr) ? 1 : 0;
   }
 }
 
@@ -201,17 +192,35 @@ struct Error {
 
 struct Plan {
   int TH, TW, tiles_y, tiles_x, tiles, CL, passes, cap, spill_cap, halo, cells_cap;
+  int th_shift, tw_shift, pad, AH, AS;
   size_t smem;
 };
 
 constexpr size_t kSmemTarget = 110 * 1024;  // two CTAs per SM
 constexpr size_t kSmemMax = 220 * 1024;
 
+int ilog2(int v) {
+  int s = 0;
+  while ((1 << (s + 1)) <= v) ++s;
+  return s;
+}
+
+int pow2_ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// Tiles are powers of two (shift-based binning); the accumulator carries a
+// pad of 2*halo (rounded to 4 ints) on every side so that patches of halo
+// particles need no clipping.
 Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, int cl_max) {
   Plan p{};
   p.halo = halo;
-  p.TW = W <= 256 ? W : 256;
-  p.TH = std::max(1, std::min(rows, 8192 / std::max(1, p.TW)));
+  p.TW = std::min(256, std::max(4, pow2_ceil(W)));
+  p.TH = std::max(1, std::min(pow2_ceil(rows), 8192 / p.TW));
+  p.TH = 1 << ilog2(p.TH);
+  p.pad = (2 * halo + 3) / 4 * 4;
   for (;;) {
     const double ext = (double)std::min(p.TH + 2 * halo, rows + 2 * halo) *
                        (double)std::min(p.TW + 2 * halo, W + 2 * halo);
@@ -220,16 +229,20 @@ Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, 
     cap = std::min<long long>(cap, std::max<long long>(n, 1));
     cap = (cap + 7) / 8 * 8;
     p.cap = (int)cap;
+    p.AH = p.TH + 2 * p.pad;
+    p.AS = p.TW + 2 * p.pad;
     p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
                   ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
-    p.smem = (size_t)p.TH * p.TW * 4 + (size_t)nframes * p.cap * sizeof(Cand) +
+    p.smem = (size_t)p.AH * p.AS * 4 + (size_t)nframes * p.cap * sizeof(Rec) +
              sizeof(SharedHdr) + (size_t)p.cells_cap * 4;
     if (p.smem <= kSmemTarget) break;
-    if (p.TH > 1) p.TH = (p.TH + 1) / 2;
-    else if (p.TW > 4) p.TW = ((p.TW / 2) + 3) / 4 * 4;
+    if (p.TH > 1) p.TH >>= 1;
+    else if (p.TW > 4) p.TW >>= 1;
     else break;
   }
   PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
+  p.th_shift = ilog2(p.TH);
+  p.tw_shift = ilog2(p.TW);
   p.tiles_y = (rows + p.TH - 1) / p.TH;
   p.tiles_x = (W + p.TW - 1) / p.TW;
   p.tiles = p.tiles_y * p.tiles_x;
@@ -286,7 +299,9 @@ int max_active_clusters(KernelFn fn, int CL, size_t smem) {
   auto key = std::make_tuple((void*)fn, CL, smem, dev);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // The dynamic-smem limit is a per-function attribute: set it once to the
+  // largest plan we ever build so later, smaller plans never shrink it.
+  PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
   if (CL > 8) PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(CL * 64);
@@ -311,13 +326,14 @@ void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
   P.TH = pl.TH; P.TW = pl.TW; P.tiles_y = pl.tiles_y; P.tiles_x = pl.tiles_x; P.tiles = pl.tiles;
   P.CL = pl.CL; P.passes = pl.passes; P.cap = pl.cap; P.spill_cap = pl.spill_cap;
   P.halo = pl.halo; P.cells_cap = pl.cells_cap;
+  P.th_shift = pl.th_shift; P.tw_shift = pl.tw_shift; P.pad = pl.pad; P.AH = pl.AH; P.AS = pl.AS;
   const int items = P.pairs * P.passes;
   if (items <= 0) return;
   const int maxc = max_active_clusters(fn, pl.CL, pl.smem);
   const int nclusters = std::min(items, maxc);
   DevWork& w = work_for_current();
-  const size_t spill_need = (size_t)nclusters * pl.CL * 2 * pl.spill_cap * sizeof(Cand);
-  P.spill = static_cast<Cand*>(ensure(w.spill, w.spill_bytes, spill_need));
+  const size_t spill_need = (size_t)nclusters * pl.CL * 2 * pl.spill_cap * sizeof(Rec);
+  P.spill = static_cast<Rec*>(ensure(w.spill, w.spill_bytes, spill_need));
   P.overflow = w.overflow;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nclusters * pl.CL);
@@ -340,6 +356,14 @@ int grid_for(long long n, int block) {
   return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 16));
 }
 
+uint64_t hide_threshold(double p) {
+  // visible iff (w + 1/2) 2^-32 >= p  <=>  w >= ceil(p 2^32 - 1/2)   (exact in float64)
+  const double t = std::ceil(p * 4294967296.0 - 0.5);
+  if (t <= 0.0) return 0ull;
+  if (t >= 4294967296.0) return 4294967296ull;
+  return (uint64_t)t;
+}
+
 GenCfg gen_cfg_from(const pgb_config* c) {
   GenCfg g{};
   g.H = c->height;
@@ -348,13 +372,19 @@ GenCfg gen_cfg_from(const pgb_config* c) {
   g.k0 = (uint32_t)(c->seed & 0xffffffffu);
   g.k1 = (uint32_t)(c->seed >> 32);
   g.ppp_lo = c->ppp_lo; g.ppp_hi = c->ppp_hi;
-  g.d_lo = c->d_lo; g.d_hi = c->d_hi;
-  g.i0_lo = c->i0_lo; g.i0_hi = c->i0_hi;
-  g.rho_lo = c->rho_lo; g.rho_hi = c->rho_hi;
-  g.sigma_ratio = c->sigma_ratio;
+  // float32 ranges: lo + span * u with span = f32(hi) - f32(lo) (one rounding)
+  volatile float dl = (float)c->d_lo, dh = (float)c->d_hi;
+  volatile float il = (float)c->i0_lo, ih = (float)c->i0_hi;
+  volatile float rl = (float)c->rho_lo, rh = (float)c->rho_hi;
+  volatile float zl = (float)c->laser_z_lo, zh = (float)c->laser_z_hi;
+  g.d_lo = dl; g.d_span = dh - dl;
+  g.i0_lo = il; g.i0_span = ih - il;
+  g.rho_lo = rl; g.rho_span = rh - rl;
+  g.z_lo = zl; g.z_span = zh - zl;
+  g.inv_ratio = (float)(1.0 / c->sigma_ratio);
   g.patch_mult = c->patch_multiplier;
-  g.hide_p = c->hide_probability;
-  g.z_lo = c->laser_z_lo; g.z_hi = c->laser_z_hi;
+  g.d_hi = c->d_hi;
+  g.hide_thr = hide_threshold(c->hide_probability);
   g.f2_sigma_std = (float)c->f2_sigma_std;
   g.f2_rho_std = (float)c->f2_rho_std;
   g.f2_i0_std = (float)c->f2_i0_std;
@@ -764,7 +794,7 @@ int pgb_apply_hiding_dev(int64_t n, uint64_t seed, uint64_t batch, int64_t gpair
     if (n <= 0) return;
     hiding_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
         (int)n, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), (uint32_t)gpair,
-        (uint32_t)batch, p_hide, active, visible1, visible2);
+        (uint32_t)batch, hide_threshold(p_hide), active, visible1, visible2);
     g_launches.fetch_add(1);
     PGB_CK(cudaGetLastError());
   });

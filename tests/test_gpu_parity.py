@@ -93,13 +93,14 @@ def _render_golden(pg, c, out_mode, bg=0.0):
     n = c["pos1"].shape[0]
     out = [torch.zeros((1, H, W), dtype=torch.float32, device=dev) for _ in range(2)]
     tiles = ctypes.c_int(0)
-    bins = torch.full((1, 2, 4096), -1, dtype=torch.int32, device=dev)
+    bins = torch.full((2 * 4096,), -1, dtype=torch.int32, device=dev)
     sides = (ctypes.c_int * 1)(int(c["side"]))
     _lib.call("pgb_render_pairs_dev", ctypes.byref(frames[0]), ctypes.byref(frames[1]), n, 1, sides,
               H, W, 0, out_mode, bg, 0.0, 0, 0, 0, out[0].data_ptr(), out[1].data_ptr(),
               bins.data_ptr(), ctypes.byref(tiles), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    return [o[0].cpu().numpy() for o in out], bins.cpu().numpy(), tiles.value
+    nt = tiles.value
+    return [o[0].cpu().numpy() for o in out], bins[:2 * nt].reshape(1, 2, nt).cpu().numpy(), nt
 
 
 def test_render_pairs_raw_vs_reference(pg, golden):
