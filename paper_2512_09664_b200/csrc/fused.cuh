@@ -35,7 +35,7 @@ namespace cg = cooperative_groups;
 
 namespace pgb {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCluster = 16;
 constexpr int kAccShift = 22;     // max fixed-point fraction bits
@@ -186,7 +186,7 @@ __device__ __forceinline__ float laser_profile(const GenCfg& g, float z) {
 }
 
 __device__ __forceinline__ void gen_particle(const FusedParams& P, int pl, int i, int M,
-                                             Particle& pt) {
+                                             const float2* __restrict__ flow, Particle& pt) {
   const GenCfg& g = P.g;
   const RngKey key{g.k0, g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
   // sample_particles (particles.py:61-101)
@@ -240,8 +240,6 @@ __device__ __forceinline__ void gen_particle(const FusedParams& P, int pl, int i
   float tx, ty;
   fixed_cell(X, g.W, cx, tx);
   fixed_cell(Y, g.H, cy, ty);
-  const long long field = (P.pair_base + pl) / P.pairs_per_field;
-  const float2* flow = P.flows + (size_t)field * P.field_elems;
   const int cx1 = cx + 1 < g.W ? cx + 1 : g.W - 1;
   const int cy1 = cy + 1 < g.H ? cy + 1 : g.H - 1;
   const float2 q00 = __ldg(flow + (size_t)cy * g.W + cx);
@@ -302,9 +300,10 @@ __device__ __forceinline__ Rec make_rec(const Frame& fr, int psf) {
   const float sx = fr.sx, sy = fr.sy, rho = fr.rho;
   if (psf == kPsfPoint) {
     const float q = 1.0f - rho * rho;
-    r.A = 0.5f * kLog2e / (q * sx * sx);
-    r.C = 0.5f * kLog2e / (q * sy * sy);
-    r.B = -kLog2e * rho / (q * sx * sy);
+    const float isx = __frcp_rn(sx), isy = __frcp_rn(sy), iq = __frcp_rn(q);
+    r.A = (0.5f * kLog2e) * iq * isx * isx;
+    r.C = (0.5f * kLog2e) * iq * isy * isy;
+    r.B = -kLog2e * rho * iq * isx * isy;
     r.L = __log2f(fr.amp);
     r.aux = fr.amp;
   } else {
@@ -388,10 +387,9 @@ __device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, 
 }
 
 template <int S, int PSF>
-__device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ local,
-                           const Rec* __restrict__ spill, int cap, int K, int side, int r0p,
-                           int c0p, int AS, float s_log2, float scale) {
-  const int side_ = S > 0 ? S : side;
+__device__ __forceinline__ void splat_range(int* __restrict__ acc, const Rec* __restrict__ recs,
+                                            int K, int side_, int r0p, int c0p, int AS,
+                                            float s_log2, float scale) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   if (side_ <= 32) {
@@ -399,20 +397,31 @@ __device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ local,
     const int slot = lane / side_;
     const int j = lane - slot * side_;
     if (slot >= cpw) return;
-    for (int kb = warp * cpw; kb < K; kb += kWarps * cpw) {
-      const int k = kb + slot;
-      if (k >= K) break;
-      const Rec r = k < cap ? local[k] : spill[k - cap];
+    for (int k = warp * cpw + slot; k < K; k += kWarps * cpw) {
+      const float4* q = reinterpret_cast<const float4*>(recs + k);
+      const float4 a = q[0], b = q[1];
+      Rec r;
+      r.axy = __float_as_int(a.x); r.fx = a.y; r.fy = a.z; r.L = a.w;
+      r.A = b.x; r.B = b.y; r.C = b.z; r.aux = b.w;
       splat_lane<S, PSF>(acc, r, side_, j, r0p, c0p, AS, s_log2, scale);
     }
   } else {
     // very large patches: the warp walks one candidate, lanes stride the columns
     for (int k = warp; k < K; k += kWarps) {
-      const Rec r = k < cap ? local[k] : spill[k - cap];
+      const Rec r = recs[k];
       for (int jj = lane; jj < side_; jj += 32)
         splat_lane<0, PSF>(acc, r, side_, jj, r0p, c0p, AS, s_log2, scale);
     }
   }
+}
+
+template <int S, int PSF>
+__device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ local,
+                           const Rec* __restrict__ spill, int cap, int K, int side, int r0p,
+                           int c0p, int AS, float s_log2, float scale) {
+  const int side_ = S > 0 ? S : side;
+  splat_range<S, PSF>(acc, local, min(K, cap), side_, r0p, c0p, AS, s_log2, scale);
+  if (K > cap) splat_range<S, PSF>(acc, spill, K - cap, side_, r0p, c0p, AS, s_log2, scale);
 }
 
 template <int PSF>
@@ -470,97 +479,123 @@ __device__ __forceinline__ float acc_to_float(int a) {
   return __int_as_float(a | 0x4B000000) - 8388608.0f;
 }
 
+// One output quad (4 pixels) of frame f.
+template <int OUT, bool NOISE>
+__device__ __forceinline__ void store_quad(const FusedParams& P, const int4 a, char* dst,
+                                           size_t pix, int f, uint32_t gpair, float inv_scale) {
+  float4 v;
+  if ((a.x | a.y | a.z | a.w) >= (1 << 23)) {
+    v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
+  } else {
+    v = make_float4(acc_to_float(a.x), acc_to_float(a.y), acc_to_float(a.z), acc_to_float(a.w));
+  }
+  if (OUT == kOutRaw) {
+    v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
+    __stcs(reinterpret_cast<float4*>(dst), v);
+  } else if (OUT == kOutAccum) {
+    float4* o = reinterpret_cast<float4*>(dst);
+    float4 old = *o;
+    old.x = fmaf(v.x, inv_scale, old.x); old.y = fmaf(v.y, inv_scale, old.y);
+    old.z = fmaf(v.z, inv_scale, old.z); old.w = fmaf(v.w, inv_scale, old.w);
+    *o = old;
+  } else {
+    const float bg = P.bg_offset;
+    if (NOISE) {
+      const float sd = P.noise_std;
+      const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(pix >> 2));
+      v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
+      v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
+      v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
+      v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
+    } else {
+      v.x = fminf(fmaxf(fmaf(v.x, inv_scale, bg), 0.f), 1.f);
+      v.y = fminf(fmaxf(fmaf(v.y, inv_scale, bg), 0.f), 1.f);
+      v.z = fminf(fmaxf(fmaf(v.z, inv_scale, bg), 0.f), 1.f);
+      v.w = fminf(fmaxf(fmaf(v.w, inv_scale, bg), 0.f), 1.f);
+    }
+    if (OUT == kOutF32) {
+      __stcs(reinterpret_cast<float4*>(dst), v);
+    } else {
+      ushort4 u = make_ushort4(quant_u16(v.x), quant_u16(v.y), quant_u16(v.z), quant_u16(v.w));
+      __stcs(reinterpret_cast<ushort4*>(dst), u);
+    }
+  }
+}
+
+template <int OUT, bool NOISE>
+__device__ void store_tile_vec(const FusedParams& P, const int* __restrict__ acc, int pl, int f,
+                               int r0, int nr, int c0, int nc, float inv_scale) {
+  constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
+  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
+  const int qpr = nc >> 2;
+  char* outb = static_cast<char*>(P.out[f]) + (size_t)pl * (size_t)P.out_pair_elems * ESZ;
+  if ((qpr & (qpr - 1)) == 0 && qpr <= kThreads) {
+    // each thread owns one column quad and walks rows with constant pointer steps
+    const int cq = threadIdx.x & (qpr - 1);
+    const int row0 = threadIdx.x / qpr;
+    const int rstep = kThreads / qpr;
+    const int* ap = acc + (row0 + P.pad) * P.AS + P.pad + cq * 4;
+    const int astep = rstep * P.AS;
+    size_t pix = (size_t)(r0 + row0) * P.W + (size_t)(c0 + cq * 4);
+    const size_t pstep = (size_t)rstep * P.W;
+    for (int row = row0; row < nr; row += rstep, ap += astep, pix += pstep)
+      store_quad<OUT, NOISE>(P, *reinterpret_cast<const int4*>(ap), outb + pix * ESZ, pix, f,
+                             gpair, inv_scale);
+  } else {
+    const int total = nr * qpr;
+    for (int e = threadIdx.x; e < total; e += kThreads) {
+      const int row = e / qpr;
+      const int c = e - row * qpr;
+      const size_t pix = (size_t)(r0 + row) * P.W + (size_t)(c0 + c * 4);
+      store_quad<OUT, NOISE>(P, *reinterpret_cast<const int4*>(acc + (row + P.pad) * P.AS + P.pad + c * 4),
+                             outb + pix * ESZ, pix, f, gpair, inv_scale);
+    }
+  }
+}
+
 __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, int pl, int f,
                            int r0, int nr, int c0, int nc, float inv_scale) {
-  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
   const int AS = P.AS, pad = P.pad;
-  const size_t pair_off = (size_t)pl * (size_t)P.out_pair_elems;
   const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
+  const bool noise = P.noise_std > 0.f;
+  if (vec) {
+    switch (P.out_mode) {
+      case kOutRaw: store_tile_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
+      case kOutAccum: store_tile_vec<kOutAccum, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
+      case kOutF32:
+        if (noise) store_tile_vec<kOutF32, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        else store_tile_vec<kOutF32, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        return;
+      default:
+        if (noise) store_tile_vec<kOutU16, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        else store_tile_vec<kOutU16, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        return;
+    }
+  }
+  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
+  const size_t pair_off = (size_t)pl * (size_t)P.out_pair_elems;
   const int mode = P.out_mode;
   const float bg = P.bg_offset, sd = P.noise_std;
-  if (vec) {
-    const int qpr = nc >> 2;
-    // Fast path: a power-of-two number of quads per row that divides the block:
-    // every thread owns one fixed column quad and walks rows with pointer steps.
-    const bool fast = (qpr & (qpr - 1)) == 0 && qpr <= kThreads;
-    const int cq = fast ? (threadIdx.x & (qpr - 1)) : 0;
-    const int row0 = fast ? (threadIdx.x >> __ffs(qpr) - 1) : 0;
-    const int rstep = fast ? kThreads / qpr : 0;
-    const uint32_t magic = fast ? 0u : (uint32_t)((0x100000000ull + qpr - 1) / qpr);
-    const int total = nr * qpr;
-    const char* outb = static_cast<const char*>(P.out[f]);
-    const size_t esz = mode == kOutU16 ? 2 : 4;
-    for (int e = threadIdx.x, rowf = row0; e < total; e += kThreads, rowf += rstep) {
-      int row, c;
-      if (fast) {
-        if (rowf >= nr) break;
-        row = rowf;
-        c = cq;
-      } else {
-        row = (int)__umulhi((uint32_t)e, magic);
-        c = e - row * qpr;
+  const int total = nr * nc;
+  for (int e = threadIdx.x; e < total; e += kThreads) {
+    const int row = e / nc;
+    const int col = e - row * nc;
+    float v = (float)acc[(row + pad) * AS + pad + col] * inv_scale;
+    const size_t p = (size_t)(r0 + row) * P.W + (size_t)(c0 + col);
+    if (mode == kOutRaw) {
+      static_cast<float*>(P.out[f])[pair_off + p] = v;
+    } else if (mode == kOutAccum) {
+      static_cast<float*>(P.out[f])[pair_off + p] += v;
+    } else {
+      float nzv = 0.f;
+      if (sd > 0.f) {
+        const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
+        const int jn = (int)(p & 3);
+        nzv = jn == 0 ? nz.x : (jn == 1 ? nz.y : (jn == 2 ? nz.z : nz.w));
       }
-      const int4 a = *reinterpret_cast<const int4*>(acc + (row + pad) * AS + pad + c * 4);
-      float4 v;
-      if ((a.x | a.y | a.z | a.w) >= (1 << 23)) {
-        v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
-      } else {
-        v = make_float4(acc_to_float(a.x), acc_to_float(a.y), acc_to_float(a.z), acc_to_float(a.w));
-      }
-      const size_t p = (size_t)(r0 + row) * P.W + (size_t)(c0 + c * 4);
-      char* dst = const_cast<char*>(outb) + (pair_off + p) * esz;
-      if (mode == kOutRaw) {
-        v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
-        __stcs(reinterpret_cast<float4*>(dst), v);
-      } else if (mode == kOutAccum) {
-        float4* o = reinterpret_cast<float4*>(dst);
-        float4 old = *o;
-        old.x = fmaf(v.x, inv_scale, old.x); old.y = fmaf(v.y, inv_scale, old.y);
-        old.z = fmaf(v.z, inv_scale, old.z); old.w = fmaf(v.w, inv_scale, old.w);
-        *o = old;
-      } else {
-        if (sd > 0.f) {
-          const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
-          v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
-          v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
-          v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
-          v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
-        } else {
-          v.x = fminf(fmaxf(fmaf(v.x, inv_scale, bg), 0.f), 1.f);
-          v.y = fminf(fmaxf(fmaf(v.y, inv_scale, bg), 0.f), 1.f);
-          v.z = fminf(fmaxf(fmaf(v.z, inv_scale, bg), 0.f), 1.f);
-          v.w = fminf(fmaxf(fmaf(v.w, inv_scale, bg), 0.f), 1.f);
-        }
-        if (mode == kOutF32) {
-          __stcs(reinterpret_cast<float4*>(dst), v);
-        } else {
-          ushort4 u = make_ushort4(quant_u16(v.x), quant_u16(v.y), quant_u16(v.z), quant_u16(v.w));
-          __stcs(reinterpret_cast<ushort4*>(dst), u);
-        }
-      }
-    }
-  } else {
-    const int total = nr * nc;
-    for (int e = threadIdx.x; e < total; e += kThreads) {
-      const int row = e / nc;
-      const int col = e - row * nc;
-      float v = (float)acc[(row + pad) * AS + pad + col] * inv_scale;
-      const size_t p = (size_t)(r0 + row) * P.W + (size_t)(c0 + col);
-      if (mode == kOutRaw) {
-        static_cast<float*>(P.out[f])[pair_off + p] = v;
-      } else if (mode == kOutAccum) {
-        static_cast<float*>(P.out[f])[pair_off + p] += v;
-      } else {
-        float nzv = 0.f;
-        if (sd > 0.f) {
-          const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
-          const int jn = (int)(p & 3);
-          nzv = jn == 0 ? nz.x : (jn == 1 ? nz.y : (jn == 2 ? nz.z : nz.w));
-        }
-        v = finalize_px(v, bg, sd, nzv);
-        if (mode == kOutF32) static_cast<float*>(P.out[f])[pair_off + p] = v;
-        else static_cast<uint16_t*>(P.out[f])[pair_off + p] = quant_u16(v);
-      }
+      v = finalize_px(v, bg, sd, nzv);
+      if (mode == kOutF32) static_cast<float*>(P.out[f])[pair_off + p] = v;
+      else static_cast<uint16_t*>(P.out[f])[pair_off + p] = quant_u16(v);
     }
   }
 }
@@ -598,7 +633,7 @@ __device__ __forceinline__ void exchange(cg::cluster_group& cluster, const Fused
 }
 
 template <int MODE, int PSF>
-__global__ void __launch_bounds__(kThreads, 2) fused_generate_kernel(const FusedParams P) {
+__global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const FusedParams P) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = P.CL;
   const int rank = (int)cluster.block_rank();
@@ -653,12 +688,14 @@ __global__ void __launch_bounds__(kThreads, 2) fused_generate_kernel(const Fused
     // ---- seeding + distributed binning (one pass) ----------------------------
     const int hx = P.halo;
     const int t_lo = pass * CL;
+    const float2* flow = MODE == 0
+        ? P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems : nullptr;
     unsigned dmax_local = 0u, amp_local = 0u;
     for (int base = i_lo; base < i_hi; base += kThreads) {
       const int i = base + tid;
       Particle pt;
       if (i < i_hi) {
-        if (MODE == 0) gen_particle(P, pl, i, M, pt);
+        if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
         else inject_particle(P, pl, i, pt);
       } else {
         pt.fr[0].on = pt.fr[1].on = false;

@@ -90,9 +90,10 @@ __global__ void sample_particles_kernel(FusedParams P, pgb_particle_out O) {
   __syncthreads();
   const int M = sM;
   unsigned dm = 0u;
+  const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     Particle pt;
-    gen_particle(P, pl, i, M, pt);
+    gen_particle(P, pl, i, M, flow, pt);
     const size_t o = (size_t)pl * P.n + i;
     const Frame& a = pt.fr[0];
     const Frame& b = pt.fr[1];
@@ -196,8 +197,9 @@ struct Plan {
   size_t smem;
 };
 
-constexpr size_t kSmemTarget = 110 * 1024;  // two CTAs per SM
+constexpr size_t kSmemTarget = 55 * 1024;   // four CTAs per SM
 constexpr size_t kSmemMax = 220 * 1024;
+constexpr int kMaxClusterRun = 16;      // non-portable cluster size (opt-in attribute)
 
 int ilog2(int v) {
   int s = 0;
@@ -217,8 +219,8 @@ int pow2_ceil(int v) {
 Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, int cl_max) {
   Plan p{};
   p.halo = halo;
-  p.TW = std::min(256, std::max(4, pow2_ceil(W)));
-  p.TH = std::max(1, std::min(pow2_ceil(rows), 8192 / p.TW));
+  p.TW = std::min(128, std::max(4, pow2_ceil(W)));
+  p.TH = std::max(1, std::min(pow2_ceil(rows), 4096 / p.TW));
   p.TH = 1 << ilog2(p.TH);
   p.pad = (2 * halo + 3) / 4 * 4;
   for (;;) {
@@ -476,7 +478,7 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
     P.st_dmax = stats->d_max;
   }
   P.bin_counts = bin_counts;
-  const Plan pl = make_plan(cfg->height, cfg->height, cfg->width, cfg->n_capacity, halo, 2, 8);
+  const Plan pl = make_plan(cfg->height, cfg->height, cfg->width, cfg->n_capacity, halo, 2, kMaxClusterRun);
   launch_fused(P, pl, stream);
 }
 
@@ -501,7 +503,7 @@ int pgb_plan(int height, int width, int64_t n_per_pair, double ppp_hi, int halo,
   (void)ppp_hi;
   return guarded([&] {
     PGB_REQUIRE(info != nullptr, "info is NULL");
-    const Plan p = make_plan(height, height, width, n_per_pair, halo, frames, 8);
+    const Plan p = make_plan(height, height, width, n_per_pair, halo, frames, kMaxClusterRun);
     info->tile_h = p.TH; info->tile_w = p.TW; info->tiles_y = p.tiles_y; info->tiles_x = p.tiles_x;
     info->cluster = p.CL; info->passes = p.passes; info->capacity = p.cap; info->halo = p.halo;
     info->smem_bytes = (int)p.smem; info->threads = kThreads;
@@ -537,7 +539,7 @@ int pgb_splat_accumulate_dev(const double* pos, const float* i0, const float* si
     PGB_CK(cudaMemcpyAsync(side_dev, &side, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
     P.side_in = side_dev;
     P.out[0] = out;
-    const Plan pl = make_plan(height, row_stop - row_start, width, n, side / 2, 1, 8);
+    const Plan pl = make_plan(height, row_stop - row_start, width, n, side / 2, 1, kMaxClusterRun);
     launch_fused(P, pl, (cudaStream_t)stream);
     PGB_CK(cudaGetLastError());
     // the side staging slot is reused: keep the host value alive until the copy ran
@@ -625,7 +627,7 @@ int pgb_render_pairs_dev(const pgb_particles* frame1, const pgb_particles* frame
     P.out[0] = out1;
     P.out[1] = out2;
     P.bin_counts = bin_counts;
-    const Plan pl = make_plan(height, height, width, n_per_pair, smax / 2, 2, 8);
+    const Plan pl = make_plan(height, height, width, n_per_pair, smax / 2, 2, kMaxClusterRun);
     if (tiles_out) *tiles_out = pl.tiles;
     launch_fused(P, pl, (cudaStream_t)stream);
     PGB_CK(cudaGetLastError());
