@@ -35,8 +35,7 @@ namespace cg = cooperative_groups;
 
 namespace pgb {
 
-constexpr int kThreads = 128;
-constexpr int kWarps = kThreads / 32;
+constexpr int kThreads = 512;   // 16 warps: producer warps + consumer warps
 constexpr int kMaxCluster = 16;
 constexpr int kAccShift = 22;     // max fixed-point fraction bits
 constexpr int kCellMin = 8;       // coverage-guard cell size floor
@@ -84,6 +83,7 @@ struct FusedParams {
   int TH, TW, tiles_y, tiles_x, tiles, CL, passes, th_shift, tw_shift;
   int cap, spill_cap, halo, nframes, cells_cap;
   int pad, AH, AS;   // accumulator: AH rows x AS ints (tile + pad on each side)
+  int prod_warps;    // producer warps per CTA (the rest render)
   int n, pairs;
   long long pair_base;
   uint32_t batch_lo;
@@ -107,13 +107,20 @@ struct FusedParams {
   int* overflow;
 };
 
+// Per-CTA control block. Index [b] = record buffer (double-buffered items).
 struct SharedHdr {
-  int fill[2];
-  unsigned dmax_bits;
-  unsigned amp_bits;
+  unsigned long long full[2];    // mbarrier: all CL producers wrote item into buffer b
+  unsigned long long empty[2];   // mbarrier: all CL consumers finished rendering buffer b
+  int fill[2][2];                // [b][frame] records received (remote atomicAdd)
+  unsigned dmax_bits[2];         // [b] max active diameter of the item (remote atomicMax)
+  unsigned amp_bits[2];          // [b] max record amplitude
+  int M[2];                      // [b] active count (local producers)
+  double ppp[2];                 // [b] seeding density
+  unsigned pdmax, pamp;          // producer-local partial maxima
+  int rcnt[2][kMaxCluster];      // producer round: records per (frame, destination)
+  int rbase[2][kMaxCluster];     // producer round: reserved base slot in the owner
+  int shift[2];                  // consumer scratch: fixed-point shift per frame
   int cov_max;
-  int M;
-  double ppp;
 };
 
 // ----------------------------------------------------------------------------
@@ -389,9 +396,8 @@ __device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, 
 template <int S, int PSF>
 __device__ __forceinline__ void splat_range(int* __restrict__ acc, const Rec* __restrict__ recs,
                                             int K, int side_, int r0p, int c0p, int AS,
-                                            float s_log2, float scale) {
+                                            float s_log2, float scale, int warp, int kWarps) {
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   if (side_ <= 32) {
     const int cpw = 32 / side_;                       // candidates per warp-step
     const int slot = lane / side_;
@@ -418,27 +424,32 @@ __device__ __forceinline__ void splat_range(int* __restrict__ acc, const Rec* __
 template <int S, int PSF>
 __device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ local,
                            const Rec* __restrict__ spill, int cap, int K, int side, int r0p,
-                           int c0p, int AS, float s_log2, float scale) {
+                           int c0p, int AS, float s_log2, float scale, int warp, int nwarps) {
   const int side_ = S > 0 ? S : side;
-  splat_range<S, PSF>(acc, local, min(K, cap), side_, r0p, c0p, AS, s_log2, scale);
-  if (K > cap) splat_range<S, PSF>(acc, spill, K - cap, side_, r0p, c0p, AS, s_log2, scale);
+  splat_range<S, PSF>(acc, local, min(K, cap), side_, r0p, c0p, AS, s_log2, scale, warp, nwarps);
+  if (K > cap)
+    splat_range<S, PSF>(acc, spill, K - cap, side_, r0p, c0p, AS, s_log2, scale, warp, nwarps);
 }
 
 template <int PSF>
 __device__ void splat_dispatch(int* acc, const Rec* local, const Rec* spill, int cap, int K,
-                               int side, int r0p, int c0p, int AS, float s_log2, float scale) {
+                               int side, int r0p, int c0p, int AS, float s_log2, float scale,
+                               int warp, int nwarps) {
+#define PGB_SPLAT(SIDE) splat_tile<SIDE, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, \
+                                              s_log2, scale, warp, nwarps)
   if (PSF == kPsfPoint) {
     switch (side) {
-      case 3: splat_tile<3, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
-      case 5: splat_tile<5, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
-      case 7: splat_tile<7, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
-      case 9: splat_tile<9, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
-      case 11: splat_tile<11, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
-      case 13: splat_tile<13, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale); return;
+      case 3: PGB_SPLAT(3); return;
+      case 5: PGB_SPLAT(5); return;
+      case 7: PGB_SPLAT(7); return;
+      case 9: PGB_SPLAT(9); return;
+      case 11: PGB_SPLAT(11); return;
+      case 13: PGB_SPLAT(13); return;
       default: break;
     }
   }
-  splat_tile<0, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, s_log2, scale);
+  PGB_SPLAT(0);
+#undef PGB_SPLAT
 }
 
 // Largest fixed-point shift s <= kAccShift with cnt * (amp_max * 2^s + 1/2) < 2^31.
@@ -524,16 +535,16 @@ __device__ __forceinline__ void store_quad(const FusedParams& P, const int4 a, c
 
 template <int OUT, bool NOISE>
 __device__ void store_tile_vec(const FusedParams& P, const int* __restrict__ acc, int pl, int f,
-                               int r0, int nr, int c0, int nc, float inv_scale) {
+                               int r0, int nr, int c0, int nc, float inv_scale, int tix, int nth) {
   constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
   const int qpr = nc >> 2;
   char* outb = static_cast<char*>(P.out[f]) + (size_t)pl * (size_t)P.out_pair_elems * ESZ;
-  if ((qpr & (qpr - 1)) == 0 && qpr <= kThreads) {
+  if ((qpr & (qpr - 1)) == 0 && qpr <= nth && (nth % qpr) == 0) {
     // each thread owns one column quad and walks rows with constant pointer steps
-    const int cq = threadIdx.x & (qpr - 1);
-    const int row0 = threadIdx.x / qpr;
-    const int rstep = kThreads / qpr;
+    const int cq = tix & (qpr - 1);
+    const int row0 = tix / qpr;
+    const int rstep = nth / qpr;
     const int* ap = acc + (row0 + P.pad) * P.AS + P.pad + cq * 4;
     const int astep = rstep * P.AS;
     size_t pix = (size_t)(r0 + row0) * P.W + (size_t)(c0 + cq * 4);
@@ -543,7 +554,7 @@ __device__ void store_tile_vec(const FusedParams& P, const int* __restrict__ acc
                              gpair, inv_scale);
   } else {
     const int total = nr * qpr;
-    for (int e = threadIdx.x; e < total; e += kThreads) {
+    for (int e = tix; e < total; e += nth) {
       const int row = e / qpr;
       const int c = e - row * qpr;
       const size_t pix = (size_t)(r0 + row) * P.W + (size_t)(c0 + c * 4);
@@ -554,21 +565,21 @@ __device__ void store_tile_vec(const FusedParams& P, const int* __restrict__ acc
 }
 
 __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, int pl, int f,
-                           int r0, int nr, int c0, int nc, float inv_scale) {
+                           int r0, int nr, int c0, int nc, float inv_scale, int tix, int nth) {
   const int AS = P.AS, pad = P.pad;
   const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
   const bool noise = P.noise_std > 0.f;
   if (vec) {
     switch (P.out_mode) {
-      case kOutRaw: store_tile_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
-      case kOutAccum: store_tile_vec<kOutAccum, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
+      case kOutRaw: store_tile_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth); return;
+      case kOutAccum: store_tile_vec<kOutAccum, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth); return;
       case kOutF32:
-        if (noise) store_tile_vec<kOutF32, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
-        else store_tile_vec<kOutF32, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        if (noise) store_tile_vec<kOutF32, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
+        else store_tile_vec<kOutF32, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
         return;
       default:
-        if (noise) store_tile_vec<kOutU16, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
-        else store_tile_vec<kOutU16, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        if (noise) store_tile_vec<kOutU16, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
+        else store_tile_vec<kOutU16, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
         return;
     }
   }
@@ -577,7 +588,7 @@ __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, in
   const int mode = P.out_mode;
   const float bg = P.bg_offset, sd = P.noise_std;
   const int total = nr * nc;
-  for (int e = threadIdx.x; e < total; e += kThreads) {
+  for (int e = tix; e < total; e += nth) {
     const int row = e / nc;
     const int col = e - row * nc;
     float v = (float)acc[(row + pad) * AS + pad + col] * inv_scale;
@@ -601,39 +612,256 @@ __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, in
 }
 
 // ----------------------------------------------------------------------------
-// Exchange: lanes with the same destination are grouped with match.any; the
-// leader reserves a slot range with ONE remote atomicAdd; records go straight
-// to the owner's shared memory through DSMEM.
+// Cluster-scope mbarriers (producer -> consumer handoff without cluster.sync)
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ void exchange(cg::cluster_group& cluster, const FusedParams& P,
-                                         SharedHdr* sh, Rec* rec_base, int cluster_first, int f,
-                                         int dest, const Rec& r) {
-  const int lane = threadIdx.x & 31;
-  const unsigned peers = __match_any_sync(~0u, dest);
-  const int leader = __ffs(peers) - 1;
-  int base = 0;
-  if (dest >= 0 && lane == leader)
-    base = atomicAdd(cluster.map_shared_rank(&sh->fill[f], dest), __popc(peers));
-  base = __shfl_sync(~0u, base, leader);
-  if (dest < 0) return;
-  const int slot = base + __popc(peers & ((1u << lane) - 1u));
-  Rec* dst;
-  if (slot < P.cap) {
-    dst = cluster.map_shared_rank(rec_base, dest) + (size_t)f * P.cap + slot;
-  } else if (slot - P.cap < P.spill_cap) {
-    dst = P.spill + ((size_t)(cluster_first + dest) * 2 + f) * P.spill_cap + (slot - P.cap);
-  } else {
-    atomicAdd(P.overflow, 1);
-    return;
-  }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+// Arrive (release, cluster scope) on the same barrier in CTA `cta` of the cluster.
+__device__ __forceinline__ void mbar_arrive_remote(unsigned long long* bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+// Wait (acquire, cluster scope) for completion of the phase with the given parity.
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ----------------------------------------------------------------------------
+// Producer role: seed / inject one item's particle slice and bin it into the
+// owners' buffer b -- a distributed counting sort through DSMEM, in rounds of
+// np particles: (1) local ranks per (frame, owner) from shared-memory atomics,
+// (2) one remote atomicAdd per (frame, owner) reserves the round's slot range
+// (a single round trip, issued in parallel), (3) fire-and-forget DSMEM stores.
+// ----------------------------------------------------------------------------
+constexpr int kMaxDest = 4;   // plans keep tiles >= 2*halo+1, so a window spans <= 2x2 tiles
+
+__device__ __forceinline__ void store_rec(Rec* dst, const Rec& r) {
   const float4* s4 = reinterpret_cast<const float4*>(&r);
   float4* d4 = reinterpret_cast<float4*>(dst);
   d4[0] = s4[0];
   d4[1] = s4[1];
 }
 
+template <int MODE>
+__device__ void produce_item(cg::cluster_group& cluster, const FusedParams& P, SharedHdr* sh,
+                             Rec* rec_b, int b, int pl, int pass, int rank, int cluster_first,
+                             int i_lo, int i_hi, int ptid, int np) {
+  const int CL = P.CL;
+  const int hx = P.halo;
+  const int t_lo = pass * CL;
+  const int M = sh->M[b];
+  const float2* flow = MODE == 0
+      ? P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems : nullptr;
+  unsigned dmax_local = 0u, amp_local = 0u;
+  for (int base = i_lo; base < i_hi; base += np) {
+    const int i = base + ptid;
+    Particle pt;
+    if (i < i_hi) {
+      if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
+      else inject_particle(P, pl, i, pt);
+    } else {
+      pt.fr[0].on = pt.fr[1].on = false;
+      pt.active = false;
+    }
+    if (MODE == 0 && pt.active) dmax_local = max(dmax_local, __float_as_uint(pt.diam));
+    Rec r[2];
+    int dst[2][kMaxDest], rk[2][kMaxDest];   // statically indexed: slot = 2*dy + dx, dst < 0 = none
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+#pragma unroll
+      for (int k = 0; k < kMaxDest; ++k) dst[f][k] = -1;
+      if (f >= P.nframes) continue;
+      const Frame& fr = pt.fr[f];
+      if (!fr.on) continue;
+      const int rlo = max(fr.ay - hx, P.row_lo), rhi = min(fr.ay + hx, P.row_hi - 1);
+      const int clo = max(fr.ax - hx, 0), chi = min(fr.ax + hx, P.W - 1);
+      if (rlo > rhi || clo > chi) continue;
+      const int ty0 = (rlo - P.row_lo) >> P.th_shift, ty1 = (rhi - P.row_lo) >> P.th_shift;
+      const int tx0 = clo >> P.tw_shift, tx1 = chi >> P.tw_shift;
+      r[f] = make_rec(fr, P.psf);
+      amp_local = max(amp_local, __float_as_uint(fr.amp));
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const int ty = ty0 + dy, tx = tx0 + dx;
+          if (ty > ty1 || tx > tx1) continue;
+          const int d = ty * P.tiles_x + tx - t_lo;
+          if (d < 0 || d >= CL) continue;
+          dst[f][2 * dy + dx] = d;
+          rk[f][2 * dy + dx] = atomicAdd(&sh->rcnt[f][d], 1);   // local rank in this round
+        }
+    }
+    named_sync(1, np);
+    if (ptid < 2 * CL) {
+      const int f = ptid / CL, d = ptid - (ptid / CL) * CL;
+      const int c = sh->rcnt[f][d];
+      if (c) {
+        sh->rbase[f][d] = atomicAdd(cluster.map_shared_rank(&sh->fill[b][f], d), c);
+        sh->rcnt[f][d] = 0;
+      }
+    }
+    named_sync(1, np);
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+#pragma unroll
+      for (int k = 0; k < kMaxDest; ++k) {
+        const int d = dst[f][k];
+        if (d < 0) continue;
+        const int slot = sh->rbase[f][d] + rk[f][k];
+        if (slot < P.cap) {
+          store_rec(cluster.map_shared_rank(rec_b, d) + (size_t)f * P.cap + slot, r[f]);
+        } else if (slot - P.cap < P.spill_cap) {
+          store_rec(P.spill + (((size_t)(cluster_first + d) * 2 + b) * 2 + f) * P.spill_cap +
+                        (slot - P.cap), r[f]);
+        } else {
+          atomicAdd(P.overflow, 1);
+        }
+      }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    dmax_local = max(dmax_local, __shfl_xor_sync(~0u, dmax_local, o));
+    amp_local = max(amp_local, __shfl_xor_sync(~0u, amp_local, o));
+  }
+  if ((ptid & 31) == 0) {
+    if (dmax_local) atomicMax(&sh->pdmax, dmax_local);
+    if (amp_local) atomicMax(&sh->pamp, amp_local);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Consumer role: render one item from buffer b into this CTA's tile.
+// ----------------------------------------------------------------------------
 template <int MODE, int PSF>
-__global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const FusedParams P) {
+__device__ void consume_item(const FusedParams& P, SharedHdr* sh, int* acc0, Rec* rec_b,
+                             int* cells, int b, int pl, int pass, int rank, int ctid, int nc_thr) {
+  const int CL = P.CL;
+  const int cwarp = ctid >> 5, cwarps = nc_thr >> 5;
+  const int acc_ints = P.AH * P.AS;
+  const int t = pass * CL + rank;
+  const int M = sh->M[b];
+  int side;
+  float dmax = 0.f;
+  if (MODE == 0) {
+    dmax = __uint_as_float(sh->dmax_bits[b]);
+    // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
+    side = patch_side_exact(M == 0 ? P.g.d_hi : (double)dmax, P.g.patch_mult);
+    if (M == 0) dmax = (float)P.g.d_hi;
+  } else {
+    side = P.side_in[pl];
+  }
+  if (MODE == 0 && rank == 0 && pass == 0 && ctid == 0) {
+    if (P.st_ppp) P.st_ppp[pl] = sh->ppp[b];
+    if (P.st_M) P.st_M[pl] = M;
+    if (P.st_side) P.st_side[pl] = side;
+    if (P.st_dmax) P.st_dmax[pl] = dmax;
+  }
+  if (t < P.tiles) {
+    const int ty = t / P.tiles_x, tx = t - (t / P.tiles_x) * P.tiles_x;
+    const int r0 = P.row_lo + ty * P.TH;
+    const int nr = min(P.TH, P.row_hi - r0);
+    const int c0 = tx * P.TW;
+    const int nc = min(P.TW, P.W - c0);
+    const int h = side >> 1;
+    const float amp_max = fmaxf(__uint_as_float(sh->amp_bits[b]), 1e-30f);
+    // -- fixed-point shift per frame (the per-pixel sum of rounded contributions
+    //    must stay below 2^31): cheap bound from K; cell histogram only if the
+    //    cheap bound would cost precision (cells >= 2h+1 wide, so a pixel's
+    //    anchor window lies in a 2x2 block of cells).
+    if (ctid < P.nframes) {
+      const int K = min(sh->fill[b][ctid], P.cap + P.spill_cap);
+      sh->shift[ctid] = shift_for(max(K, 1), amp_max);
+      if (P.bin_counts) P.bin_counts[((size_t)pl * 2 + ctid) * P.tiles + t] = sh->fill[b][ctid];
+    }
+    named_sync(2, nc_thr);
+    for (int f = 0; f < P.nframes; ++f) {
+      if (sh->shift[f] >= kAccShift - 1) continue;
+      const int K = min(sh->fill[b][f], P.cap + P.spill_cap);
+      const Rec* local = rec_b + (size_t)f * P.cap;
+      const Rec* spill = P.spill + (((size_t)blockIdx.x * 2 + b) * 2 + f) * P.spill_cap;
+      const int S = max(2 * h + 1, kCellMin);
+      const int ncy = (nr + 2 * h + S - 1) / S, ncx = (nc + 2 * h + S - 1) / S;
+      if (ncy * ncx > P.cells_cap) continue;
+      if (ctid == 0) sh->cov_max = 0;
+      for (int e = ctid; e < ncy * ncx; e += nc_thr) cells[e] = 0;
+      named_sync(2, nc_thr);
+      for (int k = ctid; k < K; k += nc_thr) {
+        const Rec& c = k < P.cap ? local[k] : spill[k - P.cap];
+        const int cy = (c.axy >> 16) - (r0 - h), cx = (int)(short)(c.axy & 0xffff) - (c0 - h);
+        if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
+          atomicAdd(&cells[(cy / S) * ncx + cx / S], 1);
+      }
+      named_sync(2, nc_thr);
+      int cm = 0;
+      for (int e = ctid; e < ncy * ncx; e += nc_thr) {
+        const int cy = e / ncx, cx = e - (e / ncx) * ncx;
+        int sm = cells[e];
+        if (cx + 1 < ncx) sm += cells[e + 1];
+        if (cy + 1 < ncy) sm += cells[e + ncx];
+        if (cx + 1 < ncx && cy + 1 < ncy) sm += cells[e + ncx + 1];
+        cm = max(cm, sm);
+      }
+      for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
+      if ((ctid & 31) == 0) atomicMax(&sh->cov_max, cm);
+      named_sync(2, nc_thr);
+      if (ctid == 0) sh->shift[f] = shift_for(max(sh->cov_max, 1), amp_max);
+      named_sync(2, nc_thr);
+    }
+    // -- splat both frames (integer accumulation in shared memory)
+    for (int f = 0; f < P.nframes; ++f) {
+      const int K = min(sh->fill[b][f], P.cap + P.spill_cap);
+      const int shift = sh->shift[f];
+      splat_dispatch<PSF>(acc0 + (size_t)f * acc_ints, rec_b + (size_t)f * P.cap,
+                          P.spill + (((size_t)blockIdx.x * 2 + b) * 2 + f) * P.spill_cap, P.cap,
+                          K, side, r0 - P.pad, c0 - P.pad, P.AS, (float)shift,
+                          exp2f((float)shift), cwarp, cwarps);
+    }
+    named_sync(2, nc_thr);
+    // -- fused epilogue, then clear the accumulators for the next item
+    for (int f = 0; f < P.nframes; ++f)
+      store_tile(P, acc0 + (size_t)f * acc_ints, pl, f, r0, nr, c0, nc,
+                 exp2f(-(float)sh->shift[f]), ctid, nc_thr);
+    named_sync(2, nc_thr);
+    for (int e = ctid; e < (P.nframes * acc_ints) >> 2; e += nc_thr)
+      reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+  }
+  named_sync(2, nc_thr);
+  // -- release buffer b: reset its counters, then tell every producer
+  if (ctid == 0) {
+    sh->fill[b][0] = sh->fill[b][1] = 0;
+    sh->dmax_bits[b] = 0u;
+    sh->amp_bits[b] = 0u;
+    fence_cluster();
+    for (int d = 0; d < CL; ++d) mbar_arrive_remote(&sh->empty[b], d);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// The kernel: persistent clusters, warp-specialized producer / consumer
+// pipeline over double-buffered record lists.
+// ----------------------------------------------------------------------------
+template <int MODE, int PSF>
+__global__ void __launch_bounds__(kThreads, 1) fused_generate_kernel(const FusedParams P) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = P.CL;
   const int rank = (int)cluster.block_rank();
@@ -641,201 +869,93 @@ __global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const Fused
   const int nclusters = gridDim.x / CL;
   const int cluster_first = blockIdx.x - rank;
   const int tid = threadIdx.x;
+  const int np = P.prod_warps * 32;       // producer threads
+  const int nc_thr = kThreads - np;       // consumer threads
 
   extern __shared__ __align__(16) unsigned char smem[];
-  int* acc = reinterpret_cast<int*>(smem);
+  int* acc = reinterpret_cast<int*>(smem);                       // [nframes][AH*AS]
   const int acc_ints = P.AH * P.AS;
-  Rec* rec = reinterpret_cast<Rec*>(smem + (size_t)acc_ints * sizeof(int));
-  SharedHdr* sh = reinterpret_cast<SharedHdr*>(rec + (size_t)P.nframes * P.cap);
+  Rec* rec = reinterpret_cast<Rec*>(smem + (size_t)P.nframes * acc_ints * sizeof(int));
+  SharedHdr* sh = reinterpret_cast<SharedHdr*>(rec + (size_t)2 * P.nframes * P.cap);
   int* cells = reinterpret_cast<int*>(sh + 1);
-  Rec* my_spill = P.spill + (size_t)blockIdx.x * 2 * P.spill_cap;
 
-  for (int e = tid; e < (acc_ints >> 2); e += kThreads)
+  for (int e = tid; e < (P.nframes * acc_ints) >> 2; e += kThreads)
     reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sh->full[b], CL);
+      mbar_init(&sh->empty[b], CL);
+      sh->fill[b][0] = sh->fill[b][1] = 0;
+      sh->dmax_bits[b] = sh->amp_bits[b] = 0u;
+    }
+    sh->pdmax = sh->pamp = 0u;
+    for (int k = 0; k < kMaxCluster; ++k) sh->rcnt[0][k] = sh->rcnt[1][k] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster.sync();
 
   // this CTA's particle slice (fixed for every item)
   const int i_lo = (int)((long long)rank * P.n / CL);
   const int i_hi = (int)((long long)(rank + 1) * P.n / CL);
-
   const int items = P.pairs * P.passes;
-  for (int item = cid; item < items; item += nclusters) {
-    const int pl = item / P.passes;
-    const int pass = item - pl * P.passes;
 
-    // ---- init (local state only; remote traffic starts after the sync) -----
-    if (tid == 0) {
-      sh->fill[0] = sh->fill[1] = 0;
-      sh->dmax_bits = 0u;
-      sh->amp_bits = 0u;
-      sh->cov_max = 0;
-      int M = 0;
-      double ppp = 0.0;
-      if (MODE == 0) {
-        const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
-        const uint4 w = draw(key, 0u, kTagPair);
-        ppp = lerp_exact(P.g.ppp_lo, P.g.ppp_hi, u53_to_unit(w.x, w.y));
-        // m = round(ppp * H * W) clamped to [0, N]   (particles.py:80-83)
-        double m = rint(dmul(dmul(ppp, (double)P.g.H), (double)P.g.W));
-        m = fmin(fmax(m, 0.0), (double)P.n);
-        M = (int)m;
+  if (tid < np) {
+    // ===================== producers =====================
+    uint32_t eparity[2] = {1u, 1u};
+    int j = 0;
+    for (int item = cid; item < items; item += nclusters, ++j) {
+      const int b = j & 1;
+      const int pl = item / P.passes;
+      const int pass = item - pl * P.passes;
+      mbar_wait(&sh->empty[b], eparity[b]);
+      eparity[b] ^= 1u;
+      if (tid == 0) {
+        int M = 0;
+        double ppp = 0.0;
+        if (MODE == 0) {
+          const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
+          const uint4 w = draw(key, 0u, kTagPair);
+          ppp = lerp_exact(P.g.ppp_lo, P.g.ppp_hi, u53_to_unit(w.x, w.y));
+          // m = round(ppp * H * W) clamped to [0, N]   (particles.py:80-83)
+          double m = rint(dmul(dmul(ppp, (double)P.g.H), (double)P.g.W));
+          m = fmin(fmax(m, 0.0), (double)P.n);
+          M = (int)m;
+        }
+        sh->M[b] = M;
+        sh->ppp[b] = ppp;
       }
-      sh->M = M;
-      sh->ppp = ppp;
-    }
-    cluster.sync();
-    const int M = sh->M;
-
-    // ---- seeding + distributed binning (one pass) ----------------------------
-    const int hx = P.halo;
-    const int t_lo = pass * CL;
-    const float2* flow = MODE == 0
-        ? P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems : nullptr;
-    unsigned dmax_local = 0u, amp_local = 0u;
-    for (int base = i_lo; base < i_hi; base += kThreads) {
-      const int i = base + tid;
-      Particle pt;
-      if (i < i_hi) {
-        if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
-        else inject_particle(P, pl, i, pt);
-      } else {
-        pt.fr[0].on = pt.fr[1].on = false;
-        pt.active = false;
-      }
-      if (MODE == 0 && pt.active) dmax_local = max(dmax_local, __float_as_uint(pt.diam));
-#pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        if (f >= P.nframes) break;
-        const Frame& fr = pt.fr[f];
-        // destination tiles of the (2 hx + 1)^2 window within this pass
-        int ty0 = 1, ty1 = 0, tx0 = 1, tx1 = 0;
-        if (fr.on) {
-          const int rlo = max(fr.ay - hx, P.row_lo), rhi = min(fr.ay + hx, P.row_hi - 1);
-          const int clo = max(fr.ax - hx, 0), chi = min(fr.ax + hx, P.W - 1);
-          if (rlo <= rhi && clo <= chi) {
-            ty0 = (rlo - P.row_lo) >> P.th_shift;
-            ty1 = (rhi - P.row_lo) >> P.th_shift;
-            tx0 = clo >> P.tw_shift;
-            tx1 = chi >> P.tw_shift;
-          }
+      named_sync(1, np);
+      produce_item<MODE>(cluster, P, sh, rec + (size_t)b * P.nframes * P.cap, b, pl, pass, rank,
+                         cluster_first, i_lo, i_hi, tid, np);
+      named_sync(1, np);
+      if (tid == 0) {
+        const unsigned m = sh->pdmax, am = sh->pamp;
+        sh->pdmax = sh->pamp = 0u;
+        for (int d = 0; d < CL; ++d) {
+          if (m) atomicMax(cluster.map_shared_rank(&sh->dmax_bits[b], d), m);
+          if (am) atomicMax(cluster.map_shared_rank(&sh->amp_bits[b], d), am);
         }
-        const int nty = ty1 - ty0 + 1, ntx = tx1 - tx0 + 1;
-        const int ndest = (nty > 0 && ntx > 0) ? nty * ntx : 0;
-        Rec r;
-        if (ndest) {
-          r = make_rec(fr, P.psf);
-          amp_local = max(amp_local, __float_as_uint(fr.amp));
-        }
-        for (int e = 0; __any_sync(~0u, e < ndest); ++e) {
-          int dest = -1;
-          if (e < ndest) {
-            const int q = ntx == 1 ? e : e / ntx;
-            const int ty = ty0 + q, tx = tx0 + (e - q * ntx);
-            const int d = ty * P.tiles_x + tx - t_lo;
-            if (d >= 0 && d < CL) dest = d;
-          }
-          exchange(cluster, P, sh, rec, cluster_first, f, dest, r);
-        }
+        fence_cluster();
+        for (int d = 0; d < CL; ++d) mbar_arrive_remote(&sh->full[b], d);
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      dmax_local = max(dmax_local, __shfl_xor_sync(~0u, dmax_local, o));
-      amp_local = max(amp_local, __shfl_xor_sync(~0u, amp_local, o));
-    }
-    if ((tid & 31) == 0) {
-      if (dmax_local) atomicMax(&sh->dmax_bits, dmax_local);
-      if (amp_local) atomicMax(&sh->amp_bits, amp_local);
-    }
-    __syncthreads();
-    if (tid < CL) {
-      const unsigned m = sh->dmax_bits, am = sh->amp_bits;
-      if (m) atomicMax(cluster.map_shared_rank(&sh->dmax_bits, tid), m);
-      if (am) atomicMax(cluster.map_shared_rank(&sh->amp_bits, tid), am);
-    }
-    cluster.sync();
-
-    // ---- render --------------------------------------------------------------
-    const int t = pass * CL + rank;
-    int side;
-    float dmax = 0.f;
-    if (MODE == 0) {
-      dmax = __uint_as_float(sh->dmax_bits);
-      // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
-      side = patch_side_exact(M == 0 ? P.g.d_hi : (double)dmax, P.g.patch_mult);
-      if (M == 0) dmax = (float)P.g.d_hi;
-    } else {
-      side = P.side_in[pl];
-    }
-    if (MODE == 0 && rank == 0 && pass == 0 && tid == 0) {
-      if (P.st_ppp) P.st_ppp[pl] = sh->ppp;
-      if (P.st_M) P.st_M[pl] = M;
-      if (P.st_side) P.st_side[pl] = side;
-      if (P.st_dmax) P.st_dmax[pl] = dmax;
-    }
-    if (t >= P.tiles) continue;
-    const int ty = t / P.tiles_x, tx = t - (t / P.tiles_x) * P.tiles_x;
-    const int r0 = P.row_lo + ty * P.TH;
-    const int nr = min(P.TH, P.row_hi - r0);
-    const int c0 = tx * P.TW;
-    const int nc = min(P.TW, P.W - c0);
-    const int h = side >> 1;
-    const float amp_max = fmaxf(__uint_as_float(sh->amp_bits), 1e-30f);
-
-    for (int f = 0; f < P.nframes; ++f) {
-      int K = sh->fill[f];
-      if (P.bin_counts && tid == 0) P.bin_counts[((size_t)pl * 2 + f) * P.tiles + t] = K;
-      if (K > P.cap + P.spill_cap) K = P.cap + P.spill_cap;
-      const Rec* local = rec + (size_t)f * P.cap;
-      const Rec* spill = my_spill + (size_t)f * P.spill_cap;
-      // -- fixed-point shift: the per-pixel sum of rounded contributions must
-      //    stay below 2^31. Cheap bound from K first (one thread); if it would
-      //    cost precision (shift < 21) bound the per-pixel coverage with a cell
-      //    histogram (cells >= 2h+1 wide: a pixel's anchor window lies in a
-      //    2x2 block of cells).
-      if (tid == 0) sh->cov_max = shift_for(K, amp_max);
-      __syncthreads();
-      int shift = sh->cov_max;
-      if (shift < kAccShift - 1) {
-        const int S = max(2 * h + 1, kCellMin);
-        const int ncy = (nr + 2 * h + S - 1) / S, ncx = (nc + 2 * h + S - 1) / S;
-        if (ncy * ncx <= P.cells_cap) {
-          __syncthreads();
-          if (tid == 0) sh->cov_max = 0;
-          for (int e = tid; e < ncy * ncx; e += kThreads) cells[e] = 0;
-          __syncthreads();
-          for (int k = tid; k < K; k += kThreads) {
-            const Rec& c = k < P.cap ? local[k] : spill[k - P.cap];
-            const int cy = (c.axy >> 16) - (r0 - h), cx = (int)(short)(c.axy & 0xffff) - (c0 - h);
-            if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
-              atomicAdd(&cells[(cy / S) * ncx + cx / S], 1);
-          }
-          __syncthreads();
-          int cm = 0;
-          for (int e = tid; e < ncy * ncx; e += kThreads) {
-            const int cy = e / ncx, cx = e - (e / ncx) * ncx;
-            int sm = cells[e];
-            if (cx + 1 < ncx) sm += cells[e + 1];
-            if (cy + 1 < ncy) sm += cells[e + ncx];
-            if (cx + 1 < ncx && cy + 1 < ncy) sm += cells[e + ncx + 1];
-            cm = max(cm, sm);
-          }
-          for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
-          if ((tid & 31) == 0) atomicMax(&sh->cov_max, cm);
-          __syncthreads();
-          if (tid == 0) sh->cov_max = shift_for(max(sh->cov_max, 1), amp_max);
-          __syncthreads();
-          shift = sh->cov_max;
-        }
-      }
-      splat_dispatch<PSF>(acc, local, spill, P.cap, K, side, r0 - P.pad, c0 - P.pad, P.AS,
-                          (float)shift, exp2f((float)shift));
-      __syncthreads();
-      store_tile(P, acc, pl, f, r0, nr, c0, nc, exp2f(-(float)shift));
-      __syncthreads();
-      for (int e = tid; e < (acc_ints >> 2); e += kThreads)
-        reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
-      __syncthreads();
+  } else {
+    // ===================== consumers =====================
+    const int ctid = tid - np;
+    uint32_t fparity[2] = {0u, 0u};
+    int j = 0;
+    for (int item = cid; item < items; item += nclusters, ++j) {
+      const int b = j & 1;
+      const int pl = item / P.passes;
+      const int pass = item - pl * P.passes;
+      mbar_wait(&sh->full[b], fparity[b]);
+      fparity[b] ^= 1u;
+      consume_item<MODE, PSF>(P, sh, acc, rec + (size_t)b * P.nframes * P.cap, cells, b, pl, pass,
+                              rank, ctid, nc_thr);
     }
   }
+  // no CTA may leave while cluster peers can still reach its shared memory
+  cluster.sync();
 }
 
 }  // namespace pgb

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -193,11 +194,11 @@ struct Error {
 
 struct Plan {
   int TH, TW, tiles_y, tiles_x, tiles, CL, passes, cap, spill_cap, halo, cells_cap;
-  int th_shift, tw_shift, pad, AH, AS;
+  int th_shift, tw_shift, pad, AH, AS, prod_warps;
   size_t smem;
 };
 
-constexpr size_t kSmemTarget = 55 * 1024;   // four CTAs per SM
+constexpr size_t kSmemTarget = 200 * 1024;  // one 16-warp CTA per SM
 constexpr size_t kSmemMax = 220 * 1024;
 constexpr int kMaxClusterRun = 16;      // non-portable cluster size (opt-in attribute)
 
@@ -219,9 +220,11 @@ int pow2_ceil(int v) {
 Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, int cl_max) {
   Plan p{};
   p.halo = halo;
-  p.TW = std::min(128, std::max(4, pow2_ceil(W)));
-  p.TH = std::max(1, std::min(pow2_ceil(rows), 4096 / p.TW));
+  p.TW = std::min(256, std::max(4, pow2_ceil(W)));
+  p.TH = std::max(1, std::min(pow2_ceil(rows), 8192 / p.TW));
   p.TH = 1 << ilog2(p.TH);
+  // a (2*halo+1)-wide window must span at most 2 tiles per axis (kMaxDest = 4)
+  const int tmin = pow2_ceil(2 * halo + 1);
   p.pad = (2 * halo + 3) / 4 * 4;
   for (;;) {
     const double ext = (double)std::min(p.TH + 2 * halo, rows + 2 * halo) *
@@ -235,11 +238,12 @@ Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, 
     p.AS = p.TW + 2 * p.pad;
     p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
                   ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
-    p.smem = (size_t)p.AH * p.AS * 4 + (size_t)nframes * p.cap * sizeof(Rec) +
+    // nframes accumulators + double-buffered record lists
+    p.smem = (size_t)nframes * p.AH * p.AS * 4 + (size_t)2 * nframes * p.cap * sizeof(Rec) +
              sizeof(SharedHdr) + (size_t)p.cells_cap * 4;
     if (p.smem <= kSmemTarget) break;
-    if (p.TH > 1) p.TH >>= 1;
-    else if (p.TW > 4) p.TW >>= 1;
+    if (p.TH > std::max(1, std::min(tmin, pow2_ceil(rows)))) p.TH >>= 1;
+    else if (p.TW > std::max(4, std::min(tmin, pow2_ceil(W)))) p.TW >>= 1;
     else break;
   }
   PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
@@ -251,6 +255,8 @@ Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, 
   p.CL = std::max(1, std::min(p.tiles, cl_max));
   p.passes = (p.tiles + p.CL - 1) / p.CL;
   p.spill_cap = std::max(256, 2 * p.cap);
+  p.prod_warps = 4;
+  if (const char* e = std::getenv("PGB_PROD_WARPS")) p.prod_warps = std::max(1, std::min(15, std::atoi(e)));
   return p;
 }
 
@@ -329,12 +335,13 @@ void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
   P.CL = pl.CL; P.passes = pl.passes; P.cap = pl.cap; P.spill_cap = pl.spill_cap;
   P.halo = pl.halo; P.cells_cap = pl.cells_cap;
   P.th_shift = pl.th_shift; P.tw_shift = pl.tw_shift; P.pad = pl.pad; P.AH = pl.AH; P.AS = pl.AS;
+  P.prod_warps = pl.prod_warps;
   const int items = P.pairs * P.passes;
   if (items <= 0) return;
   const int maxc = max_active_clusters(fn, pl.CL, pl.smem);
   const int nclusters = std::min(items, maxc);
   DevWork& w = work_for_current();
-  const size_t spill_need = (size_t)nclusters * pl.CL * 2 * pl.spill_cap * sizeof(Rec);
+  const size_t spill_need = (size_t)nclusters * pl.CL * 4 * pl.spill_cap * sizeof(Rec);
   P.spill = static_cast<Rec*>(ensure(w.spill, w.spill_bytes, spill_need));
   P.overflow = w.overflow;
   cudaLaunchConfig_t cfg{};
