@@ -185,9 +185,11 @@ int pgb_apply_hiding_dev(int64_t n, uint64_t seed, uint64_t batch, int64_t gpair
                          const unsigned char* active, unsigned char* visible1,
                          unsigned char* visible2, void* stream);
 
-/* Tiling plan of the fused kernel for a config (for tests / tooling). */
+/* Tiling plan of the fused kernel for a config (for tests / tooling):
+ * screen tiles (render work items), particle chunks (generate work items),
+ * record capacity per (pair slot, frame, tile), shared memory per CTA. */
 typedef struct pgb_plan_info {
-  int tile_h, tile_w, tiles_y, tiles_x, cluster, passes, capacity, halo, smem_bytes, threads;
+  int tile_h, tile_w, tiles_y, tiles_x, chunks, chunk, capacity, halo, smem_bytes, threads;
 } pgb_plan_info;
 int pgb_plan(int height, int width, int64_t n_per_pair, double ppp_hi, int halo, int frames,
              pgb_plan_info* info);

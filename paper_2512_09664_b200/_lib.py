@@ -64,7 +64,7 @@ class PgbParticleOut(C.Structure):
 
 class PgbPlanInfo(C.Structure):
     _fields_ = [(name, C.c_int) for name in (
-        "tile_h", "tile_w", "tiles_y", "tiles_x", "cluster", "passes", "capacity", "halo",
+        "tile_h", "tile_w", "tiles_y", "tiles_x", "chunks", "chunk", "capacity", "halo",
         "smem_bytes", "threads")]
 
 

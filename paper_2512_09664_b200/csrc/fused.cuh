@@ -1,4 +1,4 @@
-// fused.cuh -- the batched image-pair generator as ONE persistent cluster kernel.
+// fused.cuh -- the batched image-pair generator as ONE persistent kernel.
 //
 // Replaces the body of Sampler._render_batch (reference pipeline.py:278-329):
 // per pair, sample_particles / perturb_frame2 / advect / apply_hiding
@@ -6,25 +6,23 @@
 // splat (raster.py:108-126 -> _native.pyx:14-66) and finalize
 // (raster.py:154-161) + quantize_u16 (export.py:19-20).
 //
-// Decomposition (B200-first):
-//   * a persistent grid of thread-block CLUSTERS; each cluster loops over
-//     (pair, pass) work items; CTA r of the cluster owns screen tile
-//     (pass * CL + r) of the image for both frames;
-//   * seeding (one pass): CTA r generates the particle slice
-//     [r*N/CL, (r+1)*N/CL) with Philox4x32-10 in fixed point + float32 (or
-//     reads injected oracle arrays), advects it through the bilinear flow,
-//     and bins every particle by destination tile -- a distributed counting
-//     sort: lanes with the same destination are grouped with match.any, the
-//     group leader reserves a contiguous slot range with ONE remote atomicAdd
-//     on the owner's fill counter, and the render-ready 32-byte records are
-//     stored straight into the owner CTA's shared memory through DSMEM;
-//   * render: each CTA splats its tile's records into a padded shared-memory
-//     fixed-point accumulator (int32, 2^-s units); integer addition is
-//     associative, so the per-pixel sum is exact and ORDER-INDEPENDENT: the
-//     output bits do not depend on scheduling, tiling, cluster size or GPU
-//     count (bit-identical shards);
-//   * fused epilogue: offset + Philox noise + clamp (+ uint16 quantisation),
-//     128-bit coalesced streaming stores of each frame of the tile.
+// Schedule (B200-first): a persistent grid pulls work tickets
+// from one global counter. Two kinds of work item:
+//   * GENERATE (pair p, chunk c): Philox seeding in fixed point + float32 (or
+//     oracle injection), bilinear advection, and a counting sort of the
+//     chunk's particles into per-(frame, screen tile) record lists of pair
+//     slot p % ring -- local shared-memory ranks, ONE global atomicAdd per
+//     (frame, tile) per round reserves the slots, coalesced record stores.
+//   * RENDER (pair p, tile t): waits until all chunks of p are binned, splats
+//     the tile's records into a padded shared-memory fixed-point accumulator
+//     (int32, 2^-s units; integer addition is associative, so pixel sums are
+//     exact and order-independent -> bit-identical output for any schedule,
+//     tiling or GPU count), then the fused epilogue (offset + Philox noise +
+//     clamp, optional uint16 quantisation) with 128-bit streaming stores.
+// Tickets are ordered so every wait targets an earlier ticket (deadlock-free):
+// generation runs `lookahead` pairs ahead of rendering; the record ring stays
+// L2-resident. Patch pixels whose value provably rounds to zero in the
+// fixed-point accumulator are skipped (tight window), which cannot change a bit.
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -35,8 +33,10 @@ namespace cg = cooperative_groups;
 
 namespace pgb {
 
-constexpr int kThreads = 512;   // 16 warps: producer warps + consumer warps
-constexpr int kMaxCluster = 16;
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+// generate-item staging (aliases the accumulator): 2 x kThreads records + 2 x 4 x kThreads (tile, rank)
+constexpr int kStageInts = 2 * kThreads * 8 + 16 * kThreads;
 constexpr int kAccShift = 22;     // max fixed-point fraction bits
 constexpr int kCellMin = 8;       // coverage-guard cell size floor
 constexpr float kLog2e = 1.4426950408889634f;
@@ -78,13 +78,25 @@ struct InjFrame {
   const uint8_t* mask;
 };
 
+// Per pair-slot bookkeeping in global memory (ring of `ring` slots).
+struct __align__(16) SlotHdr {
+  int gen_done;        // generate items of the current occupant finished
+  int render_done;     // render items finished
+  int epoch;           // number of occupants retired (slot of pair p is free when epoch == p / ring)
+  int M;               // active count
+  unsigned dmax;       // max active diameter (float bits)
+  unsigned amp;        // max record amplitude (float bits)
+  unsigned smax[2];    // per frame max(sigma_x, sigma_y) (float bits)
+  double ppp;          // realised seeding density
+};
+
 struct FusedParams {
   int H, W, row_lo, row_hi;
-  int TH, TW, tiles_y, tiles_x, tiles, CL, passes, th_shift, tw_shift;
-  int cap, spill_cap, halo, nframes, cells_cap;
-  int pad, AH, AS;   // accumulator: AH rows x AS ints (tile + pad on each side)
-  int prod_warps;    // producer warps per CTA (the rest render)
-  int n, pairs;
+  int TH, TW, tiles_y, tiles_x, tiles, th_shift, tw_shift;
+  int cap;                 // record capacity per (slot, frame, tile)
+  int halo, nframes, cells_cap;
+  int pad, AH, AS;         // accumulator: AH rows x AS ints (tile + pad on each side)
+  int n, pairs, chunk, chunks, ring, lookahead;
   long long pair_base;
   uint32_t batch_lo;
   int psf, out_mode;
@@ -103,24 +115,21 @@ struct FusedParams {
   int* st_side;
   float* st_dmax;
   int* bin_counts;
-  Rec* spill;
+  // workspace
+  Rec* recs;           // [ring][nframes][tiles][cap]
+  int* fills;          // [ring][nframes][tiles]
+  SlotHdr* slots;      // [ring]
+  int* ticket;         // work counter (zeroed before launch)
   int* overflow;
 };
 
-// Per-CTA control block. Index [b] = record buffer (double-buffered items).
-struct SharedHdr {
-  unsigned long long full[2];    // mbarrier: all CL producers wrote item into buffer b
-  unsigned long long empty[2];   // mbarrier: all CL consumers finished rendering buffer b
-  int fill[2][2];                // [b][frame] records received (remote atomicAdd)
-  unsigned dmax_bits[2];         // [b] max active diameter of the item (remote atomicMax)
-  unsigned amp_bits[2];          // [b] max record amplitude
-  int M[2];                      // [b] active count (local producers)
-  double ppp[2];                 // [b] seeding density
-  unsigned pdmax, pamp;          // producer-local partial maxima
-  int rcnt[2][kMaxCluster];      // producer round: records per (frame, destination)
-  int rbase[2][kMaxCluster];     // producer round: reserved base slot in the owner
-  int shift[2];                  // consumer scratch: fixed-point shift per frame
-  int cov_max;
+// Per-CTA shared control block.
+struct __align__(16) SharedHdr {
+  int item;            // current ticket
+  int rcnt[2][4];      // generate round: unused (kept for layout)
+  unsigned dmax, amp, smax[2];
+  int shift, weff, cov_max;
+  int M;
 };
 
 // ----------------------------------------------------------------------------
@@ -327,7 +336,7 @@ __device__ __forceinline__ Rec make_rec(const Frame& fr, int psf) {
 }
 
 // ----------------------------------------------------------------------------
-// Render: lanes = (candidate slot, patch column); each lane walks the rows.
+// Render: lanes = (candidate slot, patch column); each lane walks W rows.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -345,22 +354,35 @@ constexpr int kGLPoints = 8;
 __constant__ float kGLx[kGLPoints] = {-0.48014492824876809f, -0.39833323870681336f, -0.2627662049581645f, -0.09171732124782489f, 0.091717321247824893f, 0.2627662049581645f, 0.39833323870681336f, 0.48014492824876809f};
 __constant__ float kGLw[kGLPoints] = {0.050614268145188532f, 0.11119051722668721f, 0.15685332293894344f, 0.18134189168918083f, 0.18134189168918083f, 0.15685332293894344f, 0.11119051722668721f, 0.050614268145188532f};
 
-template <int S, int PSF>
-__device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, int side, int j,
-                                           int r0p, int c0p, int AS, float s_log2, float scale) {
-  const int side_ = S > 0 ? S : side;
-  const int h = side_ >> 1;
+// Tight window: the patch columns/rows a record can reach with a non-zero
+// fixed-point contribution. Column offsets j (relative to the anchor) with
+// |j - fx| > R give amp 2^s exp(-(j-fx)^2 / (2 sigma_x^2)) < 1/2 -> 0, because
+// min over dy of the quadratic form is dx^2 / (2 sigma_x^2). The window of W
+// offsets starts at clamp(ceil(fx - R), -h, h - W + 1) and so stays inside the
+// reference patch [-h, h] while covering every non-zero offset.
+__device__ __forceinline__ int window_start(float f, float R, int h, int W) {
+  const int lo = (int)ceilf(f - R);
+  return min(max(lo, -h), h - W + 1);
+}
+
+template <int WC, int PSF>
+__device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, int Wrt, int j,
+                                           int h, float R, int r0p, int c0p, int AS,
+                                           float s_log2, float scale) {
+  const int W = WC > 0 ? WC : Wrt;
   const int ay = r.axy >> 16;
   const int ax = (int)(short)(r.axy & 0xffff);
-  int* p = acc + (ay - h - r0p) * AS + (ax - h + j - c0p);
-  const float dx = (float)(j - h) - r.fx;
+  const int jo = window_start(r.fx, R, h, W) + j;      // this lane's column offset
+  const int io = window_start(r.fy, R, h, W);          // first row offset
+  int* p = acc + (ay + io - r0p) * AS + (ax + jo - c0p);
+  const float dx = (float)jo - r.fx;
   if (PSF == kPsfPoint) {
     const float Lx = fmaf(-r.A * dx, dx, r.L + s_log2);
     const float Bdx = r.B * dx;
-#pragma unroll
-    for (int i = 0; i < (S > 0 ? S : 64); ++i) {
-      if (S == 0 && i >= side_) break;
-      const float dy = (float)(i - h) - r.fy;
+#pragma unroll 5
+    for (int i = 0; i < (WC > 0 ? WC : 64); ++i) {
+      if (WC == 0 && i >= W) break;
+      const float dy = (float)(io + i) - r.fy;
       const float t = fmaf(r.C, dy, Bdx);
       const float e = fmaf(-t, dy, Lx);
       atomicAdd(p + i * AS, round_small(ex2_approx(e)));
@@ -369,8 +391,8 @@ __device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, 
     const bool sep = r.aux != 0.f;
     float ex = 0.f;
     if (sep) ex = erff((dx + 0.5f) * r.A) - erff((dx - 0.5f) * r.A);
-    for (int i = 0; i < side_; ++i) {
-      const float dy = (float)(i - h) - r.fy;
+    for (int i = 0; i < W; ++i) {
+      const float dy = (float)(io + i) - r.fy;
       float val;
       if (sep) {
         val = ex * (erff((dy + 0.5f) * r.B) - erff((dy - 0.5f) * r.B));
@@ -393,55 +415,51 @@ __device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, 
   }
 }
 
-template <int S, int PSF>
-__device__ __forceinline__ void splat_range(int* __restrict__ acc, const Rec* __restrict__ recs,
-                                            int K, int side_, int r0p, int c0p, int AS,
-                                            float s_log2, float scale, int warp, int kWarps) {
+__device__ __forceinline__ Rec load_rec(const Rec* q) {
+  const float4 a = __ldcg(reinterpret_cast<const float4*>(q));
+  const float4 b = __ldcg(reinterpret_cast<const float4*>(q) + 1);
+  Rec r;
+  r.axy = __float_as_int(a.x); r.fx = a.y; r.fy = a.z; r.L = a.w;
+  r.A = b.x; r.B = b.y; r.C = b.z; r.aux = b.w;
+  return r;
+}
+
+template <int WC, int PSF>
+__device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ recs, int K, int Wrt,
+                           int h, float R, int r0p, int c0p, int AS, float s_log2, float scale) {
+  const int W = WC > 0 ? WC : Wrt;
   const int lane = threadIdx.x & 31;
-  if (side_ <= 32) {
-    const int cpw = 32 / side_;                       // candidates per warp-step
-    const int slot = lane / side_;
-    const int j = lane - slot * side_;
+  const int warp = threadIdx.x >> 5;
+  if (W <= 32) {
+    const int cpw = 32 / W;                         // candidates per warp-step
+    const int slot = lane / W;
+    const int j = lane - slot * W;
     if (slot >= cpw) return;
-    for (int k = warp * cpw + slot; k < K; k += kWarps * cpw) {
-      const float4* q = reinterpret_cast<const float4*>(recs + k);
-      const float4 a = q[0], b = q[1];
-      Rec r;
-      r.axy = __float_as_int(a.x); r.fx = a.y; r.fy = a.z; r.L = a.w;
-      r.A = b.x; r.B = b.y; r.C = b.z; r.aux = b.w;
-      splat_lane<S, PSF>(acc, r, side_, j, r0p, c0p, AS, s_log2, scale);
-    }
+    for (int k = warp * cpw + slot; k < K; k += kWarps * cpw)
+      splat_lane<WC, PSF>(acc, load_rec(recs + k), W, j, h, R, r0p, c0p, AS, s_log2, scale);
   } else {
     // very large patches: the warp walks one candidate, lanes stride the columns
     for (int k = warp; k < K; k += kWarps) {
-      const Rec r = recs[k];
-      for (int jj = lane; jj < side_; jj += 32)
-        splat_lane<0, PSF>(acc, r, side_, jj, r0p, c0p, AS, s_log2, scale);
+      const Rec r = load_rec(recs + k);
+      for (int jj = lane; jj < W; jj += 32)
+        splat_lane<0, PSF>(acc, r, W, jj, h, R, r0p, c0p, AS, s_log2, scale);
     }
   }
 }
 
-template <int S, int PSF>
-__device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ local,
-                           const Rec* __restrict__ spill, int cap, int K, int side, int r0p,
-                           int c0p, int AS, float s_log2, float scale, int warp, int nwarps) {
-  const int side_ = S > 0 ? S : side;
-  splat_range<S, PSF>(acc, local, min(K, cap), side_, r0p, c0p, AS, s_log2, scale, warp, nwarps);
-  if (K > cap)
-    splat_range<S, PSF>(acc, spill, K - cap, side_, r0p, c0p, AS, s_log2, scale, warp, nwarps);
-}
-
 template <int PSF>
-__device__ void splat_dispatch(int* acc, const Rec* local, const Rec* spill, int cap, int K,
-                               int side, int r0p, int c0p, int AS, float s_log2, float scale,
-                               int warp, int nwarps) {
-#define PGB_SPLAT(SIDE) splat_tile<SIDE, PSF>(acc, local, spill, cap, K, side, r0p, c0p, AS, \
-                                              s_log2, scale, warp, nwarps)
+__device__ void splat_dispatch(int* acc, const Rec* recs, int K, int W, int h, float R, int r0p,
+                               int c0p, int AS, float s_log2, float scale) {
+#define PGB_SPLAT(WW) splat_tile<WW, PSF>(acc, recs, K, W, h, R, r0p, c0p, AS, s_log2, scale)
   if (PSF == kPsfPoint) {
-    switch (side) {
+    switch (W) {
+      case 2: PGB_SPLAT(2); return;
       case 3: PGB_SPLAT(3); return;
+      case 4: PGB_SPLAT(4); return;
       case 5: PGB_SPLAT(5); return;
+      case 6: PGB_SPLAT(6); return;
       case 7: PGB_SPLAT(7); return;
+      case 8: PGB_SPLAT(8); return;
       case 9: PGB_SPLAT(9); return;
       case 11: PGB_SPLAT(11); return;
       case 13: PGB_SPLAT(13); return;
@@ -458,6 +476,13 @@ __device__ __forceinline__ int shift_for(int cnt, float amp_max) {
   if (!(per >= 1.0)) return 0;
   int e = ilogb(per);                      // floor(log2(per)), exact
   return e < kAccShift ? e : kAccShift;
+}
+
+// Conservative zero radius (pixels) for records with sigma <= smax, amp <= amp_max.
+__device__ __forceinline__ float zero_radius(float smax, float amp_max, int shift) {
+  const double lnv = log((double)amp_max * ldexp(1.0, shift) / 0.49);
+  if (!(lnv > 0.0)) return 0.f;
+  return (float)((double)smax * sqrt(2.0 * lnv) * 1.0001 + 1e-4);
 }
 
 // ----------------------------------------------------------------------------
@@ -489,7 +514,6 @@ __device__ __forceinline__ uint16_t quant_u16(float x) {
 __device__ __forceinline__ float acc_to_float(int a) {
   return __int_as_float(a | 0x4B000000) - 8388608.0f;
 }
-
 // One output quad (4 pixels) of frame f.
 template <int OUT, bool NOISE>
 __device__ __forceinline__ void store_quad(const FusedParams& P, const int4 a, char* dst,
@@ -535,16 +559,16 @@ __device__ __forceinline__ void store_quad(const FusedParams& P, const int4 a, c
 
 template <int OUT, bool NOISE>
 __device__ void store_tile_vec(const FusedParams& P, const int* __restrict__ acc, int pl, int f,
-                               int r0, int nr, int c0, int nc, float inv_scale, int tix, int nth) {
+                               int r0, int nr, int c0, int nc, float inv_scale) {
   constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
   const int qpr = nc >> 2;
   char* outb = static_cast<char*>(P.out[f]) + (size_t)pl * (size_t)P.out_pair_elems * ESZ;
-  if ((qpr & (qpr - 1)) == 0 && qpr <= nth && (nth % qpr) == 0) {
+  if ((qpr & (qpr - 1)) == 0 && qpr <= kThreads) {
     // each thread owns one column quad and walks rows with constant pointer steps
-    const int cq = tix & (qpr - 1);
-    const int row0 = tix / qpr;
-    const int rstep = nth / qpr;
+    const int cq = threadIdx.x & (qpr - 1);
+    const int row0 = threadIdx.x / qpr;
+    const int rstep = kThreads / qpr;
     const int* ap = acc + (row0 + P.pad) * P.AS + P.pad + cq * 4;
     const int astep = rstep * P.AS;
     size_t pix = (size_t)(r0 + row0) * P.W + (size_t)(c0 + cq * 4);
@@ -554,7 +578,7 @@ __device__ void store_tile_vec(const FusedParams& P, const int* __restrict__ acc
                              gpair, inv_scale);
   } else {
     const int total = nr * qpr;
-    for (int e = tix; e < total; e += nth) {
+    for (int e = threadIdx.x; e < total; e += kThreads) {
       const int row = e / qpr;
       const int c = e - row * qpr;
       const size_t pix = (size_t)(r0 + row) * P.W + (size_t)(c0 + c * 4);
@@ -565,21 +589,21 @@ __device__ void store_tile_vec(const FusedParams& P, const int* __restrict__ acc
 }
 
 __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, int pl, int f,
-                           int r0, int nr, int c0, int nc, float inv_scale, int tix, int nth) {
+                           int r0, int nr, int c0, int nc, float inv_scale) {
   const int AS = P.AS, pad = P.pad;
   const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
   const bool noise = P.noise_std > 0.f;
   if (vec) {
     switch (P.out_mode) {
-      case kOutRaw: store_tile_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth); return;
-      case kOutAccum: store_tile_vec<kOutAccum, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth); return;
+      case kOutRaw: store_tile_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
+      case kOutAccum: store_tile_vec<kOutAccum, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
       case kOutF32:
-        if (noise) store_tile_vec<kOutF32, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
-        else store_tile_vec<kOutF32, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
+        if (noise) store_tile_vec<kOutF32, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        else store_tile_vec<kOutF32, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
         return;
       default:
-        if (noise) store_tile_vec<kOutU16, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
-        else store_tile_vec<kOutU16, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale, tix, nth);
+        if (noise) store_tile_vec<kOutU16, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        else store_tile_vec<kOutU16, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
         return;
     }
   }
@@ -588,7 +612,7 @@ __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, in
   const int mode = P.out_mode;
   const float bg = P.bg_offset, sd = P.noise_std;
   const int total = nr * nc;
-  for (int e = tix; e < total; e += nth) {
+  for (int e = threadIdx.x; e < total; e += kThreads) {
     const int row = e / nc;
     const int col = e - row * nc;
     float v = (float)acc[(row + pad) * AS + pad + col] * inv_scale;
@@ -612,69 +636,77 @@ __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, in
 }
 
 // ----------------------------------------------------------------------------
-// Cluster-scope mbarriers (producer -> consumer handoff without cluster.sync)
+// Work items
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void spin_until_geq(const int* p, int target) {
+  int ns = 32;
+  while (ld_acquire(p) < target) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : 1024;
+  }
 }
 
-// Arrive (release, cluster scope) on the same barrier in CTA `cta` of the cluster.
-__device__ __forceinline__ void mbar_arrive_remote(unsigned long long* bar, uint32_t cta) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
-}
-
-// Wait (acquire, cluster scope) for completion of the phase with the given parity.
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
-
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// ----------------------------------------------------------------------------
-// Producer role: seed / inject one item's particle slice and bin it into the
-// owners' buffer b -- a distributed counting sort through DSMEM, in rounds of
-// np particles: (1) local ranks per (frame, owner) from shared-memory atomics,
-// (2) one remote atomicAdd per (frame, owner) reserves the round's slot range
-// (a single round trip, issued in parallel), (3) fire-and-forget DSMEM stores.
-// ----------------------------------------------------------------------------
-constexpr int kMaxDest = 4;   // plans keep tiles >= 2*halo+1, so a window spans <= 2x2 tiles
-
-__device__ __forceinline__ void store_rec(Rec* dst, const Rec& r) {
+__device__ __forceinline__ void store_rec_global(Rec* dst, const Rec& r) {
   const float4* s4 = reinterpret_cast<const float4*>(&r);
-  float4* d4 = reinterpret_cast<float4*>(dst);
-  d4[0] = s4[0];
-  d4[1] = s4[1];
+  __stcg(reinterpret_cast<float4*>(dst), s4[0]);
+  __stcg(reinterpret_cast<float4*>(dst) + 1, s4[1]);
 }
 
+__device__ __forceinline__ int pair_M(const FusedParams& P, int pl, double* ppp_out) {
+  const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
+  const uint4 w = draw(key, 0u, kTagPair);
+  const double ppp = lerp_exact(P.g.ppp_lo, P.g.ppp_hi, u53_to_unit(w.x, w.y));
+  // m = round(ppp * H * W) clamped to [0, N]   (particles.py:80-83)
+  double m = rint(dmul(dmul(ppp, (double)P.g.H), (double)P.g.W));
+  m = fmin(fmax(m, 0.0), (double)P.n);
+  *ppp_out = ppp;
+  return (int)m;
+}
+
+// GENERATE (pair pl, chunk c): counting sort of the chunk's particles into the
+// per-(frame, tile) lists of the pair's slot, in rounds of kThreads particles:
+// local ranks from shared atomics, one global atomicAdd per (frame, tile) per
+// round, then the record stores.
+// `stage` aliases the render accumulator (re-zeroed at the end).
 template <int MODE>
-__device__ void produce_item(cg::cluster_group& cluster, const FusedParams& P, SharedHdr* sh,
-                             Rec* rec_b, int b, int pl, int pass, int rank, int cluster_first,
-                             int i_lo, int i_hi, int ptid, int np) {
-  const int CL = P.CL;
-  const int hx = P.halo;
-  const int t_lo = pass * CL;
-  const int M = sh->M[b];
+__device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int* base,
+                              int* stage, int pl, int c) {
+  const int tid = threadIdx.x;
+  const int slot = pl % P.ring;
+  SlotHdr* S = P.slots + slot;
+  const int T = P.tiles;
+  const int nf = P.nframes;
+  if (tid == 0) {
+    // the slot is free once its previous occupant (pair pl - ring) is fully rendered
+    spin_until_geq(&S->epoch, pl / P.ring);
+    double ppp = 0.0;
+    const int M = MODE == 0 ? pair_M(P, pl, &ppp) : 0;
+    sh->M = M;
+    sh->dmax = sh->amp = sh->smax[0] = sh->smax[1] = 0u;
+    if (c == 0) {
+      S->M = M;
+      S->ppp = ppp;
+    }
+  }
+  for (int e = tid; e < nf * T; e += kThreads) cnt[e] = 0;
+  __syncthreads();
+  const int M = sh->M;
+  int* fills = P.fills + (size_t)slot * nf * T;
+  Rec* recs = P.recs + (size_t)slot * nf * T * P.cap;
   const float2* flow = MODE == 0
       ? P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems : nullptr;
-  unsigned dmax_local = 0u, amp_local = 0u;
-  for (int base = i_lo; base < i_hi; base += np) {
-    const int i = base + ptid;
+  const int i_lo = c * P.chunk;
+  const int i_hi = min(P.n, i_lo + P.chunk);
+  const int hx = P.halo;
+  unsigned dmax_l = 0u, amp_l = 0u, smax_l[2] = {0u, 0u};
+  for (int b0 = i_lo; b0 < i_hi; b0 += kThreads) {
+    const int i = b0 + tid;
     Particle pt;
     if (i < i_hi) {
       if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
@@ -683,14 +715,16 @@ __device__ void produce_item(cg::cluster_group& cluster, const FusedParams& P, S
       pt.fr[0].on = pt.fr[1].on = false;
       pt.active = false;
     }
-    if (MODE == 0 && pt.active) dmax_local = max(dmax_local, __float_as_uint(pt.diam));
-    Rec r[2];
-    int dst[2][kMaxDest], rk[2][kMaxDest];   // statically indexed: slot = 2*dy + dx, dst < 0 = none
+    if (MODE == 0 && pt.active) dmax_l = max(dmax_l, __float_as_uint(pt.diam));
+    // stage records and (tile, rank) pairs in shared memory (keeps registers free)
+    Rec* st_rec = reinterpret_cast<Rec*>(stage);                   // [2][kThreads]
+    int* st_dst = reinterpret_cast<int*>(st_rec + 2 * kThreads);   // [2][4][kThreads]
+    int* st_rk = st_dst + 8 * kThreads;                            // [2][4][kThreads]
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
 #pragma unroll
-      for (int k = 0; k < kMaxDest; ++k) dst[f][k] = -1;
-      if (f >= P.nframes) continue;
+      for (int k = 0; k < 4; ++k) st_dst[(f * 4 + k) * kThreads + tid] = -1;
+      if (f >= nf) continue;
       const Frame& fr = pt.fr[f];
       if (!fr.on) continue;
       const int rlo = max(fr.ay - hx, P.row_lo), rhi = min(fr.ay + hx, P.row_hi - 1);
@@ -698,264 +732,220 @@ __device__ void produce_item(cg::cluster_group& cluster, const FusedParams& P, S
       if (rlo > rhi || clo > chi) continue;
       const int ty0 = (rlo - P.row_lo) >> P.th_shift, ty1 = (rhi - P.row_lo) >> P.th_shift;
       const int tx0 = clo >> P.tw_shift, tx1 = chi >> P.tw_shift;
-      r[f] = make_rec(fr, P.psf);
-      amp_local = max(amp_local, __float_as_uint(fr.amp));
+      const Rec r = make_rec(fr, P.psf);
+      {
+        const float4* s4 = reinterpret_cast<const float4*>(&r);
+        float4* d4 = reinterpret_cast<float4*>(st_rec + f * kThreads + tid);
+        d4[0] = s4[0];
+        d4[1] = s4[1];
+      }
+      amp_l = max(amp_l, __float_as_uint(fr.amp));
+      smax_l[f] = max(smax_l[f], __float_as_uint(fmaxf(fr.sx, fr.sy)));
 #pragma unroll
       for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
           const int ty = ty0 + dy, tx = tx0 + dx;
           if (ty > ty1 || tx > tx1) continue;
-          const int d = ty * P.tiles_x + tx - t_lo;
-          if (d < 0 || d >= CL) continue;
-          dst[f][2 * dy + dx] = d;
-          rk[f][2 * dy + dx] = atomicAdd(&sh->rcnt[f][d], 1);   // local rank in this round
+          const int t = ty * P.tiles_x + tx;
+          st_dst[(f * 4 + 2 * dy + dx) * kThreads + tid] = t;
+          st_rk[(f * 4 + 2 * dy + dx) * kThreads + tid] = atomicAdd(&cnt[f * T + t], 1);
         }
     }
-    named_sync(1, np);
-    if (ptid < 2 * CL) {
-      const int f = ptid / CL, d = ptid - (ptid / CL) * CL;
-      const int c = sh->rcnt[f][d];
-      if (c) {
-        sh->rbase[f][d] = atomicAdd(cluster.map_shared_rank(&sh->fill[b][f], d), c);
-        sh->rcnt[f][d] = 0;
+    __syncthreads();
+    for (int e = tid; e < nf * T; e += kThreads) {
+      const int n = cnt[e];
+      if (n) {
+        base[e] = atomicAdd(&fills[e], n);
+        cnt[e] = 0;
       }
     }
-    named_sync(1, np);
+    __syncthreads();
+    for (int f = 0; f < nf; ++f)
 #pragma unroll
-    for (int f = 0; f < 2; ++f)
-#pragma unroll
-      for (int k = 0; k < kMaxDest; ++k) {
-        const int d = dst[f][k];
-        if (d < 0) continue;
-        const int slot = sh->rbase[f][d] + rk[f][k];
-        if (slot < P.cap) {
-          store_rec(cluster.map_shared_rank(rec_b, d) + (size_t)f * P.cap + slot, r[f]);
-        } else if (slot - P.cap < P.spill_cap) {
-          store_rec(P.spill + (((size_t)(cluster_first + d) * 2 + b) * 2 + f) * P.spill_cap +
-                        (slot - P.cap), r[f]);
-        } else {
-          atomicAdd(P.overflow, 1);
-        }
+      for (int k = 0; k < 4; ++k) {
+        const int t = st_dst[(f * 4 + k) * kThreads + tid];
+        if (t < 0) continue;
+        const int sl = base[f * T + t] + st_rk[(f * 4 + k) * kThreads + tid];
+        if (sl < P.cap) store_rec_global(recs + ((size_t)f * T + t) * P.cap + sl, st_rec[f * kThreads + tid]);
+        else atomicAdd(P.overflow, 1);
       }
+    __syncthreads();   // base[] is rewritten next round
   }
   for (int o = 16; o > 0; o >>= 1) {
-    dmax_local = max(dmax_local, __shfl_xor_sync(~0u, dmax_local, o));
-    amp_local = max(amp_local, __shfl_xor_sync(~0u, amp_local, o));
+    dmax_l = max(dmax_l, __shfl_xor_sync(~0u, dmax_l, o));
+    amp_l = max(amp_l, __shfl_xor_sync(~0u, amp_l, o));
+    smax_l[0] = max(smax_l[0], __shfl_xor_sync(~0u, smax_l[0], o));
+    smax_l[1] = max(smax_l[1], __shfl_xor_sync(~0u, smax_l[1], o));
   }
-  if ((ptid & 31) == 0) {
-    if (dmax_local) atomicMax(&sh->pdmax, dmax_local);
-    if (amp_local) atomicMax(&sh->pamp, amp_local);
+  if ((tid & 31) == 0) {
+    atomicMax(&sh->dmax, dmax_l);
+    atomicMax(&sh->amp, amp_l);
+    atomicMax(&sh->smax[0], smax_l[0]);
+    atomicMax(&sh->smax[1], smax_l[1]);
   }
+  __syncthreads();
+  if (tid == 0) {
+    if (sh->dmax) atomicMax(&S->dmax, sh->dmax);
+    if (sh->amp) atomicMax(&S->amp, sh->amp);
+    if (sh->smax[0]) atomicMax(&S->smax[0], sh->smax[0]);
+    if (sh->smax[1]) atomicMax(&S->smax[1], sh->smax[1]);
+    __threadfence();   // records + counters before the release
+    atomicAdd(&S->gen_done, 1);
+  }
+  // restore the accumulator the staging area borrowed
+  for (int e = tid; e < kStageInts / 4; e += kThreads)
+    reinterpret_cast<int4*>(stage)[e] = make_int4(0, 0, 0, 0);
 }
 
-// ----------------------------------------------------------------------------
-// Consumer role: render one item from buffer b into this CTA's tile.
-// ----------------------------------------------------------------------------
+// RENDER (pair pl, tile t): both frames of one screen tile.
 template <int MODE, int PSF>
-__device__ void consume_item(const FusedParams& P, SharedHdr* sh, int* acc0, Rec* rec_b,
-                             int* cells, int b, int pl, int pass, int rank, int ctid, int nc_thr) {
-  const int CL = P.CL;
-  const int cwarp = ctid >> 5, cwarps = nc_thr >> 5;
-  const int acc_ints = P.AH * P.AS;
-  const int t = pass * CL + rank;
-  const int M = sh->M[b];
+__device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, int* cells, int pl,
+                            int t) {
+  const int tid = threadIdx.x;
+  const int slot = pl % P.ring;
+  SlotHdr* S = P.slots + slot;
+  const int T = P.tiles;
+  const int nf = P.nframes;
+  if (tid == 0) spin_until_geq(&S->gen_done, P.chunks);
+  __syncthreads();
+  const int M = MODE == 0 ? __ldcg(&S->M) : 0;
   int side;
   float dmax = 0.f;
   if (MODE == 0) {
-    dmax = __uint_as_float(sh->dmax_bits[b]);
+    dmax = __uint_as_float(__ldcg(&S->dmax));
     // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
     side = patch_side_exact(M == 0 ? P.g.d_hi : (double)dmax, P.g.patch_mult);
     if (M == 0) dmax = (float)P.g.d_hi;
   } else {
     side = P.side_in[pl];
   }
-  if (MODE == 0 && rank == 0 && pass == 0 && ctid == 0) {
-    if (P.st_ppp) P.st_ppp[pl] = sh->ppp[b];
+  if (MODE == 0 && t == 0 && tid == 0) {
+    if (P.st_ppp) P.st_ppp[pl] = __ldcg(&S->ppp);
     if (P.st_M) P.st_M[pl] = M;
     if (P.st_side) P.st_side[pl] = side;
     if (P.st_dmax) P.st_dmax[pl] = dmax;
   }
-  if (t < P.tiles) {
-    const int ty = t / P.tiles_x, tx = t - (t / P.tiles_x) * P.tiles_x;
-    const int r0 = P.row_lo + ty * P.TH;
-    const int nr = min(P.TH, P.row_hi - r0);
-    const int c0 = tx * P.TW;
-    const int nc = min(P.TW, P.W - c0);
-    const int h = side >> 1;
-    const float amp_max = fmaxf(__uint_as_float(sh->amp_bits[b]), 1e-30f);
-    // -- fixed-point shift per frame (the per-pixel sum of rounded contributions
-    //    must stay below 2^31): cheap bound from K; cell histogram only if the
-    //    cheap bound would cost precision (cells >= 2h+1 wide, so a pixel's
-    //    anchor window lies in a 2x2 block of cells).
-    if (ctid < P.nframes) {
-      const int K = min(sh->fill[b][ctid], P.cap + P.spill_cap);
-      sh->shift[ctid] = shift_for(max(K, 1), amp_max);
-      if (P.bin_counts) P.bin_counts[((size_t)pl * 2 + ctid) * P.tiles + t] = sh->fill[b][ctid];
-    }
-    named_sync(2, nc_thr);
-    for (int f = 0; f < P.nframes; ++f) {
-      if (sh->shift[f] >= kAccShift - 1) continue;
-      const int K = min(sh->fill[b][f], P.cap + P.spill_cap);
-      const Rec* local = rec_b + (size_t)f * P.cap;
-      const Rec* spill = P.spill + (((size_t)blockIdx.x * 2 + b) * 2 + f) * P.spill_cap;
-      const int S = max(2 * h + 1, kCellMin);
-      const int ncy = (nr + 2 * h + S - 1) / S, ncx = (nc + 2 * h + S - 1) / S;
-      if (ncy * ncx > P.cells_cap) continue;
-      if (ctid == 0) sh->cov_max = 0;
-      for (int e = ctid; e < ncy * ncx; e += nc_thr) cells[e] = 0;
-      named_sync(2, nc_thr);
-      for (int k = ctid; k < K; k += nc_thr) {
-        const Rec& c = k < P.cap ? local[k] : spill[k - P.cap];
-        const int cy = (c.axy >> 16) - (r0 - h), cx = (int)(short)(c.axy & 0xffff) - (c0 - h);
-        if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
-          atomicAdd(&cells[(cy / S) * ncx + cx / S], 1);
+  const int ty = t / P.tiles_x, tx = t - (t / P.tiles_x) * P.tiles_x;
+  const int r0 = P.row_lo + ty * P.TH;
+  const int nr = min(P.TH, P.row_hi - r0);
+  const int c0 = tx * P.TW;
+  const int nc = min(P.TW, P.W - c0);
+  const int h = side >> 1;
+  const float amp_max = fmaxf(__uint_as_float(__ldcg(&S->amp)), 1e-30f);
+  const int* fills = P.fills + (size_t)slot * nf * T;
+  const Rec* recs = P.recs + (size_t)slot * nf * T * P.cap;
+  const int acc_ints = P.AH * P.AS;
+  for (int f = 0; f < nf; ++f) {
+    const int Kf = __ldcg(&fills[f * T + t]);
+    const int K = min(Kf, P.cap);
+    const Rec* rl = recs + ((size_t)f * T + t) * P.cap;
+    if (P.bin_counts && tid == 0) P.bin_counts[((size_t)pl * 2 + f) * T + t] = Kf;
+    // -- fixed-point shift: per-pixel sum of rounded contributions < 2^31.
+    //    Cheap bound from K; cell histogram only if it would cost precision
+    //    (cells >= 2h+1 wide, so a pixel's anchor window lies in 2x2 cells).
+    int shift = shift_for(max(K, 1), amp_max);
+    if (shift < kAccShift - 1) {
+      const int Sc = max(2 * h + 1, kCellMin);
+      const int ncy = (nr + 2 * h + Sc - 1) / Sc, ncx = (nc + 2 * h + Sc - 1) / Sc;
+      if (ncy * ncx <= P.cells_cap) {
+        if (tid == 0) sh->cov_max = 0;
+        for (int e = tid; e < ncy * ncx; e += kThreads) cells[e] = 0;
+        __syncthreads();
+        for (int k = tid; k < K; k += kThreads) {
+          const int axy = __ldcg(&rl[k].axy);
+          const int cy = (axy >> 16) - (r0 - h), cx = (int)(short)(axy & 0xffff) - (c0 - h);
+          if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
+            atomicAdd(&cells[(cy / Sc) * ncx + cx / Sc], 1);
+        }
+        __syncthreads();
+        int cm = 0;
+        for (int e = tid; e < ncy * ncx; e += kThreads) {
+          const int cy = e / ncx, cx = e - (e / ncx) * ncx;
+          int sm = cells[e];
+          if (cx + 1 < ncx) sm += cells[e + 1];
+          if (cy + 1 < ncy) sm += cells[e + ncx];
+          if (cx + 1 < ncx && cy + 1 < ncy) sm += cells[e + ncx + 1];
+          cm = max(cm, sm);
+        }
+        for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
+        if ((tid & 31) == 0) atomicMax(&sh->cov_max, cm);
+        __syncthreads();
+        shift = shift_for(max(sh->cov_max, 1), amp_max);
       }
-      named_sync(2, nc_thr);
-      int cm = 0;
-      for (int e = ctid; e < ncy * ncx; e += nc_thr) {
-        const int cy = e / ncx, cx = e - (e / ncx) * ncx;
-        int sm = cells[e];
-        if (cx + 1 < ncx) sm += cells[e + 1];
-        if (cy + 1 < ncy) sm += cells[e + ncx];
-        if (cx + 1 < ncx && cy + 1 < ncy) sm += cells[e + ncx + 1];
-        cm = max(cm, sm);
-      }
-      for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
-      if ((ctid & 31) == 0) atomicMax(&sh->cov_max, cm);
-      named_sync(2, nc_thr);
-      if (ctid == 0) sh->shift[f] = shift_for(max(sh->cov_max, 1), amp_max);
-      named_sync(2, nc_thr);
     }
-    // -- splat both frames (integer accumulation in shared memory)
-    for (int f = 0; f < P.nframes; ++f) {
-      const int K = min(sh->fill[b][f], P.cap + P.spill_cap);
-      const int shift = sh->shift[f];
-      splat_dispatch<PSF>(acc0 + (size_t)f * acc_ints, rec_b + (size_t)f * P.cap,
-                          P.spill + (((size_t)blockIdx.x * 2 + b) * 2 + f) * P.spill_cap, P.cap,
-                          K, side, r0 - P.pad, c0 - P.pad, P.AS, (float)shift,
-                          exp2f((float)shift), cwarp, cwarps);
+    // -- tight window (exact: skipped pixels would round to 0)
+    const int side_w = 2 * h + 1;
+    int W = side_w;
+    float R = (float)(h + 1);
+    if (PSF == kPsfPoint) {
+      const float smax = __uint_as_float(__ldcg(&S->smax[f]));
+      R = zero_radius(smax, amp_max, shift);
+      W = min(side_w, (int)floorf(2.0f * R) + 1);
+      W = max(W, 1);
     }
-    named_sync(2, nc_thr);
-    // -- fused epilogue, then clear the accumulators for the next item
-    for (int f = 0; f < P.nframes; ++f)
-      store_tile(P, acc0 + (size_t)f * acc_ints, pl, f, r0, nr, c0, nc,
-                 exp2f(-(float)sh->shift[f]), ctid, nc_thr);
-    named_sync(2, nc_thr);
-    for (int e = ctid; e < (P.nframes * acc_ints) >> 2; e += nc_thr)
-      reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+    splat_dispatch<PSF>(acc, rl, K, W, h, R, r0 - P.pad, c0 - P.pad, P.AS, (float)shift,
+                        exp2f((float)shift));
+    __syncthreads();
+    store_tile(P, acc, pl, f, r0, nr, c0, nc, exp2f(-(float)shift));
+    __syncthreads();
+    for (int e = tid; e < acc_ints >> 2; e += kThreads)
+      reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
+    __syncthreads();
   }
-  named_sync(2, nc_thr);
-  // -- release buffer b: reset its counters, then tell every producer
-  if (ctid == 0) {
-    sh->fill[b][0] = sh->fill[b][1] = 0;
-    sh->dmax_bits[b] = 0u;
-    sh->amp_bits[b] = 0u;
-    fence_cluster();
-    for (int d = 0; d < CL; ++d) mbar_arrive_remote(&sh->empty[b], d);
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&S->render_done, 1) == T - 1) {
+      // last renderer retires the slot: reset it, then publish the new epoch
+      int* fl = P.fills + (size_t)slot * nf * T;
+      for (int e = 0; e < nf * T; ++e) fl[e] = 0;
+      S->gen_done = 0;
+      S->render_done = 0;
+      S->dmax = S->amp = S->smax[0] = S->smax[1] = 0u;
+      __threadfence();
+      atomicAdd(&S->epoch, 1);
+    }
   }
 }
 
 // ----------------------------------------------------------------------------
-// The kernel: persistent clusters, warp-specialized producer / consumer
-// pipeline over double-buffered record lists.
+// The kernel: persistent CTAs pulling ordered tickets.
+//   [gen items of pairs 0 .. L-1] then, per pair p: [render tiles of p][gen chunks of p + L]
 // ----------------------------------------------------------------------------
 template <int MODE, int PSF>
-__global__ void __launch_bounds__(kThreads, 1) fused_generate_kernel(const FusedParams P) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CL = P.CL;
-  const int rank = (int)cluster.block_rank();
-  const int cid = blockIdx.x / CL;
-  const int nclusters = gridDim.x / CL;
-  const int cluster_first = blockIdx.x - rank;
-  const int tid = threadIdx.x;
-  const int np = P.prod_warps * 32;       // producer threads
-  const int nc_thr = kThreads - np;       // consumer threads
-
+__global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const FusedParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  int* acc = reinterpret_cast<int*>(smem);                       // [nframes][AH*AS]
+  int* acc = reinterpret_cast<int*>(smem);
   const int acc_ints = P.AH * P.AS;
-  Rec* rec = reinterpret_cast<Rec*>(smem + (size_t)P.nframes * acc_ints * sizeof(int));
-  SharedHdr* sh = reinterpret_cast<SharedHdr*>(rec + (size_t)2 * P.nframes * P.cap);
-  int* cells = reinterpret_cast<int*>(sh + 1);
-
-  for (int e = tid; e < (P.nframes * acc_ints) >> 2; e += kThreads)
+  SharedHdr* sh = reinterpret_cast<SharedHdr*>(acc + max(acc_ints, kStageInts));
+  int* cnt = reinterpret_cast<int*>(sh + 1);               // [nframes * tiles]
+  int* base = cnt + P.nframes * P.tiles;                   // [nframes * tiles]
+  int* cells = base + P.nframes * P.tiles;                 // [cells_cap]
+  const int tid = threadIdx.x;
+  for (int e = tid; e < max(acc_ints, kStageInts) >> 2; e += kThreads)
     reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
-  if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sh->full[b], CL);
-      mbar_init(&sh->empty[b], CL);
-      sh->fill[b][0] = sh->fill[b][1] = 0;
-      sh->dmax_bits[b] = sh->amp_bits[b] = 0u;
-    }
-    sh->pdmax = sh->pamp = 0u;
-    for (int k = 0; k < kMaxCluster; ++k) sh->rcnt[0][k] = sh->rcnt[1][k] = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  cluster.sync();
-
-  // this CTA's particle slice (fixed for every item)
-  const int i_lo = (int)((long long)rank * P.n / CL);
-  const int i_hi = (int)((long long)(rank + 1) * P.n / CL);
-  const int items = P.pairs * P.passes;
-
-  if (tid < np) {
-    // ===================== producers =====================
-    uint32_t eparity[2] = {1u, 1u};
-    int j = 0;
-    for (int item = cid; item < items; item += nclusters, ++j) {
-      const int b = j & 1;
-      const int pl = item / P.passes;
-      const int pass = item - pl * P.passes;
-      mbar_wait(&sh->empty[b], eparity[b]);
-      eparity[b] ^= 1u;
-      if (tid == 0) {
-        int M = 0;
-        double ppp = 0.0;
-        if (MODE == 0) {
-          const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
-          const uint4 w = draw(key, 0u, kTagPair);
-          ppp = lerp_exact(P.g.ppp_lo, P.g.ppp_hi, u53_to_unit(w.x, w.y));
-          // m = round(ppp * H * W) clamped to [0, N]   (particles.py:80-83)
-          double m = rint(dmul(dmul(ppp, (double)P.g.H), (double)P.g.W));
-          m = fmin(fmax(m, 0.0), (double)P.n);
-          M = (int)m;
-        }
-        sh->M[b] = M;
-        sh->ppp[b] = ppp;
-      }
-      named_sync(1, np);
-      produce_item<MODE>(cluster, P, sh, rec + (size_t)b * P.nframes * P.cap, b, pl, pass, rank,
-                         cluster_first, i_lo, i_hi, tid, np);
-      named_sync(1, np);
-      if (tid == 0) {
-        const unsigned m = sh->pdmax, am = sh->pamp;
-        sh->pdmax = sh->pamp = 0u;
-        for (int d = 0; d < CL; ++d) {
-          if (m) atomicMax(cluster.map_shared_rank(&sh->dmax_bits[b], d), m);
-          if (am) atomicMax(cluster.map_shared_rank(&sh->amp_bits[b], d), am);
-        }
-        fence_cluster();
-        for (int d = 0; d < CL; ++d) mbar_arrive_remote(&sh->full[b], d);
+  const int T = P.tiles, G = P.chunks, L = P.lookahead, NP = P.pairs;
+  const long long pre = (long long)min(L, NP) * G;
+  const long long total = pre + (long long)NP * (T + G);
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) sh->item = atomicAdd(P.ticket, 1);
+    __syncthreads();
+    const long long tk = sh->item;
+    if (tk >= total) break;
+    if (tk < pre) {
+      generate_item<MODE>(P, sh, cnt, base, acc, (int)(tk / G), (int)(tk % G));
+    } else {
+      const long long u = tk - pre;
+      const int p = (int)(u / (T + G));
+      const int r = (int)(u - (long long)p * (T + G));
+      if (r < T) {
+        render_item<MODE, PSF>(P, sh, acc, cells, p, r);
+      } else if (p + L < NP) {
+        generate_item<MODE>(P, sh, cnt, base, acc, p + L, r - T);
       }
     }
-  } else {
-    // ===================== consumers =====================
-    const int ctid = tid - np;
-    uint32_t fparity[2] = {0u, 0u};
-    int j = 0;
-    for (int item = cid; item < items; item += nclusters, ++j) {
-      const int b = j & 1;
-      const int pl = item / P.passes;
-      const int pass = item - pl * P.passes;
-      mbar_wait(&sh->full[b], fparity[b]);
-      fparity[b] ^= 1u;
-      consume_item<MODE, PSF>(P, sh, acc, rec + (size_t)b * P.nframes * P.cap, cells, b, pl, pass,
-                              rank, ctid, nc_thr);
-    }
   }
-  // no CTA may leave while cluster peers can still reach its shared memory
-  cluster.sync();
 }
 
 }  // namespace pgb

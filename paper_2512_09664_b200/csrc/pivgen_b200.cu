@@ -193,14 +193,14 @@ struct Error {
   } while (0)
 
 struct Plan {
-  int TH, TW, tiles_y, tiles_x, tiles, CL, passes, cap, spill_cap, halo, cells_cap;
-  int th_shift, tw_shift, pad, AH, AS, prod_warps;
+  int TH, TW, tiles_y, tiles_x, tiles, cap, halo, cells_cap;
+  int th_shift, tw_shift, pad, AH, AS;
+  int chunk, chunks;
   size_t smem;
 };
 
-constexpr size_t kSmemTarget = 200 * 1024;  // one 16-warp CTA per SM
+constexpr size_t kSmemTarget = 44 * 1024;   // four-five 128-thread CTAs per SM
 constexpr size_t kSmemMax = 220 * 1024;
-constexpr int kMaxClusterRun = 16;      // non-portable cluster size (opt-in attribute)
 
 int ilog2(int v) {
   int s = 0;
@@ -214,55 +214,54 @@ int pow2_ceil(int v) {
   return p;
 }
 
-// Tiles are powers of two (shift-based binning); the accumulator carries a
-// pad of 2*halo (rounded to 4 ints) on every side so that patches of halo
-// particles need no clipping.
-Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, int cl_max) {
+// Tiles are powers of two (shift-based binning) and at least 2*halo+1 wide
+// (a window spans <= 2x2 tiles); the accumulator carries a pad of 2*halo
+// (rounded to 4 ints) on every side so halo records need no clipping.
+Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes) {
   Plan p{};
   p.halo = halo;
   p.TW = std::min(256, std::max(4, pow2_ceil(W)));
   p.TH = std::max(1, std::min(pow2_ceil(rows), 8192 / p.TW));
   p.TH = 1 << ilog2(p.TH);
-  // a (2*halo+1)-wide window must span at most 2 tiles per axis (kMaxDest = 4)
   const int tmin = pow2_ceil(2 * halo + 1);
   p.pad = (2 * halo + 3) / 4 * 4;
   for (;;) {
-    const double ext = (double)std::min(p.TH + 2 * halo, rows + 2 * halo) *
-                       (double)std::min(p.TW + 2 * halo, W + 2 * halo);
-    const double lam = std::min((double)n, (double)n * ext / ((double)H_full * (double)W));
-    long long cap = (long long)std::ceil(lam + 6.0 * std::sqrt(lam) + 32.0);
-    cap = std::min<long long>(cap, std::max<long long>(n, 1));
-    cap = (cap + 7) / 8 * 8;
-    p.cap = (int)cap;
     p.AH = p.TH + 2 * p.pad;
     p.AS = p.TW + 2 * p.pad;
-    p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
-                  ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
-    // nframes accumulators + double-buffered record lists
-    p.smem = (size_t)nframes * p.AH * p.AS * 4 + (size_t)2 * nframes * p.cap * sizeof(Rec) +
-             sizeof(SharedHdr) + (size_t)p.cells_cap * 4;
+    p.smem = (size_t)p.AH * p.AS * 4;
     if (p.smem <= kSmemTarget) break;
     if (p.TH > std::max(1, std::min(tmin, pow2_ceil(rows)))) p.TH >>= 1;
     else if (p.TW > std::max(4, std::min(tmin, pow2_ceil(W)))) p.TW >>= 1;
     else break;
   }
-  PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
   p.th_shift = ilog2(p.TH);
   p.tw_shift = ilog2(p.TW);
   p.tiles_y = (rows + p.TH - 1) / p.TH;
   p.tiles_x = (W + p.TW - 1) / p.TW;
   p.tiles = p.tiles_y * p.tiles_x;
-  p.CL = std::max(1, std::min(p.tiles, cl_max));
-  p.passes = (p.tiles + p.CL - 1) / p.CL;
-  p.spill_cap = std::max(256, 2 * p.cap);
-  p.prod_warps = 4;
-  if (const char* e = std::getenv("PGB_PROD_WARPS")) p.prod_warps = std::max(1, std::min(15, std::atoi(e)));
+  // record capacity per (slot, frame, tile): generous (global memory), so
+  // only pathological flows (strong convergence) can overflow
+  const double ext = (double)std::min(p.TH + 2 * halo, rows + 2 * halo) *
+                     (double)std::min(p.TW + 2 * halo, W + 2 * halo);
+  const double lam = std::min((double)n, (double)n * ext / ((double)H_full * (double)W));
+  long long cap = (long long)std::ceil(2.0 * lam + 10.0 * std::sqrt(lam) + 64.0);
+  cap = std::min<long long>(cap, std::max<long long>(n, 1));
+  p.cap = (int)((cap + 7) / 8 * 8);
+  p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
+                ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
+  p.chunk = 4 * kThreads;
+  p.chunks = (int)std::max<long long>(1, (n + p.chunk - 1) / p.chunk);
+  p.smem = std::max(p.smem, (size_t)kStageInts * 4);   // generate staging aliases the accumulator
+  p.smem += sizeof(SharedHdr) + (size_t)(2 * nframes * p.tiles + p.cells_cap) * 4;
+  PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
   return p;
 }
 
 struct DevWork {
-  void* spill = nullptr;
-  size_t spill_bytes = 0;
+  void* ring = nullptr;       // recs
+  size_t ring_bytes = 0;
+  void* ctl = nullptr;        // ticket + slots + fills (memset per launch)
+  size_t ctl_bytes = 0;
   int* overflow = nullptr;
   // host-API staging
   void* stage = nullptr;
@@ -300,63 +299,53 @@ KernelFn pick_kernel(int mode, int psf) {
   return psf == kPsfErf ? fused_generate_kernel<1, kPsfErf> : fused_generate_kernel<1, kPsfPoint>;
 }
 
-int max_active_clusters(KernelFn fn, int CL, size_t smem) {
-  static std::map<std::tuple<void*, int, size_t, int>, int> cache;
+int resident_ctas(KernelFn fn, size_t smem) {
+  static std::map<std::tuple<void*, size_t, int>, int> cache;
   int dev = 0;
   PGB_CK(cudaGetDevice(&dev));
-  auto key = std::make_tuple((void*)fn, CL, smem, dev);
+  auto key = std::make_tuple((void*)fn, smem, dev);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  // The dynamic-smem limit is a per-function attribute: set it once to the
-  // largest plan we ever build so later, smaller plans never shrink it.
   PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
-  if (CL > 8) PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CL * 64);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int num = 0;
-  PGB_CK(cudaOccupancyMaxActiveClusters(&num, (const void*)fn, &cfg));
-  PGB_REQUIRE(num > 0, "cluster configuration cannot be scheduled");
-  cache[key] = num;
-  return num;
+  int per_sm = 0, sms = 0;
+  PGB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kThreads, smem));
+  PGB_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PGB_REQUIRE(per_sm > 0, "kernel configuration cannot be scheduled");
+  cache[key] = per_sm * sms;
+  return per_sm * sms;
 }
 
 void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
   KernelFn fn = pick_kernel(P.mode, P.psf);
   P.TH = pl.TH; P.TW = pl.TW; P.tiles_y = pl.tiles_y; P.tiles_x = pl.tiles_x; P.tiles = pl.tiles;
-  P.CL = pl.CL; P.passes = pl.passes; P.cap = pl.cap; P.spill_cap = pl.spill_cap;
-  P.halo = pl.halo; P.cells_cap = pl.cells_cap;
-  P.th_shift = pl.th_shift; P.tw_shift = pl.tw_shift; P.pad = pl.pad; P.AH = pl.AH; P.AS = pl.AS;
-  P.prod_warps = pl.prod_warps;
-  const int items = P.pairs * P.passes;
-  if (items <= 0) return;
-  const int maxc = max_active_clusters(fn, pl.CL, pl.smem);
-  const int nclusters = std::min(items, maxc);
+  P.th_shift = pl.th_shift; P.tw_shift = pl.tw_shift; P.cap = pl.cap; P.halo = pl.halo;
+  P.cells_cap = pl.cells_cap; P.pad = pl.pad; P.AH = pl.AH; P.AS = pl.AS;
+  P.chunk = pl.chunk; P.chunks = pl.chunks;
+  if (P.pairs <= 0) return;
+  const int ctas = resident_ctas(fn, pl.smem);
+  const long long items_per_pair = (long long)pl.tiles + pl.chunks;
+  // generation runs `lookahead` pairs ahead of rendering; the ring holds the
+  // pairs in flight (> lookahead, so every wait targets an earlier ticket)
+  int L = (int)std::ceil(1.5 * ctas / (double)items_per_pair);
+  L = std::max(1, std::min(L, P.pairs));
+  const int ring = std::min(P.pairs, L + std::max(4, L / 4));
+  P.lookahead = L;
+  P.ring = std::max(ring, std::min(P.pairs, L + 1));
   DevWork& w = work_for_current();
-  const size_t spill_need = (size_t)nclusters * pl.CL * 4 * pl.spill_cap * sizeof(Rec);
-  P.spill = static_cast<Rec*>(ensure(w.spill, w.spill_bytes, spill_need));
+  const size_t recs_bytes = (size_t)P.ring * P.nframes * pl.tiles * pl.cap * sizeof(Rec);
+  const size_t slots_bytes = (size_t)P.ring * sizeof(SlotHdr);
+  const size_t fills_bytes = (size_t)P.ring * P.nframes * pl.tiles * sizeof(int);
+  const size_t ctl_bytes = 256 + slots_bytes + fills_bytes;
+  P.recs = static_cast<Rec*>(ensure(w.ring, w.ring_bytes, recs_bytes));
+  char* ctl = static_cast<char*>(ensure(w.ctl, w.ctl_bytes, ctl_bytes));
+  P.ticket = reinterpret_cast<int*>(ctl);
+  P.slots = reinterpret_cast<SlotHdr*>(ctl + 256);
+  P.fills = reinterpret_cast<int*>(ctl + 256 + slots_bytes);
   P.overflow = w.overflow;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(nclusters * pl.CL);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = pl.smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = pl.CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PGB_CK(cudaLaunchKernelEx(&cfg, fn, P));
+  PGB_CK(cudaMemsetAsync(ctl, 0, ctl_bytes, stream));
+  const long long total = (long long)std::min(L, P.pairs) * pl.chunks + (long long)P.pairs * items_per_pair;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(ctas, total));
+  fn<<<grid, kThreads, pl.smem, stream>>>(P);
   g_launches.fetch_add(1);
 }
 
@@ -485,7 +474,7 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
     P.st_dmax = stats->d_max;
   }
   P.bin_counts = bin_counts;
-  const Plan pl = make_plan(cfg->height, cfg->height, cfg->width, cfg->n_capacity, halo, 2, kMaxClusterRun);
+  const Plan pl = make_plan(cfg->height, cfg->height, cfg->width, cfg->n_capacity, halo, 2);
   launch_fused(P, pl, stream);
 }
 
@@ -510,9 +499,9 @@ int pgb_plan(int height, int width, int64_t n_per_pair, double ppp_hi, int halo,
   (void)ppp_hi;
   return guarded([&] {
     PGB_REQUIRE(info != nullptr, "info is NULL");
-    const Plan p = make_plan(height, height, width, n_per_pair, halo, frames, kMaxClusterRun);
+    const Plan p = make_plan(height, height, width, n_per_pair, halo, frames);
     info->tile_h = p.TH; info->tile_w = p.TW; info->tiles_y = p.tiles_y; info->tiles_x = p.tiles_x;
-    info->cluster = p.CL; info->passes = p.passes; info->capacity = p.cap; info->halo = p.halo;
+    info->chunks = p.chunks; info->chunk = p.chunk; info->capacity = p.cap; info->halo = p.halo;
     info->smem_bytes = (int)p.smem; info->threads = kThreads;
   });
 }
@@ -546,7 +535,7 @@ int pgb_splat_accumulate_dev(const double* pos, const float* i0, const float* si
     PGB_CK(cudaMemcpyAsync(side_dev, &side, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
     P.side_in = side_dev;
     P.out[0] = out;
-    const Plan pl = make_plan(height, row_stop - row_start, width, n, side / 2, 1, kMaxClusterRun);
+    const Plan pl = make_plan(height, row_stop - row_start, width, n, side / 2, 1);
     launch_fused(P, pl, (cudaStream_t)stream);
     PGB_CK(cudaGetLastError());
     // the side staging slot is reused: keep the host value alive until the copy ran
@@ -634,7 +623,7 @@ int pgb_render_pairs_dev(const pgb_particles* frame1, const pgb_particles* frame
     P.out[0] = out1;
     P.out[1] = out2;
     P.bin_counts = bin_counts;
-    const Plan pl = make_plan(height, height, width, n_per_pair, smax / 2, 2, kMaxClusterRun);
+    const Plan pl = make_plan(height, height, width, n_per_pair, smax / 2, 2);
     if (tiles_out) *tiles_out = pl.tiles;
     launch_fused(P, pl, (cudaStream_t)stream);
     PGB_CK(cudaGetLastError());
