@@ -35,8 +35,6 @@ namespace pgb {
 
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
-// generate-item staging (aliases the accumulator): 2 x kThreads records + 2 x 4 x kThreads (tile, rank)
-constexpr int kStageInts = 2 * kThreads * 8 + 16 * kThreads;
 constexpr int kAccShift = 22;     // max fixed-point fraction bits
 constexpr int kCellMin = 8;       // coverage-guard cell size floor
 constexpr float kLog2e = 1.4426950408889634f;
@@ -93,7 +91,8 @@ struct __align__(16) SlotHdr {
 struct FusedParams {
   int H, W, row_lo, row_hi;
   int TH, TW, tiles_y, tiles_x, tiles, th_shift, tw_shift;
-  int cap;                 // record capacity per (slot, frame, tile)
+  int cap;                 // record capacity per (slot, frame, tile, chunk) segment
+  int rbuf;                // shared-memory record buffer per frame (render)
   int halo, nframes, cells_cap;
   int pad, AH, AS;         // accumulator: AH rows x AS ints (tile + pad on each side)
   int n, pairs, chunk, chunks, ring, lookahead;
@@ -116,8 +115,8 @@ struct FusedParams {
   float* st_dmax;
   int* bin_counts;
   // workspace
-  Rec* recs;           // [ring][nframes][tiles][cap]
-  int* fills;          // [ring][nframes][tiles]
+  Rec* recs;           // [ring][nframes][tiles][chunks][cap]
+  int* fills;          // [ring][nframes][tiles][chunks] segment counts
   SlotHdr* slots;      // [ring]
   int* ticket;         // work counter (zeroed before launch)
   int* overflow;
@@ -125,11 +124,12 @@ struct FusedParams {
 
 // Per-CTA shared control block.
 struct __align__(16) SharedHdr {
-  int item;            // current ticket
-  int rcnt[2][4];      // generate round: unused (kept for layout)
+  unsigned long long bar;   // mbarrier: TMA bulk loads of a render item's records
+  int item;                 // current ticket
   unsigned dmax, amp, smax[2];
-  int shift, weff, cov_max;
+  int cov_max;
   int M;
+  int K[2];                 // records per frame of the current render item
 };
 
 // ----------------------------------------------------------------------------
@@ -415,9 +415,16 @@ __device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, 
   }
 }
 
+// Records come from shared memory (TMA-staged) or, for oversized lists, L2.
 __device__ __forceinline__ Rec load_rec(const Rec* q) {
-  const float4 a = __ldcg(reinterpret_cast<const float4*>(q));
-  const float4 b = __ldcg(reinterpret_cast<const float4*>(q) + 1);
+  float4 a, b;
+  if (__isShared(q)) {
+    a = reinterpret_cast<const float4*>(q)[0];
+    b = reinterpret_cast<const float4*>(q)[1];
+  } else {
+    a = __ldcg(reinterpret_cast<const float4*>(q));
+    b = __ldcg(reinterpret_cast<const float4*>(q) + 1);
+  }
   Rec r;
   r.axy = __float_as_int(a.x); r.fx = a.y; r.fy = a.z; r.L = a.w;
   r.A = b.x; r.B = b.y; r.C = b.z; r.aux = b.w;
@@ -669,18 +676,15 @@ __device__ __forceinline__ int pair_M(const FusedParams& P, int pl, double* ppp_
   return (int)m;
 }
 
-// GENERATE (pair pl, chunk c): counting sort of the chunk's particles into the
-// per-(frame, tile) lists of the pair's slot, in rounds of kThreads particles:
-// local ranks from shared atomics, one global atomicAdd per (frame, tile) per
-// round, then the record stores.
-// `stage` aliases the render accumulator (re-zeroed at the end).
+// GENERATE (pair pl, chunk c): counting sort of the chunk's particles into
+// its PRIVATE per-(frame, tile) segments of the pair's slot. Ranks come from
+// shared-memory atomics only: no global round trips, no barriers per round.
 template <int MODE>
-__device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int* base,
-                              int* stage, int pl, int c) {
+__device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int pl, int c) {
   const int tid = threadIdx.x;
   const int slot = pl % P.ring;
   SlotHdr* S = P.slots + slot;
-  const int T = P.tiles;
+  const int T = P.tiles, G = P.chunks;
   const int nf = P.nframes;
   if (tid == 0) {
     // the slot is free once its previous occupant (pair pl - ring) is fully rendered
@@ -697,33 +701,20 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
   for (int e = tid; e < nf * T; e += kThreads) cnt[e] = 0;
   __syncthreads();
   const int M = sh->M;
-  int* fills = P.fills + (size_t)slot * nf * T;
-  Rec* recs = P.recs + (size_t)slot * nf * T * P.cap;
+  Rec* recs = P.recs + (size_t)slot * nf * T * G * P.cap;
   const float2* flow = MODE == 0
       ? P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems : nullptr;
   const int i_lo = c * P.chunk;
   const int i_hi = min(P.n, i_lo + P.chunk);
   const int hx = P.halo;
   unsigned dmax_l = 0u, amp_l = 0u, smax_l[2] = {0u, 0u};
-  for (int b0 = i_lo; b0 < i_hi; b0 += kThreads) {
-    const int i = b0 + tid;
+  for (int i = i_lo + tid; i < i_hi; i += kThreads) {
     Particle pt;
-    if (i < i_hi) {
-      if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
-      else inject_particle(P, pl, i, pt);
-    } else {
-      pt.fr[0].on = pt.fr[1].on = false;
-      pt.active = false;
-    }
+    if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
+    else inject_particle(P, pl, i, pt);
     if (MODE == 0 && pt.active) dmax_l = max(dmax_l, __float_as_uint(pt.diam));
-    // stage records and (tile, rank) pairs in shared memory (keeps registers free)
-    Rec* st_rec = reinterpret_cast<Rec*>(stage);                   // [2][kThreads]
-    int* st_dst = reinterpret_cast<int*>(st_rec + 2 * kThreads);   // [2][4][kThreads]
-    int* st_rk = st_dst + 8 * kThreads;                            // [2][4][kThreads]
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) st_dst[(f * 4 + k) * kThreads + tid] = -1;
       if (f >= nf) continue;
       const Frame& fr = pt.fr[f];
       if (!fr.on) continue;
@@ -733,12 +724,6 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
       const int ty0 = (rlo - P.row_lo) >> P.th_shift, ty1 = (rhi - P.row_lo) >> P.th_shift;
       const int tx0 = clo >> P.tw_shift, tx1 = chi >> P.tw_shift;
       const Rec r = make_rec(fr, P.psf);
-      {
-        const float4* s4 = reinterpret_cast<const float4*>(&r);
-        float4* d4 = reinterpret_cast<float4*>(st_rec + f * kThreads + tid);
-        d4[0] = s4[0];
-        d4[1] = s4[1];
-      }
       amp_l = max(amp_l, __float_as_uint(fr.amp));
       smax_l[f] = max(smax_l[f], __float_as_uint(fmaxf(fr.sx, fr.sy)));
 #pragma unroll
@@ -748,29 +733,11 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
           const int ty = ty0 + dy, tx = tx0 + dx;
           if (ty > ty1 || tx > tx1) continue;
           const int t = ty * P.tiles_x + tx;
-          st_dst[(f * 4 + 2 * dy + dx) * kThreads + tid] = t;
-          st_rk[(f * 4 + 2 * dy + dx) * kThreads + tid] = atomicAdd(&cnt[f * T + t], 1);
+          const int k = atomicAdd(&cnt[f * T + t], 1);
+          if (k < P.cap) store_rec_global(recs + (((size_t)f * T + t) * G + c) * P.cap + k, r);
+          else atomicAdd(P.overflow, 1);
         }
     }
-    __syncthreads();
-    for (int e = tid; e < nf * T; e += kThreads) {
-      const int n = cnt[e];
-      if (n) {
-        base[e] = atomicAdd(&fills[e], n);
-        cnt[e] = 0;
-      }
-    }
-    __syncthreads();
-    for (int f = 0; f < nf; ++f)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int t = st_dst[(f * 4 + k) * kThreads + tid];
-        if (t < 0) continue;
-        const int sl = base[f * T + t] + st_rk[(f * 4 + k) * kThreads + tid];
-        if (sl < P.cap) store_rec_global(recs + ((size_t)f * T + t) * P.cap + sl, st_rec[f * kThreads + tid]);
-        else atomicAdd(P.overflow, 1);
-      }
-    __syncthreads();   // base[] is rewritten next round
   }
   for (int o = 16; o > 0; o >>= 1) {
     dmax_l = max(dmax_l, __shfl_xor_sync(~0u, dmax_l, o));
@@ -785,29 +752,96 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
     atomicMax(&sh->smax[1], smax_l[1]);
   }
   __syncthreads();
+  int* counts = P.fills + (size_t)slot * nf * T * G;
+  for (int e = tid; e < nf * T; e += kThreads) counts[(size_t)e * G + c] = min(cnt[e], P.cap);
+  __syncthreads();
   if (tid == 0) {
     if (sh->dmax) atomicMax(&S->dmax, sh->dmax);
     if (sh->amp) atomicMax(&S->amp, sh->amp);
     if (sh->smax[0]) atomicMax(&S->smax[0], sh->smax[0]);
     if (sh->smax[1]) atomicMax(&S->smax[1], sh->smax[1]);
-    __threadfence();   // records + counters before the release
+    __threadfence();   // records + counts before the release
     atomicAdd(&S->gen_done, 1);
   }
-  // restore the accumulator the staging area borrowed
-  for (int e = tid; e < kStageInts / 4; e += kThreads)
-    reinterpret_cast<int4*>(stage)[e] = make_int4(0, 0, 0, 0);
 }
 
-// RENDER (pair pl, tile t): both frames of one screen tile.
+// ----------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk) + mbarrier transaction counting
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1D bulk copy global -> shared, completion signalled on `bar` (complete_tx).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// RENDER (pair pl, tile t): both frames of one screen tile. The tile's
+// record segments (one per generate chunk) are pulled into shared memory with
+// TMA bulk copies (one elected thread, mbarrier transaction count), then
+// splatted from shared memory.
 template <int MODE, int PSF>
-__device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, int* cells, int pl,
-                            int t) {
+__device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* rbuf, int* cells,
+                            int pl, int t, uint32_t& bar_phase) {
   const int tid = threadIdx.x;
   const int slot = pl % P.ring;
   SlotHdr* S = P.slots + slot;
-  const int T = P.tiles;
+  const int T = P.tiles, G = P.chunks;
   const int nf = P.nframes;
-  if (tid == 0) spin_until_geq(&S->gen_done, P.chunks);
+  const int* counts = P.fills + (size_t)slot * nf * T * G;
+  const Rec* recs = P.recs + (size_t)slot * nf * T * G * P.cap;
+  if (tid == 0) {
+    spin_until_geq(&S->gen_done, G);
+    // records per frame, then one transaction-counted barrier for all copies
+    uint32_t bytes = 0;
+    for (int f = 0; f < nf; ++f) {
+      int K = 0;
+      for (int c = 0; c < G; ++c) K += __ldcg(&counts[((size_t)f * T + t) * G + c]);
+      sh->K[f] = K;
+      if (K <= P.rbuf) bytes += (uint32_t)K * sizeof(Rec);
+    }
+    mbar_arrive_expect_tx(&sh->bar, bytes);
+    // the buffer was last read through the generic proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int f = 0; f < nf; ++f) {
+      if (sh->K[f] > P.rbuf) continue;
+      int off = 0;
+      for (int c = 0; c < G; ++c) {
+        const int n = __ldcg(&counts[((size_t)f * T + t) * G + c]);
+        if (n) {
+          bulk_g2s(rbuf + (size_t)f * P.rbuf + off, recs + (((size_t)f * T + t) * G + c) * P.cap,
+                   (uint32_t)n * sizeof(Rec), &sh->bar);
+          off += n;
+        }
+      }
+    }
+  }
   __syncthreads();
   const int M = MODE == 0 ? __ldcg(&S->M) : 0;
   int side;
@@ -833,14 +867,14 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, int* 
   const int nc = min(P.TW, P.W - c0);
   const int h = side >> 1;
   const float amp_max = fmaxf(__uint_as_float(__ldcg(&S->amp)), 1e-30f);
-  const int* fills = P.fills + (size_t)slot * nf * T;
-  const Rec* recs = P.recs + (size_t)slot * nf * T * P.cap;
   const int acc_ints = P.AH * P.AS;
+  mbar_wait(&sh->bar, bar_phase);
+  bar_phase ^= 1u;
   for (int f = 0; f < nf; ++f) {
-    const int Kf = __ldcg(&fills[f * T + t]);
-    const int K = min(Kf, P.cap);
-    const Rec* rl = recs + ((size_t)f * T + t) * P.cap;
-    if (P.bin_counts && tid == 0) P.bin_counts[((size_t)pl * 2 + f) * T + t] = Kf;
+    const int K = sh->K[f];
+    const bool staged = K <= P.rbuf;
+    const Rec* rl = rbuf + (size_t)f * P.rbuf;
+    if (P.bin_counts && tid == 0) P.bin_counts[((size_t)pl * 2 + f) * T + t] = K;
     // -- fixed-point shift: per-pixel sum of rounded contributions < 2^31.
     //    Cheap bound from K; cell histogram only if it would cost precision
     //    (cells >= 2h+1 wide, so a pixel's anchor window lies in 2x2 cells).
@@ -852,11 +886,15 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, int* 
         if (tid == 0) sh->cov_max = 0;
         for (int e = tid; e < ncy * ncx; e += kThreads) cells[e] = 0;
         __syncthreads();
-        for (int k = tid; k < K; k += kThreads) {
-          const int axy = __ldcg(&rl[k].axy);
-          const int cy = (axy >> 16) - (r0 - h), cx = (int)(short)(axy & 0xffff) - (c0 - h);
-          if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
-            atomicAdd(&cells[(cy / Sc) * ncx + cx / Sc], 1);
+        for (int c = 0; c < G; ++c) {
+          const int n = staged ? (c == 0 ? K : 0) : __ldcg(&counts[((size_t)f * T + t) * G + c]);
+          const Rec* seg = staged ? rl : recs + (((size_t)f * T + t) * G + c) * P.cap;
+          for (int k = tid; k < n; k += kThreads) {
+            const int axy = staged ? seg[k].axy : __ldcg(&seg[k].axy);
+            const int cy = (axy >> 16) - (r0 - h), cx = (int)(short)(axy & 0xffff) - (c0 - h);
+            if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
+              atomicAdd(&cells[(cy / Sc) * ncx + cx / Sc], 1);
+          }
         }
         __syncthreads();
         int cm = 0;
@@ -881,11 +919,17 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, int* 
     if (PSF == kPsfPoint) {
       const float smax = __uint_as_float(__ldcg(&S->smax[f]));
       R = zero_radius(smax, amp_max, shift);
-      W = min(side_w, (int)floorf(2.0f * R) + 1);
-      W = max(W, 1);
+      W = max(1, min(side_w, (int)floorf(2.0f * R) + 1));
     }
-    splat_dispatch<PSF>(acc, rl, K, W, h, R, r0 - P.pad, c0 - P.pad, P.AS, (float)shift,
-                        exp2f((float)shift));
+    if (staged) {
+      splat_dispatch<PSF>(acc, rl, K, W, h, R, r0 - P.pad, c0 - P.pad, P.AS, (float)shift,
+                          exp2f((float)shift));
+    } else {
+      for (int c = 0; c < G; ++c)
+        splat_dispatch<PSF>(acc, recs + (((size_t)f * T + t) * G + c) * P.cap,
+                            __ldcg(&counts[((size_t)f * T + t) * G + c]), W, h, R, r0 - P.pad,
+                            c0 - P.pad, P.AS, (float)shift, exp2f((float)shift));
+    }
     __syncthreads();
     store_tile(P, acc, pl, f, r0, nr, c0, nc, exp2f(-(float)shift));
     __syncthreads();
@@ -897,8 +941,6 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, int* 
     __threadfence();
     if (atomicAdd(&S->render_done, 1) == T - 1) {
       // last renderer retires the slot: reset it, then publish the new epoch
-      int* fl = P.fills + (size_t)slot * nf * T;
-      for (int e = 0; e < nf * T; ++e) fl[e] = 0;
       S->gen_done = 0;
       S->render_done = 0;
       S->dmax = S->amp = S->smax[0] = S->smax[1] = 0u;
@@ -917,13 +959,15 @@ __global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const Fused
   extern __shared__ __align__(16) unsigned char smem[];
   int* acc = reinterpret_cast<int*>(smem);
   const int acc_ints = P.AH * P.AS;
-  SharedHdr* sh = reinterpret_cast<SharedHdr*>(acc + max(acc_ints, kStageInts));
-  int* cnt = reinterpret_cast<int*>(sh + 1);               // [nframes * tiles]
-  int* base = cnt + P.nframes * P.tiles;                   // [nframes * tiles]
-  int* cells = base + P.nframes * P.tiles;                 // [cells_cap]
+  Rec* rbuf = reinterpret_cast<Rec*>(acc + acc_ints);                 // [nframes][rbuf]
+  SharedHdr* sh = reinterpret_cast<SharedHdr*>(rbuf + (size_t)P.nframes * P.rbuf);
+  int* cnt = reinterpret_cast<int*>(sh + 1);                          // [nframes * tiles]
+  int* cells = cnt + P.nframes * P.tiles;                             // [cells_cap]
   const int tid = threadIdx.x;
-  for (int e = tid; e < max(acc_ints, kStageInts) >> 2; e += kThreads)
+  for (int e = tid; e < acc_ints >> 2; e += kThreads)
     reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
+  if (tid == 0) mbar_init(&sh->bar, 1);
+  uint32_t bar_phase = 0;
   const int T = P.tiles, G = P.chunks, L = P.lookahead, NP = P.pairs;
   const long long pre = (long long)min(L, NP) * G;
   const long long total = pre + (long long)NP * (T + G);
@@ -934,15 +978,15 @@ __global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const Fused
     const long long tk = sh->item;
     if (tk >= total) break;
     if (tk < pre) {
-      generate_item<MODE>(P, sh, cnt, base, acc, (int)(tk / G), (int)(tk % G));
+      generate_item<MODE>(P, sh, cnt, (int)(tk / G), (int)(tk % G));
     } else {
       const long long u = tk - pre;
       const int p = (int)(u / (T + G));
       const int r = (int)(u - (long long)p * (T + G));
       if (r < T) {
-        render_item<MODE, PSF>(P, sh, acc, cells, p, r);
+        render_item<MODE, PSF>(P, sh, acc, rbuf, cells, p, r, bar_phase);
       } else if (p + L < NP) {
-        generate_item<MODE>(P, sh, cnt, base, acc, p + L, r - T);
+        generate_item<MODE>(P, sh, cnt, p + L, r - T);
       }
     }
   }

@@ -195,11 +195,11 @@ struct Error {
 struct Plan {
   int TH, TW, tiles_y, tiles_x, tiles, cap, halo, cells_cap;
   int th_shift, tw_shift, pad, AH, AS;
-  int chunk, chunks;
+  int chunk, chunks, rbuf;
   size_t smem;
 };
 
-constexpr size_t kSmemTarget = 44 * 1024;   // four-five 128-thread CTAs per SM
+constexpr size_t kSmemTarget = 54 * 1024;   // four 128-thread CTAs per SM
 constexpr size_t kSmemMax = 220 * 1024;
 
 int ilog2(int v) {
@@ -220,15 +220,33 @@ int pow2_ceil(int v) {
 Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes) {
   Plan p{};
   p.halo = halo;
+  // generate items: >= 4 particles per thread, at most ~16 chunks (segments) per pair
+  const long long per16 = (n + 15) / 16;
+  p.chunk = (int)std::max<long long>(4 * kThreads, (per16 + kThreads - 1) / kThreads * kThreads);
+  p.chunks = (int)std::max<long long>(1, (n + p.chunk - 1) / p.chunk);
   p.TW = std::min(256, std::max(4, pow2_ceil(W)));
   p.TH = std::max(1, std::min(pow2_ceil(rows), 8192 / p.TW));
   p.TH = 1 << ilog2(p.TH);
   const int tmin = pow2_ceil(2 * halo + 1);
   p.pad = (2 * halo + 3) / 4 * 4;
+  double lam = 0.0;
   for (;;) {
     p.AH = p.TH + 2 * p.pad;
     p.AS = p.TW + 2 * p.pad;
-    p.smem = (size_t)p.AH * p.AS * 4;
+    const double ext = (double)std::min(p.TH + 2 * halo, rows + 2 * halo) *
+                       (double)std::min(p.TW + 2 * halo, W + 2 * halo);
+    lam = std::min((double)n, (double)n * ext / ((double)H_full * (double)W));
+    // shared record buffer per frame: lambda + 4 sigma (bigger lists fall back to L2)
+    p.rbuf = (int)std::min<long long>(std::max<long long>(n, 8),
+                                      (long long)std::ceil(lam + 4.0 * std::sqrt(lam) + 16.0));
+    p.rbuf = (p.rbuf + 7) / 8 * 8;
+    p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
+                  ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
+    p.tiles_y = (rows + p.TH - 1) / p.TH;
+    p.tiles_x = (W + p.TW - 1) / p.TW;
+    p.tiles = p.tiles_y * p.tiles_x;
+    p.smem = (size_t)p.AH * p.AS * 4 + (size_t)nframes * p.rbuf * sizeof(Rec) + sizeof(SharedHdr) +
+             (size_t)(nframes * p.tiles + p.cells_cap) * 4;
     if (p.smem <= kSmemTarget) break;
     if (p.TH > std::max(1, std::min(tmin, pow2_ceil(rows)))) p.TH >>= 1;
     else if (p.TW > std::max(4, std::min(tmin, pow2_ceil(W)))) p.TW >>= 1;
@@ -236,23 +254,11 @@ Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes) 
   }
   p.th_shift = ilog2(p.TH);
   p.tw_shift = ilog2(p.TW);
-  p.tiles_y = (rows + p.TH - 1) / p.TH;
-  p.tiles_x = (W + p.TW - 1) / p.TW;
-  p.tiles = p.tiles_y * p.tiles_x;
-  // record capacity per (slot, frame, tile): generous (global memory), so
-  // only pathological flows (strong convergence) can overflow
-  const double ext = (double)std::min(p.TH + 2 * halo, rows + 2 * halo) *
-                     (double)std::min(p.TW + 2 * halo, W + 2 * halo);
-  const double lam = std::min((double)n, (double)n * ext / ((double)H_full * (double)W));
-  long long cap = (long long)std::ceil(2.0 * lam + 10.0 * std::sqrt(lam) + 64.0);
-  cap = std::min<long long>(cap, std::max<long long>(n, 1));
+  // private segment capacity per (frame, tile, chunk): generous (global memory)
+  const double lc = lam * (double)std::min<long long>(p.chunk, n) / (double)std::max<long long>(n, 1);
+  long long cap = (long long)std::ceil(2.0 * lc + 10.0 * std::sqrt(lc) + 32.0);
+  cap = std::min<long long>(cap, std::max<long long>(std::min<long long>(p.chunk, n), 1));
   p.cap = (int)((cap + 7) / 8 * 8);
-  p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
-                ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
-  p.chunk = 4 * kThreads;
-  p.chunks = (int)std::max<long long>(1, (n + p.chunk - 1) / p.chunk);
-  p.smem = std::max(p.smem, (size_t)kStageInts * 4);   // generate staging aliases the accumulator
-  p.smem += sizeof(SharedHdr) + (size_t)(2 * nframes * p.tiles + p.cells_cap) * 4;
   PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
   return p;
 }
@@ -320,21 +326,24 @@ void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
   P.TH = pl.TH; P.TW = pl.TW; P.tiles_y = pl.tiles_y; P.tiles_x = pl.tiles_x; P.tiles = pl.tiles;
   P.th_shift = pl.th_shift; P.tw_shift = pl.tw_shift; P.cap = pl.cap; P.halo = pl.halo;
   P.cells_cap = pl.cells_cap; P.pad = pl.pad; P.AH = pl.AH; P.AS = pl.AS;
-  P.chunk = pl.chunk; P.chunks = pl.chunks;
+  P.chunk = pl.chunk; P.chunks = pl.chunks; P.rbuf = pl.rbuf;
   if (P.pairs <= 0) return;
   const int ctas = resident_ctas(fn, pl.smem);
   const long long items_per_pair = (long long)pl.tiles + pl.chunks;
   // generation runs `lookahead` pairs ahead of rendering; the ring holds the
   // pairs in flight (> lookahead, so every wait targets an earlier ticket)
-  int L = (int)std::ceil(1.5 * ctas / (double)items_per_pair);
+  double la = 3.0;
+  if (const char* e = std::getenv("PGB_LOOKAHEAD")) la = std::atof(e);
+  int L = (int)std::ceil(la * ctas / (double)items_per_pair);
   L = std::max(1, std::min(L, P.pairs));
   const int ring = std::min(P.pairs, L + std::max(4, L / 4));
   P.lookahead = L;
   P.ring = std::max(ring, std::min(P.pairs, L + 1));
   DevWork& w = work_for_current();
-  const size_t recs_bytes = (size_t)P.ring * P.nframes * pl.tiles * pl.cap * sizeof(Rec);
+  const size_t segs = (size_t)P.ring * P.nframes * pl.tiles * pl.chunks;
+  const size_t recs_bytes = segs * pl.cap * sizeof(Rec);
   const size_t slots_bytes = (size_t)P.ring * sizeof(SlotHdr);
-  const size_t fills_bytes = (size_t)P.ring * P.nframes * pl.tiles * sizeof(int);
+  const size_t fills_bytes = segs * sizeof(int);
   const size_t ctl_bytes = 256 + slots_bytes + fills_bytes;
   P.recs = static_cast<Rec*>(ensure(w.ring, w.ring_bytes, recs_bytes));
   char* ctl = static_cast<char*>(ensure(w.ctl, w.ctl_bytes, ctl_bytes));
