@@ -139,25 +139,54 @@ def quantize_u16(img: np.ndarray) -> np.ndarray:
     return np.rint(x * np.float32(65535.0)).astype(np.uint16)
 
 
-def tile_counts(pos, on, halo, tile_h, tile_w, height, width, row_lo=0, row_hi=None) -> np.ndarray:
-    """Number of contributing particles whose (2*halo+1)^2 window touches each
-    tile (row-major tiles over rows [row_lo, row_hi) x [0, width))."""
+K_TIGHT_R = np.float32(5.6508017)   # sqrt(2 ln(2^22 / 0.49)) * 1.0001, as csrc/fused.cuh kTightR
+
+
+def tight_window(fx, fy, sx, sy, halo, erf=False):
+    """Per-record tight window of the B200 kernel (anchor offsets jlo..jhi,
+    ilo..ihi): pixels outside it contribute an integer 0 at the maximum
+    fixed-point shift (amp <= 1). Float32 ops mirror csrc/fused.cuh exactly."""
+    fx = np.asarray(fx, np.float32)
+    fy = np.asarray(fy, np.float32)
+    R = (np.maximum(np.asarray(sx, np.float32), np.asarray(sy, np.float32)) * K_TIGHT_R).astype(np.float32)
+    if erf:
+        R = (R + np.float32(0.5)).astype(np.float32)
+    jlo = np.maximum(-halo, np.ceil((fx - R).astype(np.float32)).astype(np.int64))
+    jhi = np.minimum(halo, np.floor((fx + R).astype(np.float32)).astype(np.int64))
+    ilo = np.maximum(-halo, np.ceil((fy - R).astype(np.float32)).astype(np.int64))
+    ihi = np.minimum(halo, np.floor((fy + R).astype(np.float32)).astype(np.int64))
+    return jlo, jhi, ilo, ihi
+
+
+def anchors_f64(pos):
+    """Anchor floor(x + 1/2) and float32 fraction of float64 positions (oracle mode)."""
+    ax = np.floor(pos[:, 0] + 0.5)
+    ay = np.floor(pos[:, 1] + 0.5)
+    return ax.astype(np.int64), ay.astype(np.int64), (pos[:, 0] - ax).astype(np.float32), \
+        (pos[:, 1] - ay).astype(np.float32)
+
+
+def tile_counts(pos, on, sx, sy, halo, tile_h, tile_w, height, width, row_lo=0, row_hi=None,
+                erf=False) -> np.ndarray:
+    """Records per tile of the fused kernel's counting sort: each contributing
+    particle goes to every tile its tight window (clipped to the image) touches."""
     row_hi = height if row_hi is None else row_hi
     rows = row_hi - row_lo
     tiles_y = -(-rows // tile_h)
     tiles_x = -(-width // tile_w)
     counts = np.zeros(tiles_y * tiles_x, dtype=np.int64)
     sel = np.flatnonzero(np.asarray(on) != 0)
-    ax = np.floor(pos[sel, 0] + 0.5)
-    ay = np.floor(pos[sel, 1] + 0.5)
-    ok = (ax >= -halo) & (ax <= width - 1 + halo) & (ay >= row_lo - halo) & (ay <= row_hi - 1 + halo)
-    ax = ax[ok].astype(np.int64)
-    ay = ay[ok].astype(np.int64)
-    rlo = np.maximum(ay - halo, row_lo) - row_lo
-    rhi = np.minimum(ay + halo, row_hi - 1) - row_lo
-    clo = np.maximum(ax - halo, 0)
-    chi = np.minimum(ax + halo, width - 1)
-    for ty0, ty1, tx0, tx1 in zip(rlo // tile_h, rhi // tile_h, clo // tile_w, chi // tile_w):
-        for ty in range(ty0, ty1 + 1):
-            counts[ty * tiles_x + tx0: ty * tiles_x + tx1 + 1] += 1
+    if sel.size == 0:
+        return counts
+    ax, ay, fx, fy = anchors_f64(pos[sel])
+    jlo, jhi, ilo, ihi = tight_window(fx, fy, np.asarray(sx)[sel], np.asarray(sy)[sel], halo, erf)
+    rlo = np.maximum(ay + ilo, row_lo)
+    rhi = np.minimum(ay + ihi, row_hi - 1)
+    clo = np.maximum(ax + jlo, 0)
+    chi = np.minimum(ax + jhi, width - 1)
+    ok = (jlo <= jhi) & (ilo <= ihi) & (rlo <= rhi) & (clo <= chi)
+    for r_lo, r_hi, c_lo, c_hi in zip((rlo - row_lo)[ok] // tile_h, (rhi - row_lo)[ok] // tile_h,
+                                      clo[ok] // tile_w, chi[ok] // tile_w):
+        for ty in range(r_lo, r_hi + 1):
+            counts[ty * tiles_x + c_lo: ty * tiles_x + c_hi + 1] += 1
     return counts

@@ -42,15 +42,20 @@ constexpr float kLog2e = 1.4426950408889634f;
 enum OutMode { kOutRaw = 0, kOutF32 = 1, kOutU16 = 2, kOutAccum = 3 };
 enum Psf { kPsfPoint = 0, kPsfErf = 1 };
 
-// 32-byte render-ready particle record exchanged between CTAs.
-//   point PSF:  value * 2^s = exp2(L + s - (A dx^2 + B dx dy + C dy^2))
-//   erf PSF:    L = amp', A = 1/(sc sqrt2), B = 1/(sy sqrt2), C = slope, aux = separable
+// 32-byte render-ready particle record, addressed for its owning tile.
+//   point PSF:  value * 2^s = exp2(L + s - (A dx^2 + B dx dy + C dy^2)), with
+//               dx = dx0 + j, dy = dy0 + i for window lane column j / row i
+//   erf PSF:    L = amp', A = 1/(sc sqrt2), B = 1/(sy sqrt2), C = slope (0: separable)
+// The window (Wr x Hr pixels starting at anchor offset (jlo, ilo)) is the
+// record's TIGHT window: every pixel outside it would contribute an integer 0
+// at the maximum fixed-point shift, so skipping it cannot change a bit.
 struct __align__(16) Rec {
-  int axy;      // anchor: ax in low 16 bits, ay in high 16 bits (both signed)
-  float fx, fy; // sub-pixel offset from the anchor: x - ax, y - ay
+  int addr;      // accumulator offset (ints) of the window's first pixel in the owning tile
+  float dx0;     // jlo - fx
+  float dy0;     // ilo - fy
   float L;
   float A, B, C;
-  float aux;
+  int meta;      // jlo (int8) | ilo (int8) << 8 | Wr << 16 | Hr << 24
 };
 
 struct GenCfg {
@@ -66,6 +71,10 @@ struct GenCfg {
   int laser;
   int need_b, need_perturb;
 };
+
+// Tight-window radius factor: R = sigma * kR, kR = sqrt(2 ln(2^22 / 0.49)) * 1.0001
+// (records with amp <= 1; larger amplitudes widen R by ln(amp), see record_radius).
+constexpr float kTightR = 5.6508017f;
 
 struct InjFrame {
   const double* pos;
@@ -84,7 +93,7 @@ struct __align__(16) SlotHdr {
   int M;               // active count
   unsigned dmax;       // max active diameter (float bits)
   unsigned amp;        // max record amplitude (float bits)
-  unsigned smax[2];    // per frame max(sigma_x, sigma_y) (float bits)
+  int wmax[2];         // per frame max record window width (columns or rows)
   double ppp;          // realised seeding density
 };
 
@@ -126,8 +135,9 @@ struct FusedParams {
 struct __align__(16) SharedHdr {
   unsigned long long bar;   // mbarrier: TMA bulk loads of a render item's records
   int item;                 // current ticket
-  unsigned dmax, amp, smax[2];
-  int cov_max;
+  unsigned dmax, amp;
+  int wmax[2];
+  int cov_max, shift;
   int M;
   int K[2];                 // records per frame of the current render item
 };
@@ -308,11 +318,23 @@ __device__ __forceinline__ void inject_particle(const FusedParams& P, int pl, in
   pt.active = false;
 }
 
-__device__ __forceinline__ Rec make_rec(const Frame& fr, int psf) {
+// Tight-window radius of a record (pixels); exact-reproducible for amp <= 1
+// (one float32 multiply); larger amplitudes add ln(amp) to the exponent budget.
+__device__ __forceinline__ float record_radius(const Frame& fr, int psf) {
+  const float sm = fmaxf(fr.sx, fr.sy);
+  float R = __fmul_rn(sm, kTightR);
+  if (fr.amp > 1.0f) R = sm * sqrtf(2.0f * (15.962588f + logf(fr.amp))) * 1.0001f;
+  if (psf != kPsfPoint) R += 0.5f;     // pixel-area mean: nearest point of the pixel
+  return R;
+}
+
+// Coefficients + window of a record; addr is filled in per destination tile.
+__device__ __forceinline__ Rec make_rec(const Frame& fr, int psf, int jlo, int ilo, int Wr, int Hr) {
   Rec r;
-  r.axy = (fr.ay << 16) | (fr.ax & 0xffff);
-  r.fx = fr.fx;
-  r.fy = fr.fy;
+  r.addr = 0;
+  r.dx0 = (float)jlo - fr.fx;
+  r.dy0 = (float)ilo - fr.fy;
+  r.meta = (jlo & 0xff) | ((ilo & 0xff) << 8) | (Wr << 16) | (Hr << 24);
   const float sx = fr.sx, sy = fr.sy, rho = fr.rho;
   if (psf == kPsfPoint) {
     const float q = 1.0f - rho * rho;
@@ -321,7 +343,6 @@ __device__ __forceinline__ Rec make_rec(const Frame& fr, int psf) {
     r.C = (0.5f * kLog2e) * iq * isy * isy;
     r.B = -kLog2e * rho * iq * isx * isy;
     r.L = __log2f(fr.amp);
-    r.aux = fr.amp;
   } else {
     const float k = 1.2533141373155001f;  // sqrt(pi/2)
     const float sc = sx * sqrtf(fmaxf(1.0f - rho * rho, 0.f));
@@ -329,14 +350,13 @@ __device__ __forceinline__ Rec make_rec(const Frame& fr, int psf) {
     r.L = sep ? fr.amp * (k * sx) * (k * sy) : fr.amp * (k * sc);
     r.A = 0.70710678118654752f / sc;
     r.B = 0.70710678118654752f / sy;
-    r.C = rho * sx / sy;
-    r.aux = sep ? 1.f : 0.f;
+    r.C = sep ? 0.f : rho * sx / sy;
   }
   return r;
 }
 
 // ----------------------------------------------------------------------------
-// Render: lanes = (candidate slot, patch column); each lane walks W rows.
+// Render: lanes = (record slot, window column); each lane walks the rows.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -354,45 +374,40 @@ constexpr int kGLPoints = 8;
 __constant__ float kGLx[kGLPoints] = {-0.48014492824876809f, -0.39833323870681336f, -0.2627662049581645f, -0.09171732124782489f, 0.091717321247824893f, 0.2627662049581645f, 0.39833323870681336f, 0.48014492824876809f};
 __constant__ float kGLw[kGLPoints] = {0.050614268145188532f, 0.11119051722668721f, 0.15685332293894344f, 0.18134189168918083f, 0.18134189168918083f, 0.15685332293894344f, 0.11119051722668721f, 0.050614268145188532f};
 
-// Tight window: the patch columns/rows a record can reach with a non-zero
-// fixed-point contribution. Column offsets j (relative to the anchor) with
-// |j - fx| > R give amp 2^s exp(-(j-fx)^2 / (2 sigma_x^2)) < 1/2 -> 0, because
-// min over dy of the quadratic form is dx^2 / (2 sigma_x^2). The window of W
-// offsets starts at clamp(ceil(fx - R), -h, h - W + 1) and so stays inside the
-// reference patch [-h, h] while covering every non-zero offset.
-__device__ __forceinline__ int window_start(float f, float R, int h, int W) {
-  const int lo = (int)ceilf(f - R);
-  return min(max(lo, -h), h - W + 1);
-}
-
+// One lane: column j of the record's window, rows 0..Hr-1; columns/rows beyond
+// the pair's patch half-width h are the reference's truncation (_native.pyx:34-49).
 template <int WC, int PSF>
 __device__ __forceinline__ void splat_lane(int* __restrict__ acc, const Rec& r, int Wrt, int j,
-                                           int h, float R, int r0p, int c0p, int AS,
-                                           float s_log2, float scale) {
+                                           int h, int AS, float s_log2, float scale) {
   const int W = WC > 0 ? WC : Wrt;
-  const int ay = r.axy >> 16;
-  const int ax = (int)(short)(r.axy & 0xffff);
-  const int jo = window_start(r.fx, R, h, W) + j;      // this lane's column offset
-  const int io = window_start(r.fy, R, h, W);          // first row offset
-  int* p = acc + (ay + io - r0p) * AS + (ax + jo - c0p);
-  const float dx = (float)jo - r.fx;
+  const int jlo = (int)(signed char)(r.meta & 0xff);
+  const int ilo = (int)(signed char)((r.meta >> 8) & 0xff);
+  const int Wr = (r.meta >> 16) & 0xff;
+  const int Hr = (r.meta >> 24) & 0xff;
+  const int jo = jlo + j;
+  if (j >= Wr || jo < -h || jo > h) return;
+  const int ib = max(0, -h - ilo);
+  const int ie = min(Hr, h - ilo + 1);
+  int* p = acc + r.addr + j;
+  const float dx = r.dx0 + (float)j;
   if (PSF == kPsfPoint) {
     const float Lx = fmaf(-r.A * dx, dx, r.L + s_log2);
     const float Bdx = r.B * dx;
 #pragma unroll 5
     for (int i = 0; i < (WC > 0 ? WC : 64); ++i) {
       if (WC == 0 && i >= W) break;
-      const float dy = (float)(io + i) - r.fy;
+      if (i < ib || i >= ie) continue;
+      const float dy = r.dy0 + (float)i;
       const float t = fmaf(r.C, dy, Bdx);
       const float e = fmaf(-t, dy, Lx);
       atomicAdd(p + i * AS, round_small(ex2_approx(e)));
     }
   } else {
-    const bool sep = r.aux != 0.f;
+    const bool sep = r.C == 0.f;
     float ex = 0.f;
     if (sep) ex = erff((dx + 0.5f) * r.A) - erff((dx - 0.5f) * r.A);
-    for (int i = 0; i < W; ++i) {
-      const float dy = (float)(io + i) - r.fy;
+    for (int i = ib; i < ie; ++i) {
+      const float dy = r.dy0 + (float)i;
       float val;
       if (sep) {
         val = ex * (erff((dy + 0.5f) * r.B) - erff((dy - 0.5f) * r.B));
@@ -426,38 +441,38 @@ __device__ __forceinline__ Rec load_rec(const Rec* q) {
     b = __ldcg(reinterpret_cast<const float4*>(q) + 1);
   }
   Rec r;
-  r.axy = __float_as_int(a.x); r.fx = a.y; r.fy = a.z; r.L = a.w;
-  r.A = b.x; r.B = b.y; r.C = b.z; r.aux = b.w;
+  r.addr = __float_as_int(a.x); r.dx0 = a.y; r.dy0 = a.z; r.L = a.w;
+  r.A = b.x; r.B = b.y; r.C = b.z; r.meta = __float_as_int(b.w);
   return r;
 }
 
 template <int WC, int PSF>
 __device__ void splat_tile(int* __restrict__ acc, const Rec* __restrict__ recs, int K, int Wrt,
-                           int h, float R, int r0p, int c0p, int AS, float s_log2, float scale) {
+                           int h, int AS, float s_log2, float scale) {
   const int W = WC > 0 ? WC : Wrt;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   if (W <= 32) {
-    const int cpw = 32 / W;                         // candidates per warp-step
+    const int cpw = 32 / W;                         // records per warp-step
     const int slot = lane / W;
     const int j = lane - slot * W;
     if (slot >= cpw) return;
     for (int k = warp * cpw + slot; k < K; k += kWarps * cpw)
-      splat_lane<WC, PSF>(acc, load_rec(recs + k), W, j, h, R, r0p, c0p, AS, s_log2, scale);
+      splat_lane<WC, PSF>(acc, load_rec(recs + k), W, j, h, AS, s_log2, scale);
   } else {
-    // very large patches: the warp walks one candidate, lanes stride the columns
+    // very large windows: the warp walks one record, lanes stride the columns
     for (int k = warp; k < K; k += kWarps) {
       const Rec r = load_rec(recs + k);
       for (int jj = lane; jj < W; jj += 32)
-        splat_lane<0, PSF>(acc, r, W, jj, h, R, r0p, c0p, AS, s_log2, scale);
+        splat_lane<0, PSF>(acc, r, W, jj, h, AS, s_log2, scale);
     }
   }
 }
 
 template <int PSF>
-__device__ void splat_dispatch(int* acc, const Rec* recs, int K, int W, int h, float R, int r0p,
-                               int c0p, int AS, float s_log2, float scale) {
-#define PGB_SPLAT(WW) splat_tile<WW, PSF>(acc, recs, K, W, h, R, r0p, c0p, AS, s_log2, scale)
+__device__ void splat_dispatch(int* acc, const Rec* recs, int K, int W, int h, int AS,
+                               float s_log2, float scale) {
+#define PGB_SPLAT(WW) splat_tile<WW, PSF>(acc, recs, K, W, h, AS, s_log2, scale)
   if (PSF == kPsfPoint) {
     switch (W) {
       case 2: PGB_SPLAT(2); return;
@@ -483,13 +498,6 @@ __device__ __forceinline__ int shift_for(int cnt, float amp_max) {
   if (!(per >= 1.0)) return 0;
   int e = ilogb(per);                      // floor(log2(per)), exact
   return e < kAccShift ? e : kAccShift;
-}
-
-// Conservative zero radius (pixels) for records with sigma <= smax, amp <= amp_max.
-__device__ __forceinline__ float zero_radius(float smax, float amp_max, int shift) {
-  const double lnv = log((double)amp_max * ldexp(1.0, shift) / 0.49);
-  if (!(lnv > 0.0)) return 0.f;
-  return (float)((double)smax * sqrt(2.0 * lnv) * 1.0001 + 1e-4);
 }
 
 // ----------------------------------------------------------------------------
@@ -692,7 +700,8 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
     double ppp = 0.0;
     const int M = MODE == 0 ? pair_M(P, pl, &ppp) : 0;
     sh->M = M;
-    sh->dmax = sh->amp = sh->smax[0] = sh->smax[1] = 0u;
+    sh->dmax = sh->amp = 0u;
+    sh->wmax[0] = sh->wmax[1] = 0;
     if (c == 0) {
       S->M = M;
       S->ppp = ppp;
@@ -707,7 +716,8 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
   const int i_lo = c * P.chunk;
   const int i_hi = min(P.n, i_lo + P.chunk);
   const int hx = P.halo;
-  unsigned dmax_l = 0u, amp_l = 0u, smax_l[2] = {0u, 0u};
+  unsigned dmax_l = 0u, amp_l = 0u;
+  int wmax_l[2] = {0, 0};
   for (int i = i_lo + tid; i < i_hi; i += kThreads) {
     Particle pt;
     if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
@@ -718,14 +728,21 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
       if (f >= nf) continue;
       const Frame& fr = pt.fr[f];
       if (!fr.on) continue;
-      const int rlo = max(fr.ay - hx, P.row_lo), rhi = min(fr.ay + hx, P.row_hi - 1);
-      const int clo = max(fr.ax - hx, 0), chi = min(fr.ax + hx, P.W - 1);
+      // tight window (anchor offsets), clipped to the config half-width hx
+      const float R = record_radius(fr, P.psf);
+      const int jlo = max(-hx, (int)ceilf(__fsub_rn(fr.fx, R)));
+      const int jhi = min(hx, (int)floorf(__fadd_rn(fr.fx, R)));
+      const int ilo = max(-hx, (int)ceilf(__fsub_rn(fr.fy, R)));
+      const int ihi = min(hx, (int)floorf(__fadd_rn(fr.fy, R)));
+      if (jlo > jhi || ilo > ihi) continue;
+      const int rlo = max(fr.ay + ilo, P.row_lo), rhi = min(fr.ay + ihi, P.row_hi - 1);
+      const int clo = max(fr.ax + jlo, 0), chi = min(fr.ax + jhi, P.W - 1);
       if (rlo > rhi || clo > chi) continue;
       const int ty0 = (rlo - P.row_lo) >> P.th_shift, ty1 = (rhi - P.row_lo) >> P.th_shift;
       const int tx0 = clo >> P.tw_shift, tx1 = chi >> P.tw_shift;
-      const Rec r = make_rec(fr, P.psf);
+      Rec r = make_rec(fr, P.psf, jlo, ilo, jhi - jlo + 1, ihi - ilo + 1);
       amp_l = max(amp_l, __float_as_uint(fr.amp));
-      smax_l[f] = max(smax_l[f], __float_as_uint(fmaxf(fr.sx, fr.sy)));
+      wmax_l[f] = max(wmax_l[f], max(jhi - jlo, ihi - ilo) + 1);
 #pragma unroll
       for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
@@ -734,6 +751,9 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
           if (ty > ty1 || tx > tx1) continue;
           const int t = ty * P.tiles_x + tx;
           const int k = atomicAdd(&cnt[f * T + t], 1);
+          // accumulator offset of the window's first pixel in tile (ty, tx)
+          r.addr = (fr.ay + ilo - (P.row_lo + ty * P.TH - P.pad)) * P.AS +
+                   (fr.ax + jlo - (tx * P.TW - P.pad));
           if (k < P.cap) store_rec_global(recs + (((size_t)f * T + t) * G + c) * P.cap + k, r);
           else atomicAdd(P.overflow, 1);
         }
@@ -742,14 +762,14 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
   for (int o = 16; o > 0; o >>= 1) {
     dmax_l = max(dmax_l, __shfl_xor_sync(~0u, dmax_l, o));
     amp_l = max(amp_l, __shfl_xor_sync(~0u, amp_l, o));
-    smax_l[0] = max(smax_l[0], __shfl_xor_sync(~0u, smax_l[0], o));
-    smax_l[1] = max(smax_l[1], __shfl_xor_sync(~0u, smax_l[1], o));
+    wmax_l[0] = max(wmax_l[0], __shfl_xor_sync(~0u, wmax_l[0], o));
+    wmax_l[1] = max(wmax_l[1], __shfl_xor_sync(~0u, wmax_l[1], o));
   }
   if ((tid & 31) == 0) {
     atomicMax(&sh->dmax, dmax_l);
     atomicMax(&sh->amp, amp_l);
-    atomicMax(&sh->smax[0], smax_l[0]);
-    atomicMax(&sh->smax[1], smax_l[1]);
+    atomicMax(&sh->wmax[0], wmax_l[0]);
+    atomicMax(&sh->wmax[1], wmax_l[1]);
   }
   __syncthreads();
   int* counts = P.fills + (size_t)slot * nf * T * G;
@@ -758,8 +778,8 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
   if (tid == 0) {
     if (sh->dmax) atomicMax(&S->dmax, sh->dmax);
     if (sh->amp) atomicMax(&S->amp, sh->amp);
-    if (sh->smax[0]) atomicMax(&S->smax[0], sh->smax[0]);
-    if (sh->smax[1]) atomicMax(&S->smax[1], sh->smax[1]);
+    if (sh->wmax[0]) atomicMax(&S->wmax[0], sh->wmax[0]);
+    if (sh->wmax[1]) atomicMax(&S->wmax[1], sh->wmax[1]);
     __threadfence();   // records + counts before the release
     atomicAdd(&S->gen_done, 1);
   }
@@ -878,10 +898,14 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* 
     // -- fixed-point shift: per-pixel sum of rounded contributions < 2^31.
     //    Cheap bound from K; cell histogram only if it would cost precision
     //    (cells >= 2h+1 wide, so a pixel's anchor window lies in 2x2 cells).
-    int shift = shift_for(max(K, 1), amp_max);
+    if (tid == 0) sh->shift = shift_for(max(K, 1), amp_max);
+    __syncthreads();
+    int shift = sh->shift;
     if (shift < kAccShift - 1) {
-      const int Sc = max(2 * h + 1, kCellMin);
-      const int ncy = (nr + 2 * h + Sc - 1) / Sc, ncx = (nc + 2 * h + Sc - 1) / Sc;
+      // cells >= 2*hx+1 over the accumulator: a pixel's contributing window
+      // starts lie in a 2x2 block of cells
+      const int Sc = max(2 * P.halo + 1, kCellMin);
+      const int ncy = (P.AH + Sc - 1) / Sc, ncx = (P.AS + Sc - 1) / Sc;
       if (ncy * ncx <= P.cells_cap) {
         if (tid == 0) sh->cov_max = 0;
         for (int e = tid; e < ncy * ncx; e += kThreads) cells[e] = 0;
@@ -890,10 +914,9 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* 
           const int n = staged ? (c == 0 ? K : 0) : __ldcg(&counts[((size_t)f * T + t) * G + c]);
           const Rec* seg = staged ? rl : recs + (((size_t)f * T + t) * G + c) * P.cap;
           for (int k = tid; k < n; k += kThreads) {
-            const int axy = staged ? seg[k].axy : __ldcg(&seg[k].axy);
-            const int cy = (axy >> 16) - (r0 - h), cx = (int)(short)(axy & 0xffff) - (c0 - h);
-            if (cy >= 0 && cy < nr + 2 * h && cx >= 0 && cx < nc + 2 * h)
-              atomicAdd(&cells[(cy / Sc) * ncx + cx / Sc], 1);
+            const int addr = staged ? seg[k].addr : __ldcg(&seg[k].addr);
+            const int wr = addr / P.AS, wc = addr - (addr / P.AS) * P.AS;
+            atomicAdd(&cells[(wr / Sc) * ncx + wc / Sc], 1);
           }
         }
         __syncthreads();
@@ -909,26 +932,20 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* 
         for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
         if ((tid & 31) == 0) atomicMax(&sh->cov_max, cm);
         __syncthreads();
-        shift = shift_for(max(sh->cov_max, 1), amp_max);
+        if (tid == 0) sh->shift = shift_for(max(sh->cov_max, 1), amp_max);
+        __syncthreads();
+        shift = sh->shift;
       }
     }
-    // -- tight window (exact: skipped pixels would round to 0)
-    const int side_w = 2 * h + 1;
-    int W = side_w;
-    float R = (float)(h + 1);
-    if (PSF == kPsfPoint) {
-      const float smax = __uint_as_float(__ldcg(&S->smax[f]));
-      R = zero_radius(smax, amp_max, shift);
-      W = max(1, min(side_w, (int)floorf(2.0f * R) + 1));
-    }
+    // lanes per record = widest tight window of the frame (exact skipping)
+    const int W = max(1, min(2 * h + 1, __ldcg(&S->wmax[f])));
     if (staged) {
-      splat_dispatch<PSF>(acc, rl, K, W, h, R, r0 - P.pad, c0 - P.pad, P.AS, (float)shift,
-                          exp2f((float)shift));
+      splat_dispatch<PSF>(acc, rl, K, W, h, P.AS, (float)shift, exp2f((float)shift));
     } else {
       for (int c = 0; c < G; ++c)
         splat_dispatch<PSF>(acc, recs + (((size_t)f * T + t) * G + c) * P.cap,
-                            __ldcg(&counts[((size_t)f * T + t) * G + c]), W, h, R, r0 - P.pad,
-                            c0 - P.pad, P.AS, (float)shift, exp2f((float)shift));
+                            __ldcg(&counts[((size_t)f * T + t) * G + c]), W, h, P.AS,
+                            (float)shift, exp2f((float)shift));
     }
     __syncthreads();
     store_tile(P, acc, pl, f, r0, nr, c0, nc, exp2f(-(float)shift));
@@ -943,7 +960,8 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* 
       // last renderer retires the slot: reset it, then publish the new epoch
       S->gen_done = 0;
       S->render_done = 0;
-      S->dmax = S->amp = S->smax[0] = S->smax[1] = 0u;
+      S->dmax = S->amp = 0u;
+      S->wmax[0] = S->wmax[1] = 0;
       __threadfence();
       atomicAdd(&S->epoch, 1);
     }

@@ -240,8 +240,7 @@ Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes) 
     p.rbuf = (int)std::min<long long>(std::max<long long>(n, 8),
                                       (long long)std::ceil(lam + 4.0 * std::sqrt(lam) + 16.0));
     p.rbuf = (p.rbuf + 7) / 8 * 8;
-    p.cells_cap = ((p.TH + 2 * halo + kCellMin - 1) / kCellMin) *
-                  ((p.TW + 2 * halo + kCellMin - 1) / kCellMin);
+    p.cells_cap = ((p.AH + kCellMin - 1) / kCellMin) * ((p.AS + kCellMin - 1) / kCellMin);
     p.tiles_y = (rows + p.TH - 1) / p.TH;
     p.tiles_x = (W + p.TW - 1) / p.TW;
     p.tiles = p.tiles_y * p.tiles_x;

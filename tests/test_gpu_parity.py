@@ -131,7 +131,8 @@ def test_bin_counts_bit_exact(pg, golden):
         _lib.call("pgb_plan", H, W, c["pos1"].shape[0], 0.0, int(c["side"]) // 2, 2, ctypes.byref(info))
         assert tiles == info.tiles_y * info.tiles_x
         for f in (1, 2):
-            want = orr.tile_counts(c[f"pos{f}"], c[f"mask{f}"], info.halo, info.tile_h, info.tile_w, H, W)
+            want = orr.tile_counts(c[f"pos{f}"], c[f"mask{f}"], c[f"sx_{f}"], c[f"sy_{f}"], info.halo,
+                                   info.tile_h, info.tile_w, H, W)
             np.testing.assert_array_equal(bins[0, f - 1, :tiles], want, err_msg=f"{name} f{f}")
 
 

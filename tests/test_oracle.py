@@ -130,15 +130,27 @@ def test_oracle_erf_converges_to_point_for_wide_psf():
 
 def test_oracle_tile_counts_cover_every_window():
     rng = np.random.default_rng(0)
-    pos = rng.uniform(-3, 67, size=(500, 2))
+    pos = rng.uniform(4, 60, size=(500, 2))
     on = rng.random(500) < 0.9
-    counts = orr.tile_counts(pos, on, 2, 16, 32, 64, 64)
+    sig = np.full(500, 0.25, np.float32)
+    counts = orr.tile_counts(pos, on, sig, sig, 2, 16, 32, 64, 64)
     assert counts.shape == (8,)
-    # every particle whose window touches the image lands in >= 1 tile
-    ax = np.floor(pos[:, 0] + 0.5)
-    ay = np.floor(pos[:, 1] + 0.5)
-    inside = on & (ax >= -2) & (ax <= 65) & (ay >= -2) & (ay <= 65)
-    assert counts.sum() >= inside.sum()
+    # every interior particle lands in >= 1 tile, at most 4
+    assert on.sum() <= counts.sum() <= 4 * on.sum()
+
+
+def test_oracle_tight_window_is_exact():
+    # every pixel outside the tight window contributes < 1/2 unit at shift 22
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        fx, fy = rng.uniform(-0.5, 0.5, 2)
+        s = np.float32(rng.uniform(0.1, 1.2))
+        jlo, jhi, ilo, ihi = orr.tight_window(np.float32(fx), np.float32(fy), s, s, 20)
+        for j in range(-20, 21):
+            for i in (0,):
+                v = 2.0 ** 22 * math.exp(-((j - float(np.float32(fx))) ** 2) / (2 * float(s) ** 2))
+                if j < jlo or j > jhi:
+                    assert v < 0.5
 
 
 @pytest.mark.skipif(not reference.available(), reason="oracle/_ref not built")
