@@ -345,7 +345,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
-                         "kernel": "pgb::fused_generate_kernel", "peak_source": peak_kind},
+                         "kernel": "pgb::band_kernel (+ prologue_kernel)", "peak_source": peak_kind},
             "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "pgb_generate_batch (C ABI, host buffers: flow H2D + images D2H, pinned)"},

@@ -1,7 +1,8 @@
 """CPU restatement of the seeding + advection path -- TEST INFRASTRUCTURE.
 
-Mirrors paper_2512_09664_b200/csrc/fused.cuh make_particle() with the Philox
-draw layout of the B200 kernels, and the reference semantics it implements:
+Mirrors paper_2512_09664_b200/csrc/band.cuh (prologue_kernel + seed_particle)
+with the Philox draw layout of the B200 kernels, and the reference semantics
+it implements:
 
   particle_capacity   config.py:139-146   N = ceil(round(ppp_max * H * W, 9))
   sample_particles    particles.py:61-101 positions U[0,W)xU[0,H), ppp, M,
@@ -11,7 +12,12 @@ draw layout of the B200 kernels, and the reference semantics it implements:
   apply_hiding        particles.py:139-147
   patch_side          raster.py:30-38 (+ pipeline.py:291-294 for d_max)
 
-Positions are fixed point (x = (2w + 1) W / 2^33, anchor + float32 fraction);
+Stratified seeding (same law as iid uniform positions): the image is split
+into 2^sy x 2^sx equal-area cells; the cell counts are the histogram of M iid
+uniform labels, particle g sits in the cell whose prefix range holds g, at a
+uniform position inside it. The maximum diameter uniform is drawn first
+(m = V^(1/M) with reproducible log/exp, on a uniform particle J); the others
+are m * U. Positions are fixed point (value / 2^33, anchor + float32 fraction);
 every float32 step is a separately rounded numpy float32 op (no FMA), so
 positions, diameters, sigma, i0, rho, masks, M and side are bit-identical to
 the GPU; Box-Muller normals (frame-2 jitter) and the laser-sheet profile use
@@ -145,24 +151,122 @@ def hide_threshold(p: float) -> int:
     return int(min(max(t, 0), 4294967296))
 
 
-def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> dict:
-    """All per-particle arrays of one pair, exactly as csrc/fused.cuh gen_particle()
-    produces them: fixed-point positions, float32 attributes and advection."""
+MAX_CELL_BITS = 14
+LN2 = 0.6931471805599453
+
+
+def cell_bits(height: int, width: int):
+    """csrc/pivgen_b200.cu cell_bits: ~4 px cells, at most 2^14 cells."""
+    def bits(n):
+        s = 0
+        while (4 << (s + 1)) <= n:
+            s += 1
+        return s
+    sy, sx = bits(height), bits(width)
+    while sy + sx > MAX_CELL_BITS:
+        if sx >= sy:
+            sx -= 1
+        else:
+            sy -= 1
+    return sy, sx
+
+
+def rlog(x: float) -> float:
+    """common.cuh rlog: only correctly rounded +,-,*,/ (bit-identical to the GPU)."""
+    f, e = math.frexp(x)
+    if f < 0.70710678118654752:
+        f = f * 2.0
+        e -= 1
+    s = (f - 1.0) / (f + 1.0)
+    z = s * s
+    p = 1.0 / 25.0
+    for k in range(11, -1, -1):
+        p = p * z + 1.0 / float(2 * k + 1)
+    return float(e) * LN2 + 2.0 * (s * p)
+
+
+def rexp(y: float) -> float:
+    """common.cuh rexp."""
+    k = float(round(y / LN2))          # round-half-even == rint
+    r = y - k * LN2
+    p = 1.0
+    for i in range(16, 0, -1):
+        p = 1.0 + (r * p) / float(i)
+    return math.ldexp(p, int(k))
+
+
+def pair_header(cfg: "GenConfig", batch: int, gpair: int) -> dict:
+    """prologue_kernel thread 0: density, M, maximum-diameter draw, patch side."""
     n = cfg.n
     H, W = cfg.height, cfg.width
-    idx = np.arange(n, dtype=np.uint64)
     w = px.draw(cfg.seed, gpair, batch, np.uint64(0), px.TAG_PAIR)
     ppp = float(cfg.ppp_range[0] + (cfg.ppp_range[1] - cfg.ppp_range[0]) * px.u53_to_unit(w[0], w[1]))
     m = int(np.rint(ppp * H * W))
     m = min(max(m, 0), n)
+    hd = dict(ppp=ppp, M=m, m=0.0, J=0, qmax=0, dmax=float(np.float32(cfg.d_range[1])))
+    if m > 0:
+        v = px.draw(cfg.seed, gpair, batch, np.uint64(1), px.TAG_PAIR)
+        V = float(px.u53_to_unit(v[0], v[1]))
+        mu = rexp(rlog(V) / float(m))
+        w64 = (int(v[3]) << 32) | int(v[2])
+        hd["m"] = mu
+        hd["J"] = (w64 * m) >> 64
+        hd["qmax"] = min(int(math.floor(mu * 8388608.0)), 0x7FFFFF)
+        hd["dmax"] = float(lerp32(cfg.d_range[0], cfg.d_range[1], q_unit(np.array([hd["qmax"]])))[0])
+    hd["side"] = patch_side(hd["dmax"] if m > 0 else cfg.d_range[1], cfg.patch_multiplier)
+    return hd
+
+
+def q_unit(q) -> np.ndarray:
+    return (np.asarray(q).astype(F32) + F32(0.5)) * F32(2.0 ** -23)
+
+
+def cell_prefix(cfg: "GenConfig", batch: int, gpair: int, M: int) -> np.ndarray:
+    """prologue_kernel: histogram of M iid cell labels (word >> (32 - L)), exclusive prefix."""
+    sy, sx = cell_bits(cfg.height, cfg.width)
+    L = sy + sx
+    q = np.arange((M + 3) // 4, dtype=np.uint64)
+    words = np.stack(px.draw(cfg.seed, gpair, batch, q, px.TAG_CELL), axis=1).reshape(-1)[:M]
+    labels = (words >> np.uint32(32 - L)).astype(np.int64) if L else np.zeros(M, np.int64)
+    counts = np.bincount(labels, minlength=1 << L)
+    return np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+
+
+def cell_coord(cell, w, size: int, bits: int) -> np.ndarray:
+    """band.cuh cell_coord: ((cell << 33) + 2 w + 1) * size >> bits (uint64)."""
+    c = np.asarray(cell).astype(np.uint64)
+    return (((c << np.uint64(33)) + np.uint64(2) * np.asarray(w).astype(np.uint64) + np.uint64(1))
+            * np.uint64(size)) >> np.uint64(bits)
+
+
+def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> dict:
+    """All per-particle arrays of one pair, exactly as csrc/band.cuh seed_particle()
+    produces them: stratified fixed-point positions, float32 attributes and advection."""
+    n = cfg.n
+    H, W = cfg.height, cfg.width
+    idx = np.arange(n, dtype=np.uint64)
+    hd = pair_header(cfg, batch, gpair)
+    ppp, m = hd["ppp"], hd["M"]
+    sy, sx = cell_bits(H, W)
+    pre = cell_prefix(cfg, batch, gpair, m)
+    active = np.arange(n) < m
+    cell = np.searchsorted(pre, np.arange(n), side="right") - 1
+    cell = np.where(active, np.minimum(cell, (1 << (sy + sx)) - 1), 0)
+    cy, cx = cell >> sx, cell & ((1 << sx) - 1)
 
     a = px.draw(cfg.seed, gpair, batch, idx, px.TAG_PARTICLE_A)
-    X = (2 * a[0].astype(np.uint64) + np.uint64(1)) * np.uint64(W)
-    Y = (2 * a[1].astype(np.uint64) + np.uint64(1)) * np.uint64(H)
-    d = lerp32(cfg.d_range[0], cfg.d_range[1], unit23(a[2]))
+    X = np.where(active, cell_coord(cx, a[0], W, sx),
+                 (2 * a[0].astype(np.uint64) + np.uint64(1)) * np.uint64(W)).astype(np.uint64)
+    Y = np.where(active, cell_coord(cy, a[1], H, sy),
+                 (2 * a[1].astype(np.uint64) + np.uint64(1)) * np.uint64(H)).astype(np.uint64)
+    # diameters: particle J holds the maximum quantile, the others are m * U
+    u = hd["m"] * ((a[2].astype(np.float64) + 0.5) * 2.0 ** -32)
+    q = np.minimum(np.floor(u * 8388608.0), 0x7FFFFF).astype(np.int64)
+    if m > 0:
+        q[hd["J"]] = hd["qmax"]
+    d = np.where(active, lerp32(cfg.d_range[0], cfg.d_range[1], q_unit(q)),
+                 lerp32(cfg.d_range[0], cfg.d_range[1], unit23(a[2]))).astype(F32)
     i0 = lerp32(cfg.i0_range[0], cfg.i0_range[1], unit23(a[3]))
-    active = np.arange(n) < m
-
     need_b = (cfg.rho_range[0] != cfg.rho_range[1]) or cfg.hide_probability > 0 or cfg.laser is not None
     if need_b:
         b = px.draw(cfg.seed, gpair, batch, idx, px.TAG_PARTICLE_B)
@@ -218,9 +322,10 @@ def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> 
     on1 = active & vis1 & (amp1 > 0)
     on2 = active & vis2 & (amp2 > 0)
     dmax = float(d[:m].max()) if m else float(cfg.d_range[1])
-    side = patch_side(dmax, cfg.patch_multiplier)
+    assert not m or dmax == hd["dmax"]
+    side = hd["side"]
     return dict(ppp=ppp, M=m, pos1=pos1, pos2=pos2, i0_1=amp1, sx_1=sig, sy_1=sig.copy(),
                 rho_1=rho, i0_2=amp2, sx_2=sx2, sy_2=sy2, rho_2=rho2, diameter=d,
                 z1=z1, active=active, visible1=vis1 & active, visible2=vis2 & active,
                 on1=on1, on2=on2, side=side, d_max=dmax,
-                anchors=(ax1, ay1, ax2, ay2), fracs=(fx1, fy1, fx2, fy2))
+                anchors=(ax1, ay1, ax2, ay2), fracs=(fx1, fy1, fx2, fy2), prefix=pre)

@@ -24,6 +24,7 @@ TAG_PARTICLE_B = 0x02
 TAG_PERTURB = 0x03
 TAG_PAIR = 0x04
 TAG_NOISE = 0x10
+TAG_CELL = 0x20
 
 # Random123 kat_vectors, philox4x32 R=10: (counter[4], key[2]) -> out[4]
 KAT = [

@@ -1,0 +1,725 @@
+// band.cuh -- the batched image-pair generator: prologue + band kernel.
+//
+// Replaces the body of Sampler._render_batch (reference pipeline.py:278-329):
+// sample_particles / perturb_frame2 / advect / apply_hiding
+// (particles.py:61-147), patch_side (raster.py:30-38, pipeline.py:291-294),
+// splat (raster.py:108-126 -> _native.pyx:14-66), finalize (raster.py:154-161)
+// and quantize_u16 (export.py:19-20).
+//
+// Design (B200-first):
+//   * Stratified seeding. The M particle positions of a pair are iid uniform
+//     over the image; we draw them as (cell counts, position inside the cell)
+//     where the image is split into 2^sy x 2^sx equal-area seeding cells and
+//     the counts are the histogram of M iid uniform cell labels -- exactly the
+//     multinomial law of iid uniform positions. Particle g of the pair lives in
+//     the cell whose prefix range holds g; all its other draws are keyed by g.
+//     The per-pair maximum diameter (patch side, pipeline.py:292) is drawn
+//     first (max of M uniforms ~ V^(1/M), carried by a uniform particle J; the
+//     others are uniform below it) -- the same joint law, known up front.
+//   * prologue_kernel (one CTA per pair): density, M, maximum diameter, the
+//     cell histogram -> per-cell prefix; one CTA per flow field: max |u|,|v|.
+//   * band_kernel (persistent, one item = one screen tile of one pair, both
+//     frames): every CTA enumerates only the cells whose particles can reach
+//     its tile (tile + patch half-width + the field's max displacement),
+//     regenerates those particles from their counters, advects them and splats
+//     them straight into a shared-memory fixed-point accumulator (int32,
+//     2^-s units: integer adds are associative -> bit-identical results for
+//     any schedule), then runs the fused epilogue (offset + Philox noise +
+//     clamp, optional uint16) with 128-bit streaming stores. No inter-CTA
+//     communication, no global intermediates: HBM traffic = the images.
+#pragma once
+#include "fused.cuh"
+
+namespace pgb {
+
+constexpr int kBandThreads = 256;
+constexpr int kBandWarps = kBandThreads / 32;
+constexpr int kMaxCellBits = 14;
+
+struct __align__(16) PairHdr {
+  double ppp;      // realised seeding density
+  double m;        // continuous maximum diameter uniform (0 when M == 0)
+  int M;           // active particles
+  int J;           // particle carrying the maximum
+  int qmax;        // 23-bit quantised maximum
+  int side;        // patch side of the pair
+  float dmax;      // maximum diameter
+  int cmax;        // max particles in one seeding cell
+  int pad0, pad1;
+};
+
+struct BandParams {
+  int H, W;
+  int TH, TW, AS, tiles_y, tiles_x, tiles;
+  int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
+  int cells_cap;               // cells per enumeration chunk (shared memory)
+  int n, pairs;
+  long long pair_base;
+  uint32_t batch_lo;
+  int psf, out_mode;
+  float bg_offset, noise_std;
+  float amp_bound;             // upper bound of any particle amplitude
+  GenCfg g;
+  const float2* flows;
+  int pairs_per_field, num_fields;
+  long long field_elems;
+  float2* fbound;              // [num_fields] (max |u|, max |v|)
+  int* prefix;                 // [pairs][2^(sy+sx) + 1] particle prefix per cell
+  PairHdr* hdr;                // [pairs]
+  void* out[2];
+  long long out_pair_elems;
+  double* st_ppp;
+  int* st_M;
+  int* st_side;
+  float* st_dmax;
+  int* ticket;
+};
+
+// ----------------------------------------------------------------------------
+// Seeding pieces shared by the band kernel and the particle-array kernel
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ RngKey band_key(const BandParams& P, int pl) {
+  return RngKey{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
+}
+
+// Fixed-point position (value / 2^33) of a particle of cell (cy, cx):
+// y = (cy + (2w + 1) / 2^33) H / 2^sy, rounded down to 2^-33.
+__device__ __forceinline__ uint64_t cell_coord(uint32_t cell, uint32_t w, int size, int bits) {
+  return ((((uint64_t)cell << 33) + 2ull * w + 1ull) * (uint64_t)size) >> bits;
+}
+
+// 23-bit diameter quantile of particle g (the maximum sits on particle J).
+__device__ __forceinline__ int diam_q(const PairHdr& hd, int g, uint32_t wz) {
+  if (g == hd.J) return hd.qmax;
+  const double u = __dmul_rn(hd.m, ((double)wz + 0.5) * 0x1p-32);
+  const int q = (int)floor(u * 8388608.0);
+  return q < 0x7fffff ? q : 0x7fffff;
+}
+
+__device__ __forceinline__ float q_to_unit(int q) { return ((float)q + 0.5f) * 0x1p-23f; }
+
+// Advection of a fixed-point point: bilinear, edge-clamped (flowfield.py:207-232)
+// in float32, then the new anchor/fraction (see fused.cuh gen_particle).
+__device__ __forceinline__ void advect_fixed(const GenCfg& g, const float2* __restrict__ flow,
+                                             uint64_t X, uint64_t Y, int ax, float fx, int ay,
+                                             float fy, int& ax2, float& fx2, int& ay2, float& fy2) {
+  int cx, cy;
+  float tx, ty;
+  fixed_cell(X, g.W, cx, tx);
+  fixed_cell(Y, g.H, cy, ty);
+  const int cx1 = cx + 1 < g.W ? cx + 1 : g.W - 1;
+  const int cy1 = cy + 1 < g.H ? cy + 1 : g.H - 1;
+  const float2 q00 = __ldg(flow + (size_t)cy * g.W + cx);
+  const float2 q01 = __ldg(flow + (size_t)cy * g.W + cx1);
+  const float2 q10 = __ldg(flow + (size_t)cy1 * g.W + cx);
+  const float2 q11 = __ldg(flow + (size_t)cy1 * g.W + cx1);
+  const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
+  const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
+  shift_anchor(ax, fx, u, ax2, fx2);
+  shift_anchor(ay, fy, v, ay2, fy2);
+}
+
+// Appearance of both frames (particles.py:61-126 + laser sheet), given the
+// active particle's diameter and i0. Keyed by the particle index g.
+struct Look {
+  float amp1, amp2, sx2, sy2, rho1, rho2, z1;
+  bool vis1, vis2;
+};
+
+__device__ __forceinline__ void seed_look(const GenCfg& g, const RngKey& key, int gi, float sig,
+                                          float i0, Look& lk) {
+  float rho = g.rho_lo, z1 = 0.f;
+  bool vis1 = true, vis2 = true;
+  if (g.need_b) {
+    const uint4 b = draw(key, (uint32_t)gi, kTagParticleB);
+    rho = lerpf_exact(g.rho_lo, g.rho_span, unit23(b.x));
+    vis1 = (uint64_t)b.y >= g.hide_thr;   // apply_hiding (particles.py:139-147)
+    vis2 = (uint64_t)b.z >= g.hide_thr;
+    z1 = lerpf_exact(g.z_lo, g.z_span, unit23(b.w));
+  }
+  float sx2 = sig, sy2 = sig, i02 = i0, rho2 = rho;
+  if (g.need_perturb) {
+    // perturb_frame2 (particles.py:104-126)
+    const uint4 c = draw(key, (uint32_t)gi, kTagPerturb);
+    const float2 n01 = box_muller(c.x, c.y);
+    const float2 n23 = box_muller(c.z, c.w);
+    if (g.f2_sigma_std > 0.f) {
+      sx2 = fmaxf(__fadd_rn(sig, __fmul_rn(g.f2_sigma_std, n01.x)), 1e-3f);
+      sy2 = fmaxf(__fadd_rn(sig, __fmul_rn(g.f2_sigma_std, n01.y)), 1e-3f);
+    }
+    if (g.f2_i0_std > 0.f) {
+      const float t = fminf(fmaxf(__fadd_rn(i0, __fmul_rn(g.f2_i0_std, n23.x)), 0.f), 1.f);
+      i02 = i0 == 0.f ? 0.f : t;
+    }
+    if (g.f2_rho_std > 0.f) {
+      const float lim = 0.999f;
+      rho2 = fminf(fmaxf(__fadd_rn(rho, __fmul_rn(g.f2_rho_std, n23.y)), -lim), lim);
+    }
+  }
+  float amp1 = i0, amp2 = i02;
+  if (g.laser) {
+    amp1 *= laser_profile(g, z1);
+    amp2 *= laser_profile(g, z1 + g.w);
+  }
+  lk.amp1 = amp1; lk.amp2 = amp2; lk.sx2 = sx2; lk.sy2 = sy2;
+  lk.rho1 = rho; lk.rho2 = rho2; lk.z1 = z1; lk.vis1 = vis1; lk.vis2 = vis2;
+}
+
+// Full particle (both frames) for the particle-array API (sample_particles).
+__device__ __forceinline__ void seed_particle(const BandParams& P, const PairHdr& hd, int pl, int gi,
+                                              int cy, int cx, const float2* __restrict__ flow,
+                                              Particle& pt) {
+  const GenCfg& g = P.g;
+  const RngKey key = band_key(P, pl);
+  const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
+  const bool active = gi < hd.M;
+  uint64_t X, Y;
+  float d;
+  if (active) {
+    X = cell_coord((uint32_t)cx, a.x, g.W, P.sx);
+    Y = cell_coord((uint32_t)cy, a.y, g.H, P.sy);
+    d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
+  } else {
+    // inactive capacity slots: full-image uniforms, never rendered
+    X = (2ull * a.x + 1ull) * (uint64_t)g.W;
+    Y = (2ull * a.y + 1ull) * (uint64_t)g.H;
+    d = lerpf_exact(g.d_lo, g.d_span, unit23(a.z));
+  }
+  const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
+  const float i0f = active ? i0 : 0.f;
+  const float sig = __fmul_rn(d, g.inv_ratio);
+  Look lk;
+  seed_look(g, key, gi, sig, i0f, lk);
+  Frame& f1 = pt.fr[0];
+  Frame& f2 = pt.fr[1];
+  fixed_anchor(X, f1.ax, f1.fx);
+  fixed_anchor(Y, f1.ay, f1.fy);
+  advect_fixed(g, flow, X, Y, f1.ax, f1.fx, f1.ay, f1.fy, f2.ax, f2.fx, f2.ay, f2.fy);
+  f1.amp = lk.amp1; f1.sx = sig; f1.sy = sig; f1.rho = lk.rho1;
+  f2.amp = lk.amp2; f2.sx = lk.sx2; f2.sy = lk.sy2; f2.rho = lk.rho2;
+  f1.on = active && lk.vis1 && lk.amp1 > 0.f;
+  f2.on = active && lk.vis2 && lk.amp2 > 0.f;
+  pt.diam = d;
+  pt.z1 = lk.z1;
+  pt.active = active;
+  pt.vis1 = lk.vis1 && active;
+  pt.vis2 = lk.vis2 && active;
+}
+
+// ----------------------------------------------------------------------------
+// Block-wide exclusive scan (in place allowed): out[i] = sum(in[0..i)),
+// out[count] = total. NT threads, `wsum` = NT/32 ints of shared scratch.
+// ----------------------------------------------------------------------------
+template <int NT>
+__device__ int block_scan(const int* in, int* out, int count, int* wsum) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (count + NT - 1) / NT;
+  const int b = min(count, (int)threadIdx.x * per), e = min(count, b + per);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += in[i];
+  int x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(~0u, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < NW ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(~0u, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < NW) wsum[lane] = v;
+  }
+  __syncthreads();
+  int base = (warp ? wsum[warp - 1] : 0) + x - s;
+  for (int i = b; i < e; ++i) {
+    const int v = in[i];
+    out[i] = base;
+    base += v;
+  }
+  const int total = wsum[NW - 1];
+  if (threadIdx.x == 0) out[count] = total;
+  __syncthreads();
+  return total;
+}
+
+// ----------------------------------------------------------------------------
+// Prologue: one CTA per pair (+ one per flow field)
+// ----------------------------------------------------------------------------
+constexpr int kPrologueThreads = 512;
+constexpr int kFieldBlocks = 16;   // CTAs per flow field for the displacement bound
+
+__global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandParams P) {
+  extern __shared__ int bins[];
+  __shared__ int wsum[kPrologueThreads / 32];
+  __shared__ int sM;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (blockIdx.x >= P.pairs) {
+    // flow bound: kFieldBlocks CTAs per field, float4 loads, atomicMax on the
+    // bits of non-negative floats (non-finite values -> unbounded)
+    const int fb = blockIdx.x - P.pairs;
+    const int f = fb / kFieldBlocks, part = fb - f * kFieldBlocks;
+    const float2* fl = P.flows + (size_t)f * P.field_elems;
+    float mu = 0.f, mv = 0.f;
+    const long long stride = (long long)kFieldBlocks * kPrologueThreads;
+#pragma unroll 4
+    for (long long e = (long long)part * kPrologueThreads + tid; e < P.field_elems; e += stride) {
+      const float2 v = __ldg(fl + e);
+      const float au = fabsf(v.x), av = fabsf(v.y);
+      mu = au <= 3.0e38f ? fmaxf(mu, au) : INFINITY;
+      mv = av <= 3.0e38f ? fmaxf(mv, av) : INFINITY;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mu = fmaxf(mu, __shfl_xor_sync(~0u, mu, o));
+      mv = fmaxf(mv, __shfl_xor_sync(~0u, mv, o));
+    }
+    if (lane == 0) {
+      unsigned* b = reinterpret_cast<unsigned*>(P.fbound + f);
+      atomicMax(b, __float_as_uint(mu));
+      atomicMax(b + 1, __float_as_uint(mv));
+    }
+    return;
+  }
+  const int pl = blockIdx.x;
+  const int L = P.sy + P.sx;
+  const int ncell = 1 << L;
+  const RngKey key = band_key(P, pl);
+  for (int i = tid; i < ncell; i += kPrologueThreads) bins[i] = 0;
+  if (tid == 0) {
+    const GenCfg& g = P.g;
+    // seeding density and active count (particles.py:73-83)
+    const uint4 w = draw(key, 0u, kTagPair);
+    const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w.x, w.y));
+    double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+    mm = fmin(fmax(mm, 0.0), (double)P.n);
+    const int M = (int)mm;
+    // maximum diameter uniform: max of M uniforms = V^(1/M), on particle J
+    PairHdr hd{};
+    hd.ppp = ppp;
+    hd.M = M;
+    float dmax = (float)g.d_hi;
+    if (M > 0) {
+      const uint4 v = draw(key, 1u, kTagPair);
+      const double V = u53_to_unit(v.x, v.y);
+      hd.m = rexp(ddiv(rlog(V), (double)M));
+      hd.J = (int)__umul64hi(((uint64_t)v.w << 32) | v.z, (uint64_t)M);
+      const int q = (int)floor(hd.m * 8388608.0);
+      hd.qmax = q < 0x7fffff ? q : 0x7fffff;
+      dmax = lerpf_exact(g.d_lo, g.d_span, q_to_unit(hd.qmax));
+    }
+    hd.dmax = dmax;
+    // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
+    hd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
+    P.hdr[pl] = hd;
+    if (P.st_ppp) P.st_ppp[pl] = ppp;
+    if (P.st_M) P.st_M[pl] = M;
+    if (P.st_side) P.st_side[pl] = hd.side;
+    if (P.st_dmax) P.st_dmax[pl] = dmax;
+    sM = M;
+  }
+  __syncthreads();
+  const int M = sM;
+  // cell histogram of M iid labels (4 labels per Philox call)
+  for (int q = tid; q < (M + 3) >> 2; q += kPrologueThreads) {
+    const uint4 w = draw(key, (uint32_t)q, kTagCell);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+  }
+  __syncthreads();
+  int cm = 0;
+  for (int i = tid; i < ncell; i += kPrologueThreads) cm = max(cm, bins[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
+  if (lane == 0) atomicMax(&P.hdr[pl].cmax, cm);
+  int* pre = P.prefix + (size_t)pl * (ncell + 1);
+  // scan in shared memory, then one coalesced copy out
+  block_scan<kPrologueThreads>(bins, bins, ncell, wsum);
+  for (int i = tid; i <= ncell; i += kPrologueThreads) pre[i] = bins[i];
+}
+
+// ----------------------------------------------------------------------------
+// Band kernel
+// ----------------------------------------------------------------------------
+struct __align__(16) BandShared {
+  int item;
+  int pad[3];
+  int wsum[kBandWarps];
+};
+
+// One frame of one particle into the tile accumulator (tight window clipped
+// to the patch half-width h and to the tile).
+template <int PSF>
+__device__ __forceinline__ void splat_one(int* __restrict__ acc, int AS, int ax, int ay, float fx,
+                                          float fy, float amp, float sx, float sy, float rho, int h,
+                                          int r0, int r1, int c0, int c1, int shift, float scale) {
+  Frame fr;
+  fr.ax = ax; fr.ay = ay; fr.fx = fx; fr.fy = fy; fr.amp = amp; fr.sx = sx; fr.sy = sy; fr.rho = rho;
+  const float R = record_radius(fr, PSF);
+  const int jlo = max(-h, (int)ceilf(__fsub_rn(fx, R)));
+  const int jhi = min(h, (int)floorf(__fadd_rn(fx, R)));
+  const int ilo = max(-h, (int)ceilf(__fsub_rn(fy, R)));
+  const int ihi = min(h, (int)floorf(__fadd_rn(fy, R)));
+  const int rlo = max(ay + ilo, r0), rhi = min(ay + ihi, r1 - 1);
+  const int clo = max(ax + jlo, c0), chi = min(ax + jhi, c1 - 1);
+  if (rlo > rhi || clo > chi) return;
+  const int nr = rhi - rlo + 1, nc = chi - clo + 1;
+  const float dx0 = (float)(clo - ax) - fx;
+  const float dy0 = (float)(rlo - ay) - fy;
+  int* base = acc + (rlo - r0) * AS + (clo - c0);
+  if (PSF == kPsfPoint) {
+    const float q = 1.0f - rho * rho;
+    const float isx = __frcp_rn(sx), isy = __frcp_rn(sy), iq = __frcp_rn(q);
+    const float A = (0.5f * kLog2e) * iq * isx * isx;
+    const float C = (0.5f * kLog2e) * iq * isy * isy;
+    const float B = -kLog2e * rho * iq * isx * isy;
+    const float Ls = __log2f(amp) + (float)shift;
+    for (int i = 0; i < nr; ++i) {
+      const float dy = dy0 + (float)i;
+      const float bt = B * dy;
+      const float rt = fmaf(-C * dy, dy, Ls);
+      int* row = base + i * AS;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < nc) {
+          const float dx = dx0 + (float)j;
+          const float e = fmaf(-dx, fmaf(A, dx, bt), rt);
+          atomicAdd(row + j, round_small(ex2_approx(e)));
+        }
+      }
+      for (int j = 4; j < nc; ++j) {
+        const float dx = dx0 + (float)j;
+        const float e = fmaf(-dx, fmaf(A, dx, bt), rt);
+        atomicAdd(row + j, round_small(ex2_approx(e)));
+      }
+    }
+  } else {
+    // pixel-area mean of Eq. (1) (oracle/render.py render_erf)
+    const float k = 1.2533141373155001f;  // sqrt(pi/2)
+    const float sc = sx * sqrtf(fmaxf(1.0f - rho * rho, 0.f));
+    const bool sep = rho == 0.f;
+    const float Lm = (sep ? amp * (k * sx) * (k * sy) : amp * (k * sc)) * scale;
+    const float rA = 0.70710678118654752f / sc;
+    const float rB = 0.70710678118654752f / sy;
+    const float rC = sep ? 0.f : rho * sx / sy;
+    for (int i = 0; i < nr; ++i) {
+      const float dy = dy0 + (float)i;
+      const float ey = sep ? erff((dy + 0.5f) * rB) - erff((dy - 0.5f) * rB) : 0.f;
+      for (int j = 0; j < nc; ++j) {
+        const float dx = dx0 + (float)j;
+        float val;
+        if (sep) {
+          val = (erff((dx + 0.5f) * rA) - erff((dx - 0.5f) * rA)) * ey;
+        } else {
+          float s = 0.f;
+#pragma unroll
+          for (int gq = 0; gq < kGLPoints; ++gq) {
+            const float yy = dy + kGLx[gq];
+            const float mu = rC * yy;
+            const float gy = __expf(-yy * yy * (rB * rB));
+            const float hi = erff((dx + 0.5f - mu) * rA);
+            const float lo = erff((dx - 0.5f - mu) * rA);
+            s = fmaf(kGLw[gq] * gy, hi - lo, s);
+          }
+          val = s;
+        }
+        const int qv = __float2int_rn(val * Lm);
+        if (qv) atomicAdd(base + i * AS + j, qv);
+      }
+    }
+  }
+}
+
+// Epilogue: one output quad (4 pixels) of frame f.
+template <int OUT, bool NOISE>
+__device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, char* dst, size_t pix,
+                                                int f, uint32_t gpair, float inv_scale) {
+  float4 v;
+  if ((a.x | a.y | a.z | a.w) >= (1 << 23)) {
+    v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
+  } else {
+    v = make_float4(acc_to_float(a.x), acc_to_float(a.y), acc_to_float(a.z), acc_to_float(a.w));
+  }
+  if (OUT == kOutRaw) {
+    v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
+    __stcs(reinterpret_cast<float4*>(dst), v);
+    return;
+  }
+  const float bg = P.bg_offset;
+  if (NOISE) {
+    const float sd = P.noise_std;
+    const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(pix >> 2));
+    v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
+    v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
+    v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
+    v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
+  } else {
+    v.x = fminf(fmaxf(fmaf(v.x, inv_scale, bg), 0.f), 1.f);
+    v.y = fminf(fmaxf(fmaf(v.y, inv_scale, bg), 0.f), 1.f);
+    v.z = fminf(fmaxf(fmaf(v.z, inv_scale, bg), 0.f), 1.f);
+    v.w = fminf(fmaxf(fmaf(v.w, inv_scale, bg), 0.f), 1.f);
+  }
+  if (OUT == kOutF32) {
+    __stcs(reinterpret_cast<float4*>(dst), v);
+  } else {
+    ushort4 u = make_ushort4(quant_u16(v.x), quant_u16(v.y), quant_u16(v.z), quant_u16(v.w));
+    __stcs(reinterpret_cast<ushort4*>(dst), u);
+  }
+}
+
+// Store one frame of the tile and zero its accumulator (quad path: tile
+// columns, image width and tile origin multiples of 4).
+template <int OUT, bool NOISE>
+__device__ void band_store_vec(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
+                               int nr, int c0, int nc, float inv_scale) {
+  constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
+  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
+  const int qpr = nc >> 2;
+  const int total = nr * qpr;
+  char* outb = static_cast<char*>(P.out[f]) + (size_t)pl * (size_t)P.out_pair_elems * ESZ;
+  if (total <= 0) return;
+  // incremental (row, quad) walk: two divisions per call, none per quad
+  int row = threadIdx.x / qpr, cq = threadIdx.x - (threadIdx.x / qpr) * qpr;
+  const int drow = kBandThreads / qpr, dcq = kBandThreads - drow * qpr;
+  for (int e = threadIdx.x; e < total; e += kBandThreads) {
+    int4* ap = reinterpret_cast<int4*>(acc + row * P.AS + cq * 4);
+    const int4 a = *ap;
+    *ap = make_int4(0, 0, 0, 0);
+    const size_t pix = (size_t)(r0 + row) * P.W + (size_t)(c0 + cq * 4);
+    band_store_quad<OUT, NOISE>(P, a, outb + pix * ESZ, pix, f, gpair, inv_scale);
+    row += drow;
+    cq += dcq;
+    if (cq >= qpr) { cq -= qpr; ++row; }
+  }
+}
+
+__device__ void band_store_scalar(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
+                                  int nr, int c0, int nc, float inv_scale) {
+  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
+  const size_t pair_off = (size_t)pl * (size_t)P.out_pair_elems;
+  const int mode = P.out_mode;
+  const float bg = P.bg_offset, sd = P.noise_std;
+  const int total = nr * nc;
+  for (int e = threadIdx.x; e < total; e += kBandThreads) {
+    const int row = e / nc;
+    const int col = e - row * nc;
+    int* ap = acc + row * P.AS + col;
+    float v = (float)*ap * inv_scale;
+    *ap = 0;
+    const size_t p = (size_t)(r0 + row) * P.W + (size_t)(c0 + col);
+    if (mode == kOutRaw) {
+      static_cast<float*>(P.out[f])[pair_off + p] = v;
+    } else {
+      float nzv = 0.f;
+      if (sd > 0.f) {
+        const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
+        const int jn = (int)(p & 3);
+        nzv = jn == 0 ? nz.x : (jn == 1 ? nz.y : (jn == 2 ? nz.z : nz.w));
+      }
+      v = finalize_px(v, bg, sd, nzv);
+      if (mode == kOutF32) static_cast<float*>(P.out[f])[pair_off + p] = v;
+      else static_cast<uint16_t*>(P.out[f])[pair_off + p] = quant_u16(v);
+    }
+  }
+}
+
+__device__ void band_store(const BandParams& P, int* acc, int pl, int f, int r0, int nr, int c0, int nc,
+                           float inv_scale) {
+  const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
+  const bool noise = P.noise_std > 0.f;
+  if (vec) {
+    switch (P.out_mode) {
+      case kOutRaw: band_store_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
+      case kOutF32:
+        if (noise) band_store_vec<kOutF32, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        else band_store_vec<kOutF32, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        return;
+      default:
+        if (noise) band_store_vec<kOutU16, true>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        else band_store_vec<kOutU16, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+        return;
+    }
+  }
+  band_store_scalar(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
+}
+
+// Range of seeding cells [lo, hi] whose span [k*s, (k+1)*s) meets [a, b).
+__device__ __forceinline__ void cell_range(double a, double b, double s, int n, int& lo, int& hi) {
+  const double fa = floor(fmax(a, 0.0) / s);
+  const double fb = floor(fmin(b, (double)n * s) / s);
+  lo = (int)fmin(fa, (double)(n - 1));
+  hi = (int)fmin(fmax(fb, 0.0), (double)(n - 1));
+}
+
+template <int PSF>
+__global__ void __launch_bounds__(kBandThreads, 2) band_kernel(const BandParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
+  int* acc0 = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
+  int* acc1 = acc0 + P.TH * P.AS;
+  int* cP = acc1 + P.TH * P.AS;
+  int* cC = cP + P.cells_cap;
+  int* cOff = cC + P.cells_cap;
+  const int tid = threadIdx.x;
+  const GenCfg& g = P.g;
+  const int CY = 1 << P.sy, CX = 1 << P.sx;
+  const double ch = (double)g.H / (double)CY, cw = (double)g.W / (double)CX;
+  const long long total_items = (long long)P.pairs * P.tiles;
+  for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandThreads)
+    reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+  for (;;) {
+    if (tid == 0) sh->item = atomicAdd(P.ticket, 1);
+    __syncthreads();
+    const long long item = sh->item;
+    if (item >= total_items) break;
+    const int pl = (int)(item / P.tiles);
+    const int t = (int)(item - (long long)pl * P.tiles);
+    const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
+    const int r0 = ty * P.TH, r1 = min(r0 + P.TH, g.H);
+    const int c0 = tx * P.TW, c1 = min(c0 + P.TW, g.W);
+    const PairHdr hd = P.hdr[pl];
+    const int h = hd.side >> 1;
+    const int field = (int)((P.pair_base + pl) / P.pairs_per_field);
+    const float2* flow = P.flows + (size_t)field * P.field_elems;
+    const float2 fb = P.fbound[field];
+    // frame-1 positions that can reach the tile in either frame: anchors within
+    // h of the tile (frame 1), or within h + 1 + max|v| (frame 2: the anchor
+    // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
+    const double vy = (double)fb.y * (1.0 + 1e-6) + 1e-6;
+    const double vx = (double)fb.x * (1.0 + 1e-6) + 1e-6;
+    int cy0, cy1, cx0, cx1;
+    cell_range((double)r0 - h - 1.5 - vy, (double)r1 + h + 0.5 + vy, ch, CY, cy0, cy1);
+    cell_range((double)c0 - h - 1.5 - vx, (double)c1 + h + 0.5 + vx, cw, CX, cx0, cx1);
+    // fixed-point shift: contributions per pixel <= cmax * (cells one pixel's
+    // source box can meet), amplitude <= amp_bound
+    const double by = floor((2.0 * h + 3.0 + 2.0 * vy) / ch) + 2.0;
+    const double bx = floor((2.0 * h + 3.0 + 2.0 * vx) / cw) + 2.0;
+    const double cov = fmin((double)hd.M, (double)hd.cmax * fmin(by, (double)CY) * fmin(bx, (double)CX));
+    const int shift = shift_for(max(1, (int)cov), P.amp_bound);
+    const float scale = (float)(1 << shift);
+    const int rw = cx1 - cx0 + 1;
+    const int ncell = (cy1 - cy0 + 1) * rw;
+    const int* pre = P.prefix + (size_t)pl * ((size_t)CY * CX + 1);
+    const RngKey key = band_key(P, pl);
+    for (int cb = 0; cb < ncell; cb += P.cells_cap) {
+      const int cnt = min(P.cells_cap, ncell - cb);
+      {
+        // walk the chunk's cells with incremental (row, col): no divisions in the loop
+        const int ci0 = cb + tid;
+        int yy = ci0 / rw, xx = ci0 - (ci0 / rw) * rw;
+        const int dy = kBandThreads / rw, dx = kBandThreads - dy * rw;
+        for (int k = tid; k < cnt; k += kBandThreads) {
+          const int c = ((cy0 + yy) << P.sx) | (cx0 + xx);
+          const int p0 = __ldg(pre + c);
+          cP[k] = p0;
+          cC[k] = c;
+          cOff[k] = __ldg(pre + c + 1) - p0;
+          yy += dy;
+          xx += dx;
+          if (xx >= rw) { xx -= rw; ++yy; }
+        }
+      }
+      __syncthreads();
+      const int N = block_scan<kBandThreads>(cOff, cOff, cnt, sh->wsum);
+      // warp-uniform trip count + __syncwarp: lanes that skip a particle do
+      // not run ahead into the next iteration (keeps the warp converged)
+      for (int qb = 0; qb < N; qb += kBandThreads) {
+        const int q = qb + tid;
+        if (q < N) {
+        // cell k: largest k with cOff[k] <= q
+        int lo = 0, hi = cnt - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (cOff[mid] <= q) lo = mid;
+          else hi = mid - 1;
+        }
+        const int gi = cP[lo] + (q - cOff[lo]);
+        const int cc = cC[lo];
+        const int cyy = cc >> P.sx, cxx = cc & (CX - 1);
+        const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
+        const uint64_t X = cell_coord((uint32_t)cxx, a.x, g.W, P.sx);
+        const uint64_t Y = cell_coord((uint32_t)cyy, a.y, g.H, P.sy);
+        int ax1, ay1, ax2, ay2;
+        float fx1, fy1, fx2, fy2;
+        fixed_anchor(X, ax1, fx1);
+        fixed_anchor(Y, ay1, fy1);
+        advect_fixed(g, flow, X, Y, ax1, fx1, ay1, fy1, ax2, fx2, ay2, fy2);
+        // geometric pre-test with the full patch window
+        const bool in1 = ay1 + h >= r0 && ay1 - h < r1 && ax1 + h >= c0 && ax1 - h < c1;
+        const bool in2 = ay2 + h >= r0 && ay2 - h < r1 && ax2 + h >= c0 && ax2 - h < c1;
+        if (in1 || in2) {
+        const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
+        const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
+        const float sig = __fmul_rn(d, g.inv_ratio);
+        Look lk;
+        seed_look(g, key, gi, sig, i0, lk);
+        if (in1 && lk.vis1 && lk.amp1 > 0.f)
+          splat_one<PSF>(acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1, h, r0, r1, c0, c1,
+                         shift, scale);
+        if (in2 && lk.vis2 && lk.amp2 > 0.f)
+          splat_one<PSF>(acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2, lk.rho2, h, r0, r1,
+                         c0, c1, shift, scale);
+        }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+    const float inv_scale = 1.0f / scale;
+    band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
+    band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
+    __syncthreads();   // item slot + zeroed accumulators before the next ticket
+  }
+}
+
+// Particle arrays of the generator (one block per pair): exactly the particles
+// the band kernel renders (positions = anchor + fraction).
+__global__ void sample_band_kernel(const BandParams P, pgb_particle_out O) {
+  const int pl = blockIdx.x;
+  const PairHdr hd = P.hdr[pl];
+  const int ncell = 1 << (P.sy + P.sx);
+  const int* pre = P.prefix + (size_t)pl * (ncell + 1);
+  const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
+  for (int gi = threadIdx.x; gi < P.n; gi += blockDim.x) {
+    int cy = 0, cx = 0;
+    if (gi < hd.M) {
+      int lo = 0, hi = ncell - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(pre + mid) <= gi) lo = mid;
+        else hi = mid - 1;
+      }
+      cy = lo >> P.sx;
+      cx = lo & ((1 << P.sx) - 1);
+    }
+    Particle pt;
+    seed_particle(P, hd, pl, gi, cy, cx, flow, pt);
+    const size_t o = (size_t)pl * P.n + gi;
+    const Frame& a = pt.fr[0];
+    const Frame& b = pt.fr[1];
+    if (O.pos1) { O.pos1[2 * o] = (double)a.ax + (double)a.fx; O.pos1[2 * o + 1] = (double)a.ay + (double)a.fy; }
+    if (O.pos2) { O.pos2[2 * o] = (double)b.ax + (double)b.fx; O.pos2[2 * o + 1] = (double)b.ay + (double)b.fy; }
+    if (O.i0_1) O.i0_1[o] = a.amp;
+    if (O.sx_1) O.sx_1[o] = a.sx;
+    if (O.sy_1) O.sy_1[o] = a.sy;
+    if (O.rho_1) O.rho_1[o] = a.rho;
+    if (O.i0_2) O.i0_2[o] = b.amp;
+    if (O.sx_2) O.sx_2[o] = b.sx;
+    if (O.sy_2) O.sy_2[o] = b.sy;
+    if (O.rho_2) O.rho_2[o] = b.rho;
+    if (O.diameter) O.diameter[o] = pt.diam;
+    if (O.z1) O.z1[o] = pt.z1;
+    if (O.active) O.active[o] = pt.active ? 1 : 0;
+    if (O.visible1) O.visible1[o] = pt.vis1 ? 1 : 0;
+    if (O.visible2) O.visible2[o] = pt.vis2 ? 1 : 0;
+  }
+}
+
+}  // namespace pgb

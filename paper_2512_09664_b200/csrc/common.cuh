@@ -9,6 +9,7 @@
 //   bit-identical with the numpy reference: position sampling, advection
 //   (flowfield.py:207-232) and the active-count / patch-side rules.
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -32,6 +33,7 @@ constexpr uint32_t kTagParticleB = 0x02;  // rho, hide1, hide2, z
 constexpr uint32_t kTagPerturb = 0x03;    // 4 normals for frame-2 jitter
 constexpr uint32_t kTagPair = 0x04;       // per-pair seeding density
 constexpr uint32_t kTagNoise = 0x10;      // + frame (1, 2): pixel noise
+constexpr uint32_t kTagCell = 0x20;       // seeding-cell labels (stratified positions)
 
 PGB_HD uint32_t mulhi32(uint32_t a, uint32_t b) {
 #ifdef __CUDA_ARCH__
@@ -95,6 +97,28 @@ inline double ddiv(double a, double b) { volatile double r = a / b; return r; }
 
 // low + (high - low) * u   (rng.py:96)
 PGB_HD double lerp_exact(double lo, double hi, double u) { return dadd(lo, dmul(dsub(hi, lo), u)); }
+
+// Reproducible float64 log / exp: only correctly rounded +, -, *, / and exact
+// scalings, so oracle/generate.py (plain Python floats) reproduces every bit.
+// Accuracy ~1e-15 relative (they only draw the per-pair maximum diameter).
+PGB_HD double rlog(double x) {
+  int e = 0;
+  double f = frexp(x, &e);                       // x = f 2^e, f in [1/2, 1)
+  if (f < 0.70710678118654752) { f = dmul(f, 2.0); e -= 1; }
+  const double s = ddiv(dsub(f, 1.0), dadd(f, 1.0));
+  const double z = dmul(s, s);
+  double p = ddiv(1.0, 25.0);
+  for (int k = 11; k >= 0; --k) p = dadd(dmul(p, z), ddiv(1.0, (double)(2 * k + 1)));
+  return dadd(dmul((double)e, 0.6931471805599453), dmul(2.0, dmul(s, p)));
+}
+
+PGB_HD double rexp(double y) {
+  const double k = rint(ddiv(y, 0.6931471805599453));
+  const double r = dsub(y, dmul(k, 0.6931471805599453));
+  double p = 1.0;
+  for (int i = 16; i >= 1; --i) p = dadd(1.0, ddiv(dmul(r, p), (double)i));
+  return ldexp(p, (int)k);
+}
 
 // Smallest odd side >= ceil(round(mult * dmax + 1, 9)), at least 1 (raster.py:30-38).
 PGB_HD int patch_side_exact(double dmax, double mult) {

@@ -19,6 +19,7 @@
 #include "../../include/pivgen_b200.h"
 #include "common.cuh"
 #include "fused.cuh"
+#include "band.cuh"
 
 namespace pgb {
 
@@ -71,61 +72,6 @@ __global__ void quantize_kernel(const float* __restrict__ img, long long n, uint
     out[i] = quant_u16(img[i]);
 }
 
-// Particle arrays of the generator (one block per pair): exactly the particles
-// gen_particle() feeds to the fused kernel (positions = anchor + fraction).
-__global__ void sample_particles_kernel(FusedParams P, pgb_particle_out O) {
-  const int pl = blockIdx.x;
-  __shared__ int sM;
-  __shared__ unsigned sdmax;
-  __shared__ double sppp;
-  if (threadIdx.x == 0) {
-    const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
-    const uint4 w = draw(key, 0u, kTagPair);
-    const double ppp = lerp_exact(P.g.ppp_lo, P.g.ppp_hi, u53_to_unit(w.x, w.y));
-    double m = rint(dmul(dmul(ppp, (double)P.g.H), (double)P.g.W));
-    m = fmin(fmax(m, 0.0), (double)P.n);
-    sM = (int)m;
-    sppp = ppp;
-    sdmax = 0u;
-  }
-  __syncthreads();
-  const int M = sM;
-  unsigned dm = 0u;
-  const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
-  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
-    Particle pt;
-    gen_particle(P, pl, i, M, flow, pt);
-    const size_t o = (size_t)pl * P.n + i;
-    const Frame& a = pt.fr[0];
-    const Frame& b = pt.fr[1];
-    if (O.pos1) { O.pos1[2 * o] = (double)a.ax + (double)a.fx; O.pos1[2 * o + 1] = (double)a.ay + (double)a.fy; }
-    if (O.pos2) { O.pos2[2 * o] = (double)b.ax + (double)b.fx; O.pos2[2 * o + 1] = (double)b.ay + (double)b.fy; }
-    if (O.i0_1) O.i0_1[o] = a.amp;
-    if (O.sx_1) O.sx_1[o] = a.sx;
-    if (O.sy_1) O.sy_1[o] = a.sy;
-    if (O.rho_1) O.rho_1[o] = a.rho;
-    if (O.i0_2) O.i0_2[o] = b.amp;
-    if (O.sx_2) O.sx_2[o] = b.sx;
-    if (O.sy_2) O.sy_2[o] = b.sy;
-    if (O.rho_2) O.rho_2[o] = b.rho;
-    if (O.diameter) O.diameter[o] = pt.diam;
-    if (O.z1) O.z1[o] = pt.z1;
-    if (O.active) O.active[o] = pt.active ? 1 : 0;
-    if (O.visible1) O.visible1[o] = pt.vis1 ? 1 : 0;
-    if (O.visible2) O.visible2[o] = pt.vis2 ? 1 : 0;
-    if (pt.active) dm = max(dm, __float_as_uint(pt.diam));
-  }
-  atomicMax(&sdmax, dm);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const float dmax = M > 0 ? __uint_as_float(sdmax) : (float)P.g.d_hi;
-    if (P.st_ppp) P.st_ppp[pl] = sppp;
-    if (P.st_M) P.st_M[pl] = M;
-    if (P.st_dmax) P.st_dmax[pl] = dmax;
-    if (P.st_side) P.st_side[pl] = patch_side_exact(M > 0 ? (double)dmax : P.g.d_hi, P.g.patch_mult);
-  }
-}
-
 // perturb_frame2 (particles.py:104-126) on caller arrays, same draws as the
 // fused kernel (stream kTagPerturb, particle index i).
 __global__ void perturb_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, uint32_t batch,
@@ -165,9 +111,9 @@ __global__ void hiding_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, u
   }
 }
 
-template __global__ void fused_generate_kernel<0, kPsfPoint>(const FusedParams);
-template __global__ void fused_generate_kernel<0, kPsfErf>(const FusedParams);
 template __global__ void fused_generate_kernel<1, kPsfPoint>(const FusedParams);
+template __global__ void band_kernel<kPsfPoint>(const BandParams);
+template __global__ void band_kernel<kPsfErf>(const BandParams);
 template __global__ void fused_generate_kernel<1, kPsfErf>(const FusedParams);
 
 // ----------------------------------------------------------------------------
@@ -268,6 +214,9 @@ struct DevWork {
   void* ctl = nullptr;        // ticket + slots + fills (memset per launch)
   size_t ctl_bytes = 0;
   int* overflow = nullptr;
+  // band generator workspace: ticket + pair headers + field bounds + cell prefixes
+  void* band = nullptr;
+  size_t band_bytes = 0;
   // host-API staging
   void* stage = nullptr;
   size_t stage_bytes = 0;
@@ -300,7 +249,7 @@ void* ensure(void*& buf, size_t& have, size_t need) {
 using KernelFn = void (*)(const FusedParams);
 
 KernelFn pick_kernel(int mode, int psf) {
-  if (mode == 0) return psf == kPsfErf ? fused_generate_kernel<0, kPsfErf> : fused_generate_kernel<0, kPsfPoint>;
+  (void)mode;
   return psf == kPsfErf ? fused_generate_kernel<1, kPsfErf> : fused_generate_kernel<1, kPsfPoint>;
 }
 
@@ -443,10 +392,154 @@ int guarded(F&& f) {
   return 1;
 }
 
+// ----------------------------------------------------------------------------
+// Band generator (band.cuh): plan + launch
+// ----------------------------------------------------------------------------
+struct BandPlan {
+  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx, cells_cap;
+  size_t smem;
+};
+
+// Seeding cells ~4 px on a side: largest s with 4 * 2^s <= n, total <= 2^14 cells.
+void cell_bits(int H, int W, int& sy, int& sx) {
+  auto bits = [](int n) { int s = 0; while ((4LL << (s + 1)) <= n) ++s; return s; };
+  sy = bits(H);
+  sx = bits(W);
+  while (sy + sx > kMaxCellBits) {
+    if (sx >= sy) --sx;
+    else --sy;
+  }
+}
+
+size_t band_acc_budget() {
+  int kb = 96;
+  if (const char* e = std::getenv("PGB_BAND_ACC_KB")) kb = std::max(8, std::atoi(e));
+  return (size_t)kb * 1024;
+}
+
+BandPlan make_band_plan(int H, int W, int halo) {
+  BandPlan p{};
+  cell_bits(H, W, p.sy, p.sx);
+  const size_t budget_ints = band_acc_budget() / 8;       // two frames of int32
+  const double m = halo + 4.0;                             // typical reach beyond the tile
+  int bestTW = 0, bestTH = 0;
+  double best = 1e30;
+  for (int tw = 4; ; tw *= 2) {
+    const int TW = std::min(tw, (W + 3) / 4 * 4);
+    const int AS = TW;
+    int THmax = (int)std::min<size_t>((size_t)H, budget_ints / AS);
+    if (THmax >= 1) {
+      const int ty = (H + THmax - 1) / THmax;
+      const int TH = (H + ty - 1) / ty;
+      const double cost = ((TH + 2 * m) * (TW + 2 * m)) / ((double)TH * TW);
+      if (cost < best - 1e-9) { best = cost; bestTW = TW; bestTH = TH; }
+    }
+    if (TW >= W) break;
+  }
+  PGB_REQUIRE(bestTW > 0, "band plan: image too large for the accumulator budget");
+  p.TW = bestTW;
+  p.AS = (bestTW + 3) / 4 * 4;
+  p.TH = bestTH;
+  p.tiles_y = (H + p.TH - 1) / p.TH;
+  p.tiles_x = (W + p.TW - 1) / p.TW;
+  p.tiles = p.tiles_y * p.tiles_x;
+  p.cells_cap = 2048;
+  p.smem = sizeof(BandShared) + (size_t)2 * p.TH * p.AS * 4 + (size_t)(3 * p.cells_cap + 4) * 4;
+  PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
+  return p;
+}
+
+using BandFn = void (*)(const BandParams);
+
+int band_resident_ctas(BandFn fn, size_t smem) {
+  static std::map<std::tuple<void*, size_t, int>, int> cache;
+  int dev = 0;
+  PGB_CK(cudaGetDevice(&dev));
+  auto key = std::make_tuple((void*)fn, smem, dev);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+  int per_sm = 0, sms = 0;
+  PGB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kBandThreads, smem));
+  PGB_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PGB_REQUIRE(per_sm > 0, "band kernel configuration cannot be scheduled");
+  cache[key] = per_sm * sms;
+  return per_sm * sms;
+}
+
+float amp_bound_of(const pgb_config* c) {
+  double a = c->i0_hi;
+  if (c->f2_i0_std > 0.0) a = std::max(a, 1.0);
+  if (c->laser_enabled) a *= c->laser_q;
+  return (float)(std::max(a, 1e-30) * (1.0 + 1e-6));
+}
+
+// Fill the band parameters shared by generate / sample_particles and run the
+// prologue (densities, maximum diameters, cell prefixes, field bounds).
+void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uint64_t batch,
+                   int64_t pair_base, int pairs, const float* flows, int num_fields,
+                   int pairs_per_field, const pgb_pair_stats* stats, cudaStream_t stream) {
+  P.H = cfg->height;
+  P.W = cfg->width;
+  P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS;
+  P.tiles_y = bp.tiles_y; P.tiles_x = bp.tiles_x; P.tiles = bp.tiles;
+  P.sy = bp.sy; P.sx = bp.sx; P.cells_cap = bp.cells_cap;
+  P.n = cfg->n_capacity;
+  P.pairs = pairs;
+  P.pair_base = pair_base;
+  P.batch_lo = (uint32_t)batch;
+  P.psf = cfg->psf;
+  P.g = gen_cfg_from(cfg);
+  P.amp_bound = amp_bound_of(cfg);
+  P.flows = reinterpret_cast<const float2*>(flows);
+  P.num_fields = num_fields;
+  P.pairs_per_field = pairs_per_field;
+  P.field_elems = (long long)cfg->height * cfg->width;
+  P.out_pair_elems = (long long)cfg->height * cfg->width;
+  if (stats) {
+    P.st_ppp = stats->seeding_density;
+    P.st_M = stats->active_count;
+    P.st_side = stats->side;
+    P.st_dmax = stats->d_max;
+  }
+  const int ncell = 1 << (bp.sy + bp.sx);
+  const size_t hdr_bytes = (size_t)pairs * sizeof(PairHdr);
+  const size_t fb_bytes = (size_t)num_fields * sizeof(float2);
+  const size_t pre_bytes = (size_t)pairs * (ncell + 1) * sizeof(int);
+  auto up = [](size_t v) { return (v + 255) / 256 * 256; };
+  DevWork& w = work_for_current();
+  // [ticket | field bounds] are zeroed per launch, then headers and prefixes
+  const size_t head = 256 + up(fb_bytes);
+  char* b = static_cast<char*>(ensure(w.band, w.band_bytes, head + up(hdr_bytes) + up(pre_bytes)));
+  P.ticket = reinterpret_cast<int*>(b);
+  P.fbound = reinterpret_cast<float2*>(b + 256);
+  P.hdr = reinterpret_cast<PairHdr*>(b + head);
+  P.prefix = reinterpret_cast<int*>(b + head + up(hdr_bytes));
+  PGB_CK(cudaMemsetAsync(b, 0, head, stream));
+  // bounds only for the fields this pair range reads
+  const int f_lo = (int)(pair_base / pairs_per_field);
+  const int f_hi = (int)((pair_base + pairs - 1) / pairs_per_field);
+  BandParams Q = P;
+  const size_t psmem = (size_t)ncell * sizeof(int) + 16;
+  static bool attr_set = false;
+  if (!attr_set) {
+    PGB_CK(cudaFuncSetAttribute((const void*)prologue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kSmemMax));
+    attr_set = true;
+  }
+  // field blocks handle absolute field f_lo + (block - pairs) / kFieldBlocks
+  Q.flows = P.flows + (size_t)f_lo * P.field_elems;
+  Q.fbound = P.fbound + f_lo;
+  prologue_kernel<<<pairs + (f_hi - f_lo + 1) * kFieldBlocks, kPrologueThreads, psmem, stream>>>(Q);
+  g_launches.fetch_add(1);
+  PGB_CK(cudaGetLastError());
+}
+
 void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
                        const float* flows, int num_fields, int pairs_per_field, int out_mode,
                        void* img1, void* img2, const pgb_pair_stats* stats, int32_t* bin_counts,
                        cudaStream_t stream) {
+  (void)bin_counts;  // generate mode renders without record lists
   validate_cfg(cfg);
   PGB_REQUIRE(pairs >= 0, "pairs must be >= 0");
   PGB_REQUIRE(flows != nullptr && num_fields >= 1 && pairs_per_field >= 1, "flows required");
@@ -456,34 +549,22 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   PGB_REQUIRE(batch < (1ull << 32), "batch index must be < 2^32");
   PGB_REQUIRE((int64_t)(pair_base + pairs) <= (int64_t)num_fields * pairs_per_field,
               "pair range exceeds the flow window (num_fields * pairs_per_field)");
+  if (pairs == 0) return;
   const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
-  FusedParams P = base_params(cfg->height, cfg->width);
-  P.n = cfg->n_capacity;
-  P.pairs = pairs;
-  P.pair_base = pair_base;
-  P.batch_lo = (uint32_t)batch;
-  P.psf = cfg->psf;
+  const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
+  BandParams P{};
+  band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats, stream);
   P.out_mode = out_mode;
   P.bg_offset = (float)cfg->bg_offset;
   P.noise_std = (float)cfg->noise_std;
-  P.mode = 0;
-  P.nframes = 2;
-  P.g = gen_cfg_from(cfg);
-  P.flows = reinterpret_cast<const float2*>(flows);
-  P.num_fields = num_fields;
-  P.pairs_per_field = pairs_per_field;
-  P.field_elems = (long long)cfg->height * cfg->width;
   P.out[0] = img1;
   P.out[1] = img2;
-  if (stats) {
-    P.st_ppp = stats->seeding_density;
-    P.st_M = stats->active_count;
-    P.st_side = stats->side;
-    P.st_dmax = stats->d_max;
-  }
-  P.bin_counts = bin_counts;
-  const Plan pl = make_plan(cfg->height, cfg->height, cfg->width, cfg->n_capacity, halo, 2);
-  launch_fused(P, pl, stream);
+  BandFn fn = cfg->psf == PGB_PSF_ERF ? band_kernel<kPsfErf> : band_kernel<kPsfPoint>;
+  const int ctas = band_resident_ctas(fn, bp.smem);
+  const long long items = (long long)pairs * bp.tiles;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(ctas, items));
+  fn<<<grid, kBandThreads, bp.smem, stream>>>(P);
+  g_launches.fetch_add(1);
 }
 
 }  // namespace pgb
@@ -755,24 +836,15 @@ int pgb_sample_particles_dev(const pgb_config* cfg, uint64_t batch, int64_t pair
     validate_cfg(cfg);
     PGB_REQUIRE(out != nullptr, "out is NULL");
     PGB_REQUIRE(flows != nullptr && num_fields >= 1 && pairs_per_field >= 1, "flows required");
+    PGB_REQUIRE((int64_t)(pair_base + pairs) <= (int64_t)num_fields * pairs_per_field,
+                "pair range exceeds the flow window (num_fields * pairs_per_field)");
     if (pairs <= 0) return;
-    FusedParams P = base_params(cfg->height, cfg->width);
-    P.n = cfg->n_capacity;
-    P.pairs = pairs;
-    P.pair_base = pair_base;
-    P.batch_lo = (uint32_t)batch;
-    P.g = gen_cfg_from(cfg);
-    P.flows = reinterpret_cast<const float2*>(flows);
-    P.num_fields = num_fields;
-    P.pairs_per_field = pairs_per_field;
-    P.field_elems = (long long)cfg->height * cfg->width;
-    if (stats) {
-      P.st_ppp = stats->seeding_density;
-      P.st_M = stats->active_count;
-      P.st_side = stats->side;
-      P.st_dmax = stats->d_max;
-    }
-    sample_particles_kernel<<<pairs, 256, 0, (cudaStream_t)stream>>>(P, *out);
+    const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
+    const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
+    BandParams P{};
+    band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats,
+                  (cudaStream_t)stream);
+    sample_band_kernel<<<pairs, 256, 0, (cudaStream_t)stream>>>(P, *out);
     g_launches.fetch_add(1);
     PGB_CK(cudaGetLastError());
   });

@@ -194,10 +194,10 @@ def test_functional_layer_roundtrip(pg):
     pg.apply_hiding(key, ps, cfg.hide_probability)
     side = pg.patch_side(float(params.diameters[:params.active_count].max()))
     r1, r2 = pg.render_pair(ps, 64, 64, side, cfg.noise, None, key)
-    # the Sampler renders the same pair: frame 1 bit-identically; frame 2 to
-    # float32 rounding (functional advect is the reference's float64
-    # arithmetic, the fused kernel advects in fixed point + float32)
+    # the Sampler renders the same pair (same particles; the band kernel picks
+    # its own fixed-point scale, and functional advect is the reference's
+    # float64 arithmetic while the generator advects in fixed point + float32)
     with pg.make_sampler(pg.with_updates(cfg, batch_size=2)) as s:
         b = next(s)
-    np.testing.assert_array_equal(b.images1[1].cpu().numpy(), r1)
+    np.testing.assert_allclose(b.images1[1].cpu().numpy(), r1, atol=1e-5)
     np.testing.assert_allclose(b.images2[1].cpu().numpy(), r2, atol=1e-5)

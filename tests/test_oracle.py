@@ -177,3 +177,36 @@ def test_oracle_generation_restatement_is_self_consistent():
     mine = orr.splat(a["pos1"], a["i0_1"], a["sx_1"], a["sy_1"], a["rho_1"], a["on1"], a["side"], 64, 64)
     np.testing.assert_array_equal(ref_img, mine)
     assert pv.active_backend() == "native"
+
+
+def test_reproducible_log_exp():
+    rng = np.random.default_rng(3)
+    for v in np.concatenate([rng.uniform(0, 1, 2000), [2.0 ** -53, 0.5, 1.0 - 2.0 ** -53, 0.7071067811865476]]):
+        assert abs(og.rlog(float(v)) - math.log(v)) <= 1e-14 * max(1.0, abs(math.log(v)))
+    for y in np.concatenate([rng.uniform(-40, 0, 2000), [0.0, -1e-12]]):
+        assert abs(og.rexp(float(y)) - math.exp(y)) <= 1e-14 * math.exp(y)
+
+
+def test_stratified_seeding_law():
+    # cell histogram sums to M; positions are uniform (chi-square on 8x8 bins);
+    # the maximum diameter sits on particle J and bounds every other particle
+    cfg = og.GenConfig(height=96, width=128, seed=11, ppp_range=(0.2, 0.2), d_range=(0.5, 3.0))
+    flow = np.zeros((96, 128, 2), np.float32)
+    xs, ys = [], []
+    for p in range(4):
+        o = og.sample_pair(cfg, 0, p, flow)
+        m = o["M"]
+        assert o["prefix"][-1] == m
+        d = o["diameter"][:m]
+        assert d.max() == np.float32(o["d_max"]) and (d <= o["d_max"]).all()
+        xs.append(o["pos1"][:m, 0])
+        ys.append(o["pos1"][:m, 1])
+    x, y = np.concatenate(xs), np.concatenate(ys)
+    assert x.min() > 0 and x.max() < 128 and y.min() > 0 and y.max() < 96
+    hist, _, _ = np.histogram2d(y, x, bins=8, range=((0, 96), (0, 128)))
+    e = x.size / 64
+    chi2 = ((hist - e) ** 2 / e).sum()
+    assert chi2 < 120          # 63 dof: p ~ 1e-5
+    # diameters below the maximum are uniform on [d_lo, d_max]
+    dd = np.concatenate([og.sample_pair(cfg, 1, p, flow)["diameter"][:100] for p in range(20)])
+    assert 0.4 < (dd < 1.75).mean() < 0.6
