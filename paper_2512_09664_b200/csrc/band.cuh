@@ -348,105 +348,173 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
 // ----------------------------------------------------------------------------
 // Band kernel
 // ----------------------------------------------------------------------------
-struct __align__(16) BandShared {
-  int item;
-  int pad[3];
-  int wsum[kBandWarps];
+// Per-item parameters, computed once by thread 0 and broadcast.
+struct ItemCfg {
+  int pl, r0, r1, c0, c1;
+  int cy0, cx0, rw, ncell;
+  int h, wt, shift, field;
+  PairHdr hd;
 };
 
-// One frame of one particle into the tile accumulator (tight window clipped
-// to the patch half-width h and to the tile).
-template <int PSF>
-__device__ __forceinline__ void splat_one(int* __restrict__ acc, int AS, int ax, int ay, float fx,
-                                          float fy, float amp, float sx, float sy, float rho, int h,
-                                          int r0, int r1, int c0, int c1, int shift, float scale) {
-  Frame fr;
-  fr.ax = ax; fr.ay = ay; fr.fx = fx; fr.fy = fy; fr.amp = amp; fr.sx = sx; fr.sy = sy; fr.rho = rho;
-  const float R = record_radius(fr, PSF);
+struct __align__(16) BandShared {
+  long long item;
+  int pad[2];
+  int wsum[kBandWarps];
+  ItemCfg ic;
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Tight window of one particle-frame (anchor offsets clipped to +-h), then
+// clipped to the tile [r0, r1) x [c0, c1). Returns false when empty.
+__device__ __forceinline__ bool tile_window(int ax, int ay, float fx, float fy, float R, int h, int r0,
+                                            int r1, int c0, int c1, int& rlo, int& clo, int& nr,
+                                            int& nc) {
   const int jlo = max(-h, (int)ceilf(__fsub_rn(fx, R)));
   const int jhi = min(h, (int)floorf(__fadd_rn(fx, R)));
   const int ilo = max(-h, (int)ceilf(__fsub_rn(fy, R)));
   const int ihi = min(h, (int)floorf(__fadd_rn(fy, R)));
-  const int rlo = max(ay + ilo, r0), rhi = min(ay + ihi, r1 - 1);
-  const int clo = max(ax + jlo, c0), chi = min(ax + jhi, c1 - 1);
-  if (rlo > rhi || clo > chi) return;
-  const int nr = rhi - rlo + 1, nc = chi - clo + 1;
+  rlo = max(ay + ilo, r0);
+  const int rhi = min(ay + ihi, r1 - 1);
+  clo = max(ax + jlo, c0);
+  const int chi = min(ax + jhi, c1 - 1);
+  nr = rhi - rlo + 1;
+  nc = chi - clo + 1;
+  return nr > 0 && nc > 0;
+}
+
+// Point PSF, one particle-frame (one lane): WM = compile-time bound of the
+// window side (columns and rows fully unrolled, predicated), 0 = dynamic.
+// value * 2^s = exp2(Ls - A dx^2 - B dx dy - C dy^2), rounded to an integer.
+template <int WM>
+__device__ __forceinline__ void splat_point(int* __restrict__ acc, int AS, int ax, int ay, float fx,
+                                            float fy, float amp, float sx, float sy, float rho, int h,
+                                            int r0, int r1, int c0, int c1, int shift) {
+  const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
+  int rlo, clo, nr, nc;
+  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return;
   const float dx0 = (float)(clo - ax) - fx;
   const float dy0 = (float)(rlo - ay) - fy;
   int* base = acc + (rlo - r0) * AS + (clo - c0);
-  if (PSF == kPsfPoint) {
-    const float q = 1.0f - rho * rho;
-    const float isx = __frcp_rn(sx), isy = __frcp_rn(sy), iq = __frcp_rn(q);
-    const float A = (0.5f * kLog2e) * iq * isx * isx;
-    const float C = (0.5f * kLog2e) * iq * isy * isy;
-    const float B = -kLog2e * rho * iq * isx * isy;
-    const float Ls = __log2f(amp) + (float)shift;
+  const float isx = rcp_approx(sx), isy = rcp_approx(sy);
+  const float iq = rcp_approx(1.0f - rho * rho);
+  const float A = (0.5f * kLog2e) * iq * isx * isx;
+  const float C = (0.5f * kLog2e) * iq * isy * isy;
+  const float B = -kLog2e * rho * iq * isx * isy;
+  const float Ls = __log2f(amp) + (float)shift;
+  if (WM > 0) {
+    // pixels beyond the bound lie outside the tight radius (they round to 0)
+    nr = min(nr, WM);
+    nc = min(nc, WM);
+    float ct[WM > 0 ? WM : 1], bx[WM > 0 ? WM : 1];
+#pragma unroll
+    for (int j = 0; j < WM; ++j) {
+      const float dx = dx0 + (float)j;
+      ct[j] = fmaf(-A * dx, dx, Ls);
+      bx[j] = B * dx;
+    }
+#pragma unroll
+    for (int i = 0; i < WM; ++i) {
+      if (i < nr) {
+        const float dy = dy0 + (float)i;
+        const float rt = -C * dy * dy;
+        int* row = base + i * AS;
+#pragma unroll
+        for (int j = 0; j < WM; ++j)
+          if (j < nc) atomicAdd(row + j, round_small(ex2_approx(fmaf(-bx[j], dy, ct[j] + rt))));
+      }
+    }
+  } else {
     for (int i = 0; i < nr; ++i) {
       const float dy = dy0 + (float)i;
       const float bt = B * dy;
       const float rt = fmaf(-C * dy, dy, Ls);
       int* row = base + i * AS;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j < nc) {
-          const float dx = dx0 + (float)j;
-          const float e = fmaf(-dx, fmaf(A, dx, bt), rt);
-          atomicAdd(row + j, round_small(ex2_approx(e)));
-        }
-      }
-      for (int j = 4; j < nc; ++j) {
-        const float dx = dx0 + (float)j;
-        const float e = fmaf(-dx, fmaf(A, dx, bt), rt);
-        atomicAdd(row + j, round_small(ex2_approx(e)));
-      }
-    }
-  } else {
-    // pixel-area mean of Eq. (1) (oracle/render.py render_erf)
-    const float k = 1.2533141373155001f;  // sqrt(pi/2)
-    const float sc = sx * sqrtf(fmaxf(1.0f - rho * rho, 0.f));
-    const bool sep = rho == 0.f;
-    const float Lm = (sep ? amp * (k * sx) * (k * sy) : amp * (k * sc)) * scale;
-    const float rA = 0.70710678118654752f / sc;
-    const float rB = 0.70710678118654752f / sy;
-    const float rC = sep ? 0.f : rho * sx / sy;
-    for (int i = 0; i < nr; ++i) {
-      const float dy = dy0 + (float)i;
-      const float ey = sep ? erff((dy + 0.5f) * rB) - erff((dy - 0.5f) * rB) : 0.f;
       for (int j = 0; j < nc; ++j) {
         const float dx = dx0 + (float)j;
-        float val;
-        if (sep) {
-          val = (erff((dx + 0.5f) * rA) - erff((dx - 0.5f) * rA)) * ey;
-        } else {
-          float s = 0.f;
-#pragma unroll
-          for (int gq = 0; gq < kGLPoints; ++gq) {
-            const float yy = dy + kGLx[gq];
-            const float mu = rC * yy;
-            const float gy = __expf(-yy * yy * (rB * rB));
-            const float hi = erff((dx + 0.5f - mu) * rA);
-            const float lo = erff((dx - 0.5f - mu) * rA);
-            s = fmaf(kGLw[gq] * gy, hi - lo, s);
-          }
-          val = s;
-        }
-        const int qv = __float2int_rn(val * Lm);
-        if (qv) atomicAdd(base + i * AS + j, qv);
+        atomicAdd(row + j, round_small(ex2_approx(fmaf(-dx, fmaf(A, dx, bt), rt))));
       }
     }
   }
 }
 
-// Epilogue: one output quad (4 pixels) of frame f.
-template <int OUT, bool NOISE>
-__device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, char* dst, size_t pix,
-                                                int f, uint32_t gpair, float inv_scale) {
-  float4 v;
-  if ((a.x | a.y | a.z | a.w) >= (1 << 23)) {
-    v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
-  } else {
-    v = make_float4(acc_to_float(a.x), acc_to_float(a.y), acc_to_float(a.z), acc_to_float(a.w));
+// Pixel-area mean of Eq. (1) (oracle/render.py render_erf), one particle-frame.
+__device__ __forceinline__ void splat_erf(int* __restrict__ acc, int AS, int ax, int ay, float fx,
+                                          float fy, float amp, float sx, float sy, float rho, int h,
+                                          int r0, int r1, int c0, int c1, float scale) {
+  const float R = __fadd_rn(__fmul_rn(fmaxf(sx, sy), kTightR), 0.5f);
+  int rlo, clo, nr, nc;
+  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return;
+  const float dx0 = (float)(clo - ax) - fx;
+  const float dy0 = (float)(rlo - ay) - fy;
+  int* base = acc + (rlo - r0) * AS + (clo - c0);
+  const float k = 1.2533141373155001f;  // sqrt(pi/2)
+  const float sc = sx * sqrtf(fmaxf(1.0f - rho * rho, 0.f));
+  const bool sep = rho == 0.f;
+  const float Lm = (sep ? amp * (k * sx) * (k * sy) : amp * (k * sc)) * scale;
+  const float rA = 0.70710678118654752f / sc;
+  const float rB = 0.70710678118654752f / sy;
+  const float rC = sep ? 0.f : rho * sx / sy;
+  for (int i = 0; i < nr; ++i) {
+    const float dy = dy0 + (float)i;
+    const float ey = sep ? erff((dy + 0.5f) * rB) - erff((dy - 0.5f) * rB) : 0.f;
+    for (int j = 0; j < nc; ++j) {
+      const float dx = dx0 + (float)j;
+      float val;
+      if (sep) {
+        val = (erff((dx + 0.5f) * rA) - erff((dx - 0.5f) * rA)) * ey;
+      } else {
+        float s = 0.f;
+#pragma unroll
+        for (int gq = 0; gq < kGLPoints; ++gq) {
+          const float yy = dy + kGLx[gq];
+          const float mu = rC * yy;
+          const float gy = __expf(-yy * yy * (rB * rB));
+          const float hi = erff((dx + 0.5f - mu) * rA);
+          const float lo = erff((dx - 0.5f - mu) * rA);
+          s = fmaf(kGLw[gq] * gy, hi - lo, s);
+        }
+        val = s;
+      }
+      const int qv = __float2int_rn(val * Lm);
+      if (qv) atomicAdd(base + i * AS + j, qv);
+    }
   }
+}
+
+template <int PSF>
+__device__ __forceinline__ void splat_dispatch_b(int wt, int* acc, int AS, int ax, int ay, float fx,
+                                                 float fy, float amp, float sx, float sy, float rho,
+                                                 int h, int r0, int r1, int c0, int c1, int shift,
+                                                 float scale) {
+  if (PSF == kPsfErf) {
+    splat_erf(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, scale);
+    return;
+  }
+#define PGB_SP(WW) splat_point<WW>(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, shift)
+  switch (wt) {   // warp-uniform (per item)
+    case 1: PGB_SP(1); return;
+    case 2: PGB_SP(2); return;
+    case 3: PGB_SP(3); return;
+    case 4: PGB_SP(4); return;
+    case 5: PGB_SP(5); return;
+    case 6: PGB_SP(6); return;
+    case 7: PGB_SP(7); return;
+    default: PGB_SP(0); return;
+  }
+#undef PGB_SP
+}
+
+// Epilogue: one output quad (4 pixels) of frame f. (float)a is exact below
+// 2^24 and correctly rounded above (the accumulator stays < 2^31).
+template <int OUT, bool NOISE>
+__device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, char* dst, uint32_t pix,
+                                                int f, uint32_t gpair, float inv_scale) {
+  float4 v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
   if (OUT == kOutRaw) {
     v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
     __stcs(reinterpret_cast<float4*>(dst), v);
@@ -455,7 +523,7 @@ __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, cha
   const float bg = P.bg_offset;
   if (NOISE) {
     const float sd = P.noise_std;
-    const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(pix >> 2));
+    const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, pix >> 2);
     v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
     v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
     v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
@@ -475,28 +543,44 @@ __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, cha
 }
 
 // Store one frame of the tile and zero its accumulator (quad path: tile
-// columns, image width and tile origin multiples of 4).
+// columns, image width and tile origin multiples of 4). Each thread walks its
+// quads with incremental row/column/pointer updates (no per-quad division or
+// 64-bit index arithmetic).
 template <int OUT, bool NOISE>
 __device__ void band_store_vec(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
                                int nr, int c0, int nc, float inv_scale) {
   constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
   const int qpr = nc >> 2;
-  const int total = nr * qpr;
-  char* outb = static_cast<char*>(P.out[f]) + (size_t)pl * (size_t)P.out_pair_elems * ESZ;
-  if (total <= 0) return;
-  // incremental (row, quad) walk: two divisions per call, none per quad
-  int row = threadIdx.x / qpr, cq = threadIdx.x - (threadIdx.x / qpr) * qpr;
+  if (nr <= 0 || qpr <= 0) return;
+  const int tid = threadIdx.x;
+  int row = tid / qpr, cq = tid - (tid / qpr) * qpr;
   const int drow = kBandThreads / qpr, dcq = kBandThreads - drow * qpr;
-  for (int e = threadIdx.x; e < total; e += kBandThreads) {
-    int4* ap = reinterpret_cast<int4*>(acc + row * P.AS + cq * 4);
+  const int W = P.W, AS = P.AS;
+  uint32_t pix = (uint32_t)((r0 + row) * W + c0 + cq * 4);
+  int ao = row * AS + cq * 4;
+  char* dst = static_cast<char*>(P.out[f]) + ((size_t)pl * (size_t)P.out_pair_elems + pix) * ESZ;
+  const uint32_t dpix = (uint32_t)(drow * W + dcq * 4);
+  const int dao = drow * AS + dcq * 4;
+  const uint32_t wrap_pix = (uint32_t)(W - qpr * 4);
+  const int wrap_ao = AS - qpr * 4;
+  while (row < nr) {
+    int4* ap = reinterpret_cast<int4*>(acc + ao);
     const int4 a = *ap;
     *ap = make_int4(0, 0, 0, 0);
-    const size_t pix = (size_t)(r0 + row) * P.W + (size_t)(c0 + cq * 4);
-    band_store_quad<OUT, NOISE>(P, a, outb + pix * ESZ, pix, f, gpair, inv_scale);
+    band_store_quad<OUT, NOISE>(P, a, dst, pix, f, gpair, inv_scale);
     row += drow;
     cq += dcq;
-    if (cq >= qpr) { cq -= qpr; ++row; }
+    pix += dpix;
+    ao += dao;
+    dst += (size_t)dpix * ESZ;
+    if (cq >= qpr) {
+      cq -= qpr;
+      ++row;
+      pix += wrap_pix;
+      ao += wrap_ao;
+      dst += (size_t)wrap_pix * ESZ;
+    }
   }
 }
 
@@ -558,6 +642,54 @@ __device__ __forceinline__ void cell_range(double a, double b, double s, int n, 
   hi = (int)fmin(fmax(fb, 0.0), (double)(n - 1));
 }
 
+// Item parameters (thread 0): tile, the cells whose particles can reach it,
+// the fixed-point shift and the window bound.
+__device__ __forceinline__ void item_setup(const BandParams& P, long long item, ItemCfg& ic) {
+  const GenCfg& g = P.g;
+  const int CY = 1 << P.sy, CX = 1 << P.sx;
+  const double ch = (double)g.H / (double)CY, cw = (double)g.W / (double)CX;
+  const int pl = (int)(item / P.tiles);
+  const int t = (int)(item - (long long)pl * P.tiles);
+  const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
+  ic.pl = pl;
+  ic.r0 = ty * P.TH;
+  ic.r1 = min(ic.r0 + P.TH, g.H);
+  ic.c0 = tx * P.TW;
+  ic.c1 = min(ic.c0 + P.TW, g.W);
+  ic.hd = P.hdr[pl];
+  const int h = ic.hd.side >> 1;
+  ic.h = h;
+  ic.field = (int)((P.pair_base + pl) / P.pairs_per_field);
+  const float2 fb = P.fbound[ic.field];
+  // frame-1 positions that can reach the tile in either frame: anchors within
+  // h of the tile (frame 1), or within h + 1 + max|v| (frame 2: the anchor
+  // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
+  const double vy = (double)fb.y * (1.0 + 1e-6) + 1e-6;
+  const double vx = (double)fb.x * (1.0 + 1e-6) + 1e-6;
+  int cy0, cy1, cx0, cx1;
+  cell_range((double)ic.r0 - h - 1.5 - vy, (double)ic.r1 + h + 0.5 + vy, ch, CY, cy0, cy1);
+  cell_range((double)ic.c0 - h - 1.5 - vx, (double)ic.c1 + h + 0.5 + vx, cw, CX, cx0, cx1);
+  ic.cy0 = cy0;
+  ic.cx0 = cx0;
+  ic.rw = cx1 - cx0 + 1;
+  ic.ncell = (cy1 - cy0 + 1) * ic.rw;
+  // fixed-point shift: contributions per pixel <= cmax * (cells one pixel's
+  // source box can meet), amplitude <= amp_bound
+  const double by = floor((2.0 * h + 3.0 + 2.0 * vy) / ch) + 2.0;
+  const double bx = floor((2.0 * h + 3.0 + 2.0 * vx) / cw) + 2.0;
+  const double cov = fmin((double)ic.hd.M, (double)ic.hd.cmax * fmin(by, (double)CY) * fmin(bx, (double)CX));
+  ic.shift = shift_for(max(1, (int)cov), P.amp_bound);
+  // window side bound: floor(2 R_max) + 1 columns/rows, R_max from the largest
+  // sigma (frame-2 sigma jitter is unbounded -> patch side)
+  int wt = 2 * h + 1;
+  if (P.psf == kPsfPoint && !(g.f2_sigma_std > 0.f)) {
+    const float smax = __fmul_rn(ic.hd.M > 0 ? ic.hd.dmax : (float)g.d_hi, g.inv_ratio);
+    const float Rm = __fmul_rn(smax, kTightR);
+    wt = min(wt, (int)floorf(2.0f * Rm) + 1);
+  }
+  ic.wt = max(1, wt);
+}
+
 template <int PSF>
 __global__ void __launch_bounds__(kBandThreads, 2) band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -569,44 +701,27 @@ __global__ void __launch_bounds__(kBandThreads, 2) band_kernel(const BandParams 
   int* cOff = cC + P.cells_cap;
   const int tid = threadIdx.x;
   const GenCfg& g = P.g;
-  const int CY = 1 << P.sy, CX = 1 << P.sx;
-  const double ch = (double)g.H / (double)CY, cw = (double)g.W / (double)CX;
+  const int CX = 1 << P.sx;
   const long long total_items = (long long)P.pairs * P.tiles;
   for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandThreads)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
   for (;;) {
-    if (tid == 0) sh->item = atomicAdd(P.ticket, 1);
+    if (tid == 0) {
+      const long long item = atomicAdd(P.ticket, 1);
+      sh->item = item;
+      if (item < total_items) item_setup(P, item, sh->ic);
+    }
     __syncthreads();
-    const long long item = sh->item;
-    if (item >= total_items) break;
-    const int pl = (int)(item / P.tiles);
-    const int t = (int)(item - (long long)pl * P.tiles);
-    const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
-    const int r0 = ty * P.TH, r1 = min(r0 + P.TH, g.H);
-    const int c0 = tx * P.TW, c1 = min(c0 + P.TW, g.W);
-    const PairHdr hd = P.hdr[pl];
-    const int h = hd.side >> 1;
-    const int field = (int)((P.pair_base + pl) / P.pairs_per_field);
-    const float2* flow = P.flows + (size_t)field * P.field_elems;
-    const float2 fb = P.fbound[field];
-    // frame-1 positions that can reach the tile in either frame: anchors within
-    // h of the tile (frame 1), or within h + 1 + max|v| (frame 2: the anchor
-    // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
-    const double vy = (double)fb.y * (1.0 + 1e-6) + 1e-6;
-    const double vx = (double)fb.x * (1.0 + 1e-6) + 1e-6;
-    int cy0, cy1, cx0, cx1;
-    cell_range((double)r0 - h - 1.5 - vy, (double)r1 + h + 0.5 + vy, ch, CY, cy0, cy1);
-    cell_range((double)c0 - h - 1.5 - vx, (double)c1 + h + 0.5 + vx, cw, CX, cx0, cx1);
-    // fixed-point shift: contributions per pixel <= cmax * (cells one pixel's
-    // source box can meet), amplitude <= amp_bound
-    const double by = floor((2.0 * h + 3.0 + 2.0 * vy) / ch) + 2.0;
-    const double bx = floor((2.0 * h + 3.0 + 2.0 * vx) / cw) + 2.0;
-    const double cov = fmin((double)hd.M, (double)hd.cmax * fmin(by, (double)CY) * fmin(bx, (double)CX));
-    const int shift = shift_for(max(1, (int)cov), P.amp_bound);
+    if (sh->item >= total_items) break;
+    const ItemCfg& ic = sh->ic;
+    const int pl = ic.pl;
+    const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
+    const int h = ic.h, wt = ic.wt, shift = ic.shift;
+    const int rw = ic.rw, ncell = ic.ncell, cy0 = ic.cy0, cx0 = ic.cx0;
+    const PairHdr& hd = ic.hd;
     const float scale = (float)(1 << shift);
-    const int rw = cx1 - cx0 + 1;
-    const int ncell = (cy1 - cy0 + 1) * rw;
-    const int* pre = P.prefix + (size_t)pl * ((size_t)CY * CX + 1);
+    const float2* flow = P.flows + (size_t)ic.field * P.field_elems;
+    const int* pre = P.prefix + (size_t)pl * ((size_t)(1 << P.sy) * CX + 1);
     const RngKey key = band_key(P, pl);
     for (int cb = 0; cb < ncell; cb += P.cells_cap) {
       const int cnt = min(P.cells_cap, ncell - cb);
@@ -633,40 +748,39 @@ __global__ void __launch_bounds__(kBandThreads, 2) band_kernel(const BandParams 
       for (int qb = 0; qb < N; qb += kBandThreads) {
         const int q = qb + tid;
         if (q < N) {
-        // cell k: largest k with cOff[k] <= q
-        int lo = 0, hi = cnt - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (cOff[mid] <= q) lo = mid;
-          else hi = mid - 1;
-        }
-        const int gi = cP[lo] + (q - cOff[lo]);
-        const int cc = cC[lo];
-        const int cyy = cc >> P.sx, cxx = cc & (CX - 1);
-        const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
-        const uint64_t X = cell_coord((uint32_t)cxx, a.x, g.W, P.sx);
-        const uint64_t Y = cell_coord((uint32_t)cyy, a.y, g.H, P.sy);
-        int ax1, ay1, ax2, ay2;
-        float fx1, fy1, fx2, fy2;
-        fixed_anchor(X, ax1, fx1);
-        fixed_anchor(Y, ay1, fy1);
-        advect_fixed(g, flow, X, Y, ax1, fx1, ay1, fy1, ax2, fx2, ay2, fy2);
-        // geometric pre-test with the full patch window
-        const bool in1 = ay1 + h >= r0 && ay1 - h < r1 && ax1 + h >= c0 && ax1 - h < c1;
-        const bool in2 = ay2 + h >= r0 && ay2 - h < r1 && ax2 + h >= c0 && ax2 - h < c1;
-        if (in1 || in2) {
-        const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
-        const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
-        const float sig = __fmul_rn(d, g.inv_ratio);
-        Look lk;
-        seed_look(g, key, gi, sig, i0, lk);
-        if (in1 && lk.vis1 && lk.amp1 > 0.f)
-          splat_one<PSF>(acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1, h, r0, r1, c0, c1,
-                         shift, scale);
-        if (in2 && lk.vis2 && lk.amp2 > 0.f)
-          splat_one<PSF>(acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2, lk.rho2, h, r0, r1,
-                         c0, c1, shift, scale);
-        }
+          // cell k: largest k with cOff[k] <= q
+          int lo = 0, hi = cnt - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cOff[mid] <= q) lo = mid;
+            else hi = mid - 1;
+          }
+          const int gi = cP[lo] + (q - cOff[lo]);
+          const int cc = cC[lo];
+          const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
+          const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
+          const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
+          int ax1, ay1, ax2, ay2;
+          float fx1, fy1, fx2, fy2;
+          fixed_anchor(X, ax1, fx1);
+          fixed_anchor(Y, ay1, fy1);
+          advect_fixed(g, flow, X, Y, ax1, fx1, ay1, fy1, ax2, fx2, ay2, fy2);
+          // geometric pre-test with the full patch window
+          const bool in1 = ay1 + h >= r0 && ay1 - h < r1 && ax1 + h >= c0 && ax1 - h < c1;
+          const bool in2 = ay2 + h >= r0 && ay2 - h < r1 && ax2 + h >= c0 && ax2 - h < c1;
+          if (in1 || in2) {
+            const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
+            const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
+            const float sig = __fmul_rn(d, g.inv_ratio);
+            Look lk;
+            seed_look(g, key, gi, sig, i0, lk);
+            if (in1 && lk.vis1 && lk.amp1 > 0.f)
+              splat_dispatch_b<PSF>(wt, acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1, h,
+                                    r0, r1, c0, c1, shift, scale);
+            if (in2 && lk.vis2 && lk.amp2 > 0.f)
+              splat_dispatch_b<PSF>(wt, acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2, lk.rho2,
+                                    h, r0, r1, c0, c1, shift, scale);
+          }
         }
         __syncwarp();
       }

@@ -174,7 +174,8 @@ __device__ __forceinline__ void fixed_anchor(uint64_t F, int& a, float& f) {
   const uint64_t an = (F + (1ull << 32)) >> 33;
   a = (int)an;
   const long long diff = (long long)(F - (an << 33));
-  f = __double2float_rn((double)diff * 0x1p-33);
+  // one rounding (|diff| < 2^33): float(diff) * 2^-33 == float(diff * 2^-33)
+  f = __ll2float_rn(diff) * 0x1p-33f;
 }
 
 // Clamped bilinear cell: x = min(v, N-1), c = min(floor x, N-2), t = x - c.
@@ -185,7 +186,7 @@ __device__ __forceinline__ void fixed_cell(uint64_t F, int N, int& c, float& t) 
   const int cmax = N - 2 > 0 ? N - 2 : 0;
   cc = cc < cmax ? cc : cmax;
   c = cc;
-  t = __double2float_rn((double)(long long)(xc - ((uint64_t)cc << 33)) * 0x1p-33);
+  t = __ll2float_rn((long long)(xc - ((uint64_t)cc << 33))) * 0x1p-33f;
 }
 
 __device__ __forceinline__ float bilerp(float g00, float g01, float g10, float g11, float tx,
