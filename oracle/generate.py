@@ -171,6 +171,10 @@ def cell_bits(height: int, width: int):
     return sy, sx
 
 
+INV_ODD = [1.0 / float(2 * k + 1) for k in range(13)]
+INV_INT = [0.0] + [1.0 / float(i) for i in range(1, 17)]
+
+
 def rlog(x: float) -> float:
     """common.cuh rlog: only correctly rounded +,-,*,/ (bit-identical to the GPU)."""
     f, e = math.frexp(x)
@@ -179,19 +183,19 @@ def rlog(x: float) -> float:
         e -= 1
     s = (f - 1.0) / (f + 1.0)
     z = s * s
-    p = 1.0 / 25.0
+    p = INV_ODD[12]
     for k in range(11, -1, -1):
-        p = p * z + 1.0 / float(2 * k + 1)
+        p = p * z + INV_ODD[k]
     return float(e) * LN2 + 2.0 * (s * p)
 
 
 def rexp(y: float) -> float:
     """common.cuh rexp."""
-    k = float(round(y / LN2))          # round-half-even == rint
+    k = float(round(y * 1.4426950408889634))   # round-half-even == rint
     r = y - k * LN2
     p = 1.0
     for i in range(16, 0, -1):
-        p = 1.0 + (r * p) / float(i)
+        p = 1.0 + (r * p) * INV_INT[i]
     return math.ldexp(p, int(k))
 
 

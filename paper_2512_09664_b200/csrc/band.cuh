@@ -32,6 +32,9 @@
 
 namespace pgb {
 
+#ifndef PGB_BAND_MINB
+#define PGB_BAND_MINB 2
+#endif
 constexpr int kBandThreads = 256;
 constexpr int kBandWarps = kBandThreads / 32;
 constexpr int kMaxCellBits = 14;
@@ -53,6 +56,7 @@ struct BandParams {
   int TH, TW, AS, tiles_y, tiles_x, tiles;
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
   int cells_cap;               // cells per enumeration chunk (shared memory)
+  int map_cap;                 // particle -> cell map entries (shared memory)
   int n, pairs;
   long long pair_base;
   uint32_t batch_lo;
@@ -357,10 +361,9 @@ struct ItemCfg {
 };
 
 struct __align__(16) BandShared {
-  long long item;
-  int pad[2];
+  long long item[2];   // item[buf] mirrors the loop's item (kept for debugging)
   int wsum[kBandWarps];
-  ItemCfg ic;
+  ItemCfg ic[2];
 };
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -564,6 +567,17 @@ __device__ void band_store_vec(const BandParams& P, int* __restrict__ acc, int p
   const int dao = drow * AS + dcq * 4;
   const uint32_t wrap_pix = (uint32_t)(W - qpr * 4);
   const int wrap_ao = AS - qpr * 4;
+  if (dcq == 0) {
+    // qpr divides the block: every thread keeps its column quad
+    const size_t ddst = (size_t)dpix * ESZ;
+    for (; row < nr; row += drow, pix += dpix, ao += dao, dst += ddst) {
+      int4* ap = reinterpret_cast<int4*>(acc + ao);
+      const int4 a = *ap;
+      *ap = make_int4(0, 0, 0, 0);
+      band_store_quad<OUT, NOISE>(P, a, dst, pix, f, gpair, inv_scale);
+    }
+    return;
+  }
   while (row < nr) {
     int4* ap = reinterpret_cast<int4*>(acc + ao);
     const int4 a = *ap;
@@ -690,73 +704,144 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   ic.wt = max(1, wt);
 }
 
+// Cell table of one enumeration chunk, staged in registers (kCellRegs cells
+// per thread) so its L2 loads overlap the previous item's epilogue.
+constexpr int kCellRegs = 8;
+constexpr int kCellsCap = kCellRegs * kBandThreads;
+
+struct CellRegs {
+  int p0[kCellRegs], n[kCellRegs], c[kCellRegs];
+};
+
+__device__ __forceinline__ void cells_load(const BandParams& P, const ItemCfg& ic, int cb, int cnt,
+                                           CellRegs& cr) {
+  const int* pre = P.prefix + (size_t)ic.pl * ((size_t)1 << (P.sy + P.sx)) + ic.pl;
+  const int rw = ic.rw;
+  const int ci0 = cb + (int)threadIdx.x;
+  int yy = ci0 / rw, xx = ci0 - (ci0 / rw) * rw;
+  const int dy = kBandThreads / rw, dx = kBandThreads - dy * rw;
+#pragma unroll
+  for (int u = 0; u < kCellRegs; ++u) {
+    const int k = (int)threadIdx.x + u * kBandThreads;
+    cr.n[u] = 0;
+    if (k < cnt) {
+      const int c = ((ic.cy0 + yy) << P.sx) | (ic.cx0 + xx);
+      cr.c[u] = c;
+      cr.p0[u] = __ldg(pre + c);
+      cr.n[u] = __ldg(pre + c + 1);
+    }
+    yy += dy;
+    xx += dx;
+    if (xx >= rw) { xx -= rw; ++yy; }
+  }
+}
+
+// Per-cell particle counts of the staged chunk (-> shared memory for the scan).
+__device__ __forceinline__ void cells_count(CellRegs& cr, int cnt, int* cOff) {
+#pragma unroll
+  for (int u = 0; u < kCellRegs; ++u) {
+    const int k = (int)threadIdx.x + u * kBandThreads;
+    if (k < cnt) {
+      cr.n[u] -= cr.p0[u];
+      if (cOff) cOff[k] = cr.n[u];
+    }
+  }
+}
+
+// Scatter the (particle index, cell) pairs of enumeration slots [q0, q1) into
+// the particle map (slot q -> map[q - q0]).
+__device__ __forceinline__ void cells_scatter(const CellRegs& cr, int cnt, const int* cOff, int q0,
+                                              int q1, int* mapG, unsigned short* mapC) {
+#pragma unroll
+  for (int u = 0; u < kCellRegs; ++u) {
+    const int k = (int)threadIdx.x + u * kBandThreads;
+    if (k < cnt) {
+      const int off = cOff[k];
+      const int jb = max(0, q0 - off), je = min(cr.n[u], q1 - off);
+      for (int j = jb; j < je; ++j) {
+        mapG[off + j - q0] = cr.p0[u] + j;
+        mapC[off + j - q0] = (unsigned short)cr.c[u];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <int PSF>
-__global__ void __launch_bounds__(kBandThreads, 2) band_kernel(const BandParams P) {
+__global__ void __launch_bounds__(kBandThreads, PGB_BAND_MINB) band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
   int* acc0 = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
   int* acc1 = acc0 + P.TH * P.AS;
-  int* cP = acc1 + P.TH * P.AS;
-  int* cC = cP + P.cells_cap;
-  int* cOff = cC + P.cells_cap;
+  int* cOff = acc1 + P.TH * P.AS;                 // kCellsCap + 4
+  int* mapG = cOff + kCellsCap + 4;                // map_cap particle indices
+  unsigned short* mapC = reinterpret_cast<unsigned short*>(mapG + P.map_cap);  // their cells
   const int tid = threadIdx.x;
   const GenCfg& g = P.g;
   const int CX = 1 << P.sx;
   const long long total_items = (long long)P.pairs * P.tiles;
   for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandThreads)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
-  for (;;) {
-    if (tid == 0) {
-      const long long item = atomicAdd(P.ticket, 1);
-      sh->item = item;
-      if (item < total_items) item_setup(P, item, sh->ic);
-    }
-    __syncthreads();
-    if (sh->item >= total_items) break;
-    const ItemCfg& ic = sh->ic;
+  // static schedule: items blockIdx.x, + gridDim.x, ... Item k+1's setup (thread
+  // 0, operands prefetched into L1) and cell-table loads (registers) overlap
+  // item k's epilogue.
+  long long item = blockIdx.x;
+  if (tid == 0) {
+    sh->item[0] = item;
+    if (item < total_items) item_setup(P, item, sh->ic[0]);
+  }
+  __syncthreads();
+  CellRegs cr;
+  if (sh->item[0] < total_items) {
+    const int cnt = min(kCellsCap, sh->ic[0].ncell);
+    cells_load(P, sh->ic[0], 0, cnt, cr);
+    cells_count(cr, cnt, cOff);
+  }
+  __syncthreads();
+  for (int buf = 0;; buf ^= 1, item += gridDim.x) {
+    if (item >= total_items) break;
+    const ItemCfg& ic = sh->ic[buf];
     const int pl = ic.pl;
     const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
     const int h = ic.h, wt = ic.wt, shift = ic.shift;
-    const int rw = ic.rw, ncell = ic.ncell, cy0 = ic.cy0, cx0 = ic.cx0;
+    const int ncell = ic.ncell;
     const PairHdr& hd = ic.hd;
     const float scale = (float)(1 << shift);
     const float2* flow = P.flows + (size_t)ic.field * P.field_elems;
-    const int* pre = P.prefix + (size_t)pl * ((size_t)(1 << P.sy) * CX + 1);
     const RngKey key = band_key(P, pl);
-    for (int cb = 0; cb < ncell; cb += P.cells_cap) {
-      const int cnt = min(P.cells_cap, ncell - cb);
-      {
-        // walk the chunk's cells with incremental (row, col): no divisions in the loop
-        const int ci0 = cb + tid;
-        int yy = ci0 / rw, xx = ci0 - (ci0 / rw) * rw;
-        const int dy = kBandThreads / rw, dx = kBandThreads - dy * rw;
-        for (int k = tid; k < cnt; k += kBandThreads) {
-          const int c = ((cy0 + yy) << P.sx) | (cx0 + xx);
-          const int p0 = __ldg(pre + c);
-          cP[k] = p0;
-          cC[k] = c;
-          cOff[k] = __ldg(pre + c + 1) - p0;
-          yy += dy;
-          xx += dx;
-          if (xx >= rw) { xx -= rw; ++yy; }
-        }
+    const long long nxt = item + gridDim.x;
+    if (tid == 0 && nxt < total_items) {
+      const int npl = (int)(nxt / P.tiles);
+      prefetch_l1(P.hdr + npl);
+      prefetch_l1(P.fbound + (int)((P.pair_base + npl) / P.pairs_per_field));
+    }
+    for (int cb = 0; cb < ncell; cb += kCellsCap) {
+      const int cnt = min(kCellsCap, ncell - cb);
+      if (cb > 0) {   // oversized cell ranges: later chunks load directly
+        cells_load(P, ic, cb, cnt, cr);
+        cells_count(cr, cnt, cOff);
+        __syncthreads();
       }
-      __syncthreads();
       const int N = block_scan<kBandThreads>(cOff, cOff, cnt, sh->wsum);
+      // enumeration slots in batches of map_cap: slot -> (particle index, cell)
+      for (int q0 = 0; q0 < N; q0 += P.map_cap) {
+      const int q1 = min(N, q0 + P.map_cap);
+      if (q0 > 0) {   // rare: re-stage the cell registers (they die after the first scatter)
+        cells_load(P, ic, cb, cnt, cr);
+        cells_count(cr, cnt, nullptr);
+      }
+      cells_scatter(cr, cnt, cOff, q0, q1, mapG, mapC);
+      __syncthreads();
       // warp-uniform trip count + __syncwarp: lanes that skip a particle do
       // not run ahead into the next iteration (keeps the warp converged)
-      for (int qb = 0; qb < N; qb += kBandThreads) {
+      for (int qb = q0; qb < q1; qb += kBandThreads) {
         const int q = qb + tid;
-        if (q < N) {
-          // cell k: largest k with cOff[k] <= q
-          int lo = 0, hi = cnt - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (cOff[mid] <= q) lo = mid;
-            else hi = mid - 1;
-          }
-          const int gi = cP[lo] + (q - cOff[lo]);
-          const int cc = cC[lo];
+        if (q < q1) {
+          const int gi = mapG[q - q0];
+          const int cc = mapC[q - q0];
           const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
           const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
           const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
@@ -785,11 +870,22 @@ __global__ void __launch_bounds__(kBandThreads, 2) band_kernel(const BandParams 
         __syncwarp();
       }
       __syncthreads();
+      }
     }
+    // next item: setup (thread 0), then its cell loads fly during this epilogue
+    if (tid == 0) {
+      sh->item[buf ^ 1] = nxt;
+      if (nxt < total_items) item_setup(P, nxt, sh->ic[buf ^ 1]);
+    }
+    __syncthreads();
+    const bool has_next = nxt < total_items;
+    const int ncnt = has_next ? min(kCellsCap, sh->ic[buf ^ 1].ncell) : 0;
+    if (has_next) cells_load(P, sh->ic[buf ^ 1], 0, ncnt, cr);
     const float inv_scale = 1.0f / scale;
     band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
     band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
-    __syncthreads();   // item slot + zeroed accumulators before the next ticket
+    if (has_next) cells_count(cr, ncnt, cOff);
+    __syncthreads();   // zeroed accumulators + next cell table before the next item
   }
 }
 

@@ -107,16 +107,22 @@ PGB_HD double rlog(double x) {
   if (f < 0.70710678118654752) { f = dmul(f, 2.0); e -= 1; }
   const double s = ddiv(dsub(f, 1.0), dadd(f, 1.0));
   const double z = dmul(s, s);
-  double p = ddiv(1.0, 25.0);
-  for (int k = 11; k >= 0; --k) p = dadd(dmul(p, z), ddiv(1.0, (double)(2 * k + 1)));
+  // 2 atanh(s) = 2 s sum z^k / (2k + 1); constants folded at compile time
+  constexpr double kInvOdd[13] = {1.0, 1.0 / 3, 1.0 / 5, 1.0 / 7, 1.0 / 9, 1.0 / 11, 1.0 / 13,
+                                  1.0 / 15, 1.0 / 17, 1.0 / 19, 1.0 / 21, 1.0 / 23, 1.0 / 25};
+  double p = kInvOdd[12];
+  for (int k = 11; k >= 0; --k) p = dadd(dmul(p, z), kInvOdd[k]);
   return dadd(dmul((double)e, 0.6931471805599453), dmul(2.0, dmul(s, p)));
 }
 
 PGB_HD double rexp(double y) {
-  const double k = rint(ddiv(y, 0.6931471805599453));
+  const double k = rint(dmul(y, 1.4426950408889634));
   const double r = dsub(y, dmul(k, 0.6931471805599453));
+  constexpr double kInv[17] = {0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8,
+                               1.0 / 9, 1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15,
+                               1.0 / 16};
   double p = 1.0;
-  for (int i = 16; i >= 1; --i) p = dadd(1.0, ddiv(dmul(r, p), (double)i));
+  for (int i = 16; i >= 1; --i) p = dadd(1.0, dmul(dmul(r, p), kInv[i]));
   return ldexp(p, (int)k);
 }
 

@@ -396,7 +396,7 @@ int guarded(F&& f) {
 // Band generator (band.cuh): plan + launch
 // ----------------------------------------------------------------------------
 struct BandPlan {
-  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx, cells_cap;
+  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx, cells_cap, map_cap;
   size_t smem;
 };
 
@@ -412,7 +412,7 @@ void cell_bits(int H, int W, int& sy, int& sx) {
 }
 
 size_t band_acc_budget() {
-  int kb = 96;
+  int kb = 88;
   if (const char* e = std::getenv("PGB_BAND_ACC_KB")) kb = std::max(8, std::atoi(e));
   return (size_t)kb * 1024;
 }
@@ -443,8 +443,10 @@ BandPlan make_band_plan(int H, int W, int halo) {
   p.tiles_y = (H + p.TH - 1) / p.TH;
   p.tiles_x = (W + p.TW - 1) / p.TW;
   p.tiles = p.tiles_y * p.tiles_x;
-  p.cells_cap = 2048;
-  p.smem = sizeof(BandShared) + (size_t)2 * p.TH * p.AS * 4 + (size_t)(3 * p.cells_cap + 4) * 4;
+  p.cells_cap = kCellsCap;
+  p.map_cap = 2048;
+  p.smem = sizeof(BandShared) + (size_t)2 * p.TH * p.AS * 4 + (size_t)(p.cells_cap + 4) * 4 +
+           (size_t)p.map_cap * 6;
   PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
   return p;
 }
@@ -483,7 +485,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   P.W = cfg->width;
   P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS;
   P.tiles_y = bp.tiles_y; P.tiles_x = bp.tiles_x; P.tiles = bp.tiles;
-  P.sy = bp.sy; P.sx = bp.sx; P.cells_cap = bp.cells_cap;
+  P.sy = bp.sy; P.sx = bp.sx; P.cells_cap = bp.cells_cap; P.map_cap = bp.map_cap;
   P.n = cfg->n_capacity;
   P.pairs = pairs;
   P.pair_base = pair_base;
