@@ -55,8 +55,6 @@ struct BandParams {
   int H, W;
   int TH, TW, AS, tiles_y, tiles_x, tiles;
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
-  int cells_cap;               // cells per enumeration chunk (shared memory)
-  int map_cap;                 // particle -> cell map entries (shared memory)
   int n, pairs;
   long long pair_base;
   uint32_t batch_lo;
@@ -69,6 +67,7 @@ struct BandParams {
   long long field_elems;
   float2* fbound;              // [num_fields] (max |u|, max |v|)
   int* prefix;                 // [pairs][2^(sy+sx) + 1] particle prefix per cell
+  unsigned short* cell_of;     // [pairs][n] seeding cell of every active particle
   PairHdr* hdr;                // [pairs]
   void* out[2];
   long long out_pair_elems;
@@ -347,23 +346,33 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
   // scan in shared memory, then one coalesced copy out
   block_scan<kPrologueThreads>(bins, bins, ncell, wsum);
   for (int i = tid; i <= ncell; i += kPrologueThreads) pre[i] = bins[i];
+  // particle -> cell (counting-sort order: particles of cell c are pre[c] .. pre[c+1]-1)
+  unsigned short* cof = P.cell_of + (size_t)pl * P.n;
+  for (int c = tid; c < ncell; c += kPrologueThreads)
+    for (int j = bins[c]; j < bins[c + 1]; ++j) cof[j] = (unsigned short)c;
 }
 
 // ----------------------------------------------------------------------------
 // Band kernel
 // ----------------------------------------------------------------------------
-// Per-item parameters, computed once by thread 0 and broadcast.
+// Per-item parameters (warp 0 computes them for the next item while the
+// block finishes the current one; double-buffered).
+constexpr int kMaxSeg = 256;   // particle segments (cell rows) per enumeration pass
+
 struct ItemCfg {
   int pl, r0, r1, c0, c1;
-  int cy0, cx0, rw, ncell;
-  int h, wt, shift, field;
+  int cy0, cy1, cx0, cx1;
+  int h, wt, shift, field, sep;
   PairHdr hd;
 };
 
 struct __align__(16) BandShared {
-  long long item[2];   // item[buf] mirrors the loop's item (kept for debugging)
   int wsum[kBandWarps];
+  int nseg[2];                       // segments of the staged pass
+  int rows_left[2];                  // cell rows not yet staged (rare multi-pass items)
   ItemCfg ic[2];
+  int seg_start[2][kMaxSeg];         // first particle index of each segment
+  int seg_off[2][kMaxSeg + 1];       // exclusive prefix of segment lengths
 };
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -489,14 +498,66 @@ __device__ __forceinline__ void splat_erf(int* __restrict__ acc, int AS, int ax,
   }
 }
 
+// Uncorrelated point PSF (rho == 0): value * 2^s = X_j * Y_i with
+// X_j = exp2(Ls - A dx_j^2), Y_i = exp2(-C dy_i^2): 2 WM exponentials per
+// particle-frame, one multiply per pixel.
+template <int WM>
+__device__ __forceinline__ void splat_point_sep(int* __restrict__ acc, int AS, int ax, int ay,
+                                                float fx, float fy, float amp, float sx, float sy, int h,
+                                                int r0, int r1, int c0, int c1, int shift) {
+  const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
+  int rlo, clo, nr, nc;
+  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return;
+  nr = min(nr, WM);
+  nc = min(nc, WM);
+  const float dx0 = (float)(clo - ax) - fx;
+  const float dy0 = (float)(rlo - ay) - fy;
+  int* base = acc + (rlo - r0) * AS + (clo - c0);
+  const float isx = rcp_approx(sx), isy = rcp_approx(sy);
+  const float A = (0.5f * kLog2e) * isx * isx;
+  const float C = (0.5f * kLog2e) * isy * isy;
+  const float Ls = __log2f(amp) + (float)shift;
+  float X[WM], Y[WM];
+#pragma unroll
+  for (int j = 0; j < WM; ++j) {
+    const float dx = dx0 + (float)j;
+    X[j] = ex2_approx(fmaf(-A * dx, dx, Ls));
+    const float dy = dy0 + (float)j;
+    Y[j] = ex2_approx(-C * dy * dy);
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+    if (i < nr) {
+      int* row = base + i * AS;
+#pragma unroll
+      for (int j = 0; j < WM; ++j)
+        if (j < nc) atomicAdd(row + j, round_small(X[j] * Y[i]));
+    }
+  }
+}
+
 template <int PSF>
-__device__ __forceinline__ void splat_dispatch_b(int wt, int* acc, int AS, int ax, int ay, float fx,
-                                                 float fy, float amp, float sx, float sy, float rho,
-                                                 int h, int r0, int r1, int c0, int c1, int shift,
-                                                 float scale) {
+__device__ __forceinline__ void splat_dispatch_b(int wt, int sep, int* acc, int AS, int ax, int ay,
+                                                 float fx, float fy, float amp, float sx, float sy,
+                                                 float rho, int h, int r0, int r1, int c0, int c1,
+                                                 int shift, float scale) {
   if (PSF == kPsfErf) {
     splat_erf(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, scale);
     return;
+  }
+  if (sep) {
+#define PGB_SS(WW) splat_point_sep<WW>(acc, AS, ax, ay, fx, fy, amp, sx, sy, h, r0, r1, c0, c1, shift)
+    switch (wt) {   // warp-uniform (per item)
+      case 1: PGB_SS(1); return;
+      case 2: PGB_SS(2); return;
+      case 3: PGB_SS(3); return;
+      case 4: PGB_SS(4); return;
+      case 5: PGB_SS(5); return;
+      case 6: PGB_SS(6); return;
+      case 7: PGB_SS(7); return;
+      default: break;
+    }
+#undef PGB_SS
   }
 #define PGB_SP(WW) splat_point<WW>(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, shift)
   switch (wt) {   // warp-uniform (per item)
@@ -656,8 +717,8 @@ __device__ __forceinline__ void cell_range(double a, double b, double s, int n, 
   hi = (int)fmin(fmax(fb, 0.0), (double)(n - 1));
 }
 
-// Item parameters (thread 0): tile, the cells whose particles can reach it,
-// the fixed-point shift and the window bound.
+// Item parameters (lane 0 of warp 0): tile, the cells whose particles can reach
+// it, the fixed-point shift and the window bound.
 __device__ __forceinline__ void item_setup(const BandParams& P, long long item, ItemCfg& ic) {
   const GenCfg& g = P.g;
   const int CY = 1 << P.sy, CX = 1 << P.sx;
@@ -680,13 +741,8 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
   const double vy = (double)fb.y * (1.0 + 1e-6) + 1e-6;
   const double vx = (double)fb.x * (1.0 + 1e-6) + 1e-6;
-  int cy0, cy1, cx0, cx1;
-  cell_range((double)ic.r0 - h - 1.5 - vy, (double)ic.r1 + h + 0.5 + vy, ch, CY, cy0, cy1);
-  cell_range((double)ic.c0 - h - 1.5 - vx, (double)ic.c1 + h + 0.5 + vx, cw, CX, cx0, cx1);
-  ic.cy0 = cy0;
-  ic.cx0 = cx0;
-  ic.rw = cx1 - cx0 + 1;
-  ic.ncell = (cy1 - cy0 + 1) * ic.rw;
+  cell_range((double)ic.r0 - h - 1.5 - vy, (double)ic.r1 + h + 0.5 + vy, ch, CY, ic.cy0, ic.cy1);
+  cell_range((double)ic.c0 - h - 1.5 - vx, (double)ic.c1 + h + 0.5 + vx, cw, CX, ic.cx0, ic.cx1);
   // fixed-point shift: contributions per pixel <= cmax * (cells one pixel's
   // source box can meet), amplitude <= amp_bound
   const double by = floor((2.0 * h + 3.0 + 2.0 * vy) / ch) + 2.0;
@@ -702,72 +758,55 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
     wt = min(wt, (int)floorf(2.0f * Rm) + 1);
   }
   ic.wt = max(1, wt);
+  // uncorrelated particles (rho == 0 in both frames): separable splat
+  ic.sep = (g.rho_lo == 0.f && g.rho_span == 0.f && !(g.f2_rho_std > 0.f)) ? 1 : 0;
 }
 
-// Cell table of one enumeration chunk, staged in registers (kCellRegs cells
-// per thread) so its L2 loads overlap the previous item's epilogue.
-constexpr int kCellRegs = 8;
-constexpr int kCellsCap = kCellRegs * kBandThreads;
-
-struct CellRegs {
-  int p0[kCellRegs], n[kCellRegs], c[kCellRegs];
-};
-
-__device__ __forceinline__ void cells_load(const BandParams& P, const ItemCfg& ic, int cb, int cnt,
-                                           CellRegs& cr) {
-  const int* pre = P.prefix + (size_t)ic.pl * ((size_t)1 << (P.sy + P.sx)) + ic.pl;
-  const int rw = ic.rw;
-  const int ci0 = cb + (int)threadIdx.x;
-  int yy = ci0 / rw, xx = ci0 - (ci0 / rw) * rw;
-  const int dy = kBandThreads / rw, dx = kBandThreads - dy * rw;
-#pragma unroll
-  for (int u = 0; u < kCellRegs; ++u) {
-    const int k = (int)threadIdx.x + u * kBandThreads;
-    cr.n[u] = 0;
-    if (k < cnt) {
-      const int c = ((ic.cy0 + yy) << P.sx) | (ic.cx0 + xx);
-      cr.c[u] = c;
-      cr.p0[u] = __ldg(pre + c);
-      cr.n[u] = __ldg(pre + c + 1);
-    }
-    yy += dy;
-    xx += dx;
-    if (xx >= rw) { xx -= rw; ++yy; }
-  }
-}
-
-// Per-cell particle counts of the staged chunk (-> shared memory for the scan).
-__device__ __forceinline__ void cells_count(CellRegs& cr, int cnt, int* cOff) {
-#pragma unroll
-  for (int u = 0; u < kCellRegs; ++u) {
-    const int k = (int)threadIdx.x + u * kBandThreads;
-    if (k < cnt) {
-      cr.n[u] -= cr.p0[u];
-      if (cOff) cOff[k] = cr.n[u];
-    }
-  }
-}
-
-// Scatter the (particle index, cell) pairs of enumeration slots [q0, q1) into
-// the particle map (slot q -> map[q - q0]).
-__device__ __forceinline__ void cells_scatter(const CellRegs& cr, int cnt, const int* cOff, int q0,
-                                              int q1, int* mapG, unsigned short* mapC) {
-#pragma unroll
-  for (int u = 0; u < kCellRegs; ++u) {
-    const int k = (int)threadIdx.x + u * kBandThreads;
-    if (k < cnt) {
-      const int off = cOff[k];
-      const int jb = max(0, q0 - off), je = min(cr.n[u], q1 - off);
-      for (int j = jb; j < je; ++j) {
-        mapG[off + j - q0] = cr.p0[u] + j;
-        mapC[off + j - q0] = (unsigned short)cr.c[u];
+// Warp 0: next item's parameters + particle segments (one per cell row of the
+// cell rectangle; a full-width rectangle is one contiguous segment).
+__device__ __forceinline__ void item_stage(const BandParams& P, long long item, BandShared* sh, int b,
+                                           int row_lo) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0 && row_lo < 0) item_setup(P, item, sh->ic[b]);
+  __syncwarp();
+  const ItemCfg& ic = sh->ic[b];
+  const int CX = 1 << P.sx;
+  const int* pre = P.prefix + (size_t)ic.pl * ((size_t)(1 << P.sy) * CX + 1);
+  const bool full = ic.cx0 == 0 && ic.cx1 == CX - 1;
+  const int y0 = row_lo < 0 ? ic.cy0 : row_lo;
+  const int nrows = ic.cy1 - y0 + 1;
+  const int nseg = full ? 1 : min(nrows, kMaxSeg);
+  int base = 0;
+  for (int s0 = 0; s0 < nseg; s0 += 32) {
+    const int sidx = s0 + lane;
+    int st = 0, len = 0;
+    if (sidx < nseg) {
+      if (full) {
+        st = __ldg(pre + ((size_t)ic.cy0 << P.sx));
+        len = __ldg(pre + ((size_t)(ic.cy1 + 1) << P.sx)) - st;
+      } else {
+        const int cy = y0 + sidx;
+        st = __ldg(pre + ((size_t)cy << P.sx) + ic.cx0);
+        len = __ldg(pre + ((size_t)cy << P.sx) + ic.cx1 + 1) - st;
       }
     }
+    int x = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(~0u, x, o);
+      if (lane >= o) x += y;
+    }
+    if (sidx < nseg) {
+      sh->seg_start[b][sidx] = st;
+      sh->seg_off[b][sidx] = base + x - len;
+    }
+    base += __shfl_sync(~0u, x, 31);
   }
-}
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  if (lane == 0) {
+    sh->seg_off[b][nseg] = base;
+    sh->nseg[b] = nseg;
+    sh->rows_left[b] = full ? 0 : nrows - nseg;
+  }
 }
 
 template <int PSF>
@@ -776,72 +815,49 @@ __global__ void __launch_bounds__(kBandThreads, PGB_BAND_MINB) band_kernel(const
   BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
   int* acc0 = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
   int* acc1 = acc0 + P.TH * P.AS;
-  int* cOff = acc1 + P.TH * P.AS;                 // kCellsCap + 4
-  int* mapG = cOff + kCellsCap + 4;                // map_cap particle indices
-  unsigned short* mapC = reinterpret_cast<unsigned short*>(mapG + P.map_cap);  // their cells
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const GenCfg& g = P.g;
   const int CX = 1 << P.sx;
   const long long total_items = (long long)P.pairs * P.tiles;
   for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandThreads)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
-  // static schedule: items blockIdx.x, + gridDim.x, ... Item k+1's setup (thread
-  // 0, operands prefetched into L1) and cell-table loads (registers) overlap
-  // item k's epilogue.
+  // static schedule: items blockIdx.x, + gridDim.x, ...; warp 0 stages item
+  // k+1 (parameters + particle segments) while the block stores item k.
   long long item = blockIdx.x;
-  if (tid == 0) {
-    sh->item[0] = item;
-    if (item < total_items) item_setup(P, item, sh->ic[0]);
-  }
+  if (warp == 0 && item < total_items) item_stage(P, item, sh, 0, -1);
   __syncthreads();
-  CellRegs cr;
-  if (sh->item[0] < total_items) {
-    const int cnt = min(kCellsCap, sh->ic[0].ncell);
-    cells_load(P, sh->ic[0], 0, cnt, cr);
-    cells_count(cr, cnt, cOff);
-  }
-  __syncthreads();
-  for (int buf = 0;; buf ^= 1, item += gridDim.x) {
-    if (item >= total_items) break;
+  for (int buf = 0; item < total_items; buf ^= 1, item += gridDim.x) {
     const ItemCfg& ic = sh->ic[buf];
     const int pl = ic.pl;
     const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
-    const int h = ic.h, wt = ic.wt, shift = ic.shift;
-    const int ncell = ic.ncell;
+    const int h = ic.h, wt = ic.wt, shift = ic.shift, sep = ic.sep;
     const PairHdr& hd = ic.hd;
     const float scale = (float)(1 << shift);
     const float2* flow = P.flows + (size_t)ic.field * P.field_elems;
+    const unsigned short* cof = P.cell_of + (size_t)pl * P.n;
     const RngKey key = band_key(P, pl);
-    const long long nxt = item + gridDim.x;
-    if (tid == 0 && nxt < total_items) {
-      const int npl = (int)(nxt / P.tiles);
-      prefetch_l1(P.hdr + npl);
-      prefetch_l1(P.fbound + (int)((P.pair_base + npl) / P.pairs_per_field));
-    }
-    for (int cb = 0; cb < ncell; cb += kCellsCap) {
-      const int cnt = min(kCellsCap, ncell - cb);
-      if (cb > 0) {   // oversized cell ranges: later chunks load directly
-        cells_load(P, ic, cb, cnt, cr);
-        cells_count(cr, cnt, cOff);
-        __syncthreads();
-      }
-      const int N = block_scan<kBandThreads>(cOff, cOff, cnt, sh->wsum);
-      // enumeration slots in batches of map_cap: slot -> (particle index, cell)
-      for (int q0 = 0; q0 < N; q0 += P.map_cap) {
-      const int q1 = min(N, q0 + P.map_cap);
-      if (q0 > 0) {   // rare: re-stage the cell registers (they die after the first scatter)
-        cells_load(P, ic, cb, cnt, cr);
-        cells_count(cr, cnt, nullptr);
-      }
-      cells_scatter(cr, cnt, cOff, q0, q1, mapG, mapC);
-      __syncthreads();
+    int next_row = ic.cy0;   // first cell row of the current pass
+    for (;;) {
+      const int nseg = sh->nseg[buf];
+      const int N = sh->seg_off[buf][nseg];
+      const int* soff = sh->seg_off[buf];
+      const int* sst = sh->seg_start[buf];
       // warp-uniform trip count + __syncwarp: lanes that skip a particle do
       // not run ahead into the next iteration (keeps the warp converged)
-      for (int qb = q0; qb < q1; qb += kBandThreads) {
+      for (int qb = 0; qb < N; qb += kBandThreads) {
         const int q = qb + tid;
-        if (q < q1) {
-          const int gi = mapG[q - q0];
-          const int cc = mapC[q - q0];
+        if (q < N) {
+          int sg = 0;
+          if (nseg > 1) {
+            int hi = nseg - 1;
+            while (sg < hi) {
+              const int mid = (sg + hi + 1) >> 1;
+              if (soff[mid] <= q) sg = mid;
+              else hi = mid - 1;
+            }
+          }
+          const int gi = sst[sg] + (q - soff[sg]);
+          const int cc = __ldg(cof + gi);
           const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
           const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
           const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
@@ -860,32 +876,29 @@ __global__ void __launch_bounds__(kBandThreads, PGB_BAND_MINB) band_kernel(const
             Look lk;
             seed_look(g, key, gi, sig, i0, lk);
             if (in1 && lk.vis1 && lk.amp1 > 0.f)
-              splat_dispatch_b<PSF>(wt, acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1, h,
-                                    r0, r1, c0, c1, shift, scale);
-            if (in2 && lk.vis2 && lk.amp2 > 0.f)
-              splat_dispatch_b<PSF>(wt, acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2, lk.rho2,
+              splat_dispatch_b<PSF>(wt, sep, acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1,
                                     h, r0, r1, c0, c1, shift, scale);
+            if (in2 && lk.vis2 && lk.amp2 > 0.f)
+              splat_dispatch_b<PSF>(wt, sep, acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2,
+                                    lk.rho2, h, r0, r1, c0, c1, shift, scale);
           }
         }
         __syncwarp();
       }
       __syncthreads();
-      }
+      if (sh->rows_left[buf] <= 0) break;
+      // rare: more cell rows than one segment table -> stage the next rows
+      next_row += kMaxSeg;
+      if (warp == 0) item_stage(P, item, sh, buf, next_row);
+      __syncthreads();
     }
-    // next item: setup (thread 0), then its cell loads fly during this epilogue
-    if (tid == 0) {
-      sh->item[buf ^ 1] = nxt;
-      if (nxt < total_items) item_setup(P, nxt, sh->ic[buf ^ 1]);
-    }
-    __syncthreads();
-    const bool has_next = nxt < total_items;
-    const int ncnt = has_next ? min(kCellsCap, sh->ic[buf ^ 1].ncell) : 0;
-    if (has_next) cells_load(P, sh->ic[buf ^ 1], 0, ncnt, cr);
+    // warp 0 stages the next item, then everyone stores this one
+    const long long nxt = item + gridDim.x;
+    if (warp == 0 && nxt < total_items) item_stage(P, nxt, sh, buf ^ 1, -1);
     const float inv_scale = 1.0f / scale;
     band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
     band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
-    if (has_next) cells_count(cr, ncnt, cOff);
-    __syncthreads();   // zeroed accumulators + next cell table before the next item
+    __syncthreads();   // zeroed accumulators + staged next item
   }
 }
 

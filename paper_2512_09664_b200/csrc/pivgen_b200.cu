@@ -396,7 +396,7 @@ int guarded(F&& f) {
 // Band generator (band.cuh): plan + launch
 // ----------------------------------------------------------------------------
 struct BandPlan {
-  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx, cells_cap, map_cap;
+  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx;
   size_t smem;
 };
 
@@ -443,10 +443,7 @@ BandPlan make_band_plan(int H, int W, int halo) {
   p.tiles_y = (H + p.TH - 1) / p.TH;
   p.tiles_x = (W + p.TW - 1) / p.TW;
   p.tiles = p.tiles_y * p.tiles_x;
-  p.cells_cap = kCellsCap;
-  p.map_cap = 2048;
-  p.smem = sizeof(BandShared) + (size_t)2 * p.TH * p.AS * 4 + (size_t)(p.cells_cap + 4) * 4 +
-           (size_t)p.map_cap * 6;
+  p.smem = sizeof(BandShared) + (size_t)2 * p.TH * p.AS * 4;
   PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
   return p;
 }
@@ -485,7 +482,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   P.W = cfg->width;
   P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS;
   P.tiles_y = bp.tiles_y; P.tiles_x = bp.tiles_x; P.tiles = bp.tiles;
-  P.sy = bp.sy; P.sx = bp.sx; P.cells_cap = bp.cells_cap; P.map_cap = bp.map_cap;
+  P.sy = bp.sy; P.sx = bp.sx;
   P.n = cfg->n_capacity;
   P.pairs = pairs;
   P.pair_base = pair_base;
@@ -508,15 +505,18 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const size_t hdr_bytes = (size_t)pairs * sizeof(PairHdr);
   const size_t fb_bytes = (size_t)num_fields * sizeof(float2);
   const size_t pre_bytes = (size_t)pairs * (ncell + 1) * sizeof(int);
+  const size_t cof_bytes = (size_t)pairs * cfg->n_capacity * sizeof(unsigned short);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
   DevWork& w = work_for_current();
-  // [ticket | field bounds] are zeroed per launch, then headers and prefixes
+  // [ticket | field bounds] are zeroed per launch, then headers, prefixes, cells
   const size_t head = 256 + up(fb_bytes);
-  char* b = static_cast<char*>(ensure(w.band, w.band_bytes, head + up(hdr_bytes) + up(pre_bytes)));
+  char* b = static_cast<char*>(
+      ensure(w.band, w.band_bytes, head + up(hdr_bytes) + up(pre_bytes) + up(cof_bytes)));
   P.ticket = reinterpret_cast<int*>(b);
   P.fbound = reinterpret_cast<float2*>(b + 256);
   P.hdr = reinterpret_cast<PairHdr*>(b + head);
   P.prefix = reinterpret_cast<int*>(b + head + up(hdr_bytes));
+  P.cell_of = reinterpret_cast<unsigned short*>(b + head + up(hdr_bytes) + up(pre_bytes));
   PGB_CK(cudaMemsetAsync(b, 0, head, stream));
   // bounds only for the fields this pair range reads
   const int f_lo = (int)(pair_base / pairs_per_field);
