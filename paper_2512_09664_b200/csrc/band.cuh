@@ -37,6 +37,7 @@ namespace pgb {
 #endif
 constexpr int kBandThreads = 256;
 constexpr int kBandWarps = kBandThreads / 32;
+constexpr int kBandBlock = kBandThreads + 32;   // + one staging warp
 constexpr int kMaxCellBits = 14;
 
 struct __align__(16) PairHdr {
@@ -293,59 +294,71 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
   const int L = P.sy + P.sx;
   const int ncell = 1 << L;
   const RngKey key = band_key(P, pl);
+  __shared__ PairHdr shd;
+  __shared__ int scm;
   for (int i = tid; i < ncell; i += kPrologueThreads) bins[i] = 0;
+  const GenCfg& g = P.g;
   if (tid == 0) {
-    const GenCfg& g = P.g;
     // seeding density and active count (particles.py:73-83)
     const uint4 w = draw(key, 0u, kTagPair);
     const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w.x, w.y));
     double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
     mm = fmin(fmax(mm, 0.0), (double)P.n);
-    const int M = (int)mm;
+    sM = (int)mm;
+    shd.ppp = ppp;
+    scm = 0;
+  }
+  __syncthreads();
+  const int M = sM;
+  if (tid == 0) {
     // maximum diameter uniform: max of M uniforms = V^(1/M), on particle J
-    PairHdr hd{};
-    hd.ppp = ppp;
-    hd.M = M;
+    // (a serial float64 chain: overlapped with the histogram below)
+    shd.M = M;
+    shd.m = 0.0;
+    shd.J = 0;
+    shd.qmax = 0;
     float dmax = (float)g.d_hi;
     if (M > 0) {
       const uint4 v = draw(key, 1u, kTagPair);
       const double V = u53_to_unit(v.x, v.y);
-      hd.m = rexp(ddiv(rlog(V), (double)M));
-      hd.J = (int)__umul64hi(((uint64_t)v.w << 32) | v.z, (uint64_t)M);
-      const int q = (int)floor(hd.m * 8388608.0);
-      hd.qmax = q < 0x7fffff ? q : 0x7fffff;
-      dmax = lerpf_exact(g.d_lo, g.d_span, q_to_unit(hd.qmax));
+      shd.m = rexp(ddiv(rlog(V), (double)M));
+      shd.J = (int)__umul64hi(((uint64_t)v.w << 32) | v.z, (uint64_t)M);
+      const int q = (int)floor(shd.m * 8388608.0);
+      shd.qmax = q < 0x7fffff ? q : 0x7fffff;
+      dmax = lerpf_exact(g.d_lo, g.d_span, q_to_unit(shd.qmax));
     }
-    hd.dmax = dmax;
+    shd.dmax = dmax;
     // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
-    hd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
-    P.hdr[pl] = hd;
-    if (P.st_ppp) P.st_ppp[pl] = ppp;
-    if (P.st_M) P.st_M[pl] = M;
-    if (P.st_side) P.st_side[pl] = hd.side;
-    if (P.st_dmax) P.st_dmax[pl] = dmax;
-    sM = M;
-  }
-  __syncthreads();
-  const int M = sM;
-  // cell histogram of M iid labels (4 labels per Philox call)
-  for (int q = tid; q < (M + 3) >> 2; q += kPrologueThreads) {
-    const uint4 w = draw(key, (uint32_t)q, kTagCell);
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    shd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
+  } else {
+    // cell histogram of M iid labels (4 labels per Philox call)
+    for (int q = tid - 1; q < (M + 3) >> 2; q += kPrologueThreads - 1) {
+      const uint4 w = draw(key, (uint32_t)q, kTagCell);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+      for (int k = 0; k < 4; ++k)
+        if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+    }
   }
   __syncthreads();
   int cm = 0;
   for (int i = tid; i < ncell; i += kPrologueThreads) cm = max(cm, bins[i]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
-  if (lane == 0) atomicMax(&P.hdr[pl].cmax, cm);
+  if (lane == 0) atomicMax(&scm, cm);
   int* pre = P.prefix + (size_t)pl * (ncell + 1);
   // scan in shared memory, then one coalesced copy out
   block_scan<kPrologueThreads>(bins, bins, ncell, wsum);
   for (int i = tid; i <= ncell; i += kPrologueThreads) pre[i] = bins[i];
+  if (tid == 0) {
+    PairHdr hd = shd;
+    hd.cmax = scm;     // final after the scan's barriers
+    P.hdr[pl] = hd;
+    if (P.st_ppp) P.st_ppp[pl] = hd.ppp;
+    if (P.st_M) P.st_M[pl] = hd.M;
+    if (P.st_side) P.st_side[pl] = hd.side;
+    if (P.st_dmax) P.st_dmax[pl] = hd.dmax;
+  }
   // particle -> cell (counting-sort order: particles of cell c are pre[c] .. pre[c+1]-1)
   unsigned short* cof = P.cell_of + (size_t)pl * P.n;
   for (int c = tid; c < ncell; c += kPrologueThreads)
@@ -810,23 +823,32 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
 }
 
 template <int PSF>
-__global__ void __launch_bounds__(kBandThreads, PGB_BAND_MINB) band_kernel(const BandParams P) {
+__global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
   int* acc0 = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
   int* acc1 = acc0 + P.TH * P.AS;
   const int tid = threadIdx.x, warp = tid >> 5;
+  const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
   const GenCfg& g = P.g;
   const int CX = 1 << P.sx;
   const long long total_items = (long long)P.pairs * P.tiles;
-  for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandThreads)
+  for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandBlock)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
-  // static schedule: items blockIdx.x, + gridDim.x, ...; warp 0 stages item
-  // k+1 (parameters + particle segments) while the block stores item k.
+  // static schedule: items blockIdx.x, + gridDim.x, ...; the staging warp
+  // prepares item k+1 (parameters + particle segments) while the workers
+  // splat item k.
   long long item = blockIdx.x;
-  if (warp == 0 && item < total_items) item_stage(P, item, sh, 0, -1);
+  if (stager && item < total_items) item_stage(P, item, sh, 0, -1);
   __syncthreads();
   for (int buf = 0; item < total_items; buf ^= 1, item += gridDim.x) {
+    const long long nxt = item + gridDim.x;
+    if (stager) {
+      if (nxt < total_items) item_stage(P, nxt, sh, buf ^ 1, -1);
+      __syncthreads();   // particles done
+      __syncthreads();   // store done
+      continue;
+    }
     const ItemCfg& ic = sh->ic[buf];
     const int pl = ic.pl;
     const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
@@ -842,22 +864,35 @@ __global__ void __launch_bounds__(kBandThreads, PGB_BAND_MINB) band_kernel(const
       const int N = sh->seg_off[buf][nseg];
       const int* soff = sh->seg_off[buf];
       const int* sst = sh->seg_start[buf];
+      // slot q -> particle index (segment search) -> its cell (L2 load); the
+      // next iteration's cell load is issued one iteration ahead
+      auto locate = [&](int q) {
+        int sg = 0;
+        if (nseg > 1) {
+          int hi = nseg - 1;
+          while (sg < hi) {
+            const int mid = (sg + hi + 1) >> 1;
+            if (soff[mid] <= q) sg = mid;
+            else hi = mid - 1;
+          }
+        }
+        return sst[sg] + (q - soff[sg]);
+      };
+      int gi_n = 0, cc_n = 0;
+      if (tid < N) {
+        gi_n = locate(tid);
+        cc_n = __ldg(cof + gi_n);
+      }
       // warp-uniform trip count + __syncwarp: lanes that skip a particle do
       // not run ahead into the next iteration (keeps the warp converged)
       for (int qb = 0; qb < N; qb += kBandThreads) {
         const int q = qb + tid;
+        const int gi = gi_n, cc = cc_n;
+        if (q + kBandThreads < N) {
+          gi_n = locate(q + kBandThreads);
+          cc_n = __ldg(cof + gi_n);
+        }
         if (q < N) {
-          int sg = 0;
-          if (nseg > 1) {
-            int hi = nseg - 1;
-            while (sg < hi) {
-              const int mid = (sg + hi + 1) >> 1;
-              if (soff[mid] <= q) sg = mid;
-              else hi = mid - 1;
-            }
-          }
-          const int gi = sst[sg] + (q - soff[sg]);
-          const int cc = __ldg(cof + gi);
           const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
           const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
           const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
@@ -885,20 +920,19 @@ __global__ void __launch_bounds__(kBandThreads, PGB_BAND_MINB) band_kernel(const
         }
         __syncwarp();
       }
-      __syncthreads();
       if (sh->rows_left[buf] <= 0) break;
-      // rare: more cell rows than one segment table -> stage the next rows
+      // rare: more cell rows than one segment table -> worker warp 0 stages
+      // the next rows of this item (named barrier: workers only)
+      asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
       next_row += kMaxSeg;
       if (warp == 0) item_stage(P, item, sh, buf, next_row);
-      __syncthreads();
+      asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
     }
-    // warp 0 stages the next item, then everyone stores this one
-    const long long nxt = item + gridDim.x;
-    if (warp == 0 && nxt < total_items) item_stage(P, nxt, sh, buf ^ 1, -1);
+    __syncthreads();   // particles done (stager: next item staged)
     const float inv_scale = 1.0f / scale;
     band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
     band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
-    __syncthreads();   // zeroed accumulators + staged next item
+    __syncthreads();   // accumulators zeroed
   }
 }
 

@@ -459,7 +459,7 @@ int band_resident_ctas(BandFn fn, size_t smem) {
   if (it != cache.end()) return it->second;
   PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
   int per_sm = 0, sms = 0;
-  PGB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kBandThreads, smem));
+  PGB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kBandBlock, smem));
   PGB_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   PGB_REQUIRE(per_sm > 0, "band kernel configuration cannot be scheduled");
   cache[key] = per_sm * sms;
@@ -565,7 +565,7 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   const int ctas = band_resident_ctas(fn, bp.smem);
   const long long items = (long long)pairs * bp.tiles;
   const int grid = (int)std::max<long long>(1, std::min<long long>(ctas, items));
-  fn<<<grid, kBandThreads, bp.smem, stream>>>(P);
+  fn<<<grid, kBandBlock, bp.smem, stream>>>(P);
   g_launches.fetch_add(1);
 }
 
