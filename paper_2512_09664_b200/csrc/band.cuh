@@ -70,6 +70,10 @@ struct BandParams {
   int* prefix;                 // [pairs][2^(sy+sx) + 1] particle prefix per cell
   unsigned short* cell_of;     // [pairs][n] seeding cell of every active particle
   PairHdr* hdr;                // [pairs]
+  int* pair_ready;             // [pairs] prologue done (in-kernel prologue), else null
+  int* fb_done;                // [num_fields] finished bound chunks, else null
+  int inline_prologue;         // band kernel runs the prologue work items itself
+  int field_lo, field_cnt;     // flow fields read by this pair range
   void* out[2];
   long long out_pair_elems;
   double* st_ppp;
@@ -256,47 +260,64 @@ __device__ int block_scan(const int* in, int* out, int count, int* wsum) {
 // Prologue: one CTA per pair (+ one per flow field)
 // ----------------------------------------------------------------------------
 constexpr int kPrologueThreads = 512;
-constexpr int kFieldBlocks = 16;   // CTAs per flow field for the displacement bound
+constexpr int kFieldBlocks = 16;   // work chunks per flow field for the displacement bound
 
-__global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandParams P) {
-  extern __shared__ int bins[];
-  __shared__ int wsum[kPrologueThreads / 32];
-  __shared__ int sM;
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_b(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Flow bound, one of kFieldBlocks chunks of field f (whole block): max |u|,
+// max |v| by atomicMax on the bits of non-negative floats (non-finite values
+// -> unbounded); the chunk counter fb_done[f] releases the bound.
+template <int NT>
+__device__ void field_bound_chunk(const BandParams& P, int f, int part) {
   const int tid = threadIdx.x, lane = tid & 31;
-  if (blockIdx.x >= P.pairs) {
-    // flow bound: kFieldBlocks CTAs per field, float4 loads, atomicMax on the
-    // bits of non-negative floats (non-finite values -> unbounded)
-    const int fb = blockIdx.x - P.pairs;
-    const int f = fb / kFieldBlocks, part = fb - f * kFieldBlocks;
-    const float2* fl = P.flows + (size_t)f * P.field_elems;
-    float mu = 0.f, mv = 0.f;
-    const long long stride = (long long)kFieldBlocks * kPrologueThreads;
+  const float2* fl = P.flows + (size_t)f * P.field_elems;
+  float mu = 0.f, mv = 0.f;
+  const long long stride = (long long)kFieldBlocks * NT;
 #pragma unroll 4
-    for (long long e = (long long)part * kPrologueThreads + tid; e < P.field_elems; e += stride) {
-      const float2 v = __ldg(fl + e);
-      const float au = fabsf(v.x), av = fabsf(v.y);
-      mu = au <= 3.0e38f ? fmaxf(mu, au) : INFINITY;
-      mv = av <= 3.0e38f ? fmaxf(mv, av) : INFINITY;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mu = fmaxf(mu, __shfl_xor_sync(~0u, mu, o));
-      mv = fmaxf(mv, __shfl_xor_sync(~0u, mv, o));
-    }
-    if (lane == 0) {
-      unsigned* b = reinterpret_cast<unsigned*>(P.fbound + f);
-      atomicMax(b, __float_as_uint(mu));
-      atomicMax(b + 1, __float_as_uint(mv));
-    }
-    return;
+  for (long long e = (long long)part * NT + tid; e < P.field_elems; e += stride) {
+    const float2 v = __ldg(fl + e);
+    const float au = fabsf(v.x), av = fabsf(v.y);
+    mu = au <= 3.0e38f ? fmaxf(mu, au) : INFINITY;
+    mv = av <= 3.0e38f ? fmaxf(mv, av) : INFINITY;
   }
-  const int pl = blockIdx.x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mu = fmaxf(mu, __shfl_xor_sync(~0u, mu, o));
+    mv = fmaxf(mv, __shfl_xor_sync(~0u, mv, o));
+  }
+  if (lane == 0) {
+    unsigned* b = reinterpret_cast<unsigned*>(P.fbound + f);
+    atomicMax(b, __float_as_uint(mu));
+    atomicMax(b + 1, __float_as_uint(mv));
+  }
+  __syncthreads();
+  if (tid == 0 && P.fb_done) {
+    __threadfence();
+    atomicAdd(P.fb_done + f, 1);
+  }
+}
+
+// Per-pair prologue (whole block, NT threads, `bins` = 2^(sy+sx) + 1 ints of
+// shared scratch): density, M, maximum diameter, the cell histogram -> per-cell
+// prefix and the particle -> cell array; pair_ready[pl] releases them.
+template <int NT>
+__device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
+  __shared__ int wsum[NT / 32];
+  __shared__ int sM;
+  __shared__ PairHdr shd;
+  __shared__ int scm;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int L = P.sy + P.sx;
   const int ncell = 1 << L;
   const RngKey key = band_key(P, pl);
-  __shared__ PairHdr shd;
-  __shared__ int scm;
-  for (int i = tid; i < ncell; i += kPrologueThreads) bins[i] = 0;
+  for (int i = tid; i < ncell; i += NT) bins[i] = 0;
   const GenCfg& g = P.g;
   if (tid == 0) {
     // seeding density and active count (particles.py:73-83)
@@ -332,7 +353,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
     shd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
   } else {
     // cell histogram of M iid labels (4 labels per Philox call)
-    for (int q = tid - 1; q < (M + 3) >> 2; q += kPrologueThreads - 1) {
+    for (int q = tid - 1; q < (M + 3) >> 2; q += NT - 1) {
       const uint4 w = draw(key, (uint32_t)q, kTagCell);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -342,14 +363,14 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
   }
   __syncthreads();
   int cm = 0;
-  for (int i = tid; i < ncell; i += kPrologueThreads) cm = max(cm, bins[i]);
+  for (int i = tid; i < ncell; i += NT) cm = max(cm, bins[i]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
   if (lane == 0) atomicMax(&scm, cm);
   int* pre = P.prefix + (size_t)pl * (ncell + 1);
   // scan in shared memory, then one coalesced copy out
-  block_scan<kPrologueThreads>(bins, bins, ncell, wsum);
-  for (int i = tid; i <= ncell; i += kPrologueThreads) pre[i] = bins[i];
+  block_scan<NT>(bins, bins, ncell, wsum);
+  for (int i = tid; i <= ncell; i += NT) pre[i] = bins[i];
   if (tid == 0) {
     PairHdr hd = shd;
     hd.cmax = scm;     // final after the scan's barriers
@@ -361,8 +382,25 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
   }
   // particle -> cell (counting-sort order: particles of cell c are pre[c] .. pre[c+1]-1)
   unsigned short* cof = P.cell_of + (size_t)pl * P.n;
-  for (int c = tid; c < ncell; c += kPrologueThreads)
+  for (int c = tid; c < ncell; c += NT)
     for (int j = bins[c]; j < bins[c + 1]; ++j) cof[j] = (unsigned short)c;
+  __syncthreads();
+  if (tid == 0 && P.pair_ready) {
+    __threadfence();
+    st_release(P.pair_ready + pl, 1);
+  }
+}
+
+// Standalone prologue (sample_particles path): one CTA per pair + kFieldBlocks
+// per flow field.
+__global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandParams P) {
+  extern __shared__ int bins[];
+  if (blockIdx.x >= P.pairs) {
+    const int fb = blockIdx.x - P.pairs;
+    field_bound_chunk<kPrologueThreads>(P, fb / kFieldBlocks, fb % kFieldBlocks);
+    return;
+  }
+  pair_prologue<kPrologueThreads>(P, blockIdx.x, bins);
 }
 
 // ----------------------------------------------------------------------------
@@ -744,11 +782,22 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   ic.r1 = min(ic.r0 + P.TH, g.H);
   ic.c0 = tx * P.TW;
   ic.c1 = min(ic.c0 + P.TW, g.W);
-  ic.hd = P.hdr[pl];
+  ic.field = (int)((P.pair_base + pl) / P.pairs_per_field);
+  if (P.inline_prologue) {
+    // produced inside this launch by other CTAs (their first work items)
+    int ns = 32;
+    while (ld_acquire_b(P.pair_ready + pl) == 0) { __nanosleep(ns); ns = min(ns * 2, 256); }
+    while (ld_acquire_b(P.fb_done + ic.field) < kFieldBlocks) { __nanosleep(ns); ns = min(ns * 2, 256); }
+  }
+  {
+    const int4* src = reinterpret_cast<const int4*>(P.hdr + pl);
+    int4* dst = reinterpret_cast<int4*>(&ic.hd);
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(PairHdr) / 16); ++k) dst[k] = __ldcg(src + k);
+  }
   const int h = ic.hd.side >> 1;
   ic.h = h;
-  ic.field = (int)((P.pair_base + pl) / P.pairs_per_field);
-  const float2 fb = P.fbound[ic.field];
+  const float2 fb = __ldcg(P.fbound + ic.field);
   // frame-1 positions that can reach the tile in either frame: anchors within
   // h of the tile (frame 1), or within h + 1 + max|v| (frame 2: the anchor
   // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
@@ -795,12 +844,12 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
     int st = 0, len = 0;
     if (sidx < nseg) {
       if (full) {
-        st = __ldg(pre + ((size_t)ic.cy0 << P.sx));
-        len = __ldg(pre + ((size_t)(ic.cy1 + 1) << P.sx)) - st;
+        st = __ldcg(pre + ((size_t)ic.cy0 << P.sx));
+        len = __ldcg(pre + ((size_t)(ic.cy1 + 1) << P.sx)) - st;
       } else {
         const int cy = y0 + sidx;
-        st = __ldg(pre + ((size_t)cy << P.sx) + ic.cx0);
-        len = __ldg(pre + ((size_t)cy << P.sx) + ic.cx1 + 1) - st;
+        st = __ldcg(pre + ((size_t)cy << P.sx) + ic.cx0);
+        len = __ldcg(pre + ((size_t)cy << P.sx) + ic.cx1 + 1) - st;
       }
     }
     int x = len;
@@ -833,8 +882,24 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
   const GenCfg& g = P.g;
   const int CX = 1 << P.sx;
   const long long total_items = (long long)P.pairs * P.tiles;
+  if (P.inline_prologue) {
+    // prologue work items first (pairs, then flow-bound chunks); band items
+    // wait on their readiness flags, so every wait targets work that some
+    // co-resident CTA runs before it waits on anything
+    const int npro = P.pairs + P.field_cnt * kFieldBlocks;
+    for (int w = blockIdx.x; w < npro; w += gridDim.x) {
+      if (w < P.pairs) {
+        pair_prologue<kBandBlock>(P, w, acc0);
+      } else {
+        const int fc = w - P.pairs;
+        field_bound_chunk<kBandBlock>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
+      }
+      __syncthreads();
+    }
+  }
   for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandBlock)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+  __syncthreads();
   // static schedule: items blockIdx.x, + gridDim.x, ...; the staging warp
   // prepares item k+1 (parameters + particle segments) while the workers
   // splat item k.
@@ -881,7 +946,7 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
       int gi_n = 0, cc_n = 0;
       if (tid < N) {
         gi_n = locate(tid);
-        cc_n = __ldg(cof + gi_n);
+        cc_n = __ldcg(cof + gi_n);
       }
       // warp-uniform trip count + __syncwarp: lanes that skip a particle do
       // not run ahead into the next iteration (keeps the warp converged)
@@ -890,7 +955,7 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
         const int gi = gi_n, cc = cc_n;
         if (q + kBandThreads < N) {
           gi_n = locate(q + kBandThreads);
-          cc_n = __ldg(cof + gi_n);
+          cc_n = __ldcg(cof + gi_n);
         }
         if (q < N) {
           const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);

@@ -475,9 +475,14 @@ float amp_bound_of(const pgb_config* c) {
 
 // Fill the band parameters shared by generate / sample_particles and run the
 // prologue (densities, maximum diameters, cell prefixes, field bounds).
+// Fill the band parameters shared by generate / sample_particles and lay out
+// the workspace; `launch` runs the standalone prologue kernel (densities,
+// maximum diameters, cell prefixes, field bounds), otherwise the band kernel
+// runs that work itself (inline_prologue).
 void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uint64_t batch,
                    int64_t pair_base, int pairs, const float* flows, int num_fields,
-                   int pairs_per_field, const pgb_pair_stats* stats, cudaStream_t stream) {
+                   int pairs_per_field, const pgb_pair_stats* stats, cudaStream_t stream,
+                   bool launch) {
   P.H = cfg->height;
   P.W = cfg->width;
   P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS;
@@ -504,16 +509,19 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const int ncell = 1 << (bp.sy + bp.sx);
   const size_t hdr_bytes = (size_t)pairs * sizeof(PairHdr);
   const size_t fb_bytes = (size_t)num_fields * sizeof(float2);
+  const size_t flag_bytes = ((size_t)pairs + num_fields) * sizeof(int);
   const size_t pre_bytes = (size_t)pairs * (ncell + 1) * sizeof(int);
   const size_t cof_bytes = (size_t)pairs * cfg->n_capacity * sizeof(unsigned short);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
   DevWork& w = work_for_current();
-  // [ticket | field bounds] are zeroed per launch, then headers, prefixes, cells
-  const size_t head = 256 + up(fb_bytes);
+  // [ticket | field bounds | ready flags] are zeroed per launch, then headers,
+  // prefixes and the particle -> cell arrays
+  const size_t head = 256 + up(fb_bytes) + up(flag_bytes);
   char* b = static_cast<char*>(
       ensure(w.band, w.band_bytes, head + up(hdr_bytes) + up(pre_bytes) + up(cof_bytes)));
   P.ticket = reinterpret_cast<int*>(b);
   P.fbound = reinterpret_cast<float2*>(b + 256);
+  int* flags = reinterpret_cast<int*>(b + 256 + up(fb_bytes));
   P.hdr = reinterpret_cast<PairHdr*>(b + head);
   P.prefix = reinterpret_cast<int*>(b + head + up(hdr_bytes));
   P.cell_of = reinterpret_cast<unsigned short*>(b + head + up(hdr_bytes) + up(pre_bytes));
@@ -521,15 +529,24 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   // bounds only for the fields this pair range reads
   const int f_lo = (int)(pair_base / pairs_per_field);
   const int f_hi = (int)((pair_base + pairs - 1) / pairs_per_field);
+  P.field_lo = f_lo;
+  P.field_cnt = f_hi - f_lo + 1;
+  if (!launch) {
+    P.inline_prologue = 1;
+    P.pair_ready = flags;
+    P.fb_done = flags + pairs;
+    return;
+  }
+  P.inline_prologue = 0;
   BandParams Q = P;
-  const size_t psmem = (size_t)ncell * sizeof(int) + 16;
+  const size_t psmem = (size_t)(ncell + 1) * sizeof(int) + 16;
   static bool attr_set = false;
   if (!attr_set) {
     PGB_CK(cudaFuncSetAttribute((const void*)prologue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kSmemMax));
     attr_set = true;
   }
-  // field blocks handle absolute field f_lo + (block - pairs) / kFieldBlocks
+  // field blocks handle relative field (block - pairs) / kFieldBlocks
   Q.flows = P.flows + (size_t)f_lo * P.field_elems;
   Q.fbound = P.fbound + f_lo;
   prologue_kernel<<<pairs + (f_hi - f_lo + 1) * kFieldBlocks, kPrologueThreads, psmem, stream>>>(Q);
@@ -555,7 +572,8 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
   const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
   BandParams P{};
-  band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats, stream);
+  band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats, stream,
+                false);
   P.out_mode = out_mode;
   P.bg_offset = (float)cfg->bg_offset;
   P.noise_std = (float)cfg->noise_std;
@@ -845,7 +863,7 @@ int pgb_sample_particles_dev(const pgb_config* cfg, uint64_t batch, int64_t pair
     const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
     BandParams P{};
     band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats,
-                  (cudaStream_t)stream);
+                  (cudaStream_t)stream, true);
     sample_band_kernel<<<pairs, 256, 0, (cudaStream_t)stream>>>(P, *out);
     g_launches.fetch_add(1);
     PGB_CK(cudaGetLastError());
