@@ -72,59 +72,94 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed region:
+    NVML polled every ~1 ms on a thread (nvidia-smi -lms 20 as a fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NAMES = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self._stop = threading.Event()
+        self._thr = None
+        self._smi = None
+        self._lines: list[str] = []
+
+    def _handle(self, nv):
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self, nv, h):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.mx.append(float(mx))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h) if hasattr(
+                    nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for bit, name in self.NAMES.items():
+                    if bits & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self._thr = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self._thr.start()
         except Exception:
-            self.proc = None
+            try:
+                self._smi = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index),
+                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "20"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                threading.Thread(target=lambda: self._lines.extend(l.strip() for l in self._smi.stdout),
+                                 daemon=True).start()
+            except Exception:
+                self._smi = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join(2)
+        if self._smi is not None:
+            self._smi.terminate()
             try:
-                self.proc.wait(2)
+                self._smi.wait(2)
             except Exception:
-                self.proc.kill()
+                self._smi.kill()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in self._lines:
+                parts = [p.strip() for p in line.split(",")]
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx.append(float(parts[1]))
+                except (ValueError, IndexError):
+                    continue
+                for name, val in zip(names, parts[2:6]):
+                    if val.lower() == "active":
+                        self.reasons.add(name)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[3:7]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        if not sm:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 def make_cfg(pg, name, per_gpu_batch):
@@ -323,13 +358,17 @@ def run_ours(args):
         bytes_per_launch = 2 * per_gpu * H * W * 4
         kernel_s = (total_ms / 1000.0) / args.steps
         achieved = bytes_per_launch / kernel_s / 1e9
-        traffic = None
+        traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
                 with open(tp) as fh:
-                    tj = json.load(fh)
-                traffic = tj.get(name)
+                    tj = json.load(fh).get(name)
+                if tj:
+                    # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full
+                    # capture (L2 is write-back: part of the output leaves later)
+                    traffic = float(tj["dram_bytes_per_launch"])
+                    traffic_src = "profiles/" + tj.get("source", "traffic.json")
             except Exception:
                 traffic = None
         line = {
@@ -343,9 +382,10 @@ def run_ours(args):
                        "l2": "flushed between steps (256 MiB write, untimed); per-step CUDA events summed",
                        "output": "float32 images1+images2 in HBM"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
-                         "kernel": "pgb::band_kernel (+ prologue_kernel)", "peak_source": peak_kind},
+                         "kernel": "pgb::band_kernel<PSF> (one launch per batch; in-kernel prologue)",
+                         "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy burst)"},
             "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "pgb_generate_batch (C ABI, host buffers: flow H2D + images D2H, pinned)"},

@@ -1,0 +1,88 @@
+"""Summarise ncu captures for profiles/ (committed evidence).
+
+Usage: python scripts/profile_summary.py <full.ncu-rep> <launches.csv> <out_prefix>
+Writes <out_prefix>_launches.txt (kernel launch list with durations) and
+<out_prefix>_band_kernel.txt (speed-of-light, memory traffic, occupancy,
+stall reasons and per-phase instruction split of the dominant kernel), and
+updates profiles/traffic.json with the kernel's measured DRAM bytes/launch.
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# ---- launch list
+rows = [r for r in csv.DictReader(l for l in open(launches) if not l.startswith("=="))]
+with open(prefix + "_launches.txt", "w") as fh:
+    fh.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n")
+    fh.write("# command: python bench.py --steps 5 --warmup 3 --no-cpu-baseline (config c2)\n")
+    for r in rows:
+        fh.write(f"{r['ID']:>4s}  {r['Kernel Name'][:70]:70s}  {float(r['Metric Value'])/1000:9.2f} us\n")
+    band = [float(r["Metric Value"]) for r in rows if "band_kernel" in r["Kernel Name"]]
+    other = [float(r["Metric Value"]) for r in rows if "band_kernel" not in r["Kernel Name"]]
+    if band:
+        fh.write(f"# band_kernel launches: {len(band)}, mean {sum(band)/len(band)/1000:.2f} us; "
+                 f"other kernels (bench L2 flush): {len(other)}\n")
+
+# ---- full capture
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(io.StringIO(raw)))
+hdr, units, vals = r[0], r[1], r[2]
+d = dict(zip(hdr, vals))
+un = dict(zip(hdr, units))
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+         "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}
+
+
+def f(k):
+    # bytes for byte metrics, nanoseconds for time metrics, raw otherwise
+    try:
+        return float(d[k]) * SCALE.get(un.get(k, ""), 1)
+    except (KeyError, ValueError):
+        return float("nan")
+
+
+dram_r, dram_w = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
+dur_ns = f("gpu__time_duration.sum")
+stalls = {k[len("smsp__pcsamp_warps_issue_stalled_"):]: f(k) for k in hdr
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
+tot = sum(v for v in stalls.values() if v == v) or 1.0
+phases = subprocess.run([sys.executable, os.path.join(root, "scripts", "ncu_lines.py"), rep, "0",
+                         "splat=band.cuh:395-610,store=band.cuh:611-760,stage=band.cuh:761-860,"
+                         "gen=band.cuh:80-215,prologue=band.cuh:216-400,loop=band.cuh:861-1000,"
+                         "fused_helpers=fused.cuh:1-1200,philox=common.cuh:1-400"],
+                        capture_output=True, text=True).stdout
+with open(prefix + "_band_kernel.txt", "w") as fh:
+    fh.write("# ncu --set full --clock-control none --import-source on -k regex:band_kernel -s 3 -c 1\n")
+    fh.write("#   python bench.py --steps 3 --warmup 3 --no-cpu-baseline   (c2: 256x256, B=256, f32)\n")
+    fh.write(f"duration_us                {dur_ns/1000:.2f}\n")
+    fh.write(f"dram_bytes_read            {dram_r:.0f}\n")
+    fh.write(f"dram_bytes_write           {dram_w:.0f}\n")
+    fh.write(f"algorithmic_bytes          {256*2*256*256*4} (2 f32 frames x 256 pairs)\n")
+    for k in ["sm__throughput.avg.pct_of_peak_sustained_elapsed",
+              "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+              "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+              "smsp__inst_executed.sum", "sm__inst_executed.avg.per_cycle_active",
+              "sm__warps_active.avg.pct_of_peak_sustained_active",
+              "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
+              "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
+              "launch__occupancy_limit_shared_mem"]:
+        fh.write(f"{k:60s} {d.get(k, 'n/a')}\n")
+    fh.write("\n# warp stall samples (% of all)\n")
+    for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:12]:
+        fh.write(f"  {k:30s} {100*v/tot:5.1f}\n")
+    fh.write("\n# instruction / stall-sample split by source region (scripts/ncu_lines.py)\n")
+    fh.write(phases)
+
+tp = os.path.join(root, "profiles", "traffic.json")
+tj = json.load(open(tp)) if os.path.exists(tp) else {}
+tj["c2"] = {"kernel": "pgb::band_kernel<0>", "dram_bytes_per_launch": dram_r + dram_w,
+            "dram_read": dram_r, "dram_write": dram_w, "duration_us_ncu": dur_ns / 1000,
+            "source": os.path.basename(prefix) + "_band_kernel.txt"}
+json.dump(tj, open(tp, "w"), indent=1)
+print(open(prefix + "_band_kernel.txt").read())
