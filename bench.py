@@ -376,7 +376,9 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Lamb-Oseen vortex flow; Philox-seeded particles)",
-            "config": {"workload": f"{name}: {H}x{W}, B={per_gpu} pairs per GPU, ppp 0.06, d in [0.8,1.2]",
+            "config": {"workload": f"{name}: {H}x{W}, B={per_gpu} pairs per GPU, ppp {CONFIGS[name][3][1]}, "
+                                   f"d in [{CONFIGS[name][4][0]},{CONFIGS[name][4][1]}], {CONFIGS[name][5]} flow"
+                                   + (", " + ",".join(sorted(CONFIGS[name][6])) if CONFIGS[name][6] else ""),
                        "global_batch": global_batch, "seq_len": None, "image": [H, W],
                        "parallelism": f"dp{world} (pairs sharded, no collective)",
                        "l2": "flushed between steps (256 MiB write, untimed); per-step CUDA events summed",
