@@ -412,7 +412,7 @@ void cell_bits(int H, int W, int& sy, int& sx) {
 }
 
 size_t band_acc_budget() {
-  int kb = 88;
+  int kb = 110;
   if (const char* e = std::getenv("PGB_BAND_ACC_KB")) kb = std::max(8, std::atoi(e));
   return (size_t)kb * 1024;
 }
@@ -431,12 +431,22 @@ BandPlan make_band_plan(int H, int W, int halo) {
     if (THmax >= 1) {
       const int ty = (H + THmax - 1) / THmax;
       const int TH = (H + ty - 1) / ty;
-      const double cost = ((TH + 2 * m) * (TW + 2 * m)) / ((double)TH * TW);
+      // regenerated particles per rendered one: the reach is clipped at the
+      // image border (full-width/-height tiles have no margin on that axis)
+      const double ey = std::min<double>(TH + 2 * m, H), ex = std::min<double>(TW + 2 * m, W);
+      const double cost = (ey * ex) / ((double)TH * TW);
       if (cost < best - 1e-9) { best = cost; bestTW = TW; bestTH = TH; }
     }
     if (TW >= W) break;
   }
   PGB_REQUIRE(bestTW > 0, "band plan: image too large for the accumulator budget");
+  if (const char* e = std::getenv("PGB_TILE")) {     // tuning override "TH,TW"
+    int th = 0, tw = 0;
+    if (std::sscanf(e, "%d,%d", &th, &tw) == 2 && th > 0 && tw >= 4 && (size_t)th * tw <= budget_ints) {
+      bestTH = std::min(th, H);
+      bestTW = std::min(tw, (W + 3) / 4 * 4);
+    }
+  }
   p.TW = bestTW;
   p.AS = (bestTW + 3) / 4 * 4;
   p.TH = bestTH;
