@@ -50,6 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     extra = []
     if os.environ.get("PGB_BAND_MINB"):      # tuning knob: band kernel CTAs per SM
         extra.append(f"-DPGB_BAND_MINB={int(os.environ['PGB_BAND_MINB'])}")
+    if os.environ.get("PGB_PHASE_TIMING"):   # debug: per-phase cycle counters in the band kernel
+        extra.append("-DPGB_PHASE_TIMING")
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if proc.returncode != 0:

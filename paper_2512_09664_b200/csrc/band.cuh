@@ -74,6 +74,7 @@ struct BandParams {
   int* fb_done;                // [num_fields] finished bound chunks, else null
   int inline_prologue;         // band kernel runs the prologue work items itself
   int field_lo, field_cnt;     // flow fields read by this pair range
+  unsigned long long* timing;  // optional per-CTA phase cycle counters (PGB_PHASE_TIMING)
   void* out[2];
   long long out_pair_elems;
   double* st_ppp;
@@ -914,6 +915,9 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
       __syncthreads();   // store done
       continue;
     }
+#ifdef PGB_PHASE_TIMING
+    const long long t_item0 = clock64();
+#endif
     const ItemCfg& ic = sh->ic[buf];
     const int pl = ic.pl;
     const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
@@ -993,11 +997,34 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
       if (warp == 0) item_stage(P, item, sh, buf, next_row);
       asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
     }
+#ifdef PGB_PHASE_TIMING
+    const long long t_part = clock64();
+#endif
     __syncthreads();   // particles done (stager: next item staged)
+#ifdef PGB_PHASE_TIMING
+    const long long t_bar1 = clock64();
+#endif
     const float inv_scale = 1.0f / scale;
     band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
     band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
+#ifdef PGB_PHASE_TIMING
+    const long long t_store = clock64();
+#endif
     __syncthreads();   // accumulators zeroed
+#ifdef PGB_PHASE_TIMING
+    if (P.timing) {
+      // per warp: [particles, barrier1, store, barrier2] cycles of this item
+      const long long t_end = clock64();
+      unsigned long long* T = P.timing + ((size_t)blockIdx.x * kBandWarps + warp) * 5;
+      if ((tid & 31) == 0) {
+        atomicAdd(T + 0, (unsigned long long)(t_part - t_item0));
+        atomicAdd(T + 1, (unsigned long long)(t_bar1 - t_part));
+        atomicAdd(T + 2, (unsigned long long)(t_store - t_bar1));
+        atomicAdd(T + 3, (unsigned long long)(t_end - t_store));
+        atomicAdd(T + 4, 1ull);
+      }
+    }
+#endif
   }
 }
 

@@ -120,6 +120,7 @@ template __global__ void fused_generate_kernel<1, kPsfErf>(const FusedParams);
 // Host side: errors, workspace, plan, launch
 // ----------------------------------------------------------------------------
 thread_local std::string g_err;
+unsigned long long* g_timing = nullptr;   // PGB_PHASE_TIMING builds only
 std::atomic<long long> g_launches{0};
 
 struct Error {
@@ -589,6 +590,15 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.noise_std = (float)cfg->noise_std;
   P.out[0] = img1;
   P.out[1] = img2;
+#ifdef PGB_PHASE_TIMING
+  {
+    static unsigned long long* tbuf = nullptr;
+    if (!tbuf) PGB_CK(cudaMalloc(&tbuf, (size_t)148 * 8 * kBandWarps * 5 * 8));
+    PGB_CK(cudaMemsetAsync(tbuf, 0, (size_t)148 * 8 * kBandWarps * 5 * 8, stream));
+    P.timing = tbuf;
+    g_timing = tbuf;
+  }
+#endif
   BandFn fn = cfg->psf == PGB_PSF_ERF ? band_kernel<kPsfErf> : band_kernel<kPsfPoint>;
   const int ctas = band_resident_ctas(fn, bp.smem);
   const long long items = (long long)pairs * bp.tiles;
@@ -612,6 +622,15 @@ int pgb_patch_side(double max_diameter, double multiplier) {
 }
 
 int64_t pgb_launch_count(void) { return g_launches.load(); }
+
+// Debug (PGB_PHASE_TIMING builds): copy the per-CTA/warp phase counters of the
+// last generate launch; returns the number of uint64 written (0 otherwise).
+int pgb_debug_phase_timing(unsigned long long* out, int cap) {
+  if (!g_timing || !out) return 0;
+  const int n = std::min(cap, 148 * 8 * kBandWarps * 5);
+  if (cudaMemcpy(out, g_timing, (size_t)n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return n;
+}
 
 int pgb_plan(int height, int width, int64_t n_per_pair, double ppp_hi, int halo, int frames,
              pgb_plan_info* info) {
