@@ -39,6 +39,7 @@ constexpr int kBandThreads = 256;
 constexpr int kBandWarps = kBandThreads / 32;
 constexpr int kBandBlock = kBandThreads + 32;   // + one staging warp
 constexpr int kMaxCellBits = 14;
+constexpr int kTimingCtaBase = 148 * 8 * 8 * 5 / 2;   // PGB_PHASE_TIMING: per-CTA timestamps
 
 struct __align__(16) PairHdr {
   double ppp;      // realised seeding density
@@ -55,6 +56,7 @@ struct __align__(16) PairHdr {
 struct BandParams {
   int H, W;
   int TH, TW, AS, tiles_y, tiles_x, tiles;
+  int pad_rows;                // zero rows after the frame-2 accumulator (unpredicated splat windows)
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
   int n, pairs;
   long long pair_base;
@@ -308,6 +310,12 @@ __device__ void field_bound_chunk(const BandParams& P, int f, int part) {
 // Per-pair prologue (whole block, NT threads, `bins` = 2^(sy+sx) + 1 ints of
 // shared scratch): density, M, maximum diameter, the cell histogram -> per-cell
 // prefix and the particle -> cell array; pair_ready[pl] releases them.
+#ifdef PGB_PHASE_TIMING
+#define PGB_STAMP(k) do { if (P.timing && threadIdx.x == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); P.timing[kTimingCtaBase + 4 * 2048 + (size_t)blockIdx.x * 8 + (k)] = t_; } } while (0)
+#else
+#define PGB_STAMP(k) do { } while (0)
+#endif
 template <int NT>
 __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
   __shared__ int wsum[NT / 32];
@@ -331,6 +339,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
     scm = 0;
   }
   __syncthreads();
+  PGB_STAMP(0);
   const int M = sM;
   if (tid == 0) {
     // maximum diameter uniform: max of M uniforms = V^(1/M), on particle J
@@ -352,6 +361,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
     shd.dmax = dmax;
     // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
     shd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
+    PGB_STAMP(1);
   } else {
     // cell histogram of M iid labels (4 labels per Philox call)
     for (int q = tid - 1; q < (M + 3) >> 2; q += NT - 1) {
@@ -363,6 +373,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
     }
   }
   __syncthreads();
+  PGB_STAMP(2);
   int cm = 0;
   for (int i = tid; i < ncell; i += NT) cm = max(cm, bins[i]);
 #pragma unroll
@@ -371,6 +382,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
   int* pre = P.prefix + (size_t)pl * (ncell + 1);
   // scan in shared memory, then one coalesced copy out
   block_scan<NT>(bins, bins, ncell, wsum);
+  PGB_STAMP(3);
   for (int i = tid; i <= ncell; i += NT) pre[i] = bins[i];
   if (tid == 0) {
     PairHdr hd = shd;
@@ -386,6 +398,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
   for (int c = tid; c < ncell; c += NT)
     for (int j = bins[c]; j < bins[c + 1]; ++j) cof[j] = (unsigned short)c;
   __syncthreads();
+  PGB_STAMP(4);
   if (tid == 0 && P.pair_ready) {
     __threadfence();
     st_release(P.pair_ready + pl, 1);
@@ -415,6 +428,7 @@ struct ItemCfg {
   int pl, r0, r1, c0, c1;
   int cy0, cy1, cx0, cx1;
   int h, wt, shift, field, sep;
+  int var;                 // particle-loop variant: 8 * sep + WM (0 = dynamic windows)
   PairHdr hd;
 };
 
@@ -588,6 +602,99 @@ __device__ __forceinline__ void splat_point_sep(int* __restrict__ acc, int AS, i
   }
 }
 
+
+// Unpredicated point-PSF windows (WM = compile-time window bound, 1..7).
+// Every particle-frame adds all WM x WM slots; slots outside its clipped
+// window add exactly 0 (their factor is 0, resp. their exponent -inf), so no
+// per-slot branch is needed. Slots past the tile's last row / column land on
+// the next row or on the zero padding after the frame-2 accumulator
+// (pad_rows >= WM - 1 rows), always with value 0.
+template <int WM>
+__device__ __forceinline__ void splat_sep_u(int* __restrict__ acc, int AS, int ax, int ay, float fx,
+                                            float fy, float amp, float sx, float sy, int h, int r0,
+                                            int r1, int c0, int c1, int shift) {
+  const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
+  int rlo, clo, nr, nc;
+  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return;
+  const float dx0 = (float)(clo - ax) - fx;
+  const float dy0 = (float)(rlo - ay) - fy;
+  int* base = acc + (rlo - r0) * AS + (clo - c0);
+  const float isx = rcp_approx(sx), isy = rcp_approx(sy);
+  const float A = (0.5f * kLog2e) * isx * isx;
+  const float C = (0.5f * kLog2e) * isy * isy;
+  const float Ls = __log2f(amp) + (float)shift;
+  float X[WM], Y[WM];
+#pragma unroll
+  for (int j = 0; j < WM; ++j) {
+    const float dx = dx0 + (float)j;
+    const float xv = ex2_approx(fmaf(-A * dx, dx, Ls));
+    X[j] = j < nc ? xv : 0.f;
+    const float dy = dy0 + (float)j;
+    const float yv = ex2_approx(-C * dy * dy);
+    Y[j] = j < nr ? yv : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+    int* row = base + i * AS;
+#pragma unroll
+    for (int j = 0; j < WM; ++j)
+      atomicAdd(row + j, __float_as_int(fmaf(X[j], Y[i], 12582912.0f)) - 0x4B400000);
+  }
+}
+
+template <int WM>
+__device__ __forceinline__ void splat_point_u(int* __restrict__ acc, int AS, int ax, int ay, float fx,
+                                              float fy, float amp, float sx, float sy, float rho, int h,
+                                              int r0, int r1, int c0, int c1, int shift) {
+  const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
+  int rlo, clo, nr, nc;
+  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return;
+  const float dx0 = (float)(clo - ax) - fx;
+  const float dy0 = (float)(rlo - ay) - fy;
+  int* base = acc + (rlo - r0) * AS + (clo - c0);
+  const float isx = rcp_approx(sx), isy = rcp_approx(sy);
+  const float iq = rcp_approx(1.0f - rho * rho);
+  const float A = (0.5f * kLog2e) * iq * isx * isx;
+  const float C = (0.5f * kLog2e) * iq * isy * isy;
+  const float B = -kLog2e * rho * iq * isx * isy;
+  const float Ls = __log2f(amp) + (float)shift;
+  float ct[WM], bx[WM];
+#pragma unroll
+  for (int j = 0; j < WM; ++j) {
+    const float dx = dx0 + (float)j;
+    const float cv = fmaf(-A * dx, dx, Ls);
+    ct[j] = j < nc ? cv : -INFINITY;
+    bx[j] = B * dx;
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+    const float dy = dy0 + (float)i;
+    const float rv = -C * dy * dy;
+    const float rt = i < nr ? rv : -INFINITY;
+    int* row = base + i * AS;
+#pragma unroll
+    for (int j = 0; j < WM; ++j)
+      atomicAdd(row + j, round_small(ex2_approx(fmaf(-bx[j], dy, ct[j] + rt))));
+  }
+}
+
+// One particle-frame, variant fixed per item: SEP (rho == 0 everywhere),
+// WM (1..7 unpredicated windows; 0 = dynamic loops).
+template <int PSF, int SEP, int WM>
+__device__ __forceinline__ void splat_v(int* acc, int AS, int ax, int ay, float fx, float fy, float amp,
+                                        float sx, float sy, float rho, int h, int r0, int r1, int c0,
+                                        int c1, int shift, float scale) {
+  if constexpr (PSF == kPsfErf) {
+    splat_erf(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, scale);
+  } else if constexpr (WM == 0) {
+    splat_point<0>(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, shift);
+  } else if constexpr (SEP != 0) {
+    splat_sep_u<WM>(acc, AS, ax, ay, fx, fy, amp, sx, sy, h, r0, r1, c0, c1, shift);
+  } else {
+    splat_point_u<WM>(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, shift);
+  }
+}
+
 template <int PSF>
 __device__ __forceinline__ void splat_dispatch_b(int wt, int sep, int* acc, int AS, int ax, int ay,
                                                  float fx, float fy, float amp, float sx, float sy,
@@ -645,10 +752,10 @@ __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, cha
     v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
     v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
   } else {
-    v.x = fminf(fmaxf(fmaf(v.x, inv_scale, bg), 0.f), 1.f);
-    v.y = fminf(fmaxf(fmaf(v.y, inv_scale, bg), 0.f), 1.f);
-    v.z = fminf(fmaxf(fmaf(v.z, inv_scale, bg), 0.f), 1.f);
-    v.w = fminf(fmaxf(fmaf(v.w, inv_scale, bg), 0.f), 1.f);
+    v.x = __saturatef(fmaf(v.x, inv_scale, bg));   // clip(raw + offset, 0, 1): FFMA.SAT
+    v.y = __saturatef(fmaf(v.y, inv_scale, bg));
+    v.z = __saturatef(fmaf(v.z, inv_scale, bg));
+    v.w = __saturatef(fmaf(v.w, inv_scale, bg));
   }
   if (OUT == kOutF32) {
     __stcs(reinterpret_cast<float4*>(dst), v);
@@ -711,6 +818,25 @@ __device__ void band_store_vec(const BandParams& P, int* __restrict__ acc, int p
   }
 }
 
+// Full-width tile (c0 == 0, nc == W == AS): the tile is one contiguous run of
+// quads in shared memory and in the output; each thread strides the quads.
+template <int OUT, bool NOISE>
+__device__ __forceinline__ void band_store_lin(const BandParams& P, int* __restrict__ acc, int pl, int f,
+                                               int r0, int nr, float inv_scale) {
+  constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
+  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
+  const int nq = (nr * P.W) >> 2;
+  const uint32_t pix0 = (uint32_t)(r0 * P.W);
+  char* dst = static_cast<char*>(P.out[f]) + ((size_t)pl * (size_t)P.out_pair_elems + pix0) * ESZ;
+  int4* ap = reinterpret_cast<int4*>(acc);
+#pragma unroll 4
+  for (int q = threadIdx.x; q < nq; q += kBandThreads) {
+    const int4 a = ap[q];
+    ap[q] = make_int4(0, 0, 0, 0);
+    band_store_quad<OUT, NOISE>(P, a, dst + (size_t)q * 4 * ESZ, pix0 + 4u * q, f, gpair, inv_scale);
+  }
+}
+
 __device__ void band_store_scalar(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
                                   int nr, int c0, int nc, float inv_scale) {
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
@@ -745,6 +871,19 @@ __device__ void band_store(const BandParams& P, int* acc, int pl, int f, int r0,
                            float inv_scale) {
   const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
   const bool noise = P.noise_std > 0.f;
+  if (vec && c0 == 0 && nc == P.W && P.AS == P.W) {
+    switch (P.out_mode) {
+      case kOutRaw: band_store_lin<kOutRaw, false>(P, acc, pl, f, r0, nr, inv_scale); return;
+      case kOutF32:
+        if (noise) band_store_lin<kOutF32, true>(P, acc, pl, f, r0, nr, inv_scale);
+        else band_store_lin<kOutF32, false>(P, acc, pl, f, r0, nr, inv_scale);
+        return;
+      default:
+        if (noise) band_store_lin<kOutU16, true>(P, acc, pl, f, r0, nr, inv_scale);
+        else band_store_lin<kOutU16, false>(P, acc, pl, f, r0, nr, inv_scale);
+        return;
+    }
+  }
   if (vec) {
     switch (P.out_mode) {
       case kOutRaw: band_store_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
@@ -823,6 +962,8 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   ic.wt = max(1, wt);
   // uncorrelated particles (rho == 0 in both frames): separable splat
   ic.sep = (g.rho_lo == 0.f && g.rho_span == 0.f && !(g.f2_rho_std > 0.f)) ? 1 : 0;
+  const int wm = (P.psf == kPsfPoint && ic.wt <= 7 && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
+  ic.var = (P.psf == kPsfPoint ? 8 * ic.sep : 0) + wm;
 }
 
 // Warp 0: next item's parameters + particle segments (one per cell row of the
@@ -872,6 +1013,95 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
   }
 }
 
+// Worker warps: regenerate, advect and splat the particles of one item
+// (variant fixed per item, see ItemCfg::var).
+template <int PSF, int SEP, int WM>
+__device__ __forceinline__ void band_particles(const BandParams& P, BandShared* sh, int buf, long long item,
+                                               int* acc0, int* acc1) {
+  const GenCfg& g = P.g;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int CX = 1 << P.sx;
+  const ItemCfg& ic = sh->ic[buf];
+  const int pl = ic.pl;
+  const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
+  const int h = ic.h, shift = ic.shift;
+  const PairHdr& hd = ic.hd;
+  const float scale = (float)(1 << shift);
+  const float2* flow = P.flows + (size_t)ic.field * P.field_elems;
+  const unsigned short* cof = P.cell_of + (size_t)pl * P.n;
+  const RngKey key = band_key(P, pl);
+  int next_row = ic.cy0;   // first cell row of the current pass
+  for (;;) {
+    const int nseg = sh->nseg[buf];
+    const int N = sh->seg_off[buf][nseg];
+    const int* soff = sh->seg_off[buf];
+    const int* sst = sh->seg_start[buf];
+    // slot q -> particle index (segment search) -> its cell (L2 load); the
+    // next iteration's cell load is issued one iteration ahead
+    auto locate = [&](int q) {
+      int sg = 0;
+      if (nseg > 1) {
+        int hi = nseg - 1;
+        while (sg < hi) {
+          const int mid = (sg + hi + 1) >> 1;
+          if (soff[mid] <= q) sg = mid;
+          else hi = mid - 1;
+        }
+      }
+      return sst[sg] + (q - soff[sg]);
+    };
+    int gi_n = 0, cc_n = 0;
+    if (tid < N) {
+      gi_n = locate(tid);
+      cc_n = __ldcg(cof + gi_n);
+    }
+    // warp-uniform trip count + __syncwarp: lanes that skip a particle do
+    // not run ahead into the next iteration (keeps the warp converged)
+    for (int qb = 0; qb < N; qb += kBandThreads) {
+      const int q = qb + tid;
+      const int gi = gi_n, cc = cc_n;
+      if (q + kBandThreads < N) {
+        gi_n = locate(q + kBandThreads);
+        cc_n = __ldcg(cof + gi_n);
+      }
+      if (q < N) {
+        const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
+        const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
+        const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
+        int ax1, ay1, ax2, ay2;
+        float fx1, fy1, fx2, fy2;
+        fixed_anchor(X, ax1, fx1);
+        fixed_anchor(Y, ay1, fy1);
+        advect_fixed(g, flow, X, Y, ax1, fx1, ay1, fy1, ax2, fx2, ay2, fy2);
+        // geometric pre-test with the full patch window
+        const bool in1 = ay1 + h >= r0 && ay1 - h < r1 && ax1 + h >= c0 && ax1 - h < c1;
+        const bool in2 = ay2 + h >= r0 && ay2 - h < r1 && ax2 + h >= c0 && ax2 - h < c1;
+        if (in1 || in2) {
+          const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
+          const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
+          const float sig = __fmul_rn(d, g.inv_ratio);
+          Look lk;
+          seed_look(g, key, gi, sig, i0, lk);
+          if (in1 && lk.vis1 && lk.amp1 > 0.f)
+            splat_v<PSF, SEP, WM>(acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1, h, r0, r1,
+                                  c0, c1, shift, scale);
+          if (in2 && lk.vis2 && lk.amp2 > 0.f)
+            splat_v<PSF, SEP, WM>(acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2, lk.rho2, h, r0,
+                                  r1, c0, c1, shift, scale);
+        }
+      }
+      __syncwarp();
+    }
+    if (sh->rows_left[buf] <= 0) break;
+    // rare: more cell rows than one segment table -> worker warp 0 stages
+    // the next rows of this item (named barrier: workers only)
+    asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
+    next_row += kMaxSeg;
+    if (warp == 0) item_stage(P, item, sh, buf, next_row);
+    asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
+  }
+}
+
 template <int PSF>
 __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -880,9 +1110,12 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
   int* acc1 = acc0 + P.TH * P.AS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
-  const GenCfg& g = P.g;
-  const int CX = 1 << P.sx;
   const long long total_items = (long long)P.pairs * P.tiles;
+#ifdef PGB_PHASE_TIMING
+  auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; };
+  unsigned long long* CT = P.timing ? P.timing + kTimingCtaBase + (size_t)blockIdx.x * 4 : nullptr;
+  if (CT && tid == 0) CT[0] = gtime();
+#endif
   if (P.inline_prologue) {
     // prologue work items first (pairs, then flow-bound chunks); band items
     // wait on their readiness flags, so every wait targets work that some
@@ -898,15 +1131,22 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
       __syncthreads();
     }
   }
-  for (int e = tid; e < P.TH * P.AS * 2 / 4; e += kBandBlock)
+  // both frame accumulators + the zero padding behind them
+  for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 8) / 4; e += kBandBlock)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
   __syncthreads();
   // static schedule: items blockIdx.x, + gridDim.x, ...; the staging warp
   // prepares item k+1 (parameters + particle segments) while the workers
   // splat item k.
   long long item = blockIdx.x;
+#ifdef PGB_PHASE_TIMING
+  if (CT && tid == 0) CT[1] = gtime();
+#endif
   if (stager && item < total_items) item_stage(P, item, sh, 0, -1);
   __syncthreads();
+#ifdef PGB_PHASE_TIMING
+  if (CT && tid == 0) CT[2] = gtime();
+#endif
   for (int buf = 0; item < total_items; buf ^= 1, item += gridDim.x) {
     const long long nxt = item + gridDim.x;
     if (stager) {
@@ -921,81 +1161,17 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
     const ItemCfg& ic = sh->ic[buf];
     const int pl = ic.pl;
     const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
-    const int h = ic.h, wt = ic.wt, shift = ic.shift, sep = ic.sep;
-    const PairHdr& hd = ic.hd;
-    const float scale = (float)(1 << shift);
-    const float2* flow = P.flows + (size_t)ic.field * P.field_elems;
-    const unsigned short* cof = P.cell_of + (size_t)pl * P.n;
-    const RngKey key = band_key(P, pl);
-    int next_row = ic.cy0;   // first cell row of the current pass
-    for (;;) {
-      const int nseg = sh->nseg[buf];
-      const int N = sh->seg_off[buf][nseg];
-      const int* soff = sh->seg_off[buf];
-      const int* sst = sh->seg_start[buf];
-      // slot q -> particle index (segment search) -> its cell (L2 load); the
-      // next iteration's cell load is issued one iteration ahead
-      auto locate = [&](int q) {
-        int sg = 0;
-        if (nseg > 1) {
-          int hi = nseg - 1;
-          while (sg < hi) {
-            const int mid = (sg + hi + 1) >> 1;
-            if (soff[mid] <= q) sg = mid;
-            else hi = mid - 1;
-          }
-        }
-        return sst[sg] + (q - soff[sg]);
-      };
-      int gi_n = 0, cc_n = 0;
-      if (tid < N) {
-        gi_n = locate(tid);
-        cc_n = __ldcg(cof + gi_n);
+    const float scale = (float)(1 << ic.shift);
+    if constexpr (PSF == kPsfErf) {
+      band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1);
+    } else {
+      switch (ic.var) {
+#define PGB_V(S, W) case 8 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
+        PGB_V(0, 1) PGB_V(0, 2) PGB_V(0, 3) PGB_V(0, 4) PGB_V(0, 5) PGB_V(0, 6) PGB_V(0, 7)
+        PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6) PGB_V(1, 7)
+#undef PGB_V
+        default: band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1); break;
       }
-      // warp-uniform trip count + __syncwarp: lanes that skip a particle do
-      // not run ahead into the next iteration (keeps the warp converged)
-      for (int qb = 0; qb < N; qb += kBandThreads) {
-        const int q = qb + tid;
-        const int gi = gi_n, cc = cc_n;
-        if (q + kBandThreads < N) {
-          gi_n = locate(q + kBandThreads);
-          cc_n = __ldcg(cof + gi_n);
-        }
-        if (q < N) {
-          const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
-          const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
-          const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
-          int ax1, ay1, ax2, ay2;
-          float fx1, fy1, fx2, fy2;
-          fixed_anchor(X, ax1, fx1);
-          fixed_anchor(Y, ay1, fy1);
-          advect_fixed(g, flow, X, Y, ax1, fx1, ay1, fy1, ax2, fx2, ay2, fy2);
-          // geometric pre-test with the full patch window
-          const bool in1 = ay1 + h >= r0 && ay1 - h < r1 && ax1 + h >= c0 && ax1 - h < c1;
-          const bool in2 = ay2 + h >= r0 && ay2 - h < r1 && ax2 + h >= c0 && ax2 - h < c1;
-          if (in1 || in2) {
-            const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
-            const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
-            const float sig = __fmul_rn(d, g.inv_ratio);
-            Look lk;
-            seed_look(g, key, gi, sig, i0, lk);
-            if (in1 && lk.vis1 && lk.amp1 > 0.f)
-              splat_dispatch_b<PSF>(wt, sep, acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1,
-                                    h, r0, r1, c0, c1, shift, scale);
-            if (in2 && lk.vis2 && lk.amp2 > 0.f)
-              splat_dispatch_b<PSF>(wt, sep, acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2,
-                                    lk.rho2, h, r0, r1, c0, c1, shift, scale);
-          }
-        }
-        __syncwarp();
-      }
-      if (sh->rows_left[buf] <= 0) break;
-      // rare: more cell rows than one segment table -> worker warp 0 stages
-      // the next rows of this item (named barrier: workers only)
-      asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
-      next_row += kMaxSeg;
-      if (warp == 0) item_stage(P, item, sh, buf, next_row);
-      asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
     }
 #ifdef PGB_PHASE_TIMING
     const long long t_part = clock64();
@@ -1026,6 +1202,9 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
     }
 #endif
   }
+#ifdef PGB_PHASE_TIMING
+  if (CT && tid == 0) CT[3] = gtime();
+#endif
 }
 
 // Particle arrays of the generator (one block per pair): exactly the particles

@@ -397,7 +397,7 @@ int guarded(F&& f) {
 // Band generator (band.cuh): plan + launch
 // ----------------------------------------------------------------------------
 struct BandPlan {
-  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx;
+  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx, pad_rows;
   size_t smem;
 };
 
@@ -421,14 +421,20 @@ size_t band_acc_budget() {
 BandPlan make_band_plan(int H, int W, int halo) {
   BandPlan p{};
   cell_bits(H, W, p.sy, p.sx);
-  const size_t budget_ints = band_acc_budget() / 8;       // two frames of int32
+  // zero rows behind the accumulators for unpredicated splat windows (<= 7 wide)
+  p.pad_rows = std::min(6, 2 * halo);
+  const size_t budget_all = band_acc_budget() / 4;        // int32: two frames + padding
+  auto th_cap = [&](int AS) -> size_t {
+    const size_t pad = (size_t)p.pad_rows * AS + 8;
+    return budget_all > pad ? (budget_all - pad) / (2 * (size_t)AS) : 0;
+  };
   const double m = halo + 4.0;                             // typical reach beyond the tile
   int bestTW = 0, bestTH = 0;
   double best = 1e30;
   for (int tw = 4; ; tw *= 2) {
     const int TW = std::min(tw, (W + 3) / 4 * 4);
     const int AS = TW;
-    int THmax = (int)std::min<size_t>((size_t)H, budget_ints / AS);
+    int THmax = (int)std::min<size_t>((size_t)H, th_cap(AS));
     if (THmax >= 1) {
       const int ty = (H + THmax - 1) / THmax;
       const int TH = (H + ty - 1) / ty;
@@ -443,7 +449,7 @@ BandPlan make_band_plan(int H, int W, int halo) {
   PGB_REQUIRE(bestTW > 0, "band plan: image too large for the accumulator budget");
   if (const char* e = std::getenv("PGB_TILE")) {     // tuning override "TH,TW"
     int th = 0, tw = 0;
-    if (std::sscanf(e, "%d,%d", &th, &tw) == 2 && th > 0 && tw >= 4 && (size_t)th * tw <= budget_ints) {
+    if (std::sscanf(e, "%d,%d", &th, &tw) == 2 && th > 0 && tw >= 4 && (size_t)th <= th_cap((tw + 3) / 4 * 4)) {
       bestTH = std::min(th, H);
       bestTW = std::min(tw, (W + 3) / 4 * 4);
     }
@@ -454,7 +460,7 @@ BandPlan make_band_plan(int H, int W, int halo) {
   p.tiles_y = (H + p.TH - 1) / p.TH;
   p.tiles_x = (W + p.TW - 1) / p.TW;
   p.tiles = p.tiles_y * p.tiles_x;
-  p.smem = sizeof(BandShared) + (size_t)2 * p.TH * p.AS * 4;
+  p.smem = sizeof(BandShared) + ((size_t)(2 * p.TH + p.pad_rows) * p.AS + 8) * 4;
   PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
   return p;
 }
@@ -496,7 +502,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
                    bool launch) {
   P.H = cfg->height;
   P.W = cfg->width;
-  P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS;
+  P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS; P.pad_rows = bp.pad_rows;
   P.tiles_y = bp.tiles_y; P.tiles_x = bp.tiles_x; P.tiles = bp.tiles;
   P.sy = bp.sy; P.sx = bp.sx;
   P.n = cfg->n_capacity;

@@ -40,3 +40,15 @@ print(f"warps with items: {len(t)}, items/warp mean {t[:, 4].mean():.2f}")
 for k, nm in enumerate(names):
     print(f"{nm:28s} {100 * t[:, k].sum() / tot.sum():5.1f}%   mean cycles/item {t[:, k].sum() / t[:, 4].sum():9.0f}")
 print(f"per-warp total cycles: min {tot.min():.0f} max {tot.max():.0f} mean {tot.mean():.0f}")
+base = 148 * 8 * 8 * 5 // 2
+ct = buf[base:base + 4 * 2048].reshape(-1, 4)
+pt = buf[base + 4 * 2048:base + 4 * 2048 + 8 * 296].reshape(-1, 8).astype(np.float64)
+ct = ct[ct[:, 0] > 0].astype(np.float64)
+t0 = ct[:, 0].min()
+ct -= t0
+print(f"CTAs {len(ct)}: start max {ct[:,0].max()/1e3:.1f} us; prologue end mean {ct[:,1].mean()/1e3:.1f} max {ct[:,1].max()/1e3:.1f} us; "
+      f"loop start mean {ct[:,2].mean()/1e3:.1f} max {ct[:,2].max()/1e3:.1f} us; end mean {ct[:,3].mean()/1e3:.1f} max {ct[:,3].max()/1e3:.1f} us")
+pt = pt[pt[:, 0] > 0]
+pt = (pt - t0) / 1e3
+for k, nm in enumerate(["ppp/M done", "fp64 chain done", "histogram done", "scan done", "cof done"]):
+    print(f"prologue {nm:18s} mean {pt[:, k].mean():6.2f} us  max {pt[:, k].max():6.2f} us")
