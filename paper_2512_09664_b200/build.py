@@ -48,8 +48,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB_PATH
     tmp = LIB_PATH + ".tmp"
     extra = []
-    if os.environ.get("PGB_BAND_MINB"):      # tuning knob: band kernel CTAs per SM
-        extra.append(f"-DPGB_BAND_MINB={int(os.environ['PGB_BAND_MINB'])}")
+    if os.environ.get("PGB_BAND_MAXREG"):      # tuning knob: band kernel register cap
+        extra.append(f"-DPGB_BAND_MAXREG={int(os.environ['PGB_BAND_MAXREG'])}")
+    for knob in ("PGB_ILP", "PGB_TILE_CELLS"):
+        if os.environ.get(knob):
+            extra.append(f"-D{knob}={int(os.environ[knob])}")
     if os.environ.get("PGB_PHASE_TIMING"):   # debug: per-phase cycle counters in the band kernel
         extra.append("-DPGB_PHASE_TIMING")
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]

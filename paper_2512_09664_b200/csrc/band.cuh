@@ -32,8 +32,13 @@
 
 namespace pgb {
 
-#ifndef PGB_BAND_MINB
-#define PGB_BAND_MINB 2
+#ifndef PGB_ILP
+#define PGB_ILP 1   // particles regenerated per thread per loop iteration
+#endif
+#ifdef PGB_BAND_MAXREG
+#define PGB_BAND_BOUNDS __maxnreg__(PGB_BAND_MAXREG)
+#else
+#define PGB_BAND_BOUNDS __launch_bounds__(kBandBlock, 2)   // 2 CTAs x 288 threads per SM
 #endif
 constexpr int kBandThreads = 256;
 constexpr int kBandWarps = kBandThreads / 32;
@@ -57,6 +62,7 @@ struct BandParams {
   int H, W;
   int TH, TW, AS, tiles_y, tiles_x, tiles;
   int pad_rows;                // zero rows after the frame-2 accumulator (unpredicated splat windows)
+  int pro_smem;                // dynamic shared bytes of the standalone prologue kernel
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
   int n, pairs;
   long long pair_base;
@@ -70,7 +76,7 @@ struct BandParams {
   long long field_elems;
   float2* fbound;              // [num_fields] (max |u|, max |v|)
   int* prefix;                 // [pairs][2^(sy+sx) + 1] particle prefix per cell
-  unsigned short* cell_of;     // [pairs][n] seeding cell of every active particle
+  unsigned short* cell_of;     // [pairs][cof_stride(n)] seeding cell of every active particle
   PairHdr* hdr;                // [pairs]
   int* pair_ready;             // [pairs] prologue done (in-kernel prologue), else null
   int* fb_done;                // [num_fields] finished bound chunks, else null
@@ -85,6 +91,11 @@ struct BandParams {
   float* st_dmax;
   int* ticket;
 };
+
+// Per-pair cell prefix stride (ints): ncell + 1 entries, padded for 16-byte rows.
+__host__ __device__ __forceinline__ size_t pre_stride(int ncell) { return (size_t)ncell + 4; }
+// Per-pair particle -> cell stride (u16): n padded to 16-byte rows.
+__host__ __device__ __forceinline__ size_t cof_stride(int n) { return ((size_t)n + 7) & ~(size_t)7; }
 
 // ----------------------------------------------------------------------------
 // Seeding pieces shared by the band kernel and the particle-array kernel
@@ -142,7 +153,7 @@ __device__ __forceinline__ void seed_look(const GenCfg& g, const RngKey& key, in
   float rho = g.rho_lo, z1 = 0.f;
   bool vis1 = true, vis2 = true;
   if (g.need_b) {
-    const uint4 b = draw(key, (uint32_t)gi, kTagParticleB);
+    const uint4 b = philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagParticleB), g.rk);
     rho = lerpf_exact(g.rho_lo, g.rho_span, unit23(b.x));
     vis1 = (uint64_t)b.y >= g.hide_thr;   // apply_hiding (particles.py:139-147)
     vis2 = (uint64_t)b.z >= g.hide_thr;
@@ -151,7 +162,7 @@ __device__ __forceinline__ void seed_look(const GenCfg& g, const RngKey& key, in
   float sx2 = sig, sy2 = sig, i02 = i0, rho2 = rho;
   if (g.need_perturb) {
     // perturb_frame2 (particles.py:104-126)
-    const uint4 c = draw(key, (uint32_t)gi, kTagPerturb);
+    const uint4 c = philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagPerturb), g.rk);
     const float2 n01 = box_muller(c.x, c.y);
     const float2 n23 = box_muller(c.z, c.w);
     if (g.f2_sigma_std > 0.f) {
@@ -182,7 +193,7 @@ __device__ __forceinline__ void seed_particle(const BandParams& P, const PairHdr
                                               Particle& pt) {
   const GenCfg& g = P.g;
   const RngKey key = band_key(P, pl);
-  const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
+  const uint4 a = philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagParticleA), g.rk);
   const bool active = gi < hd.M;
   uint64_t X, Y;
   float d;
@@ -317,7 +328,7 @@ __device__ void field_bound_chunk(const BandParams& P, int f, int part) {
 #define PGB_STAMP(k) do { } while (0)
 #endif
 template <int NT>
-__device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
+__device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes) {
   __shared__ int wsum[NT / 32];
   __shared__ int sM;
   __shared__ PairHdr shd;
@@ -326,11 +337,11 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
   const int L = P.sy + P.sx;
   const int ncell = 1 << L;
   const RngKey key = band_key(P, pl);
-  for (int i = tid; i < ncell; i += NT) bins[i] = 0;
+  for (int i = tid; i < (ncell < 4 ? 4 : ncell); i += NT) bins[i] = 0;
   const GenCfg& g = P.g;
   if (tid == 0) {
     // seeding density and active count (particles.py:73-83)
-    const uint4 w = draw(key, 0u, kTagPair);
+    const uint4 w = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
     const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w.x, w.y));
     double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
     mm = fmin(fmax(mm, 0.0), (double)P.n);
@@ -350,7 +361,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
     shd.qmax = 0;
     float dmax = (float)g.d_hi;
     if (M > 0) {
-      const uint4 v = draw(key, 1u, kTagPair);
+      const uint4 v = philox_rk(make_uint4(1u, key.pair, key.batch, kTagPair), g.rk);
       const double V = u53_to_unit(v.x, v.y);
       shd.m = rexp(ddiv(rlog(V), (double)M));
       shd.J = (int)__umul64hi(((uint64_t)v.w << 32) | v.z, (uint64_t)M);
@@ -365,7 +376,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
   } else {
     // cell histogram of M iid labels (4 labels per Philox call)
     for (int q = tid - 1; q < (M + 3) >> 2; q += NT - 1) {
-      const uint4 w = draw(key, (uint32_t)q, kTagCell);
+      const uint4 w = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -374,29 +385,93 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins) {
   }
   __syncthreads();
   PGB_STAMP(2);
-  int cm = 0;
-  for (int i = tid; i < ncell; i += NT) cm = max(cm, bins[i]);
+  // One pass: per-thread runs of `per` cells (a multiple of 4, int4 loads),
+  // block exclusive scan -> prefix (int4 stores) and the particle -> cell
+  // array (counting-sort order: particles of cell c are pre[c] .. pre[c+1]-1),
+  // plus the maximum cell count.
+  constexpr int NW = NT / 32;
+  __shared__ int wmax[NW];
+  const int warp = tid >> 5;
+  const int nc4 = ncell < 4 ? 4 : ncell;
+  const int per = (((nc4 + NT - 1) / NT) + 3) & ~3;
+  const int b = min(nc4, tid * per), e = min(nc4, b + per);
+  int sum = 0, cm = 0;
+  for (int i = b; i < e; i += 4) {
+    const int4 v = *reinterpret_cast<const int4*>(bins + i);
+    sum += v.x + v.y + v.z + v.w;
+    cm = max(cm, max(max(v.x, v.y), max(v.z, v.w)));
+  }
+  int x = sum;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
-  if (lane == 0) atomicMax(&scm, cm);
-  int* pre = P.prefix + (size_t)pl * (ncell + 1);
-  // scan in shared memory, then one coalesced copy out
-  block_scan<NT>(bins, bins, ncell, wsum);
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(~0u, x, o);
+    if (lane >= o) x += y;
+    cm = max(cm, __shfl_xor_sync(~0u, cm, o));
+  }
+  if (lane == 31) wsum[warp] = x;
+  if (lane == 0) wmax[warp] = cm;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < NW ? wsum[lane] : 0;
+    int m = lane < NW ? wmax[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(~0u, v, o);
+      if (lane >= o) v += y;
+      m = max(m, __shfl_xor_sync(~0u, m, o));
+    }
+    if (lane < NW) wsum[lane] = v;
+    if (lane == 0) scm = m;
+  }
+  __syncthreads();
   PGB_STAMP(3);
-  for (int i = tid; i <= ncell; i += NT) pre[i] = bins[i];
+  int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
+  unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
+  int base = (warp ? wsum[warp - 1] : 0) + x - sum;
+  for (int i = b; i < e; i += 4) {
+    int4* bp = reinterpret_cast<int4*>(bins + i);
+    const int4 v = *bp;
+    const int4 o = make_int4(base, base + v.x, base + v.x + v.y, base + v.x + v.y + v.z);
+    *bp = o;   // exclusive prefix, in place
+    if (i + 4 <= ncell) {
+      *reinterpret_cast<int4*>(pre + i) = o;
+    } else {
+      const int oo[4] = {o.x, o.y, o.z, o.w};
+      for (int k = 0; i + k < ncell; ++k) pre[i + k] = oo[k];
+    }
+    base = o.w + v.w;
+  }
+  if (tid == 0) bins[ncell] = wsum[NW - 1];
+  __syncthreads();
+  PGB_STAMP(5);
+  // particle -> cell, one cell per thread (neighbouring lanes write
+  // neighbouring runs); staged in shared memory when it fits, then copied out
+  // with 16-byte stores
+  const int M16 = (M + 7) & ~7;
+  unsigned short* scof = reinterpret_cast<unsigned short*>(bins + ((nc4 + 4) & ~3));
+  const bool staged = (size_t)((nc4 + 4) & ~3) * 4 + (size_t)M16 * 2 <= (size_t)smem_bytes;
+  unsigned short* dstc = staged ? scof : cof;
+  for (int c = tid; c < ncell; c += NT) {
+    const int j1 = bins[c + 1];
+    for (int j = bins[c]; j < j1; ++j) dstc[j] = (unsigned short)c;
+  }
+  if (staged) {
+    if (tid < M16 - M) scof[M + tid] = 0;
+    __syncthreads();
+    PGB_STAMP(6);
+    for (int q = tid; q < M16 / 8; q += NT)
+      reinterpret_cast<int4*>(cof)[q] = reinterpret_cast<const int4*>(scof)[q];
+  }
   if (tid == 0) {
+    pre[ncell] = wsum[NW - 1];
     PairHdr hd = shd;
-    hd.cmax = scm;     // final after the scan's barriers
+    hd.cmax = scm;
     P.hdr[pl] = hd;
     if (P.st_ppp) P.st_ppp[pl] = hd.ppp;
     if (P.st_M) P.st_M[pl] = hd.M;
     if (P.st_side) P.st_side[pl] = hd.side;
     if (P.st_dmax) P.st_dmax[pl] = hd.dmax;
   }
-  // particle -> cell (counting-sort order: particles of cell c are pre[c] .. pre[c+1]-1)
-  unsigned short* cof = P.cell_of + (size_t)pl * P.n;
-  for (int c = tid; c < ncell; c += NT)
-    for (int j = bins[c]; j < bins[c + 1]; ++j) cof[j] = (unsigned short)c;
   __syncthreads();
   PGB_STAMP(4);
   if (tid == 0 && P.pair_ready) {
@@ -414,7 +489,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
     field_bound_chunk<kPrologueThreads>(P, fb / kFieldBlocks, fb % kFieldBlocks);
     return;
   }
-  pair_prologue<kPrologueThreads>(P, blockIdx.x, bins);
+  pair_prologue<kPrologueThreads>(P, blockIdx.x, bins, P.pro_smem);
 }
 
 // ----------------------------------------------------------------------------
@@ -746,7 +821,7 @@ __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, cha
   const float bg = P.bg_offset;
   if (NOISE) {
     const float sd = P.noise_std;
-    const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, pix >> 2);
+    const float4 nz = noise4_rk(P.g.rk, gpair, P.batch_lo, (uint32_t)f + 1, pix >> 2);
     v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
     v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
     v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
@@ -856,7 +931,7 @@ __device__ void band_store_scalar(const BandParams& P, int* __restrict__ acc, in
     } else {
       float nzv = 0.f;
       if (sd > 0.f) {
-        const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
+        const float4 nz = noise4_rk(P.g.rk, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
         const int jn = (int)(p & 3);
         nzv = jn == 0 ? nz.x : (jn == 1 ? nz.y : (jn == 2 ? nz.z : nz.w));
       }
@@ -975,7 +1050,7 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
   __syncwarp();
   const ItemCfg& ic = sh->ic[b];
   const int CX = 1 << P.sx;
-  const int* pre = P.prefix + (size_t)ic.pl * ((size_t)(1 << P.sy) * CX + 1);
+  const int* pre = P.prefix + (size_t)ic.pl * pre_stride((1 << P.sy) * CX);
   const bool full = ic.cx0 == 0 && ic.cx1 == CX - 1;
   const int y0 = row_lo < 0 ? ic.cy0 : row_lo;
   const int nrows = ic.cy1 - y0 + 1;
@@ -1013,14 +1088,52 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
   }
 }
 
+// One regenerated particle, both frames (what the splat needs).
+struct PFrames {
+  int ax1, ay1, ax2, ay2;
+  float fx1, fy1, fx2, fy2;
+  float amp1, amp2, sig, sx2, sy2, rho1, rho2;
+  bool on1, on2;
+};
+
+// Regenerate particle gi of seeding cell cc (branch-free, so that two
+// particles per thread interleave: two Philox chains and eight flow loads in
+// flight): position, advection, appearance, and whether each frame can touch
+// the tile [r0, r1) x [c0, c1) (full patch window).
+__device__ __forceinline__ void band_gen(const BandParams& P, const RngKey& key, const PairHdr& hd,
+                                         const float2* __restrict__ flow, int gi, int cc, int h, int r0,
+                                         int r1, int c0, int c1, PFrames& o) {
+  const GenCfg& g = P.g;
+  const int CX = 1 << P.sx;
+  const uint4 a = philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagParticleA), g.rk);
+  const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
+  const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
+  fixed_anchor(X, o.ax1, o.fx1);
+  fixed_anchor(Y, o.ay1, o.fy1);
+  advect_fixed(g, flow, X, Y, o.ax1, o.fx1, o.ay1, o.fy1, o.ax2, o.fx2, o.ay2, o.fy2);
+  const bool in1 = o.ay1 + h >= r0 && o.ay1 - h < r1 && o.ax1 + h >= c0 && o.ax1 - h < c1;
+  const bool in2 = o.ay2 + h >= r0 && o.ay2 - h < r1 && o.ax2 + h >= c0 && o.ax2 - h < c1;
+  const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
+  const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
+  o.sig = __fmul_rn(d, g.inv_ratio);
+  Look lk;
+  seed_look(g, key, gi, o.sig, i0, lk);
+  o.amp1 = lk.amp1; o.amp2 = lk.amp2;
+  o.sx2 = lk.sx2; o.sy2 = lk.sy2;
+  o.rho1 = lk.rho1; o.rho2 = lk.rho2;
+  o.on1 = in1 && lk.vis1 && lk.amp1 > 0.f;
+  o.on2 = in2 && lk.vis2 && lk.amp2 > 0.f;
+}
+
 // Worker warps: regenerate, advect and splat the particles of one item
-// (variant fixed per item, see ItemCfg::var).
+// (variant fixed per item, see ItemCfg::var). Two particles per thread per
+// iteration; the next iteration's particle -> cell loads are issued one
+// iteration ahead.
 template <int PSF, int SEP, int WM>
 __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* sh, int buf, long long item,
                                                int* acc0, int* acc1) {
-  const GenCfg& g = P.g;
+  constexpr int STEP = 2 * kBandThreads;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int CX = 1 << P.sx;
   const ItemCfg& ic = sh->ic[buf];
   const int pl = ic.pl;
   const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
@@ -1028,7 +1141,7 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
   const PairHdr& hd = ic.hd;
   const float scale = (float)(1 << shift);
   const float2* flow = P.flows + (size_t)ic.field * P.field_elems;
-  const unsigned short* cof = P.cell_of + (size_t)pl * P.n;
+  const unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
   const RngKey key = band_key(P, pl);
   int next_row = ic.cy0;   // first cell row of the current pass
   for (;;) {
@@ -1036,9 +1149,9 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
     const int N = sh->seg_off[buf][nseg];
     const int* soff = sh->seg_off[buf];
     const int* sst = sh->seg_start[buf];
-    // slot q -> particle index (segment search) -> its cell (L2 load); the
-    // next iteration's cell load is issued one iteration ahead
+    // slot q (clamped into [0, N)) -> particle index (segment search)
     auto locate = [&](int q) {
+      q = min(q, N - 1);
       int sg = 0;
       if (nseg > 1) {
         int hi = nseg - 1;
@@ -1050,47 +1163,67 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
       }
       return sst[sg] + (q - soff[sg]);
     };
-    int gi_n = 0, cc_n = 0;
-    if (tid < N) {
-      gi_n = locate(tid);
-      cc_n = __ldcg(cof + gi_n);
-    }
-    // warp-uniform trip count + __syncwarp: lanes that skip a particle do
-    // not run ahead into the next iteration (keeps the warp converged)
-    for (int qb = 0; qb < N; qb += kBandThreads) {
-      const int q = qb + tid;
-      const int gi = gi_n, cc = cc_n;
-      if (q + kBandThreads < N) {
-        gi_n = locate(q + kBandThreads);
-        cc_n = __ldcg(cof + gi_n);
+    if constexpr (PGB_ILP == 2) {
+      int gA = 0, cA = 0, gB = 0, cB = 0;
+      if (N > 0) {
+        gA = locate(tid);
+        gB = locate(tid + kBandThreads);
+        cA = __ldcg(cof + gA);
+        cB = __ldcg(cof + gB);
       }
-      if (q < N) {
-        const uint4 a = draw(key, (uint32_t)gi, kTagParticleA);
-        const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
-        const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
-        int ax1, ay1, ax2, ay2;
-        float fx1, fy1, fx2, fy2;
-        fixed_anchor(X, ax1, fx1);
-        fixed_anchor(Y, ay1, fy1);
-        advect_fixed(g, flow, X, Y, ax1, fx1, ay1, fy1, ax2, fx2, ay2, fy2);
-        // geometric pre-test with the full patch window
-        const bool in1 = ay1 + h >= r0 && ay1 - h < r1 && ax1 + h >= c0 && ax1 - h < c1;
-        const bool in2 = ay2 + h >= r0 && ay2 - h < r1 && ax2 + h >= c0 && ax2 - h < c1;
-        if (in1 || in2) {
-          const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
-          const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
-          const float sig = __fmul_rn(d, g.inv_ratio);
-          Look lk;
-          seed_look(g, key, gi, sig, i0, lk);
-          if (in1 && lk.vis1 && lk.amp1 > 0.f)
-            splat_v<PSF, SEP, WM>(acc0, P.AS, ax1, ay1, fx1, fy1, lk.amp1, sig, sig, lk.rho1, h, r0, r1,
-                                  c0, c1, shift, scale);
-          if (in2 && lk.vis2 && lk.amp2 > 0.f)
-            splat_v<PSF, SEP, WM>(acc1, P.AS, ax2, ay2, fx2, fy2, lk.amp2, lk.sx2, lk.sy2, lk.rho2, h, r0,
+      // warp-uniform trip count + __syncwarp: keeps the warp converged
+      for (int qb = 0; qb < N; qb += STEP) {
+        const int qa = qb + tid, qb2 = qa + kBandThreads;
+        const int giA = gA, ccA = cA, giB = gB, ccB = cB;
+        if (qb + STEP < N) {
+          gA = locate(qa + STEP);
+          gB = locate(qb2 + STEP);
+          cA = __ldcg(cof + gA);
+          cB = __ldcg(cof + gB);
+        }
+        PFrames A, B;
+        band_gen(P, key, hd, flow, giA, ccA, h, r0, r1, c0, c1, A);
+        band_gen(P, key, hd, flow, giB, ccB, h, r0, r1, c0, c1, B);
+        const bool okA = qa < N, okB = qb2 < N;
+        if (okA && A.on1)
+          splat_v<PSF, SEP, WM>(acc0, P.AS, A.ax1, A.ay1, A.fx1, A.fy1, A.amp1, A.sig, A.sig, A.rho1, h, r0, r1,
+                                c0, c1, shift, scale);
+        if (okA && A.on2)
+          splat_v<PSF, SEP, WM>(acc1, P.AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, A.rho2, h, r0, r1,
+                                c0, c1, shift, scale);
+        if (okB && B.on1)
+          splat_v<PSF, SEP, WM>(acc0, P.AS, B.ax1, B.ay1, B.fx1, B.fy1, B.amp1, B.sig, B.sig, B.rho1, h, r0, r1,
+                                c0, c1, shift, scale);
+        if (okB && B.on2)
+          splat_v<PSF, SEP, WM>(acc1, P.AS, B.ax2, B.ay2, B.fx2, B.fy2, B.amp2, B.sx2, B.sy2, B.rho2, h, r0, r1,
+                                c0, c1, shift, scale);
+        __syncwarp();
+      }
+    } else {
+      int gA = 0, cA = 0;
+      if (N > 0) {
+        gA = locate(tid);
+        cA = __ldcg(cof + gA);
+      }
+      for (int qb = 0; qb < N; qb += kBandThreads) {
+        const int qa = qb + tid;
+        const int giA = gA, ccA = cA;
+        if (qb + kBandThreads < N) {
+          gA = locate(qa + kBandThreads);
+          cA = __ldcg(cof + gA);
+        }
+        if (qa < N) {
+          PFrames A;
+          band_gen(P, key, hd, flow, giA, ccA, h, r0, r1, c0, c1, A);
+          if (A.on1)
+            splat_v<PSF, SEP, WM>(acc0, P.AS, A.ax1, A.ay1, A.fx1, A.fy1, A.amp1, A.sig, A.sig, A.rho1, h, r0,
+                                  r1, c0, c1, shift, scale);
+          if (A.on2)
+            splat_v<PSF, SEP, WM>(acc1, P.AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, A.rho2, h, r0,
                                   r1, c0, c1, shift, scale);
         }
+        __syncwarp();
       }
-      __syncwarp();
     }
     if (sh->rows_left[buf] <= 0) break;
     // rare: more cell rows than one segment table -> worker warp 0 stages
@@ -1103,7 +1236,7 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
 }
 
 template <int PSF>
-__global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const BandParams P) {
+__global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
   int* acc0 = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
@@ -1123,7 +1256,7 @@ __global__ void __launch_bounds__(kBandBlock, PGB_BAND_MINB) band_kernel(const B
     const int npro = P.pairs + P.field_cnt * kFieldBlocks;
     for (int w = blockIdx.x; w < npro; w += gridDim.x) {
       if (w < P.pairs) {
-        pair_prologue<kBandBlock>(P, w, acc0);
+        pair_prologue<kBandBlock>(P, w, acc0, ((2 * P.TH + P.pad_rows) * P.AS + 8) * 4);
       } else {
         const int fc = w - P.pairs;
         field_bound_chunk<kBandBlock>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
@@ -1213,7 +1346,7 @@ __global__ void sample_band_kernel(const BandParams P, pgb_particle_out O) {
   const int pl = blockIdx.x;
   const PairHdr hd = P.hdr[pl];
   const int ncell = 1 << (P.sy + P.sx);
-  const int* pre = P.prefix + (size_t)pl * (ncell + 1);
+  const int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
   const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
   for (int gi = threadIdx.x; gi < P.n; gi += blockDim.x) {
     int cy = 0, cx = 0;

@@ -55,6 +55,34 @@ PGB_HD uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// Device Philox with precomputed round keys (kernel parameters: each round's
+// key is a constant-bank operand) and one 32x32->64 multiply per product.
+struct PhiloxKeys {
+  uint32_t k0[10], k1[10];
+};
+
+PGB_HD PhiloxKeys philox_keys(uint32_t k0, uint32_t k1) {
+  PhiloxKeys K;
+  for (int r = 0; r < 10; ++r) {
+    K.k0[r] = k0;
+    K.k1[r] = k1;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+  return K;
+}
+
+__device__ __forceinline__ uint4 philox_rk(uint4 c, const PhiloxKeys& K) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c.x;
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ K.k0[r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ K.k1[r],
+                   (uint32_t)p0);
+  }
+  return c;
+}
+
 struct RngKey {
   uint32_t k0, k1;   // seed (lo, hi)
   uint32_t pair;     // global pair index within the batch

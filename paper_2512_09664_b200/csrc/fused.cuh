@@ -61,6 +61,7 @@ struct __align__(16) Rec {
 struct GenCfg {
   int H, W, n;
   uint32_t k0, k1;
+  PhiloxKeys rk;             // round keys of (k0, k1)
   double ppp_lo, ppp_hi;
   float d_lo, d_span, i0_lo, i0_span, rho_lo, rho_span, inv_ratio;
   double patch_mult, d_hi;
@@ -506,6 +507,14 @@ __device__ __forceinline__ int shift_for(int cnt, float amp_max) {
 // ----------------------------------------------------------------------------
 // Pixel noise: Philox(quad = p >> 2, pair, batch, kTagNoise + frame) ->
 // two Box-Muller pairs -> normals for pixels 4q .. 4q+3.
+__device__ __forceinline__ float4 noise4_rk(const PhiloxKeys& K, uint32_t gpair, uint32_t batch,
+                                            uint32_t frame, uint32_t quad) {
+  const uint4 w = philox_rk(make_uint4(quad, gpair, batch, kTagNoise + frame), K);
+  const float2 a = box_muller(w.x, w.y);
+  const float2 b = box_muller(w.z, w.w);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
 __device__ __forceinline__ float4 noise4(uint32_t k0, uint32_t k1, uint32_t gpair,
                                          uint32_t batch, uint32_t frame, uint32_t quad) {
   const uint4 w = philox4x32_10(make_uint4(quad, gpair, batch, kTagNoise + frame), k0, k1);

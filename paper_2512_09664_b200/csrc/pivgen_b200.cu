@@ -327,6 +327,7 @@ GenCfg gen_cfg_from(const pgb_config* c) {
   g.n = c->n_capacity;
   g.k0 = (uint32_t)(c->seed & 0xffffffffu);
   g.k1 = (uint32_t)(c->seed >> 32);
+  g.rk = philox_keys(g.k0, g.k1);
   g.ppp_lo = c->ppp_lo; g.ppp_hi = c->ppp_hi;
   // float32 ranges: lo + span * u with span = f32(hi) - f32(lo) (one rounding)
   volatile float dl = (float)c->d_lo, dh = (float)c->d_hi;
@@ -527,8 +528,8 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const size_t hdr_bytes = (size_t)pairs * sizeof(PairHdr);
   const size_t fb_bytes = (size_t)num_fields * sizeof(float2);
   const size_t flag_bytes = ((size_t)pairs + num_fields) * sizeof(int);
-  const size_t pre_bytes = (size_t)pairs * (ncell + 1) * sizeof(int);
-  const size_t cof_bytes = (size_t)pairs * cfg->n_capacity * sizeof(unsigned short);
+  const size_t pre_bytes = (size_t)pairs * pre_stride(ncell) * sizeof(int);
+  const size_t cof_bytes = (size_t)pairs * cof_stride(cfg->n_capacity) * sizeof(unsigned short);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
   DevWork& w = work_for_current();
   // [ticket | field bounds | ready flags] are zeroed per launch, then headers,
@@ -556,7 +557,9 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   }
   P.inline_prologue = 0;
   BandParams Q = P;
-  const size_t psmem = (size_t)(ncell + 1) * sizeof(int) + 16;
+  const size_t psmem = std::min<size_t>(kSmemMax, (size_t)((std::max(ncell, 4) + 4) & ~3) * sizeof(int) +
+                                                    ((size_t)cfg->n_capacity + 8) * sizeof(unsigned short));
+  Q.pro_smem = (int)psmem;
   static bool attr_set = false;
   if (!attr_set) {
     PGB_CK(cudaFuncSetAttribute((const void*)prologue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -32,7 +32,7 @@ fn.restype = ctypes.c_int
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = np.zeros(148 * 8 * 8 * 5, np.uint64)
 n = fn(buf.ctypes.data, buf.size)
-t = buf[:n].reshape(-1, 5).astype(np.float64)
+t = buf[:148 * 8 * 8 * 5 // 2].reshape(-1, 5).astype(np.float64)
 t = t[t[:, 4] > 0]
 tot = t[:, :4].sum(axis=1)
 names = ["particles", "barrier(after particles)", "store", "barrier(after store)"]
@@ -50,5 +50,5 @@ print(f"CTAs {len(ct)}: start max {ct[:,0].max()/1e3:.1f} us; prologue end mean 
       f"loop start mean {ct[:,2].mean()/1e3:.1f} max {ct[:,2].max()/1e3:.1f} us; end mean {ct[:,3].mean()/1e3:.1f} max {ct[:,3].max()/1e3:.1f} us")
 pt = pt[pt[:, 0] > 0]
 pt = (pt - t0) / 1e3
-for k, nm in enumerate(["ppp/M done", "fp64 chain done", "histogram done", "scan done", "cof done"]):
+for k, nm in enumerate(["ppp/M done", "fp64 chain done", "histogram done", "scan done", "cof done", "prefix stored", "cof staged"]):
     print(f"prologue {nm:18s} mean {pt[:, k].mean():6.2f} us  max {pt[:, k].max():6.2f} us")
