@@ -17,7 +17,8 @@ into 2^sy x 2^sx equal-area cells; the cell counts are the histogram of M iid
 uniform labels, particle g sits in the cell whose prefix range holds g, at a
 uniform position inside it. The maximum diameter uniform is drawn first
 (m = V^(1/M) with reproducible log/exp, on a uniform particle J); the others
-are m * U. Positions are fixed point (value / 2^33, anchor + float32 fraction);
+are uniform on [0, qmax]. Positions are Q17 fixed point (X / 2^17, X odd: the
+centre of a 2^-16 px bin; anchor + exact float32 fraction);
 every float32 step is a separately rounded numpy float32 op (no FMA), so
 positions, diameters, sigma, i0, rho, masks, M and side are bit-identical to
 the GPU; Box-Muller normals (frame-2 jitter) and the laser-sheet profile use
@@ -114,21 +115,18 @@ def lerp32(lo: float, hi: float, u: np.ndarray) -> np.ndarray:
     return (lo32 + span * u).astype(F32)
 
 
-def fixed_anchor(F: np.ndarray):
-    """Fixed-point coordinate F / 2^33 -> (anchor floor(v + 1/2), float32 fraction)."""
-    F = F.astype(np.uint64)
-    an = (F + np.uint64(1 << 32)) >> np.uint64(33)
-    diff = (F - (an << np.uint64(33))).astype(np.int64)
-    return an.astype(np.int64), (diff.astype(np.float64) * 2.0 ** -33).astype(F32)
+def fixed_anchor(X: np.ndarray):
+    """Q17 coordinate X / 2^17 -> (anchor floor(v + 1/2), float32 fraction) (fused.cuh fixed_anchor)."""
+    X = np.asarray(X).astype(np.int64)
+    an = (X + (1 << 16)) >> 17
+    return an, ((X - (an << 17)).astype(np.float64) * 2.0 ** -17).astype(F32)
 
 
-def fixed_cell(F: np.ndarray, n: int):
-    lim = np.uint64((n - 1) << 33)
-    xc = np.minimum(F.astype(np.uint64), lim)
-    c = np.minimum((xc >> np.uint64(33)).astype(np.int64), max(n - 2, 0))
-    t = ((xc - (c.astype(np.uint64) << np.uint64(33))).astype(np.int64).astype(np.float64)
-         * 2.0 ** -33).astype(F32)
-    return c, t
+def fixed_cell(X: np.ndarray, n: int):
+    """Clamped bilinear cell of a Q17 coordinate (fused.cuh fixed_cell)."""
+    xc = np.minimum(np.asarray(X).astype(np.int64), (n - 1) << 17)
+    c = np.minimum(xc >> 17, max(n - 2, 0))
+    return c, ((xc - (c << 17)).astype(np.float64) * 2.0 ** -17).astype(F32)
 
 
 def bilerp32(g00, g01, g10, g11, tx, ty):
@@ -237,10 +235,11 @@ def cell_prefix(cfg: "GenConfig", batch: int, gpair: int, M: int) -> np.ndarray:
 
 
 def cell_coord(cell, w, size: int, bits: int) -> np.ndarray:
-    """band.cuh cell_coord: ((cell << 33) + 2 w + 1) * size >> bits (uint64)."""
-    c = np.asarray(cell).astype(np.uint64)
-    return (((c << np.uint64(33)) + np.uint64(2) * np.asarray(w).astype(np.uint64) + np.uint64(1))
-            * np.uint64(size)) >> np.uint64(bits)
+    """fused.cuh cell_coord: Q17 X = 2 (cell CW + floor(w CW / 2^32)) + 1, CW = size << (16 - bits)."""
+    cw = np.int64(size << (16 - bits))
+    c = np.asarray(cell).astype(np.int64)
+    w = np.asarray(w).astype(np.int64)
+    return (((c * cw + ((w * cw) >> 32)) << 1) | 1).astype(np.int64)
 
 
 def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> dict:
@@ -259,13 +258,11 @@ def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> 
     cy, cx = cell >> sx, cell & ((1 << sx) - 1)
 
     a = px.draw(cfg.seed, gpair, batch, idx, px.TAG_PARTICLE_A)
-    X = np.where(active, cell_coord(cx, a[0], W, sx),
-                 (2 * a[0].astype(np.uint64) + np.uint64(1)) * np.uint64(W)).astype(np.uint64)
-    Y = np.where(active, cell_coord(cy, a[1], H, sy),
-                 (2 * a[1].astype(np.uint64) + np.uint64(1)) * np.uint64(H)).astype(np.uint64)
-    # diameters: particle J holds the maximum quantile, the others are m * U
-    u = hd["m"] * ((a[2].astype(np.float64) + 0.5) * 2.0 ** -32)
-    q = np.minimum(np.floor(u * 8388608.0), 0x7FFFFF).astype(np.int64)
+    X = np.where(active, cell_coord(cx, a[0], W, sx), cell_coord(0, a[0], W, 0))
+    Y = np.where(active, cell_coord(cy, a[1], H, sy), cell_coord(0, a[1], H, 0))
+    # diameters: particle J holds the maximum quantile qmax, the others are
+    # uniform on [0, qmax]: floor(w (qmax + 1) / 2^32)
+    q = (a[2].astype(np.int64) * (hd["qmax"] + 1)) >> 32
     if m > 0:
         q[hd["J"]] = hd["qmax"]
     d = np.where(active, lerp32(cfg.d_range[0], cfg.d_range[1], q_unit(q)),

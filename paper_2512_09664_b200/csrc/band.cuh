@@ -38,9 +38,15 @@ namespace pgb {
 #ifdef PGB_BAND_MAXREG
 #define PGB_BAND_BOUNDS __maxnreg__(PGB_BAND_MAXREG)
 #else
-#define PGB_BAND_BOUNDS __launch_bounds__(kBandBlock, 2)   // 2 CTAs x 288 threads per SM
+#ifndef PGB_BAND_MINB
+#define PGB_BAND_MINB 2
 #endif
-constexpr int kBandThreads = 256;
+#define PGB_BAND_BOUNDS __launch_bounds__(kBandBlock, PGB_BAND_MINB)   // 2 CTAs x 288 threads per SM
+#endif
+#ifndef PGB_WORKER_WARPS
+#define PGB_WORKER_WARPS 8
+#endif
+constexpr int kBandThreads = 32 * PGB_WORKER_WARPS;
 constexpr int kBandWarps = kBandThreads / 32;
 constexpr int kBandBlock = kBandThreads + 32;   // + one staging warp
 constexpr int kMaxCellBits = 14;
@@ -61,6 +67,12 @@ struct __align__(16) PairHdr {
 struct BandParams {
   int H, W;
   int TH, TW, AS, tiles_y, tiles_x, tiles;
+  // items: (pair, tile) for item < split_base; the remaining tiles are split
+  // into split_s row parts each (the last, partial round of the static
+  // schedule spread over all CTAs); total_items = split_base + rem * split_s
+  long long split_base, total_items;
+  int split_s;
+  int pro_stride;              // band tickets between two next-batch prologue tickets
   int pad_rows;                // zero rows after the frame-2 accumulator (unpredicated splat windows)
   int pro_smem;                // dynamic shared bytes of the standalone prologue kernel
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
@@ -80,7 +92,14 @@ struct BandParams {
   PairHdr* hdr;                // [pairs]
   int* pair_ready;             // [pairs] prologue done (in-kernel prologue), else null
   int* fb_done;                // [num_fields] finished bound chunks, else null
-  int inline_prologue;         // band kernel runs the prologue work items itself
+  int inline_prologue;         // band kernel runs prologue work items (field bounds; pairs if inline_pairs)
+  int inline_pairs;            // this batch's pair prologue runs in this launch (else precomputed)
+  int tma_store;               // full-width f32 tiles leave through TMA bulk stores
+  int ablate;                  // debug timing only (PGB_ABLATE): 1 no particles, 2 no splat, 4 no store
+  PairHdr* nx_hdr;             // next batch's pair prologue (tail work of this launch), or null
+  int* nx_prefix;
+  unsigned short* nx_cof;
+  uint32_t nx_batch_lo;
   int field_lo, field_cnt;     // flow fields read by this pair range
   unsigned long long* timing;  // optional per-CTA phase cycle counters (PGB_PHASE_TIMING)
   void* out[2];
@@ -104,18 +123,10 @@ __device__ __forceinline__ RngKey band_key(const BandParams& P, int pl) {
   return RngKey{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
 }
 
-// Fixed-point position (value / 2^33) of a particle of cell (cy, cx):
-// y = (cy + (2w + 1) / 2^33) H / 2^sy, rounded down to 2^-33.
-__device__ __forceinline__ uint64_t cell_coord(uint32_t cell, uint32_t w, int size, int bits) {
-  return ((((uint64_t)cell << 33) + 2ull * w + 1ull) * (uint64_t)size) >> bits;
-}
-
-// 23-bit diameter quantile of particle g (the maximum sits on particle J).
+// 23-bit diameter quantile of particle g: the maximum qmax sits on particle J,
+// the others are uniform on [0, qmax] (floor(w (qmax + 1) / 2^32)).
 __device__ __forceinline__ int diam_q(const PairHdr& hd, int g, uint32_t wz) {
-  if (g == hd.J) return hd.qmax;
-  const double u = __dmul_rn(hd.m, ((double)wz + 0.5) * 0x1p-32);
-  const int q = (int)floor(u * 8388608.0);
-  return q < 0x7fffff ? q : 0x7fffff;
+  return g == hd.J ? hd.qmax : (int)__umulhi(wz, (uint32_t)hd.qmax + 1u);
 }
 
 __device__ __forceinline__ float q_to_unit(int q) { return ((float)q + 0.5f) * 0x1p-23f; }
@@ -123,7 +134,7 @@ __device__ __forceinline__ float q_to_unit(int q) { return ((float)q + 0.5f) * 0
 // Advection of a fixed-point point: bilinear, edge-clamped (flowfield.py:207-232)
 // in float32, then the new anchor/fraction (see fused.cuh gen_particle).
 __device__ __forceinline__ void advect_fixed(const GenCfg& g, const float2* __restrict__ flow,
-                                             uint64_t X, uint64_t Y, int ax, float fx, int ay,
+                                             uint32_t X, uint32_t Y, int ax, float fx, int ay,
                                              float fy, int& ax2, float& fx2, int& ay2, float& fy2) {
   int cx, cy;
   float tx, ty;
@@ -195,7 +206,7 @@ __device__ __forceinline__ void seed_particle(const BandParams& P, const PairHdr
   const RngKey key = band_key(P, pl);
   const uint4 a = philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagParticleA), g.rk);
   const bool active = gi < hd.M;
-  uint64_t X, Y;
+  uint32_t X, Y;
   float d;
   if (active) {
     X = cell_coord((uint32_t)cx, a.x, g.W, P.sx);
@@ -203,8 +214,8 @@ __device__ __forceinline__ void seed_particle(const BandParams& P, const PairHdr
     d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
   } else {
     // inactive capacity slots: full-image uniforms, never rendered
-    X = (2ull * a.x + 1ull) * (uint64_t)g.W;
-    Y = (2ull * a.y + 1ull) * (uint64_t)g.H;
+    X = cell_coord(0u, a.x, g.W, 0);
+    Y = cell_coord(0u, a.y, g.H, 0);
     d = lerpf_exact(g.d_lo, g.d_span, unit23(a.z));
   }
   const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
@@ -327,8 +338,33 @@ __device__ void field_bound_chunk(const BandParams& P, int f, int part) {
 #else
 #define PGB_STAMP(k) do { } while (0)
 #endif
+__device__ __forceinline__ void write_stats(const BandParams& P, int pl, const PairHdr& hd) {
+  if (P.st_ppp) P.st_ppp[pl] = hd.ppp;
+  if (P.st_M) P.st_M[pl] = hd.M;
+  if (P.st_side) P.st_side[pl] = hd.side;
+  if (P.st_dmax) P.st_dmax[pl] = hd.dmax;
+}
+
+// Where a pair prologue writes: this batch's tables (+ readiness flag and
+// stats), or the next batch's (cross-launch pipeline, no flag / stats).
+struct ProOut {
+  PairHdr* hdr;
+  int* prefix;
+  unsigned short* cof;
+  uint32_t batch;
+  int* ready;
+  bool stats;
+};
+
+__device__ __forceinline__ ProOut pro_cur(const BandParams& P) {
+  return ProOut{P.hdr, P.prefix, P.cell_of, P.batch_lo, P.pair_ready, true};
+}
+__device__ __forceinline__ ProOut pro_next(const BandParams& P) {
+  return ProOut{P.nx_hdr, P.nx_prefix, P.nx_cof, P.nx_batch_lo, nullptr, false};
+}
+
 template <int NT>
-__device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes) {
+__device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes, const ProOut out) {
   __shared__ int wsum[NT / 32];
   __shared__ int sM;
   __shared__ PairHdr shd;
@@ -336,7 +372,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
   const int tid = threadIdx.x, lane = tid & 31;
   const int L = P.sy + P.sx;
   const int ncell = 1 << L;
-  const RngKey key = band_key(P, pl);
+  const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), out.batch};
   for (int i = tid; i < (ncell < 4 ? 4 : ncell); i += NT) bins[i] = 0;
   const GenCfg& g = P.g;
   if (tid == 0) {
@@ -351,6 +387,9 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
   }
   __syncthreads();
   PGB_STAMP(0);
+#ifdef PGB_PHASE_TIMING
+  const long long c0_ = clock64();
+#endif
   const int M = sM;
   if (tid == 0) {
     // maximum diameter uniform: max of M uniforms = V^(1/M), on particle J
@@ -401,6 +440,14 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
     sum += v.x + v.y + v.z + v.w;
     cm = max(cm, max(max(v.x, v.y), max(v.z, v.w)));
   }
+  {
+    // zero the staged particle -> cell slots (marked in pass 2)
+    const int M16z = (M + 7) & ~7;
+    const int off = ((nc4 + 4) & ~3) * 4;
+    if ((size_t)off + (size_t)M16z * 2 <= (size_t)smem_bytes)
+      for (int q = tid; q < M16z / 8; q += NT)
+        reinterpret_cast<int4*>(reinterpret_cast<char*>(bins) + off)[q] = make_int4(0, 0, 0, 0);
+  }
   int x = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -425,8 +472,15 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
   }
   __syncthreads();
   PGB_STAMP(3);
-  int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
-  unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
+  int* pre = out.prefix + (size_t)pl * pre_stride(ncell);
+  unsigned short* cof = out.cof + (size_t)pl * cof_stride(P.n);
+  // particle -> cell (counting-sort order: particles of cell c are pre[c] ..
+  // pre[c+1]-1). Staged in shared memory when it fits: mark the first slot
+  // of every non-empty cell with the cell id (slots zeroed in pass 1), then a
+  // block max-scan fills the runs; else one cell per thread into global memory.
+  const int M16 = (M + 7) & ~7;
+  unsigned short* scof = reinterpret_cast<unsigned short*>(bins + ((nc4 + 4) & ~3));
+  const bool staged = (size_t)((nc4 + 4) & ~3) * 4 + (size_t)M16 * 2 <= (size_t)smem_bytes;
   int base = (warp ? wsum[warp - 1] : 0) + x - sum;
   for (int i = b; i < e; i += 4) {
     int4* bp = reinterpret_cast<int4*>(bins + i);
@@ -439,44 +493,83 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
       const int oo[4] = {o.x, o.y, o.z, o.w};
       for (int k = 0; i + k < ncell; ++k) pre[i + k] = oo[k];
     }
+    if (staged) {
+      if (v.x) scof[o.x] = (unsigned short)i;
+      if (v.y) scof[o.y] = (unsigned short)(i + 1);
+      if (v.z) scof[o.z] = (unsigned short)(i + 2);
+      if (v.w) scof[o.w] = (unsigned short)(i + 3);
+    }
     base = o.w + v.w;
   }
   if (tid == 0) bins[ncell] = wsum[NW - 1];
   __syncthreads();
   PGB_STAMP(5);
-  // particle -> cell, one cell per thread (neighbouring lanes write
-  // neighbouring runs); staged in shared memory when it fits, then copied out
-  // with 16-byte stores
-  const int M16 = (M + 7) & ~7;
-  unsigned short* scof = reinterpret_cast<unsigned short*>(bins + ((nc4 + 4) & ~3));
-  const bool staged = (size_t)((nc4 + 4) & ~3) * 4 + (size_t)M16 * 2 <= (size_t)smem_bytes;
-  unsigned short* dstc = staged ? scof : cof;
-  for (int c = tid; c < ncell; c += NT) {
-    const int j1 = bins[c + 1];
-    for (int j = bins[c]; j < j1; ++j) dstc[j] = (unsigned short)c;
-  }
   if (staged) {
-    if (tid < M16 - M) scof[M + tid] = 0;
+    // inclusive max-scan of the marks: per-thread runs of K slots (16-byte
+    // chunks), warp shuffles, one block combine
+    const int K = (((M16 + NT - 1) / NT) + 7) & ~7;
+    const int jb = min(M16, tid * K), je = min(M16, jb + K);
+    int mx = 0;
+    for (int j = jb; j < je; j += 8) {
+      const int4 w4 = *reinterpret_cast<const int4*>(scof + j);
+      const int ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mx = max(mx, max(ws[k] & 0xffff, (int)((unsigned)ws[k] >> 16)));
+    }
+    int y = mx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(~0u, y, o);
+      if (lane >= o) y = max(y, t);
+    }
+    if (lane == 31) wmax[warp] = y;
     __syncthreads();
+    if (warp == 0) {
+      int m = lane < NW ? wmax[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(~0u, m, o);
+        if (lane >= o) m = max(m, t);
+      }
+      if (lane < NW) wmax[lane] = m;
+    }
+    __syncthreads();
+    int run = max(warp ? wmax[warp - 1] : 0, __shfl_up_sync(~0u, y, 1) * (lane > 0));
+    for (int j = jb; j < je; j += 8) {
+      const int4 w4 = *reinterpret_cast<const int4*>(scof + j);
+      const int ws[4] = {w4.x, w4.y, w4.z, w4.w};
+      int os[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int lo = run = max(run, ws[k] & 0xffff);
+        const int hi = run = max(run, (int)((unsigned)ws[k] >> 16));
+        os[k] = lo | (hi << 16);
+      }
+      *reinterpret_cast<int4*>(cof + j) = make_int4(os[0], os[1], os[2], os[3]);
+    }
     PGB_STAMP(6);
-    for (int q = tid; q < M16 / 8; q += NT)
-      reinterpret_cast<int4*>(cof)[q] = reinterpret_cast<const int4*>(scof)[q];
+  } else {
+    for (int c = tid; c < ncell; c += NT) {
+      const int j1 = bins[c + 1];
+      for (int j = bins[c]; j < j1; ++j) cof[j] = (unsigned short)c;
+    }
   }
   if (tid == 0) {
     pre[ncell] = wsum[NW - 1];
     PairHdr hd = shd;
     hd.cmax = scm;
-    P.hdr[pl] = hd;
-    if (P.st_ppp) P.st_ppp[pl] = hd.ppp;
-    if (P.st_M) P.st_M[pl] = hd.M;
-    if (P.st_side) P.st_side[pl] = hd.side;
-    if (P.st_dmax) P.st_dmax[pl] = hd.dmax;
+    out.hdr[pl] = hd;
+    if (out.stats) write_stats(P, pl, hd);
   }
   __syncthreads();
   PGB_STAMP(4);
-  if (tid == 0 && P.pair_ready) {
+#ifdef PGB_PHASE_TIMING
+  if (P.timing && threadIdx.x == 0)
+    P.timing[kTimingCtaBase + 4 * 2048 + (size_t)blockIdx.x * 8 + 7] = (unsigned long long)(clock64() - c0_);
+#endif
+  if (tid == 0 && out.ready) {
     __threadfence();
-    st_release(P.pair_ready + pl, 1);
+    st_release(out.ready + pl, 1);
   }
 }
 
@@ -489,7 +582,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
     field_bound_chunk<kPrologueThreads>(P, fb / kFieldBlocks, fb % kFieldBlocks);
     return;
   }
-  pair_prologue<kPrologueThreads>(P, blockIdx.x, bins, P.pro_smem);
+  pair_prologue<kPrologueThreads>(P, blockIdx.x, bins, P.pro_smem, pro_cur(P));
 }
 
 // ----------------------------------------------------------------------------
@@ -504,11 +597,15 @@ struct ItemCfg {
   int cy0, cy1, cx0, cx1;
   int h, wt, shift, field, sep;
   int var;                 // particle-loop variant: 8 * sep + WM (0 = dynamic windows)
+  int kind;                // kItemBand, kItemPro (next batch's pair prologue), kItemEnd
+  long long item;          // band item index (kItemBand) / pair (kItemPro)
   PairHdr hd;
 };
+enum { kItemBand = 0, kItemPro = 1, kItemEnd = 2 };
 
 struct __align__(16) BandShared {
   int wsum[kBandWarps];
+
   int nseg[2];                       // segments of the staged pass
   int rows_left[2];                  // cell rows not yet staged (rare multi-pass items)
   ItemCfg ic[2];
@@ -975,6 +1072,92 @@ __device__ void band_store(const BandParams& P, int* acc, int pl, int f, int r0,
   band_store_scalar(P, acc, pl, f, r0, nr, c0, nc, inv_scale);
 }
 
+
+// ---- TMA bulk store of finalized full-width tiles ----------------------------
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(sa), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Finalize one full-width frame tile in place (int accumulator -> float32 image
+// values: raw * 2^-s, or clip(raw + offset + noise, 0, 1)).
+template <int OUT, bool NOISE>
+__device__ __forceinline__ void band_finalize_inplace(const BandParams& P, int* __restrict__ acc, int pl, int f,
+                                                      int r0, int nr, float inv_scale) {
+  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
+  const int nq = (nr * P.W) >> 2;
+  const uint32_t pix0 = (uint32_t)(r0 * P.W);
+  int4* ap = reinterpret_cast<int4*>(acc);
+  const float bg = P.bg_offset;
+#pragma unroll 4
+  for (int q = threadIdx.x; q < nq; q += kBandThreads) {
+    const int4 a = ap[q];
+    float4 v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
+    if (OUT == kOutRaw) {
+      v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
+    } else if (NOISE) {
+      const float sd = P.noise_std;
+      const float4 nz = noise4_rk(P.g.rk, gpair, P.batch_lo, (uint32_t)f + 1, (pix0 >> 2) + q);
+      v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
+      v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
+      v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
+      v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
+    } else {
+      v.x = __saturatef(fmaf(v.x, inv_scale, bg));
+      v.y = __saturatef(fmaf(v.y, inv_scale, bg));
+      v.z = __saturatef(fmaf(v.z, inv_scale, bg));
+      v.w = __saturatef(fmaf(v.w, inv_scale, bg));
+    }
+    reinterpret_cast<float4*>(ap)[q] = v;
+  }
+}
+
+// Both frames of a full-width item: finalize in place, one thread issues the
+// two bulk stores (TMA engine, no per-quad global store instructions) and
+// waits until they have read shared memory, then the accumulators are zeroed.
+// Workers only (named barrier 1).
+template <int OUT, bool NOISE>
+__device__ void band_store_tma(const BandParams& P, int* acc0, int* acc1, int pl, int r0, int nr,
+                               float inv_scale) {
+  band_finalize_inplace<OUT, NOISE>(P, acc0, pl, 0, r0, nr, inv_scale);
+  band_finalize_inplace<OUT, NOISE>(P, acc1, pl, 1, r0, nr, inv_scale);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
+  if (threadIdx.x == 0) {
+    const size_t off = ((size_t)pl * (size_t)P.out_pair_elems + (size_t)r0 * P.W) * 4;
+    const unsigned bytes = (unsigned)nr * (unsigned)P.W * 4u;
+    bulk_store(static_cast<char*>(P.out[0]) + off, acc0, bytes);
+    bulk_store(static_cast<char*>(P.out[1]) + off, acc1, bytes);
+    bulk_commit_wait_read();
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
+  const int nq = (nr * P.W) >> 2;
+  int4* a0 = reinterpret_cast<int4*>(acc0);
+  int4* a1 = reinterpret_cast<int4*>(acc1);
+#pragma unroll 4
+  for (int q = threadIdx.x; q < nq; q += kBandThreads) {
+    a0[q] = make_int4(0, 0, 0, 0);
+    a1[q] = make_int4(0, 0, 0, 0);
+  }
+}
+
+// Returns true when the item was stored through the TMA path.
+__device__ __forceinline__ bool band_store_items_tma(const BandParams& P, int* acc0, int* acc1, int pl, int r0,
+                                                     int nr, int c0, int nc, float inv_scale) {
+  if (!(P.tma_store && c0 == 0 && nc == P.W && P.AS == P.W && (P.W & 3) == 0 && P.out_mode != kOutU16))
+    return false;
+  if (nr <= 0) return true;
+  if (P.out_mode == kOutRaw) band_store_tma<kOutRaw, false>(P, acc0, acc1, pl, r0, nr, inv_scale);
+  else if (P.noise_std > 0.f) band_store_tma<kOutF32, true>(P, acc0, acc1, pl, r0, nr, inv_scale);
+  else band_store_tma<kOutF32, false>(P, acc0, acc1, pl, r0, nr, inv_scale);
+  return true;
+}
+
 // Range of seeding cells [lo, hi] whose span [k*s, (k+1)*s) meets [a, b).
 __device__ __forceinline__ void cell_range(double a, double b, double s, int n, int& lo, int& hi) {
   const double fa = floor(fmax(a, 0.0) / s);
@@ -989,19 +1172,34 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   const GenCfg& g = P.g;
   const int CY = 1 << P.sy, CX = 1 << P.sx;
   const double ch = (double)g.H / (double)CY, cw = (double)g.W / (double)CX;
-  const int pl = (int)(item / P.tiles);
-  const int t = (int)(item - (long long)pl * P.tiles);
+  long long ti = item;
+  int sub = 0, nsub = 1;
+  if (item >= P.split_base) {
+    const long long j = item - P.split_base;
+    ti = P.split_base + j / P.split_s;
+    sub = (int)(j % P.split_s);
+    nsub = P.split_s;
+  }
+  const int pl = (int)(ti / P.tiles);
+  const int t = (int)(ti - (long long)pl * P.tiles);
   const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
   ic.pl = pl;
   ic.r0 = ty * P.TH;
   ic.r1 = min(ic.r0 + P.TH, g.H);
+  if (nsub > 1) {
+    const int ph = (ic.r1 - ic.r0 + nsub - 1) / nsub;
+    const int a = min(ic.r1, ic.r0 + sub * ph);
+    ic.r1 = min(ic.r1, a + ph);
+    ic.r0 = a;   // may be empty (r0 == r1): no particles, no store
+  }
   ic.c0 = tx * P.TW;
   ic.c1 = min(ic.c0 + P.TW, g.W);
   ic.field = (int)((P.pair_base + pl) / P.pairs_per_field);
   if (P.inline_prologue) {
     // produced inside this launch by other CTAs (their first work items)
     int ns = 32;
-    while (ld_acquire_b(P.pair_ready + pl) == 0) { __nanosleep(ns); ns = min(ns * 2, 256); }
+    if (P.inline_pairs)
+      while (ld_acquire_b(P.pair_ready + pl) == 0) { __nanosleep(ns); ns = min(ns * 2, 256); }
     while (ld_acquire_b(P.fb_done + ic.field) < kFieldBlocks) { __nanosleep(ns); ns = min(ns * 2, 256); }
   }
   {
@@ -1046,7 +1244,7 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
 __device__ __forceinline__ void item_stage(const BandParams& P, long long item, BandShared* sh, int b,
                                            int row_lo) {
   const int lane = threadIdx.x & 31;
-  if (lane == 0 && row_lo < 0) item_setup(P, item, sh->ic[b]);
+  if (lane == 0 && row_lo == -1) item_setup(P, item, sh->ic[b]);
   __syncwarp();
   const ItemCfg& ic = sh->ic[b];
   const int CX = 1 << P.sx;
@@ -1054,7 +1252,7 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
   const bool full = ic.cx0 == 0 && ic.cx1 == CX - 1;
   const int y0 = row_lo < 0 ? ic.cy0 : row_lo;
   const int nrows = ic.cy1 - y0 + 1;
-  const int nseg = full ? 1 : min(nrows, kMaxSeg);
+  const int nseg = ic.r0 >= ic.r1 ? 0 : (full ? 1 : min(nrows, kMaxSeg));   // empty split part: nothing
   int base = 0;
   for (int s0 = 0; s0 < nseg; s0 += 32) {
     const int sidx = s0 + lane;
@@ -1088,6 +1286,51 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
   }
 }
 
+// Dynamic schedule (stager lane 0 takes a ticket): the first gridDim.x
+// tickets are band items; after them, when the next batch's pair prologues
+// ride along (cross-launch pipeline), one prologue ticket follows every
+// `pro_stride` band tickets, so that prologue work (latency-bound) overlaps the
+// band work of the co-resident CTA; then the remaining band items.
+__device__ __forceinline__ void ticket_item(const BandParams& P, long long t, int& kind, long long& idx) {
+  const long long B = P.total_items, G = gridDim.x;
+  const long long npro = P.nx_hdr ? P.pairs : 0;
+  kind = kItemBand;
+  idx = t;
+  if (npro > 0 && t >= G) {
+    const long long u = t - G, s = P.pro_stride;
+    const long long grp = u / (s + 1), r = u - grp * (s + 1);
+    if (grp < npro) {
+      if (r == s) { kind = kItemPro; idx = grp; return; }
+      idx = G + grp * s + r;
+    } else {
+      idx = G + npro * s + (u - npro * (s + 1));
+    }
+  }
+  if (idx >= B) kind = kItemEnd;
+}
+
+__device__ __forceinline__ void stage_next(const BandParams& P, BandShared* sh, int b) {
+  const int lane = threadIdx.x & 31;
+  ItemCfg& ic = sh->ic[b];
+  if (lane == 0) {
+    int kind;
+    long long idx;
+    ticket_item(P, (long long)atomicAdd(P.ticket, 1), kind, idx);
+    ic.kind = kind;
+    ic.item = idx;
+    if (kind == kItemBand) item_setup(P, idx, ic);
+    else ic.pl = (int)idx;
+  }
+  __syncwarp();
+  if (ic.kind == kItemBand) {
+    item_stage(P, ic.item, sh, b, -2);
+  } else if (lane == 0) {
+    sh->nseg[b] = 0;
+    sh->seg_off[b][0] = 0;
+    sh->rows_left[b] = 0;
+  }
+}
+
 // One regenerated particle, both frames (what the splat needs).
 struct PFrames {
   int ax1, ay1, ax2, ay2;
@@ -1096,23 +1339,33 @@ struct PFrames {
   bool on1, on2;
 };
 
-// Regenerate particle gi of seeding cell cc (branch-free, so that two
-// particles per thread interleave: two Philox chains and eight flow loads in
-// flight): position, advection, appearance, and whether each frame can touch
-// the tile [r0, r1) x [c0, c1) (full patch window).
+// Regenerate particle gi of seeding cell cc from its ParticleA draw `a`:
+// position, advection, appearance, and whether each frame can touch the tile
+// [r0, r1) x [c0, c1) (full patch window). `between` runs after the four flow
+// loads are issued and before their values are used (the caller draws the
+// next particle's Philox there, hiding the L2 latency of the loads).
+template <class Between>
 __device__ __forceinline__ void band_gen(const BandParams& P, const RngKey& key, const PairHdr& hd,
-                                         const float2* __restrict__ flow, int gi, int cc, int h, int r0,
-                                         int r1, int c0, int c1, PFrames& o) {
+                                         const float2* __restrict__ flow, int gi, int cc, const uint4 a,
+                                         int h, int r0, int r1, int c0, int c1, PFrames& o,
+                                         Between between) {
   const GenCfg& g = P.g;
   const int CX = 1 << P.sx;
-  const uint4 a = philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagParticleA), g.rk);
-  const uint64_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
-  const uint64_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
+  const uint32_t X = cell_coord((uint32_t)(cc & (CX - 1)), a.x, g.W, P.sx);
+  const uint32_t Y = cell_coord((uint32_t)(cc >> P.sx), a.y, g.H, P.sy);
   fixed_anchor(X, o.ax1, o.fx1);
   fixed_anchor(Y, o.ay1, o.fy1);
-  advect_fixed(g, flow, X, Y, o.ax1, o.fx1, o.ay1, o.fy1, o.ax2, o.fx2, o.ay2, o.fy2);
-  const bool in1 = o.ay1 + h >= r0 && o.ay1 - h < r1 && o.ax1 + h >= c0 && o.ax1 - h < c1;
-  const bool in2 = o.ay2 + h >= r0 && o.ay2 - h < r1 && o.ax2 + h >= c0 && o.ax2 - h < c1;
+  // advect (particles.py:129-136): bilinear, edge-clamped (flowfield.py:207-232)
+  int fcx, fcy;
+  float tx, ty;
+  fixed_cell(X, g.W, fcx, tx);
+  fixed_cell(Y, g.H, fcy, ty);
+  const int cx1 = fcx + 1 < g.W ? fcx + 1 : g.W - 1;
+  const int cy1 = fcy + 1 < g.H ? fcy + 1 : g.H - 1;
+  const float2 q00 = __ldg(flow + fcy * g.W + fcx);
+  const float2 q01 = __ldg(flow + fcy * g.W + cx1);
+  const float2 q10 = __ldg(flow + cy1 * g.W + fcx);
+  const float2 q11 = __ldg(flow + cy1 * g.W + cx1);
   const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
   const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
   o.sig = __fmul_rn(d, g.inv_ratio);
@@ -1121,8 +1374,19 @@ __device__ __forceinline__ void band_gen(const BandParams& P, const RngKey& key,
   o.amp1 = lk.amp1; o.amp2 = lk.amp2;
   o.sx2 = lk.sx2; o.sy2 = lk.sy2;
   o.rho1 = lk.rho1; o.rho2 = lk.rho2;
+  const bool in1 = o.ay1 + h >= r0 && o.ay1 - h < r1 && o.ax1 + h >= c0 && o.ax1 - h < c1;
   o.on1 = in1 && lk.vis1 && lk.amp1 > 0.f;
+  between(o);   // frame-1 work while the flow loads are in flight
+  const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
+  const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
+  shift_anchor(o.ax1, o.fx1, u, o.ax2, o.fx2);
+  shift_anchor(o.ay1, o.fy1, v, o.ay2, o.fy2);
+  const bool in2 = o.ay2 + h >= r0 && o.ay2 - h < r1 && o.ax2 + h >= c0 && o.ax2 - h < c1;
   o.on2 = in2 && lk.vis2 && lk.amp2 > 0.f;
+}
+
+__device__ __forceinline__ uint4 draw_a(const GenCfg& g, const RngKey& key, int gi) {
+  return philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagParticleA), g.rk);
 }
 
 // Worker warps: regenerate, advect and splat the particles of one item
@@ -1146,7 +1410,7 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
   int next_row = ic.cy0;   // first cell row of the current pass
   for (;;) {
     const int nseg = sh->nseg[buf];
-    const int N = sh->seg_off[buf][nseg];
+    const int N = (P.ablate & 1) ? 0 : sh->seg_off[buf][nseg];
     const int* soff = sh->seg_off[buf];
     const int* sst = sh->seg_start[buf];
     // slot q (clamped into [0, N)) -> particle index (segment search)
@@ -1182,8 +1446,9 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
           cB = __ldcg(cof + gB);
         }
         PFrames A, B;
-        band_gen(P, key, hd, flow, giA, ccA, h, r0, r1, c0, c1, A);
-        band_gen(P, key, hd, flow, giB, ccB, h, r0, r1, c0, c1, B);
+        const uint4 aA = draw_a(P.g, key, giA), aB = draw_a(P.g, key, giB);
+        band_gen(P, key, hd, flow, giA, ccA, aA, h, r0, r1, c0, c1, A, [](const PFrames&) {});
+        band_gen(P, key, hd, flow, giB, ccB, aB, h, r0, r1, c0, c1, B, [](const PFrames&) {});
         const bool okA = qa < N, okB = qb2 < N;
         if (okA && A.on1)
           splat_v<PSF, SEP, WM>(acc0, P.AS, A.ax1, A.ay1, A.fx1, A.fy1, A.amp1, A.sig, A.sig, A.rho1, h, r0, r1,
@@ -1200,24 +1465,33 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
         __syncwarp();
       }
     } else {
+      // software pipeline: the Philox draw of the next slot is computed while
+      // this slot's flow loads are in flight; its cell load one slot ahead
       int gA = 0, cA = 0;
+      uint4 aA = make_uint4(0, 0, 0, 0);
       if (N > 0) {
         gA = locate(tid);
         cA = __ldcg(cof + gA);
+        aA = draw_a(P.g, key, gA);
       }
       for (int qb = 0; qb < N; qb += kBandThreads) {
         const int qa = qb + tid;
         const int giA = gA, ccA = cA;
-        if (qb + kBandThreads < N) {
+        const uint4 a = aA;
+        const bool more = qb + kBandThreads < N;
+        if (more) {
           gA = locate(qa + kBandThreads);
           cA = __ldcg(cof + gA);
         }
-        if (qa < N) {
-          PFrames A;
-          band_gen(P, key, hd, flow, giA, ccA, h, r0, r1, c0, c1, A);
-          if (A.on1)
-            splat_v<PSF, SEP, WM>(acc0, P.AS, A.ax1, A.ay1, A.fx1, A.fy1, A.amp1, A.sig, A.sig, A.rho1, h, r0,
+        PFrames A;
+        const bool ok = qa < N;
+        band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
+          if (ok && F.on1 && !(P.ablate & 2))
+            splat_v<PSF, SEP, WM>(acc0, P.AS, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, F.rho1, h, r0,
                                   r1, c0, c1, shift, scale);
+          if (more) aA = draw_a(P.g, key, gA);
+        });
+        if (ok && !(P.ablate & 2)) {
           if (A.on2)
             splat_v<PSF, SEP, WM>(acc1, P.AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, A.rho2, h, r0,
                                   r1, c0, c1, shift, scale);
@@ -1243,47 +1517,72 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   int* acc1 = acc0 + P.TH * P.AS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
-  const long long total_items = (long long)P.pairs * P.tiles;
 #ifdef PGB_PHASE_TIMING
   auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; };
   unsigned long long* CT = P.timing ? P.timing + kTimingCtaBase + (size_t)blockIdx.x * 4 : nullptr;
   if (CT && tid == 0) CT[0] = gtime();
 #endif
+  const int acc_bytes = ((2 * P.TH + P.pad_rows) * P.AS + 8) * 4;
   if (P.inline_prologue) {
-    // prologue work items first (pairs, then flow-bound chunks); band items
-    // wait on their readiness flags, so every wait targets work that some
-    // co-resident CTA runs before it waits on anything
-    const int npro = P.pairs + P.field_cnt * kFieldBlocks;
+    // prologue work items first (this batch's pairs unless precomputed by the
+    // previous launch, then flow-bound chunks); band items wait on their
+    // readiness flags, so every wait targets work that some co-resident CTA
+    // runs before it waits on anything
+    const int npp = P.inline_pairs ? P.pairs : 0;
+    const int npro = npp + P.field_cnt * kFieldBlocks;
     for (int w = blockIdx.x; w < npro; w += gridDim.x) {
-      if (w < P.pairs) {
-        pair_prologue<kBandBlock>(P, w, acc0, ((2 * P.TH + P.pad_rows) * P.AS + 8) * 4);
+      if (w < npp) {
+        pair_prologue<kBandBlock>(P, w, acc0, acc_bytes, pro_cur(P));
       } else {
-        const int fc = w - P.pairs;
+        const int fc = w - npp;
         field_bound_chunk<kBandBlock>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
       }
       __syncthreads();
     }
+    if (!P.inline_pairs && tid == 0)
+      for (int pl = blockIdx.x; pl < P.pairs; pl += gridDim.x) write_stats(P, pl, P.hdr[pl]);
   }
   // both frame accumulators + the zero padding behind them
   for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 8) / 4; e += kBandBlock)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
   __syncthreads();
-  // static schedule: items blockIdx.x, + gridDim.x, ...; the staging warp
-  // prepares item k+1 (parameters + particle segments) while the workers
-  // splat item k.
-  long long item = blockIdx.x;
+  // dynamic schedule: the staging warp takes the ticket of item k+1 and
+  // prepares it (parameters + particle segments) while the workers splat item k
 #ifdef PGB_PHASE_TIMING
   if (CT && tid == 0) CT[1] = gtime();
 #endif
-  if (stager && item < total_items) item_stage(P, item, sh, 0, -1);
+  if (stager) stage_next(P, sh, 0);
   __syncthreads();
 #ifdef PGB_PHASE_TIMING
   if (CT && tid == 0) CT[2] = gtime();
 #endif
-  for (int buf = 0; item < total_items; buf ^= 1, item += gridDim.x) {
-    const long long nxt = item + gridDim.x;
+  for (int buf = 0;; buf ^= 1) {
+    const int kind = sh->ic[buf].kind;
+    if (kind == kItemEnd) break;
     if (stager) {
-      if (nxt < total_items) item_stage(P, nxt, sh, buf ^ 1, -1);
+#ifdef PGB_PHASE_TIMING
+      const long long ts0 = clock64();
+#endif
+      stage_next(P, sh, buf ^ 1);
+#ifdef PGB_PHASE_TIMING
+      if (P.timing && (tid & 31) == 0) {
+        unsigned long long* T = P.timing + kTimingCtaBase + 4 * 2048 + 8 * 296 + (size_t)blockIdx.x * 2;
+        T[0] += (unsigned long long)(clock64() - ts0);
+        T[1] += 1;
+      }
+#endif
+    }
+    if (kind == kItemPro) {
+      // the next batch's pair prologue (whole block), then re-zero its scratch
+      pair_prologue<kBandBlock>(P, sh->ic[buf].pl, acc0, acc_bytes, pro_next(P));
+      const int ncell = 1 << (P.sy + P.sx);
+      const int scratch = min(acc_bytes, (((ncell < 4 ? 4 : ncell) + 4) & ~3) * 4 + (int)cof_stride(P.n) * 2);
+      for (int e = tid; e < (scratch + 15) / 16; e += kBandBlock)
+        reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+      __syncthreads();
+      continue;
+    }
+    if (stager) {
       __syncthreads();   // particles done
       __syncthreads();   // store done
       continue;
@@ -1292,6 +1591,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
     const long long t_item0 = clock64();
 #endif
     const ItemCfg& ic = sh->ic[buf];
+    const long long item = ic.item;
     const int pl = ic.pl;
     const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
     const float scale = (float)(1 << ic.shift);
@@ -1314,8 +1614,10 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
     const long long t_bar1 = clock64();
 #endif
     const float inv_scale = 1.0f / scale;
-    band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
-    band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
+    if (!(P.ablate & 4) && !band_store_items_tma(P, acc0, acc1, pl, r0, r1 - r0, c0, c1 - c0, inv_scale)) {
+      band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
+      band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
+    }
 #ifdef PGB_PHASE_TIMING
     const long long t_store = clock64();
 #endif

@@ -170,24 +170,31 @@ __device__ __forceinline__ float lerpf_exact(float lo, float span, float u) {
   return __fadd_rn(lo, __fmul_rn(span, u));
 }
 
-// Fixed-point coordinate -> (anchor, fraction), value = F / 2^33.
-__device__ __forceinline__ void fixed_anchor(uint64_t F, int& a, float& f) {
-  const uint64_t an = (F + (1ull << 32)) >> 33;
+// Fixed-point coordinates (Q17): value = X / 2^17 with X odd, i.e. the centre
+// of a 2^-16 px bin; all position arithmetic is 32-bit integer (images < 30000 px).
+// Coordinate -> (anchor floor(v + 1/2), float32 fraction; exact, |f| <= 1/2).
+__device__ __forceinline__ void fixed_anchor(uint32_t X, int& a, float& f) {
+  const uint32_t an = (X + (1u << 16)) >> 17;
   a = (int)an;
-  const long long diff = (long long)(F - (an << 33));
-  // one rounding (|diff| < 2^33): float(diff) * 2^-33 == float(diff * 2^-33)
-  f = __ll2float_rn(diff) * 0x1p-33f;
+  f = (float)(int)(X - (an << 17)) * 0x1p-17f;
 }
 
-// Clamped bilinear cell: x = min(v, N-1), c = min(floor x, N-2), t = x - c.
-__device__ __forceinline__ void fixed_cell(uint64_t F, int N, int& c, float& t) {
-  const uint64_t lim = (uint64_t)(N - 1) << 33;
-  const uint64_t xc = F < lim ? F : lim;
-  int cc = (int)(xc >> 33);
+// Clamped bilinear cell: x = min(v, N-1), c = min(floor x, N-2), t = x - c (exact).
+__device__ __forceinline__ void fixed_cell(uint32_t X, int N, int& c, float& t) {
+  const uint32_t lim = (uint32_t)(N - 1) << 17;
+  const uint32_t xc = X < lim ? X : lim;
+  int cc = (int)(xc >> 17);
   const int cmax = N - 2 > 0 ? N - 2 : 0;
   cc = cc < cmax ? cc : cmax;
   c = cc;
-  t = __ll2float_rn((long long)(xc - ((uint64_t)cc << 33))) * 0x1p-33f;
+  t = (float)(int)(xc - ((uint32_t)cc << 17)) * 0x1p-17f;
+}
+
+// Uniform Q17 coordinate inside seeding cell `cell` of width CW = size / 2^bits
+// px (CW << 16 is an integer for bits <= 16): X = 2 (cell CW16 + floor(w CW16 / 2^32)) + 1.
+__device__ __forceinline__ uint32_t cell_coord(uint32_t cell, uint32_t w, int size, int bits) {
+  const uint32_t cw = (uint32_t)size << (16 - bits);
+  return ((cell * cw + __umulhi(w, cw)) << 1) | 1u;
 }
 
 __device__ __forceinline__ float bilerp(float g00, float g01, float g10, float g11, float tx,
@@ -219,8 +226,8 @@ __device__ __forceinline__ void gen_particle(const FusedParams& P, int pl, int i
   const RngKey key{g.k0, g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
   // sample_particles (particles.py:61-101)
   const uint4 a = draw(key, (uint32_t)i, kTagParticleA);
-  const uint64_t X = (2ull * a.x + 1ull) * (uint64_t)g.W;
-  const uint64_t Y = (2ull * a.y + 1ull) * (uint64_t)g.H;
+  const uint32_t X = cell_coord(0u, a.x, g.W, 0);
+  const uint32_t Y = cell_coord(0u, a.y, g.H, 0);
   const float d = lerpf_exact(g.d_lo, g.d_span, unit23(a.z));
   const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
   const bool active = i < M;

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <map>
 #include <mutex>
 #include <string>
@@ -218,6 +219,13 @@ struct DevWork {
   // band generator workspace: ticket + pair headers + field bounds + cell prefixes
   void* band = nullptr;
   size_t band_bytes = 0;
+  // cross-launch prologue pipeline: table slot `pro_slot` holds the pair
+  // prologue of the launch described by `pro_key` (computed as the tail work
+  // of the previous launch on `pro_stream`)
+  bool pro_valid = false;
+  int pro_slot = 0;
+  cudaStream_t pro_stream = nullptr;
+  std::array<uint64_t, 16> pro_key{};
   // host-API staging
   void* stage = nullptr;
   size_t stage_bytes = 0;
@@ -532,17 +540,22 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const size_t cof_bytes = (size_t)pairs * cof_stride(cfg->n_capacity) * sizeof(unsigned short);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
   DevWork& w = work_for_current();
-  // [ticket | field bounds | ready flags] are zeroed per launch, then headers,
-  // prefixes and the particle -> cell arrays
+  // [ticket | field bounds | ready flags] are zeroed per launch, then two
+  // table slots of [headers | prefixes | particle -> cell arrays]
   const size_t head = 256 + up(fb_bytes) + up(flag_bytes);
-  char* b = static_cast<char*>(
-      ensure(w.band, w.band_bytes, head + up(hdr_bytes) + up(pre_bytes) + up(cof_bytes)));
+  const size_t slot_bytes = up(hdr_bytes) + up(pre_bytes) + up(cof_bytes);
+  void* before = w.band;
+  char* b = static_cast<char*>(ensure(w.band, w.band_bytes, head + 2 * slot_bytes));
+  if (b != before) w.pro_valid = false;
   P.ticket = reinterpret_cast<int*>(b);
   P.fbound = reinterpret_cast<float2*>(b + 256);
   int* flags = reinterpret_cast<int*>(b + 256 + up(fb_bytes));
-  P.hdr = reinterpret_cast<PairHdr*>(b + head);
-  P.prefix = reinterpret_cast<int*>(b + head + up(hdr_bytes));
-  P.cell_of = reinterpret_cast<unsigned short*>(b + head + up(hdr_bytes) + up(pre_bytes));
+  auto slot_ptrs = [&](int k, PairHdr*& hdr, int*& pre, unsigned short*& cof) {
+    char* sb = b + head + (size_t)k * slot_bytes;
+    hdr = reinterpret_cast<PairHdr*>(sb);
+    pre = reinterpret_cast<int*>(sb + up(hdr_bytes));
+    cof = reinterpret_cast<unsigned short*>(sb + up(hdr_bytes) + up(pre_bytes));
+  };
   PGB_CK(cudaMemsetAsync(b, 0, head, stream));
   // bounds only for the fields this pair range reads
   const int f_lo = (int)(pair_base / pairs_per_field);
@@ -550,11 +563,47 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   P.field_lo = f_lo;
   P.field_cnt = f_hi - f_lo + 1;
   if (!launch) {
+    // everything the pair prologue depends on, plus the batch
+    auto key_of = [&](uint64_t bt) {
+      std::array<uint64_t, 16> k{};
+      auto dbits = [](double v) { uint64_t u; std::memcpy(&u, &v, 8); return u; };
+      k[0] = ((uint64_t)cfg->height << 32) | (uint32_t)cfg->width;
+      k[1] = (uint64_t)cfg->n_capacity;
+      k[2] = cfg->seed;
+      k[3] = dbits(cfg->ppp_lo); k[4] = dbits(cfg->ppp_hi);
+      k[5] = dbits(cfg->d_lo); k[6] = dbits(cfg->d_hi);
+      k[7] = dbits(cfg->patch_multiplier);
+      k[8] = ((uint64_t)bp.sy << 32) | (uint32_t)bp.sx;
+      k[9] = bt;
+      k[10] = (uint64_t)pair_base;
+      k[11] = (uint64_t)pairs;
+      k[12] = (uint64_t)slot_bytes;
+      return k;
+    };
+    const bool pipeline = !std::getenv("PGB_NO_PIPELINE") || std::atoi(std::getenv("PGB_NO_PIPELINE")) == 0;
+    int cur = 0;
+    P.inline_pairs = 1;
+    if (pipeline && w.pro_valid && w.pro_stream == stream && w.pro_key == key_of(batch)) {
+      cur = w.pro_slot;
+      P.inline_pairs = 0;
+    }
+    slot_ptrs(cur, P.hdr, P.prefix, P.cell_of);
     P.inline_prologue = 1;
     P.pair_ready = flags;
     P.fb_done = flags + pairs;
+    w.pro_valid = false;
+    if (pipeline && batch + 1 < (1ull << 32)) {
+      slot_ptrs(1 - cur, P.nx_hdr, P.nx_prefix, P.nx_cof);
+      P.nx_batch_lo = (uint32_t)(batch + 1);
+      w.pro_valid = true;
+      w.pro_slot = 1 - cur;
+      w.pro_stream = stream;
+      w.pro_key = key_of(batch + 1);
+    }
     return;
   }
+  w.pro_valid = false;   // the standalone prologue overwrites slot 0
+  slot_ptrs(0, P.hdr, P.prefix, P.cell_of);
   P.inline_prologue = 0;
   BandParams Q = P;
   const size_t psmem = std::min<size_t>(kSmemMax, (size_t)((std::max(ncell, 4) + 4) & ~3) * sizeof(int) +
@@ -599,6 +648,8 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.noise_std = (float)cfg->noise_std;
   P.out[0] = img1;
   P.out[1] = img2;
+  if (const char* e = std::getenv("PGB_ABLATE")) P.ablate = std::atoi(e);   // debug timing only
+  P.tma_store = std::getenv("PGB_NO_TMA_STORE") ? 0 : 1;
 #ifdef PGB_PHASE_TIMING
   {
     static unsigned long long* tbuf = nullptr;
@@ -610,8 +661,27 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
 #endif
   BandFn fn = cfg->psf == PGB_PSF_ERF ? band_kernel<kPsfErf> : band_kernel<kPsfPoint>;
   const int ctas = band_resident_ctas(fn, bp.smem);
-  const long long items = (long long)pairs * bp.tiles;
-  const int grid = (int)std::max<long long>(1, std::min<long long>(ctas, items));
+  // static schedule over `grid` CTAs: whole rounds of (pair, tile) items, then
+  // the remaining tiles split into row parts (>= 8 rows) spread over the grid
+  const long long F = (long long)pairs * bp.tiles;
+  const int smax = std::max(1, bp.TH / 8);
+  long long G = ctas, R = 0, rem = 0;
+  int sp = 1;
+  if (F >= ctas) {
+    R = F / G;
+    rem = F - R * G;
+  } else {
+    rem = F;
+  }
+  if (rem > 0) sp = (int)std::max<long long>(1, std::min<long long>(smax, ctas / rem));
+  if (std::getenv("PGB_NO_SPLIT")) sp = 1;
+  if (F < ctas) G = std::max<long long>(1, std::min<long long>(ctas, rem * sp));
+  P.split_base = R * G;
+  P.split_s = sp;
+  P.total_items = R * G + rem * sp;
+  // next-batch prologue tickets interleaved after the first round
+  P.pro_stride = P.nx_hdr ? (int)std::max<long long>(0, (P.total_items - G) / pairs) : 0;
+  const int grid = (int)G;
   fn<<<grid, kBandBlock, bp.smem, stream>>>(P);
   g_launches.fetch_add(1);
 }

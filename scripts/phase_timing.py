@@ -52,3 +52,10 @@ pt = pt[pt[:, 0] > 0]
 pt = (pt - t0) / 1e3
 for k, nm in enumerate(["ppp/M done", "fp64 chain done", "histogram done", "scan done", "cof done", "prefix stored", "cof staged"]):
     print(f"prologue {nm:18s} mean {pt[:, k].mean():6.2f} us  max {pt[:, k].max():6.2f} us")
+cyc = buf[base + 4 * 2048:base + 4 * 2048 + 8 * 296].reshape(-1, 8)[:, 7].astype(np.float64)
+ok = (pt_raw := buf[base + 4 * 2048:base + 4 * 2048 + 8 * 296].reshape(-1, 8).astype(np.float64))[:, 0] > 0
+ns = pt_raw[ok, 4] - pt_raw[ok, 0]
+print(f"prologue stage0->4: {cyc[ok].mean():.0f} cycles over {ns.mean():.0f} ns -> {cyc[ok].mean() / ns.mean():.3f} GHz")
+st = buf[base + 4 * 2048 + 8 * 296:base + 4 * 2048 + 8 * 296 + 2 * 296].reshape(-1, 2).astype(np.float64)
+st = st[st[:, 1] > 0]
+print(f"stager item_stage: mean {st[:, 0].sum() / st[:, 1].sum():.0f} cycles per item over {st[:, 1].sum():.0f} items")
