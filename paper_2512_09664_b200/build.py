@@ -53,6 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for knob in ("PGB_ILP", "PGB_BAND_MINB", "PGB_WORKER_WARPS"):
         if os.environ.get(knob):
             extra.append(f"-D{knob}={int(os.environ[knob])}")
+    if os.environ.get("PGB_DBG_NOATOM"):
+        extra.append("-DPGB_DBG_NOATOM")
     if os.environ.get("PGB_PHASE_TIMING"):   # debug: per-phase cycle counters in the band kernel
         extra.append("-DPGB_PHASE_TIMING")
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]

@@ -50,6 +50,7 @@ constexpr int kBandThreads = 32 * PGB_WORKER_WARPS;
 constexpr int kBandWarps = kBandThreads / 32;
 constexpr int kBandBlock = kBandThreads + 32;   // + one staging warp
 constexpr int kMaxCellBits = 14;
+constexpr int kMaxUnpredWM = 12;   // largest unpredicated (separable) splat window
 constexpr int kTimingCtaBase = 148 * 8 * 8 * 5 / 2;   // PGB_PHASE_TIMING: per-CTA timestamps
 
 struct __align__(16) PairHdr {
@@ -596,7 +597,7 @@ struct ItemCfg {
   int pl, r0, r1, c0, c1;
   int cy0, cy1, cx0, cx1;
   int h, wt, shift, field, sep;
-  int var;                 // particle-loop variant: 8 * sep + WM (0 = dynamic windows)
+  int var;                 // particle-loop variant: 16 * sep + WM (0 = dynamic windows)
   int kind;                // kItemBand, kItemPro (next batch's pair prologue), kItemEnd
   long long item;          // band item index (kItemBand) / pair (kItemPro)
   PairHdr hd;
@@ -612,6 +613,12 @@ struct __align__(16) BandShared {
   int seg_start[2][kMaxSeg];         // first particle index of each segment
   int seg_off[2][kMaxSeg + 1];       // exclusive prefix of segment lengths
 };
+
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
@@ -655,7 +662,7 @@ __device__ __forceinline__ void splat_point(int* __restrict__ acc, int AS, int a
   const float A = (0.5f * kLog2e) * iq * isx * isx;
   const float C = (0.5f * kLog2e) * iq * isy * isy;
   const float B = -kLog2e * rho * iq * isx * isy;
-  const float Ls = __log2f(amp) + (float)shift;
+  const float Ls = lg2_approx(amp) + (float)shift;
   if (WM > 0) {
     // pixels beyond the bound lie outside the tight radius (they round to 0)
     nr = min(nr, WM);
@@ -754,7 +761,7 @@ __device__ __forceinline__ void splat_point_sep(int* __restrict__ acc, int AS, i
   const float isx = rcp_approx(sx), isy = rcp_approx(sy);
   const float A = (0.5f * kLog2e) * isx * isx;
   const float C = (0.5f * kLog2e) * isy * isy;
-  const float Ls = __log2f(amp) + (float)shift;
+  const float Ls = lg2_approx(amp) + (float)shift;
   float X[WM], Y[WM];
 #pragma unroll
   for (int j = 0; j < WM; ++j) {
@@ -775,7 +782,8 @@ __device__ __forceinline__ void splat_point_sep(int* __restrict__ acc, int AS, i
 }
 
 
-// Unpredicated point-PSF windows (WM = compile-time window bound, 1..7).
+// Unpredicated point-PSF windows (WM = compile-time window bound: 1..13
+// separable, 1..7 correlated).
 // Every particle-frame adds all WM x WM slots; slots outside its clipped
 // window add exactly 0 (their factor is 0, resp. their exponent -inf), so no
 // per-slot branch is needed. Slots past the tile's last row / column land on
@@ -794,23 +802,41 @@ __device__ __forceinline__ void splat_sep_u(int* __restrict__ acc, int AS, int a
   const float isx = rcp_approx(sx), isy = rcp_approx(sy);
   const float A = (0.5f * kLog2e) * isx * isx;
   const float C = (0.5f * kLog2e) * isy * isy;
-  const float Ls = __log2f(amp) + (float)shift;
-  float X[WM], Y[WM];
+  const float Ls = lg2_approx(amp) + (float)shift;
+  float X[WM];
 #pragma unroll
   for (int j = 0; j < WM; ++j) {
     const float dx = dx0 + (float)j;
     const float xv = ex2_approx(fmaf(-A * dx, dx, Ls));
     X[j] = j < nc ? xv : 0.f;
-    const float dy = dy0 + (float)j;
-    const float yv = ex2_approx(-C * dy * dy);
-    Y[j] = j < nr ? yv : 0.f;
   }
+  if constexpr (WM <= 7) {
+    float Y[WM];
 #pragma unroll
-  for (int i = 0; i < WM; ++i) {
-    int* row = base + i * AS;
+    for (int i = 0; i < WM; ++i) {
+      const float dy = dy0 + (float)i;
+      const float yv = ex2_approx(-C * dy * dy);
+      Y[i] = i < nr ? yv : 0.f;
+    }
 #pragma unroll
-    for (int j = 0; j < WM; ++j)
-      atomicAdd(row + j, __float_as_int(fmaf(X[j], Y[i], 12582912.0f)) - 0x4B400000);
+    for (int i = 0; i < WM; ++i) {
+      int* row = base + i * AS;
+#pragma unroll
+      for (int j = 0; j < WM; ++j)
+        atomicAdd(row + j, __float_as_int(fmaf(X[j], Y[i], 12582912.0f)) - 0x4B400000);
+    }
+  } else {
+    // large windows: rows in a loop (one exponential per row), columns unrolled
+#pragma unroll 1
+    for (int i = 0; i < WM; ++i) {
+      const float dy = dy0 + (float)i;
+      const float yv = ex2_approx(-C * dy * dy);
+      const float Y = i < nr ? yv : 0.f;
+      int* row = base + i * AS;
+#pragma unroll
+      for (int j = 0; j < WM; ++j)
+        atomicAdd(row + j, __float_as_int(fmaf(X[j], Y, 12582912.0f)) - 0x4B400000);
+    }
   }
 }
 
@@ -829,7 +855,7 @@ __device__ __forceinline__ void splat_point_u(int* __restrict__ acc, int AS, int
   const float A = (0.5f * kLog2e) * iq * isx * isx;
   const float C = (0.5f * kLog2e) * iq * isy * isy;
   const float B = -kLog2e * rho * iq * isx * isy;
-  const float Ls = __log2f(amp) + (float)shift;
+  const float Ls = lg2_approx(amp) + (float)shift;
   float ct[WM], bx[WM];
 #pragma unroll
   for (int j = 0; j < WM; ++j) {
@@ -1235,8 +1261,9 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   ic.wt = max(1, wt);
   // uncorrelated particles (rho == 0 in both frames): separable splat
   ic.sep = (g.rho_lo == 0.f && g.rho_span == 0.f && !(g.f2_rho_std > 0.f)) ? 1 : 0;
-  const int wm = (P.psf == kPsfPoint && ic.wt <= 7 && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
-  ic.var = (P.psf == kPsfPoint ? 8 * ic.sep : 0) + wm;
+  const int wmax = ic.sep ? kMaxUnpredWM : 7;
+  const int wm = (P.psf == kPsfPoint && ic.wt <= wmax && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
+  ic.var = (P.psf == kPsfPoint ? 16 * ic.sep : 0) + wm;
 }
 
 // Warp 0: next item's parameters + particle segments (one per cell row of the
@@ -1360,12 +1387,12 @@ __device__ __forceinline__ void band_gen(const BandParams& P, const RngKey& key,
   float tx, ty;
   fixed_cell(X, g.W, fcx, tx);
   fixed_cell(Y, g.H, fcy, ty);
-  const int cx1 = fcx + 1 < g.W ? fcx + 1 : g.W - 1;
-  const int cy1 = fcy + 1 < g.H ? fcy + 1 : g.H - 1;
-  const float2 q00 = __ldg(flow + fcy * g.W + fcx);
-  const float2 q01 = __ldg(flow + fcy * g.W + cx1);
-  const float2 q10 = __ldg(flow + cy1 * g.W + fcx);
-  const float2 q11 = __ldg(flow + cy1 * g.W + cx1);
+  // fcx <= W - 2 and fcy <= H - 2 (H, W >= 2): the four nodes are
+  // fp[0], fp[1], fp[W], fp[W + 1]
+  const float2* fp = flow + (fcy * g.W + fcx);
+  const float2* fq = fp + g.W;
+  const float2 q00 = __ldg(fp), q01 = __ldg(fp + 1);
+  const float2 q10 = __ldg(fq), q11 = __ldg(fq + 1);
   const float d = lerpf_exact(g.d_lo, g.d_span, q_to_unit(diam_q(hd, gi, a.z)));
   const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
   o.sig = __fmul_rn(d, g.inv_ratio);
@@ -1374,14 +1401,17 @@ __device__ __forceinline__ void band_gen(const BandParams& P, const RngKey& key,
   o.amp1 = lk.amp1; o.amp2 = lk.amp2;
   o.sx2 = lk.sx2; o.sy2 = lk.sy2;
   o.rho1 = lk.rho1; o.rho2 = lk.rho2;
-  const bool in1 = o.ay1 + h >= r0 && o.ay1 - h < r1 && o.ax1 + h >= c0 && o.ax1 - h < c1;
+  // anchor rows [r0 - h, r1 + h) and columns [c0 - h, c1 + h) reach the tile
+  const bool in1 = (unsigned)(o.ay1 - (r0 - h)) < (unsigned)(r1 - r0 + 2 * h) &&
+                   (unsigned)(o.ax1 - (c0 - h)) < (unsigned)(c1 - c0 + 2 * h);
   o.on1 = in1 && lk.vis1 && lk.amp1 > 0.f;
   between(o);   // frame-1 work while the flow loads are in flight
   const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
   const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
   shift_anchor(o.ax1, o.fx1, u, o.ax2, o.fx2);
   shift_anchor(o.ay1, o.fy1, v, o.ay2, o.fy2);
-  const bool in2 = o.ay2 + h >= r0 && o.ay2 - h < r1 && o.ax2 + h >= c0 && o.ax2 - h < c1;
+  const bool in2 = (unsigned)(o.ay2 - (r0 - h)) < (unsigned)(r1 - r0 + 2 * h) &&
+                   (unsigned)(o.ax2 - (c0 - h)) < (unsigned)(c1 - c0 + 2 * h);
   o.on2 = in2 && lk.vis2 && lk.amp2 > 0.f;
 }
 
@@ -1414,10 +1444,12 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
     const int* soff = sh->seg_off[buf];
     const int* sst = sh->seg_start[buf];
     // slot q (clamped into [0, N)) -> particle index (segment search)
+    const int sst0 = sst[0];
     auto locate = [&](int q) {
       q = min(q, N - 1);
+      if (nseg == 1) return sst0 + q;
       int sg = 0;
-      if (nseg > 1) {
+      {
         int hi = nseg - 1;
         while (sg < hi) {
           const int mid = (sg + hi + 1) >> 1;
@@ -1599,9 +1631,10 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
       band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1);
     } else {
       switch (ic.var) {
-#define PGB_V(S, W) case 8 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
+#define PGB_V(S, W) case 16 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
         PGB_V(0, 1) PGB_V(0, 2) PGB_V(0, 3) PGB_V(0, 4) PGB_V(0, 5) PGB_V(0, 6) PGB_V(0, 7)
         PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6) PGB_V(1, 7)
+        PGB_V(1, 8) PGB_V(1, 9) PGB_V(1, 10) PGB_V(1, 11) PGB_V(1, 12)
 #undef PGB_V
         default: band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1); break;
       }

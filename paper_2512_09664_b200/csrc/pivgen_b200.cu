@@ -365,7 +365,7 @@ GenCfg gen_cfg_from(const pgb_config* c) {
 
 void validate_cfg(const pgb_config* c) {
   PGB_REQUIRE(c != nullptr, "config is NULL");
-  PGB_REQUIRE(c->height > 0 && c->width > 0, "image size must be positive");
+  PGB_REQUIRE(c->height >= 2 && c->width >= 2, "image sides must be >= 2 px (bilinear flow sampling)");
   PGB_REQUIRE(c->height < 30000 && c->width < 30000, "image side must be < 30000");
   PGB_REQUIRE(c->n_capacity >= 1, "n_capacity must be >= 1");
   PGB_REQUIRE(c->psf == PGB_PSF_POINT || c->psf == PGB_PSF_ERF, "unknown psf");
@@ -431,7 +431,7 @@ BandPlan make_band_plan(int H, int W, int halo) {
   BandPlan p{};
   cell_bits(H, W, p.sy, p.sx);
   // zero rows behind the accumulators for unpredicated splat windows (<= 7 wide)
-  p.pad_rows = std::min(6, 2 * halo);
+  p.pad_rows = std::min(kMaxUnpredWM - 1, 2 * halo);
   const size_t budget_all = band_acc_budget() / 4;        // int32: two frames + padding
   auto th_cap = [&](int AS) -> size_t {
     const size_t pad = (size_t)p.pad_rows * AS + 8;
@@ -580,7 +580,9 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
       k[12] = (uint64_t)slot_bytes;
       return k;
     };
-    const bool pipeline = !std::getenv("PGB_NO_PIPELINE") || std::atoi(std::getenv("PGB_NO_PIPELINE")) == 0;
+    // opt-in (PGB_PIPELINE=1): measured slower on B200 at c2 -- the next batch's
+    // prologue work steals issue slots from the co-resident CTA's band work
+    const bool pipeline = std::getenv("PGB_PIPELINE") && std::atoi(std::getenv("PGB_PIPELINE")) != 0;
     int cur = 0;
     P.inline_pairs = 1;
     if (pipeline && w.pro_valid && w.pro_stream == stream && w.pro_key == key_of(batch)) {
@@ -649,7 +651,9 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.out[0] = img1;
   P.out[1] = img2;
   if (const char* e = std::getenv("PGB_ABLATE")) P.ablate = std::atoi(e);   // debug timing only
-  P.tma_store = std::getenv("PGB_NO_TMA_STORE") ? 0 : 1;
+  // opt-in (PGB_TMA_STORE=1): the bulk store's read wait stalls the CTA; the
+  // per-thread streaming stores measured faster at c2
+  P.tma_store = (std::getenv("PGB_TMA_STORE") && std::atoi(std::getenv("PGB_TMA_STORE")) != 0) ? 1 : 0;
 #ifdef PGB_PHASE_TIMING
   {
     static unsigned long long* tbuf = nullptr;
