@@ -32,6 +32,9 @@
 
 namespace pgb {
 
+#ifndef PGB_FRAME_LOOP
+#define PGB_FRAME_LOOP 0   // 1: one splat code copy looped over both frames
+#endif
 #ifndef PGB_ILP
 #define PGB_ILP 1   // particles regenerated per thread per loop iteration
 #endif
@@ -96,6 +99,8 @@ struct BandParams {
   int inline_prologue;         // band kernel runs prologue work items (field bounds; pairs if inline_pairs)
   int inline_pairs;            // this batch's pair prologue runs in this launch (else precomputed)
   int tma_store;               // full-width f32 tiles leave through TMA bulk stores
+  int4* zero_head;             // the other control head: zeroed here for the next launch (or null)
+  int zero_head_n;
   int ablate;                  // debug timing only (PGB_ABLATE): 1 no particles, 2 no splat, 4 no store
   PairHdr* nx_hdr;             // next batch's pair prologue (tail work of this launch), or null
   int* nx_prefix;
@@ -1517,6 +1522,20 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
         }
         PFrames A;
         const bool ok = qa < N;
+#if PGB_FRAME_LOOP
+        // one copy of the splat code for both frames (smaller hot loop)
+        band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames&) {
+          if (more) aA = draw_a(P.g, key, gA);
+        });
+#pragma unroll 1
+        for (int f = 0; f < 2; ++f) {
+          const bool on = f ? A.on2 : A.on1;
+          if (ok && on && !(P.ablate & 2))
+            splat_v<PSF, SEP, WM>(f ? acc1 : acc0, P.AS, f ? A.ax2 : A.ax1, f ? A.ay2 : A.ay1, f ? A.fx2 : A.fx1,
+                                  f ? A.fy2 : A.fy1, f ? A.amp2 : A.amp1, f ? A.sx2 : A.sig, f ? A.sy2 : A.sig,
+                                  f ? A.rho2 : A.rho1, h, r0, r1, c0, c1, shift, scale);
+        }
+#else
         band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
           if (ok && F.on1 && !(P.ablate & 2))
             splat_v<PSF, SEP, WM>(acc0, P.AS, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, F.rho1, h, r0,
@@ -1528,6 +1547,7 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
             splat_v<PSF, SEP, WM>(acc1, P.AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, A.rho2, h, r0,
                                   r1, c0, c1, shift, scale);
         }
+#endif
         __syncwarp();
       }
     }
@@ -1555,6 +1575,8 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   if (CT && tid == 0) CT[0] = gtime();
 #endif
   const int acc_bytes = ((2 * P.TH + P.pad_rows) * P.AS + 8) * 4;
+  if (blockIdx.x == gridDim.x - 1 && P.zero_head)
+    for (int e = tid; e < P.zero_head_n; e += kBandBlock) P.zero_head[e] = make_int4(0, 0, 0, 0);
   if (P.inline_prologue) {
     // prologue work items first (this batch's pairs unless precomputed by the
     // previous launch, then flow-bound chunks); band items wait on their

@@ -224,6 +224,12 @@ struct DevWork {
   // of the previous launch on `pro_stream`)
   bool pro_valid = false;
   int pro_slot = 0;
+  // two per-launch control heads [ticket | field bounds | flags]: a generate
+  // launch uses one and zeroes the other for the next launch on the same
+  // stream (no memset node between back-to-back launches)
+  bool head_zero[2] = {false, false};
+  int head_next = 0;
+  cudaStream_t head_stream = nullptr;
   cudaStream_t pro_stream = nullptr;
   std::array<uint64_t, 16> pro_key{};
   // host-API staging
@@ -542,21 +548,39 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   DevWork& w = work_for_current();
   // [ticket | field bounds | ready flags] are zeroed per launch, then two
   // table slots of [headers | prefixes | particle -> cell arrays]
-  const size_t head = 256 + up(fb_bytes) + up(flag_bytes);
+  const size_t head = up(256 + up(fb_bytes) + up(flag_bytes));
   const size_t slot_bytes = up(hdr_bytes) + up(pre_bytes) + up(cof_bytes);
   void* before = w.band;
-  char* b = static_cast<char*>(ensure(w.band, w.band_bytes, head + 2 * slot_bytes));
-  if (b != before) w.pro_valid = false;
+  char* base = static_cast<char*>(ensure(w.band, w.band_bytes, 2 * head + 2 * slot_bytes));
+  if (base != before) {
+    w.pro_valid = false;
+    w.head_zero[0] = w.head_zero[1] = false;
+  }
+  int hsel = 0;
+  if (!launch) {
+    hsel = w.head_next;
+    if (!(w.head_zero[hsel] && w.head_stream == stream)) PGB_CK(cudaMemsetAsync(base + hsel * head, 0, head, stream));
+    P.zero_head = reinterpret_cast<int4*>(base + (1 - hsel) * head);
+    P.zero_head_n = (int)(head / 16);
+    w.head_zero[hsel] = false;
+    w.head_zero[1 - hsel] = true;   // zeroed by this launch
+    w.head_stream = stream;
+    w.head_next = 1 - hsel;
+  } else {
+    PGB_CK(cudaMemsetAsync(base, 0, head, stream));
+    w.head_zero[0] = false;
+  }
+  char* b = base + hsel * head;
+  char* slots = base + 2 * head;
   P.ticket = reinterpret_cast<int*>(b);
   P.fbound = reinterpret_cast<float2*>(b + 256);
   int* flags = reinterpret_cast<int*>(b + 256 + up(fb_bytes));
   auto slot_ptrs = [&](int k, PairHdr*& hdr, int*& pre, unsigned short*& cof) {
-    char* sb = b + head + (size_t)k * slot_bytes;
+    char* sb = slots + (size_t)k * slot_bytes;
     hdr = reinterpret_cast<PairHdr*>(sb);
     pre = reinterpret_cast<int*>(sb + up(hdr_bytes));
     cof = reinterpret_cast<unsigned short*>(sb + up(hdr_bytes) + up(pre_bytes));
   };
-  PGB_CK(cudaMemsetAsync(b, 0, head, stream));
   // bounds only for the fields this pair range reads
   const int f_lo = (int)(pair_base / pairs_per_field);
   const int f_hi = (int)((pair_base + pairs - 1) / pairs_per_field);
