@@ -76,7 +76,6 @@ struct BandParams {
   // schedule spread over all CTAs); total_items = split_base + rem * split_s
   long long split_base, total_items;
   int split_s;
-  int pro_stride;              // band tickets between two next-batch prologue tickets
   int pad_rows;                // zero rows after the frame-2 accumulator (unpredicated splat windows)
   int pro_smem;                // dynamic shared bytes of the standalone prologue kernel
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
@@ -430,42 +429,47 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
   }
   __syncthreads();
   PGB_STAMP(2);
-  // One pass: per-thread runs of `per` cells (a multiple of 4, int4 loads),
-  // block exclusive scan -> prefix (int4 stores) and the particle -> cell
-  // array (counting-sort order: particles of cell c are pre[c] .. pre[c+1]-1),
-  // plus the maximum cell count.
+  // Cell counts -> exclusive prefix (in place + global), the maximum cell
+  // count, and the particle -> cell array. Warps own 512-cell chunks; lanes
+  // read consecutive int4s (conflict-free), a warp shuffle scan per 128-cell
+  // layer, chunk totals combined by warp 0 (<= 32 chunks: ncell <= 2^14).
   constexpr int NW = NT / 32;
-  __shared__ int wmax[NW];
+  int* wmax = wsum;        // NW entries, reused after the block combine below
+  __shared__ int ctot[32];
   const int warp = tid >> 5;
   const int nc4 = ncell < 4 ? 4 : ncell;
-  const int per = (((nc4 + NT - 1) / NT) + 3) & ~3;
-  const int b = min(nc4, tid * per), e = min(nc4, b + per);
-  int sum = 0, cm = 0;
-  for (int i = b; i < e; i += 4) {
-    const int4 v = *reinterpret_cast<const int4*>(bins + i);
-    sum += v.x + v.y + v.z + v.w;
-    cm = max(cm, max(max(v.x, v.y), max(v.z, v.w)));
+  const int nq4 = nc4 >> 2;                 // int4 groups of cells
+  const int nchunk = (nq4 + 127) >> 7;       // 128 int4 = 512 cells per chunk
+  int4* bins4 = reinterpret_cast<int4*>(bins);
+  int cm = 0;
+  for (int ch = warp; ch < nchunk; ch += NW) {
+    int tot = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = (ch << 7) + (j << 5) + lane;
+      const int4 v = q < nq4 ? bins4[q] : make_int4(0, 0, 0, 0);
+      tot += v.x + v.y + v.z + v.w;
+      cm = max(cm, max(max(v.x, v.y), max(v.z, v.w)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(~0u, tot, o);
+    if (lane == 0) ctot[ch] = tot;
   }
   {
     // zero the staged particle -> cell slots (marked in pass 2)
     const int M16z = (M + 7) & ~7;
     const int off = ((nc4 + 4) & ~3) * 4;
-    if ((size_t)off + (size_t)M16z * 2 <= (size_t)smem_bytes)
+    if ((size_t)off + (size_t)M16z * 2 <= (size_t)smem_bytes && M16z <= 65536)
       for (int q = tid; q < M16z / 8; q += NT)
         reinterpret_cast<int4*>(reinterpret_cast<char*>(bins) + off)[q] = make_int4(0, 0, 0, 0);
   }
-  int x = sum;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(~0u, x, o);
-    if (lane >= o) x += y;
-    cm = max(cm, __shfl_xor_sync(~0u, cm, o));
-  }
-  if (lane == 31) wsum[warp] = x;
+  for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
   if (lane == 0) wmax[warp] = cm;
   __syncthreads();
   if (warp == 0) {
-    int v = lane < NW ? wsum[lane] : 0;
+    const int t = lane < nchunk ? ctot[lane] : 0;
+    int v = t;
     int m = lane < NW ? wmax[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -473,7 +477,8 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
       if (lane >= o) v += y;
       m = max(m, __shfl_xor_sync(~0u, m, o));
     }
-    if (lane < NW) wsum[lane] = v;
+    if (lane < nchunk) ctot[lane] = v - t;   // exclusive chunk bases
+    if (lane == 31) wsum[0] = v;             // total
     if (lane == 0) scm = m;
   }
   __syncthreads();
@@ -482,76 +487,105 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
   unsigned short* cof = out.cof + (size_t)pl * cof_stride(P.n);
   // particle -> cell (counting-sort order: particles of cell c are pre[c] ..
   // pre[c+1]-1). Staged in shared memory when it fits: mark the first slot
-  // of every non-empty cell with the cell id (slots zeroed in pass 1), then a
+  // of every non-empty cell with the cell id (slots zeroed above), then a
   // block max-scan fills the runs; else one cell per thread into global memory.
   const int M16 = (M + 7) & ~7;
   unsigned short* scof = reinterpret_cast<unsigned short*>(bins + ((nc4 + 4) & ~3));
-  const bool staged = (size_t)((nc4 + 4) & ~3) * 4 + (size_t)M16 * 2 <= (size_t)smem_bytes;
-  int base = (warp ? wsum[warp - 1] : 0) + x - sum;
-  for (int i = b; i < e; i += 4) {
-    int4* bp = reinterpret_cast<int4*>(bins + i);
-    const int4 v = *bp;
-    const int4 o = make_int4(base, base + v.x, base + v.x + v.y, base + v.x + v.y + v.z);
-    *bp = o;   // exclusive prefix, in place
-    if (i + 4 <= ncell) {
-      *reinterpret_cast<int4*>(pre + i) = o;
-    } else {
-      const int oo[4] = {o.x, o.y, o.z, o.w};
-      for (int k = 0; i + k < ncell; ++k) pre[i + k] = oo[k];
+  const bool staged = (size_t)((nc4 + 4) & ~3) * 4 + (size_t)M16 * 2 <= (size_t)smem_bytes && M16 <= 65536;
+  int4* pre4 = reinterpret_cast<int4*>(pre);
+  for (int ch = warp; ch < nchunk; ch += NW) {
+    int run = ctot[ch];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = (ch << 7) + (j << 5) + lane;
+      const int4 v = q < nq4 ? bins4[q] : make_int4(0, 0, 0, 0);
+      const int sv = v.x + v.y + v.z + v.w;
+      int inc = sv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(~0u, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int b0 = run + inc - sv;
+      const int4 o4 = make_int4(b0, b0 + v.x, b0 + v.x + v.y, b0 + v.x + v.y + v.z);
+      if (q < nq4) {
+        bins4[q] = o4;   // exclusive prefix, in place
+        const int i = q << 2;
+        if (i + 4 <= ncell) {
+          pre4[q] = o4;
+        } else {
+          const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
+          for (int k = 0; i + k < ncell; ++k) pre[i + k] = oo[k];
+        }
+        if (staged) {
+          if (v.x) scof[o4.x] = (unsigned short)i;
+          if (v.y) scof[o4.y] = (unsigned short)(i + 1);
+          if (v.z) scof[o4.z] = (unsigned short)(i + 2);
+          if (v.w) scof[o4.w] = (unsigned short)(i + 3);
+        }
+      }
+      run += __shfl_sync(~0u, inc, 31);
     }
-    if (staged) {
-      if (v.x) scof[o.x] = (unsigned short)i;
-      if (v.y) scof[o.y] = (unsigned short)(i + 1);
-      if (v.z) scof[o.z] = (unsigned short)(i + 2);
-      if (v.w) scof[o.w] = (unsigned short)(i + 3);
-    }
-    base = o.w + v.w;
   }
-  if (tid == 0) bins[ncell] = wsum[NW - 1];
+  if (tid == 0) bins[ncell] = wsum[0];
   __syncthreads();
   PGB_STAMP(5);
   if (staged) {
-    // inclusive max-scan of the marks: per-thread runs of K slots (16-byte
-    // chunks), warp shuffles, one block combine
-    const int K = (((M16 + NT - 1) / NT) + 7) & ~7;
-    const int jb = min(M16, tid * K), je = min(M16, jb + K);
-    int mx = 0;
-    for (int j = jb; j < je; j += 8) {
-      const int4 w4 = *reinterpret_cast<const int4*>(scof + j);
-      const int ws[4] = {w4.x, w4.y, w4.z, w4.w};
+    // inclusive max-scan of the marks: one warp layer (32 lanes x int4 of 8
+    // slots = 256 slots) per chunk; chunk maxima -> exclusive carries in
+    // bins[] (the prefix is no longer needed there), scanned by warp 0
+    const int ns4 = M16 >> 3;                  // int4 groups of 8 slots
+    const int nsch = (ns4 + 31) >> 5;
+    int4* s4 = reinterpret_cast<int4*>(scof);
+    auto max8 = [](const int4 w) {
+      const int a = max(max(w.x & 0xffff, (int)((unsigned)w.x >> 16)), max(w.y & 0xffff, (int)((unsigned)w.y >> 16)));
+      const int b = max(max(w.z & 0xffff, (int)((unsigned)w.z >> 16)), max(w.w & 0xffff, (int)((unsigned)w.w >> 16)));
+      return max(a, b);
+    };
+    for (int ch = warp; ch < nsch; ch += NW) {
+      const int q = (ch << 5) + lane;
+      int mx = q < ns4 ? max8(s4[q]) : 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) mx = max(mx, max(ws[k] & 0xffff, (int)((unsigned)ws[k] >> 16)));
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(~0u, mx, o));
+      if (lane == 0) bins[ch] = mx;
     }
-    int y = mx;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(~0u, y, o);
-      if (lane >= o) y = max(y, t);
-    }
-    if (lane == 31) wmax[warp] = y;
     __syncthreads();
     if (warp == 0) {
-      int m = lane < NW ? wmax[lane] : 0;
+      int carry = 0;
+      for (int c0 = 0; c0 < nsch; c0 += 32) {
+        const int c = c0 + lane;
+        int m = c < nsch ? bins[c] : 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(~0u, m, o);
-        if (lane >= o) m = max(m, t);
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(~0u, m, o);
+          if (lane >= o) m = max(m, y);
+        }
+        const int up = __shfl_up_sync(~0u, m, 1);
+        const int ex = max(carry, lane ? up : 0);
+        if (c < nsch) bins[c] = ex;
+        carry = max(carry, __shfl_sync(~0u, m, 31));
       }
-      if (lane < NW) wmax[lane] = m;
     }
     __syncthreads();
-    int run = max(warp ? wmax[warp - 1] : 0, __shfl_up_sync(~0u, y, 1) * (lane > 0));
-    for (int j = jb; j < je; j += 8) {
-      const int4 w4 = *reinterpret_cast<const int4*>(scof + j);
-      const int ws[4] = {w4.x, w4.y, w4.z, w4.w};
-      int os[4];
+    int4* c4 = reinterpret_cast<int4*>(cof);
+    for (int ch = warp; ch < nsch; ch += NW) {
+      const int q = (ch << 5) + lane;
+      int4 w4 = make_int4(0, 0, 0, 0);
+      if (q < ns4) w4 = s4[q];
+      int m = max8(w4);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int lo = run = max(run, ws[k] & 0xffff);
-        const int hi = run = max(run, (int)((unsigned)ws[k] >> 16));
-        os[k] = lo | (hi << 16);
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(~0u, m, o);
+        if (lane >= o) m = max(m, y);
       }
-      *reinterpret_cast<int4*>(cof + j) = make_int4(os[0], os[1], os[2], os[3]);
+      const int prev = __shfl_up_sync(~0u, m, 1);
+      int r = lane > 0 ? max(bins[ch], prev) : bins[ch];
+      int lo, hi, o0, o1, o2, o3;
+      lo = r = max(r, w4.x & 0xffff); hi = r = max(r, (int)((unsigned)w4.x >> 16)); o0 = lo | (hi << 16);
+      lo = r = max(r, w4.y & 0xffff); hi = r = max(r, (int)((unsigned)w4.y >> 16)); o1 = lo | (hi << 16);
+      lo = r = max(r, w4.z & 0xffff); hi = r = max(r, (int)((unsigned)w4.z >> 16)); o2 = lo | (hi << 16);
+      lo = r = max(r, w4.w & 0xffff); hi = r = max(r, (int)((unsigned)w4.w >> 16)); o3 = lo | (hi << 16);
+      if (q < ns4) c4[q] = make_int4(o0, o1, o2, o3);
     }
     PGB_STAMP(6);
   } else {
@@ -561,7 +595,7 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
     }
   }
   if (tid == 0) {
-    pre[ncell] = wsum[NW - 1];
+    pre[ncell] = wsum[0];
     PairHdr hd = shd;
     hd.cmax = scm;
     out.hdr[pl] = hd;
@@ -603,11 +637,11 @@ struct ItemCfg {
   int cy0, cy1, cx0, cx1;
   int h, wt, shift, field, sep;
   int var;                 // particle-loop variant: 16 * sep + WM (0 = dynamic windows)
-  int kind;                // kItemBand, kItemPro (next batch's pair prologue), kItemEnd
-  long long item;          // band item index (kItemBand) / pair (kItemPro)
+  int kind;                // kItemBand or kItemEnd
+  long long item;          // band item index
   PairHdr hd;
 };
-enum { kItemBand = 0, kItemPro = 1, kItemEnd = 2 };
+enum { kItemBand = 0, kItemEnd = 2 };
 
 struct __align__(16) BandShared {
   int wsum[kBandWarps];
@@ -1318,27 +1352,11 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
   }
 }
 
-// Dynamic schedule (stager lane 0 takes a ticket): the first gridDim.x
-// tickets are band items; after them, when the next batch's pair prologues
-// ride along (cross-launch pipeline), one prologue ticket follows every
-// `pro_stride` band tickets, so that prologue work (latency-bound) overlaps the
-// band work of the co-resident CTA; then the remaining band items.
+// Dynamic schedule: the stager's lane 0 takes the next ticket (band items in
+// order, then kItemEnd).
 __device__ __forceinline__ void ticket_item(const BandParams& P, long long t, int& kind, long long& idx) {
-  const long long B = P.total_items, G = gridDim.x;
-  const long long npro = P.nx_hdr ? P.pairs : 0;
-  kind = kItemBand;
+  kind = t < P.total_items ? kItemBand : kItemEnd;
   idx = t;
-  if (npro > 0 && t >= G) {
-    const long long u = t - G, s = P.pro_stride;
-    const long long grp = u / (s + 1), r = u - grp * (s + 1);
-    if (grp < npro) {
-      if (r == s) { kind = kItemPro; idx = grp; return; }
-      idx = G + grp * s + r;
-    } else {
-      idx = G + npro * s + (u - npro * (s + 1));
-    }
-  }
-  if (idx >= B) kind = kItemEnd;
 }
 
 __device__ __forceinline__ void stage_next(const BandParams& P, BandShared* sh, int b) {
@@ -1626,16 +1644,6 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
       }
 #endif
     }
-    if (kind == kItemPro) {
-      // the next batch's pair prologue (whole block), then re-zero its scratch
-      pair_prologue<kBandBlock>(P, sh->ic[buf].pl, acc0, acc_bytes, pro_next(P));
-      const int ncell = 1 << (P.sy + P.sx);
-      const int scratch = min(acc_bytes, (((ncell < 4 ? 4 : ncell) + 4) & ~3) * 4 + (int)cof_stride(P.n) * 2);
-      for (int e = tid; e < (scratch + 15) / 16; e += kBandBlock)
-        reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
-      __syncthreads();
-      continue;
-    }
     if (stager) {
       __syncthreads();   // particles done
       __syncthreads();   // store done
@@ -1691,6 +1699,18 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
       }
     }
 #endif
+  }
+  // tail work (cross-launch pipeline, opt-in): the next batch's pair
+  // prologues, taken by whichever CTAs finish their band items first
+  if (P.nx_hdr) {
+    for (;;) {
+      if (tid == 0) sh->nseg[0] = atomicAdd(P.ticket + 1, 1);
+      __syncthreads();
+      const int w = sh->nseg[0];
+      if (w >= P.pairs) break;
+      pair_prologue<kBandBlock>(P, w, acc0, acc_bytes, pro_next(P));
+      __syncthreads();
+    }
   }
 #ifdef PGB_PHASE_TIMING
   if (CT && tid == 0) CT[3] = gtime();

@@ -707,8 +707,6 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.split_base = R * G;
   P.split_s = sp;
   P.total_items = R * G + rem * sp;
-  // next-batch prologue tickets interleaved after the first round
-  P.pro_stride = P.nx_hdr ? (int)std::max<long long>(0, (P.total_items - G) / pairs) : 0;
   const int grid = (int)G;
   fn<<<grid, kBandBlock, bp.smem, stream>>>(P);
   g_launches.fetch_add(1);
