@@ -427,10 +427,28 @@ void cell_bits(int H, int W, int& sy, int& sx) {
   }
 }
 
+// Accumulator bytes per CTA such that two band CTAs fit on one SM: half the
+// SM's shared memory minus the per-block reservation, the kernel's static
+// shared memory and the BandShared control block (PGB_BAND_ACC_KB overrides).
 size_t band_acc_budget() {
-  int kb = 110;
-  if (const char* e = std::getenv("PGB_BAND_ACC_KB")) kb = std::max(8, std::atoi(e));
-  return (size_t)kb * 1024;
+  if (const char* e = std::getenv("PGB_BAND_ACC_KB")) return (size_t)std::max(8, std::atoi(e)) * 1024;
+  static size_t cached = 0;
+  if (cached) return cached;
+  int dev = 0, per_sm = 0, reserved = 0;
+  cudaFuncAttributes fa{}, fe{};
+  const bool ok = cudaGetDevice(&dev) == cudaSuccess &&
+                  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess &&
+                  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) == cudaSuccess &&
+                  cudaFuncGetAttributes(&fa, (const void*)band_kernel<kPsfPoint>) == cudaSuccess &&
+                  cudaFuncGetAttributes(&fe, (const void*)band_kernel<kPsfErf>) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    return 110 * 1024;   // no device (host-side planning): the B200 figure
+  }
+  const long long st = (long long)std::max(fa.sharedSizeBytes, fe.sharedSizeBytes);
+  const long long b = (long long)per_sm / 2 - reserved - st - (long long)sizeof(BandShared);
+  cached = (size_t)std::max<long long>(8 * 1024, b);
+  return cached;
 }
 
 BandPlan make_band_plan(int H, int W, int halo) {
