@@ -18,7 +18,8 @@ uniform labels, particle g sits in the cell whose prefix range holds g, at a
 uniform position inside it. The maximum diameter uniform is drawn first
 (m = V^(1/M) with reproducible log/exp, on a uniform particle J); the others
 are uniform on [0, qmax]. Positions are Q17 fixed point (X / 2^17, X odd: the
-centre of a 2^-16 px bin; anchor + exact float32 fraction);
+centre of a 2^-16 px bin; anchor + exact float32 fraction), advected in Q17
+(displacement rounded to 2^-17 px);
 every float32 step is a separately rounded numpy float32 op (no FMA), so
 positions, diameters, sigma, i0, rho, masks, M and side are bit-identical to
 the GPU; Box-Muller normals (frame-2 jitter) and the laser-sheet profile use
@@ -137,10 +138,10 @@ def bilerp32(g00, g01, g10, g11, tx, ty):
     return ((sy * top).astype(F32) + (ty * bot).astype(F32)).astype(F32)
 
 
-def shift_anchor(a, f, d):
-    t = (f + d).astype(F32)
-    k = np.floor((t + F32(0.5)).astype(F32)).astype(F32)
-    return a + k.astype(np.int64), (t - k).astype(F32)
+def advect_anchor(X, d):
+    """fused.cuh advect_anchor: Q17 X2 = X + rint(d 2^17) (round half even), then the anchor/fraction."""
+    X2 = np.asarray(X).astype(np.int64) + np.rint(np.asarray(d, np.float32).astype(np.float64) * 131072.0).astype(np.int64)
+    return fixed_anchor(X2)
 
 
 def hide_threshold(p: float) -> int:
@@ -315,8 +316,8 @@ def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> 
     g = flow_uv.astype(F32)
     u = bilerp32(g[cy, cx, 0], g[cy, cx1, 0], g[cy1, cx, 0], g[cy1, cx1, 0], tx, ty)
     v = bilerp32(g[cy, cx, 1], g[cy, cx1, 1], g[cy1, cx, 1], g[cy1, cx1, 1], tx, ty)
-    ax2, fx2 = shift_anchor(ax1, fx1, u)
-    ay2, fy2 = shift_anchor(ay1, fy1, v)
+    ax2, fx2 = advect_anchor(X, u)
+    ay2, fy2 = advect_anchor(Y, v)
 
     pos1 = np.stack([ax1 + fx1.astype(np.float64), ay1 + fy1.astype(np.float64)], axis=1)
     pos2 = np.stack([ax2 + fx2.astype(np.float64), ay2 + fy2.astype(np.float64)], axis=1)

@@ -231,9 +231,9 @@ def validate_config(cfg: GeneratorConfig) -> None:
         _fail("flow_fields_per_batch",
               f"must divide batch_size ({cfg.flow_fields_per_batch} does not divide "
               f"{cfg.batch_size})")
-    if cfg.image_height >= 30000 or cfg.image_width >= 30000:
-        _fail("image_height" if cfg.image_height >= 30000 else "image_width",
-              "must be below 30000 pixels")
+    if cfg.image_height >= 16384 or cfg.image_width >= 16384:
+        _fail("image_height" if cfg.image_height >= 16384 else "image_width",
+              "must be below 16384 pixels")
 
     _check_range(cfg, "seeding_density_range", 0.0, math.inf, open_lo=True, open_hi=True)
     _check_range(cfg, "diameter_range", 0.0, math.inf, open_lo=True, open_hi=True)

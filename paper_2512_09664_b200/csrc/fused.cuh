@@ -171,7 +171,7 @@ __device__ __forceinline__ float lerpf_exact(float lo, float span, float u) {
 }
 
 // Fixed-point coordinates (Q17): value = X / 2^17 with X odd, i.e. the centre
-// of a 2^-16 px bin; all position arithmetic is 32-bit integer (images < 30000 px).
+// of a 2^-16 px bin; all position arithmetic is 32-bit integer (images < 16384 px).
 // Coordinate -> (anchor floor(v + 1/2), float32 fraction; exact, |f| <= 1/2).
 __device__ __forceinline__ void fixed_anchor(uint32_t X, int& a, float& f) {
   const uint32_t an = (X + (1u << 16)) >> 17;
@@ -205,12 +205,14 @@ __device__ __forceinline__ float bilerp(float g00, float g01, float g10, float g
   return __fadd_rn(__fmul_rn(sy, top), __fmul_rn(ty, bot));
 }
 
-// Anchor after a displacement d of the point (a, f): t = f + d, k = floor(t + 1/2).
-__device__ __forceinline__ void shift_anchor(int a, float f, float d, int& a2, float& f2) {
-  const float t = __fadd_rn(f, d);
-  const float k = floorf(__fadd_rn(t, 0.5f));
-  a2 = a + (int)k;
-  f2 = __fsub_rn(t, k);
+// Advection in Q17 fixed point: X2 = X + rint(d * 2^17) (the displacement is
+// quantised to 2^-17 px, exactly), then anchor floor(v + 1/2) and the exact
+// float32 fraction of the (possibly negative) coordinate.
+__device__ __forceinline__ void advect_anchor(uint32_t X, float d, int& a2, float& f2) {
+  const int X2 = (int)X + __float2int_rn(d * 131072.0f);
+  const int an = (X2 + (1 << 16)) >> 17;   // arithmetic shift: floor
+  a2 = an;
+  f2 = (float)(X2 - (an << 17)) * 0x1p-17f;
 }
 
 __device__ __forceinline__ float laser_profile(const GenCfg& g, float z) {
@@ -283,8 +285,8 @@ __device__ __forceinline__ void gen_particle(const FusedParams& P, int pl, int i
   const float2 q11 = __ldg(flow + (size_t)cy1 * g.W + cx1);
   const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
   const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
-  shift_anchor(f1.ax, f1.fx, u, f2.ax, f2.fx);
-  shift_anchor(f1.ay, f1.fy, v, f2.ay, f2.fy);
+  advect_anchor(X, u, f2.ax, f2.fx);
+  advect_anchor(Y, v, f2.ay, f2.fy);
   f1.amp = amp1; f1.sx = sig; f1.sy = sig; f1.rho = rho;
   f2.amp = amp2; f2.sx = sx2; f2.sy = sy2; f2.rho = rho2;
   // contribution_mask (raster.py:86-88): active & visible & i0 > 0

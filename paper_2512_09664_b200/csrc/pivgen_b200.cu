@@ -372,7 +372,7 @@ GenCfg gen_cfg_from(const pgb_config* c) {
 void validate_cfg(const pgb_config* c) {
   PGB_REQUIRE(c != nullptr, "config is NULL");
   PGB_REQUIRE(c->height >= 2 && c->width >= 2, "image sides must be >= 2 px (bilinear flow sampling)");
-  PGB_REQUIRE(c->height < 30000 && c->width < 30000, "image side must be < 30000");
+  PGB_REQUIRE(c->height < 16384 && c->width < 16384, "image side must be < 16384 (Q17 positions in int32)");
   PGB_REQUIRE(c->n_capacity >= 1, "n_capacity must be >= 1");
   PGB_REQUIRE(c->psf == PGB_PSF_POINT || c->psf == PGB_PSF_ERF, "unknown psf");
   PGB_REQUIRE(c->sigma_ratio > 0 && c->patch_multiplier > 0, "ratio/multiplier must be > 0");

@@ -1,6 +1,6 @@
 """Summarise ncu captures for profiles/ (committed evidence).
 
-Usage: python scripts/profile_summary.py <full.ncu-rep> <launches.csv> <out_prefix>
+Usage: python scripts/profile_summary.py <full.ncu-rep> <launches.csv|-> <out_prefix> [config]
 Writes <out_prefix>_launches.txt (kernel launch list with durations) and
 <out_prefix>_band_kernel.txt (speed-of-light, memory traffic, occupancy,
 stall reasons and per-phase instruction split of the dominant kernel), and
@@ -14,13 +14,35 @@ import subprocess
 import sys
 
 rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
+cfgname = sys.argv[4] if len(sys.argv) > 4 else "c2"
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
+
+def band_ranges():
+    """Source regions of band.cuh located by their section comments."""
+    src = open(os.path.join(root, "paper_2512_09664_b200", "csrc", "band.cuh")).read().split("\n")
+    marks = [("prologue", "// Per-pair prologue"), ("splat", "// Tight window of one particle-frame"),
+             ("store", "// Epilogue: one output quad"), ("stage", "// Range of seeding cells"),
+             ("gen", "// One regenerated particle"), ("loop", "// Worker warps: regenerate"),
+             ("kernel", "__global__ void PGB_BAND_BOUNDS band_kernel"),
+             ("end", "// Particle arrays of the generator")]
+    pos = []
+    for name, m in marks:
+        ln = next(i + 1 for i, l in enumerate(src) if l.startswith(m))
+        pos.append((name, ln))
+    pos.sort(key=lambda t: t[1])
+    out = []
+    for (n, a), (_, b) in zip(pos, pos[1:]):
+        if n != "end":
+            out.append(f"{n}=band.cuh:{a}-{b - 1}")
+    return ",".join(out + ["fused_helpers=fused.cuh:1-1200", "philox=common.cuh:1-400"])
+
+
 # ---- launch list
-rows = [r for r in csv.DictReader(l for l in open(launches) if not l.startswith("=="))]
-with open(prefix + "_launches.txt", "w") as fh:
+rows = [r for r in csv.DictReader(l for l in open(launches) if not l.startswith("=="))] if launches != "-" else []
+with open(prefix + "_launches.txt", "w") if rows else open(os.devnull, "w") as fh:
     fh.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n")
-    fh.write("# command: python bench.py --steps 5 --warmup 3 --no-cpu-baseline (config c2)\n")
+    fh.write(f"# command: python bench.py --steps 5 --warmup 3 --no-cpu-baseline --config {cfgname}\n")
     for r in rows:
         fh.write(f"{r['ID']:>4s}  {r['Kernel Name'][:70]:70s}  {float(r['Metric Value'])/1000:9.2f} us\n")
     band = [float(r["Metric Value"]) for r in rows if "band_kernel" in r["Kernel Name"]]
@@ -53,17 +75,18 @@ stalls = {k[len("smsp__pcsamp_warps_issue_stalled_"):]: f(k) for k in hdr
           if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
 tot = sum(v for v in stalls.values() if v == v) or 1.0
 phases = subprocess.run([sys.executable, os.path.join(root, "scripts", "ncu_lines.py"), rep, "0",
-                         "splat=band.cuh:395-610,store=band.cuh:611-760,stage=band.cuh:761-860,"
-                         "gen=band.cuh:80-215,prologue=band.cuh:216-400,loop=band.cuh:861-1000,"
-                         "fused_helpers=fused.cuh:1-1200,philox=common.cuh:1-400"],
+                         band_ranges()],
                         capture_output=True, text=True).stdout
 with open(prefix + "_band_kernel.txt", "w") as fh:
     fh.write("# ncu --set full --clock-control none --import-source on -k regex:band_kernel -s 3 -c 1\n")
-    fh.write("#   python bench.py --steps 3 --warmup 3 --no-cpu-baseline   (c2: 256x256, B=256, f32)\n")
+    fh.write(f"#   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --config {cfgname}\n")
     fh.write(f"duration_us                {dur_ns/1000:.2f}\n")
     fh.write(f"dram_bytes_read            {dram_r:.0f}\n")
     fh.write(f"dram_bytes_write           {dram_w:.0f}\n")
-    fh.write(f"algorithmic_bytes          {256*2*256*256*4} (2 f32 frames x 256 pairs)\n")
+    sys.path.insert(0, root)
+    import bench  # noqa: E402
+    H, W, B = bench.CONFIGS[cfgname][:3]
+    fh.write(f"algorithmic_bytes          {B*2*H*W*4} (2 f32 frames x {B} pairs of {H}x{W})\n")
     for k in ["sm__throughput.avg.pct_of_peak_sustained_elapsed",
               "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
               "dram__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -81,7 +104,7 @@ with open(prefix + "_band_kernel.txt", "w") as fh:
 
 tp = os.path.join(root, "profiles", "traffic.json")
 tj = json.load(open(tp)) if os.path.exists(tp) else {}
-tj["c2"] = {"kernel": "pgb::band_kernel<0>", "dram_bytes_per_launch": dram_r + dram_w,
+tj[cfgname] = {"kernel": "pgb::band_kernel<0>", "dram_bytes_per_launch": dram_r + dram_w,
             "dram_read": dram_r, "dram_write": dram_w, "duration_us_ncu": dur_ns / 1000,
             "source": os.path.basename(prefix) + "_band_kernel.txt"}
 json.dump(tj, open(tp, "w"), indent=1)

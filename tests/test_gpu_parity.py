@@ -384,3 +384,47 @@ def test_spec_oracle_equivalence_random_configs(pg, seed):
             got = np.zeros((64, 64), np.float32)
             pg.splat_accumulate(*args, got, 0, 64)
         _assert_close(got, want, what=f"config {seed}/{k}")
+
+
+@pytest.mark.parametrize("env", [
+    {},                                   # defaults: dynamic schedule, split last round, two control heads
+    {"PGB_NO_SPLIT": "1"},               # whole tiles only
+    {"PGB_PIPELINE": "1"},               # cross-launch prologue pipeline (tail work)
+    {"PGB_TMA_STORE": "1"},              # finalize in place + cp.async.bulk stores
+    {"PGB_TILE": "16,128"},              # other tilings: the integer accumulation and the
+    {"PGB_TILE": "32,64"},               # Q17 positions make every pixel tiling-independent
+])
+@pytest.mark.parametrize("sep", [False, True])
+def test_schedule_and_store_paths_bit_identical(pg, env, sep, monkeypatch):
+    """Every schedule / tiling / store / pipelining path yields the same bits as
+    a cold launch of the same batch, over a sequence of consecutive batches on
+    one stream (the pipeline reuses the previous launch's prologue tables)."""
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    H, W, B = 128, 128, 12
+    extra = dict(diameter_range=(0.8, 1.2), rho_range=(0.0, 0.0), frame2_sigma_std=0.0,
+                 frame2_intensity_std=0.0, frame2_rho_std=0.0, hide_probability=0.0) if sep else {}
+    cfg = _gen_cfg(pg, image_height=H, image_width=W, batch_size=B, **extra)
+    flows = pg.from_function(vortex_fn(H, W), H, W).to_device().unsqueeze(0)
+    stream = torch.cuda.current_stream()
+
+    def run(batch, mode=_lib.OUT_F32):
+        img = [torch.empty((B, H, W), dtype=torch.float32, device="cuda") for _ in range(2)]
+        _lib.call("pgb_generate_batch_dev", native_config(cfg), batch, 0, B, flows.data_ptr(), 1, B, mode,
+                  img[0].data_ptr(), img[1].data_ptr(), None, None, stream.cuda_stream)
+        return [i.cpu().numpy() for i in img]
+
+    ref = {}
+    for b in range(4):
+        run(99)                     # break any cached prologue
+        ref[b] = run(b)             # cold launch of batch b
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    run(0)
+    for b in range(1, 4):           # consecutive batches: warm pipeline
+        got = run(b)
+        for f in range(2):
+            np.testing.assert_array_equal(got[f], ref[b][f], err_msg=f"{env} batch {b} frame {f + 1}")
