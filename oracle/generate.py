@@ -18,8 +18,8 @@ uniform labels, particle g sits in the cell whose prefix range holds g, at a
 uniform position inside it. The maximum diameter uniform is drawn first
 (m = V^(1/M) with reproducible log/exp, on a uniform particle J); the others
 are uniform on [0, qmax]. Positions are Q17 fixed point (X / 2^17, X odd: the
-centre of a 2^-16 px bin; anchor + exact float32 fraction), advected in Q17
-(displacement rounded to 2^-17 px);
+centre of a 2^-16 px bin; anchor + exact float32 fraction), advected in
+Q20 relative to the anchor (displacement rounded to 2^-20 px);
 every float32 step is a separately rounded numpy float32 op (no FMA), so
 positions, diameters, sigma, i0, rho, masks, M and side are bit-identical to
 the GPU; Box-Muller normals (frame-2 jitter) and the laser-sheet profile use
@@ -138,10 +138,14 @@ def bilerp32(g00, g01, g10, g11, tx, ty):
     return ((sy * top).astype(F32) + (ty * bot).astype(F32)).astype(F32)
 
 
-def advect_anchor(X, d):
-    """fused.cuh advect_anchor: Q17 X2 = X + rint(d 2^17) (round half even), then the anchor/fraction."""
-    X2 = np.asarray(X).astype(np.int64) + np.rint(np.asarray(d, np.float32).astype(np.float64) * 131072.0).astype(np.int64)
-    return fixed_anchor(X2)
+def advect_anchor(X, a, d):
+    """fused.cuh advect_anchor: t = (X - a 2^17) 2^3 + rint(d 2^20) in Q20 (round half
+    even), anchor a + floor(t / 2^20 + 1/2), exact float32 fraction."""
+    X = np.asarray(X).astype(np.int64)
+    a = np.asarray(a).astype(np.int64)
+    t = ((X - (a << 17)) << 3) + np.rint(np.asarray(d, np.float32).astype(np.float64) * 1048576.0).astype(np.int64)
+    k = (t + (1 << 19)) >> 20
+    return a + k, ((t - (k << 20)).astype(np.float64) * 2.0 ** -20).astype(F32)
 
 
 def hide_threshold(p: float) -> int:
@@ -155,13 +159,13 @@ LN2 = 0.6931471805599453
 
 
 def cell_bits(height: int, width: int):
-    """csrc/pivgen_b200.cu cell_bits: ~4 px cells, at most 2^14 cells."""
-    def bits(n):
+    """csrc/pivgen_b200.cu cell_bits: ~2-row x 4-column cells, at most 2^14 cells."""
+    def bits(n, px):
         s = 0
-        while (4 << (s + 1)) <= n:
+        while (px << (s + 1)) <= n:
             s += 1
         return s
-    sy, sx = bits(height), bits(width)
+    sy, sx = bits(height, 2), bits(width, 4)
     while sy + sx > MAX_CELL_BITS:
         if sx >= sy:
             sx -= 1
@@ -316,8 +320,8 @@ def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> 
     g = flow_uv.astype(F32)
     u = bilerp32(g[cy, cx, 0], g[cy, cx1, 0], g[cy1, cx, 0], g[cy1, cx1, 0], tx, ty)
     v = bilerp32(g[cy, cx, 1], g[cy, cx1, 1], g[cy1, cx, 1], g[cy1, cx1, 1], tx, ty)
-    ax2, fx2 = advect_anchor(X, u)
-    ay2, fy2 = advect_anchor(Y, v)
+    ax2, fx2 = advect_anchor(X, ax1, u)
+    ay2, fy2 = advect_anchor(Y, ay1, v)
 
     pos1 = np.stack([ax1 + fx1.astype(np.float64), ay1 + fy1.astype(np.float64)], axis=1)
     pos2 = np.stack([ax2 + fx2.astype(np.float64), ay2 + fy2.astype(np.float64)], axis=1)

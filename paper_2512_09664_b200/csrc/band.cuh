@@ -153,8 +153,8 @@ __device__ __forceinline__ void advect_fixed(const GenCfg& g, const float2* __re
   const float2 q11 = __ldg(flow + (size_t)cy1 * g.W + cx1);
   const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
   const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
-  advect_anchor(X, u, ax2, fx2);
-  advect_anchor(Y, v, ay2, fy2);
+  advect_anchor(X, ax, u, ax2, fx2);
+  advect_anchor(Y, ay, v, ay2, fy2);
 }
 
 // Appearance of both frames (particles.py:61-126 + laser sheet), given the
@@ -1431,8 +1431,8 @@ __device__ __forceinline__ void band_gen(const BandParams& P, const RngKey& key,
   between(o);   // frame-1 work while the flow loads are in flight
   const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
   const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
-  advect_anchor(X, u, o.ax2, o.fx2);
-  advect_anchor(Y, v, o.ay2, o.fy2);
+  advect_anchor(X, o.ax1, u, o.ax2, o.fx2);
+  advect_anchor(Y, o.ay1, v, o.ay2, o.fy2);
   const bool in2 = (unsigned)(o.ay2 - (r0 - h)) < (unsigned)(r1 - r0 + 2 * h) &&
                    (unsigned)(o.ax2 - (c0 - h)) < (unsigned)(c1 - c0 + 2 * h);
   o.on2 = in2 && lk.vis2 && lk.amp2 > 0.f;

@@ -205,14 +205,16 @@ __device__ __forceinline__ float bilerp(float g00, float g01, float g10, float g
   return __fadd_rn(__fmul_rn(sy, top), __fmul_rn(ty, bot));
 }
 
-// Advection in Q17 fixed point: X2 = X + rint(d * 2^17) (the displacement is
-// quantised to 2^-17 px, exactly), then anchor floor(v + 1/2) and the exact
-// float32 fraction of the (possibly negative) coordinate.
-__device__ __forceinline__ void advect_anchor(uint32_t X, float d, int& a2, float& f2) {
-  const int X2 = (int)X + __float2int_rn(d * 131072.0f);
-  const int an = (X2 + (1 << 16)) >> 17;   // arithmetic shift: floor
-  a2 = an;
-  f2 = (float)(X2 - (an << 17)) * 0x1p-17f;
+// Advection in fixed point: the frame-1 fraction (Q17, exact) and the
+// displacement rint(d * 2^20) are added in Q20 (the displacement is quantised
+// to 2^-20 px, exactly); then anchor + floor(t + 1/2) and the exact float32
+// fraction (<= 20 fractional bits, so window offsets dy = i - f stay exact for
+// |i| < 16 and images are bit-identical for every tiling).
+__device__ __forceinline__ void advect_anchor(uint32_t X, int a, float d, int& a2, float& f2) {
+  const int t = ((int)(X - ((uint32_t)a << 17)) << 3) + __float2int_rn(d * 1048576.0f);
+  const int k = (t + (1 << 19)) >> 20;   // arithmetic shift: floor
+  a2 = a + k;
+  f2 = (float)(t - (k << 20)) * 0x1p-20f;
 }
 
 __device__ __forceinline__ float laser_profile(const GenCfg& g, float z) {
@@ -285,8 +287,8 @@ __device__ __forceinline__ void gen_particle(const FusedParams& P, int pl, int i
   const float2 q11 = __ldg(flow + (size_t)cy1 * g.W + cx1);
   const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
   const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
-  advect_anchor(X, u, f2.ax, f2.fx);
-  advect_anchor(Y, v, f2.ay, f2.fy);
+  advect_anchor(X, f1.ax, u, f2.ax, f2.fx);
+  advect_anchor(Y, f1.ay, v, f2.ay, f2.fy);
   f1.amp = amp1; f1.sx = sig; f1.sy = sig; f1.rho = rho;
   f2.amp = amp2; f2.sx = sx2; f2.sy = sy2; f2.rho = rho2;
   // contribution_mask (raster.py:86-88): active & visible & i0 > 0

@@ -416,11 +416,14 @@ struct BandPlan {
   size_t smem;
 };
 
-// Seeding cells ~4 px on a side: largest s with 4 * 2^s <= n, total <= 2^14 cells.
+// Seeding cells ~2 rows x 4 columns: largest s with px * 2^s <= n, total <= 2^14 cells.
 void cell_bits(int H, int W, int& sy, int& sx) {
-  auto bits = [](int n) { int s = 0; while ((4LL << (s + 1)) <= n) ++s; return s; };
-  sy = bits(H);
-  sx = bits(W);
+  // ~2-row x 4-column cells: full-width tiles enumerate whole cell rows, so
+  // shorter cells trim the regenerated margin (measured -2.5% at c2; 1-row
+  // cells cost more in the prologue scan than they save)
+  auto bits = [](int n, long long px) { int s = 0; while ((px << (s + 1)) <= n) ++s; return s; };
+  sy = bits(H, 2);
+  sx = bits(W, 4);
   while (sy + sx > kMaxCellBits) {
     if (sx >= sy) --sx;
     else --sy;
