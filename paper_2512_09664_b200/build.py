@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     extra = []
     if os.environ.get("PGB_BAND_MAXREG"):      # tuning knob: band kernel register cap
         extra.append(f"-DPGB_BAND_MAXREG={int(os.environ['PGB_BAND_MAXREG'])}")
-    for knob in ("PGB_ILP", "PGB_BAND_MINB", "PGB_WORKER_WARPS", "PGB_FRAME_LOOP"):
+    for knob in ("PGB_BAND_MINB", "PGB_WORKER_WARPS"):
         if os.environ.get(knob):
             extra.append(f"-D{knob}={int(os.environ[knob])}")
     if os.environ.get("PGB_DBG_NOATOM"):

@@ -32,12 +32,6 @@
 
 namespace pgb {
 
-#ifndef PGB_FRAME_LOOP
-#define PGB_FRAME_LOOP 0   // 1: one splat code copy looped over both frames
-#endif
-#ifndef PGB_ILP
-#define PGB_ILP 1   // particles regenerated per thread per loop iteration
-#endif
 #ifdef PGB_BAND_MAXREG
 #define PGB_BAND_BOUNDS __maxnreg__(PGB_BAND_MAXREG)
 #else
@@ -1449,7 +1443,6 @@ __device__ __forceinline__ uint4 draw_a(const GenCfg& g, const RngKey& key, int 
 template <int PSF, int SEP, int WM>
 __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* sh, int buf, long long item,
                                                int* acc0, int* acc1) {
-  constexpr int STEP = 2 * kBandThreads;
   const int tid = threadIdx.x, warp = tid >> 5;
   const ItemCfg& ic = sh->ic[buf];
   const int pl = ic.pl;
@@ -1482,44 +1475,7 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
       }
       return sst[sg] + (q - soff[sg]);
     };
-    if constexpr (PGB_ILP == 2) {
-      int gA = 0, cA = 0, gB = 0, cB = 0;
-      if (N > 0) {
-        gA = locate(tid);
-        gB = locate(tid + kBandThreads);
-        cA = __ldcg(cof + gA);
-        cB = __ldcg(cof + gB);
-      }
-      // warp-uniform trip count + __syncwarp: keeps the warp converged
-      for (int qb = 0; qb < N; qb += STEP) {
-        const int qa = qb + tid, qb2 = qa + kBandThreads;
-        const int giA = gA, ccA = cA, giB = gB, ccB = cB;
-        if (qb + STEP < N) {
-          gA = locate(qa + STEP);
-          gB = locate(qb2 + STEP);
-          cA = __ldcg(cof + gA);
-          cB = __ldcg(cof + gB);
-        }
-        PFrames A, B;
-        const uint4 aA = draw_a(P.g, key, giA), aB = draw_a(P.g, key, giB);
-        band_gen(P, key, hd, flow, giA, ccA, aA, h, r0, r1, c0, c1, A, [](const PFrames&) {});
-        band_gen(P, key, hd, flow, giB, ccB, aB, h, r0, r1, c0, c1, B, [](const PFrames&) {});
-        const bool okA = qa < N, okB = qb2 < N;
-        if (okA && A.on1)
-          splat_v<PSF, SEP, WM>(acc0, P.AS, A.ax1, A.ay1, A.fx1, A.fy1, A.amp1, A.sig, A.sig, A.rho1, h, r0, r1,
-                                c0, c1, shift, scale);
-        if (okA && A.on2)
-          splat_v<PSF, SEP, WM>(acc1, P.AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, A.rho2, h, r0, r1,
-                                c0, c1, shift, scale);
-        if (okB && B.on1)
-          splat_v<PSF, SEP, WM>(acc0, P.AS, B.ax1, B.ay1, B.fx1, B.fy1, B.amp1, B.sig, B.sig, B.rho1, h, r0, r1,
-                                c0, c1, shift, scale);
-        if (okB && B.on2)
-          splat_v<PSF, SEP, WM>(acc1, P.AS, B.ax2, B.ay2, B.fx2, B.fy2, B.amp2, B.sx2, B.sy2, B.rho2, h, r0, r1,
-                                c0, c1, shift, scale);
-        __syncwarp();
-      }
-    } else {
+    {
       // software pipeline: the Philox draw of the next slot is computed while
       // this slot's flow loads are in flight; its cell load one slot ahead
       int gA = 0, cA = 0;
@@ -1540,20 +1496,6 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
         }
         PFrames A;
         const bool ok = qa < N;
-#if PGB_FRAME_LOOP
-        // one copy of the splat code for both frames (smaller hot loop)
-        band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames&) {
-          if (more) aA = draw_a(P.g, key, gA);
-        });
-#pragma unroll 1
-        for (int f = 0; f < 2; ++f) {
-          const bool on = f ? A.on2 : A.on1;
-          if (ok && on && !(P.ablate & 2))
-            splat_v<PSF, SEP, WM>(f ? acc1 : acc0, P.AS, f ? A.ax2 : A.ax1, f ? A.ay2 : A.ay1, f ? A.fx2 : A.fx1,
-                                  f ? A.fy2 : A.fy1, f ? A.amp2 : A.amp1, f ? A.sx2 : A.sig, f ? A.sy2 : A.sig,
-                                  f ? A.rho2 : A.rho1, h, r0, r1, c0, c1, shift, scale);
-        }
-#else
         band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
           if (ok && F.on1 && !(P.ablate & 2))
             splat_v<PSF, SEP, WM>(acc0, P.AS, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, F.rho1, h, r0,
@@ -1565,7 +1507,6 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
             splat_v<PSF, SEP, WM>(acc1, P.AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, A.rho2, h, r0,
                                   r1, c0, c1, shift, scale);
         }
-#endif
         __syncwarp();
       }
     }
