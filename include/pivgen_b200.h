@@ -23,6 +23,7 @@
  *   pgb_sample_flow_dev       <- flowfield.py:207-232 sample_flow()
  *   pgb_finalize_dev          <- raster.py:154-161 finalize()
  *   pgb_quantize_u16_dev      <- export.py:19-20 quantize_u16()
+ *   pgb_match_histogram_dev   <- raster.py:164-187 match_histogram()
  *   pgb_generate_batch_dev    <- pipeline.py:278-329 Sampler._render_batch()
  *   pgb_generate_batch        <- same, host buffers (end-to-end path)
  *   pgb_sample_particles_dev  <- particles.py:61-147 sample_particles /
@@ -142,6 +143,14 @@ int pgb_finalize_dev(const float* raw, int pairs, int height, int width, double 
                      int frame, int out_mode, void* out, void* stream);
 
 int pgb_quantize_u16_dev(const float* img, int64_t count, uint16_t* out, void* stream);
+
+/* Histogram specification of `images` float32 images of `pixels` each (one
+ * after another, in place allowed): levels rint(x*255) clipped to [0, 255],
+ * midpoint-CDF source quantiles, searchsorted('left') into target_cdf
+ * (device float64[256] = cumsum(hist) / sum(hist)), output mapping / 255.
+ * Bit-identical to raster.py:164-187 match_histogram(). */
+int pgb_match_histogram_dev(const float* img, float* out, int64_t images, int64_t pixels,
+                            const double* target_cdf, void* stream);
 
 /* Full generation of one batch shard: global pairs [pair_base, pair_base + pairs)
  * of batch `batch`. flows: device float32 [num_fields][height][width][2];

@@ -190,3 +190,21 @@ def tile_counts(pos, on, sx, sy, halo, tile_h, tile_w, height, width, row_lo=0, 
         for ty in range(r_lo, r_hi + 1):
             counts[ty * tiles_x + c_lo: ty * tiles_x + c_hi + 1] += 1
     return counts
+
+
+def match_histogram(img: np.ndarray, target) -> np.ndarray:
+    """Histogram specification on 256 levels (restates reference raster.py:164-187):
+    float32 levels rint(x * 255) clipped to [0, 255]; midpoint-CDF source
+    quantile (cum - counts/2) / total in float64; first target-CDF entry >= it
+    (searchsorted 'left', clipped to 255); output level / 255 as float32."""
+    hist = np.asarray(target, dtype=np.float64)
+    x = np.asarray(img, dtype=np.float32)
+    lev = np.rint(x * np.float32(255.0)).astype(np.float32)
+    lev = np.where(np.isnan(lev), np.float32(0.0), np.clip(lev, 0, 255)).astype(np.int64)
+    counts = np.zeros(256, np.int64)
+    np.add.at(counts, lev.reshape(-1), 1)
+    cum = np.cumsum(counts).astype(np.float64)
+    q = (cum - 0.5 * counts.astype(np.float64)) / float(x.size)
+    cdf = np.cumsum(hist) / hist.sum()
+    mapping = np.minimum(np.searchsorted(cdf, q, side="left"), 255)
+    return (mapping[lev].astype(np.float64) / 255.0).astype(np.float32)

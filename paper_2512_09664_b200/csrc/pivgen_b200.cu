@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "fused.cuh"
 #include "band.cuh"
+#include "histmatch.cuh"
 
 namespace pgb {
 
@@ -940,6 +941,19 @@ int pgb_quantize_u16_dev(const float* img, int64_t count, uint16_t* out, void* s
   return guarded([&] {
     if (count <= 0) return;
     quantize_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(img, count, out);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_match_histogram_dev(const float* img, float* out, int64_t images, int64_t pixels,
+                            const double* target_cdf, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(images >= 0 && pixels >= 0, "images and pixels must be >= 0");
+    PGB_REQUIRE(images <= 0x7fffffff, "too many images");
+    if (images == 0 || pixels == 0) return;
+    PGB_REQUIRE(img && out && target_cdf, "null pointer");
+    hist_match_kernel<<<(unsigned)images, kHistThreads, 0, (cudaStream_t)stream>>>(img, out, pixels, target_cdf);
     g_launches.fetch_add(1);
     PGB_CK(cudaGetLastError());
   });

@@ -163,28 +163,38 @@ def quantize_u16(img):
     return like_input(out, img)
 
 
-def match_histogram(img, target):
-    """Histogram specification on 256 levels (raster.py:164-187), on the GPU.
-
-    Interim implementation with torch device ops (bincount/cumsum/searchsorted);
-    SURVEY 8(f) row f1 (fused CUDA pass) is the planned replacement."""
-    hist = torch.as_tensor(np.asarray(target, dtype=np.float64))
+def target_cdf(target) -> np.ndarray:
+    """cumsum(hist) / sum(hist) in float64, exactly as the reference (raster.py:181)."""
+    hist = np.asarray(target, dtype=np.float64)
     if hist.shape != (256,):
-        raise ValueError(f"target histogram must have 256 bins, got {tuple(hist.shape)}")
-    if (hist < 0).any() or not torch.isfinite(hist).all() or hist.sum() <= 0:
+        raise ValueError(f"target histogram must have 256 bins, got {hist.shape}")
+    if (hist < 0).any() or not np.isfinite(hist).all() or hist.sum() <= 0:
         raise ValueError("target histogram must be non-negative with positive sum")
+    return np.cumsum(hist) / hist.sum()
+
+
+def match_histogram(img, target, out=None):
+    """Histogram specification on 256 levels (raster.py:164-187), one CUDA
+    block per image (csrc/histmatch.cuh), bit-identical to the reference.
+
+    img: (H, W) or (N, H, W) float32 (numpy or torch); returns the same kind.
+    `out` (a CUDA float32 tensor of img's shape, may be img itself) receives
+    the result in place."""
+    cdf = target_cdf(target)
     is_tensor = isinstance(img, torch.Tensor)
     dev = img.device if is_tensor and img.is_cuda else cuda_device()
-    x = to_dev(img, torch.float32, dev)
-    levels = torch.clamp(torch.round(x.double() * 255.0), 0, 255).to(torch.int64)
-    counts = torch.bincount(levels.reshape(-1), minlength=256).double()
-    cum = torch.cumsum(counts, 0)
-    src_q = (cum - 0.5 * counts) / counts.sum()
-    tgt = hist.to(dev)
-    tgt_cdf = torch.cumsum(tgt, 0) / tgt.sum()
-    mapping = torch.clamp(torch.searchsorted(tgt_cdf, src_q, right=False), 0, 255)
-    out = (mapping[levels].double() / 255.0).to(torch.float32)
-    return out if is_tensor else out.cpu().numpy()
+    x = to_dev(img, torch.float32, dev).contiguous()
+    if x.dim() < 2:
+        raise ValueError("match_histogram expects an (H, W) or (N, H, W) image")
+    pixels = x.shape[-1] * x.shape[-2]
+    images = x.numel() // pixels if pixels else 0
+    dst = out if out is not None else torch.empty_like(x)
+    if dst.dtype != torch.float32 or not dst.is_contiguous() or dst.shape != x.shape or dst.device != x.device:
+        raise ValueError("out must be a contiguous float32 tensor of the image's shape on its device")
+    cdf_dev = torch.from_numpy(cdf).to(dev)
+    _lib.call("pgb_match_histogram_dev", x.data_ptr(), dst.data_ptr(), images, pixels, cdf_dev.data_ptr(),
+              stream_ptr(dev))
+    return dst if is_tensor else dst.cpu().numpy()
 
 
 def render_pair(pset: ParticleSet, height: int, width: int, side: int, noise: NoiseConfig,

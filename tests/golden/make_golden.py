@@ -93,11 +93,50 @@ def main() -> None:
     np.savez_compressed(path, **out)
     print("wrote", path, os.path.getsize(path), "bytes,", len(names), "cases")
 
+    make_histmatch(raster)
+
     exe = os.path.join(ROOT, "oracle", "_ref", "philox_curand_check")
     txt = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
     with open(os.path.join(HERE, "philox_curand.txt"), "w") as fh:
         fh.write(txt)
     print("wrote philox_curand.txt")
+
+
+def make_histmatch(raster) -> None:
+    """tests/golden/histmatch_cases.npz: reference raster.match_histogram (raster.py:164-187)
+    on rendered-looking and edge-case images against several target histograms."""
+    rng = np.random.default_rng(2512)
+    H, W = 48, 64
+    yy, xx = np.mgrid[0:H, 0:W].astype(np.float64)
+    blobs = np.zeros((H, W))
+    for _ in range(60):
+        cy, cx, s = rng.uniform(0, H), rng.uniform(0, W), rng.uniform(0.3, 1.5)
+        blobs += np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / (2 * s * s))
+    images = {
+        "blobs": np.clip(blobs, 0, 1).astype(np.float32),
+        "uniform": rng.uniform(0, 1, (H, W)).astype(np.float32),
+        "constant": np.full((H, W), 0.37, np.float32),
+        "out_of_range": rng.normal(0.5, 0.6, (H, W)).astype(np.float32),
+        "half_levels": ((rng.integers(0, 256, (H, W)) + 0.5) / 255.0).astype(np.float32),
+    }
+    lev = np.arange(256, dtype=np.float64)
+    targets = {
+        "flat": np.ones(256),
+        "dark": np.exp(-lev / 20.0),
+        "gauss": np.exp(-0.5 * ((lev - 128.0) / 30.0) ** 2),
+        "sparse": np.where(lev % 17 == 0, 3.0, 0.0),
+        "random": rng.uniform(0, 1, 256),
+    }
+    out = {}
+    for iname, img in images.items():
+        out[f"img/{iname}"] = img
+        for tname, tgt in targets.items():
+            out[f"out/{iname}/{tname}"] = raster.match_histogram(img, tgt)
+    for tname, tgt in targets.items():
+        out[f"tgt/{tname}"] = tgt
+    path = os.path.join(HERE, "histmatch_cases.npz")
+    np.savez_compressed(path, **out)
+    print("wrote", path, os.path.getsize(path), "bytes")
 
 
 if __name__ == "__main__":

@@ -428,3 +428,52 @@ def test_schedule_and_store_paths_bit_identical(pg, env, sep, monkeypatch):
         got = run(b)
         for f in range(2):
             np.testing.assert_array_equal(got[f], ref[b][f], err_msg=f"{env} batch {b} frame {f + 1}")
+
+
+def test_match_histogram_kernel_bit_exact(pg):
+    """CUDA histogram specification (csrc/histmatch.cuh) vs the reference's own
+    outputs (golden) and the oracle: single images, one batched launch over a
+    stack, and in place."""
+    import os
+
+    import torch
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "histmatch_cases.npz"))
+    inames = sorted({k.split("/")[1] for k in g.files if k.startswith("img/")})
+    tnames = sorted({k.split("/")[1] for k in g.files if k.startswith("tgt/")})
+    for t in tnames:
+        tgt = g[f"tgt/{t}"]
+        for i in inames:
+            got = pg.match_histogram(g[f"img/{i}"], tgt)
+            np.testing.assert_array_equal(got, g[f"out/{i}/{t}"], err_msg=f"{i}/{t}")
+        stack = torch.from_numpy(np.stack([g[f"img/{i}"] for i in inames])).cuda()
+        pg.match_histogram(stack, tgt, out=stack)
+        for n, i in enumerate(inames):
+            np.testing.assert_array_equal(stack[n].cpu().numpy(), g[f"out/{i}/{t}"], err_msg=f"stack {i}/{t}")
+    rng = np.random.default_rng(5)
+    for shape in ((37, 53), (3, 256, 256), (2, 17, 31)):
+        img = rng.uniform(-0.1, 1.1, shape).astype(np.float32)
+        tgt = rng.uniform(0, 1, 256)
+        got = pg.match_histogram(img, tgt)
+        want = np.stack([orr.match_histogram(x, tgt) for x in img.reshape(-1, *shape[-2:])]).reshape(shape)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_sampler_target_histogram_float_and_u16(pg):
+    """Sampler with target_histogram: every frame equals match_histogram of the
+    plain frame (float32), and the uint16 output is its quantisation."""
+    tgt = tuple(float(x) for x in np.exp(-np.arange(256) / 40.0))
+    pg.register_flow_function("vortex64", vortex_fn(64, 64))
+    base = pg.GeneratorConfig(image_height=64, image_width=64, batch_size=3, seed=21,
+                              flow_sources=(pg.FlowSource(function="vortex64"),))
+    with pg.make_sampler(base) as s:
+        plain = next(s)
+    with pg.make_sampler(pg.with_updates(base, target_histogram=tgt)) as s:
+        matched = next(s)
+    with pg.make_sampler(pg.with_updates(base, target_histogram=tgt, output_dtype="uint16")) as s:
+        q = next(s)
+    for a, b, c in ((plain.images1, matched.images1, q.images1), (plain.images2, matched.images2, q.images2)):
+        for p in range(3):
+            want = orr.match_histogram(a[p].cpu().numpy(), tgt)
+            np.testing.assert_array_equal(b[p].cpu().numpy(), want)
+            np.testing.assert_array_equal(c[p].cpu().numpy(), orr.quantize_u16(want))

@@ -210,3 +210,20 @@ def test_stratified_seeding_law():
     # diameters below the maximum are uniform on [d_lo, d_max]
     dd = np.concatenate([og.sample_pair(cfg, 1, p, flow)["diameter"][:100] for p in range(20)])
     assert 0.4 < (dd < 1.75).mean() < 0.6
+
+
+def test_match_histogram_oracle_bit_exact_vs_reference_golden():
+    """oracle.render.match_histogram == reference raster.match_histogram
+    (raster.py:164-187) on the committed golden cases, bit for bit."""
+    import os
+
+    from oracle import render as orr
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "histmatch_cases.npz"))
+    keys = [k for k in g.files if k.startswith("out/")]
+    assert len(keys) == 25
+    for k in keys:
+        _, iname, tname = k.split("/")
+        got = orr.match_histogram(g[f"img/{iname}"], g[f"tgt/{tname}"])
+        assert got.dtype == np.float32
+        np.testing.assert_array_equal(got, g[k], err_msg=k)
