@@ -365,7 +365,6 @@ __device__ __forceinline__ ProOut pro_next(const BandParams& P) {
 template <int NT>
 __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes, const ProOut out) {
   __shared__ int wsum[NT / 32];
-  __shared__ int sM;
   __shared__ PairHdr shd;
   __shared__ int scm;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -374,13 +373,14 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
   const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), out.batch};
   for (int i = tid; i < (ncell < 4 ? 4 : ncell); i += NT) bins[i] = 0;
   const GenCfg& g = P.g;
+  // seeding density and active count (particles.py:73-83), computed by every
+  // thread (identical values): no serial step before the histogram
+  const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
+  const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
+  double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+  mm = fmin(fmax(mm, 0.0), (double)P.n);
+  const int M = (int)mm;
   if (tid == 0) {
-    // seeding density and active count (particles.py:73-83)
-    const uint4 w = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
-    const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w.x, w.y));
-    double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
-    mm = fmin(fmax(mm, 0.0), (double)P.n);
-    sM = (int)mm;
     shd.ppp = ppp;
     scm = 0;
   }
@@ -389,7 +389,6 @@ __device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_b
 #ifdef PGB_PHASE_TIMING
   const long long c0_ = clock64();
 #endif
-  const int M = sM;
   if (tid == 0) {
     // maximum diameter uniform: max of M uniforms = V^(1/M), on particle J
     // (a serial float64 chain: overlapped with the histogram below)
