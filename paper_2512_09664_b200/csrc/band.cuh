@@ -623,7 +623,8 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
 // ----------------------------------------------------------------------------
 // Per-item parameters (warp 0 computes them for the next item while the
 // block finishes the current one; double-buffered).
-constexpr int kMaxSeg = 256;   // particle segments (cell rows) per enumeration pass
+constexpr int kMaxSeg = 128;   // particle segments (cell rows) per enumeration pass
+constexpr int kStageSlots = 3; // staged item slots (band2 keeps items k, k+1, k+2 live)
 
 struct ItemCfg {
   int pl, r0, r1, c0, c1;
@@ -639,11 +640,11 @@ enum { kItemBand = 0, kItemEnd = 2 };
 struct __align__(16) BandShared {
   int wsum[kBandWarps];
 
-  int nseg[2];                       // segments of the staged pass
-  int rows_left[2];                  // cell rows not yet staged (rare multi-pass items)
-  ItemCfg ic[2];
-  int seg_start[2][kMaxSeg];         // first particle index of each segment
-  int seg_off[2][kMaxSeg + 1];       // exclusive prefix of segment lengths
+  int nseg[kStageSlots];             // segments of the staged pass
+  int rows_left[kStageSlots];        // cell rows not yet staged (rare multi-pass items)
+  ItemCfg ic[kStageSlots];
+  int seg_start[kStageSlots][kMaxSeg];       // first particle index of each segment
+  int seg_off[kStageSlots][kMaxSeg + 1];     // exclusive prefix of segment lengths
 };
 
 __device__ __forceinline__ float lg2_approx(float x) {
@@ -1052,7 +1053,8 @@ __device__ void band_store_vec(const BandParams& P, int* __restrict__ acc, int p
 // quads in shared memory and in the output; each thread strides the quads.
 template <int OUT, bool NOISE>
 __device__ __forceinline__ void band_store_lin(const BandParams& P, int* __restrict__ acc, int pl, int f,
-                                               int r0, int nr, float inv_scale) {
+                                               int r0, int nr, float inv_scale, int t = threadIdx.x,
+                                               int nt = kBandThreads) {
   constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
   const int nq = (nr * P.W) >> 2;
@@ -1060,7 +1062,7 @@ __device__ __forceinline__ void band_store_lin(const BandParams& P, int* __restr
   char* dst = static_cast<char*>(P.out[f]) + ((size_t)pl * (size_t)P.out_pair_elems + pix0) * ESZ;
   int4* ap = reinterpret_cast<int4*>(acc);
 #pragma unroll 4
-  for (int q = threadIdx.x; q < nq; q += kBandThreads) {
+  for (int q = t; q < nq; q += nt) {
     const int4 a = ap[q];
     ap[q] = make_int4(0, 0, 0, 0);
     band_store_quad<OUT, NOISE>(P, a, dst + (size_t)q * 4 * ESZ, pix0 + 4u * q, f, gpair, inv_scale);
@@ -1214,6 +1216,39 @@ __device__ __forceinline__ bool band_store_items_tma(const BandParams& P, int* a
   else if (P.noise_std > 0.f) band_store_tma<kOutF32, true>(P, acc0, acc1, pl, r0, nr, inv_scale);
   else band_store_tma<kOutF32, false>(P, acc0, acc1, pl, r0, nr, inv_scale);
   return true;
+}
+
+
+// Full-width rows [r0, r0 + nr) of both frames, stored (and zeroed) by
+// threads t = 0..nt-1 of some warp group.
+__device__ __forceinline__ void band_store_rows(const BandParams& P, int* acc0, int* acc1, int pl, int r0, int nr,
+                                                float inv_scale, int t, int nt) {
+  if (nr <= 0) return;
+  const bool noise = P.noise_std > 0.f;
+  switch (P.out_mode) {
+    case kOutRaw:
+      band_store_lin<kOutRaw, false>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
+      band_store_lin<kOutRaw, false>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
+      return;
+    case kOutF32:
+      if (noise) {
+        band_store_lin<kOutF32, true>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
+        band_store_lin<kOutF32, true>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
+      } else {
+        band_store_lin<kOutF32, false>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
+        band_store_lin<kOutF32, false>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
+      }
+      return;
+    default:
+      if (noise) {
+        band_store_lin<kOutU16, true>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
+        band_store_lin<kOutU16, true>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
+      } else {
+        band_store_lin<kOutU16, false>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
+        band_store_lin<kOutU16, false>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
+      }
+      return;
+  }
 }
 
 // Range of seeding cells [lo, hi] whose span [k*s, (k+1)*s) meets [a, b).
@@ -1436,10 +1471,9 @@ __device__ __forceinline__ uint4 draw_a(const GenCfg& g, const RngKey& key, int 
 }
 
 // Worker warps: regenerate, advect and splat the particles of one item
-// (variant fixed per item, see ItemCfg::var). Two particles per thread per
-// iteration; the next iteration's particle -> cell loads are issued one
-// iteration ahead.
-template <int PSF, int SEP, int WM>
+// (variant fixed per item, see ItemCfg::var). NTW worker threads; BAR is the
+// workers' own named barrier (rare multi-pass staging).
+template <int PSF, int SEP, int WM, int NTW = kBandThreads, int BAR = 1>
 __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* sh, int buf, long long item,
                                                int* acc0, int* acc1) {
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -1484,13 +1518,13 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
         cA = __ldcg(cof + gA);
         aA = draw_a(P.g, key, gA);
       }
-      for (int qb = 0; qb < N; qb += kBandThreads) {
+      for (int qb = 0; qb < N; qb += NTW) {
         const int qa = qb + tid;
         const int giA = gA, ccA = cA;
         const uint4 a = aA;
-        const bool more = qb + kBandThreads < N;
+        const bool more = qb + NTW < N;
         if (more) {
-          gA = locate(qa + kBandThreads);
+          gA = locate(qa + NTW);
           cA = __ldcg(cof + gA);
         }
         PFrames A;
@@ -1512,10 +1546,10 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
     if (sh->rows_left[buf] <= 0) break;
     // rare: more cell rows than one segment table -> worker warp 0 stages
     // the next rows of this item (named barrier: workers only)
-    asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW));
     next_row += kMaxSeg;
     if (warp == 0) item_stage(P, item, sh, buf, next_row);
-    asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW));
   }
 }
 
@@ -1655,6 +1689,107 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
 #ifdef PGB_PHASE_TIMING
   if (CT && tid == 0) CT[3] = gtime();
 #endif
+}
+
+
+// ----------------------------------------------------------------------------
+// band2: one CTA per SM, warp-specialised, double-buffered accumulators
+// (experimental, PGB_BAND2=1; full-width tiles only). 16 particle warps splat
+// item k into accumulator set k&1 while 2 store warps write item k-1 from the
+// other set and one staging warp prepares item k+1: no CTA-wide barrier
+// between the particle and store phases. Named barriers:
+//   STAGED   stager arrive / workers sync        (item k's config ready)
+//   STARTED  workers arrive / stager sync        (slot of item k-1 reusable)
+//   FULL[s]  workers arrive / storers sync       (set s splatted)
+//   EMPTY[s] storers arrive / workers sync       (set s stored and zeroed)
+// ----------------------------------------------------------------------------
+constexpr int kB2Workers = 512;
+constexpr int kB2Store = 64;
+constexpr int kB2Block = kB2Workers + kB2Store + 32;
+constexpr int kB2BarStaged = 1, kB2BarStarted = 2, kB2BarFull = 3, kB2BarEmpty = 5, kB2BarWork = 7;
+
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int PSF>
+__global__ void __launch_bounds__(kB2Block, 1) band2_kernel(const BandParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
+  int* accbase = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
+  const int set_ints = (2 * P.TH + P.pad_rows) * P.AS + 8;
+  const int tid = threadIdx.x;
+  const int acc_bytes = 2 * set_ints * 4;
+  if (blockIdx.x == gridDim.x - 1 && P.zero_head)
+    for (int e = tid; e < P.zero_head_n; e += kB2Block) P.zero_head[e] = make_int4(0, 0, 0, 0);
+  if (P.inline_prologue) {
+    const int npp = P.inline_pairs ? P.pairs : 0;
+    const int npro = npp + P.field_cnt * kFieldBlocks;
+    for (int w = blockIdx.x; w < npro; w += gridDim.x) {
+      if (w < npp) {
+        pair_prologue<kB2Block>(P, w, accbase, acc_bytes, pro_cur(P));
+      } else {
+        const int fc = w - npp;
+        field_bound_chunk<kB2Block>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
+      }
+      __syncthreads();
+    }
+    if (!P.inline_pairs && tid == 0)
+      for (int pl = blockIdx.x; pl < P.pairs; pl += gridDim.x) write_stats(P, pl, P.hdr[pl]);
+  }
+  for (int e = tid; e < 2 * set_ints / 4; e += kB2Block) reinterpret_cast<int4*>(accbase)[e] = make_int4(0, 0, 0, 0);
+  __syncthreads();
+  constexpr int nSW = kB2Workers + 32, nWS = kB2Workers + kB2Store;
+  if (tid >= kB2Workers + kB2Store) {
+    // staging warp
+    stage_next(P, sh, 0);
+    nbar_arrive(kB2BarStaged, nSW);
+    for (int k = 0;; ++k) {
+      if (sh->ic[k % kStageSlots].kind == kItemEnd) break;
+      nbar_sync(kB2BarStarted, nSW);
+      stage_next(P, sh, (k + 1) % kStageSlots);
+      nbar_arrive(kB2BarStaged, nSW);
+    }
+  } else if (tid < kB2Workers) {
+    for (int k = 0;; ++k) {
+      const int slot = k % kStageSlots, s = k & 1;
+      nbar_sync(kB2BarStaged, nSW);
+      const ItemCfg& ic = sh->ic[slot];
+      if (ic.kind == kItemEnd) {
+        nbar_arrive(kB2BarFull + s, nWS);
+        break;
+      }
+      if (k >= 2) nbar_sync(kB2BarEmpty + s, nWS);
+      nbar_arrive(kB2BarStarted, nSW);
+      int* acc0 = accbase + s * set_ints;
+      int* acc1 = acc0 + P.TH * P.AS;
+      if constexpr (PSF == kPsfErf) {
+        band_particles<PSF, 0, 0, kB2Workers, kB2BarWork>(P, sh, slot, ic.item, acc0, acc1);
+      } else {
+        switch (ic.var) {
+#define PGB_V2(S, W) case 16 * S + W: band_particles<PSF, S, W, kB2Workers, kB2BarWork>(P, sh, slot, ic.item, acc0, acc1); break;
+          PGB_V2(0, 1) PGB_V2(0, 2) PGB_V2(0, 3) PGB_V2(0, 4) PGB_V2(0, 5) PGB_V2(0, 6) PGB_V2(0, 7)
+          PGB_V2(1, 1) PGB_V2(1, 2) PGB_V2(1, 3) PGB_V2(1, 4) PGB_V2(1, 5) PGB_V2(1, 6) PGB_V2(1, 7)
+          PGB_V2(1, 8) PGB_V2(1, 9) PGB_V2(1, 10) PGB_V2(1, 11) PGB_V2(1, 12)
+#undef PGB_V2
+          default: band_particles<PSF, 0, 0, kB2Workers, kB2BarWork>(P, sh, slot, ic.item, acc0, acc1); break;
+        }
+      }
+      nbar_arrive(kB2BarFull + s, nWS);
+    }
+  } else {
+    // store warps
+    const int t = tid - kB2Workers;
+    for (int k = 0;; ++k) {
+      const int slot = k % kStageSlots, s = k & 1;
+      nbar_sync(kB2BarFull + s, nWS);
+      const ItemCfg& ic = sh->ic[slot];
+      if (ic.kind == kItemEnd) break;
+      int* acc0 = accbase + s * set_ints;
+      int* acc1 = acc0 + P.TH * P.AS;
+      band_store_rows(P, acc0, acc1, ic.pl, ic.r0, ic.r1 - ic.r0, 1.0f / (float)(1 << ic.shift), t, kB2Store);
+      nbar_arrive(kB2BarEmpty + s, nWS);
+    }
+  }
 }
 
 // Particle arrays of the generator (one block per pair): exactly the particles

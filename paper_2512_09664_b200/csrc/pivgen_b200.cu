@@ -116,6 +116,7 @@ __global__ void hiding_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, u
 template __global__ void fused_generate_kernel<1, kPsfPoint>(const FusedParams);
 template __global__ void band_kernel<kPsfPoint>(const BandParams);
 template __global__ void band_kernel<kPsfErf>(const BandParams);
+template __global__ void band2_kernel<kPsfPoint>(const BandParams);
 template __global__ void fused_generate_kernel<1, kPsfErf>(const FusedParams);
 
 // ----------------------------------------------------------------------------
@@ -455,12 +456,12 @@ size_t band_acc_budget() {
   return cached;
 }
 
-BandPlan make_band_plan(int H, int W, int halo) {
+BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0) {
   BandPlan p{};
   cell_bits(H, W, p.sy, p.sx);
   // zero rows behind the accumulators for unpredicated splat windows (<= 7 wide)
   p.pad_rows = std::min(kMaxUnpredWM - 1, 2 * halo);
-  const size_t budget_all = band_acc_budget() / 4;        // int32: two frames + padding
+  const size_t budget_all = (acc_budget ? acc_budget : band_acc_budget()) / 4;   // int32: two frames + padding
   auto th_cap = [&](int AS) -> size_t {
     const size_t pad = (size_t)p.pad_rows * AS + 8;
     return budget_all > pad ? (budget_all - pad) / (2 * (size_t)AS) : 0;
@@ -687,10 +688,31 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
               "pair range exceeds the flow window (num_fields * pairs_per_field)");
   if (pairs == 0) return;
   const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
-  const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
+  BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
+  // experimental warp-specialised kernel (PGB_BAND2=1): one CTA per SM, two
+  // accumulator sets; full-width tiles only
+  bool b2 = std::getenv("PGB_BAND2") && std::atoi(std::getenv("PGB_BAND2")) != 0 && cfg->psf == PGB_PSF_POINT;
+  size_t b2_smem = 0;
+  if (b2) {
+    cudaFuncAttributes fa{};
+    PGB_CK(cudaFuncGetAttributes(&fa, (const void*)band2_kernel<kPsfPoint>));
+    const long long per_set = ((long long)kSmemMax - (long long)sizeof(BandShared) - (long long)fa.sharedSizeBytes) / 2;
+    const BandPlan b2p = make_band_plan(cfg->height, cfg->width, halo, (size_t)std::max<long long>(8192, per_set));
+    if (b2p.TW == cfg->width && b2p.AS == cfg->width) {
+      bp = b2p;
+      b2_smem = sizeof(BandShared) + 2 * (((size_t)(2 * bp.TH + bp.pad_rows) * bp.AS + 8) * 4);
+    } else {
+      b2 = false;
+    }
+  }
   BandParams P{};
   band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats, stream,
                 false);
+  if (b2 && P.nx_hdr) {
+    // band2 has no next-batch tail work: keep the prologue cache invalid
+    P.nx_hdr = nullptr;
+    work_for_current().pro_valid = false;
+  }
   P.out_mode = out_mode;
   P.bg_offset = (float)cfg->bg_offset;
   P.noise_std = (float)cfg->noise_std;
@@ -710,7 +732,17 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   }
 #endif
   BandFn fn = cfg->psf == PGB_PSF_ERF ? band_kernel<kPsfErf> : band_kernel<kPsfPoint>;
-  const int ctas = band_resident_ctas(fn, bp.smem);
+  int ctas = 0;
+  if (b2) {
+    int dev = 0, sms = 0;
+    PGB_CK(cudaGetDevice(&dev));
+    PGB_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PGB_CK(cudaFuncSetAttribute((const void*)band2_kernel<kPsfPoint>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kSmemMax));
+    ctas = sms;
+  } else {
+    ctas = band_resident_ctas(fn, bp.smem);
+  }
   // static schedule over `grid` CTAs: whole rounds of (pair, tile) items, then
   // the remaining tiles split into row parts (>= 8 rows) spread over the grid
   const long long F = (long long)pairs * bp.tiles;
@@ -730,7 +762,8 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.split_s = sp;
   P.total_items = R * G + rem * sp;
   const int grid = (int)G;
-  fn<<<grid, kBandBlock, bp.smem, stream>>>(P);
+  if (b2) band2_kernel<kPsfPoint><<<grid, kB2Block, b2_smem, stream>>>(P);
+  else fn<<<grid, kBandBlock, bp.smem, stream>>>(P);
   g_launches.fetch_add(1);
 }
 

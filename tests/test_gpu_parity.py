@@ -393,6 +393,7 @@ def test_spec_oracle_equivalence_random_configs(pg, seed):
     {"PGB_TMA_STORE": "1"},              # finalize in place + cp.async.bulk stores
     {"PGB_TILE": "16,128"},              # other tilings: the integer accumulation and the
     {"PGB_TILE": "32,64"},               # Q17 positions make every pixel tiling-independent
+    {"PGB_BAND2": "1"},                  # warp-specialised double-buffered kernel (full-width tiles)
 ])
 @pytest.mark.parametrize("sep", [False, True])
 def test_schedule_and_store_paths_bit_identical(pg, env, sep, monkeypatch):
