@@ -35,6 +35,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "image pairs/sec at 256x256, B=256 on 1/2/4/8 B200; % of HBM/SFU roofline"
 
+# Algorithmic Gaussian evaluations per pair (both frames): the reference's
+# clipped patch pixels, SURVEY 8(d) table (probe A.7); the SFU-roofline unit.
+EVALS_PER_PAIR = {"c1": 194567, "c2": 194567, "c3": 35215674, "c4": 742881, "c5": 194567}
+# nominal MUFU issue: 16 per clock per SM; no measured figure in
+# MEASURED_PEAKS.json or B200_PROFILING.md
+MUFU_PER_CLK_SM = 16
+
 CONFIGS = {
     # name: (H, W, B per GPU, ppp, d_range, flow, extra)
     "c1": (256, 256, 1, (0.06, 0.06), (0.8, 1.2), "uniform", {}),
@@ -248,6 +255,24 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def sfu_roofline(name, pairs_per_s, clk, world):
+    """Secondary roofline (BASELINE.json metric: '% of HBM/SFU roofline'): the
+    reference's Gaussian evaluations per pair at the achieved rate against the
+    nominal MUFU issue rate at the sampled SM clock."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    summ = clk.summary() if clk is not None else {}
+    mhz = summ.get("sm_mhz") or summ.get("sm_max_mhz") or 1965.0
+    peak = sms * MUFU_PER_CLK_SM * float(mhz) * 1e6 * world / 1e12
+    achieved = pairs_per_s * EVALS_PER_PAIR[name] / 1e12
+    return {"bound": "sfu", "achieved": achieved, "peak": peak, "unit": "Tevals/s", "frac": achieved / peak,
+            "evals_per_pair": EVALS_PER_PAIR[name],
+            "peak_source": f"nominal {MUFU_PER_CLK_SM} MUFU/clk/SM x {sms} SMs x {mhz:.0f} MHz (sampled)",
+            "note": "algorithmic evaluations = the reference's clipped patch pixels (SURVEY 8(d)); "
+                    "the kernel evaluates fewer (tight windows, separable exponentials)"}
+
+
 def run_ours(args):
     import torch
 
@@ -388,6 +413,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "kernel": "pgb::band_kernel<PSF> (one launch per batch; in-kernel prologue)",
                          "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy burst)"},
+            "roofline_sfu": sfu_roofline(name, value, clk, world),
             "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "pgb_generate_batch (C ABI, host buffers: flow H2D + images D2H, pinned)"},
