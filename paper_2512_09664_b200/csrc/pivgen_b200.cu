@@ -231,6 +231,7 @@ struct DevWork {
   // stream (no memset node between back-to-back launches)
   bool head_zero[2] = {false, false};
   int head_next = 0;
+  size_t head_bytes = 0;   // head size the zero flags refer to (it depends on pairs / fields)
   cudaStream_t head_stream = nullptr;
   cudaStream_t pro_stream = nullptr;
   std::array<uint64_t, 16> pro_key{};
@@ -575,9 +576,12 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const size_t slot_bytes = up(hdr_bytes) + up(pre_bytes) + up(cof_bytes);
   void* before = w.band;
   char* base = static_cast<char*>(ensure(w.band, w.band_bytes, 2 * head + 2 * slot_bytes));
-  if (base != before) {
+  if (base != before || head != w.head_bytes) {
+    // new buffer or a different head size (pairs / fields changed): the heads'
+    // zero state and the cached prologue tables are no longer where they were
     w.pro_valid = false;
     w.head_zero[0] = w.head_zero[1] = false;
+    w.head_bytes = head;
   }
   int hsel = 0;
   if (!launch) {
@@ -625,6 +629,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
       k[10] = (uint64_t)pair_base;
       k[11] = (uint64_t)pairs;
       k[12] = (uint64_t)slot_bytes;
+      k[13] = (uint64_t)head;
       return k;
     };
     // opt-in (PGB_PIPELINE=1): measured slower on B200 at c2 -- the next batch's

@@ -478,3 +478,88 @@ def test_sampler_target_histogram_float_and_u16(pg):
             want = orr.match_histogram(a[p].cpu().numpy(), tgt)
             np.testing.assert_array_equal(b[p].cpu().numpy(), want)
             np.testing.assert_array_equal(c[p].cpu().numpy(), orr.quantize_u16(want))
+
+
+def _bench_cfg(pg, name, batch=None):
+    import bench
+
+    H, W, B = bench.CONFIGS[name][:3]
+    pg.register_flow_function("bench_vortex", bench.vortex(H, W))
+    pg.register_flow_function("bench_uniform", bench.uniform)
+    return bench.make_cfg(pg, name, batch or B), H, W, batch or B, bench.vortex(H, W)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_configs_properties(pg, name):
+    """BASELINE configs at full size (size-independent properties):
+    repeatable, the union of two shards equals the whole batch, finalized
+    intensities in [0, 1], and frame statistics consistent with the seeding."""
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    cfg, H, W, B, fn = _bench_cfg(pg, name)
+    flows = pg.from_function(fn, H, W).to_device().unsqueeze(0)
+    ncfg = native_config(cfg)
+
+    def run(base, count, batch=3):
+        img = [torch.empty((count, H, W), dtype=torch.float32, device="cuda") for _ in range(2)]
+        _lib.call("pgb_generate_batch_dev", ncfg, batch, base, count, flows.data_ptr(), 1, B, _lib.OUT_F32,
+                  img[0].data_ptr(), img[1].data_ptr(), None, None, torch.cuda.current_stream().cuda_stream)
+        return img
+
+    a = run(0, B)
+    b = run(0, B)
+    h = B // 2 + 1
+    s1, s2 = run(0, h), run(h, B - h)
+    for f in range(2):
+        assert torch.equal(a[f], b[f]), f"{name}: not repeatable"
+        assert torch.equal(a[f][:h], s1[f]) and torch.equal(a[f][h:], s2[f]), f"{name}: shards differ"
+        assert float(a[f].min()) >= 0.0 and float(a[f].max()) <= 1.0
+    c = run(0, B, batch=4)
+    assert not torch.equal(a[0], c[0]), "batches must differ"
+    if name == "c2":
+        # mean raw intensity per pixel ~ ppp * E[2 pi sigma^2] (I0 = 1, images clipped at 1)
+        sig2 = np.mean((np.linspace(0.8, 1.2, 10001) / 4.0) ** 2)
+        expect = 0.06 * 2 * np.pi * sig2
+        mean = float(a[0].mean())
+        assert 0.8 * expect < mean < 1.05 * expect, (mean, expect)
+
+
+def test_generate_edge_cases(pg):
+    """Empty seeding (M = 0), a single pair, tiny and odd image sizes, very
+    large particles (dynamic windows): the fused generator matches the oracle
+    render of the oracle particles."""
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    cases = [
+        dict(image_height=16, image_width=16, batch_size=2, seeding_density_range=(0.001, 0.001)),   # M = 0
+        dict(image_height=2, image_width=2, batch_size=1, seeding_density_range=(0.5, 0.5)),
+        dict(image_height=7, image_width=13, batch_size=1, seeding_density_range=(0.1, 0.1)),
+        dict(image_height=40, image_width=36, batch_size=2, seeding_density_range=(0.01, 0.01),
+             diameter_range=(6.0, 9.0)),
+        dict(image_height=33, image_width=65, batch_size=3, seeding_density_range=(0.05, 0.08),
+             diameter_range=(0.5, 3.0), rho_range=(-0.4, 0.4)),
+    ]
+    for kw in cases:
+        kw = dict(kw, seed=77, flow_sources=(pg.FlowSource(function="edge"),))
+        cfg = pg.GeneratorConfig(**kw)
+        H, W, B = cfg.image_height, cfg.image_width, cfg.batch_size
+        fld = pg.from_function(lambda x, y: (0.3 + 0.01 * y, -0.2 + 0.02 * x), H, W)
+        flows = fld.to_device().unsqueeze(0)
+        img = [torch.empty((B, H, W), dtype=torch.float32, device="cuda") for _ in range(2)]
+        _lib.call("pgb_generate_batch_dev", native_config(cfg), 2, 0, B, flows.data_ptr(), 1, B, _lib.OUT_RAW,
+                  img[0].data_ptr(), img[1].data_ptr(), None, None, torch.cuda.current_stream().cuda_stream)
+        oc = _oracle_cfg(cfg)
+        for p in range(B):
+            o = og.sample_pair(oc, 2, p, fld.interleaved())
+            for f in (1, 2):
+                want = orr.splat(o[f"pos{f}"], o[f"i0_{f}"], o[f"sx_{f}"], o[f"sy_{f}"], o[f"rho_{f}"],
+                                 o[f"on{f}"], o["side"], H, W)
+                _assert_close(img[f - 1][p].cpu().numpy(), want, what=f"{kw} p{p} f{f}")
+        if kw["seeding_density_range"] == (0.001, 0.001):
+            assert float(img[0].abs().max()) == 0.0 and float(img[1].abs().max()) == 0.0
