@@ -241,16 +241,26 @@ struct DevWork {
 };
 
 std::recursive_mutex g_mu;
-std::map<int, DevWork> g_work;
+// Workspaces are per (device, stream): launches on different streams may run
+// concurrently and must not share tables, control heads or record rings. The
+// overflow counter is per device (shared by that device's workspaces).
+std::map<std::pair<int, cudaStream_t>, DevWork> g_work;
+std::map<int, int*> g_overflow;
 
-DevWork& work_for_current() {
+int* overflow_for(int dev) {
+  int*& o = g_overflow[dev];
+  if (!o) {
+    PGB_CK(cudaMalloc(&o, sizeof(int)));
+    PGB_CK(cudaMemset(o, 0, sizeof(int)));
+  }
+  return o;
+}
+
+DevWork& work_for(cudaStream_t stream) {
   int dev = 0;
   PGB_CK(cudaGetDevice(&dev));
-  DevWork& w = g_work[dev];
-  if (!w.overflow) {
-    PGB_CK(cudaMalloc(&w.overflow, sizeof(int)));
-    PGB_CK(cudaMemset(w.overflow, 0, sizeof(int)));
-  }
+  DevWork& w = g_work[{dev, stream}];
+  if (!w.overflow) w.overflow = overflow_for(dev);
   return w;
 }
 
@@ -305,7 +315,7 @@ void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
   const int ring = std::min(P.pairs, L + std::max(4, L / 4));
   P.lookahead = L;
   P.ring = std::max(ring, std::min(P.pairs, L + 1));
-  DevWork& w = work_for_current();
+  DevWork& w = work_for(stream);
   const size_t segs = (size_t)P.ring * P.nframes * pl.tiles * pl.chunks;
   const size_t recs_bytes = segs * pl.cap * sizeof(Rec);
   const size_t slots_bytes = (size_t)P.ring * sizeof(SlotHdr);
@@ -569,7 +579,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const size_t pre_bytes = (size_t)pairs * pre_stride(ncell) * sizeof(int);
   const size_t cof_bytes = (size_t)pairs * cof_stride(cfg->n_capacity) * sizeof(unsigned short);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
-  DevWork& w = work_for_current();
+  DevWork& w = work_for(stream);
   // [ticket | field bounds | ready flags] are zeroed per launch, then two
   // table slots of [headers | prefixes | particle -> cell arrays]
   const size_t head = up(256 + up(fb_bytes) + up(flag_bytes));
@@ -716,7 +726,7 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   if (b2 && P.nx_hdr) {
     // band2 has no next-batch tail work: keep the prologue cache invalid
     P.nx_hdr = nullptr;
-    work_for_current().pro_valid = false;
+    work_for(stream).pro_valid = false;
   }
   P.out_mode = out_mode;
   P.bg_offset = (float)cfg->bg_offset;
@@ -831,7 +841,7 @@ int pgb_splat_accumulate_dev(const double* pos, const float* i0, const float* si
     P.nframes = 1;
     P.inj[0] = InjFrame{pos, i0, sigma_x, sigma_y, rho, mask};
     int* side_dev = nullptr;
-    DevWork& w = work_for_current();
+    DevWork& w = work_for((cudaStream_t)stream);
     // side lives in the staging buffer head (4 bytes)
     ensure(w.stage, w.stage_bytes, 256);
     side_dev = static_cast<int*>(w.stage);
@@ -902,7 +912,7 @@ int pgb_render_pairs_dev(const pgb_particles* frame1, const pgb_particles* frame
       PGB_REQUIRE(side_per_pair[i] >= 1, "side must be >= 1");
       smax = std::max(smax, side_per_pair[i]);
     }
-    DevWork& w = work_for_current();
+    DevWork& w = work_for((cudaStream_t)stream);
     ensure(w.stage, w.stage_bytes, (size_t)pairs * sizeof(int) + 256);
     int* side_dev = static_cast<int*>(w.stage);
     PGB_CK(cudaMemcpyAsync(side_dev, side_per_pair, (size_t)pairs * sizeof(int),
@@ -1018,7 +1028,7 @@ int pgb_generate_batch(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
     const size_t img_bytes = (size_t)pairs * hw * px_bytes;
     const size_t flow_bytes = (size_t)num_fields * hw * 2 * sizeof(float);
     const size_t st_bytes = (size_t)pairs * (8 + 4 + 4 + 4);
-    DevWork& w = work_for_current();
+    DevWork& w = work_for(nullptr);
     const size_t need = 2 * img_bytes + flow_bytes + st_bytes + 1024;
     char* b = static_cast<char*>(ensure(w.stage, w.stage_bytes, need));
     float* d_flow = reinterpret_cast<float*>(b);
@@ -1108,16 +1118,18 @@ int pgb_apply_hiding_dev(int64_t n, uint64_t seed, uint64_t batch, int64_t gpair
 int pgb_overflow_count(void) {
   int v = -1;
   guarded([&] {
-    DevWork& w = work_for_current();
-    PGB_CK(cudaMemcpy(&v, w.overflow, sizeof(int), cudaMemcpyDeviceToHost));
+    int dev = 0;
+    PGB_CK(cudaGetDevice(&dev));
+    PGB_CK(cudaMemcpy(&v, overflow_for(dev), sizeof(int), cudaMemcpyDeviceToHost));
   });
   return v;
 }
 
 int pgb_overflow_reset(void) {
   return guarded([&] {
-    DevWork& w = work_for_current();
-    PGB_CK(cudaMemset(w.overflow, 0, sizeof(int)));
+    int dev = 0;
+    PGB_CK(cudaGetDevice(&dev));
+    PGB_CK(cudaMemset(overflow_for(dev), 0, sizeof(int)));
   });
 }
 

@@ -563,3 +563,38 @@ def test_generate_edge_cases(pg):
                 _assert_close(img[f - 1][p].cpu().numpy(), want, what=f"{kw} p{p} f{f}")
         if kw["seeding_density_range"] == (0.001, 0.001):
             assert float(img[0].abs().max()) == 0.0 and float(img[1].abs().max()) == 0.0
+
+
+def test_concurrent_streams_have_private_workspaces(pg):
+    """Launches on two streams may overlap on the device: each (device, stream)
+    has its own tables and control heads, so both results equal serial runs."""
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    H, W, B = 128, 128, 40
+    cfg = _gen_cfg(pg, image_height=H, image_width=W, batch_size=B)
+    flows = pg.from_function(vortex_fn(H, W), H, W).to_device().unsqueeze(0)
+    ncfg = native_config(cfg)
+
+    def launch(batch, base, count, stream):
+        img = [torch.empty((count, H, W), dtype=torch.float32, device="cuda") for _ in range(2)]
+        _lib.call("pgb_generate_batch_dev", ncfg, batch, base, count, flows.data_ptr(), 1, B, _lib.OUT_F32,
+                  img[0].data_ptr(), img[1].data_ptr(), None, None, stream.cuda_stream)
+        return img
+
+    main = torch.cuda.current_stream()
+    want = [launch(b, 0, B, main) for b in (5, 6, 7)]
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    got = []
+    for b, s in ((5, s1), (6, s2), (7, s1)):
+        got.append(launch(b, 0, B, s))
+    part = launch(6, 10, 17, s2)   # different pair count on the same stream
+    torch.cuda.synchronize()
+    for w, g in zip(want, got):
+        for f in range(2):
+            assert torch.equal(w[f], g[f])
+    for f in range(2):
+        assert torch.equal(part[f], want[1][f][10:27])
