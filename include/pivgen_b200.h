@@ -24,6 +24,9 @@
  *   pgb_finalize_dev          <- raster.py:154-161 finalize()
  *   pgb_quantize_u16_dev      <- export.py:19-20 quantize_u16()
  *   pgb_match_histogram_dev   <- raster.py:164-187 match_histogram()
+ *   pgb_sample_particles_splitmix_dev <- particles.py:61-147 with rng.py:33-106
+ *                                 (reference RNG mode)
+ *   pgb_finalize_splitmix_dev <- raster.py:154-161 finalize() with rng.py noise
  *   pgb_generate_batch_dev    <- pipeline.py:278-329 Sampler._render_batch()
  *   pgb_generate_batch        <- same, host buffers (end-to-end path)
  *   pgb_sample_particles_dev  <- particles.py:61-147 sample_particles /
@@ -152,6 +155,7 @@ int pgb_quantize_u16_dev(const float* img, int64_t count, uint16_t* out, void* s
 int pgb_match_histogram_dev(const float* img, float* out, int64_t images, int64_t pixels,
                             const double* target_cdf, void* stream);
 
+
 /* Full generation of one batch shard: global pairs [pair_base, pair_base + pairs)
  * of batch `batch`. flows: device float32 [num_fields][height][width][2];
  * pair g (global, within the batch) uses field g / pairs_per_field.
@@ -181,6 +185,22 @@ int pgb_sample_particles_dev(const pgb_config* cfg, uint64_t batch, int64_t pair
                              const float* flows, int num_fields, int pairs_per_field,
                              const pgb_particle_out* out, const pgb_pair_stats* stats,
                              void* stream);
+
+/* Reference-RNG mode: the reference's splitmix64 streams (rng.py:33-106) and
+ * sample_particles / perturb_frame2 / apply_hiding / advect (particles.py:
+ * 61-147) for global pairs [pair_base, pair_base + pairs) of `batch`. Fills
+ * the arrays of `out` that are non-NULL ((pairs, n[, 2])); stats->active_count,
+ * stats->side and stats->d_max are required. Uniform-derived values are
+ * bit-identical to the reference; normals use normcdfinv for scipy's ndtri. */
+int pgb_sample_particles_splitmix_dev(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
+                                      const float* flows, int num_fields, int pairs_per_field,
+                                      const pgb_particle_out* out, const pgb_pair_stats* stats, void* stream);
+
+/* finalize() with the reference's noise stream (NOISE, lane = frame) for
+ * `images` raw float32 images of `pixels` each (pairs pair_base + i). */
+int pgb_finalize_splitmix_dev(const float* raw, float* out, int64_t pixels, int images, double bg_offset,
+                              double noise_std, uint64_t seed, uint64_t batch, int64_t pair_base, int frame,
+                              void* stream);
 
 /* perturb_frame2 (particles.py:104-126) on caller arrays; same Philox draws as the
  * generator (stream "perturb", particle index). Output arrays may alias nothing. */

@@ -84,6 +84,9 @@ SIGNATURES = {
     "pgb_finalize_dev": (_I, [_P, _I, _I, _I, _D, _D, _U64, _U64, _I64, _I, _I, _P, _P]),
     "pgb_quantize_u16_dev": (_I, [_P, _I64, _P, _P]),
     "pgb_match_histogram_dev": (_I, [_P, _P, _I64, _I64, _P, _P]),
+    "pgb_sample_particles_splitmix_dev": (_I, [C.POINTER(PgbConfig), _U64, _I64, _I, _P, _I, _I,
+                                               C.POINTER(PgbParticleOut), C.POINTER(PgbPairStats), _P]),
+    "pgb_finalize_splitmix_dev": (_I, [_P, _P, _I64, _I, _D, _D, _U64, _U64, _I64, _I, _P]),
     "pgb_generate_batch_dev": (_I, [C.POINTER(PgbConfig), _U64, _I64, _I, _P, _I, _I, _I, _P, _P,
                                     C.POINTER(PgbPairStats), _P, _P]),
     "pgb_generate_batch": (_I, [C.POINTER(PgbConfig), _U64, _I64, _I, _P, _I, _I, _I, _P, _P,

@@ -13,6 +13,9 @@ Differences, all opt-in so a reference document means reference behaviour:
     (pixel-area integration).
   * ``output_dtype``: ``float32`` (reference) or ``uint16`` (fused
     ``quantize_u16``, export.py:19-20, bit-exact).
+  * ``rng``: ``philox`` (the B200 generator's Philox4x32-10 streams) or
+    ``splitmix64`` (the reference's own rng.py streams: particle arrays
+    bit-identical to the reference, images within 1e-5; point PSF only).
   * ``laser_sheet``: out-of-plane position and the Remark-1 intensity profile
     I0(z) = q exp(-(1/sqrt(2 pi)) |2 z^2 / dZ0^2|^s).
 
@@ -34,6 +37,7 @@ OUTPUT_FORMATS = ("png16", "raw_f32")
 SOURCE_FORMATS = ("flo", "npy_xyuv", "hdf5", "function")
 PSF_KINDS = ("point", "erf")
 OUTPUT_DTYPES = ("float32", "uint16")
+RNG_KINDS = ("philox", "splitmix64")   # splitmix64: the reference's rng.py streams
 
 _SUFFIX_FORMAT = (
     (".flo", "flo"),
@@ -149,6 +153,7 @@ class GeneratorConfig:
     # --- B200 extensions ---
     psf: str = "point"
     output_dtype: str = "float32"
+    rng: str = "philox"
     laser_sheet: LaserSheetConfig | None = None
 
     def __post_init__(self) -> None:
@@ -307,6 +312,10 @@ def validate_config(cfg: GeneratorConfig) -> None:
         _fail("psf", f"must be one of {PSF_KINDS}, got {cfg.psf!r}")
     if cfg.output_dtype not in OUTPUT_DTYPES:
         _fail("output_dtype", f"must be one of {OUTPUT_DTYPES}, got {cfg.output_dtype!r}")
+    if cfg.rng not in RNG_KINDS:
+        _fail("rng", f"must be one of {RNG_KINDS}, got {cfg.rng!r}")
+    if cfg.rng == "splitmix64" and (cfg.psf != "point" or cfg.laser_sheet is not None):
+        _fail("rng", "splitmix64 (reference RNG) mode renders the reference model: point PSF, no laser sheet")
     if cfg.laser_sheet is not None:
         ls = cfg.laser_sheet
         if not isinstance(ls, LaserSheetConfig):
@@ -499,6 +508,7 @@ _SCHEMA: tuple[_Field, ...] = (
     _Field("patch_multiplier", _p_float),
     _Field("psf", _p_str),
     _Field("output_dtype", _p_str),
+    _Field("rng", _p_str),
     _Field("target_histogram", _p_histogram, _r_list, optional=True),
     _Field("flow_sources", _p_sources, _r_sources, optional=True),
     _Field("laser_sheet", _p_laser, _r_laser, optional=True),

@@ -22,6 +22,7 @@
 #include "fused.cuh"
 #include "band.cuh"
 #include "histmatch.cuh"
+#include "refrng.cuh"
 
 namespace pgb {
 
@@ -1002,6 +1003,54 @@ int pgb_match_histogram_dev(const float* img, float* out, int64_t images, int64_
     if (images == 0 || pixels == 0) return;
     PGB_REQUIRE(img && out && target_cdf, "null pointer");
     hist_match_kernel<<<(unsigned)images, kHistThreads, 0, (cudaStream_t)stream>>>(img, out, pixels, target_cdf);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_sample_particles_splitmix_dev(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
+                                      const float* flows, int num_fields, int pairs_per_field,
+                                      const pgb_particle_out* out, const pgb_pair_stats* stats, void* stream) {
+  return guarded([&] {
+    validate_cfg(cfg);
+    PGB_REQUIRE(pairs >= 0 && out != nullptr && stats != nullptr, "bad arguments");
+    PGB_REQUIRE(stats->active_count && stats->side && stats->d_max, "stats arrays required");
+    PGB_REQUIRE(flows != nullptr && num_fields >= 1 && pairs_per_field >= 1, "flows required");
+    PGB_REQUIRE((int64_t)(pair_base + pairs) <= (int64_t)num_fields * pairs_per_field,
+                "pair range exceeds the flow window");
+    if (pairs == 0) return;
+    SmParams S{};
+    S.H = cfg->height; S.W = cfg->width; S.n = cfg->n_capacity; S.pairs = pairs;
+    S.seed = cfg->seed; S.batch = batch; S.pair_base = pair_base;
+    S.ppp_lo = cfg->ppp_lo; S.ppp_hi = cfg->ppp_hi; S.d_lo = cfg->d_lo; S.d_hi = cfg->d_hi;
+    S.i0_lo = cfg->i0_lo; S.i0_hi = cfg->i0_hi; S.rho_lo = cfg->rho_lo; S.rho_hi = cfg->rho_hi;
+    S.ratio = cfg->sigma_ratio; S.mult = cfg->patch_multiplier;
+    S.s_std = cfg->f2_sigma_std; S.i_std = cfg->f2_i0_std; S.r_std = cfg->f2_rho_std;
+    S.hide_p = cfg->hide_probability;
+    S.flows = reinterpret_cast<const float2*>(flows);
+    S.field_elems = (long long)cfg->height * cfg->width;
+    S.pairs_per_field = pairs_per_field;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned* dbits = reinterpret_cast<unsigned*>(stats->d_max);
+    PGB_CK(cudaMemsetAsync(dbits, 0, (size_t)pairs * sizeof(unsigned), st));
+    dim3 grid((unsigned)((S.n + 255) / 256), (unsigned)pairs);
+    sm_particles_kernel<<<grid, 256, 0, st>>>(S, *out, stats->seeding_density, stats->active_count, dbits);
+    sm_side_kernel<<<(pairs + 127) / 128, 128, 0, st>>>(S, stats->active_count, dbits, stats->side);
+    g_launches.fetch_add(2);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_finalize_splitmix_dev(const float* raw, float* out, int64_t pixels, int images, double bg_offset,
+                              double noise_std, uint64_t seed, uint64_t batch, int64_t pair_base, int frame,
+                              void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(pixels >= 0 && images >= 0, "bad sizes");
+    if (pixels == 0 || images == 0) return;
+    PGB_REQUIRE(raw && out, "null pointer");
+    const unsigned gx = (unsigned)std::min<long long>((pixels + 255) / 256, 1024);
+    sm_finalize_kernel<<<dim3(gx, (unsigned)images), 256, 0, (cudaStream_t)stream>>>(
+        raw, out, pixels, images, bg_offset, noise_std, seed, batch, pair_base, frame);
     g_launches.fetch_add(1);
     PGB_CK(cudaGetLastError());
   });

@@ -164,6 +164,44 @@ def generate_particle_arrays(cfg: GeneratorConfig, batch: int, pairs: range,
     return out
 
 
+def generate_particle_arrays_splitmix(cfg: GeneratorConfig, batch: int, pairs: range,
+                                      flows: torch.Tensor, pairs_per_field: int | None = None,
+                                      device=None) -> dict:
+    """Reference-RNG mode (rng.py:33-106 streams): the reference's
+    sample_particles / perturb_frame2 / apply_hiding / advect arrays for
+    global pairs ``pairs`` of ``batch`` (device tensors, shape (P, N[, 2])),
+    plus per-pair ``seeding_density``, ``active_count``, ``side``, ``d_max``."""
+    dev = cuda_device(device)
+    n = cfg.particle_capacity()
+    P = len(pairs)
+    base = pairs.start if P else 0
+    ppf = pairs_per_field or cfg.pairs_per_field
+    f64 = dict(dtype=torch.float64, device=dev)
+    f32 = dict(dtype=torch.float32, device=dev)
+    u8 = dict(dtype=torch.uint8, device=dev)
+    out = {
+        "pos1": torch.empty((P, n, 2), **f64), "pos2": torch.empty((P, n, 2), **f64),
+        "i0_1": torch.empty((P, n), **f32), "sx_1": torch.empty((P, n), **f32),
+        "sy_1": torch.empty((P, n), **f32), "rho_1": torch.empty((P, n), **f32),
+        "i0_2": torch.empty((P, n), **f32), "sx_2": torch.empty((P, n), **f32),
+        "sy_2": torch.empty((P, n), **f32), "rho_2": torch.empty((P, n), **f32),
+        "diameter": torch.empty((P, n), **f32), "z1": torch.empty((P, n), **f32),
+        "active": torch.empty((P, n), **u8), "visible1": torch.empty((P, n), **u8),
+        "visible2": torch.empty((P, n), **u8),
+    }
+    st = {"seeding_density": torch.empty(P, **f64),
+          "active_count": torch.empty(P, dtype=torch.int32, device=dev),
+          "side": torch.empty(P, dtype=torch.int32, device=dev),
+          "d_max": torch.empty(P, **f32)}
+    po = _lib.PgbParticleOut(**{k: v.data_ptr() for k, v in out.items()})
+    ps = _lib.PgbPairStats(**{k: v.data_ptr() for k, v in st.items()})
+    if P:
+        _lib.call("pgb_sample_particles_splitmix_dev", native_config(cfg), batch, base, P, flows.data_ptr(),
+                  flows.shape[0], ppf, po, ps, stream_ptr(dev))
+    out.update(st)
+    return out
+
+
 def sample_particles(key: RngKey, cfg: GeneratorConfig) -> tuple[ParticleSet, PairParams]:
     """Frame-1 positions/appearances (particles.py:61-101) for one pair."""
     arr = generate_particle_arrays(cfg, key.batch, range(key.pair, key.pair + 1))
