@@ -125,7 +125,10 @@ def load(require_symbols: bool = True):
             handle = C.CDLL(path)
         except OSError as exc:  # pragma: no cover - depends on the driver
             raise BackendUnavailable(f"cannot load {path}: {exc}") from exc
+        lenient = os.environ.get("PGB_LIB_LENIENT") == "1"   # A/B of older builds (debug)
         for name, (res, args) in SIGNATURES.items():
+            if lenient and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

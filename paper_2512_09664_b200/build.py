@@ -43,6 +43,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > mtime for d in deps if os.path.exists(d))
 
 
+def check_band_kernel_frame(ptxas_log: str, limit: int = 256) -> None:
+    """Fail the build when a band kernel gets a stack frame: that means the
+    kernel parameters were copied to local memory (a device function taking
+    `const BandParams&` was not inlined) and every parameter access goes
+    through local memory (measured: 64 -> 116 us per batch at c2)."""
+    import re
+
+    cur = None
+    for line in ptxas_log.splitlines():
+        m = re.search(r"Function properties for (_ZN3pgb1\d?band2?_kernel\S*)", line)
+        if m:
+            cur = m.group(1)
+            continue
+        m = re.search(r"(\d+) bytes stack frame", line)
+        if cur and m:
+            if int(m.group(1)) > limit:
+                raise RuntimeError(f"{cur}: {m.group(1)}-byte stack frame (kernel parameters spilled to "
+                                   "local memory?); make the callee __forceinline__")
+            cur = None
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB_PATH
@@ -63,6 +84,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
     if verbose:
         sys.stdout.write(proc.stdout + proc.stderr)
+    check_band_kernel_frame(proc.stdout + proc.stderr)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

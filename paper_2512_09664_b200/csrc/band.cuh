@@ -243,7 +243,7 @@ __device__ __forceinline__ void seed_particle(const BandParams& P, const PairHdr
 // out[count] = total. NT threads, `wsum` = NT/32 ints of shared scratch.
 // ----------------------------------------------------------------------------
 template <int NT>
-__device__ int block_scan(const int* in, int* out, int count, int* wsum) {
+__device__ __forceinline__ int block_scan(const int* in, int* out, int count, int* wsum) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int per = (count + NT - 1) / NT;
@@ -299,7 +299,7 @@ __device__ __forceinline__ int ld_acquire_b(const int* p) {
 // max |v| by atomicMax on the bits of non-negative floats (non-finite values
 // -> unbounded); the chunk counter fb_done[f] releases the bound.
 template <int NT>
-__device__ void field_bound_chunk(const BandParams& P, int f, int part) {
+__device__ __forceinline__ void field_bound_chunk(const BandParams& P, int f, int part) {
   const int tid = threadIdx.x, lane = tid & 31;
   const float2* fl = P.flows + (size_t)f * P.field_elems;
   float mu = 0.f, mv = 0.f;
@@ -363,7 +363,7 @@ __device__ __forceinline__ ProOut pro_next(const BandParams& P) {
 }
 
 template <int NT>
-__device__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes, const ProOut out) {
+__device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes, const ProOut out) {
   __shared__ int wsum[NT / 32];
   __shared__ PairHdr shd;
   __shared__ int scm;
@@ -1001,7 +1001,7 @@ __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, cha
 // quads with incremental row/column/pointer updates (no per-quad division or
 // 64-bit index arithmetic).
 template <int OUT, bool NOISE>
-__device__ void band_store_vec(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
+__device__ __forceinline__ void band_store_vec(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
                                int nr, int c0, int nc, float inv_scale) {
   constexpr int ESZ = OUT == kOutU16 ? 2 : 4;
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
@@ -1069,7 +1069,7 @@ __device__ __forceinline__ void band_store_lin(const BandParams& P, int* __restr
   }
 }
 
-__device__ void band_store_scalar(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
+__device__ __forceinline__ void band_store_scalar(const BandParams& P, int* __restrict__ acc, int pl, int f, int r0,
                                   int nr, int c0, int nc, float inv_scale) {
   const uint32_t gpair = (uint32_t)(P.pair_base + pl);
   const size_t pair_off = (size_t)pl * (size_t)P.out_pair_elems;
@@ -1099,7 +1099,7 @@ __device__ void band_store_scalar(const BandParams& P, int* __restrict__ acc, in
   }
 }
 
-__device__ void band_store(const BandParams& P, int* acc, int pl, int f, int r0, int nr, int c0, int nc,
+__device__ __forceinline__ void band_store(const BandParams& P, int* acc, int pl, int f, int r0, int nr, int c0, int nc,
                            float inv_scale) {
   const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
   const bool noise = P.noise_std > 0.f;
@@ -1182,7 +1182,7 @@ __device__ __forceinline__ void band_finalize_inplace(const BandParams& P, int* 
 // waits until they have read shared memory, then the accumulators are zeroed.
 // Workers only (named barrier 1).
 template <int OUT, bool NOISE>
-__device__ void band_store_tma(const BandParams& P, int* acc0, int* acc1, int pl, int r0, int nr,
+__device__ __forceinline__ void band_store_tma(const BandParams& P, int* acc0, int* acc1, int pl, int r0, int nr,
                                float inv_scale) {
   band_finalize_inplace<OUT, NOISE>(P, acc0, pl, 0, r0, nr, inv_scale);
   band_finalize_inplace<OUT, NOISE>(P, acc1, pl, 1, r0, nr, inv_scale);
