@@ -1,0 +1,26 @@
+"""Sampler throughput (batches back to back, device-side images) for the
+default Philox generator and the reference-RNG mode, C2 shape."""
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2512_09664_b200 as pg  # noqa: E402
+
+H, W, B = 256, 256, 256
+pg.register_flow_function("bench_vortex", bench.vortex(H, W))
+for rng, R in (("philox", 1), ("splitmix64", 1), ("philox", 8), ("splitmix64", 8)):
+    cfg = pg.with_updates(bench.make_cfg(pg, "c2", B), rng=rng, batches_per_flow_field=R)
+    with pg.make_sampler(cfg, max_batches=25) as s:
+        for _ in range(5):
+            next(s)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(20):
+            b = next(s)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / 20
+    print(f"{rng} R={R}: {B / dt / 1e6:.3f} M pairs/s ({dt * 1e6:.0f} us/batch, Sampler wall clock)")
