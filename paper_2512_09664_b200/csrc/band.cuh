@@ -1328,8 +1328,11 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   ic.wt = max(1, wt);
   // uncorrelated particles (rho == 0 in both frames): separable splat
   ic.sep = (g.rho_lo == 0.f && g.rho_span == 0.f && !(g.f2_rho_std > 0.f)) ? 1 : 0;
-  const int wmax = ic.sep ? kMaxUnpredWM : 7;
-  const int wm = (P.psf == kPsfPoint && ic.wt <= wmax && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
+  // unpredicated windows for uncorrelated particles only: the correlated
+  // variant (splat_point_u) showed tiling-dependent 1-ulp differences in the
+  // stress test (scripts/stress.py); correlated particles use the dynamic loops
+  const int wm = (P.psf == kPsfPoint && ic.sep && ic.wt <= kMaxUnpredWM && ic.wt - 1 <= P.pad_rows &&
+                  !(P.ablate & 64)) ? ic.wt : 0;
   ic.var = (P.psf == kPsfPoint ? 16 * ic.sep : 0) + wm;
 }
 
@@ -1636,7 +1639,6 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
     } else {
       switch (ic.var) {
 #define PGB_V(S, W) case 16 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
-        PGB_V(0, 1) PGB_V(0, 2) PGB_V(0, 3) PGB_V(0, 4) PGB_V(0, 5) PGB_V(0, 6) PGB_V(0, 7)
         PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6) PGB_V(1, 7)
         PGB_V(1, 8) PGB_V(1, 9) PGB_V(1, 10) PGB_V(1, 11) PGB_V(1, 12)
 #undef PGB_V
@@ -1767,7 +1769,6 @@ __global__ void __launch_bounds__(kB2Block, 1) band2_kernel(const BandParams P) 
       } else {
         switch (ic.var) {
 #define PGB_V2(S, W) case 16 * S + W: band_particles<PSF, S, W, kB2Workers, kB2BarWork>(P, sh, slot, ic.item, acc0, acc1); break;
-          PGB_V2(0, 1) PGB_V2(0, 2) PGB_V2(0, 3) PGB_V2(0, 4) PGB_V2(0, 5) PGB_V2(0, 6) PGB_V2(0, 7)
           PGB_V2(1, 1) PGB_V2(1, 2) PGB_V2(1, 3) PGB_V2(1, 4) PGB_V2(1, 5) PGB_V2(1, 6) PGB_V2(1, 7)
           PGB_V2(1, 8) PGB_V2(1, 9) PGB_V2(1, 10) PGB_V2(1, 11) PGB_V2(1, 12)
 #undef PGB_V2
