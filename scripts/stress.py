@@ -15,12 +15,20 @@ from paper_2512_09664_b200 import _lib  # noqa: E402
 from paper_2512_09664_b200.particles import native_config  # noqa: E402
 from _helpers import vortex_fn  # noqa: E402
 
-limit = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
-rng = np.random.default_rng(0)
-streams = [torch.cuda.Stream() for _ in range(3)]
-t0 = time.time()
-n = 0
-while time.time() - t0 < limit:
+
+
+def run_stress(limit: float, seed: int = 0) -> int:
+    """Random configs for `limit` seconds; returns the number checked, raises on a mismatch."""
+    rng = np.random.default_rng(seed)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    t0 = time.time()
+    n = 0
+    while time.time() - t0 < limit:
+        n += _one(rng, streams)
+    return n
+
+
+def _one(rng, streams) -> int:
     H = int(rng.choice([64, 96, 128, 200, 256]))
     W = int(rng.choice([64, 128, 160, 256]))
     B = int(rng.integers(1, 40))
@@ -56,7 +64,10 @@ while time.time() - t0 < limit:
     for b0, img in parts:
         for f in range(2):
             if not torch.equal(img[f], want[f][b0:b0 + img[f].shape[0]]):
-                print("MISMATCH", kw, batch, b0, f)
-                sys.exit(1)
-    n += 1
-print(f"stress ok: {n} configs in {time.time() - t0:.0f} s")
+                raise AssertionError(f"MISMATCH {kw} batch {batch} base {b0} frame {f}")
+    return 1
+if __name__ == "__main__":
+    limit = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
+    t0 = time.time()
+    n = run_stress(limit)
+    print(f"stress ok: {n} configs in {time.time() - t0:.0f} s")
