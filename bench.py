@@ -2,6 +2,11 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
 
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under `python -m torch.distributed.run --nproc-per-node N` (one rank per GPU,
+127.0.0.1 rendezvous, NCCL_DEBUG=INFO); `--dry-run` exercises the launcher and
+the rank plumbing on CPU (gloo, no GPU work).
+
 One step = one batch of synthetic PIV image pairs generated on the GPU by the
 fused kernel (Philox seeding, bilinear advection, distributed binning, splat,
 finalize) -- workload C2 (256x256, B=256 per GPU, Lamb-Oseen vortex flow,
@@ -37,9 +42,10 @@ METRIC = "image pairs/sec at 256x256, B=256 on 1/2/4/8 B200; % of HBM/SFU roofli
 
 # Algorithmic Gaussian evaluations per pair (both frames): the reference's
 # clipped patch pixels, SURVEY 8(d) table (probe A.7); the SFU-roofline unit.
-EVALS_PER_PAIR = {"c1": 194567, "c2": 194567, "c3": 35215674, "c4": 742881, "c5": 194567}
-# nominal MUFU issue: 16 per clock per SM; no measured figure in
-# MEASURED_PEAKS.json or B200_PROFILING.md
+# c6 (512^2 plain) has c4's particle law without hiding: ~742,881 as well.
+EVALS_PER_PAIR = {"c1": 194567, "c2": 194567, "c3": 35215674, "c4": 742881, "c5": 194567, "c6": 742881}
+# nominal MUFU issue, used only when profiles/peaks.json (the
+# measured ex2 rate, scripts/measure_peaks.py) is absent
 MUFU_PER_CLK_SM = 16
 
 CONFIGS = {
@@ -51,6 +57,8 @@ CONFIGS = {
            dict(noise=(0.05, 0.02), hide_probability=0.05,
                 laser_sheet=dict(thickness=1.0, shape=2.0, efficiency=1.0, out_of_plane=0.1))),
     "c5": (256, 256, 8192, (0.06, 0.06), (0.8, 1.2), "vortex", {}),
+    # the paper's own benchmark size (512^2, B=256, defaults)
+    "c6": (512, 512, 256, (0.06, 0.06), (0.8, 1.2), "vortex", {}),
 }
 
 
@@ -76,6 +84,28 @@ def load_peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def load_probe_peaks():
+    """profiles/peaks.json (scripts/measure_peaks.py on a B200): ex2 rate, PCIe."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -199,10 +229,8 @@ def ref_cfg(name, batch, threads):
     return pv, pv.GeneratorConfig(**kw)
 
 
-def cpu_baseline(name: str, budget_s: float = 15.0):
-    """Reference CPU path (oracle/_ref, native Cython kernel) on the host cores."""
-    threads = os.cpu_count() or 1
-    pv, cfg = ref_cfg(name, min(CONFIGS[name][2], 256), threads)
+def _ref_rate(name: str, threads: int, budget_s: float, batch: int | None = None):
+    pv, cfg = ref_cfg(name, batch or min(CONFIGS[name][2], 256), threads)
     from pivgen.pipeline import Sampler
 
     pairs = 0
@@ -214,10 +242,22 @@ def cpu_baseline(name: str, budget_s: float = 15.0):
             s.next_batch()
             t_total += time.perf_counter() - t0
             pairs += cfg.batch_size
-    return {"value": pairs / t_total, "unit": "pairs/s", "cores": threads, "kind": "reference",
+    return pv, cfg, pairs, pairs / t_total
+
+
+def cpu_baseline(name: str, budget_s: float = 15.0):
+    """Reference CPU path (oracle/_ref, native Cython kernel) on the host cores:
+    all threads (the reported value) plus a single-thread figure."""
+    threads = os.cpu_count() or 1
+    pv, cfg, pairs, rate = _ref_rate(name, threads, budget_s)
+    _, cfg1, pairs1, rate1 = _ref_rate(name, 1, budget_s / 2, batch=min(cfg.batch_size, 64))
+    return {"value": rate, "unit": "pairs/s", "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(),
             "sample": f"{pairs} pairs of {name} ({cfg.image_height}x{cfg.image_width}, "
                       f"B={cfg.batch_size}) via pivgen Sampler.next_batch, threads={threads}, "
-                      f"backend={pv.active_backend()}"}
+                      f"backend={pv.active_backend()}",
+            "threads_1": {"value": rate1, "unit": "pairs/s",
+                          "sample": f"{pairs1} pairs, B={cfg1.batch_size}, threads=1"}}
 
 
 def run_reference(args):
@@ -242,6 +282,7 @@ def run_reference(args):
     H, W = cfg.image_height, cfg.image_width
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s",
+        "cpu_model": cpu_model(),
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64/f32 (CPU)", "data": "synthetic (Lamb-Oseen vortex flow)",
@@ -258,17 +299,27 @@ def run_reference(args):
 def sfu_roofline(name, pairs_per_s, clk, world):
     """Secondary roofline (BASELINE.json metric: '% of HBM/SFU roofline'): the
     reference's Gaussian evaluations per pair at the achieved rate against the
-    nominal MUFU issue rate at the sampled SM clock."""
+    MUFU.EX2 issue rate measured by scripts/measure_peaks.py (per clock per
+    SM, scaled to the SM clock sampled during this run); the nominal
+    16/clk/SM only when no measurement exists."""
     import torch
 
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     summ = clk.summary() if clk is not None else {}
     mhz = summ.get("sm_mhz") or summ.get("sm_max_mhz") or 1965.0
-    peak = sms * MUFU_PER_CLK_SM * float(mhz) * 1e6 * world / 1e12
+    probe = load_probe_peaks()
+    per_clk = probe.get("ex2_per_clk_per_sm")
+    if per_clk:
+        src = (f"measured ex2.approx {per_clk:.2f}/clk/SM (profiles/peaks.json, {probe.get('when', '?')}) "
+               f"x {sms} SMs x {mhz:.0f} MHz (sampled)")
+    else:
+        per_clk = MUFU_PER_CLK_SM
+        src = f"nominal {MUFU_PER_CLK_SM} MUFU/clk/SM x {sms} SMs x {mhz:.0f} MHz (sampled)"
+    peak = sms * per_clk * float(mhz) * 1e6 * world / 1e12
     achieved = pairs_per_s * EVALS_PER_PAIR[name] / 1e12
     return {"bound": "sfu", "achieved": achieved, "peak": peak, "unit": "Tevals/s", "frac": achieved / peak,
             "evals_per_pair": EVALS_PER_PAIR[name],
-            "peak_source": f"nominal {MUFU_PER_CLK_SM} MUFU/clk/SM x {sms} SMs x {mhz:.0f} MHz (sampled)",
+            "peak_source": src,
             "note": "algorithmic evaluations = the reference's clipped patch pixels (SURVEY 8(d)); "
                     "the kernel evaluates fewer (tight windows, separable exponentials)"}
 
@@ -283,6 +334,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    if local >= ndev:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but only {ndev} device(s) are visible "
+                         f"(--gpus {args.gpus})")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -343,10 +398,13 @@ def run_ours(args):
     launches = lib.pgb_launch_count() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
+    rank_ms = [total_ms]
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        t = torch.zeros(world, dtype=torch.float64, device=dev)
+        t[rank] = total_ms
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)      # every rank's device time
+        rank_ms = [float(v) for v in t.tolist()]
+        total_ms = max(rank_ms)
     ovf = lib.pgb_overflow_count()
     value = global_batch * args.steps / (total_ms / 1000.0)
 
@@ -414,10 +472,9 @@ def run_ours(args):
                          "kernel": "pgb::band_kernel<PSF> (one launch per batch; in-kernel prologue)",
                          "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy burst)"},
             "roofline_sfu": sfu_roofline(name, value, clk, world),
-            "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "path": "pgb_generate_batch (C ABI, host buffers: flow H2D + images D2H, pinned)"},
+            "e2e": e2e_line(e2e_value, h2d, d2h, global_batch, world),
             "gpu_launches": int(launches),
+            "rank_ms_total": rank_ms,
             "clocks": clk.summary(),
             "wall_s_timed_region": t_wall,
             "overflow_events": int(ovf),
@@ -432,9 +489,66 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def e2e_line(value, h2d, d2h, global_batch, world):
+    """End-to-end record; with a measured PCIe D2H bandwidth (profiles/peaks.json)
+    also the link bound: the images must cross PCIe (per GPU)."""
+    out = {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "path": "pgb_generate_batch (C ABI, host buffers: flow H2D + images D2H, pinned)"}
+    probe = load_probe_peaks()
+    if probe.get("pcie_d2h_gbs"):
+        per_gpu_pairs = global_batch / world
+        bound = probe["pcie_d2h_gbs"] * 1e9 / (d2h / per_gpu_pairs) * world
+        out["link_bound"] = {"value": bound, "unit": "pairs/s", "frac": value / bound,
+                             "pcie_d2h_gbs": probe["pcie_d2h_gbs"], "source": "profiles/peaks.json"}
+    return out
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: re-launch this script with one rank per
+    GPU (python -m torch.distributed.run, 127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")     # NCCL reports nranks in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """Launcher check without a GPU: gloo ranks, shard bookkeeping, max-over-ranks."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    from paper_2512_09664_b200.pipeline import shard_pairs
+
+    name = args.config
+    H, W, Bcfg, *_ = CONFIGS[name]
+    per_gpu = Bcfg if name != "c5" else Bcfg // world
+    global_batch = per_gpu * world if name != "c5" else Bcfg
+    shard = shard_pairs(global_batch, rank, world)
+    t = torch.zeros(world, dtype=torch.float64)
+    t[rank] = float(len(shard))
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "global_batch": global_batch,
+                          "pairs_per_rank": [int(v) for v in t.tolist()], "config": name}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--dry-run", action="store_true", help="CPU launcher check (no GPU work)")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
@@ -443,7 +557,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

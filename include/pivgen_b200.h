@@ -17,6 +17,7 @@
  * package root pkg/src/pivgen/):
  *   pgb_splat_accumulate      <- _native.pyx:14-17  splat_accumulate(...)
  *                                 (selected by backend.py:12-23)
+ *   pgb_render_oracle_dev     <- raster.py:129-151 render_oracle() (untruncated, float64)
  *   pgb_render_pairs_dev      <- raster.py:108-126 splat() x 2 frames x B pairs
  *                                 (pipeline.py:300-313 render job fan-out)
  *   pgb_advect_dev            <- particles.py:129-136 advect()
@@ -116,6 +117,13 @@ int pgb_splat_accumulate(const double* pos, const float* i0, const float* sigma_
                          int row_start, int row_stop);
 
 /* ---- device-pointer entry points -------------------------------------- */
+/* Untruncated full-image render of one frame (render_oracle, raster.py:129-151):
+ * every masked particle at every pixel in float64, summed in index order,
+ * rounded to float32 once. O(n * height * width): a test oracle, not a renderer. */
+int pgb_render_oracle_dev(const double* pos, const float* i0, const float* sigma_x,
+                          const float* sigma_y, const float* rho, const unsigned char* mask,
+                          int64_t n, int height, int width, float* out, void* stream);
+
 int pgb_splat_accumulate_dev(const double* pos, const float* i0, const float* sigma_x,
                              const float* sigma_y, const float* rho, const unsigned char* mask,
                              int64_t n, int side, float* out, int height, int width,
@@ -230,6 +238,12 @@ int64_t pgb_launch_count(void);
  * (nonzero means some tile dropped particles: the batch is invalid). */
 int pgb_overflow_count(void);
 int pgb_overflow_reset(void);
+
+/* ---- measurement probes ------------------------------------------------- */
+/* `blocks` x 256 threads, each issuing 8 * iters dependent-free ex2.approx
+ * (MUFU.EX2): the SFU issue-rate probe behind the splat's SFU roofline
+ * (scripts/measure_peaks.py -> profiles/peaks.json). `sink` >= 256 floats. */
+int pgb_probe_ex2_dev(int blocks, int iters, float* sink, void* stream);
 
 #ifdef __cplusplus
 }

@@ -79,6 +79,7 @@ SIGNATURES = {
     "pgb_render_pairs_dev": (_I, [C.POINTER(PgbParticles), C.POINTER(PgbParticles), _I64, _I,
                                   C.POINTER(C.c_int), _I, _I, _I, _I, _D, _D, _U64, _U64, _I64,
                                   _P, _P, _P, C.POINTER(C.c_int), _P]),
+    "pgb_render_oracle_dev": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I, _I, _P, _P]),
     "pgb_advect_dev": (_I, [_P, _I64, _P, _I, _I, _P, _P]),
     "pgb_sample_flow_dev": (_I, [_P, _I64, _P, _I, _I, _P, _P]),
     "pgb_finalize_dev": (_I, [_P, _I, _I, _I, _D, _D, _U64, _U64, _I64, _I, _I, _P, _P]),
@@ -98,6 +99,7 @@ SIGNATURES = {
     "pgb_apply_hiding_dev": (_I, [_I64, _U64, _U64, _I64, _D, _P, _P, _P, _P]),
     "pgb_plan": (_I, [_I, _I, _I64, _D, _I, _I, C.POINTER(PgbPlanInfo)]),
     "pgb_launch_count": (C.c_int64, []),
+    "pgb_probe_ex2_dev": (_I, [_I, _I, _P, _P]),
     "pgb_overflow_count": (_I, []),
     "pgb_overflow_reset": (_I, []),
 }

@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libpivgen_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 SOURCES = ["pivgen_b200.cu"]
-HEADERS = ["common.cuh", "fused.cuh", "band.cuh", "histmatch.cuh", "refrng.cuh"]
+HEADERS = ["common.cuh", "fused.cuh", "band.cuh", "histmatch.cuh", "refrng.cuh", "wide.cuh", "probes.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -52,7 +52,7 @@ def check_band_kernel_frame(ptxas_log: str, limit: int = 256) -> None:
 
     cur = None
     for line in ptxas_log.splitlines():
-        m = re.search(r"Function properties for (_ZN3pgb1\d?band2?_kernel\S*)", line)
+        m = re.search(r"Function properties for (_ZN3pgb1\d?band_kernel\S*)", line)
         if m:
             cur = m.group(1)
             continue
@@ -69,15 +69,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB_PATH
     tmp = LIB_PATH + ".tmp"
     extra = []
-    if os.environ.get("PGB_BAND_MAXREG"):      # tuning knob: band kernel register cap
-        extra.append(f"-DPGB_BAND_MAXREG={int(os.environ['PGB_BAND_MAXREG'])}")
-    for knob in ("PGB_BAND_MINB", "PGB_WORKER_WARPS"):
-        if os.environ.get(knob):
-            extra.append(f"-D{knob}={int(os.environ[knob])}")
-    if os.environ.get("PGB_DBG_NOATOM"):
-        extra.append("-DPGB_DBG_NOATOM")
-    if os.environ.get("PGB_PHASE_TIMING"):   # debug: per-phase cycle counters in the band kernel
-        extra.append("-DPGB_PHASE_TIMING")
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if proc.returncode != 0:

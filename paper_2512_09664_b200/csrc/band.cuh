@@ -48,7 +48,6 @@ constexpr int kBandWarps = kBandThreads / 32;
 constexpr int kBandBlock = kBandThreads + 32;   // + one staging warp
 constexpr int kMaxCellBits = 14;
 constexpr int kMaxUnpredWM = 12;   // largest unpredicated (separable) splat window
-constexpr int kTimingCtaBase = 148 * 8 * 8 * 5 / 2;   // PGB_PHASE_TIMING: per-CTA timestamps
 
 struct __align__(16) PairHdr {
   double ppp;      // realised seeding density
@@ -89,18 +88,10 @@ struct BandParams {
   PairHdr* hdr;                // [pairs]
   int* pair_ready;             // [pairs] prologue done (in-kernel prologue), else null
   int* fb_done;                // [num_fields] finished bound chunks, else null
-  int inline_prologue;         // band kernel runs prologue work items (field bounds; pairs if inline_pairs)
-  int inline_pairs;            // this batch's pair prologue runs in this launch (else precomputed)
-  int tma_store;               // full-width f32 tiles leave through TMA bulk stores
+  long long npro;              // prologue tickets (pairs + flow-bound chunks) ahead of the band items
   int4* zero_head;             // the other control head: zeroed here for the next launch (or null)
   int zero_head_n;
-  int ablate;                  // debug timing only (PGB_ABLATE): 1 no particles, 2 no splat, 4 no store
-  PairHdr* nx_hdr;             // next batch's pair prologue (tail work of this launch), or null
-  int* nx_prefix;
-  unsigned short* nx_cof;
-  uint32_t nx_batch_lo;
   int field_lo, field_cnt;     // flow fields read by this pair range
-  unsigned long long* timing;  // optional per-CTA phase cycle counters (PGB_PHASE_TIMING)
   void* out[2];
   long long out_pair_elems;
   double* st_ppp;
@@ -331,12 +322,6 @@ __device__ __forceinline__ void field_bound_chunk(const BandParams& P, int f, in
 // Per-pair prologue (whole block, NT threads, `bins` = 2^(sy+sx) + 1 ints of
 // shared scratch): density, M, maximum diameter, the cell histogram -> per-cell
 // prefix and the particle -> cell array; pair_ready[pl] releases them.
-#ifdef PGB_PHASE_TIMING
-#define PGB_STAMP(k) do { if (P.timing && threadIdx.x == 0) { unsigned long long t_; \
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); P.timing[kTimingCtaBase + 4 * 2048 + (size_t)blockIdx.x * 8 + (k)] = t_; } } while (0)
-#else
-#define PGB_STAMP(k) do { } while (0)
-#endif
 __device__ __forceinline__ void write_stats(const BandParams& P, int pl, const PairHdr& hd) {
   if (P.st_ppp) P.st_ppp[pl] = hd.ppp;
   if (P.st_M) P.st_M[pl] = hd.M;
@@ -344,33 +329,15 @@ __device__ __forceinline__ void write_stats(const BandParams& P, int pl, const P
   if (P.st_dmax) P.st_dmax[pl] = hd.dmax;
 }
 
-// Where a pair prologue writes: this batch's tables (+ readiness flag and
-// stats), or the next batch's (cross-launch pipeline, no flag / stats).
-struct ProOut {
-  PairHdr* hdr;
-  int* prefix;
-  unsigned short* cof;
-  uint32_t batch;
-  int* ready;
-  bool stats;
-};
-
-__device__ __forceinline__ ProOut pro_cur(const BandParams& P) {
-  return ProOut{P.hdr, P.prefix, P.cell_of, P.batch_lo, P.pair_ready, true};
-}
-__device__ __forceinline__ ProOut pro_next(const BandParams& P) {
-  return ProOut{P.nx_hdr, P.nx_prefix, P.nx_cof, P.nx_batch_lo, nullptr, false};
-}
-
 template <int NT>
-__device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes, const ProOut out) {
+__device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes) {
   __shared__ int wsum[NT / 32];
   __shared__ PairHdr shd;
   __shared__ int scm;
   const int tid = threadIdx.x, lane = tid & 31;
   const int L = P.sy + P.sx;
   const int ncell = 1 << L;
-  const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), out.batch};
+  const RngKey key = band_key(P, pl);
   for (int i = tid; i < (ncell < 4 ? 4 : ncell); i += NT) bins[i] = 0;
   const GenCfg& g = P.g;
   // seeding density and active count (particles.py:73-83), computed by every
@@ -385,10 +352,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     scm = 0;
   }
   __syncthreads();
-  PGB_STAMP(0);
-#ifdef PGB_PHASE_TIMING
-  const long long c0_ = clock64();
-#endif
   if (tid == 0) {
     // maximum diameter uniform: max of M uniforms = V^(1/M), on particle J
     // (a serial float64 chain: overlapped with the histogram below)
@@ -409,7 +372,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     shd.dmax = dmax;
     // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
     shd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
-    PGB_STAMP(1);
   } else {
     // cell histogram of M iid labels (4 labels per Philox call)
     for (int q = tid - 1; q < (M + 3) >> 2; q += NT - 1) {
@@ -421,7 +383,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     }
   }
   __syncthreads();
-  PGB_STAMP(2);
   // Cell counts -> exclusive prefix (in place + global), the maximum cell
   // count, and the particle -> cell array. Warps own 512-cell chunks; lanes
   // read consecutive int4s (conflict-free), a warp shuffle scan per 128-cell
@@ -475,9 +436,8 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     if (lane == 0) scm = m;
   }
   __syncthreads();
-  PGB_STAMP(3);
-  int* pre = out.prefix + (size_t)pl * pre_stride(ncell);
-  unsigned short* cof = out.cof + (size_t)pl * cof_stride(P.n);
+  int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
+  unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
   // particle -> cell (counting-sort order: particles of cell c are pre[c] ..
   // pre[c+1]-1). Staged in shared memory when it fits: mark the first slot
   // of every non-empty cell with the cell id (slots zeroed above), then a
@@ -522,7 +482,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
   }
   if (tid == 0) bins[ncell] = wsum[0];
   __syncthreads();
-  PGB_STAMP(5);
   if (staged) {
     // inclusive max-scan of the marks: one warp layer (32 lanes x int4 of 8
     // slots = 256 slots) per chunk; chunk maxima -> exclusive carries in
@@ -580,7 +539,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
       lo = r = max(r, w4.w & 0xffff); hi = r = max(r, (int)((unsigned)w4.w >> 16)); o3 = lo | (hi << 16);
       if (q < ns4) c4[q] = make_int4(o0, o1, o2, o3);
     }
-    PGB_STAMP(6);
   } else {
     for (int c = tid; c < ncell; c += NT) {
       const int j1 = bins[c + 1];
@@ -591,18 +549,13 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     pre[ncell] = wsum[0];
     PairHdr hd = shd;
     hd.cmax = scm;
-    out.hdr[pl] = hd;
-    if (out.stats) write_stats(P, pl, hd);
+    P.hdr[pl] = hd;
+    write_stats(P, pl, hd);
   }
   __syncthreads();
-  PGB_STAMP(4);
-#ifdef PGB_PHASE_TIMING
-  if (P.timing && threadIdx.x == 0)
-    P.timing[kTimingCtaBase + 4 * 2048 + (size_t)blockIdx.x * 8 + 7] = (unsigned long long)(clock64() - c0_);
-#endif
-  if (tid == 0 && out.ready) {
+  if (tid == 0 && P.pair_ready) {
     __threadfence();
-    st_release(out.ready + pl, 1);
+    st_release(P.pair_ready + pl, 1);
   }
 }
 
@@ -615,7 +568,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
     field_bound_chunk<kPrologueThreads>(P, fb / kFieldBlocks, fb % kFieldBlocks);
     return;
   }
-  pair_prologue<kPrologueThreads>(P, blockIdx.x, bins, P.pro_smem, pro_cur(P));
+  pair_prologue<kPrologueThreads>(P, blockIdx.x, bins, P.pro_smem);
 }
 
 // ----------------------------------------------------------------------------
@@ -624,7 +577,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandPa
 // Per-item parameters (warp 0 computes them for the next item while the
 // block finishes the current one; double-buffered).
 constexpr int kMaxSeg = 128;   // particle segments (cell rows) per enumeration pass
-constexpr int kStageSlots = 3; // staged item slots (band2 keeps items k, k+1, k+2 live)
+constexpr int kStageSlots = 2; // staged item slots (current + next)
 
 struct ItemCfg {
   int pl, r0, r1, c0, c1;
@@ -639,6 +592,7 @@ enum { kItemBand = 0, kItemEnd = 2 };
 
 struct __align__(16) BandShared {
   int wsum[kBandWarps];
+  long long ticket0;                 // prologue / first band ticket of this CTA
 
   int nseg[kStageSlots];             // segments of the staged pass
   int rows_left[kStageSlots];        // cell rows not yet staged (rare multi-pass items)
@@ -1133,124 +1087,6 @@ __device__ __forceinline__ void band_store(const BandParams& P, int* acc, int pl
 }
 
 
-// ---- TMA bulk store of finalized full-width tiles ----------------------------
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(ssrc);
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(sa), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit_wait_read() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-
-// Finalize one full-width frame tile in place (int accumulator -> float32 image
-// values: raw * 2^-s, or clip(raw + offset + noise, 0, 1)).
-template <int OUT, bool NOISE>
-__device__ __forceinline__ void band_finalize_inplace(const BandParams& P, int* __restrict__ acc, int pl, int f,
-                                                      int r0, int nr, float inv_scale) {
-  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
-  const int nq = (nr * P.W) >> 2;
-  const uint32_t pix0 = (uint32_t)(r0 * P.W);
-  int4* ap = reinterpret_cast<int4*>(acc);
-  const float bg = P.bg_offset;
-#pragma unroll 4
-  for (int q = threadIdx.x; q < nq; q += kBandThreads) {
-    const int4 a = ap[q];
-    float4 v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
-    if (OUT == kOutRaw) {
-      v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
-    } else if (NOISE) {
-      const float sd = P.noise_std;
-      const float4 nz = noise4_rk(P.g.rk, gpair, P.batch_lo, (uint32_t)f + 1, (pix0 >> 2) + q);
-      v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
-      v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
-      v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
-      v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
-    } else {
-      v.x = __saturatef(fmaf(v.x, inv_scale, bg));
-      v.y = __saturatef(fmaf(v.y, inv_scale, bg));
-      v.z = __saturatef(fmaf(v.z, inv_scale, bg));
-      v.w = __saturatef(fmaf(v.w, inv_scale, bg));
-    }
-    reinterpret_cast<float4*>(ap)[q] = v;
-  }
-}
-
-// Both frames of a full-width item: finalize in place, one thread issues the
-// two bulk stores (TMA engine, no per-quad global store instructions) and
-// waits until they have read shared memory, then the accumulators are zeroed.
-// Workers only (named barrier 1).
-template <int OUT, bool NOISE>
-__device__ __forceinline__ void band_store_tma(const BandParams& P, int* acc0, int* acc1, int pl, int r0, int nr,
-                               float inv_scale) {
-  band_finalize_inplace<OUT, NOISE>(P, acc0, pl, 0, r0, nr, inv_scale);
-  band_finalize_inplace<OUT, NOISE>(P, acc1, pl, 1, r0, nr, inv_scale);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
-  if (threadIdx.x == 0) {
-    const size_t off = ((size_t)pl * (size_t)P.out_pair_elems + (size_t)r0 * P.W) * 4;
-    const unsigned bytes = (unsigned)nr * (unsigned)P.W * 4u;
-    bulk_store(static_cast<char*>(P.out[0]) + off, acc0, bytes);
-    bulk_store(static_cast<char*>(P.out[1]) + off, acc1, bytes);
-    bulk_commit_wait_read();
-  }
-  asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads));
-  const int nq = (nr * P.W) >> 2;
-  int4* a0 = reinterpret_cast<int4*>(acc0);
-  int4* a1 = reinterpret_cast<int4*>(acc1);
-#pragma unroll 4
-  for (int q = threadIdx.x; q < nq; q += kBandThreads) {
-    a0[q] = make_int4(0, 0, 0, 0);
-    a1[q] = make_int4(0, 0, 0, 0);
-  }
-}
-
-// Returns true when the item was stored through the TMA path.
-__device__ __forceinline__ bool band_store_items_tma(const BandParams& P, int* acc0, int* acc1, int pl, int r0,
-                                                     int nr, int c0, int nc, float inv_scale) {
-  if (!(P.tma_store && c0 == 0 && nc == P.W && P.AS == P.W && (P.W & 3) == 0 && P.out_mode != kOutU16))
-    return false;
-  if (nr <= 0) return true;
-  if (P.out_mode == kOutRaw) band_store_tma<kOutRaw, false>(P, acc0, acc1, pl, r0, nr, inv_scale);
-  else if (P.noise_std > 0.f) band_store_tma<kOutF32, true>(P, acc0, acc1, pl, r0, nr, inv_scale);
-  else band_store_tma<kOutF32, false>(P, acc0, acc1, pl, r0, nr, inv_scale);
-  return true;
-}
-
-
-// Full-width rows [r0, r0 + nr) of both frames, stored (and zeroed) by
-// threads t = 0..nt-1 of some warp group.
-__device__ __forceinline__ void band_store_rows(const BandParams& P, int* acc0, int* acc1, int pl, int r0, int nr,
-                                                float inv_scale, int t, int nt) {
-  if (nr <= 0) return;
-  const bool noise = P.noise_std > 0.f;
-  switch (P.out_mode) {
-    case kOutRaw:
-      band_store_lin<kOutRaw, false>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
-      band_store_lin<kOutRaw, false>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
-      return;
-    case kOutF32:
-      if (noise) {
-        band_store_lin<kOutF32, true>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
-        band_store_lin<kOutF32, true>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
-      } else {
-        band_store_lin<kOutF32, false>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
-        band_store_lin<kOutF32, false>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
-      }
-      return;
-    default:
-      if (noise) {
-        band_store_lin<kOutU16, true>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
-        band_store_lin<kOutU16, true>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
-      } else {
-        band_store_lin<kOutU16, false>(P, acc0, pl, 0, r0, nr, inv_scale, t, nt);
-        band_store_lin<kOutU16, false>(P, acc1, pl, 1, r0, nr, inv_scale, t, nt);
-      }
-      return;
-  }
-}
-
 // Range of seeding cells [lo, hi] whose span [k*s, (k+1)*s) meets [a, b).
 __device__ __forceinline__ void cell_range(double a, double b, double s, int n, int& lo, int& hi) {
   const double fa = floor(fmax(a, 0.0) / s);
@@ -1288,11 +1124,10 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   ic.c0 = tx * P.TW;
   ic.c1 = min(ic.c0 + P.TW, g.W);
   ic.field = (int)((P.pair_base + pl) / P.pairs_per_field);
-  if (P.inline_prologue) {
-    // produced inside this launch by other CTAs (their first work items)
+  if (P.pair_ready) {
+    // produced inside this launch by other CTAs (earlier tickets)
     int ns = 32;
-    if (P.inline_pairs)
-      while (ld_acquire_b(P.pair_ready + pl) == 0) { __nanosleep(ns); ns = min(ns * 2, 256); }
+    while (ld_acquire_b(P.pair_ready + pl) == 0) { __nanosleep(ns); ns = min(ns * 2, 256); }
     while (ld_acquire_b(P.fb_done + ic.field) < kFieldBlocks) { __nanosleep(ns); ns = min(ns * 2, 256); }
   }
   {
@@ -1331,8 +1166,7 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   // unpredicated windows for uncorrelated particles only: the correlated
   // variant (splat_point_u) showed tiling-dependent 1-ulp differences in the
   // stress test (scripts/stress.py); correlated particles use the dynamic loops
-  const int wm = (P.psf == kPsfPoint && ic.sep && ic.wt <= kMaxUnpredWM && ic.wt - 1 <= P.pad_rows &&
-                  !(P.ablate & 64)) ? ic.wt : 0;
+  const int wm = (P.psf == kPsfPoint && ic.sep && ic.wt <= kMaxUnpredWM && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
   ic.var = (P.psf == kPsfPoint ? 16 * ic.sep : 0) + wm;
 }
 
@@ -1386,17 +1220,18 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
 // Dynamic schedule: the stager's lane 0 takes the next ticket (band items in
 // order, then kItemEnd).
 __device__ __forceinline__ void ticket_item(const BandParams& P, long long t, int& kind, long long& idx) {
-  kind = t < P.total_items ? kItemBand : kItemEnd;
-  idx = t;
+  idx = t - P.npro;
+  kind = idx < P.total_items ? kItemBand : kItemEnd;
 }
 
-__device__ __forceinline__ void stage_next(const BandParams& P, BandShared* sh, int b) {
+// `taken` >= 0: a ticket this CTA already holds (its first band item).
+__device__ __forceinline__ void stage_next(const BandParams& P, BandShared* sh, int b, long long taken) {
   const int lane = threadIdx.x & 31;
   ItemCfg& ic = sh->ic[b];
   if (lane == 0) {
     int kind;
     long long idx;
-    ticket_item(P, (long long)atomicAdd(P.ticket, 1), kind, idx);
+    ticket_item(P, taken >= 0 ? taken : (long long)atomicAdd(P.ticket, 1), kind, idx);
     ic.kind = kind;
     ic.item = idx;
     if (kind == kItemBand) item_setup(P, idx, ic);
@@ -1492,7 +1327,7 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
   int next_row = ic.cy0;   // first cell row of the current pass
   for (;;) {
     const int nseg = sh->nseg[buf];
-    const int N = (P.ablate & 1) ? 0 : sh->seg_off[buf][nseg];
+    const int N = sh->seg_off[buf][nseg];
     const int* soff = sh->seg_off[buf];
     const int* sst = sh->seg_start[buf];
     // slot q (clamped into [0, N)) -> particle index (segment search)
@@ -1533,12 +1368,12 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
         PFrames A;
         const bool ok = qa < N;
         band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
-          if (ok && F.on1 && !(P.ablate & 2))
+          if (ok && F.on1)
             splat_v<PSF, SEP, WM>(acc0, P.AS, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, F.rho1, h, r0,
                                   r1, c0, c1, shift, scale);
           if (more) aA = draw_a(P.g, key, gA);
         });
-        if (ok && !(P.ablate & 2)) {
+        if (ok) {
           if (A.on2)
             splat_v<PSF, SEP, WM>(acc1, P.AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, A.rho2, h, r0,
                                   r1, c0, c1, shift, scale);
@@ -1564,71 +1399,47 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   int* acc1 = acc0 + P.TH * P.AS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
-#ifdef PGB_PHASE_TIMING
-  auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; };
-  unsigned long long* CT = P.timing ? P.timing + kTimingCtaBase + (size_t)blockIdx.x * 4 : nullptr;
-  if (CT && tid == 0) CT[0] = gtime();
-#endif
   const int acc_bytes = ((2 * P.TH + P.pad_rows) * P.AS + 8) * 4;
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)
     for (int e = tid; e < P.zero_head_n; e += kBandBlock) P.zero_head[e] = make_int4(0, 0, 0, 0);
-  if (P.inline_prologue) {
-    // prologue work items first (this batch's pairs unless precomputed by the
-    // previous launch, then flow-bound chunks); band items wait on their
-    // readiness flags, so every wait targets work that some co-resident CTA
-    // runs before it waits on anything
-    const int npp = P.inline_pairs ? P.pairs : 0;
-    const int npro = npp + P.field_cnt * kFieldBlocks;
-    for (int w = blockIdx.x; w < npro; w += gridDim.x) {
-      if (w < npp) {
-        pair_prologue<kBandBlock>(P, w, acc0, acc_bytes, pro_cur(P));
-      } else {
-        const int fc = w - npp;
-        field_bound_chunk<kBandBlock>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
-      }
-      __syncthreads();
+  // One ticket sequence: [0, npro) prologue items (the pairs, then the
+  // flow-bound chunks), then the band items. Band items wait on prologue
+  // flags only, and every prologue ticket precedes every band ticket, so each
+  // wait targets work already taken by a running CTA that waits on nothing:
+  // forward progress without co-residency (MPS limits, green contexts, a
+  // concurrent kernel holding SMs, any grid size).
+  long long first;
+  for (;;) {
+    if (tid == 0) sh->ticket0 = atomicAdd(P.ticket, 1);
+    __syncthreads();
+    first = sh->ticket0;
+    __syncthreads();
+    if (first >= P.npro) break;
+    const int w = (int)first;
+    if (w < P.pairs) {
+      pair_prologue<kBandBlock>(P, w, acc0, acc_bytes);
+    } else {
+      const int fc = w - P.pairs;
+      field_bound_chunk<kBandBlock>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
     }
-    if (!P.inline_pairs && tid == 0)
-      for (int pl = blockIdx.x; pl < P.pairs; pl += gridDim.x) write_stats(P, pl, P.hdr[pl]);
+    __syncthreads();
   }
   // both frame accumulators + the zero padding behind them
   for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 8) / 4; e += kBandBlock)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
-  __syncthreads();
   // dynamic schedule: the staging warp takes the ticket of item k+1 and
   // prepares it (parameters + particle segments) while the workers splat item k
-#ifdef PGB_PHASE_TIMING
-  if (CT && tid == 0) CT[1] = gtime();
-#endif
-  if (stager) stage_next(P, sh, 0);
+  if (stager) stage_next(P, sh, 0, first);
   __syncthreads();
-#ifdef PGB_PHASE_TIMING
-  if (CT && tid == 0) CT[2] = gtime();
-#endif
   for (int buf = 0;; buf ^= 1) {
     const int kind = sh->ic[buf].kind;
     if (kind == kItemEnd) break;
     if (stager) {
-#ifdef PGB_PHASE_TIMING
-      const long long ts0 = clock64();
-#endif
-      stage_next(P, sh, buf ^ 1);
-#ifdef PGB_PHASE_TIMING
-      if (P.timing && (tid & 31) == 0) {
-        unsigned long long* T = P.timing + kTimingCtaBase + 4 * 2048 + 8 * 296 + (size_t)blockIdx.x * 2;
-        T[0] += (unsigned long long)(clock64() - ts0);
-        T[1] += 1;
-      }
-#endif
-    }
-    if (stager) {
+      stage_next(P, sh, buf ^ 1, -1);
       __syncthreads();   // particles done
       __syncthreads();   // store done
       continue;
     }
-#ifdef PGB_PHASE_TIMING
-    const long long t_item0 = clock64();
-#endif
     const ItemCfg& ic = sh->ic[buf];
     const long long item = ic.item;
     const int pl = ic.pl;
@@ -1645,153 +1456,14 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
         default: band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1); break;
       }
     }
-#ifdef PGB_PHASE_TIMING
-    const long long t_part = clock64();
-#endif
     __syncthreads();   // particles done (stager: next item staged)
-#ifdef PGB_PHASE_TIMING
-    const long long t_bar1 = clock64();
-#endif
     const float inv_scale = 1.0f / scale;
-    if (!(P.ablate & 4) && !band_store_items_tma(P, acc0, acc1, pl, r0, r1 - r0, c0, c1 - c0, inv_scale)) {
-      band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
-      band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
-    }
-#ifdef PGB_PHASE_TIMING
-    const long long t_store = clock64();
-#endif
+    band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
+    band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
     __syncthreads();   // accumulators zeroed
-#ifdef PGB_PHASE_TIMING
-    if (P.timing) {
-      // per warp: [particles, barrier1, store, barrier2] cycles of this item
-      const long long t_end = clock64();
-      unsigned long long* T = P.timing + ((size_t)blockIdx.x * kBandWarps + warp) * 5;
-      if ((tid & 31) == 0) {
-        atomicAdd(T + 0, (unsigned long long)(t_part - t_item0));
-        atomicAdd(T + 1, (unsigned long long)(t_bar1 - t_part));
-        atomicAdd(T + 2, (unsigned long long)(t_store - t_bar1));
-        atomicAdd(T + 3, (unsigned long long)(t_end - t_store));
-        atomicAdd(T + 4, 1ull);
-      }
-    }
-#endif
-  }
-  // tail work (cross-launch pipeline, opt-in): the next batch's pair
-  // prologues, taken by whichever CTAs finish their band items first
-  if (P.nx_hdr) {
-    for (;;) {
-      if (tid == 0) sh->nseg[0] = atomicAdd(P.ticket + 1, 1);
-      __syncthreads();
-      const int w = sh->nseg[0];
-      if (w >= P.pairs) break;
-      pair_prologue<kBandBlock>(P, w, acc0, acc_bytes, pro_next(P));
-      __syncthreads();
-    }
-  }
-#ifdef PGB_PHASE_TIMING
-  if (CT && tid == 0) CT[3] = gtime();
-#endif
-}
-
-
-// ----------------------------------------------------------------------------
-// band2: one CTA per SM, warp-specialised, double-buffered accumulators
-// (experimental, PGB_BAND2=1; full-width tiles only). 16 particle warps splat
-// item k into accumulator set k&1 while 2 store warps write item k-1 from the
-// other set and one staging warp prepares item k+1: no CTA-wide barrier
-// between the particle and store phases. Named barriers:
-//   STAGED   stager arrive / workers sync        (item k's config ready)
-//   STARTED  workers arrive / stager sync        (slot of item k-1 reusable)
-//   FULL[s]  workers arrive / storers sync       (set s splatted)
-//   EMPTY[s] storers arrive / workers sync       (set s stored and zeroed)
-// ----------------------------------------------------------------------------
-constexpr int kB2Workers = 512;
-constexpr int kB2Store = 64;
-constexpr int kB2Block = kB2Workers + kB2Store + 32;
-constexpr int kB2BarStaged = 1, kB2BarStarted = 2, kB2BarFull = 3, kB2BarEmpty = 5, kB2BarWork = 7;
-
-__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-template <int PSF>
-__global__ void __launch_bounds__(kB2Block, 1) band2_kernel(const BandParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
-  int* accbase = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
-  const int set_ints = (2 * P.TH + P.pad_rows) * P.AS + 8;
-  const int tid = threadIdx.x;
-  const int acc_bytes = 2 * set_ints * 4;
-  if (blockIdx.x == gridDim.x - 1 && P.zero_head)
-    for (int e = tid; e < P.zero_head_n; e += kB2Block) P.zero_head[e] = make_int4(0, 0, 0, 0);
-  if (P.inline_prologue) {
-    const int npp = P.inline_pairs ? P.pairs : 0;
-    const int npro = npp + P.field_cnt * kFieldBlocks;
-    for (int w = blockIdx.x; w < npro; w += gridDim.x) {
-      if (w < npp) {
-        pair_prologue<kB2Block>(P, w, accbase, acc_bytes, pro_cur(P));
-      } else {
-        const int fc = w - npp;
-        field_bound_chunk<kB2Block>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
-      }
-      __syncthreads();
-    }
-    if (!P.inline_pairs && tid == 0)
-      for (int pl = blockIdx.x; pl < P.pairs; pl += gridDim.x) write_stats(P, pl, P.hdr[pl]);
-  }
-  for (int e = tid; e < 2 * set_ints / 4; e += kB2Block) reinterpret_cast<int4*>(accbase)[e] = make_int4(0, 0, 0, 0);
-  __syncthreads();
-  constexpr int nSW = kB2Workers + 32, nWS = kB2Workers + kB2Store;
-  if (tid >= kB2Workers + kB2Store) {
-    // staging warp
-    stage_next(P, sh, 0);
-    nbar_arrive(kB2BarStaged, nSW);
-    for (int k = 0;; ++k) {
-      if (sh->ic[k % kStageSlots].kind == kItemEnd) break;
-      nbar_sync(kB2BarStarted, nSW);
-      stage_next(P, sh, (k + 1) % kStageSlots);
-      nbar_arrive(kB2BarStaged, nSW);
-    }
-  } else if (tid < kB2Workers) {
-    for (int k = 0;; ++k) {
-      const int slot = k % kStageSlots, s = k & 1;
-      nbar_sync(kB2BarStaged, nSW);
-      const ItemCfg& ic = sh->ic[slot];
-      if (ic.kind == kItemEnd) {
-        nbar_arrive(kB2BarFull + s, nWS);
-        break;
-      }
-      if (k >= 2) nbar_sync(kB2BarEmpty + s, nWS);
-      nbar_arrive(kB2BarStarted, nSW);
-      int* acc0 = accbase + s * set_ints;
-      int* acc1 = acc0 + P.TH * P.AS;
-      if constexpr (PSF == kPsfErf) {
-        band_particles<PSF, 0, 0, kB2Workers, kB2BarWork>(P, sh, slot, ic.item, acc0, acc1);
-      } else {
-        switch (ic.var) {
-#define PGB_V2(S, W) case 16 * S + W: band_particles<PSF, S, W, kB2Workers, kB2BarWork>(P, sh, slot, ic.item, acc0, acc1); break;
-          PGB_V2(1, 1) PGB_V2(1, 2) PGB_V2(1, 3) PGB_V2(1, 4) PGB_V2(1, 5) PGB_V2(1, 6) PGB_V2(1, 7)
-          PGB_V2(1, 8) PGB_V2(1, 9) PGB_V2(1, 10) PGB_V2(1, 11) PGB_V2(1, 12)
-#undef PGB_V2
-          default: band_particles<PSF, 0, 0, kB2Workers, kB2BarWork>(P, sh, slot, ic.item, acc0, acc1); break;
-        }
-      }
-      nbar_arrive(kB2BarFull + s, nWS);
-    }
-  } else {
-    // store warps
-    const int t = tid - kB2Workers;
-    for (int k = 0;; ++k) {
-      const int slot = k % kStageSlots, s = k & 1;
-      nbar_sync(kB2BarFull + s, nWS);
-      const ItemCfg& ic = sh->ic[slot];
-      if (ic.kind == kItemEnd) break;
-      int* acc0 = accbase + s * set_ints;
-      int* acc1 = acc0 + P.TH * P.AS;
-      band_store_rows(P, acc0, acc1, ic.pl, ic.r0, ic.r1 - ic.r0, 1.0f / (float)(1 << ic.shift), t, kB2Store);
-      nbar_arrive(kB2BarEmpty + s, nWS);
-    }
   }
 }
+
 
 // Particle arrays of the generator (one block per pair): exactly the particles
 // the band kernel renders (positions = anchor + fraction).

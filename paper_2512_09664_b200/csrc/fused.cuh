@@ -91,11 +91,9 @@ struct __align__(16) SlotHdr {
   int gen_done;        // generate items of the current occupant finished
   int render_done;     // render items finished
   int epoch;           // number of occupants retired (slot of pair p is free when epoch == p / ring)
-  int M;               // active count
-  unsigned dmax;       // max active diameter (float bits)
   unsigned amp;        // max record amplitude (float bits)
   int wmax[2];         // per frame max record window width (columns or rows)
-  double ppp;          // realised seeding density
+  int pad0, pad1;
 };
 
 struct FusedParams {
@@ -110,19 +108,11 @@ struct FusedParams {
   uint32_t batch_lo;
   int psf, out_mode;
   float bg_offset, noise_std;
-  int mode;  // 0 generate, 1 inject
-  GenCfg g;
-  const float2* flows;
-  int pairs_per_field, num_fields;
-  long long field_elems;
+  uint32_t k0, k1;     // seed (noise keys)
   InjFrame inj[2];
   const int* side_in;  // device, per pair (inject mode)
   void* out[2];
   long long out_pair_elems;
-  double* st_ppp;
-  int* st_M;
-  int* st_side;
-  float* st_dmax;
   int* bin_counts;
   // workspace
   Rec* recs;           // [ring][nframes][tiles][chunks][cap]
@@ -136,10 +126,9 @@ struct FusedParams {
 struct __align__(16) SharedHdr {
   unsigned long long bar;   // mbarrier: TMA bulk loads of a render item's records
   int item;                 // current ticket
-  unsigned dmax, amp;
+  unsigned amp;
   int wmax[2];
   int cov_max, shift;
-  int M;
   int K[2];                 // records per frame of the current render item
 };
 
@@ -222,83 +211,6 @@ __device__ __forceinline__ float laser_profile(const GenCfg& g, float z) {
   const float t = 2.0f * z * z / (g.dz0 * g.dz0);
   const float p = t > 0.f ? powf(t, g.shape) : 0.f;
   return g.q * expf(-0.3989422804014327f * p);
-}
-
-__device__ __forceinline__ void gen_particle(const FusedParams& P, int pl, int i, int M,
-                                             const float2* __restrict__ flow, Particle& pt) {
-  const GenCfg& g = P.g;
-  const RngKey key{g.k0, g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
-  // sample_particles (particles.py:61-101)
-  const uint4 a = draw(key, (uint32_t)i, kTagParticleA);
-  const uint32_t X = cell_coord(0u, a.x, g.W, 0);
-  const uint32_t Y = cell_coord(0u, a.y, g.H, 0);
-  const float d = lerpf_exact(g.d_lo, g.d_span, unit23(a.z));
-  const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
-  const bool active = i < M;
-  float rho = g.rho_lo, z1 = 0.f;
-  bool vis1 = true, vis2 = true;
-  if (g.need_b) {
-    const uint4 b = draw(key, (uint32_t)i, kTagParticleB);
-    rho = lerpf_exact(g.rho_lo, g.rho_span, unit23(b.x));
-    vis1 = (uint64_t)b.y >= g.hide_thr;   // apply_hiding (particles.py:139-147)
-    vis2 = (uint64_t)b.z >= g.hide_thr;
-    z1 = lerpf_exact(g.z_lo, g.z_span, unit23(b.w));
-  }
-  const float i0f = active ? i0 : 0.f;
-  const float sig = __fmul_rn(d, g.inv_ratio);
-  float sx2 = sig, sy2 = sig, i02 = i0f, rho2 = rho;
-  if (g.need_perturb) {
-    // perturb_frame2 (particles.py:104-126)
-    const uint4 c = draw(key, (uint32_t)i, kTagPerturb);
-    const float2 n01 = box_muller(c.x, c.y);
-    const float2 n23 = box_muller(c.z, c.w);
-    if (g.f2_sigma_std > 0.f) {
-      sx2 = fmaxf(__fadd_rn(sig, __fmul_rn(g.f2_sigma_std, n01.x)), 1e-3f);
-      sy2 = fmaxf(__fadd_rn(sig, __fmul_rn(g.f2_sigma_std, n01.y)), 1e-3f);
-    }
-    if (g.f2_i0_std > 0.f) {
-      const float t = fminf(fmaxf(__fadd_rn(i0f, __fmul_rn(g.f2_i0_std, n23.x)), 0.f), 1.f);
-      i02 = i0f == 0.f ? 0.f : t;
-    }
-    if (g.f2_rho_std > 0.f) {
-      const float lim = 0.999f;
-      rho2 = fminf(fmaxf(__fadd_rn(rho, __fmul_rn(g.f2_rho_std, n23.y)), -lim), lim);
-    }
-  }
-  float amp1 = i0f, amp2 = i02;
-  if (g.laser) {
-    amp1 *= laser_profile(g, z1);
-    amp2 *= laser_profile(g, z1 + g.w);
-  }
-  Frame& f1 = pt.fr[0];
-  Frame& f2 = pt.fr[1];
-  fixed_anchor(X, f1.ax, f1.fx);
-  fixed_anchor(Y, f1.ay, f1.fy);
-  // advect (particles.py:129-136): bilinear, edge-clamped (flowfield.py:207-232)
-  int cx, cy;
-  float tx, ty;
-  fixed_cell(X, g.W, cx, tx);
-  fixed_cell(Y, g.H, cy, ty);
-  const int cx1 = cx + 1 < g.W ? cx + 1 : g.W - 1;
-  const int cy1 = cy + 1 < g.H ? cy + 1 : g.H - 1;
-  const float2 q00 = __ldg(flow + (size_t)cy * g.W + cx);
-  const float2 q01 = __ldg(flow + (size_t)cy * g.W + cx1);
-  const float2 q10 = __ldg(flow + (size_t)cy1 * g.W + cx);
-  const float2 q11 = __ldg(flow + (size_t)cy1 * g.W + cx1);
-  const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
-  const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
-  advect_anchor(X, f1.ax, u, f2.ax, f2.fx);
-  advect_anchor(Y, f1.ay, v, f2.ay, f2.fy);
-  f1.amp = amp1; f1.sx = sig; f1.sy = sig; f1.rho = rho;
-  f2.amp = amp2; f2.sx = sx2; f2.sy = sy2; f2.rho = rho2;
-  // contribution_mask (raster.py:86-88): active & visible & i0 > 0
-  f1.on = active && vis1 && amp1 > 0.f;
-  f2.on = active && vis2 && amp2 > 0.f;
-  pt.diam = d;
-  pt.z1 = z1;
-  pt.active = active;
-  pt.vis1 = vis1 && active;
-  pt.vis2 = vis2 && active;
 }
 
 // Oracle mode: float64 positions from the reference; anchor = floor(x + 1/2)
@@ -573,7 +485,7 @@ __device__ __forceinline__ void store_quad(const FusedParams& P, const int4 a, c
     const float bg = P.bg_offset;
     if (NOISE) {
       const float sd = P.noise_std;
-      const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(pix >> 2));
+      const float4 nz = noise4(P.k0, P.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(pix >> 2));
       v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
       v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
       v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
@@ -660,7 +572,7 @@ __device__ void store_tile(const FusedParams& P, const int* __restrict__ acc, in
     } else {
       float nzv = 0.f;
       if (sd > 0.f) {
-        const float4 nz = noise4(P.g.k0, P.g.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
+        const float4 nz = noise4(P.k0, P.k1, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
         const int jn = (int)(p & 3);
         nzv = jn == 0 ? nz.x : (jn == 1 ? nz.y : (jn == 2 ? nz.z : nz.w));
       }
@@ -694,21 +606,9 @@ __device__ __forceinline__ void store_rec_global(Rec* dst, const Rec& r) {
   __stcg(reinterpret_cast<float4*>(dst) + 1, s4[1]);
 }
 
-__device__ __forceinline__ int pair_M(const FusedParams& P, int pl, double* ppp_out) {
-  const RngKey key{P.g.k0, P.g.k1, (uint32_t)(P.pair_base + pl), P.batch_lo};
-  const uint4 w = draw(key, 0u, kTagPair);
-  const double ppp = lerp_exact(P.g.ppp_lo, P.g.ppp_hi, u53_to_unit(w.x, w.y));
-  // m = round(ppp * H * W) clamped to [0, N]   (particles.py:80-83)
-  double m = rint(dmul(dmul(ppp, (double)P.g.H), (double)P.g.W));
-  m = fmin(fmax(m, 0.0), (double)P.n);
-  *ppp_out = ppp;
-  return (int)m;
-}
-
 // GENERATE (pair pl, chunk c): counting sort of the chunk's particles into
 // its PRIVATE per-(frame, tile) segments of the pair's slot. Ranks come from
 // shared-memory atomics only: no global round trips, no barriers per round.
-template <int MODE>
 __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int pl, int c) {
   const int tid = threadIdx.x;
   const int slot = pl % P.ring;
@@ -718,32 +618,20 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
   if (tid == 0) {
     // the slot is free once its previous occupant (pair pl - ring) is fully rendered
     spin_until_geq(&S->epoch, pl / P.ring);
-    double ppp = 0.0;
-    const int M = MODE == 0 ? pair_M(P, pl, &ppp) : 0;
-    sh->M = M;
-    sh->dmax = sh->amp = 0u;
+    sh->amp = 0u;
     sh->wmax[0] = sh->wmax[1] = 0;
-    if (c == 0) {
-      S->M = M;
-      S->ppp = ppp;
-    }
   }
   for (int e = tid; e < nf * T; e += kThreads) cnt[e] = 0;
   __syncthreads();
-  const int M = sh->M;
   Rec* recs = P.recs + (size_t)slot * nf * T * G * P.cap;
-  const float2* flow = MODE == 0
-      ? P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems : nullptr;
   const int i_lo = c * P.chunk;
   const int i_hi = min(P.n, i_lo + P.chunk);
   const int hx = P.halo;
-  unsigned dmax_l = 0u, amp_l = 0u;
+  unsigned amp_l = 0u;
   int wmax_l[2] = {0, 0};
   for (int i = i_lo + tid; i < i_hi; i += kThreads) {
     Particle pt;
-    if (MODE == 0) gen_particle(P, pl, i, M, flow, pt);
-    else inject_particle(P, pl, i, pt);
-    if (MODE == 0 && pt.active) dmax_l = max(dmax_l, __float_as_uint(pt.diam));
+    inject_particle(P, pl, i, pt);
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
       if (f >= nf) continue;
@@ -781,13 +669,11 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
-    dmax_l = max(dmax_l, __shfl_xor_sync(~0u, dmax_l, o));
     amp_l = max(amp_l, __shfl_xor_sync(~0u, amp_l, o));
     wmax_l[0] = max(wmax_l[0], __shfl_xor_sync(~0u, wmax_l[0], o));
     wmax_l[1] = max(wmax_l[1], __shfl_xor_sync(~0u, wmax_l[1], o));
   }
   if ((tid & 31) == 0) {
-    atomicMax(&sh->dmax, dmax_l);
     atomicMax(&sh->amp, amp_l);
     atomicMax(&sh->wmax[0], wmax_l[0]);
     atomicMax(&sh->wmax[1], wmax_l[1]);
@@ -797,7 +683,6 @@ __device__ void generate_item(const FusedParams& P, SharedHdr* sh, int* cnt, int
   for (int e = tid; e < nf * T; e += kThreads) counts[(size_t)e * G + c] = min(cnt[e], P.cap);
   __syncthreads();
   if (tid == 0) {
-    if (sh->dmax) atomicMax(&S->dmax, sh->dmax);
     if (sh->amp) atomicMax(&S->amp, sh->amp);
     if (sh->wmax[0]) atomicMax(&S->wmax[0], sh->wmax[0]);
     if (sh->wmax[1]) atomicMax(&S->wmax[1], sh->wmax[1]);
@@ -847,7 +732,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // record segments (one per generate chunk) are pulled into shared memory with
 // TMA bulk copies (one elected thread, mbarrier transaction count), then
 // splatted from shared memory.
-template <int MODE, int PSF>
+template <int PSF>
 __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* rbuf, int* cells,
                             int pl, int t, uint32_t& bar_phase) {
   const int tid = threadIdx.x;
@@ -884,23 +769,7 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* 
     }
   }
   __syncthreads();
-  const int M = MODE == 0 ? __ldcg(&S->M) : 0;
-  int side;
-  float dmax = 0.f;
-  if (MODE == 0) {
-    dmax = __uint_as_float(__ldcg(&S->dmax));
-    // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
-    side = patch_side_exact(M == 0 ? P.g.d_hi : (double)dmax, P.g.patch_mult);
-    if (M == 0) dmax = (float)P.g.d_hi;
-  } else {
-    side = P.side_in[pl];
-  }
-  if (MODE == 0 && t == 0 && tid == 0) {
-    if (P.st_ppp) P.st_ppp[pl] = __ldcg(&S->ppp);
-    if (P.st_M) P.st_M[pl] = M;
-    if (P.st_side) P.st_side[pl] = side;
-    if (P.st_dmax) P.st_dmax[pl] = dmax;
-  }
+  const int side = P.side_in[pl];
   const int ty = t / P.tiles_x, tx = t - (t / P.tiles_x) * P.tiles_x;
   const int r0 = P.row_lo + ty * P.TH;
   const int nr = min(P.TH, P.row_hi - r0);
@@ -981,7 +850,7 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* 
       // last renderer retires the slot: reset it, then publish the new epoch
       S->gen_done = 0;
       S->render_done = 0;
-      S->dmax = S->amp = 0u;
+      S->amp = 0u;
       S->wmax[0] = S->wmax[1] = 0;
       __threadfence();
       atomicAdd(&S->epoch, 1);
@@ -993,8 +862,8 @@ __device__ void render_item(const FusedParams& P, SharedHdr* sh, int* acc, Rec* 
 // The kernel: persistent CTAs pulling ordered tickets.
 //   [gen items of pairs 0 .. L-1] then, per pair p: [render tiles of p][gen chunks of p + L]
 // ----------------------------------------------------------------------------
-template <int MODE, int PSF>
-__global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const FusedParams P) {
+template <int PSF>
+__global__ void __launch_bounds__(kThreads, 4) inject_render_kernel(const FusedParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   int* acc = reinterpret_cast<int*>(smem);
   const int acc_ints = P.AH * P.AS;
@@ -1017,15 +886,15 @@ __global__ void __launch_bounds__(kThreads, 4) fused_generate_kernel(const Fused
     const long long tk = sh->item;
     if (tk >= total) break;
     if (tk < pre) {
-      generate_item<MODE>(P, sh, cnt, (int)(tk / G), (int)(tk % G));
+      generate_item(P, sh, cnt, (int)(tk / G), (int)(tk % G));
     } else {
       const long long u = tk - pre;
       const int p = (int)(u / (T + G));
       const int r = (int)(u - (long long)p * (T + G));
       if (r < T) {
-        render_item<MODE, PSF>(P, sh, acc, rbuf, cells, p, r, bar_phase);
+        render_item<PSF>(P, sh, acc, rbuf, cells, p, r, bar_phase);
       } else if (p + L < NP) {
-        generate_item<MODE>(P, sh, cnt, p + L, r - T);
+        generate_item(P, sh, cnt, p + L, r - T);
       }
     }
   }

@@ -23,6 +23,8 @@
 #include "band.cuh"
 #include "histmatch.cuh"
 #include "refrng.cuh"
+#include "wide.cuh"
+#include "probes.cuh"
 
 namespace pgb {
 
@@ -114,17 +116,15 @@ __global__ void hiding_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, u
   }
 }
 
-template __global__ void fused_generate_kernel<1, kPsfPoint>(const FusedParams);
+template __global__ void inject_render_kernel<kPsfPoint>(const FusedParams);
 template __global__ void band_kernel<kPsfPoint>(const BandParams);
 template __global__ void band_kernel<kPsfErf>(const BandParams);
-template __global__ void band2_kernel<kPsfPoint>(const BandParams);
-template __global__ void fused_generate_kernel<1, kPsfErf>(const FusedParams);
+template __global__ void inject_render_kernel<kPsfErf>(const FusedParams);
 
 // ----------------------------------------------------------------------------
 // Host side: errors, workspace, plan, launch
 // ----------------------------------------------------------------------------
 thread_local std::string g_err;
-unsigned long long* g_timing = nullptr;   // PGB_PHASE_TIMING builds only
 std::atomic<long long> g_launches{0};
 
 struct Error {
@@ -168,7 +168,9 @@ int pow2_ceil(int v) {
 // Tiles are powers of two (shift-based binning) and at least 2*halo+1 wide
 // (a window spans <= 2x2 tiles); the accumulator carries a pad of 2*halo
 // (rounded to 4 ints) on every side so halo records need no clipping.
-Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes) {
+// `fits` (optional) receives whether the plan fits in shared memory; without
+// it an oversized plan throws (very large patch sides use the wide path).
+Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes, bool* fits = nullptr) {
   Plan p{};
   p.halo = halo;
   // generate items: >= 4 particles per thread, at most ~16 chunks (segments) per pair
@@ -209,7 +211,8 @@ Plan make_plan(int H_full, int rows, int W, long long n, int halo, int nframes) 
   long long cap = (long long)std::ceil(2.0 * lc + 10.0 * std::sqrt(lc) + 32.0);
   cap = std::min<long long>(cap, std::max<long long>(std::min<long long>(p.chunk, n), 1));
   p.cap = (int)((cap + 7) / 8 * 8);
-  PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
+  if (fits) *fits = p.smem <= kSmemMax && 2 * halo + 1 <= 127;   // Rec packs window sides in 8 bits
+  else PGB_REQUIRE(p.smem <= kSmemMax, "tile plan does not fit in shared memory");
   return p;
 }
 
@@ -219,23 +222,18 @@ struct DevWork {
   void* ctl = nullptr;        // ticket + slots + fills (memset per launch)
   size_t ctl_bytes = 0;
   int* overflow = nullptr;
-  // band generator workspace: ticket + pair headers + field bounds + cell prefixes
+  // band generator workspace: [two control heads | pair tables]
   void* band = nullptr;
   size_t band_bytes = 0;
-  // cross-launch prologue pipeline: table slot `pro_slot` holds the pair
-  // prologue of the launch described by `pro_key` (computed as the tail work
-  // of the previous launch on `pro_stream`)
-  bool pro_valid = false;
-  int pro_slot = 0;
+  unsigned band_gen = 0;      // bumped by every (re)allocation of `band`
   // two per-launch control heads [ticket | field bounds | flags]: a generate
   // launch uses one and zeroes the other for the next launch on the same
-  // stream (no memset node between back-to-back launches)
+  // stream (no memset node between back-to-back launches). The zero state is
+  // valid only for the allocation generation and head size it was made for.
   bool head_zero[2] = {false, false};
   int head_next = 0;
-  size_t head_bytes = 0;   // head size the zero flags refer to (it depends on pairs / fields)
-  cudaStream_t head_stream = nullptr;
-  cudaStream_t pro_stream = nullptr;
-  std::array<uint64_t, 16> pro_key{};
+  size_t head_bytes = 0;
+  unsigned head_gen = 0;
   // host-API staging
   void* stage = nullptr;
   size_t stage_bytes = 0;
@@ -265,21 +263,23 @@ DevWork& work_for(cudaStream_t stream) {
   return w;
 }
 
-void* ensure(void*& buf, size_t& have, size_t need) {
+// Grow-only device buffer; `gen` (optional) is bumped on every reallocation
+// (cudaMalloc may return the same address, so callers must not compare pointers).
+void* ensure(void*& buf, size_t& have, size_t need, unsigned* gen = nullptr) {
   if (need > have) {
     if (buf) PGB_CK(cudaFree(buf));
     buf = nullptr;
     PGB_CK(cudaMalloc(&buf, need));
     have = need;
+    if (gen) ++*gen;
   }
   return buf;
 }
 
 using KernelFn = void (*)(const FusedParams);
 
-KernelFn pick_kernel(int mode, int psf) {
-  (void)mode;
-  return psf == kPsfErf ? fused_generate_kernel<1, kPsfErf> : fused_generate_kernel<1, kPsfPoint>;
+KernelFn pick_kernel(int psf) {
+  return psf == kPsfErf ? inject_render_kernel<kPsfErf> : inject_render_kernel<kPsfPoint>;
 }
 
 int resident_ctas(KernelFn fn, size_t smem) {
@@ -299,7 +299,7 @@ int resident_ctas(KernelFn fn, size_t smem) {
 }
 
 void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
-  KernelFn fn = pick_kernel(P.mode, P.psf);
+  KernelFn fn = pick_kernel(P.psf);
   P.TH = pl.TH; P.TW = pl.TW; P.tiles_y = pl.tiles_y; P.tiles_x = pl.tiles_x; P.tiles = pl.tiles;
   P.th_shift = pl.th_shift; P.tw_shift = pl.tw_shift; P.cap = pl.cap; P.halo = pl.halo;
   P.cells_cap = pl.cells_cap; P.pad = pl.pad; P.AH = pl.AH; P.AS = pl.AS;
@@ -338,6 +338,32 @@ void launch_fused(FusedParams& P, const Plan& pl, cudaStream_t stream) {
 int grid_for(long long n, int block) {
   long long g = (n + block - 1) / block;
   return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 16));
+}
+
+// Oracle-mode render of one frame of pairs [0, pairs) without a tile plan
+// (wide.cuh): float64 reference arithmetic, 2^-32 integer accumulation.
+void wide_render(const InjFrame& fr, long long n, int pairs, const int* side_host, int H, int W, int row_lo,
+                 int row_hi, int psf, int out_mode, float bg, float sd, uint64_t seed, uint64_t batch,
+                 int64_t pair_base, int frame, void* out, cudaStream_t stream) {
+  DevWork& w = work_for(stream);
+  const size_t acc_bytes = (size_t)H * W * sizeof(unsigned long long);
+  unsigned long long* acc = static_cast<unsigned long long*>(ensure(w.ring, w.ring_bytes, acc_bytes));
+  const size_t esz = out_mode == kOutU16 ? 2 : 4;
+  for (int pl = 0; pl < pairs; ++pl) {
+    PGB_CK(cudaMemsetAsync(acc + (size_t)row_lo * W, 0, (size_t)(row_hi - row_lo) * W * 8, stream));
+    WideParams P{};
+    P.H = H; P.W = W; P.row_lo = row_lo; P.row_hi = row_hi;
+    P.n = n; P.pl = pl; P.side = side_host[pl]; P.psf = psf; P.fr = fr; P.acc = acc;
+    const long long warps = std::max<long long>(1, std::min<long long>(n, 148LL * 64));
+    wide_splat_kernel<<<(int)((warps + 7) / 8), 256, 0, stream>>>(P);
+    char* dst = static_cast<char*>(out) + (size_t)pl * H * W * esz;
+    const long long quads = ((long long)(row_hi - row_lo) * W + 7) / 4;
+    wide_store_kernel<<<grid_for(quads, 256), 256, 0, stream>>>(
+        acc, H, W, row_lo, row_hi, out_mode, bg, sd, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32),
+        (uint32_t)(pair_base + pl), (uint32_t)batch, frame, dst);
+    g_launches.fetch_add(2);
+    PGB_CK(cudaGetLastError());
+  }
 }
 
 uint64_t hide_threshold(double p) {
@@ -402,7 +428,6 @@ FusedParams base_params(int H, int W) {
   P.row_lo = 0;
   P.row_hi = H;
   P.out_pair_elems = (long long)H * W;
-  P.pairs_per_field = 1;
   return P;
 }
 
@@ -447,25 +472,31 @@ void cell_bits(int H, int W, int& sy, int& sx) {
 // Accumulator bytes per CTA such that two band CTAs fit on one SM: half the
 // SM's shared memory minus the per-block reservation, the kernel's static
 // shared memory and the BandShared control block (PGB_BAND_ACC_KB overrides).
+// Cached per device.
 size_t band_acc_budget() {
   if (const char* e = std::getenv("PGB_BAND_ACC_KB")) return (size_t)std::max(8, std::atoi(e)) * 1024;
-  static size_t cached = 0;
-  if (cached) return cached;
+  static std::map<int, size_t> cache;
   int dev = 0, per_sm = 0, reserved = 0;
   cudaFuncAttributes fa{}, fe{};
-  const bool ok = cudaGetDevice(&dev) == cudaSuccess &&
-                  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess &&
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 110 * 1024;   // no device (host-side planning): the B200 figure
+  }
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  const bool ok = cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess &&
                   cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) == cudaSuccess &&
                   cudaFuncGetAttributes(&fa, (const void*)band_kernel<kPsfPoint>) == cudaSuccess &&
                   cudaFuncGetAttributes(&fe, (const void*)band_kernel<kPsfErf>) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
-    return 110 * 1024;   // no device (host-side planning): the B200 figure
+    return 110 * 1024;
   }
   const long long st = (long long)std::max(fa.sharedSizeBytes, fe.sharedSizeBytes);
   const long long b = (long long)per_sm / 2 - reserved - st - (long long)sizeof(BandShared);
-  cached = (size_t)std::max<long long>(8 * 1024, b);
-  return cached;
+  const size_t v = (size_t)std::max<long long>(8 * 1024, b);
+  cache[dev] = v;
+  return v;
 }
 
 BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0) {
@@ -540,16 +571,14 @@ float amp_bound_of(const pgb_config* c) {
   return (float)(std::max(a, 1e-30) * (1.0 + 1e-6));
 }
 
-// Fill the band parameters shared by generate / sample_particles and run the
-// prologue (densities, maximum diameters, cell prefixes, field bounds).
 // Fill the band parameters shared by generate / sample_particles and lay out
-// the workspace; `launch` runs the standalone prologue kernel (densities,
-// maximum diameters, cell prefixes, field bounds), otherwise the band kernel
-// runs that work itself (inline_prologue).
+// the workspace. `standalone`: run the prologue kernel (densities, maximum
+// diameters, cell prefixes, field bounds) now (sample_particles path);
+// otherwise the band kernel runs that work itself as its first tickets.
 void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uint64_t batch,
                    int64_t pair_base, int pairs, const float* flows, int num_fields,
                    int pairs_per_field, const pgb_pair_stats* stats, cudaStream_t stream,
-                   bool launch) {
+                   bool standalone) {
   P.H = cfg->height;
   P.W = cfg->width;
   P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS; P.pad_rows = bp.pad_rows;
@@ -581,105 +610,59 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const size_t cof_bytes = (size_t)pairs * cof_stride(cfg->n_capacity) * sizeof(unsigned short);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
   DevWork& w = work_for(stream);
-  // [ticket | field bounds | ready flags] are zeroed per launch, then two
-  // table slots of [headers | prefixes | particle -> cell arrays]
+  // [ticket | field bounds | ready flags] are zeroed per launch (two heads),
+  // then the pair tables [headers | prefixes | particle -> cell arrays]
   const size_t head = up(256 + up(fb_bytes) + up(flag_bytes));
-  const size_t slot_bytes = up(hdr_bytes) + up(pre_bytes) + up(cof_bytes);
-  void* before = w.band;
-  char* base = static_cast<char*>(ensure(w.band, w.band_bytes, 2 * head + 2 * slot_bytes));
-  if (base != before || head != w.head_bytes) {
-    // new buffer or a different head size (pairs / fields changed): the heads'
-    // zero state and the cached prologue tables are no longer where they were
-    w.pro_valid = false;
+  const size_t table_bytes = up(hdr_bytes) + up(pre_bytes) + up(cof_bytes);
+  char* base = static_cast<char*>(ensure(w.band, w.band_bytes, 2 * head + table_bytes, &w.band_gen));
+  if (w.head_gen != w.band_gen || head != w.head_bytes) {
+    // new allocation (even at the same address) or a different head layout:
+    // the heads' zero state is unknown
     w.head_zero[0] = w.head_zero[1] = false;
     w.head_bytes = head;
+    w.head_gen = w.band_gen;
   }
-  int hsel = 0;
-  if (!launch) {
-    hsel = w.head_next;
-    if (!(w.head_zero[hsel] && w.head_stream == stream)) PGB_CK(cudaMemsetAsync(base + hsel * head, 0, head, stream));
-    P.zero_head = reinterpret_cast<int4*>(base + (1 - hsel) * head);
-    P.zero_head_n = (int)(head / 16);
-    w.head_zero[hsel] = false;
-    w.head_zero[1 - hsel] = true;   // zeroed by this launch
-    w.head_stream = stream;
-    w.head_next = 1 - hsel;
-  } else {
-    PGB_CK(cudaMemsetAsync(base, 0, head, stream));
-    w.head_zero[0] = false;
-  }
-  char* b = base + hsel * head;
-  char* slots = base + 2 * head;
-  P.ticket = reinterpret_cast<int*>(b);
-  P.fbound = reinterpret_cast<float2*>(b + 256);
-  int* flags = reinterpret_cast<int*>(b + 256 + up(fb_bytes));
-  auto slot_ptrs = [&](int k, PairHdr*& hdr, int*& pre, unsigned short*& cof) {
-    char* sb = slots + (size_t)k * slot_bytes;
-    hdr = reinterpret_cast<PairHdr*>(sb);
-    pre = reinterpret_cast<int*>(sb + up(hdr_bytes));
-    cof = reinterpret_cast<unsigned short*>(sb + up(hdr_bytes) + up(pre_bytes));
-  };
+  char* tables = base + 2 * head;
+  P.hdr = reinterpret_cast<PairHdr*>(tables);
+  P.prefix = reinterpret_cast<int*>(tables + up(hdr_bytes));
+  P.cell_of = reinterpret_cast<unsigned short*>(tables + up(hdr_bytes) + up(pre_bytes));
   // bounds only for the fields this pair range reads
   const int f_lo = (int)(pair_base / pairs_per_field);
   const int f_hi = (int)((pair_base + pairs - 1) / pairs_per_field);
   P.field_lo = f_lo;
   P.field_cnt = f_hi - f_lo + 1;
-  if (!launch) {
-    // everything the pair prologue depends on, plus the batch
-    auto key_of = [&](uint64_t bt) {
-      std::array<uint64_t, 16> k{};
-      auto dbits = [](double v) { uint64_t u; std::memcpy(&u, &v, 8); return u; };
-      k[0] = ((uint64_t)cfg->height << 32) | (uint32_t)cfg->width;
-      k[1] = (uint64_t)cfg->n_capacity;
-      k[2] = cfg->seed;
-      k[3] = dbits(cfg->ppp_lo); k[4] = dbits(cfg->ppp_hi);
-      k[5] = dbits(cfg->d_lo); k[6] = dbits(cfg->d_hi);
-      k[7] = dbits(cfg->patch_multiplier);
-      k[8] = ((uint64_t)bp.sy << 32) | (uint32_t)bp.sx;
-      k[9] = bt;
-      k[10] = (uint64_t)pair_base;
-      k[11] = (uint64_t)pairs;
-      k[12] = (uint64_t)slot_bytes;
-      k[13] = (uint64_t)head;
-      return k;
-    };
-    // opt-in (PGB_PIPELINE=1): measured slower on B200 at c2 -- the next batch's
-    // prologue work steals issue slots from the co-resident CTA's band work
-    const bool pipeline = std::getenv("PGB_PIPELINE") && std::atoi(std::getenv("PGB_PIPELINE")) != 0;
-    int cur = 0;
-    P.inline_pairs = 1;
-    if (pipeline && w.pro_valid && w.pro_stream == stream && w.pro_key == key_of(batch)) {
-      cur = w.pro_slot;
-      P.inline_pairs = 0;
-    }
-    slot_ptrs(cur, P.hdr, P.prefix, P.cell_of);
-    P.inline_prologue = 1;
+  if (!standalone) {
+    const int hsel = w.head_next;
+    if (!w.head_zero[hsel]) PGB_CK(cudaMemsetAsync(base + hsel * head, 0, head, stream));
+    P.zero_head = reinterpret_cast<int4*>(base + (1 - hsel) * head);
+    P.zero_head_n = (int)(head / 16);
+    w.head_zero[hsel] = false;
+    w.head_zero[1 - hsel] = true;   // zeroed by this launch (stream order)
+    w.head_next = 1 - hsel;
+    char* b = base + hsel * head;
+    P.ticket = reinterpret_cast<int*>(b);
+    P.fbound = reinterpret_cast<float2*>(b + 256);
+    int* flags = reinterpret_cast<int*>(b + 256 + up(fb_bytes));
     P.pair_ready = flags;
     P.fb_done = flags + pairs;
-    w.pro_valid = false;
-    if (pipeline && batch + 1 < (1ull << 32)) {
-      slot_ptrs(1 - cur, P.nx_hdr, P.nx_prefix, P.nx_cof);
-      P.nx_batch_lo = (uint32_t)(batch + 1);
-      w.pro_valid = true;
-      w.pro_slot = 1 - cur;
-      w.pro_stream = stream;
-      w.pro_key = key_of(batch + 1);
-    }
+    P.npro = (long long)pairs + (long long)P.field_cnt * kFieldBlocks;
     return;
   }
-  w.pro_valid = false;   // the standalone prologue overwrites slot 0
-  slot_ptrs(0, P.hdr, P.prefix, P.cell_of);
-  P.inline_prologue = 0;
+  // standalone prologue kernel: head 0, no readiness flags
+  PGB_CK(cudaMemsetAsync(base, 0, head, stream));
+  w.head_zero[0] = false;
+  P.ticket = reinterpret_cast<int*>(base);
+  P.fbound = reinterpret_cast<float2*>(base + 256);
+  P.pair_ready = nullptr;
+  P.fb_done = nullptr;
+  P.npro = 0;
   BandParams Q = P;
   const size_t psmem = std::min<size_t>(kSmemMax, (size_t)((std::max(ncell, 4) + 4) & ~3) * sizeof(int) +
                                                     ((size_t)cfg->n_capacity + 8) * sizeof(unsigned short));
   Q.pro_smem = (int)psmem;
-  static bool attr_set = false;
-  if (!attr_set) {
-    PGB_CK(cudaFuncSetAttribute((const void*)prologue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kSmemMax));
-    attr_set = true;
-  }
+  // the attribute is per device: set it on every call (cheap)
+  PGB_CK(cudaFuncSetAttribute((const void*)prologue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kSmemMax));
   // field blocks handle relative field (block - pairs) / kFieldBlocks
   Q.flows = P.flows + (size_t)f_lo * P.field_elems;
   Q.fbound = P.fbound + f_lo;
@@ -690,9 +673,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
 
 void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
                        const float* flows, int num_fields, int pairs_per_field, int out_mode,
-                       void* img1, void* img2, const pgb_pair_stats* stats, int32_t* bin_counts,
-                       cudaStream_t stream) {
-  (void)bin_counts;  // generate mode renders without record lists
+                       void* img1, void* img2, const pgb_pair_stats* stats, cudaStream_t stream) {
   validate_cfg(cfg);
   PGB_REQUIRE(pairs >= 0, "pairs must be >= 0");
   PGB_REQUIRE(flows != nullptr && num_fields >= 1 && pairs_per_field >= 1, "flows required");
@@ -704,63 +685,18 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
               "pair range exceeds the flow window (num_fields * pairs_per_field)");
   if (pairs == 0) return;
   const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
-  BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
-  // experimental warp-specialised kernel (PGB_BAND2=1): one CTA per SM, two
-  // accumulator sets; full-width tiles only
-  bool b2 = std::getenv("PGB_BAND2") && std::atoi(std::getenv("PGB_BAND2")) != 0 && cfg->psf == PGB_PSF_POINT;
-  size_t b2_smem = 0;
-  if (b2) {
-    cudaFuncAttributes fa{};
-    PGB_CK(cudaFuncGetAttributes(&fa, (const void*)band2_kernel<kPsfPoint>));
-    const long long per_set = ((long long)kSmemMax - (long long)sizeof(BandShared) - (long long)fa.sharedSizeBytes) / 2;
-    const BandPlan b2p = make_band_plan(cfg->height, cfg->width, halo, (size_t)std::max<long long>(8192, per_set));
-    if (b2p.TW == cfg->width && b2p.AS == cfg->width) {
-      bp = b2p;
-      b2_smem = sizeof(BandShared) + 2 * (((size_t)(2 * bp.TH + bp.pad_rows) * bp.AS + 8) * 4);
-    } else {
-      b2 = false;
-    }
-  }
+  const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
   BandParams P{};
-  band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats, stream,
-                false);
-  if (b2 && P.nx_hdr) {
-    // band2 has no next-batch tail work: keep the prologue cache invalid
-    P.nx_hdr = nullptr;
-    work_for(stream).pro_valid = false;
-  }
+  band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats, stream, false);
   P.out_mode = out_mode;
   P.bg_offset = (float)cfg->bg_offset;
   P.noise_std = (float)cfg->noise_std;
   P.out[0] = img1;
   P.out[1] = img2;
-  if (const char* e = std::getenv("PGB_ABLATE")) P.ablate = std::atoi(e);   // debug timing only
-  // opt-in (PGB_TMA_STORE=1): the bulk store's read wait stalls the CTA; the
-  // per-thread streaming stores measured faster at c2
-  P.tma_store = (std::getenv("PGB_TMA_STORE") && std::atoi(std::getenv("PGB_TMA_STORE")) != 0) ? 1 : 0;
-#ifdef PGB_PHASE_TIMING
-  {
-    static unsigned long long* tbuf = nullptr;
-    if (!tbuf) PGB_CK(cudaMalloc(&tbuf, (size_t)148 * 8 * kBandWarps * 5 * 8));
-    PGB_CK(cudaMemsetAsync(tbuf, 0, (size_t)148 * 8 * kBandWarps * 5 * 8, stream));
-    P.timing = tbuf;
-    g_timing = tbuf;
-  }
-#endif
   BandFn fn = cfg->psf == PGB_PSF_ERF ? band_kernel<kPsfErf> : band_kernel<kPsfPoint>;
-  int ctas = 0;
-  if (b2) {
-    int dev = 0, sms = 0;
-    PGB_CK(cudaGetDevice(&dev));
-    PGB_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PGB_CK(cudaFuncSetAttribute((const void*)band2_kernel<kPsfPoint>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kSmemMax));
-    ctas = sms;
-  } else {
-    ctas = band_resident_ctas(fn, bp.smem);
-  }
-  // static schedule over `grid` CTAs: whole rounds of (pair, tile) items, then
-  // the remaining tiles split into row parts (>= 8 rows) spread over the grid
+  const int ctas = band_resident_ctas(fn, bp.smem);
+  // whole rounds of (pair, tile) items over the resident CTAs, then the
+  // remaining tiles split into row parts (>= 8 rows) spread over the grid
   const long long F = (long long)pairs * bp.tiles;
   const int smax = std::max(1, bp.TH / 8);
   long long G = ctas, R = 0, rem = 0;
@@ -774,12 +710,12 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   if (rem > 0) sp = (int)std::max<long long>(1, std::min<long long>(smax, ctas / rem));
   if (std::getenv("PGB_NO_SPLIT")) sp = 1;
   if (F < ctas) G = std::max<long long>(1, std::min<long long>(ctas, rem * sp));
-  P.split_base = R * G;
+  // PGB_GRID caps the grid (tests: forward progress with few resident CTAs)
+  if (const char* e = std::getenv("PGB_GRID")) G = std::max<long long>(1, std::min<long long>(G, std::atoll(e)));
+  P.split_base = R * (F >= ctas ? (long long)ctas : G);
   P.split_s = sp;
-  P.total_items = R * G + rem * sp;
-  const int grid = (int)G;
-  if (b2) band2_kernel<kPsfPoint><<<grid, kB2Block, b2_smem, stream>>>(P);
-  else fn<<<grid, kBandBlock, bp.smem, stream>>>(P);
+  P.total_items = P.split_base + rem * sp;
+  fn<<<(int)G, kBandBlock, bp.smem, stream>>>(P);
   g_launches.fetch_add(1);
 }
 
@@ -798,15 +734,6 @@ int pgb_patch_side(double max_diameter, double multiplier) {
 }
 
 int64_t pgb_launch_count(void) { return g_launches.load(); }
-
-// Debug (PGB_PHASE_TIMING builds): copy the per-CTA/warp phase counters of the
-// last generate launch; returns the number of uint64 written (0 otherwise).
-int pgb_debug_phase_timing(unsigned long long* out, int cap) {
-  if (!g_timing || !out) return 0;
-  const int n = std::min(cap, 148 * 8 * kBandWarps * 5);
-  if (cudaMemcpy(out, g_timing, (size_t)n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
-  return n;
-}
 
 int pgb_plan(int height, int width, int64_t n_per_pair, double ppp_hi, int halo, int frames,
              pgb_plan_info* info) {
@@ -838,10 +765,17 @@ int pgb_splat_accumulate_dev(const double* pos, const float* i0, const float* si
     P.pairs = 1;
     P.psf = psf;
     P.out_mode = kOutAccum;
-    P.mode = 1;
     P.nframes = 1;
     P.inj[0] = InjFrame{pos, i0, sigma_x, sigma_y, rho, mask};
     int* side_dev = nullptr;
+    bool fits = false;
+    const Plan pl = make_plan(height, row_stop - row_start, width, n, side / 2, 1, &fits);
+    if (!fits) {
+      wide_render(P.inj[0], n, 1, &side, height, width, row_start, row_stop, psf, kOutAccum, 0.f, 0.f, 0, 0, 0,
+                  1, out, (cudaStream_t)stream);
+      PGB_CK(cudaStreamSynchronize((cudaStream_t)stream));
+      return;
+    }
     DevWork& w = work_for((cudaStream_t)stream);
     // side lives in the staging buffer head (4 bytes)
     ensure(w.stage, w.stage_bytes, 256);
@@ -849,7 +783,6 @@ int pgb_splat_accumulate_dev(const double* pos, const float* i0, const float* si
     PGB_CK(cudaMemcpyAsync(side_dev, &side, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
     P.side_in = side_dev;
     P.out[0] = out;
-    const Plan pl = make_plan(height, row_stop - row_start, width, n, side / 2, 1);
     launch_fused(P, pl, (cudaStream_t)stream);
     PGB_CK(cudaGetLastError());
     // the side staging slot is reused: keep the host value alive until the copy ran
@@ -913,6 +846,20 @@ int pgb_render_pairs_dev(const pgb_particles* frame1, const pgb_particles* frame
       PGB_REQUIRE(side_per_pair[i] >= 1, "side must be >= 1");
       smax = std::max(smax, side_per_pair[i]);
     }
+    bool fits = false;
+    const Plan pl = make_plan(height, height, width, n_per_pair, smax / 2, 2, &fits);
+    if (!fits) {
+      // very large patch sides: no tile plan; bin_counts / tiles are undefined
+      if (tiles_out) *tiles_out = 0;
+      const InjFrame f1{frame1->pos, frame1->i0, frame1->sigma_x, frame1->sigma_y, frame1->rho, frame1->mask};
+      const InjFrame f2{frame2->pos, frame2->i0, frame2->sigma_x, frame2->sigma_y, frame2->rho, frame2->mask};
+      wide_render(f1, n_per_pair, pairs, side_per_pair, height, width, 0, height, psf, out_mode, (float)bg_offset,
+                  (float)noise_std, seed, batch, pair_base, 1, out1, (cudaStream_t)stream);
+      wide_render(f2, n_per_pair, pairs, side_per_pair, height, width, 0, height, psf, out_mode, (float)bg_offset,
+                  (float)noise_std, seed, batch, pair_base, 2, out2, (cudaStream_t)stream);
+      PGB_CK(cudaStreamSynchronize((cudaStream_t)stream));
+      return;
+    }
     DevWork& w = work_for((cudaStream_t)stream);
     ensure(w.stage, w.stage_bytes, (size_t)pairs * sizeof(int) + 256);
     int* side_dev = static_cast<int*>(w.stage);
@@ -927,21 +874,34 @@ int pgb_render_pairs_dev(const pgb_particles* frame1, const pgb_particles* frame
     P.out_mode = out_mode;
     P.bg_offset = (float)bg_offset;
     P.noise_std = (float)noise_std;
-    P.mode = 1;
     P.nframes = 2;
-    P.g.k0 = (uint32_t)(seed & 0xffffffffu);
-    P.g.k1 = (uint32_t)(seed >> 32);
+    P.k0 = (uint32_t)(seed & 0xffffffffu);
+    P.k1 = (uint32_t)(seed >> 32);
     P.inj[0] = InjFrame{frame1->pos, frame1->i0, frame1->sigma_x, frame1->sigma_y, frame1->rho, frame1->mask};
     P.inj[1] = InjFrame{frame2->pos, frame2->i0, frame2->sigma_x, frame2->sigma_y, frame2->rho, frame2->mask};
     P.side_in = side_dev;
     P.out[0] = out1;
     P.out[1] = out2;
     P.bin_counts = bin_counts;
-    const Plan pl = make_plan(height, height, width, n_per_pair, smax / 2, 2);
     if (tiles_out) *tiles_out = pl.tiles;
     launch_fused(P, pl, (cudaStream_t)stream);
     PGB_CK(cudaGetLastError());
     PGB_CK(cudaStreamSynchronize((cudaStream_t)stream));  // side staging reuse
+  });
+}
+
+int pgb_render_oracle_dev(const double* pos, const float* i0, const float* sigma_x,
+                          const float* sigma_y, const float* rho, const unsigned char* mask,
+                          int64_t n, int height, int width, float* out, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(height > 0 && width > 0 && height < 65536 && width < 65536, "bad image size");
+    PGB_REQUIRE(n >= 0, "bad particle count");
+    PGB_REQUIRE(out != nullptr && (n == 0 || (pos && i0 && sigma_x && sigma_y && rho && mask)), "null pointer");
+    dim3 grid((unsigned)((width + 15) / 16), (unsigned)((height + 15) / 16));
+    oracle_render_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(pos, i0, sigma_x, sigma_y, rho, mask, n,
+                                                                  height, width, out);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
   });
 }
 
@@ -1061,8 +1021,9 @@ int pgb_generate_batch_dev(const pgb_config* cfg, uint64_t batch, int64_t pair_b
                            void* img1, void* img2, const pgb_pair_stats* stats,
                            int32_t* bin_counts, void* stream) {
   return guarded([&] {
+    (void)bin_counts;   // generate mode renders without record lists
     generate_dev_impl(cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, out_mode,
-                      img1, img2, stats, bin_counts, (cudaStream_t)stream);
+                      img1, img2, stats, (cudaStream_t)stream);
     PGB_CK(cudaGetLastError());
   });
 }
@@ -1094,7 +1055,7 @@ int pgb_generate_batch(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
     cudaStream_t s = nullptr;
     PGB_CK(cudaMemcpyAsync(d_flow, flows, flow_bytes, cudaMemcpyHostToDevice, s));
     generate_dev_impl(cfg, batch, pair_base, pairs, d_flow, num_fields, pairs_per_field, out_mode,
-                      d_img1, d_img2, stats ? &dst : nullptr, nullptr, s);
+                      d_img1, d_img2, stats ? &dst : nullptr, s);
     PGB_CK(cudaMemcpyAsync(img1, d_img1, img_bytes, cudaMemcpyDeviceToHost, s));
     PGB_CK(cudaMemcpyAsync(img2, d_img2, img_bytes, cudaMemcpyDeviceToHost, s));
     if (stats) {
@@ -1159,6 +1120,15 @@ int pgb_apply_hiding_dev(int64_t n, uint64_t seed, uint64_t batch, int64_t gpair
     hiding_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
         (int)n, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), (uint32_t)gpair,
         (uint32_t)batch, hide_threshold(p_hide), active, visible1, visible2);
+    g_launches.fetch_add(1);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
+int pgb_probe_ex2_dev(int blocks, int iters, float* sink, void* stream) {
+  return guarded([&] {
+    PGB_REQUIRE(blocks > 0 && iters > 0 && sink != nullptr, "bad probe arguments");
+    ex2_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters);
     g_launches.fetch_add(1);
     PGB_CK(cudaGetLastError());
   });

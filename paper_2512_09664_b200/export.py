@@ -84,9 +84,22 @@ def pair_paths(out_dir: str, ext: str, batch: int, pair: int) -> list[str]:
     return [f"{stem}_a.{ext}", f"{stem}_b.{ext}", f"{stem}_flow.flo"]
 
 
+def _pair_start(batch) -> int:
+    """Global index of the batch's first pair (a shard under torch.distributed)."""
+    pr = getattr(batch, "pair_range", None)
+    return pr.start if pr is not None and len(pr) else 0
+
+
+def _is_shard(cfg, batch) -> bool:
+    pr = getattr(batch, "pair_range", None)
+    return pr is not None and len(pr) > 0 and len(pr) != cfg.batch_size
+
+
 def sidecar(cfg, batch) -> dict:
-    """Per-batch parameter sidecar (schema 1, reference cli.py:62-88)."""
+    """Per-batch parameter sidecar (schema 1, reference cli.py:62-88); pair
+    indices are global (a shard's pairs keep their place in the batch)."""
     pairs = []
+    start = _pair_start(batch)
     for i, p in enumerate(batch.params):
         m = int(p.active_count)
         d = np.asarray(p.diameters)[:m]
@@ -94,7 +107,7 @@ def sidecar(cfg, batch) -> dict:
         rho = np.asarray(p.rhos)[:m]
         d_max = float(d.max()) if m else cfg.diameter_range[1]
         pairs.append({
-            "pair_index": i,
+            "pair_index": start + i,
             "seeding_density": float(p.seeding_density),
             "active_count": m,
             "allocated_count": int(np.asarray(p.diameters).shape[0]),
@@ -162,7 +175,9 @@ class DatasetWriter:
         # the sidecar and flows need host data anyway: materialise them here
         meta = sidecar(self.cfg, batch)
         flows = list(batch.flow_fields)
-        self._q.put((batch.batch_index, h1, h2, (e1, e2), flows, meta))
+        pr = getattr(batch, "pair_range", None)
+        part = (pr.start, pr.stop) if _is_shard(self.cfg, batch) else None
+        self._q.put((batch.batch_index, h1, h2, (e1, e2), flows, meta, _pair_start(batch), part))
 
     def _run(self) -> None:
         writer = write_png16 if self.png else write_raw_f32
@@ -172,7 +187,7 @@ class DatasetWriter:
                 return
             if self._err is not None:
                 continue
-            b, h1, h2, events, flows, meta = item
+            b, h1, h2, events, flows, meta, start, part = item
             written: list[str] = []
             try:
                 for ev in events:
@@ -181,7 +196,7 @@ class DatasetWriter:
                 a1 = h1.numpy() if isinstance(h1, torch.Tensor) else h1
                 a2 = h2.numpy() if isinstance(h2, torch.Tensor) else h2
                 for i in range(a1.shape[0]):
-                    pa, pb, pf = pair_paths(self.out_dir, self.ext, b, i)
+                    pa, pb, pf = pair_paths(self.out_dir, self.ext, b, start + i)
                     writer(pa, a1[i])
                     written.append(pa)
                     writer(pb, a2[i])
@@ -189,7 +204,9 @@ class DatasetWriter:
                     if flows:
                         write_flo_file(pf, flows[i])
                         written.append(pf)
-                path = os.path.join(self.out_dir, f"params_{b:06d}.json")
+                # a shard writes its part of the sidecar; merge_sidecars() joins them
+                name = f"params_{b:06d}.json" if part is None else f"params_{b:06d}.part{part[0]:05d}-{part[1]:05d}.json"
+                path = os.path.join(self.out_dir, name)
                 with open(path, "w", encoding="utf-8") as fh:
                     json.dump(meta, fh, sort_keys=True, indent=1)
                     fh.write("\n")
@@ -217,15 +234,54 @@ class DatasetWriter:
         self.close()
 
 
+def merge_sidecars(out_dir: str) -> int:
+    """Join the per-shard sidecar parts of every batch into ``params_<b>.json``
+    (pairs ordered by global index) and delete the parts. Returns the number
+    of merged batches."""
+    import glob
+    import re
+
+    groups: dict[str, list[str]] = {}
+    for path in glob.glob(os.path.join(out_dir, "params_*.part*.json")):
+        m = re.match(r"(params_\d+)\.part\d+-\d+\.json$", os.path.basename(path))
+        if m:
+            groups.setdefault(m.group(1), []).append(path)
+    for stem, parts in groups.items():
+        docs = []
+        for path in sorted(parts):
+            with open(path, encoding="utf-8") as fh:
+                docs.append(json.load(fh))
+        merged = dict(docs[0])
+        merged["pairs"] = sorted((p for d in docs for p in d["pairs"]), key=lambda p: p["pair_index"])
+        with open(os.path.join(out_dir, stem + ".json"), "w", encoding="utf-8") as fh:
+            json.dump(merged, fh, sort_keys=True, indent=1)
+            fh.write("\n")
+        for path in parts:
+            os.remove(path)
+    return len(groups)
+
+
 def generate_dataset(cfg, batches: int, out_dir: str, start_batch: int = 0) -> dict:
     """``pivgen generate`` (reference cli.py:91-131): ``batches`` batches into
-    ``out_dir`` in the reference layout. Returns counts and wall time."""
+    ``out_dir`` in the reference layout. Returns counts and wall time.
+
+    Under torch.distributed every rank writes its shard of each batch (global
+    pair indices in file names and sidecar); after a barrier rank 0 merges the
+    sidecar parts. ``pairs`` counts this rank's pairs, ``pairs_total`` the job's."""
     from .pipeline import Sampler
 
     t0 = time.perf_counter()
     total = 0
     with DatasetWriter(cfg, out_dir) as w, Sampler(cfg, start_batch=start_batch, max_batches=batches) as s:
+        shard = len(s.pair_range)
         for batch in s:
             w.submit(batch)
-            total += cfg.batch_size
-    return {"pairs": total, "batches": batches, "dir": out_dir, "seconds": time.perf_counter() - t0}
+            total += shard
+    dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
+    if dist_on and torch.distributed.get_world_size() > 1:
+        torch.distributed.barrier()
+        if torch.distributed.get_rank() == 0:
+            merge_sidecars(out_dir)
+        torch.distributed.barrier()
+    return {"pairs": total, "pairs_total": cfg.batch_size * batches, "batches": batches, "dir": out_dir,
+            "seconds": time.perf_counter() - t0}

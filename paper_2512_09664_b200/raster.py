@@ -1,7 +1,8 @@
 """Rendering on the GPU: splat, finalize, quantisation (reference raster.py).
 
-Every image is produced by the fused cluster kernel (csrc/fused.cuh) through
-the C ABI; the host functions here only move arrays and choose modes. Pixel
+Oracle-mode images (caller-supplied particles) come from the inject kernel
+(csrc/fused.cuh; csrc/wide.cuh for patch sides too large for its tile plan)
+through the C ABI; the host functions here only move arrays and choose modes. Pixel
 values accumulate as exact integers in 2^-22 units, so results do not depend
 on tiling or banding (the reference guarantees band-independence by fixed
 summation order, raster.py:108-126); they agree with the reference's float32
@@ -94,13 +95,21 @@ def splat_accumulate(pos, i0, sigma_x, sigma_y, rho, mask, side, out, row_start,
     m = to_dev(mask, torch.uint8, dev)
     if any(a.numel() < n for a in args) or m.numel() < n:
         raise ValueError("per-particle arrays are shorter than pos")
-    target = out if is_tensor else torch.from_numpy(np.asarray(out)).to(dev)
+    r0, r1 = max(0, int(row_start)), min(height, int(row_stop))
+    if is_tensor:
+        target = out
+    else:
+        # only the band's rows travel (in and back): concurrent calls on
+        # disjoint bands of one image never overwrite each other's rows
+        # (the reference's pool of splat_band jobs, raster.py:116-124)
+        target = torch.zeros((height, width), dtype=torch.float32, device=dev)
+        if r1 > r0:
+            target[r0:r1].copy_(torch.from_numpy(np.asarray(out)[r0:r1]))
     _lib.call("pgb_splat_accumulate_dev", p.data_ptr(), args[0].data_ptr(), args[1].data_ptr(),
               args[2].data_ptr(), args[3].data_ptr(), m.data_ptr(), n, int(side),
-              target.data_ptr(), height, width, int(row_start), int(row_stop),
-              _lib.PSF_CODES[psf], stream_ptr(dev))
-    if not is_tensor:
-        np.copyto(out, target.cpu().numpy())
+              target.data_ptr(), height, width, r0, r1, _lib.PSF_CODES[psf], stream_ptr(dev))
+    if not is_tensor and r1 > r0:
+        np.copyto(out[r0:r1], target[r0:r1].cpu().numpy())
 
 
 def splat_band(pset: ParticleSet, frame: int, out, side: int, row_start: int, row_stop: int) -> None:
@@ -123,10 +132,20 @@ def splat(pset: ParticleSet, frame: int, height: int, width: int, side: int,
 
 
 def render_oracle(pset: ParticleSet, frame: int, height: int, width: int) -> np.ndarray:
-    """Untruncated full-image render (raster.py:129-151): the same kernel with a
-    window covering the whole image."""
-    side = 2 * max(height, width) + 1
-    return splat(pset, frame, height, width, side)
+    """Untruncated full-image render (raster.py:129-151): every masked particle
+    at every pixel, float64, summed in particle-index order, rounded to float32
+    once (pgb_render_oracle_dev). O(N H W): bounds the splat's truncation."""
+    dev = cuda_device()
+    pos, app, _ = _frame(pset, frame)
+    p = to_dev(pos, torch.float64, dev)
+    n = p.shape[0]
+    args = [to_dev(a, torch.float32, dev) for a in (app.i0, app.sigma_x, app.sigma_y, app.rho)]
+    m = to_dev(contribution_mask(pset, frame), torch.uint8, dev)
+    out = torch.empty((height, width), dtype=torch.float32, device=dev)
+    _lib.call("pgb_render_oracle_dev", p.data_ptr(), args[0].data_ptr(), args[1].data_ptr(),
+              args[2].data_ptr(), args[3].data_ptr(), m.data_ptr(), n, height, width, out.data_ptr(),
+              stream_ptr(dev))
+    return out.cpu().numpy()
 
 
 def _noise_args(noise: NoiseConfig):

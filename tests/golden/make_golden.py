@@ -94,12 +94,87 @@ def main() -> None:
     print("wrote", path, os.path.getsize(path), "bytes,", len(names), "cases")
 
     make_histmatch(raster)
+    make_full()
 
     exe = os.path.join(ROOT, "oracle", "_ref", "philox_curand_check")
     txt = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
     with open(os.path.join(HERE, "philox_curand.txt"), "w") as fh:
         fh.write(txt)
     print("wrote philox_curand.txt")
+
+
+# BASELINE-size cases and the wide-window / untruncated
+# oracle cases. Full particle sets and images are too large to commit: the
+# fixture holds each case's config, particle checksums, image statistics and
+# 128 x 128 crops of the reference images; the GPU tests regenerate the
+# particles with the live reference (oracle/_ref) and check them against the
+# checksums, so the fixture pins the live run.
+FULL_CASES = [
+    # name, H, W, ppp, d_range, rho_range, sigma_std, i0_std, hide, seed, crop (r0, c0)
+    ("c3_1024", 1024, 1024, (0.1, 0.1), (1.0, 4.0), (-0.5, 0.5), 0.05, 0.05, 0.05, 2, (448, 512)),
+    ("c4_512", 512, 512, (0.06, 0.06), (0.8, 1.2), (0.0, 0.0), 0.0, 0.05, 0.05, 4, (192, 320)),
+    ("wide_96x128", 96, 128, (0.004, 0.004), (10.0, 25.0), (-0.3, 0.3), 0.0, 0.0, 0.0, 6, (0, 0)),
+]
+CROP = 128
+
+
+def full_case_particles(pv, name, H, W, ppp, dr, rr, ss, si, hide, seed):
+    """Reference particles of pair 0, batch 0 (pipeline.py:285-295) in the vortex flow."""
+    from pivgen import config, flowfield, particles, raster
+    from pivgen.rng import pair_key
+
+    field = flowfield.from_function(vortex(H, W), H, W)
+    cfg = config.GeneratorConfig(image_height=H, image_width=W, seeding_density_range=ppp,
+                                 diameter_range=dr, rho_range=rr, frame2_sigma_std=ss,
+                                 frame2_intensity_std=si, hide_probability=hide, seed=seed)
+    key = pair_key(seed, 0, 0)
+    ps, params = particles.sample_particles(key, cfg)
+    particles.advect(ps, field)
+    ps.app2 = particles.perturb_frame2(key, ps.app1, cfg)
+    particles.apply_hiding(key, ps, cfg.hide_probability)
+    m = params.active_count
+    dmax = float(params.diameters[:m].max()) if m else cfg.diameter_range[1]
+    side = raster.patch_side(dmax, cfg.patch_multiplier)
+    return cfg, key, ps, side
+
+
+def particle_checksum(ps) -> np.ndarray:
+    """float64 sums that change with any particle bit that matters."""
+    vals = []
+    for pos, app in ((ps.pos1, ps.app1), (ps.pos2, ps.app2)):
+        vals += [float(np.sum(pos[:, 0])), float(np.sum(pos[:, 1])), float(np.sum(app.i0, dtype=np.float64)),
+                 float(np.sum(app.sigma_x, dtype=np.float64)), float(np.sum(app.rho, dtype=np.float64))]
+    vals += [float(np.sum(ps.visible1)), float(np.sum(ps.visible2)), float(np.sum(ps.active))]
+    return np.array(vals)
+
+
+def make_full() -> None:
+    pv = reference.load()
+    from pivgen import config, raster
+    from pivgen.rng import STREAM_NOISE
+
+    out = {}
+    for name, H, W, ppp, dr, rr, ss, si, hide, seed, (r0, c0) in FULL_CASES:
+        cfg, key, ps, side = full_case_particles(pv, name, H, W, ppp, dr, rr, ss, si, hide, seed)
+        out[f"{name}/args"] = np.array([H, W, seed, side, r0, c0])
+        out[f"{name}/ranges"] = np.array([*ppp, *dr, *rr, ss, si, hide])
+        out[f"{name}/checksum"] = particle_checksum(ps)
+        for f in (1, 2):
+            raw = raster.splat(ps, f, H, W, side)
+            fin = raster.finalize(raw, config.NoiseConfig(background_offset=0.05),
+                                  key.with_stream(STREAM_NOISE, lane=f))
+            for kind, img in (("raw", raw), ("fin", fin)):
+                out[f"{name}/{kind}{f}_crop"] = img[r0:r0 + CROP, c0:c0 + CROP]
+                out[f"{name}/{kind}{f}_stats"] = np.array([img.astype(np.float64).sum(),
+                                                          (img.astype(np.float64) ** 2).sum(), img.max()])
+            if name.startswith("wide"):
+                # small image: keep the reference's untruncated render_oracle too
+                out[f"{name}/oracle{f}"] = raster.render_oracle(ps, f, H, W)
+                out[f"{name}/raw{f}"] = raw
+    out["names"] = np.array([c[0] for c in FULL_CASES])
+    path = os.path.join(HERE, "ref_full.npz")
+    np.savez_compressed(path, **out)
+    print("wrote", path, os.path.getsize(path), "bytes")
 
 
 def make_histmatch(raster) -> None:
@@ -140,4 +215,7 @@ def make_histmatch(raster) -> None:
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "full":
+        make_full()
+    else:
+        main()
