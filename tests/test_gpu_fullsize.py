@@ -138,6 +138,8 @@ def _ref_splat(args, H, W):
 @pytest.mark.parametrize("name", ["c3_1024", "c4_512", "wide_96x128"])
 def test_inject_full_size_vs_reference(pg, full, name):
     from paper_2512_09664_b200 import _lib
+
+    reference.load()
     from pivgen import config, raster
     from pivgen.rng import STREAM_NOISE, pair_key
 
