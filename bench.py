@@ -354,6 +354,10 @@ def run_ours(args):
     cfg = make_cfg(pg, name, global_batch)
     lib = _lib.load()
     ncfg = native_config(cfg)
+    law = pg.generation_law(cfg)
+    kernel_label = ("pgb::pair_kernel<PSF, REC> (one thread-block cluster per image pair, DSMEM record "
+                    "exchange; one launch per batch)" if law == "pair" else
+                    "pgb::band_kernel<PSF> (screen-tile items, in-kernel prologue; one launch per batch)")
     field = pg.from_function(vortex(H, W) if CONFIGS[name][5] == "vortex" else uniform, H, W)
     flows = field.to_device(dev).unsqueeze(0).contiguous()
     u16 = False
@@ -469,7 +473,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
-                         "kernel": "pgb::band_kernel<PSF> (one launch per batch; in-kernel prologue)",
+                         "kernel": kernel_label,
                          "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy burst)"},
             "roofline_sfu": sfu_roofline(name, value, clk, world),
             "e2e": e2e_line(e2e_value, h2d, d2h, global_batch, world),

@@ -1,0 +1,449 @@
+// pair.cuh -- one thread-block cluster per image pair (images that fit in a
+// cluster's shared memory; the band kernel handles larger ones).
+//
+// Replaces the body of Sampler._render_batch (reference pipeline.py:278-329)
+// for such images: sample_particles / perturb_frame2 / advect / apply_hiding
+// (particles.py:61-147), patch_side with the pair's maximum diameter
+// (raster.py:30-38, pipeline.py:291-294), splat (raster.py:108-126 ->
+// _native.pyx:14-66), finalize (raster.py:154-161), quantize_u16
+// (export.py:19-20).
+//
+// Design (B200-first):
+//   * A cluster of C CTAs owns one pair at a time; CTA k owns image rows
+//     [k RB, (k + 1) RB) of both frames as an int32 fixed-point accumulator
+//     in its shared memory. The C CTAs together hold the whole pair on chip.
+//   * Phase A: the cluster's threads generate the M particles (index-strided,
+//     each exactly once: Philox4x32-10 keyed by (particle, pair, batch,
+//     stream), positions iid uniform over the image -- the reference's law,
+//     particles.py:72-76 -- diameters iid uniform, advection). Every
+//     particle-frame whose window reaches a CTA's rows becomes a 16-byte
+//     (32 with correlation / sigma jitter) record stored straight into that
+//     CTA's shared-memory inbox over DSMEM (st.shared::cluster): private
+//     per-source regions, local slot counters, no remote atomics. Regions
+//     that fill up spill to an L2-resident global buffer (exact, just slower).
+//   * cluster barrier (release/acquire): the inbox, its counts and the other
+//     CTAs' maximum diameters are visible. The pair's patch side follows from
+//     the maximum diameter -- known now because every particle was generated.
+//   * Phase B: each CTA splats its inbox into its rows (integer shared-memory
+//     atomics: associative, so every pixel is bit-identical for any schedule,
+//     cluster size or GPU count), then arrives on the cluster barrier (its
+//     inbox may be refilled) and
+//   * Phase C: finalizes and stores its rows of both frames (offset, Philox
+//     noise, clamp, optional uint16; 128-bit streaming stores), zeroing the
+//     accumulator, while the barrier completes.
+// No prologue, no histogram, no regeneration: every particle is generated
+// once and never leaves the chip; HBM traffic = the images.
+#pragma once
+#include "band.cuh"
+
+namespace pgb {
+
+constexpr int kPairThreads = kBandThreads;   // band_store() strides kBandThreads threads
+constexpr int kPairMaxCluster = 8;           // portable cluster size
+
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// Shared-memory address of the same variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t cl_map(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(local)),
+               "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void cl_st1(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// One generated particle of the pair law: frame-1 position X / 2^17 (Q17,
+// uniform over [0, W) x [0, H), particles.py:72-76) kept as Q20; frame-2
+// position = frame-1 + rint(flow * 2^20) (64-bit: far displacements stay exact).
+struct PairPart {
+  int xq1, yq1;
+  long long xq2, yq2;
+  float d, sig;
+  Look lk;
+};
+
+__device__ __forceinline__ void pair_particle(const GenCfg& g, const RngKey& key, int gi,
+                                              const float2* __restrict__ flow, PairPart& o) {
+  const uint4 a = philox_rk(make_uint4((uint32_t)gi, key.pair, key.batch, kTagParticleA), g.rk);
+  const uint32_t X = cell_coord(0u, a.x, g.W, 0);
+  const uint32_t Y = cell_coord(0u, a.y, g.H, 0);
+  // advect (particles.py:129-136): bilinear, edge-clamped (flowfield.py:207-232);
+  // fcx <= W - 2 and fcy <= H - 2, so the nodes are fp[0], fp[1], fp[W], fp[W + 1]
+  int fcx, fcy;
+  float tx, ty;
+  fixed_cell(X, g.W, fcx, tx);
+  fixed_cell(Y, g.H, fcy, ty);
+  const float2* fp = flow + (fcy * g.W + fcx);
+  const float2* fq = fp + g.W;
+  const float2 q00 = __ldg(fp), q01 = __ldg(fp + 1);
+  const float2 q10 = __ldg(fq), q11 = __ldg(fq + 1);
+  o.d = lerpf_exact(g.d_lo, g.d_span, unit23(a.z));
+  const float i0 = lerpf_exact(g.i0_lo, g.i0_span, unit23(a.w));
+  o.sig = __fmul_rn(o.d, g.inv_ratio);
+  seed_look(g, key, gi, o.sig, i0, o.lk);
+  const float u = bilerp(q00.x, q01.x, q10.x, q11.x, tx, ty);
+  const float v = bilerp(q00.y, q01.y, q10.y, q11.y, tx, ty);
+  o.xq1 = (int)(X << 3);
+  o.yq1 = (int)(Y << 3);
+  o.xq2 = (long long)o.xq1 + __float2ll_rn(u * 1048576.0f);
+  o.yq2 = (long long)o.yq1 + __float2ll_rn(v * 1048576.0f);
+}
+
+// Q20 -> anchor floor(v + 1/2) and the exact float32 fraction in [-1/2, 1/2).
+__device__ __forceinline__ void q20_anchor(int q, int& a, float& f) {
+  a = (q + (1 << 19)) >> 20;
+  f = (float)(q - (a << 20)) * 0x1p-20f;
+}
+
+// Record words: SIMPLE (rho = 0, sx = sy: one uint4) {xq, yq, sigma, amp};
+// full (two uint4) {xq, yq, sx, sy} {rho, amp, 0, 0}.
+template <bool SIMPLE>
+struct RecW {
+  static constexpr int kWords = SIMPLE ? 1 : 2;
+};
+
+// Byte offsets of the shared-memory regions (identical in every CTA).
+struct PairSmem {
+  int acc_ints;     // (2 RB + pad_rows) AS + 8
+  int inbox_off;    // bytes
+  int cnt_in_off;   // [2][C] ints (written by the sources)
+  int dmax_in_off;  // [C] floats (written by the sources)
+  int cnt_out_off;  // [2][C] ints (this CTA's slot counters)
+  int total;
+};
+
+__host__ __device__ __forceinline__ PairSmem pair_smem(int rows, int pad_rows, int AS, int C, int cap, int words) {
+  PairSmem s;
+  s.acc_ints = (2 * rows + pad_rows) * AS + 8;
+  s.inbox_off = ((s.acc_ints * 4) + 15) & ~15;
+  s.cnt_in_off = s.inbox_off + 2 * C * cap * words * 16;
+  s.dmax_in_off = s.cnt_in_off + 2 * C * 4;
+  s.cnt_out_off = s.dmax_in_off + C * 4;
+  s.total = ((s.cnt_out_off + 2 * C * 4) + 15) & ~15;
+  return s;
+}
+
+// Rows [lo, hi] (clipped to the image) that a particle-frame's tight window
+// can touch (anchor offsets within +-hcfg, the config's largest half-width);
+// false when the window misses the image.
+__device__ __forceinline__ bool pair_rows(long long xq, long long yq, float R, int hcfg, int H, int W, int& lo,
+                                          int& hi) {
+  const long long ax = (xq + (1 << 19)) >> 20, ay = (yq + (1 << 19)) >> 20;
+  if (ax < -hcfg - 1 || ax > W + hcfg || ay < -hcfg - 1 || ay > H + hcfg) return false;
+  float fx, fy;
+  int a;
+  q20_anchor((int)xq, a, fx);
+  q20_anchor((int)yq, a, fy);
+  const int jlo = max(-hcfg, (int)ceilf(__fsub_rn(fx, R)));
+  const int jhi = min(hcfg, (int)floorf(__fadd_rn(fx, R)));
+  if ((int)ax + jhi < 0 || (int)ax + jlo > W - 1 || jlo > jhi) return false;
+  const int ilo = max(-hcfg, (int)ceilf(__fsub_rn(fy, R)));
+  const int ihi = min(hcfg, (int)floorf(__fadd_rn(fy, R)));
+  lo = max((int)ay + ilo, 0);
+  hi = min((int)ay + ihi, H - 1);
+  return lo <= hi && ilo <= ihi;
+}
+
+// Per-pair splat parameters (thread 0 computes, shared with the block).
+struct PairItem {
+  int h, shift[2], var;
+  int K[2];                 // records per frame (inbox + overflow)
+  int kin[2];               // records per frame in the shared-memory inbox
+  int pre[2][kPairMaxCluster + 1];   // inbox prefix over sources
+  float inv_scale[2];
+  float dmax;
+  int side;
+};
+
+template <bool SIMPLE>
+__device__ __forceinline__ void pair_emit(const BandParams& P, const PairSmem& L, unsigned char* smem, int f,
+                                          int dst, uint4 w0, uint4 w1, int* ovf_cnt, uint4* ovf) {
+  constexpr int RW = RecW<SIMPLE>::kWords;
+  const int C = P.cl_size;
+  const int k = (int)cl_rank();
+  int* cnt_out = reinterpret_cast<int*>(smem + L.cnt_out_off);
+  const int slot = atomicAdd(cnt_out + f * C + dst, 1);
+  if (slot < P.cl_cap) {
+    uint4* box = reinterpret_cast<uint4*>(smem + L.inbox_off) + ((size_t)(f * C + k) * P.cl_cap + slot) * RW;
+    const uint32_t ra = cl_map(box, (uint32_t)dst);
+    cl_st4(ra, w0);
+    if (!SIMPLE) cl_st4(ra + 16, w1);
+  } else {
+    // spill: the destination's global overflow region of this frame (L2)
+    const int o = atomicAdd(ovf_cnt + dst * 2 + f, 1);
+    uint4* dstp = ovf + ((size_t)(dst * 2 + f) * P.n + o) * RW;
+    __stcg(dstp, w0);
+    if (!SIMPLE) __stcg(dstp + 1, w1);
+  }
+}
+
+template <bool SIMPLE>
+__device__ __forceinline__ void pair_route(const BandParams& P, const PairSmem& L, unsigned char* smem, int f,
+                                           long long xq, long long yq, float sx, float sy, float rho, float amp,
+                                           int* ovf_cnt, uint4* ovf) {
+  float R = __fmul_rn(fmaxf(sx, sy), kTightR);
+  if (P.psf != kPsfPoint) R = __fadd_rn(R, 0.5f);
+  int lo, hi;
+  if (!pair_rows(xq, yq, R, P.cl_hcfg, P.H, P.W, lo, hi)) return;
+  const uint4 w0 = SIMPLE ? make_uint4((uint32_t)(int)xq, (uint32_t)(int)yq, __float_as_uint(sx), __float_as_uint(amp))
+                          : make_uint4((uint32_t)(int)xq, (uint32_t)(int)yq, __float_as_uint(sx), __float_as_uint(sy));
+  const uint4 w1 = make_uint4(__float_as_uint(rho), __float_as_uint(amp), 0u, 0u);
+  const int d0 = lo / P.cl_rows, d1 = hi / P.cl_rows;
+  for (int d = d0; d <= d1; ++d) pair_emit<SIMPLE>(P, L, smem, f, d, w0, w1, ovf_cnt, ovf);
+}
+
+// Phase B: splat this CTA's records of both frames (variant fixed per pair).
+template <int PSF, int SEP, int WM, bool SIMPLE>
+__device__ __forceinline__ void pair_splat(const BandParams& P, const PairSmem& L, unsigned char* smem,
+                                           const PairItem& it, int r0, int r1, const int* ovf_cnt,
+                                           const uint4* ovf) {
+  constexpr int RW = RecW<SIMPLE>::kWords;
+  const int C = P.cl_size;
+  const int k = (int)cl_rank();
+  int* acc0 = reinterpret_cast<int*>(smem);
+  const uint4* inbox = reinterpret_cast<const uint4*>(smem + L.inbox_off);
+  const int total = it.K[0] + it.K[1];
+  for (int q = threadIdx.x; q < total; q += kPairThreads) {
+    const int f = q >= it.K[0] ? 1 : 0;
+    const int qf = q - (f ? it.K[0] : 0);
+    const uint4* rp;
+    if (qf < it.kin[f]) {
+      int s = 0;
+#pragma unroll
+      for (int j = 1; j < kPairMaxCluster; ++j) s += (j < C && it.pre[f][j] <= qf) ? 1 : 0;
+      rp = inbox + ((size_t)(f * C + s) * P.cl_cap + (qf - it.pre[f][s])) * RW;
+    } else {
+      rp = ovf + ((size_t)(k * 2 + f) * P.n + (qf - it.kin[f])) * RW;
+    }
+    uint4 w0, w1 = make_uint4(0u, 0u, 0u, 0u);
+    if (qf < it.kin[f]) {
+      w0 = rp[0];
+      if (!SIMPLE) w1 = rp[1];
+    } else {
+      w0 = __ldcg(rp);
+      if (!SIMPLE) w1 = __ldcg(rp + 1);
+    }
+    int ax, ay;
+    float fx, fy;
+    q20_anchor((int)w0.x, ax, fx);
+    q20_anchor((int)w0.y, ay, fy);
+    const float sx = __uint_as_float(w0.z);
+    const float sy = SIMPLE ? sx : __uint_as_float(w0.w);
+    const float rho = SIMPLE ? 0.f : __uint_as_float(w1.x);
+    const float amp = SIMPLE ? __uint_as_float(w0.w) : __uint_as_float(w1.y);
+    int* acc = acc0 + f * P.cl_rows * P.AS;
+    splat_v<PSF, SEP, WM>(acc, P.AS, ax, ay, fx, fy, amp, sx, sy, rho, it.h, r0, r1, 0, P.W, it.shift[f],
+                          (float)(1 << it.shift[f]));
+  }
+}
+
+template <int PSF, bool SIMPLE>
+__global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ PairItem it;
+  __shared__ unsigned s_dmax;
+  constexpr int RW = RecW<SIMPLE>::kWords;
+  const int tid = threadIdx.x;
+  const int C = P.cl_size;
+  const int k = (int)cl_rank();
+  const PairSmem L = pair_smem(P.cl_rows, P.pad_rows, P.AS, C, P.cl_cap, RW);
+  int* acc0 = reinterpret_cast<int*>(smem);
+  int* acc1 = acc0 + P.cl_rows * P.AS;
+  int* cnt_in = reinterpret_cast<int*>(smem + L.cnt_in_off);
+  float* dmax_in = reinterpret_cast<float*>(smem + L.dmax_in_off);
+  int* cnt_out = reinterpret_cast<int*>(smem + L.cnt_out_off);
+  const int cid = (int)cl_id(), ncl = (int)cl_count();
+  int* ovf_cnt = P.cl_ovf_cnt + (size_t)cid * C * 2;
+  uint4* ovf = P.cl_ovf + (size_t)cid * C * 2 * P.n * RW;
+  const int r0 = k * P.cl_rows, r1 = min(P.H, r0 + P.cl_rows);
+  for (int e = tid; e < L.acc_ints / 4; e += kPairThreads) reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+  if (tid < 2 * C) cnt_out[tid] = 0;
+  // every CTA of the cluster runs before anyone writes into its shared memory
+  cl_arrive();
+  cl_wait();
+  const GenCfg& g = P.g;
+  for (int pl = cid; pl < P.pairs; pl += ncl) {
+    const RngKey key = band_key(P, pl);
+    // seeding density and active count (particles.py:73-83)
+    const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
+    const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
+    double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+    mm = fmin(fmax(mm, 0.0), (double)P.n);
+    const int M = (int)mm;
+    const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
+    if (tid == 0) s_dmax = 0u;
+    __syncthreads();
+    // ---- phase A: generate this CTA's share of the particles, route records
+    unsigned dloc = 0u;
+    for (int gi = k * kPairThreads + tid; gi < M; gi += C * kPairThreads) {
+      PairPart pp;
+      pair_particle(g, key, gi, flow, pp);
+      dloc = max(dloc, __float_as_uint(pp.d));   // d >= 0: float order == bit order
+      const Look& lk = pp.lk;
+      if (lk.vis1 && lk.amp1 > 0.f)
+        pair_route<SIMPLE>(P, L, smem, 0, pp.xq1, pp.yq1, pp.sig, pp.sig, lk.rho1, lk.amp1, ovf_cnt, ovf);
+      if (lk.vis2 && lk.amp2 > 0.f)
+        pair_route<SIMPLE>(P, L, smem, 1, pp.xq2, pp.yq2, lk.sx2, lk.sy2, lk.rho2, lk.amp2, ovf_cnt, ovf);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dloc = max(dloc, __shfl_xor_sync(~0u, dloc, o));
+    if ((tid & 31) == 0 && dloc) atomicMax(&s_dmax, dloc);
+    __syncthreads();
+    // publish this source's counts and maximum diameter to every destination
+    if (tid < 2 * C) {
+      const int f = tid / C, d = tid - f * C;
+      cl_st1(cl_map(cnt_in + f * C + k, (uint32_t)d), (uint32_t)cnt_out[tid]);
+    } else if (tid >= 64 && tid < 64 + C) {
+      cl_st1(cl_map(dmax_in + k, (uint32_t)(tid - 64)), s_dmax);
+    }
+    __syncthreads();
+    if (tid < 2 * C) cnt_out[tid] = 0;
+    cl_arrive();
+    cl_wait();
+    // ---- phase B: pair parameters, splat the inbox
+    if (tid == 0) {
+      float dmax = 0.f;
+      for (int s = 0; s < C; ++s) dmax = fmaxf(dmax, dmax_in[s]);
+      // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
+      it.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
+      it.dmax = M > 0 ? dmax : (float)g.d_hi;
+      it.h = it.side >> 1;
+      for (int f = 0; f < 2; ++f) {
+        int acc = 0;
+        it.pre[f][0] = 0;
+        for (int s = 0; s < C; ++s) {
+          acc += min(cnt_in[f * C + s], P.cl_cap);
+          it.pre[f][s + 1] = acc;
+        }
+        it.kin[f] = acc;
+        it.K[f] = acc + __ldcg(ovf_cnt + k * 2 + f);
+        // fixed-point shift: a pixel receives at most K contributions
+        it.shift[f] = shift_for(max(1, it.K[f]), P.amp_bound);
+        it.inv_scale[f] = 1.0f / (float)(1 << it.shift[f]);
+      }
+      // window bound (as item_setup): floor(2 R_max) + 1 from the pair's largest
+      // sigma, unless frame-2 sigma jitter makes it unbounded
+      int wt = 2 * it.h + 1;
+      if (P.psf == kPsfPoint && !(g.f2_sigma_std > 0.f))
+        wt = min(wt, (int)floorf(2.0f * __fmul_rn(__fmul_rn(it.dmax, g.inv_ratio), kTightR)) + 1);
+      wt = max(1, wt);
+      const int sep = (g.rho_lo == 0.f && g.rho_span == 0.f && !(g.f2_rho_std > 0.f)) ? 1 : 0;
+      const int wm = (P.psf == kPsfPoint && sep && wt <= kMaxUnpredWM && wt - 1 <= P.pad_rows) ? wt : 0;
+      it.var = (P.psf == kPsfPoint ? 16 * sep : 0) + wm;
+      if (k == 0) {
+        PairHdr hd{};
+        hd.ppp = ppp;
+        hd.M = M;
+        hd.side = it.side;
+        hd.dmax = it.dmax;
+        write_stats(P, pl, hd);
+      }
+    }
+    __syncthreads();
+    if constexpr (PSF == kPsfErf) {
+      pair_splat<PSF, 0, 0, SIMPLE>(P, L, smem, it, r0, r1, ovf_cnt, ovf);
+    } else {
+      switch (it.var) {
+#define PGB_PV(S, WW) case 16 * S + WW: pair_splat<PSF, S, WW, SIMPLE>(P, L, smem, it, r0, r1, ovf_cnt, ovf); break;
+        PGB_PV(1, 1) PGB_PV(1, 2) PGB_PV(1, 3) PGB_PV(1, 4) PGB_PV(1, 5) PGB_PV(1, 6) PGB_PV(1, 7)
+        PGB_PV(1, 8) PGB_PV(1, 9) PGB_PV(1, 10) PGB_PV(1, 11) PGB_PV(1, 12)
+#undef PGB_PV
+        default: pair_splat<PSF, 0, 0, SIMPLE>(P, L, smem, it, r0, r1, ovf_cnt, ovf); break;
+      }
+    }
+    __syncthreads();
+    if (tid < 2) ovf_cnt[k * 2 + tid] = 0;   // overflow region consumed (self-cleaning)
+    // the inbox and counts are consumed: sources may refill them (phase A of
+    // the next pair) once every CTA has arrived; the store overlaps that wait
+    cl_arrive();
+    // ---- phase C: finalize + store rows [r0, r1) of both frames, zeroing
+    band_store(P, acc0, pl, 0, r0, r1 - r0, 0, P.W, it.inv_scale[0]);
+    band_store(P, acc1, pl, 1, r0, r1 - r0, 0, P.W, it.inv_scale[1]);
+    __syncthreads();
+    cl_wait();
+  }
+}
+
+// Particle arrays of the pair law (sample_particles path): one thread per
+// particle; the per-pair maximum diameter by atomicMax on the float bits.
+__global__ void pair_particles_kernel(const BandParams P, pgb_particle_out O, unsigned* dmax_bits) {
+  const int pl = blockIdx.y;
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= P.n) return;
+  const GenCfg& g = P.g;
+  const RngKey key = band_key(P, pl);
+  const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
+  const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
+  double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+  mm = fmin(fmax(mm, 0.0), (double)P.n);
+  const int M = (int)mm;
+  const bool active = gi < M;
+  const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
+  PairPart pp;
+  pair_particle(g, key, gi, flow, pp);
+  if (!active) {
+    // inactive capacity slots: I0 = 0, never rendered (particles.py:89)
+    seed_look(g, key, gi, pp.sig, 0.f, pp.lk);
+  } else {
+    atomicMax(dmax_bits + pl, __float_as_uint(pp.d));
+  }
+  const Look& lk = pp.lk;
+  const size_t o = (size_t)pl * P.n + gi;
+  if (O.pos1) { O.pos1[2 * o] = (double)pp.xq1 * 0x1p-20; O.pos1[2 * o + 1] = (double)pp.yq1 * 0x1p-20; }
+  if (O.pos2) { O.pos2[2 * o] = (double)pp.xq2 * 0x1p-20; O.pos2[2 * o + 1] = (double)pp.yq2 * 0x1p-20; }
+  if (O.i0_1) O.i0_1[o] = lk.amp1;
+  if (O.sx_1) O.sx_1[o] = pp.sig;
+  if (O.sy_1) O.sy_1[o] = pp.sig;
+  if (O.rho_1) O.rho_1[o] = lk.rho1;
+  if (O.i0_2) O.i0_2[o] = lk.amp2;
+  if (O.sx_2) O.sx_2[o] = lk.sx2;
+  if (O.sy_2) O.sy_2[o] = lk.sy2;
+  if (O.rho_2) O.rho_2[o] = lk.rho2;
+  if (O.diameter) O.diameter[o] = pp.d;
+  if (O.z1) O.z1[o] = lk.z1;
+  if (O.active) O.active[o] = active ? 1 : 0;
+  if (O.visible1) O.visible1[o] = (active && lk.vis1) ? 1 : 0;
+  if (O.visible2) O.visible2[o] = (active && lk.vis2) ? 1 : 0;
+}
+
+__global__ void pair_stats_kernel(const BandParams P, const unsigned* dmax_bits) {
+  const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pl >= P.pairs) return;
+  const GenCfg& g = P.g;
+  const RngKey key = band_key(P, pl);
+  const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
+  const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
+  double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+  mm = fmin(fmax(mm, 0.0), (double)P.n);
+  PairHdr hd{};
+  hd.ppp = ppp;
+  hd.M = (int)mm;
+  hd.dmax = hd.M > 0 ? __uint_as_float(dmax_bits[pl]) : (float)g.d_hi;
+  hd.side = patch_side_exact(hd.M > 0 ? (double)hd.dmax : g.d_hi, g.patch_mult);
+  write_stats(P, pl, hd);
+}
+
+}  // namespace pgb
