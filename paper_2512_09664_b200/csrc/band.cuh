@@ -70,7 +70,7 @@ struct BandParams {
   long long split_base, total_items;
   int split_s;
   int pad_rows;                // zero rows after the frame-2 accumulator (unpredicated splat windows)
-  int pro_smem;                // dynamic shared bytes of the standalone prologue kernel
+  int pro_smem;                // shared bytes the pair prologue may use (prologue kernel / band accumulators)
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
   int n, pairs;
   long long pair_base;
@@ -1403,7 +1403,8 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   int* acc1 = acc0 + P.TH * P.AS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
-  const int acc_bytes = ((2 * P.TH + P.pad_rows) * P.AS + 8) * 4;
+  // the prologue borrows the accumulator region (>= its histogram, see make_band_plan)
+  const int acc_bytes = P.pro_smem;
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)
     for (int e = tid; e < P.zero_head_n; e += kBandBlock) P.zero_head[e] = make_int4(0, 0, 0, 0);
   // One ticket sequence: [0, npro) prologue items (the pairs, then the

@@ -552,7 +552,11 @@ BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0) {
   p.tiles_y = (H + p.TH - 1) / p.TH;
   p.tiles_x = (W + p.TW - 1) / p.TW;
   p.tiles = p.tiles_y * p.tiles_x;
-  p.smem = sizeof(BandShared) + ((size_t)(2 * p.TH + p.pad_rows) * p.AS + 8) * 4;
+  // the in-kernel pair prologue borrows the accumulator region for its cell
+  // histogram (2^(sy+sx) + 4 ints): small tiles get at least that much
+  const size_t acc_bytes = ((size_t)(2 * p.TH + p.pad_rows) * p.AS + 8) * 4;
+  const size_t hist_bytes = ((size_t)(1 << (p.sy + p.sx)) + 8) * 4;
+  p.smem = sizeof(BandShared) + std::max(acc_bytes, hist_bytes);
   PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
   return p;
 }
@@ -715,13 +719,16 @@ bool make_pair_plan(const pgb_config* c, PairPlan& p, int cap_override = 0) {
       const double lam = per_src * std::min(1.0, (double)(rows + 2 * p.hcfg + 1) / (double)H);
       int cap = (int)std::ceil(lam + 5.0 * std::sqrt(lam) + 8.0);
       cap = (cap + 1) & ~1;
-      if (cap_override > 0) cap = cap_override;
       const PairSmem L = pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words);
       if ((size_t)L.total <= budget) {
+        // the cluster size (rows per CTA) is fixed by the configuration: the
+        // fixed-point shift depends on it. A capacity override (tests: force
+        // the spill path) changes only the inbox size.
+        if (cap_override > 0) cap = cap_override;
         p.C = C;
         p.rows = rows;
         p.cap = cap;
-        p.smem = (size_t)L.total;
+        p.smem = (size_t)pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words).total;
         return true;
       }
     }
@@ -867,6 +874,7 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.noise_std = (float)cfg->noise_std;
   P.out[0] = img1;
   P.out[1] = img2;
+  P.pro_smem = (int)(bp.smem - sizeof(BandShared));
   BandFn fn = cfg->psf == PGB_PSF_ERF ? band_kernel<kPsfErf> : band_kernel<kPsfPoint>;
   const int ctas = band_resident_ctas(fn, bp.smem);
   // whole rounds of (pair, tile) items over the resident CTAs, then the
