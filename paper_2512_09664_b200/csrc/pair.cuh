@@ -146,27 +146,6 @@ __host__ __device__ __forceinline__ PairSmem pair_smem(int rows, int pad_rows, i
   return s;
 }
 
-// Rows [lo, hi] (clipped to the image) that a particle-frame's tight window
-// can touch (anchor offsets within +-hcfg, the config's largest half-width);
-// false when the window misses the image.
-__device__ __forceinline__ bool pair_rows(long long xq, long long yq, float R, int hcfg, int H, int W, int& lo,
-                                          int& hi) {
-  const long long ax = (xq + (1 << 19)) >> 20, ay = (yq + (1 << 19)) >> 20;
-  if (ax < -hcfg - 1 || ax > W + hcfg || ay < -hcfg - 1 || ay > H + hcfg) return false;
-  float fx, fy;
-  int a;
-  q20_anchor((int)xq, a, fx);
-  q20_anchor((int)yq, a, fy);
-  const int jlo = max(-hcfg, (int)ceilf(__fsub_rn(fx, R)));
-  const int jhi = min(hcfg, (int)floorf(__fadd_rn(fx, R)));
-  if ((int)ax + jhi < 0 || (int)ax + jlo > W - 1 || jlo > jhi) return false;
-  const int ilo = max(-hcfg, (int)ceilf(__fsub_rn(fy, R)));
-  const int ihi = min(hcfg, (int)floorf(__fadd_rn(fy, R)));
-  lo = max((int)ay + ilo, 0);
-  hi = min((int)ay + ihi, H - 1);
-  return lo <= hi && ilo <= ihi;
-}
-
 // Per-pair splat parameters (thread 0 computes, shared with the block).
 struct PairItem {
   int h, shift[2], var;
@@ -178,68 +157,78 @@ struct PairItem {
   int side;
 };
 
+// One record into CTA `dst`'s inbox region of this source (local slot
+// counter, then a DSMEM store); a full region spills to the destination's
+// global overflow list of this frame (L2; exact, slower).
 template <bool SIMPLE>
-__device__ __forceinline__ void pair_emit(const BandParams& P, const PairSmem& L, unsigned char* smem, int f,
-                                          int dst, uint4 w0, uint4 w1, int* ovf_cnt, uint4* ovf) {
+__device__ __forceinline__ void pair_emit(const BandParams& P, uint4* my_box, int* cnt_out, int f, int dst,
+                                          const uint4& w0, const uint4& w1, int* ovf_cnt, uint4* ovf) {
   constexpr int RW = RecW<SIMPLE>::kWords;
-  const int C = P.cl_size;
-  const int k = (int)cl_rank();
-  int* cnt_out = reinterpret_cast<int*>(smem + L.cnt_out_off);
-  const int slot = atomicAdd(cnt_out + f * C + dst, 1);
+  const int slot = atomicAdd(cnt_out + f * P.cl_size + dst, 1);
   if (slot < P.cl_cap) {
-    uint4* box = reinterpret_cast<uint4*>(smem + L.inbox_off) + ((size_t)(f * C + k) * P.cl_cap + slot) * RW;
-    const uint32_t ra = cl_map(box, (uint32_t)dst);
+    const uint32_t ra = cl_map(my_box + (size_t)(f * P.cl_size * P.cl_cap + slot) * RW, (uint32_t)dst);
     cl_st4(ra, w0);
     if (!SIMPLE) cl_st4(ra + 16, w1);
   } else {
-    // spill: the destination's global overflow region of this frame (L2)
     const int o = atomicAdd(ovf_cnt + dst * 2 + f, 1);
-    uint4* dstp = ovf + ((size_t)(dst * 2 + f) * P.n + o) * RW;
-    __stcg(dstp, w0);
-    if (!SIMPLE) __stcg(dstp + 1, w1);
+    uint4* dp = ovf + ((size_t)(dst * 2 + f) * P.n + o) * RW;
+    __stcg(dp, w0);
+    if (!SIMPLE) __stcg(dp + 1, w1);
   }
 }
 
+// Route one particle-frame (Q20 position) to the CTAs owning the rows its
+// tight window (anchor offsets within +-cl_hcfg) can touch. Windows that miss
+// the image rows produce no record; the columns are clipped at splat time.
 template <bool SIMPLE>
-__device__ __forceinline__ void pair_route(const BandParams& P, const PairSmem& L, unsigned char* smem, int f,
+__device__ __forceinline__ void pair_route(const BandParams& P, uint4* my_box, int* cnt_out, int f,
                                            long long xq, long long yq, float sx, float sy, float rho, float amp,
                                            int* ovf_cnt, uint4* ovf) {
+  const int hc = P.cl_hcfg;
+  const long long ayl = (yq + (1 << 19)) >> 20, axl = (xq + (1 << 19)) >> 20;
+  if (ayl < -hc - 1 || ayl > P.H + hc || axl < -hc - 1 || axl > P.W + hc) return;
+  const int ay = (int)ayl;
+  const float fy = (float)((int)yq - (ay << 20)) * 0x1p-20f;
   float R = __fmul_rn(fmaxf(sx, sy), kTightR);
   if (P.psf != kPsfPoint) R = __fadd_rn(R, 0.5f);
-  int lo, hi;
-  if (!pair_rows(xq, yq, R, P.cl_hcfg, P.H, P.W, lo, hi)) return;
+  const int lo = max(ay + max(-hc, (int)ceilf(__fsub_rn(fy, R))), 0);
+  const int hi = min(ay + min(hc, (int)floorf(__fadd_rn(fy, R))), P.H - 1);
+  if (lo > hi) return;
   const uint4 w0 = SIMPLE ? make_uint4((uint32_t)(int)xq, (uint32_t)(int)yq, __float_as_uint(sx), __float_as_uint(amp))
                           : make_uint4((uint32_t)(int)xq, (uint32_t)(int)yq, __float_as_uint(sx), __float_as_uint(sy));
   const uint4 w1 = make_uint4(__float_as_uint(rho), __float_as_uint(amp), 0u, 0u);
-  const int d0 = lo / P.cl_rows, d1 = hi / P.cl_rows;
-  for (int d = d0; d <= d1; ++d) pair_emit<SIMPLE>(P, L, smem, f, d, w0, w1, ovf_cnt, ovf);
+  const int d0 = (int)(((uint32_t)lo * P.cl_rdiv) >> 20), d1 = (int)(((uint32_t)hi * P.cl_rdiv) >> 20);
+  pair_emit<SIMPLE>(P, my_box, cnt_out, f, d0, w0, w1, ovf_cnt, ovf);
+  for (int d = d0 + 1; d <= d1; ++d) pair_emit<SIMPLE>(P, my_box, cnt_out, f, d, w0, w1, ovf_cnt, ovf);
 }
 
-// Phase B: splat this CTA's records of both frames (variant fixed per pair).
+// Phase B: splat this CTA's records of frame f (variant fixed per pair).
+// Thread t takes records t, t + NT, ...: its source region index only moves
+// forward (a running search over the inbox prefix).
 template <int PSF, int SEP, int WM, bool SIMPLE>
-__device__ __forceinline__ void pair_splat(const BandParams& P, const PairSmem& L, unsigned char* smem,
-                                           const PairItem& it, int r0, int r1, const int* ovf_cnt,
-                                           const uint4* ovf) {
+__device__ __forceinline__ void pair_splat_frame(const BandParams& P, const uint4* inbox, int* acc,
+                                                 const PairItem& it, int f, int r0, int r1, const uint4* ovf_f) {
   constexpr int RW = RecW<SIMPLE>::kWords;
   const int C = P.cl_size;
-  const int k = (int)cl_rank();
-  int* acc0 = reinterpret_cast<int*>(smem);
-  const uint4* inbox = reinterpret_cast<const uint4*>(smem + L.inbox_off);
-  const int total = it.K[0] + it.K[1];
-  for (int q = threadIdx.x; q < total; q += kPairThreads) {
-    const int f = q >= it.K[0] ? 1 : 0;
-    const int qf = q - (f ? it.K[0] : 0);
+  const int kin = it.kin[f], K = it.K[f];
+  const int shift = it.shift[f];
+  const float scale = (float)(1 << shift);
+  const int* pre = it.pre[f];
+  int s = 0;
+  int next = C > 1 ? pre[1] : 0x7fffffff;
+  for (int q = threadIdx.x; q < K; q += kPairThreads) {
     const uint4* rp;
-    if (qf < it.kin[f]) {
-      int s = 0;
-#pragma unroll
-      for (int j = 1; j < kPairMaxCluster; ++j) s += (j < C && it.pre[f][j] <= qf) ? 1 : 0;
-      rp = inbox + ((size_t)(f * C + s) * P.cl_cap + (qf - it.pre[f][s])) * RW;
+    if (q < kin) {
+      while (q >= next) {
+        ++s;
+        next = s + 1 < C ? pre[s + 1] : 0x7fffffff;
+      }
+      rp = inbox + ((size_t)(f * C + s) * P.cl_cap + (q - pre[s])) * RW;
     } else {
-      rp = ovf + ((size_t)(k * 2 + f) * P.n + (qf - it.kin[f])) * RW;
+      rp = ovf_f + (size_t)(q - kin) * RW;
     }
     uint4 w0, w1 = make_uint4(0u, 0u, 0u, 0u);
-    if (qf < it.kin[f]) {
+    if (q < kin) {
       w0 = rp[0];
       if (!SIMPLE) w1 = rp[1];
     } else {
@@ -254,10 +243,17 @@ __device__ __forceinline__ void pair_splat(const BandParams& P, const PairSmem& 
     const float sy = SIMPLE ? sx : __uint_as_float(w0.w);
     const float rho = SIMPLE ? 0.f : __uint_as_float(w1.x);
     const float amp = SIMPLE ? __uint_as_float(w0.w) : __uint_as_float(w1.y);
-    int* acc = acc0 + f * P.cl_rows * P.AS;
-    splat_v<PSF, SEP, WM>(acc, P.AS, ax, ay, fx, fy, amp, sx, sy, rho, it.h, r0, r1, 0, P.W, it.shift[f],
-                          (float)(1 << it.shift[f]));
+    splat_v<PSF, SEP, WM>(acc, P.AS, ax, ay, fx, fy, amp, sx, sy, rho, it.h, r0, r1, 0, P.W, shift, scale);
   }
+}
+
+template <int PSF, int SEP, int WM, bool SIMPLE>
+__device__ __forceinline__ void pair_splat(const BandParams& P, const uint4* inbox, int* acc0, const PairItem& it,
+                                           int r0, int r1, const uint4* ovf_k) {
+  constexpr int RW = RecW<SIMPLE>::kWords;
+  pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 0, r0, r1, ovf_k);
+  pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0 + P.cl_rows * P.AS, it, 1, r0, r1,
+                                         ovf_k + (size_t)P.n * RW);
 }
 
 template <int PSF, bool SIMPLE>
@@ -265,6 +261,8 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ PairItem it;
   __shared__ unsigned s_dmax;
+  __shared__ int s_M;
+  __shared__ double s_ppp;
   constexpr int RW = RecW<SIMPLE>::kWords;
   const int tid = threadIdx.x;
   const int C = P.cl_size;
@@ -279,6 +277,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
   int* ovf_cnt = P.cl_ovf_cnt + (size_t)cid * C * 2;
   uint4* ovf = P.cl_ovf + (size_t)cid * C * 2 * P.n * RW;
   const int r0 = k * P.cl_rows, r1 = min(P.H, r0 + P.cl_rows);
+  uint4* my_box = reinterpret_cast<uint4*>(smem + L.inbox_off) + (size_t)k * P.cl_cap * RW;   // [f][k] region
+  const uint4* inbox = reinterpret_cast<const uint4*>(smem + L.inbox_off);
+  const uint4* ovf_k = ovf + (size_t)k * 2 * P.n * RW;
   for (int e = tid; e < L.acc_ints / 4; e += kPairThreads) reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
   if (tid < 2 * C) cnt_out[tid] = 0;
   // every CTA of the cluster runs before anyone writes into its shared memory
@@ -287,15 +288,19 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
   const GenCfg& g = P.g;
   for (int pl = cid; pl < P.pairs; pl += ncl) {
     const RngKey key = band_key(P, pl);
-    // seeding density and active count (particles.py:73-83)
-    const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
-    const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
-    double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
-    mm = fmin(fmax(mm, 0.0), (double)P.n);
-    const int M = (int)mm;
+    if (tid == 0) {
+      // seeding density and active count (particles.py:73-83)
+      const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
+      const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
+      double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+      mm = fmin(fmax(mm, 0.0), (double)P.n);
+      s_M = (int)mm;
+      s_ppp = ppp;
+      s_dmax = 0u;
+    }
     const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
-    if (tid == 0) s_dmax = 0u;
     __syncthreads();
+    const int M = s_M;
     // ---- phase A: generate this CTA's share of the particles, route records
     unsigned dloc = 0u;
     for (int gi = k * kPairThreads + tid; gi < M; gi += C * kPairThreads) {
@@ -304,9 +309,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
       dloc = max(dloc, __float_as_uint(pp.d));   // d >= 0: float order == bit order
       const Look& lk = pp.lk;
       if (lk.vis1 && lk.amp1 > 0.f)
-        pair_route<SIMPLE>(P, L, smem, 0, pp.xq1, pp.yq1, pp.sig, pp.sig, lk.rho1, lk.amp1, ovf_cnt, ovf);
+        pair_route<SIMPLE>(P, my_box, cnt_out, 0, pp.xq1, pp.yq1, pp.sig, pp.sig, lk.rho1, lk.amp1, ovf_cnt, ovf);
       if (lk.vis2 && lk.amp2 > 0.f)
-        pair_route<SIMPLE>(P, L, smem, 1, pp.xq2, pp.yq2, lk.sx2, lk.sy2, lk.rho2, lk.amp2, ovf_cnt, ovf);
+        pair_route<SIMPLE>(P, my_box, cnt_out, 1, pp.xq2, pp.yq2, lk.sx2, lk.sy2, lk.rho2, lk.amp2, ovf_cnt, ovf);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dloc = max(dloc, __shfl_xor_sync(~0u, dloc, o));
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
       it.var = (P.psf == kPsfPoint ? 16 * sep : 0) + wm;
       if (k == 0) {
         PairHdr hd{};
-        hd.ppp = ppp;
+        hd.ppp = s_ppp;
         hd.M = M;
         hd.side = it.side;
         hd.dmax = it.dmax;
@@ -364,14 +369,14 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
     }
     __syncthreads();
     if constexpr (PSF == kPsfErf) {
-      pair_splat<PSF, 0, 0, SIMPLE>(P, L, smem, it, r0, r1, ovf_cnt, ovf);
+      pair_splat<PSF, 0, 0, SIMPLE>(P, inbox, acc0, it, r0, r1, ovf_k);
     } else {
       switch (it.var) {
-#define PGB_PV(S, WW) case 16 * S + WW: pair_splat<PSF, S, WW, SIMPLE>(P, L, smem, it, r0, r1, ovf_cnt, ovf); break;
+#define PGB_PV(S, WW) case 16 * S + WW: pair_splat<PSF, S, WW, SIMPLE>(P, inbox, acc0, it, r0, r1, ovf_k); break;
         PGB_PV(1, 1) PGB_PV(1, 2) PGB_PV(1, 3) PGB_PV(1, 4) PGB_PV(1, 5) PGB_PV(1, 6) PGB_PV(1, 7)
         PGB_PV(1, 8) PGB_PV(1, 9) PGB_PV(1, 10) PGB_PV(1, 11) PGB_PV(1, 12)
 #undef PGB_PV
-        default: pair_splat<PSF, 0, 0, SIMPLE>(P, L, smem, it, r0, r1, ovf_cnt, ovf); break;
+        default: pair_splat<PSF, 0, 0, SIMPLE>(P, inbox, acc0, it, r0, r1, ovf_k); break;
       }
     }
     __syncthreads();

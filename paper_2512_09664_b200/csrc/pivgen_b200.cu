@@ -761,7 +761,8 @@ int pair_max_clusters(PairFn fn, const PairPlan& p) {
   auto key = std::make_tuple((void*)fn, p.smem, p.C, dev);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  // the attribute is per function (and device): always the largest plan
+  PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem1));
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(p.C * 148);
   lc.blockDim = dim3(kPairThreads);
@@ -797,6 +798,10 @@ void launch_pair(BandParams& P, const PairPlan& pp, const pgb_config* cfg, cudaS
   P.cl_rows = pp.rows;
   P.cl_cap = pp.cap;
   P.cl_hcfg = pp.hcfg;
+  // row -> owning CTA by multiply-shift, checked exact for every image row
+  P.cl_rdiv = (uint32_t)(((1u << 20) + pp.rows - 1) / pp.rows);
+  for (int r = 0; r < P.H; ++r)
+    PGB_REQUIRE((int)(((uint32_t)r * P.cl_rdiv) >> 20) == r / pp.rows, "pair plan: row divisor not exact");
   P.AS = pp.AS;
   P.pad_rows = pp.pad_rows;
   cudaLaunchConfig_t lc{};

@@ -4,8 +4,11 @@ import csv
 import subprocess
 import sys
 
+import os
+
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+by = 1 if os.environ.get("NCU_BY") == "inst" else 0   # NCU_BY=inst: sort by executed instructions
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(txt.splitlines()))
@@ -37,7 +40,7 @@ for r in rows:
 tot_s = sum(v[0] for v in agg.values()) or 1
 tot_i = sum(v[1] for v in agg.values()) or 1
 print(f"total samples {tot_s}  total warp-instr {tot_i}")
-for (f, ln), (s, i, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+for (f, ln), (s, i, src) in sorted(agg.items(), key=lambda kv: -kv[1][by])[:top]:
     print(f"{100*s/tot_s:5.1f}% smp {100*i/tot_i:5.1f}% inst  {f}:{ln:<4d} {src}")
 
 if len(sys.argv) > 3:
