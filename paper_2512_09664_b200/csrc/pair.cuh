@@ -127,7 +127,7 @@ struct RecW {
 
 // Byte offsets of the shared-memory regions (identical in every CTA).
 struct PairSmem {
-  int acc_ints;     // (2 RB + pad_rows) AS + 8
+  int acc_ints;     // (frames RB + pad_rows) AS + 8
   int inbox_off;    // bytes
   int cnt_in_off;   // [2][C] ints (written by the sources)
   int dmax_in_off;  // [C] floats (written by the sources)
@@ -135,9 +135,11 @@ struct PairSmem {
   int total;
 };
 
-__host__ __device__ __forceinline__ PairSmem pair_smem(int rows, int pad_rows, int AS, int C, int cap, int words) {
+// frames 2: both frame accumulators live at once; 1: one accumulator, frames in turn.
+__host__ __device__ __forceinline__ PairSmem pair_smem(int rows, int pad_rows, int AS, int C, int cap, int words,
+                                                       int frames = 2) {
   PairSmem s;
-  s.acc_ints = (2 * rows + pad_rows) * AS + 8;
+  s.acc_ints = (frames * rows + pad_rows) * AS + 8;
   s.inbox_off = ((s.acc_ints * 4) + 15) & ~15;
   s.cnt_in_off = s.inbox_off + 2 * C * cap * words * 16;
   s.dmax_in_off = s.cnt_in_off + 2 * C * 4;
@@ -247,29 +249,31 @@ __device__ __forceinline__ void pair_splat_frame(const BandParams& P, const uint
   }
 }
 
-template <int PSF, int SEP, int WM, bool SIMPLE>
-__device__ __forceinline__ void pair_splat(const BandParams& P, const uint4* inbox, int* acc0, const PairItem& it,
-                                           int r0, int r1, const uint4* ovf_k) {
-  constexpr int RW = RecW<SIMPLE>::kWords;
-  pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 0, r0, r1, ovf_k);
-  pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0 + P.cl_rows * P.AS, it, 1, r0, r1,
-                                         ovf_k + (size_t)P.n * RW);
-}
+// Kernel variants: PSF, record format, and the particle loop's window bound
+// WM (1..kPairMaxWM: unpredicated separable windows; 0: dynamic loops),
+// chosen per launch from the configuration (the largest sigma any pair can
+// have), so every kernel carries only the registers its variant needs.
+constexpr int kPairMaxWM = 8;
+#ifndef PGB_PAIR_MINB
+#define PGB_PAIR_MINB 3   // three CTAs per SM (<= 85 registers) when the plan's shared memory allows
+#endif
 
-template <int PSF, bool SIMPLE>
-__global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams P) {
+template <int PSF, bool SIMPLE, int WM>
+__global__ void __launch_bounds__(kPairThreads, PGB_PAIR_MINB) pair_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ PairItem it;
   __shared__ unsigned s_dmax;
   __shared__ int s_M;
   __shared__ double s_ppp;
   constexpr int RW = RecW<SIMPLE>::kWords;
-  const int tid = threadIdx.x;
+  constexpr int SEP = (PSF == kPsfPoint && WM > 0) ? 1 : 0;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int C = P.cl_size;
   const int k = (int)cl_rank();
-  const PairSmem L = pair_smem(P.cl_rows, P.pad_rows, P.AS, C, P.cl_cap, RW);
+  const bool seq = P.cl_frames == 1;   // one accumulator, frames in turn
+  const PairSmem L = pair_smem(P.cl_rows, P.pad_rows, P.AS, C, P.cl_cap, RW, P.cl_frames);
   int* acc0 = reinterpret_cast<int*>(smem);
-  int* acc1 = acc0 + P.cl_rows * P.AS;
+  int* acc1 = seq ? acc0 : acc0 + P.cl_rows * P.AS;
   int* cnt_in = reinterpret_cast<int*>(smem + L.cnt_in_off);
   float* dmax_in = reinterpret_cast<float*>(smem + L.dmax_in_off);
   int* cnt_out = reinterpret_cast<int*>(smem + L.cnt_out_off);
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dloc = max(dloc, __shfl_xor_sync(~0u, dloc, o));
-    if ((tid & 31) == 0 && dloc) atomicMax(&s_dmax, dloc);
+    if (lane == 0 && dloc) atomicMax(&s_dmax, dloc);
     __syncthreads();
     // publish this source's counts and maximum diameter to every destination
     if (tid < 2 * C) {
@@ -328,65 +332,70 @@ __global__ void __launch_bounds__(kPairThreads, 1) pair_kernel(const BandParams 
     if (tid < 2 * C) cnt_out[tid] = 0;
     cl_arrive();
     cl_wait();
-    // ---- phase B: pair parameters, splat the inbox
-    if (tid == 0) {
-      float dmax = 0.f;
-      for (int s = 0; s < C; ++s) dmax = fmaxf(dmax, dmax_in[s]);
-      // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
-      it.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
-      it.dmax = M > 0 ? dmax : (float)g.d_hi;
-      it.h = it.side >> 1;
+    // ---- phase B setup (warp 0): maximum diameter -> side, inbox prefixes,
+    // fixed-point shifts
+    if (tid < 32) {
+      float dm = lane < C ? dmax_in[lane] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dm = fmaxf(dm, __shfl_xor_sync(~0u, dm, o));
+#pragma unroll
       for (int f = 0; f < 2; ++f) {
-        int acc = 0;
-        it.pre[f][0] = 0;
-        for (int s = 0; s < C; ++s) {
-          acc += min(cnt_in[f * C + s], P.cl_cap);
-          it.pre[f][s + 1] = acc;
+        const int c = lane < C ? min(cnt_in[f * C + lane], P.cl_cap) : 0;
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(~0u, x, o);
+          if (lane >= o) x += y;
         }
-        it.kin[f] = acc;
-        it.K[f] = acc + __ldcg(ovf_cnt + k * 2 + f);
-        // fixed-point shift: a pixel receives at most K contributions
-        it.shift[f] = shift_for(max(1, it.K[f]), P.amp_bound);
-        it.inv_scale[f] = 1.0f / (float)(1 << it.shift[f]);
+        if (lane < C) it.pre[f][lane + 1] = x;
+        const int kin = __shfl_sync(~0u, x, 31);
+        if (lane == 0) {
+          it.pre[f][0] = 0;
+          it.kin[f] = kin;
+          it.K[f] = kin + __ldcg(ovf_cnt + k * 2 + f);
+          // fixed-point shift: a pixel receives at most K contributions
+          it.shift[f] = shift_for(max(1, it.K[f]), P.amp_bound);
+          it.inv_scale[f] = 1.0f / (float)(1 << it.shift[f]);
+        }
       }
-      // window bound (as item_setup): floor(2 R_max) + 1 from the pair's largest
-      // sigma, unless frame-2 sigma jitter makes it unbounded
-      int wt = 2 * it.h + 1;
-      if (P.psf == kPsfPoint && !(g.f2_sigma_std > 0.f))
-        wt = min(wt, (int)floorf(2.0f * __fmul_rn(__fmul_rn(it.dmax, g.inv_ratio), kTightR)) + 1);
-      wt = max(1, wt);
-      const int sep = (g.rho_lo == 0.f && g.rho_span == 0.f && !(g.f2_rho_std > 0.f)) ? 1 : 0;
-      const int wm = (P.psf == kPsfPoint && sep && wt <= kMaxUnpredWM && wt - 1 <= P.pad_rows) ? wt : 0;
-      it.var = (P.psf == kPsfPoint ? 16 * sep : 0) + wm;
-      if (k == 0) {
-        PairHdr hd{};
-        hd.ppp = s_ppp;
-        hd.M = M;
-        hd.side = it.side;
-        hd.dmax = it.dmax;
-        write_stats(P, pl, hd);
+      if (lane == 0) {
+        // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
+        it.side = patch_side_exact(M > 0 ? (double)dm : g.d_hi, g.patch_mult);
+        it.dmax = M > 0 ? dm : (float)g.d_hi;
+        it.h = it.side >> 1;
+        if (k == 0) {
+          PairHdr hd{};
+          hd.ppp = s_ppp;
+          hd.M = M;
+          hd.side = it.side;
+          hd.dmax = it.dmax;
+          write_stats(P, pl, hd);
+        }
       }
     }
     __syncthreads();
-    if constexpr (PSF == kPsfErf) {
-      pair_splat<PSF, 0, 0, SIMPLE>(P, inbox, acc0, it, r0, r1, ovf_k);
+    // ---- phases B / C: splat the inbox, store (finalize) the rows, zeroing
+    if (seq) {
+      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 0, r0, r1, ovf_k);
+      __syncthreads();
+      band_store(P, acc0, pl, 0, r0, r1 - r0, 0, P.W, it.inv_scale[0]);
+      __syncthreads();
+      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 1, r0, r1, ovf_k + (size_t)P.n * RW);
+      __syncthreads();
+      if (tid < 2) ovf_cnt[k * 2 + tid] = 0;   // overflow region consumed (self-cleaning)
+      // the inbox and counts are consumed: sources may refill them (phase A
+      // of the next pair) once every CTA has arrived; the store overlaps that
+      cl_arrive();
+      band_store(P, acc0, pl, 1, r0, r1 - r0, 0, P.W, it.inv_scale[1]);
     } else {
-      switch (it.var) {
-#define PGB_PV(S, WW) case 16 * S + WW: pair_splat<PSF, S, WW, SIMPLE>(P, inbox, acc0, it, r0, r1, ovf_k); break;
-        PGB_PV(1, 1) PGB_PV(1, 2) PGB_PV(1, 3) PGB_PV(1, 4) PGB_PV(1, 5) PGB_PV(1, 6) PGB_PV(1, 7)
-        PGB_PV(1, 8) PGB_PV(1, 9) PGB_PV(1, 10) PGB_PV(1, 11) PGB_PV(1, 12)
-#undef PGB_PV
-        default: pair_splat<PSF, 0, 0, SIMPLE>(P, inbox, acc0, it, r0, r1, ovf_k); break;
-      }
+      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 0, r0, r1, ovf_k);
+      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc1, it, 1, r0, r1, ovf_k + (size_t)P.n * RW);
+      __syncthreads();
+      if (tid < 2) ovf_cnt[k * 2 + tid] = 0;
+      cl_arrive();
+      band_store(P, acc0, pl, 0, r0, r1 - r0, 0, P.W, it.inv_scale[0]);
+      band_store(P, acc1, pl, 1, r0, r1 - r0, 0, P.W, it.inv_scale[1]);
     }
-    __syncthreads();
-    if (tid < 2) ovf_cnt[k * 2 + tid] = 0;   // overflow region consumed (self-cleaning)
-    // the inbox and counts are consumed: sources may refill them (phase A of
-    // the next pair) once every CTA has arrived; the store overlaps that wait
-    cl_arrive();
-    // ---- phase C: finalize + store rows [r0, r1) of both frames, zeroing
-    band_store(P, acc0, pl, 0, r0, r1 - r0, 0, P.W, it.inv_scale[0]);
-    band_store(P, acc1, pl, 1, r0, r1 - r0, 0, P.W, it.inv_scale[1]);
     __syncthreads();
     cl_wait();
   }

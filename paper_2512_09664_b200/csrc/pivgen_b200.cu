@@ -121,10 +121,18 @@ template __global__ void inject_render_kernel<kPsfPoint>(const FusedParams);
 template __global__ void band_kernel<kPsfPoint>(const BandParams);
 template __global__ void band_kernel<kPsfErf>(const BandParams);
 template __global__ void inject_render_kernel<kPsfErf>(const FusedParams);
-template __global__ void pair_kernel<kPsfPoint, true>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, false>(const BandParams);
-template __global__ void pair_kernel<kPsfErf, true>(const BandParams);
-template __global__ void pair_kernel<kPsfErf, false>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 0>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 1>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 2>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 3>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 4>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 5>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 6>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 7>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, true, 8>(const BandParams);
+template __global__ void pair_kernel<kPsfPoint, false, 0>(const BandParams);
+template __global__ void pair_kernel<kPsfErf, true, 0>(const BandParams);
+template __global__ void pair_kernel<kPsfErf, false, 0>(const BandParams);
 
 // ----------------------------------------------------------------------------
 // Host side: errors, workspace, plan, launch
@@ -693,7 +701,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
 // the band law (stratified cells, band.cuh).
 // ---------------------------------------------------------------------------
 struct PairPlan {
-  int C, rows, AS, pad_rows, cap, hcfg, words;
+  int C, rows, AS, pad_rows, cap, hcfg, words, frames, wm;
   size_t smem;
 };
 
@@ -704,6 +712,19 @@ bool pair_simple(const pgb_config* c) {
   return c->rho_lo == 0.0 && c->rho_hi == 0.0 && !(c->f2_sigma_std > 0.0) && !(c->f2_rho_std > 0.0);
 }
 
+// Window bound of the unpredicated particle loop for every pair of the
+// configuration (item_setup's rule with the largest possible diameter), or 0.
+int pair_window_bound(const pgb_config* c, int hcfg, int pad_rows, bool simple) {
+  if (c->psf != PGB_PSF_POINT || !simple) return 0;
+  const float inv_ratio = (float)(1.0 / c->sigma_ratio);
+  volatile float dh = (float)c->d_hi;
+  volatile float sm = dh * inv_ratio;
+  volatile float Rm = sm * kTightR;
+  int wt = std::min(2 * hcfg + 1, (int)std::floor(2.0f * Rm) + 1);
+  wt = std::max(1, wt);
+  return (wt <= kPairMaxWM && wt - 1 <= pad_rows) ? wt : 0;
+}
+
 bool make_pair_plan(const pgb_config* c, PairPlan& p, int cap_override = 0) {
   const int H = c->height, W = c->width;
   if (H > 1024 || W > 1024) return false;   // Q20 records: |position| < 2048 px
@@ -711,6 +732,7 @@ bool make_pair_plan(const pgb_config* c, PairPlan& p, int cap_override = 0) {
   p.words = pair_simple(c) ? 1 : 2;
   p.AS = (W + 3) & ~3;
   p.pad_rows = std::min(kMaxUnpredWM - 1, 2 * p.hcfg);
+  p.wm = pair_window_bound(c, p.hcfg, p.pad_rows, p.words == 1);
   for (const size_t budget : {kPairSmem2, kPairSmem1}) {
     for (int C = 1; C <= kPairMaxCluster; ++C) {
       const int rows = (H + C - 1) / C;
@@ -719,16 +741,19 @@ bool make_pair_plan(const pgb_config* c, PairPlan& p, int cap_override = 0) {
       const double lam = per_src * std::min(1.0, (double)(rows + 2 * p.hcfg + 1) / (double)H);
       int cap = (int)std::ceil(lam + 5.0 * std::sqrt(lam) + 8.0);
       cap = (cap + 1) & ~1;
-      const PairSmem L = pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words);
+      const PairSmem L = pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, 2);
       if ((size_t)L.total <= budget) {
-        // the cluster size (rows per CTA) is fixed by the configuration: the
-        // fixed-point shift depends on it. A capacity override (tests: force
-        // the spill path) changes only the inbox size.
+        // the cluster size (rows per CTA) is fixed by the configuration (the
+        // fixed-point shift depends on it); the accumulator layout and a
+        // capacity override (tests: force the spill path) change only the
+        // schedule, never a bit of the images
         if (cap_override > 0) cap = cap_override;
         p.C = C;
         p.rows = rows;
         p.cap = cap;
-        p.smem = (size_t)pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words).total;
+        p.frames = 2;
+        if (const char* e = std::getenv("PGB_PAIR_FRAMES")) p.frames = std::atoi(e) == 1 ? 1 : 2;
+        p.smem = (size_t)pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, p.frames).total;
         return true;
       }
     }
@@ -748,9 +773,20 @@ int pair_cap_override() {
 
 using PairFn = void (*)(const BandParams);
 
-PairFn pair_fn(int psf, bool simple) {
-  if (psf == PGB_PSF_ERF) return simple ? pair_kernel<kPsfErf, true> : pair_kernel<kPsfErf, false>;
-  return simple ? pair_kernel<kPsfPoint, true> : pair_kernel<kPsfPoint, false>;
+PairFn pair_fn(int psf, bool simple, int wm) {
+  if (psf == PGB_PSF_ERF) return simple ? pair_kernel<kPsfErf, true, 0> : pair_kernel<kPsfErf, false, 0>;
+  if (!simple) return pair_kernel<kPsfPoint, false, 0>;
+  switch (wm) {
+    case 1: return pair_kernel<kPsfPoint, true, 1>;
+    case 2: return pair_kernel<kPsfPoint, true, 2>;
+    case 3: return pair_kernel<kPsfPoint, true, 3>;
+    case 4: return pair_kernel<kPsfPoint, true, 4>;
+    case 5: return pair_kernel<kPsfPoint, true, 5>;
+    case 6: return pair_kernel<kPsfPoint, true, 6>;
+    case 7: return pair_kernel<kPsfPoint, true, 7>;
+    case 8: return pair_kernel<kPsfPoint, true, 8>;
+    default: return pair_kernel<kPsfPoint, true, 0>;
+  }
 }
 
 // Resident clusters for a plan (cached per device / kernel / smem / size).
@@ -783,7 +819,7 @@ int pair_max_clusters(PairFn fn, const PairPlan& p) {
 
 void launch_pair(BandParams& P, const PairPlan& pp, const pgb_config* cfg, cudaStream_t stream) {
   const bool simple = pp.words == 1;
-  PairFn fn = pair_fn(cfg->psf, simple);
+  PairFn fn = pair_fn(cfg->psf, simple, pp.wm);
   const int maxc = pair_max_clusters(fn, pp);
   const int ncl = std::max(1, std::min(P.pairs, maxc));
   DevWork& w = work_for(stream);
@@ -798,6 +834,7 @@ void launch_pair(BandParams& P, const PairPlan& pp, const pgb_config* cfg, cudaS
   P.cl_rows = pp.rows;
   P.cl_cap = pp.cap;
   P.cl_hcfg = pp.hcfg;
+  P.cl_frames = pp.frames;
   // row -> owning CTA by multiply-shift, checked exact for every image row
   P.cl_rdiv = (uint32_t)(((1u << 20) + pp.rows - 1) / pp.rows);
   for (int r = 0; r < P.H; ++r)
