@@ -927,12 +927,7 @@ __device__ __forceinline__ void splat_dispatch_b(int wt, int sep, int* acc, int 
 template <int OUT, bool NOISE>
 __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, char* dst, uint32_t pix,
                                                 int f, uint32_t gpair, float inv_scale) {
-  // int -> float: exact two-ALU-op form below 2^23 (no conversion pipe), else I2F
-  float4 v;
-  if ((a.x | a.y | a.z | a.w) < (1 << 23))
-    v = make_float4(acc_to_float(a.x), acc_to_float(a.y), acc_to_float(a.z), acc_to_float(a.w));
-  else
-    v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
+  float4 v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
   if (OUT == kOutRaw) {
     v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
     __stcs(reinterpret_cast<float4*>(dst), v);

@@ -38,7 +38,7 @@
 
 namespace pgb {
 
-constexpr int kPairThreads = kBandThreads;   // band_store() strides kBandThreads threads
+constexpr int kPairThreads = 384;            // 12 warps; two CTAs per SM (<= 85 registers)
 constexpr int kPairMaxCluster = 8;           // portable cluster size
 
 __device__ __forceinline__ uint32_t cl_rank() {
@@ -125,25 +125,29 @@ struct RecW {
   static constexpr int kWords = SIMPLE ? 1 : 2;
 };
 
-// Byte offsets of the shared-memory regions (identical in every CTA).
+// Byte offsets of the shared-memory regions (identical in every CTA). The
+// inbox, its counts and the maximum diameters are double-buffered: pair k+1
+// is generated into buffer (k+1)&1 while buffer k&1 is being splatted.
 struct PairSmem {
   int acc_ints;     // (frames RB + pad_rows) AS + 8
-  int inbox_off;    // bytes
-  int cnt_in_off;   // [2][C] ints (written by the sources)
-  int dmax_in_off;  // [C] floats (written by the sources)
+  int inbox_off;    // bytes: [2 buffers][2 frames][C sources][cap] records
+  int cnt_in_off;   // [2][2][C] ints (written by the sources)
+  int dmax_in_off;  // [2][C] floats (written by the sources)
   int cnt_out_off;  // [2][C] ints (this CTA's slot counters)
   int total;
+  int buf_words;    // uint4 words per inbox buffer
 };
 
 // frames 2: both frame accumulators live at once; 1: one accumulator, frames in turn.
 __host__ __device__ __forceinline__ PairSmem pair_smem(int rows, int pad_rows, int AS, int C, int cap, int words,
-                                                       int frames = 2) {
+                                                       int frames = 1) {
   PairSmem s;
   s.acc_ints = (frames * rows + pad_rows) * AS + 8;
   s.inbox_off = ((s.acc_ints * 4) + 15) & ~15;
-  s.cnt_in_off = s.inbox_off + 2 * C * cap * words * 16;
-  s.dmax_in_off = s.cnt_in_off + 2 * C * 4;
-  s.cnt_out_off = s.dmax_in_off + C * 4;
+  s.buf_words = 2 * C * cap * words;
+  s.cnt_in_off = s.inbox_off + 2 * s.buf_words * 16;
+  s.dmax_in_off = s.cnt_in_off + 2 * 2 * C * 4;
+  s.cnt_out_off = s.dmax_in_off + 2 * C * 4;
   s.total = ((s.cnt_out_off + 2 * C * 4) + 15) & ~15;
   return s;
 }
@@ -254,86 +258,166 @@ __device__ __forceinline__ void pair_splat_frame(const BandParams& P, const uint
 // chosen per launch from the configuration (the largest sigma any pair can
 // have), so every kernel carries only the registers its variant needs.
 constexpr int kPairMaxWM = 8;
-#ifndef PGB_PAIR_MINB
-#define PGB_PAIR_MINB 3   // three CTAs per SM (<= 85 registers) when the plan's shared memory allows
-#endif
 
+// Rows [r0, r0 + nr) of frame f from the accumulator to the output
+// (finalize, optional uint16), zeroing it; kPairThreads threads.
+__device__ __forceinline__ void pair_store(const BandParams& P, int* acc, int pl, int f, int r0, int nr,
+                                           float inv_scale) {
+  if (nr <= 0) return;
+  if ((P.W & 3) == 0 && P.AS == P.W) {
+    const bool noise = P.noise_std > 0.f;
+    const int t = threadIdx.x;
+    switch (P.out_mode) {
+      case kOutRaw: band_store_lin<kOutRaw, false>(P, acc, pl, f, r0, nr, inv_scale, t, kPairThreads); return;
+      case kOutF32:
+        if (noise) band_store_lin<kOutF32, true>(P, acc, pl, f, r0, nr, inv_scale, t, kPairThreads);
+        else band_store_lin<kOutF32, false>(P, acc, pl, f, r0, nr, inv_scale, t, kPairThreads);
+        return;
+      default:
+        if (noise) band_store_lin<kOutU16, true>(P, acc, pl, f, r0, nr, inv_scale, t, kPairThreads);
+        else band_store_lin<kOutU16, false>(P, acc, pl, f, r0, nr, inv_scale, t, kPairThreads);
+        return;
+    }
+  }
+  // widths that are not a multiple of 4: one pixel per thread
+  const uint32_t gpair = (uint32_t)(P.pair_base + pl);
+  const size_t pair_off = (size_t)pl * (size_t)P.out_pair_elems;
+  const int total = nr * P.W;
+  for (int e = threadIdx.x; e < total; e += kPairThreads) {
+    const int row = e / P.W, col = e - (e / P.W) * P.W;
+    int* ap = acc + row * P.AS + col;
+    float v = (float)*ap * inv_scale;
+    *ap = 0;
+    const size_t p = (size_t)(r0 + row) * P.W + (size_t)col;
+    if (P.out_mode == kOutRaw) {
+      static_cast<float*>(P.out[f])[pair_off + p] = v;
+    } else {
+      float nzv = 0.f;
+      if (P.noise_std > 0.f) {
+        const float4 nz = noise4_rk(P.g.rk, gpair, P.batch_lo, (uint32_t)f + 1, (uint32_t)(p >> 2));
+        const int jn = (int)(p & 3);
+        nzv = jn == 0 ? nz.x : (jn == 1 ? nz.y : (jn == 2 ? nz.z : nz.w));
+      }
+      v = finalize_px(v, P.bg_offset, P.noise_std, nzv);
+      if (P.out_mode == kOutF32) static_cast<float*>(P.out[f])[pair_off + p] = v;
+      else static_cast<uint16_t*>(P.out[f])[pair_off + p] = quant_u16(v);
+    }
+  }
+}
+
+template <bool SIMPLE>
+struct PairCtx {
+  int C, k;
+  unsigned char* smem;
+  PairSmem L;
+  int* cnt_out;
+  int* ovf_cnt;   // this cluster's [2 buffers][C][2]
+  uint4* ovf;     // this cluster's [2 buffers][C][2][n] records
+};
+
+// Phase A of pair `pl` into inbox buffer b: generate this CTA's share of the
+// particles and route their records; publish counts and the maximum diameter.
+template <bool SIMPLE>
+__device__ __forceinline__ void pair_phase_a(const BandParams& P, const PairCtx<SIMPLE>& X, int pl, int b,
+                                             int* s_M, double* s_ppp, unsigned* s_dmax) {
+  constexpr int RW = RecW<SIMPLE>::kWords;
+  const GenCfg& g = P.g;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int C = X.C, k = X.k;
+  const RngKey key = band_key(P, pl);
+  if (tid == 0) {
+    // seeding density and active count (particles.py:73-83)
+    const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
+    const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
+    double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+    mm = fmin(fmax(mm, 0.0), (double)P.n);
+    s_M[b] = (int)mm;
+    s_ppp[b] = ppp;
+    *s_dmax = 0u;
+  }
+  __syncthreads();
+  const int M = s_M[b];
+  const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
+  uint4* my_box = reinterpret_cast<uint4*>(X.smem + X.L.inbox_off) + (size_t)b * X.L.buf_words +
+                  (size_t)k * P.cl_cap * RW;   // [b][f = 0][k] region
+  int* ovf_cnt = X.ovf_cnt + b * C * 2;
+  uint4* ovf = X.ovf + (size_t)b * C * 2 * P.n * RW;
+  unsigned dloc = 0u;
+  for (int gi = k * kPairThreads + tid; gi < M; gi += C * kPairThreads) {
+    PairPart pp;
+    pair_particle(g, key, gi, flow, pp);
+    dloc = max(dloc, __float_as_uint(pp.d));   // d >= 0: float order == bit order
+    const Look& lk = pp.lk;
+    if (lk.vis1 && lk.amp1 > 0.f)
+      pair_route<SIMPLE>(P, my_box, X.cnt_out, 0, pp.xq1, pp.yq1, pp.sig, pp.sig, lk.rho1, lk.amp1, ovf_cnt, ovf);
+    if (lk.vis2 && lk.amp2 > 0.f)
+      pair_route<SIMPLE>(P, my_box, X.cnt_out, 1, pp.xq2, pp.yq2, lk.sx2, lk.sy2, lk.rho2, lk.amp2, ovf_cnt, ovf);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dloc = max(dloc, __shfl_xor_sync(~0u, dloc, o));
+  if (lane == 0 && dloc) atomicMax(s_dmax, dloc);
+  __syncthreads();
+  // publish this source's counts and maximum diameter to every destination
+  int* cnt_in = reinterpret_cast<int*>(X.smem + X.L.cnt_in_off) + b * 2 * C;
+  float* dmax_in = reinterpret_cast<float*>(X.smem + X.L.dmax_in_off) + b * C;
+  if (tid < 2 * C) {
+    const int f = tid / C, d = tid - f * C;
+    cl_st1(cl_map(cnt_in + f * C + k, (uint32_t)d), (uint32_t)X.cnt_out[tid]);
+  } else if (tid >= 64 && tid < 64 + C) {
+    cl_st1(cl_map(dmax_in + k, (uint32_t)(tid - 64)), *s_dmax);
+  }
+  __syncthreads();
+  if (tid < 2 * C) X.cnt_out[tid] = 0;
+}
+
+// Per-pair kernel loop (pipelined over the cluster's pairs, one cluster
+// barrier per pair):
+//   A(first); barrier
+//   for each pair k:  setup(k); B_1(k); C_1(k); B_2(k); A(k+1) -> buffer (k+1)&1;
+//                     arrive; C_2(k); wait
+// A(k+1) writes the buffer B(k-1) read: every destination finished B(k-1)
+// before arriving at barrier k (after its A(k)); B(k+1) reads what A(k+1)
+// wrote before barrier k+1. The store of frame 2 overlaps the barrier.
 template <int PSF, bool SIMPLE, int WM>
-__global__ void __launch_bounds__(kPairThreads, PGB_PAIR_MINB) pair_kernel(const BandParams P) {
+__global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ PairItem it;
   __shared__ unsigned s_dmax;
-  __shared__ int s_M;
-  __shared__ double s_ppp;
+  __shared__ int s_M[2];
+  __shared__ double s_ppp[2];
   constexpr int RW = RecW<SIMPLE>::kWords;
   constexpr int SEP = (PSF == kPsfPoint && WM > 0) ? 1 : 0;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int C = P.cl_size;
-  const int k = (int)cl_rank();
-  const bool seq = P.cl_frames == 1;   // one accumulator, frames in turn
-  const PairSmem L = pair_smem(P.cl_rows, P.pad_rows, P.AS, C, P.cl_cap, RW, P.cl_frames);
-  int* acc0 = reinterpret_cast<int*>(smem);
-  int* acc1 = seq ? acc0 : acc0 + P.cl_rows * P.AS;
-  int* cnt_in = reinterpret_cast<int*>(smem + L.cnt_in_off);
-  float* dmax_in = reinterpret_cast<float*>(smem + L.dmax_in_off);
-  int* cnt_out = reinterpret_cast<int*>(smem + L.cnt_out_off);
+  PairCtx<SIMPLE> X;
+  X.C = P.cl_size;
+  X.k = (int)cl_rank();
+  X.smem = smem;
+  X.L = pair_smem(P.cl_rows, P.pad_rows, P.AS, X.C, P.cl_cap, RW, 1);
+  X.cnt_out = reinterpret_cast<int*>(smem + X.L.cnt_out_off);
+  const int C = X.C, k = X.k;
   const int cid = (int)cl_id(), ncl = (int)cl_count();
-  int* ovf_cnt = P.cl_ovf_cnt + (size_t)cid * C * 2;
-  uint4* ovf = P.cl_ovf + (size_t)cid * C * 2 * P.n * RW;
+  X.ovf_cnt = P.cl_ovf_cnt + (size_t)cid * 2 * C * 2;
+  X.ovf = P.cl_ovf + (size_t)cid * 2 * C * 2 * P.n * RW;
+  int* acc = reinterpret_cast<int*>(smem);
   const int r0 = k * P.cl_rows, r1 = min(P.H, r0 + P.cl_rows);
-  uint4* my_box = reinterpret_cast<uint4*>(smem + L.inbox_off) + (size_t)k * P.cl_cap * RW;   // [f][k] region
-  const uint4* inbox = reinterpret_cast<const uint4*>(smem + L.inbox_off);
-  const uint4* ovf_k = ovf + (size_t)k * 2 * P.n * RW;
-  for (int e = tid; e < L.acc_ints / 4; e += kPairThreads) reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
-  if (tid < 2 * C) cnt_out[tid] = 0;
+  for (int e = tid; e < X.L.acc_ints / 4; e += kPairThreads) reinterpret_cast<int4*>(acc)[e] = make_int4(0, 0, 0, 0);
+  if (tid < 2 * C) X.cnt_out[tid] = 0;
   // every CTA of the cluster runs before anyone writes into its shared memory
   cl_arrive();
   cl_wait();
   const GenCfg& g = P.g;
-  for (int pl = cid; pl < P.pairs; pl += ncl) {
-    const RngKey key = band_key(P, pl);
-    if (tid == 0) {
-      // seeding density and active count (particles.py:73-83)
-      const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
-      const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
-      double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
-      mm = fmin(fmax(mm, 0.0), (double)P.n);
-      s_M = (int)mm;
-      s_ppp = ppp;
-      s_dmax = 0u;
-    }
-    const float2* flow = P.flows + (size_t)((P.pair_base + pl) / P.pairs_per_field) * P.field_elems;
-    __syncthreads();
-    const int M = s_M;
-    // ---- phase A: generate this CTA's share of the particles, route records
-    unsigned dloc = 0u;
-    for (int gi = k * kPairThreads + tid; gi < M; gi += C * kPairThreads) {
-      PairPart pp;
-      pair_particle(g, key, gi, flow, pp);
-      dloc = max(dloc, __float_as_uint(pp.d));   // d >= 0: float order == bit order
-      const Look& lk = pp.lk;
-      if (lk.vis1 && lk.amp1 > 0.f)
-        pair_route<SIMPLE>(P, my_box, cnt_out, 0, pp.xq1, pp.yq1, pp.sig, pp.sig, lk.rho1, lk.amp1, ovf_cnt, ovf);
-      if (lk.vis2 && lk.amp2 > 0.f)
-        pair_route<SIMPLE>(P, my_box, cnt_out, 1, pp.xq2, pp.yq2, lk.sx2, lk.sy2, lk.rho2, lk.amp2, ovf_cnt, ovf);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dloc = max(dloc, __shfl_xor_sync(~0u, dloc, o));
-    if (lane == 0 && dloc) atomicMax(&s_dmax, dloc);
-    __syncthreads();
-    // publish this source's counts and maximum diameter to every destination
-    if (tid < 2 * C) {
-      const int f = tid / C, d = tid - f * C;
-      cl_st1(cl_map(cnt_in + f * C + k, (uint32_t)d), (uint32_t)cnt_out[tid]);
-    } else if (tid >= 64 && tid < 64 + C) {
-      cl_st1(cl_map(dmax_in + k, (uint32_t)(tid - 64)), s_dmax);
-    }
-    __syncthreads();
-    if (tid < 2 * C) cnt_out[tid] = 0;
-    cl_arrive();
-    cl_wait();
-    // ---- phase B setup (warp 0): maximum diameter -> side, inbox prefixes,
-    // fixed-point shifts
+  int pl = cid, b = 0;
+  if (pl < P.pairs) pair_phase_a<SIMPLE>(P, X, pl, 0, s_M, s_ppp, &s_dmax);
+  cl_arrive();
+  cl_wait();
+  for (; pl < P.pairs; pl += ncl, b ^= 1) {
+    const int M = s_M[b];
+    const int* cnt_in = reinterpret_cast<const int*>(smem + X.L.cnt_in_off) + b * 2 * C;
+    const float* dmax_in = reinterpret_cast<const float*>(smem + X.L.dmax_in_off) + b * C;
+    int* ovf_cnt_b = X.ovf_cnt + b * C * 2;
+    const uint4* inbox = reinterpret_cast<const uint4*>(smem + X.L.inbox_off) + (size_t)b * X.L.buf_words;
+    const uint4* ovf_k = X.ovf + ((size_t)b * C * 2 + (size_t)k * 2) * P.n * RW;
+    // ---- setup (warp 0): maximum diameter -> side, inbox prefixes, shifts
     if (tid < 32) {
       float dm = lane < C ? dmax_in[lane] : 0.f;
 #pragma unroll
@@ -352,7 +436,7 @@ __global__ void __launch_bounds__(kPairThreads, PGB_PAIR_MINB) pair_kernel(const
         if (lane == 0) {
           it.pre[f][0] = 0;
           it.kin[f] = kin;
-          it.K[f] = kin + __ldcg(ovf_cnt + k * 2 + f);
+          it.K[f] = kin + __ldcg(ovf_cnt_b + k * 2 + f);
           // fixed-point shift: a pixel receives at most K contributions
           it.shift[f] = shift_for(max(1, it.K[f]), P.amp_bound);
           it.inv_scale[f] = 1.0f / (float)(1 << it.shift[f]);
@@ -365,7 +449,7 @@ __global__ void __launch_bounds__(kPairThreads, PGB_PAIR_MINB) pair_kernel(const
         it.h = it.side >> 1;
         if (k == 0) {
           PairHdr hd{};
-          hd.ppp = s_ppp;
+          hd.ppp = s_ppp[b];
           hd.M = M;
           hd.side = it.side;
           hd.dmax = it.dmax;
@@ -374,28 +458,19 @@ __global__ void __launch_bounds__(kPairThreads, PGB_PAIR_MINB) pair_kernel(const
       }
     }
     __syncthreads();
-    // ---- phases B / C: splat the inbox, store (finalize) the rows, zeroing
-    if (seq) {
-      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 0, r0, r1, ovf_k);
-      __syncthreads();
-      band_store(P, acc0, pl, 0, r0, r1 - r0, 0, P.W, it.inv_scale[0]);
-      __syncthreads();
-      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 1, r0, r1, ovf_k + (size_t)P.n * RW);
-      __syncthreads();
-      if (tid < 2) ovf_cnt[k * 2 + tid] = 0;   // overflow region consumed (self-cleaning)
-      // the inbox and counts are consumed: sources may refill them (phase A
-      // of the next pair) once every CTA has arrived; the store overlaps that
-      cl_arrive();
-      band_store(P, acc0, pl, 1, r0, r1 - r0, 0, P.W, it.inv_scale[1]);
-    } else {
-      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc0, it, 0, r0, r1, ovf_k);
-      pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc1, it, 1, r0, r1, ovf_k + (size_t)P.n * RW);
-      __syncthreads();
-      if (tid < 2) ovf_cnt[k * 2 + tid] = 0;
-      cl_arrive();
-      band_store(P, acc0, pl, 0, r0, r1 - r0, 0, P.W, it.inv_scale[0]);
-      band_store(P, acc1, pl, 1, r0, r1 - r0, 0, P.W, it.inv_scale[1]);
-    }
+    // ---- B_1, C_1, B_2: the accumulator holds one frame at a time
+    pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc, it, 0, r0, r1, ovf_k);
+    __syncthreads();
+    pair_store(P, acc, pl, 0, r0, r1 - r0, it.inv_scale[0]);
+    __syncthreads();
+    pair_splat_frame<PSF, SEP, WM, SIMPLE>(P, inbox, acc, it, 1, r0, r1, ovf_k + (size_t)P.n * RW);
+    __syncthreads();
+    if (tid < 2) ovf_cnt_b[k * 2 + tid] = 0;   // spill lists of buffer b consumed (self-cleaning)
+    // ---- A(next pair) into the other buffer, while slower CTAs finish B(k)
+    if (pl + ncl < P.pairs) pair_phase_a<SIMPLE>(P, X, pl + ncl, b ^ 1, s_M, s_ppp, &s_dmax);
+    cl_arrive();
+    // ---- C_2: store frame 2 while the barrier completes
+    pair_store(P, acc, pl, 1, r0, r1 - r0, it.inv_scale[1]);
     __syncthreads();
     cl_wait();
   }

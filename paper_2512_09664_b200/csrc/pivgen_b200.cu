@@ -735,25 +735,27 @@ bool make_pair_plan(const pgb_config* c, PairPlan& p, int cap_override = 0) {
   p.wm = pair_window_bound(c, p.hcfg, p.pad_rows, p.words == 1);
   for (const size_t budget : {kPairSmem2, kPairSmem1}) {
     for (int C = 1; C <= kPairMaxCluster; ++C) {
+      // PGB_PAIR_C: experiments only (the cluster size changes the fixed-point shift)
+      if (const char* e = std::getenv("PGB_PAIR_C"))
+        if (std::atoi(e) > C) continue;
       const int rows = (H + C - 1) / C;
       if ((H + rows - 1) / rows != C) continue;   // every CTA owns rows
       const double per_src = std::ceil((double)c->n_capacity / C);
       const double lam = per_src * std::min(1.0, (double)(rows + 2 * p.hcfg + 1) / (double)H);
-      int cap = (int)std::ceil(lam + 5.0 * std::sqrt(lam) + 8.0);
+      // inbox capacity ~ lambda + 3 sigma: fuller regions spill to L2 (exact)
+      int cap = (int)std::ceil(lam + 3.0 * std::sqrt(lam) + 4.0);
       cap = (cap + 1) & ~1;
-      const PairSmem L = pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, 2);
+      const PairSmem L = pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, 1);
       if ((size_t)L.total <= budget) {
         // the cluster size (rows per CTA) is fixed by the configuration (the
-        // fixed-point shift depends on it); the accumulator layout and a
-        // capacity override (tests: force the spill path) change only the
-        // schedule, never a bit of the images
+        // fixed-point shift depends on it); a capacity override (tests: force
+        // the spill path) changes only the schedule, never a bit of the images
         if (cap_override > 0) cap = cap_override;
         p.C = C;
         p.rows = rows;
         p.cap = cap;
-        p.frames = 2;
-        if (const char* e = std::getenv("PGB_PAIR_FRAMES")) p.frames = std::atoi(e) == 1 ? 1 : 2;
-        p.smem = (size_t)pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, p.frames).total;
+        p.frames = 1;
+        p.smem = (size_t)pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, 1).total;
         return true;
       }
     }
@@ -823,8 +825,8 @@ void launch_pair(BandParams& P, const PairPlan& pp, const pgb_config* cfg, cudaS
   const int maxc = pair_max_clusters(fn, pp);
   const int ncl = std::max(1, std::min(P.pairs, maxc));
   DevWork& w = work_for(stream);
-  const size_t cnt_bytes = (size_t)ncl * pp.C * 2 * sizeof(int);
-  const size_t ovf_bytes = (size_t)ncl * pp.C * 2 * (size_t)P.n * pp.words * 16;
+  const size_t cnt_bytes = (size_t)ncl * 2 * pp.C * 2 * sizeof(int);            // [cluster][buffer][C][frame]
+  const size_t ovf_bytes = (size_t)ncl * 2 * pp.C * 2 * (size_t)P.n * pp.words * 16;
   unsigned gen_before = 0, gen_after = 0;
   void* cnt = ensure(w.pair_cnt, w.pair_cnt_bytes, cnt_bytes, &gen_after);
   if (gen_after != gen_before) PGB_CK(cudaMemsetAsync(cnt, 0, w.pair_cnt_bytes, stream));
