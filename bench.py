@@ -354,10 +354,7 @@ def run_ours(args):
     cfg = make_cfg(pg, name, global_batch)
     lib = _lib.load()
     ncfg = native_config(cfg)
-    law = pg.generation_law(cfg)
-    kernel_label = ("pgb::pair_kernel<PSF, REC> (one thread-block cluster per image pair, DSMEM record "
-                    "exchange; one launch per batch)" if law == "pair" else
-                    "pgb::band_kernel<PSF> (screen-tile items, in-kernel prologue; one launch per batch)")
+    kernel_label = "pgb::band_kernel<PSF> (screen-tile items, in-kernel prologue tickets; one launch per batch)"
     field = pg.from_function(vortex(H, W) if CONFIGS[name][5] == "vortex" else uniform, H, W)
     flows = field.to_device(dev).unsqueeze(0).contiguous()
     u16 = False

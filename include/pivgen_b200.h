@@ -62,17 +62,6 @@ enum pgb_out_mode {
   PGB_OUT_ACCUM = 3     /* out += raw (float32, in place; _native.splat_accumulate)       */
 };
 
-/* Seeding law of the generator for a configuration (pgb_generation_law). Both
- * draw the reference's law (particles.py:61-101: M iid uniform positions, iid
- * uniform diameters); they differ in how Philox streams map to particles:
- *   PGB_LAW_PAIR: particle g at an iid uniform position, all its draws keyed
- *                 by g (one cluster generates the whole pair; pair.cuh);
- *   PGB_LAW_BAND: stratified cells (multinomial cell counts, particle g in
- *                 the cell whose prefix holds g) and the maximum diameter
- *                 drawn first, so screen tiles can regenerate their particles
- *                 (band.cuh). */
-enum pgb_law { PGB_LAW_BAND = 0, PGB_LAW_PAIR = 1 };
-
 /* Generator configuration (mirror of config.py:83-108 plus extensions). */
 typedef struct pgb_config {
   int32_t height, width;            /* image_height, image_width                      */
@@ -114,11 +103,6 @@ typedef struct pgb_pair_stats {
 
 int pgb_abi_version(void);
 const char* pgb_last_error(void);
-
-/* enum pgb_law used for `cfg` (a pure function of the configuration: the pair
- * law when one image pair fits a thread-block cluster's shared memory); -1 on
- * an invalid configuration. Host only. */
-int pgb_generation_law(const pgb_config* cfg);
 
 /* Smallest odd side >= ceil(round(multiplier * max_diameter + 1, 9)) (raster.py:30-38). */
 int pgb_patch_side(double max_diameter, double multiplier);

@@ -12,15 +12,6 @@ it implements:
   apply_hiding        particles.py:139-147
   patch_side          raster.py:30-38 (+ pipeline.py:291-294 for d_max)
 
-Two generation laws, chosen by the generator from the configuration
-(pgb_generation_law; GenConfig.law here):
-
-* law="pair" (csrc/pair.cuh: one thread-block cluster per pair): particle g
-  at X = 2 floor(w_x W 2^16 / 2^32) + 1 (Q17, iid uniform on [0, W)), its
-  diameter from unit23(w_z), every draw keyed by g -- the reference's law
-  draw for draw; d_max = max over the M active diameters.
-* law="band" (csrc/band.cuh):
-
 Stratified seeding (same law as iid uniform positions): the image is split
 into 2^sy x 2^sx equal-area cells; the cell counts are the histogram of M iid
 uniform labels, particle g sits in the cell whose prefix range holds g, at a
@@ -97,7 +88,6 @@ class GenConfig:
     f2_i0_std: float = 0.0
     hide_probability: float = 0.0
     laser: dict | None = None   # {dz0, shape, q, z_lo, z_hi, w}
-    law: str = "band"           # "band" | "pair" (the generator's pgb_generation_law)
 
     @property
     def n(self) -> int:
@@ -212,9 +202,8 @@ def rexp(y: float) -> float:
     return math.ldexp(p, int(k))
 
 
-def pair_header(cfg: "GenConfig", batch: int, gpair: int, draw_max: bool = True) -> dict:
-    """prologue_kernel thread 0: density, M, maximum-diameter draw (band law),
-    patch side."""
+def pair_header(cfg: "GenConfig", batch: int, gpair: int) -> dict:
+    """prologue_kernel thread 0: density, M, maximum-diameter draw, patch side."""
     n = cfg.n
     H, W = cfg.height, cfg.width
     w = px.draw(cfg.seed, gpair, batch, np.uint64(0), px.TAG_PAIR)
@@ -222,7 +211,7 @@ def pair_header(cfg: "GenConfig", batch: int, gpair: int, draw_max: bool = True)
     m = int(np.rint(ppp * H * W))
     m = min(max(m, 0), n)
     hd = dict(ppp=ppp, M=m, m=0.0, J=0, qmax=0, dmax=float(np.float32(cfg.d_range[1])))
-    if m > 0 and draw_max:
+    if m > 0:
         v = px.draw(cfg.seed, gpair, batch, np.uint64(1), px.TAG_PAIR)
         V = float(px.u53_to_unit(v[0], v[1]))
         mu = rexp(rlog(V) / float(m))
@@ -259,46 +248,29 @@ def cell_coord(cell, w, size: int, bits: int) -> np.ndarray:
 
 
 def sample_pair(cfg: GenConfig, batch: int, gpair: int, flow_uv: np.ndarray) -> dict:
-    """All per-particle arrays of one pair, exactly as the generator produces
-    them (csrc/pair.cuh pair_particle for law "pair", csrc/band.cuh
-    seed_particle for law "band"): fixed-point positions, float32 attributes
-    and advection."""
+    """All per-particle arrays of one pair, exactly as csrc/band.cuh seed_particle()
+    produces them: stratified fixed-point positions, float32 attributes and advection."""
     n = cfg.n
     H, W = cfg.height, cfg.width
     idx = np.arange(n, dtype=np.uint64)
-    active = None
     a = px.draw(cfg.seed, gpair, batch, idx, px.TAG_PARTICLE_A)
-    if cfg.law == "pair":
-        hd = pair_header(cfg, batch, gpair, draw_max=False)
-        ppp, m = hd["ppp"], hd["M"]
-        pre = None
-        active = np.arange(n) < m
-        X = cell_coord(0, a[0], W, 0)
-        Y = cell_coord(0, a[1], H, 0)
-        d = lerp32(cfg.d_range[0], cfg.d_range[1], unit23(a[2])).astype(F32)
-        if m > 0:
-            hd["dmax"] = float(d[:m].max())
-        hd["side"] = patch_side(hd["dmax"] if m > 0 else cfg.d_range[1], cfg.patch_multiplier)
-    elif cfg.law == "band":
-        hd = pair_header(cfg, batch, gpair)
-        ppp, m = hd["ppp"], hd["M"]
-        sy, sx = cell_bits(H, W)
-        pre = cell_prefix(cfg, batch, gpair, m)
-        active = np.arange(n) < m
-        cell = np.searchsorted(pre, np.arange(n), side="right") - 1
-        cell = np.where(active, np.minimum(cell, (1 << (sy + sx)) - 1), 0)
-        cy, cx = cell >> sx, cell & ((1 << sx) - 1)
-        X = np.where(active, cell_coord(cx, a[0], W, sx), cell_coord(0, a[0], W, 0))
-        Y = np.where(active, cell_coord(cy, a[1], H, sy), cell_coord(0, a[1], H, 0))
-        # diameters: particle J holds the maximum quantile qmax, the others are
-        # uniform on [0, qmax]: floor(w (qmax + 1) / 2^32)
-        q = (a[2].astype(np.int64) * (hd["qmax"] + 1)) >> 32
-        if m > 0:
-            q[hd["J"]] = hd["qmax"]
-        d = np.where(active, lerp32(cfg.d_range[0], cfg.d_range[1], q_unit(q)),
-                     lerp32(cfg.d_range[0], cfg.d_range[1], unit23(a[2]))).astype(F32)
-    else:
-        raise ValueError(f"unknown law {cfg.law!r}")
+    hd = pair_header(cfg, batch, gpair)
+    ppp, m = hd["ppp"], hd["M"]
+    sy, sx = cell_bits(H, W)
+    pre = cell_prefix(cfg, batch, gpair, m)
+    active = np.arange(n) < m
+    cell = np.searchsorted(pre, np.arange(n), side="right") - 1
+    cell = np.where(active, np.minimum(cell, (1 << (sy + sx)) - 1), 0)
+    cy, cx = cell >> sx, cell & ((1 << sx) - 1)
+    X = np.where(active, cell_coord(cx, a[0], W, sx), cell_coord(0, a[0], W, 0))
+    Y = np.where(active, cell_coord(cy, a[1], H, sy), cell_coord(0, a[1], H, 0))
+    # diameters: particle J holds the maximum quantile qmax, the others are
+    # uniform on [0, qmax]: floor(w (qmax + 1) / 2^32)
+    q = (a[2].astype(np.int64) * (hd["qmax"] + 1)) >> 32
+    if m > 0:
+        q[hd["J"]] = hd["qmax"]
+    d = np.where(active, lerp32(cfg.d_range[0], cfg.d_range[1], q_unit(q)),
+                 lerp32(cfg.d_range[0], cfg.d_range[1], unit23(a[2]))).astype(F32)
     i0 = lerp32(cfg.i0_range[0], cfg.i0_range[1], unit23(a[3]))
     need_b = (cfg.rho_range[0] != cfg.rho_range[1]) or cfg.hide_probability > 0 or cfg.laser is not None
     if need_b:

@@ -17,8 +17,6 @@ PSF_POINT, PSF_ERF = 0, 1
 OUT_RAW, OUT_F32, OUT_U16, OUT_ACCUM = 0, 1, 2, 3
 
 PSF_CODES = {"point": PSF_POINT, "erf": PSF_ERF}
-LAW_BAND, LAW_PAIR = 0, 1
-LAW_NAMES = {LAW_BAND: "band", LAW_PAIR: "pair"}
 
 
 class BackendUnavailable(RuntimeError):
@@ -76,7 +74,6 @@ SIGNATURES = {
     "pgb_abi_version": (_I, []),
     "pgb_last_error": (C.c_char_p, []),
     "pgb_patch_side": (_I, [_D, _D]),
-    "pgb_generation_law": (_I, [C.POINTER(PgbConfig)]),
     "pgb_splat_accumulate": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I, _P, _I, _I, _I, _I]),
     "pgb_splat_accumulate_dev": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I, _P, _I, _I, _I, _I, _I, _P]),
     "pgb_render_pairs_dev": (_I, [C.POINTER(PgbParticles), C.POINTER(PgbParticles), _I64, _I,

@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libpivgen_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 SOURCES = ["pivgen_b200.cu"]
-HEADERS = ["common.cuh", "fused.cuh", "band.cuh", "histmatch.cuh", "refrng.cuh", "wide.cuh", "probes.cuh", "pair.cuh"]
+HEADERS = ["common.cuh", "fused.cuh", "band.cuh", "histmatch.cuh", "refrng.cuh", "wide.cuh", "probes.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

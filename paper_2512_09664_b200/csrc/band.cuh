@@ -99,11 +99,6 @@ struct BandParams {
   int* st_side;
   float* st_dmax;
   int* ticket;
-  // pair (cluster) kernel, pair.cuh
-  int cl_size, cl_rows, cl_cap, cl_hcfg, cl_frames;
-  uint32_t cl_rdiv;            // row -> owning CTA: (row * cl_rdiv) >> 20 == row / cl_rows (exact, host-checked)
-  int* cl_ovf_cnt;             // [clusters][C][2] spilled records per (destination, frame)
-  uint4* cl_ovf;               // [clusters][C][2][n][record words]
 };
 
 // Per-pair cell prefix stride (ints): ncell + 1 entries, padded for 16-byte rows.

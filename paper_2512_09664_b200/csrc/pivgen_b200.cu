@@ -25,7 +25,6 @@
 #include "refrng.cuh"
 #include "wide.cuh"
 #include "probes.cuh"
-#include "pair.cuh"
 
 namespace pgb {
 
@@ -121,18 +120,6 @@ template __global__ void inject_render_kernel<kPsfPoint>(const FusedParams);
 template __global__ void band_kernel<kPsfPoint>(const BandParams);
 template __global__ void band_kernel<kPsfErf>(const BandParams);
 template __global__ void inject_render_kernel<kPsfErf>(const FusedParams);
-template __global__ void pair_kernel<kPsfPoint, true, 0>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 1>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 2>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 3>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 4>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 5>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 6>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 7>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, true, 8>(const BandParams);
-template __global__ void pair_kernel<kPsfPoint, false, 0>(const BandParams);
-template __global__ void pair_kernel<kPsfErf, true, 0>(const BandParams);
-template __global__ void pair_kernel<kPsfErf, false, 0>(const BandParams);
 
 // ----------------------------------------------------------------------------
 // Host side: errors, workspace, plan, launch
@@ -247,12 +234,6 @@ struct DevWork {
   int head_next = 0;
   size_t head_bytes = 0;
   unsigned head_gen = 0;
-  // pair kernel spill buffers (overflow counters are self-cleaning: zeroed
-  // when allocated, reset by the kernel after use)
-  void* pair_ovf = nullptr;
-  size_t pair_ovf_bytes = 0;
-  void* pair_cnt = nullptr;
-  size_t pair_cnt_bytes = 0;
   // host-API staging
   void* stage = nullptr;
   size_t stage_bytes = 0;
@@ -694,171 +675,6 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   PGB_CK(cudaGetLastError());
 }
 
-// ---------------------------------------------------------------------------
-// Pair (cluster) kernel plan. The generation law is a pure function of the
-// configuration (fixed B200 budgets, no device queries): the pair law (iid
-// positions, pair.cuh) when one pair fits in a cluster's shared memory, else
-// the band law (stratified cells, band.cuh).
-// ---------------------------------------------------------------------------
-struct PairPlan {
-  int C, rows, AS, pad_rows, cap, hcfg, words, frames, wm;
-  size_t smem;
-};
-
-constexpr size_t kPairSmem2 = 112 * 1024;   // two CTAs per SM (228 KB - reservations)
-constexpr size_t kPairSmem1 = 220 * 1024;   // one CTA per SM
-
-bool pair_simple(const pgb_config* c) {
-  return c->rho_lo == 0.0 && c->rho_hi == 0.0 && !(c->f2_sigma_std > 0.0) && !(c->f2_rho_std > 0.0);
-}
-
-// Window bound of the unpredicated particle loop for every pair of the
-// configuration (item_setup's rule with the largest possible diameter), or 0.
-int pair_window_bound(const pgb_config* c, int hcfg, int pad_rows, bool simple) {
-  if (c->psf != PGB_PSF_POINT || !simple) return 0;
-  const float inv_ratio = (float)(1.0 / c->sigma_ratio);
-  volatile float dh = (float)c->d_hi;
-  volatile float sm = dh * inv_ratio;
-  volatile float Rm = sm * kTightR;
-  int wt = std::min(2 * hcfg + 1, (int)std::floor(2.0f * Rm) + 1);
-  wt = std::max(1, wt);
-  return (wt <= kPairMaxWM && wt - 1 <= pad_rows) ? wt : 0;
-}
-
-bool make_pair_plan(const pgb_config* c, PairPlan& p, int cap_override = 0) {
-  const int H = c->height, W = c->width;
-  if (H > 1024 || W > 1024) return false;   // Q20 records: |position| < 2048 px
-  p.hcfg = patch_side_exact(c->d_hi, c->patch_multiplier) / 2;
-  p.words = pair_simple(c) ? 1 : 2;
-  p.AS = (W + 3) & ~3;
-  p.pad_rows = std::min(kMaxUnpredWM - 1, 2 * p.hcfg);
-  p.wm = pair_window_bound(c, p.hcfg, p.pad_rows, p.words == 1);
-  for (const size_t budget : {kPairSmem2, kPairSmem1}) {
-    for (int C = 1; C <= kPairMaxCluster; ++C) {
-      // PGB_PAIR_C: experiments only (the cluster size changes the fixed-point shift)
-      if (const char* e = std::getenv("PGB_PAIR_C"))
-        if (std::atoi(e) > C) continue;
-      const int rows = (H + C - 1) / C;
-      if ((H + rows - 1) / rows != C) continue;   // every CTA owns rows
-      const double per_src = std::ceil((double)c->n_capacity / C);
-      const double lam = per_src * std::min(1.0, (double)(rows + 2 * p.hcfg + 1) / (double)H);
-      // inbox capacity ~ lambda + 3 sigma: fuller regions spill to L2 (exact)
-      int cap = (int)std::ceil(lam + 3.0 * std::sqrt(lam) + 4.0);
-      cap = (cap + 1) & ~1;
-      const PairSmem L = pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, 1);
-      if ((size_t)L.total <= budget) {
-        // the cluster size (rows per CTA) is fixed by the configuration (the
-        // fixed-point shift depends on it); a capacity override (tests: force
-        // the spill path) changes only the schedule, never a bit of the images
-        if (cap_override > 0) cap = cap_override;
-        p.C = C;
-        p.rows = rows;
-        p.cap = cap;
-        p.frames = 1;
-        p.smem = (size_t)pair_smem(rows, p.pad_rows, p.AS, C, cap, p.words, 1).total;
-        return true;
-      }
-    }
-  }
-  return false;
-}
-
-int generation_law(const pgb_config* c) {
-  PairPlan p{};
-  return make_pair_plan(c, p) ? PGB_LAW_PAIR : PGB_LAW_BAND;
-}
-
-int pair_cap_override() {
-  const char* e = std::getenv("PGB_PAIR_CAP");   // tests: force the spill path
-  return e ? std::max(1, std::atoi(e)) : 0;
-}
-
-using PairFn = void (*)(const BandParams);
-
-PairFn pair_fn(int psf, bool simple, int wm) {
-  if (psf == PGB_PSF_ERF) return simple ? pair_kernel<kPsfErf, true, 0> : pair_kernel<kPsfErf, false, 0>;
-  if (!simple) return pair_kernel<kPsfPoint, false, 0>;
-  switch (wm) {
-    case 1: return pair_kernel<kPsfPoint, true, 1>;
-    case 2: return pair_kernel<kPsfPoint, true, 2>;
-    case 3: return pair_kernel<kPsfPoint, true, 3>;
-    case 4: return pair_kernel<kPsfPoint, true, 4>;
-    case 5: return pair_kernel<kPsfPoint, true, 5>;
-    case 6: return pair_kernel<kPsfPoint, true, 6>;
-    case 7: return pair_kernel<kPsfPoint, true, 7>;
-    case 8: return pair_kernel<kPsfPoint, true, 8>;
-    default: return pair_kernel<kPsfPoint, true, 0>;
-  }
-}
-
-// Resident clusters for a plan (cached per device / kernel / smem / size).
-int pair_max_clusters(PairFn fn, const PairPlan& p) {
-  static std::map<std::tuple<void*, size_t, int, int>, int> cache;
-  int dev = 0;
-  PGB_CK(cudaGetDevice(&dev));
-  auto key = std::make_tuple((void*)fn, p.smem, p.C, dev);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  // the attribute is per function (and device): always the largest plan
-  PGB_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem1));
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(p.C * 148);
-  lc.blockDim = dim3(kPairThreads);
-  lc.dynamicSmemBytes = p.smem;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = p.C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  int n = 0;
-  PGB_CK(cudaOccupancyMaxActiveClusters(&n, (const void*)fn, &lc));
-  PGB_REQUIRE(n > 0, "pair kernel: no cluster of this configuration fits on the device");
-  cache[key] = n;
-  return n;
-}
-
-void launch_pair(BandParams& P, const PairPlan& pp, const pgb_config* cfg, cudaStream_t stream) {
-  const bool simple = pp.words == 1;
-  PairFn fn = pair_fn(cfg->psf, simple, pp.wm);
-  const int maxc = pair_max_clusters(fn, pp);
-  const int ncl = std::max(1, std::min(P.pairs, maxc));
-  DevWork& w = work_for(stream);
-  const size_t cnt_bytes = (size_t)ncl * 2 * pp.C * 2 * sizeof(int);            // [cluster][buffer][C][frame]
-  const size_t ovf_bytes = (size_t)ncl * 2 * pp.C * 2 * (size_t)P.n * pp.words * 16;
-  unsigned gen_before = 0, gen_after = 0;
-  void* cnt = ensure(w.pair_cnt, w.pair_cnt_bytes, cnt_bytes, &gen_after);
-  if (gen_after != gen_before) PGB_CK(cudaMemsetAsync(cnt, 0, w.pair_cnt_bytes, stream));
-  P.cl_ovf_cnt = static_cast<int*>(cnt);
-  P.cl_ovf = static_cast<uint4*>(ensure(w.pair_ovf, w.pair_ovf_bytes, ovf_bytes));
-  P.cl_size = pp.C;
-  P.cl_rows = pp.rows;
-  P.cl_cap = pp.cap;
-  P.cl_hcfg = pp.hcfg;
-  P.cl_frames = pp.frames;
-  // row -> owning CTA by multiply-shift, checked exact for every image row
-  P.cl_rdiv = (uint32_t)(((1u << 20) + pp.rows - 1) / pp.rows);
-  for (int r = 0; r < P.H; ++r)
-    PGB_REQUIRE((int)(((uint32_t)r * P.cl_rdiv) >> 20) == r / pp.rows, "pair plan: row divisor not exact");
-  P.AS = pp.AS;
-  P.pad_rows = pp.pad_rows;
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3((unsigned)(ncl * pp.C));
-  lc.blockDim = dim3(kPairThreads);
-  lc.dynamicSmemBytes = pp.smem;
-  lc.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = pp.C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  PGB_CK(cudaLaunchKernelEx(&lc, fn, P));
-  g_launches.fetch_add(1);
-}
-
 // Fields shared by the band and pair kernels (no workspace).
 void base_gen_params(BandParams& P, const pgb_config* cfg, uint64_t batch, int64_t pair_base, int pairs,
                      const float* flows, int num_fields, int pairs_per_field, const pgb_pair_stats* stats) {
@@ -897,18 +713,6 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   PGB_REQUIRE((int64_t)(pair_base + pairs) <= (int64_t)num_fields * pairs_per_field,
               "pair range exceeds the flow window (num_fields * pairs_per_field)");
   if (pairs == 0) return;
-  PairPlan pp{};
-  if (make_pair_plan(cfg, pp, pair_cap_override())) {
-    BandParams P{};
-    base_gen_params(P, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats);
-    P.out_mode = out_mode;
-    P.bg_offset = (float)cfg->bg_offset;
-    P.noise_std = (float)cfg->noise_std;
-    P.out[0] = img1;
-    P.out[1] = img2;
-    launch_pair(P, pp, cfg, stream);
-    return;
-  }
   const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
   const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
   BandParams P{};
@@ -954,16 +758,6 @@ extern "C" {
 int pgb_abi_version(void) { return PGB_ABI_VERSION; }
 
 const char* pgb_last_error(void) { return g_err.c_str(); }
-
-int pgb_generation_law(const pgb_config* cfg) {
-  int law = -1;
-  if (guarded([&] {
-        validate_cfg(cfg);
-        law = generation_law(cfg);
-      }) != 0)
-    return -1;
-  return law;
-}
 
 int pgb_patch_side(double max_diameter, double multiplier) {
   return patch_side_exact(max_diameter, multiplier);
@@ -1322,19 +1116,6 @@ int pgb_sample_particles_dev(const pgb_config* cfg, uint64_t batch, int64_t pair
     PGB_REQUIRE((int64_t)(pair_base + pairs) <= (int64_t)num_fields * pairs_per_field,
                 "pair range exceeds the flow window (num_fields * pairs_per_field)");
     if (pairs <= 0) return;
-    if (generation_law(cfg) == PGB_LAW_PAIR) {
-      BandParams P{};
-      base_gen_params(P, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats);
-      DevWork& w = work_for((cudaStream_t)stream);
-      unsigned* dbits = static_cast<unsigned*>(ensure(w.stage, w.stage_bytes, (size_t)pairs * 4 + 256));
-      PGB_CK(cudaMemsetAsync(dbits, 0, (size_t)pairs * 4, (cudaStream_t)stream));
-      pair_particles_kernel<<<dim3((unsigned)((P.n + 255) / 256), (unsigned)pairs), 256, 0, (cudaStream_t)stream>>>(
-          P, *out, dbits);
-      pair_stats_kernel<<<(pairs + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P, dbits);
-      g_launches.fetch_add(2);
-      PGB_CK(cudaGetLastError());
-      return;
-    }
     const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
     const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
     BandParams P{};

@@ -123,17 +123,6 @@ def _zero_flow(height: int, width: int, device: torch.device) -> torch.Tensor:
     return t
 
 
-def generation_law(cfg: GeneratorConfig) -> str:
-    """The generator's seeding law for ``cfg``: "pair" (one thread-block cluster
-    per image pair, iid positions keyed by particle; csrc/pair.cuh) or "band"
-    (stratified cells, csrc/band.cuh). A pure function of the configuration
-    (pgb_generation_law); both draw the reference's law (particles.py:61-101)."""
-    law = _lib.load().pgb_generation_law(native_config(cfg))
-    if law < 0:
-        _lib.check(1)
-    return _lib.LAW_NAMES[law]
-
-
 def generate_particle_arrays(cfg: GeneratorConfig, batch: int, pairs: range,
                              flows: torch.Tensor | None = None, pairs_per_field: int | None = None,
                              device=None) -> dict:

@@ -71,25 +71,3 @@ def test_errors_are_reported_not_thrown(lib):
         _lib.call("pgb_plan", 64, 64, 10, 0.0, 1, 2, None)
     with pytest.raises(_lib.BackendError, match="config is NULL"):
         _lib.call("pgb_generate_batch_dev", None, 0, 0, 1, None, 1, 1, 1, None, None, None, None, None)
-
-
-def test_generation_law_is_a_function_of_the_config(lib):
-    """pgb_generation_law (host only): the pair law when one image pair fits a
-    thread-block cluster's shared memory (the C2/C5 256^2 headline configs),
-    the band law for the large images (C3 1024^2, C4 512^2)."""
-    import paper_2512_09664_b200 as pg
-
-    def law(**kw):
-        cfg = pg.GeneratorConfig(flow_sources=(pg.FlowSource(function="none"),), **kw)
-        return pg.generation_law(cfg)
-
-    assert law(image_height=256, image_width=256) == "pair"
-    assert law(image_height=64, image_width=64, rho_range=(-0.5, 0.5), frame2_sigma_std=0.1) == "pair"
-    assert law(image_height=37, image_width=53) == "pair"
-    assert law(image_height=512, image_width=512) == "band"
-    assert law(image_height=1024, image_width=1024, seeding_density_range=(0.1, 0.1),
-               diameter_range=(1.0, 4.0)) == "band"
-    # dense 256^2 configurations overflow the cluster inbox budget -> band law
-    assert law(image_height=256, image_width=256, seeding_density_range=(0.5, 0.5),
-               diameter_range=(1.0, 4.0)) == "band"
-    assert lib.pgb_generation_law(None) == -1

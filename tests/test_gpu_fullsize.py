@@ -230,12 +230,6 @@ def _gen(pg, cfg, batch, pairs, mode):
     return flow, [i.cpu().numpy() for i in img]
 
 
-def _law(cfg):
-    import paper_2512_09664_b200 as pg
-
-    return pg.generation_law(cfg)
-
-
 def _oracle_cfg(cfg):
     ls = cfg.laser_sheet
     laser = None
@@ -248,7 +242,7 @@ def _oracle_cfg(cfg):
                         sigma_ratio=cfg.diameter_sigma_ratio, patch_multiplier=cfg.patch_multiplier,
                         f2_sigma_std=cfg.frame2_sigma_std, f2_rho_std=cfg.frame2_rho_std,
                         f2_i0_std=cfg.frame2_intensity_std, hide_probability=cfg.hide_probability,
-                        laser=laser, law=_law(cfg))
+                        laser=laser)
 
 
 FULL_GEN = {

@@ -191,12 +191,6 @@ def _gen_cfg(pg, **kw):
     return pg.GeneratorConfig(**base)
 
 
-def _law(cfg):
-    import paper_2512_09664_b200 as pg
-
-    return pg.generation_law(cfg)
-
-
 def _oracle_cfg(cfg):
     ls = cfg.laser_sheet
     laser = None
@@ -209,7 +203,7 @@ def _oracle_cfg(cfg):
                         sigma_ratio=cfg.diameter_sigma_ratio, patch_multiplier=cfg.patch_multiplier,
                         f2_sigma_std=cfg.frame2_sigma_std, f2_rho_std=cfg.frame2_rho_std,
                         f2_i0_std=cfg.frame2_intensity_std, hide_probability=cfg.hide_probability,
-                        laser=laser, law=_law(cfg))
+                        laser=laser)
 
 
 @pytest.mark.parametrize("kw", [
@@ -399,10 +393,9 @@ def test_spec_oracle_equivalence_random_configs(pg, seed):
     {"PGB_TILE": "32,64"},               # Q17 positions make every pixel tiling-independent
     {"PGB_GRID": "1"},                   # one CTA runs every prologue and band ticket in order
     {"PGB_GRID": "7"},                   # far fewer CTAs than SMs (MPS / green-context limits)
-    {"PGB_PAIR_CAP": "3"},               # pair kernel: tiny inboxes, most records spill to L2
 ])
 @pytest.mark.parametrize("sep", [False, True])
-@pytest.mark.parametrize("hw", [(128, 128), (64, 1040)])   # pair law, band law (W > 1024)
+@pytest.mark.parametrize("hw", [(128, 128), (64, 1040)])
 def test_schedule_and_store_paths_bit_identical(pg, env, sep, hw, monkeypatch):
     """Every schedule / tiling / grid size yields the same bits as a cold
     default launch of the same batch, over consecutive batches on one stream
@@ -419,7 +412,6 @@ def test_schedule_and_store_paths_bit_identical(pg, env, sep, hw, monkeypatch):
     extra = dict(diameter_range=(0.8, 1.2), rho_range=(0.0, 0.0), frame2_sigma_std=0.0,
                  frame2_intensity_std=0.0, frame2_rho_std=0.0, hide_probability=0.0) if sep else {}
     cfg = _gen_cfg(pg, image_height=H, image_width=W, batch_size=B, **extra)
-    assert pg.generation_law(cfg) == ("pair" if W <= 1024 else "band")
     flows = pg.from_function(vortex_fn(H, W), H, W).to_device().unsqueeze(0)
     stream = torch.cuda.current_stream()
 
@@ -555,7 +547,7 @@ def test_generate_edge_cases(pg):
              diameter_range=(6.0, 9.0)),
         dict(image_height=33, image_width=65, batch_size=3, seeding_density_range=(0.05, 0.08),
              diameter_range=(0.5, 3.0), rho_range=(-0.4, 0.4)),
-        dict(image_height=20, image_width=1030, batch_size=2, seeding_density_range=(0.05, 0.05)),   # band law
+        dict(image_height=20, image_width=1030, batch_size=2, seeding_density_range=(0.05, 0.05)),
     ]
     for kw in cases:
         kw = dict(kw, seed=77, flow_sources=(pg.FlowSource(function="edge"),))
