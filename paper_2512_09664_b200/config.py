@@ -11,7 +11,7 @@ Differences, all opt-in so a reference document means reference behaviour:
     no CPU generation path in this package.
   * ``psf``: ``point`` (reference Eq. (1) at pixel centres) or ``erf``
     (pixel-area integration).
-  * ``output_dtype``: ``float32`` (reference) or ``uint16`` (fused
+  * ``output_dtype``: ``float32`` (reference) or ``uint16`` (band-kernel
     ``quantize_u16``, export.py:19-20, bit-exact).
   * ``rng``: ``philox`` (the B200 generator's Philox4x32-10 streams) or
     ``splitmix64`` (the reference's own rng.py streams: particle arrays

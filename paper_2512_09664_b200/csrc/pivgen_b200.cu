@@ -237,6 +237,8 @@ struct DevWork {
   // host-API staging
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  void* host_io = nullptr;     // pgb_splat_accumulate's device copies (grow-only, reused)
+  size_t host_io_bytes = 0;
 };
 
 std::recursive_mutex g_mu;
@@ -829,10 +831,9 @@ int pgb_splat_accumulate(const double* pos, const float* i0, const float* sigma_
     const size_t np = (size_t)n;
     const size_t hw = (size_t)height * width;
     const size_t bytes = np * 16 + np * 4 * 4 + np + hw * 4 + 1024;
-    std::vector<char> dummy;
-    void* buf = nullptr;
-    PGB_CK(cudaMalloc(&buf, bytes));
-    char* b = static_cast<char*>(buf);
+    // one grow-only device buffer per device (no cudaMalloc / cudaFree per call)
+    DevWork& w = work_for(nullptr);
+    char* b = static_cast<char*>(ensure(w.host_io, w.host_io_bytes, bytes));
     double* d_pos = reinterpret_cast<double*>(b); b += np * 16;
     float* d_i0 = reinterpret_cast<float*>(b); b += np * 4;
     float* d_sx = reinterpret_cast<float*>(b); b += np * 4;
@@ -840,21 +841,17 @@ int pgb_splat_accumulate(const double* pos, const float* i0, const float* sigma_
     float* d_rho = reinterpret_cast<float*>(b); b += np * 4;
     float* d_out = reinterpret_cast<float*>(b); b += hw * 4;
     unsigned char* d_mask = reinterpret_cast<unsigned char*>(b);
-    auto fail = [&](const std::string& m) { cudaFree(buf); throw Error{m}; };
-    if (cudaMemcpy(d_pos, pos, np * 16, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d_i0, i0, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d_sx, sigma_x, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d_sy, sigma_y, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d_rho, rho, np * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d_mask, mask, np, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d_out, out, hw * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-      fail("host->device copy failed");
-    if (pgb_splat_accumulate_dev(d_pos, d_i0, d_sx, d_sy, d_rho, d_mask, n, side, d_out, height,
-                                 width, row_start, row_stop, PGB_PSF_POINT, nullptr) != 0)
-      fail(g_err);
-    if (cudaMemcpy(out, d_out, hw * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
-      fail("device->host copy failed");
-    cudaFree(buf);
+    PGB_CK(cudaMemcpy(d_pos, pos, np * 16, cudaMemcpyHostToDevice));
+    PGB_CK(cudaMemcpy(d_i0, i0, np * 4, cudaMemcpyHostToDevice));
+    PGB_CK(cudaMemcpy(d_sx, sigma_x, np * 4, cudaMemcpyHostToDevice));
+    PGB_CK(cudaMemcpy(d_sy, sigma_y, np * 4, cudaMemcpyHostToDevice));
+    PGB_CK(cudaMemcpy(d_rho, rho, np * 4, cudaMemcpyHostToDevice));
+    PGB_CK(cudaMemcpy(d_mask, mask, np, cudaMemcpyHostToDevice));
+    PGB_CK(cudaMemcpy(d_out, out, hw * 4, cudaMemcpyHostToDevice));
+    if (pgb_splat_accumulate_dev(d_pos, d_i0, d_sx, d_sy, d_rho, d_mask, n, side, d_out, height, width,
+                                 row_start, row_stop, PGB_PSF_POINT, nullptr) != 0)
+      throw Error{g_err};
+    PGB_CK(cudaMemcpy(out, d_out, hw * 4, cudaMemcpyDeviceToHost));
   });
 }
 

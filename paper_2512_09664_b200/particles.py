@@ -2,7 +2,7 @@
 
 Drop-in for the reference functional layer (particles.py:1-147). All draws
 come from Philox4x32-10 keyed by (seed, batch, pair) (``RngKey``); the
-kernels are the ones the fused generator runs, so ``sample_particles`` +
+kernels are the ones the band-kernel generator runs, so ``sample_particles`` +
 ``perturb_frame2`` + ``advect`` + ``apply_hiding`` reproduce exactly the
 particle set rendered by ``Sampler`` for that pair.
 
@@ -126,7 +126,7 @@ def _zero_flow(height: int, width: int, device: torch.device) -> torch.Tensor:
 def generate_particle_arrays(cfg: GeneratorConfig, batch: int, pairs: range,
                              flows: torch.Tensor | None = None, pairs_per_field: int | None = None,
                              device=None) -> dict:
-    """All per-particle arrays the fused kernel renders for global pairs
+    """All per-particle arrays the band kernel renders for global pairs
     ``pairs`` of ``batch`` (device tensors, shape (P, N[, 2]))."""
     dev = cuda_device(device)
     n = cfg.particle_capacity()

@@ -220,7 +220,7 @@ def render_pair(pset: ParticleSet, height: int, width: int, side: int, noise: No
                 target_histogram, key: RngKey, pool=None, bands: int = 1,
                 psf: str = "point") -> tuple[np.ndarray, np.ndarray]:
     """Splat + finalize (+ histogram) for both frames (raster.py:190-204),
-    in one fused launch."""
+    in one inject-kernel launch."""
     dev = cuda_device()
     frames = []
     for f in (1, 2):
