@@ -1,6 +1,6 @@
 """Summarise ncu captures for profiles/ (committed evidence).
 
-Usage: python scripts/profile_summary.py <full.ncu-rep> <launches.csv|-> <out_prefix> [config]
+Usage: python scripts/profile_summary.py <full.ncu-rep> <launches.csv|-> <out_prefix> [config] [pipes.csv]
 Writes <out_prefix>_launches.txt (kernel launch list with durations) and
 <out_prefix>_band_kernel.txt (speed-of-light, memory traffic, occupancy,
 stall reasons and per-phase instruction split of the dominant kernel), and
@@ -15,6 +15,7 @@ import sys
 
 rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
 cfgname = sys.argv[4] if len(sys.argv) > 4 else "c2"
+pipes_csv = sys.argv[5] if len(sys.argv) > 5 else None
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -50,6 +51,56 @@ with open(prefix + "_launches.txt", "w") if rows else open(os.devnull, "w") as f
     if band:
         fh.write(f"# band_kernel launches: {len(band)}, mean {sum(band)/len(band)/1000:.2f} us; "
                  f"other kernels (bench L2 flush): {len(other)}\n")
+
+def pipes_section(path, alg_bytes):
+    """Pipe utilisation / shared atomics / occupancy of each band-kernel launch
+    (scripts/profile_run.sh metrics pass) and its DRAM write traffic including
+    the dirty lines the following L2-flush kernel evicts."""
+    rows = [r for r in csv.DictReader(l for l in open(path) if not l.startswith("=="))]
+    launches = []
+    for r in rows:
+        key = (r["ID"], r["Kernel Name"])
+        if not launches or launches[-1]["key"] != key:
+            launches.append({"key": key, "name": r["Kernel Name"], "m": {}})
+        try:
+            v = float(r["Metric Value"].replace(",", ""))
+        except ValueError:
+            continue
+        u = r.get("Metric Unit", "")
+        v *= {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e3, "msecond": 1e6}.get(u, 1)
+        launches[-1]["m"][r["Metric Name"]] = v
+    out = ["\n# pipes / shared atomics / DRAM per band-kernel launch (ncu --metrics, scripts/profile_run.sh)\n"]
+    flush_bytes = 256 * 1024 * 1024
+    for i, L in enumerate(launches):
+        if "band_kernel" not in L["name"]:
+            continue
+        m = L["m"]
+        nxt = launches[i + 1]["m"] if i + 1 < len(launches) else {}
+        spill = max(0.0, nxt.get("dram__bytes_write.sum", 0.0) - flush_bytes) if nxt else float("nan")
+        out.append(f"launch {L['key'][0]}: {m.get('gpu__time_duration.sum', float('nan'))/1e3:.2f} us\n")
+        for k in ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+                  "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                  "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+                  "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+                  "sm__warps_active.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed.avg.per_cycle_active", "sm__inst_executed.sum",
+                  "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+                  "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+                  "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                  "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+                  "dram__bytes_read.sum", "dram__bytes_write.sum"):
+            out.append(f"  {k:78s} {m.get(k, float('nan')):.4g}\n")
+        atom = m.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", 0.0)
+        conf = m.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", 0.0)
+        if atom:
+            out.append(f"  shared-atomic wavefronts that are bank conflicts: {100*conf/atom:.1f}%\n")
+        if spill == spill:
+            tot = m.get("dram__bytes_write.sum", 0.0) + spill
+            out.append(f"  DRAM write incl. dirty lines evicted by the next flush: {tot:.4g} B "
+                       f"(algorithmic {alg_bytes} B, ratio {tot/alg_bytes:.3f})\n")
+    return "".join(out)
+
 
 # ---- full capture
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -101,6 +152,8 @@ with open(prefix + "_band_kernel.txt", "w") as fh:
         fh.write(f"  {k:30s} {100*v/tot:5.1f}\n")
     fh.write("\n# instruction / stall-sample split by source region (scripts/ncu_lines.py)\n")
     fh.write(phases)
+    if pipes_csv:
+        fh.write(pipes_section(pipes_csv, B * 2 * H * W * 4))
 
 tp = os.path.join(root, "profiles", "traffic.json")
 tj = json.load(open(tp)) if os.path.exists(tp) else {}
