@@ -63,12 +63,16 @@ CONFIGS = {
 
 
 def vortex(h, w, scale=2.0):
+    """Lamb-Oseen vortex; numpy or torch arrays (device evaluation)."""
     def fn(x, y):
+        xp = np
+        if type(x).__module__.startswith("torch"):
+            import torch as xp
         cx, cy = (w - 1) / 2.0, (h - 1) / 2.0
         rc = 0.1 * w
         dx, dy = x - cx, y - cy
-        r = np.sqrt(dx * dx + dy * dy) + 1e-12
-        vt = 1.398 * scale * (rc / r) * (1.0 - np.exp(-(r / rc) ** 2))
+        r = xp.sqrt(dx * dx + dy * dy) + 1e-12
+        vt = 1.398 * scale * (rc / r) * (1.0 - xp.exp(-(r / rc) ** 2))
         return -vt * dy / r, vt * dx / r
     return fn
 

@@ -11,8 +11,9 @@ import bench  # noqa: E402
 import paper_2512_09664_b200 as pg  # noqa: E402
 
 H, W, B = 256, 256, 256
-pg.register_flow_function("bench_vortex", bench.vortex(H, W))
-for rng, R in (("philox", 1), ("splitmix64", 1), ("philox", 8), ("splitmix64", 8)):
+for rng, R, dev in (("philox", 1, False), ("philox", 1, True), ("splitmix64", 1, True), ("philox", 8, False),
+                    ("splitmix64", 8, False)):
+    pg.register_flow_function("bench_vortex", bench.vortex(H, W), device=dev)
     cfg = pg.with_updates(bench.make_cfg(pg, "c2", B), rng=rng, batches_per_flow_field=R)
     with pg.make_sampler(cfg, max_batches=25) as s:
         for _ in range(5):
@@ -23,4 +24,5 @@ for rng, R in (("philox", 1), ("splitmix64", 1), ("philox", 8), ("splitmix64", 8
             b = next(s)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / 20
-    print(f"{rng} R={R}: {B / dt / 1e6:.3f} M pairs/s ({dt * 1e6:.0f} us/batch, Sampler wall clock)")
+    where = "device" if dev else "host"
+    print(f"{rng} R={R} flow on {where}: {B / dt / 1e6:.3f} M pairs/s ({dt * 1e6:.0f} us/batch, Sampler wall clock)")
