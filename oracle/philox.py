@@ -79,10 +79,18 @@ def u32_to_unitf(w) -> np.ndarray:
     return ((w >> np.uint32(9)).astype(np.float32) + np.float32(0.5)) * np.float32(2.0 ** -23)
 
 
+def u32_to_radius_unitf(w) -> np.ndarray:
+    """Box-Muller radius uniform of the GPU (common.cuh box_muller):
+    f32(f32(w) * 2^-32 + 2^-33), one rounding (exact in float64 before it), in (0, 1]."""
+    w = np.asarray(w, dtype=np.uint32)
+    return (w.astype(np.float32).astype(np.float64) * 2.0 ** -32 + 2.0 ** -33).astype(np.float32)
+
+
 def box_muller64(wa, wb):
-    """Float64 Box-Muller on the same 23-bit uniforms as the GPU (which uses
-    float32 fast intrinsics; agreement is to ~1e-6, not bit-exact)."""
-    u1 = u32_to_unitf(wa).astype(np.float64)
+    """Float64 Box-Muller on the same uniforms as the GPU (32-bit radius
+    uniform, 23-bit angle uniform; the GPU uses MUFU approximations, so
+    agreement is to ~1e-6, not bit-exact)."""
+    u1 = u32_to_radius_unitf(wa).astype(np.float64)
     u2 = u32_to_unitf(wb).astype(np.float64)
     r = np.sqrt(-2.0 * np.log(u1))
     t = 2.0 * np.pi * u2

@@ -919,9 +919,27 @@ __device__ __forceinline__ void splat_dispatch_b(int wt, int sep, int* acc, int 
 
 // Epilogue: one output quad (4 pixels) of frame f. (float)a is exact below
 // 2^24 and correctly rounded above (the accumulator stays < 2^31).
+// Round keys held in registers for the noise epilogue (the store loop would
+// otherwise reload the 20 key words from the constant bank every iteration).
+__device__ __forceinline__ uint32_t in_reg(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ PhiloxKeys keys_in_regs(const PhiloxKeys& K) {
+  PhiloxKeys R;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    R.k0[r] = in_reg(K.k0[r]);
+    R.k1[r] = in_reg(K.k1[r]);
+  }
+  return R;
+}
+
 template <int OUT, bool NOISE>
 __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, char* dst, uint32_t pix,
-                                                int f, uint32_t gpair, float inv_scale) {
+                                                int f, uint32_t gpair, float inv_scale,
+                                                const PhiloxKeys& K) {
   float4 v = make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
   if (OUT == kOutRaw) {
     v.x *= inv_scale; v.y *= inv_scale; v.z *= inv_scale; v.w *= inv_scale;
@@ -930,12 +948,13 @@ __device__ __forceinline__ void band_store_quad(const BandParams& P, int4 a, cha
   }
   const float bg = P.bg_offset;
   if (NOISE) {
+    // finalize_px(acc * 2^-s, ...) as FFMA.SAT(acc, 2^-s, offset + std * n)
     const float sd = P.noise_std;
-    const float4 nz = noise4_rk(P.g.rk, gpair, P.batch_lo, (uint32_t)f + 1, pix >> 2);
-    v.x = finalize_px(v.x * inv_scale, bg, sd, nz.x);
-    v.y = finalize_px(v.y * inv_scale, bg, sd, nz.y);
-    v.z = finalize_px(v.z * inv_scale, bg, sd, nz.z);
-    v.w = finalize_px(v.w * inv_scale, bg, sd, nz.w);
+    const float4 nz = noise4_rk(K, gpair, P.batch_lo, (uint32_t)f + 1, pix >> 2);
+    v.x = __saturatef(fmaf(v.x, inv_scale, fmaf(sd, nz.x, bg)));
+    v.y = __saturatef(fmaf(v.y, inv_scale, fmaf(sd, nz.y, bg)));
+    v.z = __saturatef(fmaf(v.z, inv_scale, fmaf(sd, nz.z, bg)));
+    v.w = __saturatef(fmaf(v.w, inv_scale, fmaf(sd, nz.w, bg)));
   } else {
     v.x = __saturatef(fmaf(v.x, inv_scale, bg));   // clip(raw + offset, 0, 1): FFMA.SAT
     v.y = __saturatef(fmaf(v.y, inv_scale, bg));
@@ -972,6 +991,7 @@ __device__ __forceinline__ void band_store_vec(const BandParams& P, int* __restr
   const int dao = drow * AS + dcq * 4;
   const uint32_t wrap_pix = (uint32_t)(W - qpr * 4);
   const int wrap_ao = AS - qpr * 4;
+  const PhiloxKeys K = NOISE ? keys_in_regs(P.g.rk) : P.g.rk;
   if (dcq == 0) {
     // qpr divides the block: every thread keeps its column quad
     const size_t ddst = (size_t)dpix * ESZ;
@@ -979,7 +999,7 @@ __device__ __forceinline__ void band_store_vec(const BandParams& P, int* __restr
       int4* ap = reinterpret_cast<int4*>(acc + ao);
       const int4 a = *ap;
       *ap = make_int4(0, 0, 0, 0);
-      band_store_quad<OUT, NOISE>(P, a, dst, pix, f, gpair, inv_scale);
+      band_store_quad<OUT, NOISE>(P, a, dst, pix, f, gpair, inv_scale, K);
     }
     return;
   }
@@ -987,7 +1007,7 @@ __device__ __forceinline__ void band_store_vec(const BandParams& P, int* __restr
     int4* ap = reinterpret_cast<int4*>(acc + ao);
     const int4 a = *ap;
     *ap = make_int4(0, 0, 0, 0);
-    band_store_quad<OUT, NOISE>(P, a, dst, pix, f, gpair, inv_scale);
+    band_store_quad<OUT, NOISE>(P, a, dst, pix, f, gpair, inv_scale, K);
     row += drow;
     cq += dcq;
     pix += dpix;
@@ -1015,11 +1035,21 @@ __device__ __forceinline__ void band_store_lin(const BandParams& P, int* __restr
   const uint32_t pix0 = (uint32_t)(r0 * P.W);
   char* dst = static_cast<char*>(P.out[f]) + ((size_t)pl * (size_t)P.out_pair_elems + pix0) * ESZ;
   int4* ap = reinterpret_cast<int4*>(acc);
+  if constexpr (NOISE) {
+    const PhiloxKeys K = keys_in_regs(P.g.rk);
+#pragma unroll 2
+    for (int q = t; q < nq; q += nt) {
+      const int4 a = ap[q];
+      ap[q] = make_int4(0, 0, 0, 0);
+      band_store_quad<OUT, NOISE>(P, a, dst + (size_t)q * 4 * ESZ, pix0 + 4u * q, f, gpair, inv_scale, K);
+    }
+  } else {
 #pragma unroll 4
-  for (int q = t; q < nq; q += nt) {
-    const int4 a = ap[q];
-    ap[q] = make_int4(0, 0, 0, 0);
-    band_store_quad<OUT, NOISE>(P, a, dst + (size_t)q * 4 * ESZ, pix0 + 4u * q, f, gpair, inv_scale);
+    for (int q = t; q < nq; q += nt) {
+      const int4 a = ap[q];
+      ap[q] = make_int4(0, 0, 0, 0);
+      band_store_quad<OUT, NOISE>(P, a, dst + (size_t)q * 4 * ESZ, pix0 + 4u * q, f, gpair, inv_scale, P.g.rk);
+    }
   }
 }
 

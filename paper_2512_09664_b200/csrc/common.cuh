@@ -201,10 +201,16 @@ PGB_HD void sample_flow_exact(const float2* __restrict__ flow, int H, int W, dou
 // ----------------------------------------------------------------------------
 // Box-Muller pair from two words (float32; distributional semantics only).
 // ----------------------------------------------------------------------------
+// Radius uniform u1 = f32((float)wa 2^-32 + 2^-33) in (0, 1] (32-bit resolution:
+// the tail reaches sqrt(2 ln 2^33) = 6.76 sigma); angle uniform u2 =
+// ((wb >> 9) + 1/2) 2^-23 built from its bits (exact). r = sqrt(-2 ln 2 lg2 u1)
+// with MUFU lg2/sqrt, no slow-path branch. ~14 instructions per normal pair.
 __device__ __forceinline__ float2 box_muller(uint32_t wa, uint32_t wb) {
-  const float u1 = u32_to_unitf(wa);
-  const float u2 = u32_to_unitf(wb);
-  const float r = sqrtf(-2.0f * __logf(u1));
+  const float u1 = fmaf((float)wa, 0x1p-32f, 0x1p-33f);
+  const float u2 = __fadd_rn(__uint_as_float((wb >> 9) | 0x3f800000u), -0.99999994f);
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u1));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * -1.3862943611198906f));
   float s, c;
   __sincosf(6.28318530717958647692f * u2, &s, &c);
   return make_float2(r * c, r * s);

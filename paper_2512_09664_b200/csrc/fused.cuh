@@ -446,10 +446,12 @@ __device__ __forceinline__ float4 noise4(uint32_t k0, uint32_t k1, uint32_t gpai
   return make_float4(a.x, a.y, b.x, b.y);
 }
 
+// clip(raw + offset + std * n, 0, 1) (raster.py:154-161): offset + std * n in
+// one FFMA, then one saturating add. The fused epilogue computes the same
+// value as FFMA.SAT(acc, 2^-s, offset + std * n) (acc * 2^-s is exact), so the
+// standalone and the fused finalize are bit-identical.
 __device__ __forceinline__ float finalize_px(float raw, float bg, float std_, float nz) {
-  float x = raw + bg;
-  if (std_ > 0.f) x = fmaf(std_, nz, x);
-  return fminf(fmaxf(x, 0.0f), 1.0f);
+  return __saturatef(raw + fmaf(std_, nz, bg));
 }
 
 __device__ __forceinline__ uint16_t quant_u16(float x) {

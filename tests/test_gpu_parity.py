@@ -602,3 +602,49 @@ def test_concurrent_streams_have_private_workspaces(pg):
             assert torch.equal(w[f], g[f])
     for f in range(2):
         assert torch.equal(part[f], want[1][f][10:27])
+
+
+@pytest.mark.parametrize("mode,pinned,B", [("f32", True, 100), ("u16", False, 70), ("f32", False, 7)])
+def test_host_buffer_pipeline_equals_device_path(pg, mode, pinned, B):
+    """pgb_generate_batch (HOST buffers, chunked kernel + D2H pipeline on two
+    streams) returns exactly the device path's images and pair statistics,
+    for ragged chunkings, pinned and pageable buffers."""
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    H, W = 96, 128
+    cfg = _gen_cfg(pg, image_height=H, image_width=W, batch_size=B,
+                   noise=pg.NoiseConfig(background_offset=0.05, gaussian_std=0.02))
+    field = pg.from_function(vortex_fn(H, W), H, W)
+    flows = field.to_device().unsqueeze(0)
+    ncfg = native_config(cfg)
+    om, dt, ndt = ((_lib.OUT_F32, torch.float32, np.float32) if mode == "f32"
+                   else (_lib.OUT_U16, torch.uint16, np.uint16))
+    base = 3
+    dev = [torch.empty((B, H, W), dtype=dt, device="cuda") for _ in range(2)]
+    dst = {"seeding_density": torch.empty(B, dtype=torch.float64, device="cuda"),
+           "active_count": torch.empty(B, dtype=torch.int32, device="cuda"),
+           "side": torch.empty(B, dtype=torch.int32, device="cuda"),
+           "d_max": torch.empty(B, dtype=torch.float32, device="cuda")}
+    st = _lib.PgbPairStats(**{k: v.data_ptr() for k, v in dst.items()})
+    _lib.call("pgb_generate_batch_dev", ncfg, 9, base, B, flows.data_ptr(), 1, B + base, om,
+              dev[0].data_ptr(), dev[1].data_ptr(), st, None, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    if pinned:
+        host = [torch.empty((B, H, W), dtype=dt).pin_memory() for _ in range(2)]
+        hptr = [h.data_ptr() for h in host]
+        harr = [h.numpy() for h in host]
+    else:
+        harr = [np.empty((B, H, W), dtype=ndt) for _ in range(2)]
+        hptr = [a.ctypes.data for a in harr]
+    hst = {"seeding_density": np.empty(B, np.float64), "active_count": np.empty(B, np.int32),
+           "side": np.empty(B, np.int32), "d_max": np.empty(B, np.float32)}
+    hs = _lib.PgbPairStats(**{k: v.ctypes.data for k, v in hst.items()})
+    hflow = np.ascontiguousarray(field.interleaved())
+    _lib.call("pgb_generate_batch", ncfg, 9, base, B, hflow.ctypes.data, 1, B + base, om, hptr[0], hptr[1], hs)
+    for f in range(2):
+        np.testing.assert_array_equal(harr[f], dev[f].cpu().numpy())
+    for k, v in dst.items():
+        np.testing.assert_array_equal(hst[k], v.cpu().numpy())
