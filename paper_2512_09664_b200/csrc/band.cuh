@@ -32,6 +32,21 @@
 
 namespace pgb {
 
+// Timing probes (build with -DPGB_TRACE only; scripts/trace.py reads them):
+// globaltimer stamps per CTA, slot = blockIdx.x * kTraceSlots + event.
+#ifdef PGB_TRACE
+constexpr int kTraceSlots = 16;
+__device__ unsigned long long g_trace[2048 * kTraceSlots];
+__device__ __forceinline__ void trace_stamp(int ev) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (blockIdx.x < 2048) g_trace[blockIdx.x * kTraceSlots + ev] = t;
+}
+#define PGB_STAMP(ev) do { if (threadIdx.x == 0) trace_stamp(ev); } while (0)
+#else
+#define PGB_STAMP(ev) do { } while (0)
+#endif
+
 #ifdef PGB_BAND_MAXREG
 #define PGB_BAND_BOUNDS __maxnreg__(PGB_BAND_MAXREG)
 #else
@@ -230,48 +245,6 @@ __device__ __forceinline__ void seed_particle(const BandParams& P, const PairHdr
 }
 
 // ----------------------------------------------------------------------------
-// Block-wide exclusive scan (in place allowed): out[i] = sum(in[0..i)),
-// out[count] = total. NT threads, `wsum` = NT/32 ints of shared scratch.
-// ----------------------------------------------------------------------------
-template <int NT>
-__device__ __forceinline__ int block_scan(const int* in, int* out, int count, int* wsum) {
-  constexpr int NW = NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per = (count + NT - 1) / NT;
-  const int b = min(count, (int)threadIdx.x * per), e = min(count, b + per);
-  int s = 0;
-  for (int i = b; i < e; ++i) s += in[i];
-  int x = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(~0u, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int v = lane < NW ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(~0u, v, o);
-      if (lane >= o) v += y;
-    }
-    if (lane < NW) wsum[lane] = v;
-  }
-  __syncthreads();
-  int base = (warp ? wsum[warp - 1] : 0) + x - s;
-  for (int i = b; i < e; ++i) {
-    const int v = in[i];
-    out[i] = base;
-    base += v;
-  }
-  const int total = wsum[NW - 1];
-  if (threadIdx.x == 0) out[count] = total;
-  __syncthreads();
-  return total;
-}
-
-// ----------------------------------------------------------------------------
 // Prologue: one CTA per pair (+ one per flow field)
 // ----------------------------------------------------------------------------
 constexpr int kPrologueThreads = 512;
@@ -319,9 +292,6 @@ __device__ __forceinline__ void field_bound_chunk(const BandParams& P, int f, in
   }
 }
 
-// Per-pair prologue (whole block, NT threads, `bins` = 2^(sy+sx) + 1 ints of
-// shared scratch): density, M, maximum diameter, the cell histogram -> per-cell
-// prefix and the particle -> cell array; pair_ready[pl] releases them.
 __device__ __forceinline__ void write_stats(const BandParams& P, int pl, const PairHdr& hd) {
   if (P.st_ppp) P.st_ppp[pl] = hd.ppp;
   if (P.st_M) P.st_M[pl] = hd.M;
@@ -329,224 +299,274 @@ __device__ __forceinline__ void write_stats(const BandParams& P, int pl, const P
   if (P.st_dmax) P.st_dmax[pl] = hd.dmax;
 }
 
+// Named barrier of the scan warps (every warp of the block but the last).
+template <int NTS>
+__device__ __forceinline__ void scan_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NTS) : "memory");
+}
+
+// The last warp's share of the prologue: the pair's maximum diameter. The max
+// of M uniforms is V^(1/M) (a serial float64 chain), carried by particle J.
+__device__ __forceinline__ void pair_max_diameter(const GenCfg& g, const RngKey& key, int M, PairHdr& hd) {
+  hd.M = M;
+  hd.m = 0.0;
+  hd.J = 0;
+  hd.qmax = 0;
+  float dmax = (float)g.d_hi;
+  if (M > 0) {
+    const uint4 v = philox_rk(make_uint4(1u, key.pair, key.batch, kTagPair), g.rk);
+    const double V = u53_to_unit(v.x, v.y);
+    hd.m = rexp(ddiv(rlog(V), (double)M));
+    hd.J = (int)__umul64hi(((uint64_t)v.w << 32) | v.z, (uint64_t)M);
+    const int q = (int)floor(hd.m * 8388608.0);
+    hd.qmax = q < 0x7fffff ? q : 0x7fffff;
+    dmax = lerpf_exact(g.d_lo, g.d_span, q_to_unit(hd.qmax));
+  }
+  hd.dmax = dmax;
+  // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
+  hd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
+}
+
+// Per-pair prologue (whole block of NT threads; `bins` = the shared scratch of
+// smem_bytes bytes): density, M, maximum diameter, the cell histogram -> per-cell
+// prefix and the particle -> cell array; pair_ready[pl] releases them.
+// Latency-bound (one pair per CTA at the start of every launch), so the last
+// warp draws the maximum diameter (a serial float64 chain) while the others
+// histogram and scan, synchronised by a named barrier of their own.
 template <int NT>
 __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes) {
-  __shared__ int wsum[NT / 32];
+  constexpr int NW = NT / 32;
+  constexpr int NS = NW - 1;          // scan warps
+  constexpr int NTS = NS * 32;
+  static_assert(NS >= 1 && NS <= 32, "prologue warps");
   __shared__ PairHdr shd;
-  __shared__ int scm;
-  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ int ctot[32];            // chunk bases (<= 32 chunks of 512 cells)
+  __shared__ int wmx[NS];
+  __shared__ int stot, scm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = P.sy + P.sx;
   const int ncell = 1 << L;
+  const int nc4 = ncell < 4 ? 4 : ncell;
   const RngKey key = band_key(P, pl);
-  for (int i = tid; i < (ncell < 4 ? 4 : ncell); i += NT) bins[i] = 0;
   const GenCfg& g = P.g;
+  PGB_STAMP(2);
   // seeding density and active count (particles.py:73-83), computed by every
-  // thread (identical values): no serial step before the histogram
+  // thread (identical values)
   const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
   const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
   double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
   mm = fmin(fmax(mm, 0.0), (double)P.n);
   const int M = (int)mm;
-  if (tid == 0) {
-    shd.ppp = ppp;
-    scm = 0;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // maximum diameter uniform: max of M uniforms = V^(1/M), on particle J
-    // (a serial float64 chain: overlapped with the histogram below)
-    shd.M = M;
-    shd.m = 0.0;
-    shd.J = 0;
-    shd.qmax = 0;
-    float dmax = (float)g.d_hi;
-    if (M > 0) {
-      const uint4 v = philox_rk(make_uint4(1u, key.pair, key.batch, kTagPair), g.rk);
-      const double V = u53_to_unit(v.x, v.y);
-      shd.m = rexp(ddiv(rlog(V), (double)M));
-      shd.J = (int)__umul64hi(((uint64_t)v.w << 32) | v.z, (uint64_t)M);
-      const int q = (int)floor(shd.m * 8388608.0);
-      shd.qmax = q < 0x7fffff ? q : 0x7fffff;
-      dmax = lerpf_exact(g.d_lo, g.d_span, q_to_unit(shd.qmax));
-    }
-    shd.dmax = dmax;
-    // no active particle: the reference falls back to diameter_range[1] (pipeline.py:292)
-    shd.side = patch_side_exact(M > 0 ? (double)dmax : g.d_hi, g.patch_mult);
-  } else {
-    // cell histogram of M iid labels (4 labels per Philox call)
-    for (int q = tid - 1; q < (M + 3) >> 2; q += NT - 1) {
-      const uint4 w = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
-    }
-  }
-  __syncthreads();
-  // Cell counts -> exclusive prefix (in place + global), the maximum cell
-  // count, and the particle -> cell array. Warps own 512-cell chunks; lanes
-  // read consecutive int4s (conflict-free), a warp shuffle scan per 128-cell
-  // layer, chunk totals combined by warp 0 (<= 32 chunks: ncell <= 2^14).
-  constexpr int NW = NT / 32;
-  int* wmax = wsum;        // NW entries, reused after the block combine below
-  __shared__ int ctot[32];
-  const int warp = tid >> 5;
-  const int nc4 = ncell < 4 ? 4 : ncell;
-  const int nq4 = nc4 >> 2;                 // int4 groups of cells
-  const int nchunk = (nq4 + 127) >> 7;       // 128 int4 = 512 cells per chunk
-  int4* bins4 = reinterpret_cast<int4*>(bins);
-  int cm = 0;
-  for (int ch = warp; ch < nchunk; ch += NW) {
-    int tot = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int q = (ch << 7) + (j << 5) + lane;
-      const int4 v = q < nq4 ? bins4[q] : make_int4(0, 0, 0, 0);
-      tot += v.x + v.y + v.z + v.w;
-      cm = max(cm, max(max(v.x, v.y), max(v.z, v.w)));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(~0u, tot, o);
-    if (lane == 0) ctot[ch] = tot;
-  }
-  {
-    // zero the staged particle -> cell slots (marked in pass 2)
-    const int M16z = (M + 7) & ~7;
-    const int off = ((nc4 + 4) & ~3) * 4;
-    if ((size_t)off + (size_t)M16z * 2 <= (size_t)smem_bytes && M16z <= 65536)
-      for (int q = tid; q < M16z / 8; q += NT)
-        reinterpret_cast<int4*>(reinterpret_cast<char*>(bins) + off)[q] = make_int4(0, 0, 0, 0);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
-  if (lane == 0) wmax[warp] = cm;
-  __syncthreads();
-  if (warp == 0) {
-    const int t = lane < nchunk ? ctot[lane] : 0;
-    int v = t;
-    int m = lane < NW ? wmax[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(~0u, v, o);
-      if (lane >= o) v += y;
-      m = max(m, __shfl_xor_sync(~0u, m, o));
-    }
-    if (lane < nchunk) ctot[lane] = v - t;   // exclusive chunk bases
-    if (lane == 31) wsum[0] = v;             // total
-    if (lane == 0) scm = m;
-  }
-  __syncthreads();
   int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
   unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
-  // particle -> cell (counting-sort order: particles of cell c are pre[c] ..
-  // pre[c+1]-1). Staged in shared memory when it fits: mark the first slot
-  // of every non-empty cell with the cell id (slots zeroed above), then a
-  // block max-scan fills the runs; else one cell per thread into global memory.
-  const int M16 = (M + 7) & ~7;
-  unsigned short* scof = reinterpret_cast<unsigned short*>(bins + ((nc4 + 4) & ~3));
-  const bool staged = (size_t)((nc4 + 4) & ~3) * 4 + (size_t)M16 * 2 <= (size_t)smem_bytes && M16 <= 65536;
-  int4* pre4 = reinterpret_cast<int4*>(pre);
-  for (int ch = warp; ch < nchunk; ch += NW) {
-    int run = ctot[ch];
+  if (warp == NS) {
+    if (lane == 0) {
+      PairHdr hd;
+      pair_max_diameter(g, key, M, hd);
+      hd.ppp = ppp;
+      shd = hd;
+#ifdef PGB_TRACE
+      trace_stamp(14);
+#endif
+    }
+  } else {
+    int4* bins4 = reinterpret_cast<int4*>(bins);
+    const int nq4 = nc4 >> 2;                    // int4 groups of cells
+    for (int i = tid; i < nq4; i += NTS) bins4[i] = make_int4(0, 0, 0, 0);
+    scan_sync<NTS>();
+    // cell histogram of M iid labels (4 labels per Philox call, two calls in flight)
+    const int nq = (M + 3) >> 2;
+    for (int q = tid; q < nq; q += 2 * NTS) {
+      const int q2 = q + NTS;
+      const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
+      const uint4 b = philox_rk(make_uint4((uint32_t)q2, key.pair, key.batch, kTagCell), g.rk);
+      const uint32_t ws[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int q = (ch << 7) + (j << 5) + lane;
-      const int4 v = q < nq4 ? bins4[q] : make_int4(0, 0, 0, 0);
-      const int sv = v.x + v.y + v.z + v.w;
-      int inc = sv;
+      for (int k = 0; k < 8; ++k) {
+        const int idx = k < 4 ? 4 * q + k : 4 * q2 + (k - 4);
+        if (idx < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+      }
+    }
+    scan_sync<NTS>();
+#ifdef PGB_TRACE
+    if (tid == 32) trace_stamp(15);
+#endif
+    PGB_STAMP(3);
+    // Cell counts -> exclusive prefix (in place + global) and the maximum cell
+    // count. Warps own 512-cell chunks (four 128-cell layers, lanes reading
+    // consecutive int4s); chunk totals combined by warp 0.
+    const int nchunk = (nq4 + 127) >> 7;
+    int cm = 0;
+    for (int ch = warp; ch < nchunk; ch += NS) {
+      int tot = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int q = (ch << 7) + (j << 5) + lane;
+        const int4 v = q < nq4 ? bins4[q] : make_int4(0, 0, 0, 0);
+        tot += v.x + v.y + v.z + v.w;
+        cm = max(cm, max(max(v.x, v.y), max(v.z, v.w)));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(~0u, tot, o);
+      if (lane == 0) ctot[ch] = tot;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(~0u, cm, o));
+    if (lane == 0) wmx[warp] = cm;
+    scan_sync<NTS>();
+    if (warp == 0) {
+      const int t = lane < nchunk ? ctot[lane] : 0;
+      int v = t;
+      int m = lane < NS ? wmx[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(~0u, inc, o);
-        if (lane >= o) inc += y;
+        const int y = __shfl_up_sync(~0u, v, o);
+        if (lane >= o) v += y;
+        m = max(m, __shfl_xor_sync(~0u, m, o));
       }
-      const int b0 = run + inc - sv;
-      const int4 o4 = make_int4(b0, b0 + v.x, b0 + v.x + v.y, b0 + v.x + v.y + v.z);
-      if (q < nq4) {
-        bins4[q] = o4;   // exclusive prefix, in place
-        const int i = q << 2;
-        if (i + 4 <= ncell) {
-          pre4[q] = o4;
-        } else {
-          const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
-          for (int k = 0; i + k < ncell; ++k) pre[i + k] = oo[k];
-        }
-        if (staged) {
-          if (v.x) scof[o4.x] = (unsigned short)i;
-          if (v.y) scof[o4.y] = (unsigned short)(i + 1);
-          if (v.z) scof[o4.z] = (unsigned short)(i + 2);
-          if (v.w) scof[o4.w] = (unsigned short)(i + 3);
-        }
-      }
-      run += __shfl_sync(~0u, inc, 31);
+      if (lane < nchunk) ctot[lane] = v - t;   // exclusive chunk bases
+      if (lane == 31) stot = v;
+      if (lane == 0) scm = m;
     }
-  }
-  if (tid == 0) bins[ncell] = wsum[0];
-  __syncthreads();
-  if (staged) {
-    // inclusive max-scan of the marks: one warp layer (32 lanes x int4 of 8
-    // slots = 256 slots) per chunk; chunk maxima -> exclusive carries in
-    // bins[] (the prefix is no longer needed there), scanned by warp 0
-    const int ns4 = M16 >> 3;                  // int4 groups of 8 slots
-    const int nsch = (ns4 + 31) >> 5;
+    scan_sync<NTS>();
+    PGB_STAMP(4);
+    // in-chunk prefix: the four layers' warp scans interleaved (independent),
+    // then chained by their totals
+    int4* pre4 = reinterpret_cast<int4*>(pre);
+    for (int ch = warp; ch < nchunk; ch += NS) {
+      int4 v[4];
+      int sv[4], inc[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int q = (ch << 7) + (j << 5) + lane;
+        v[j] = q < nq4 ? bins4[q] : make_int4(0, 0, 0, 0);
+        sv[j] = v[j].x + v[j].y + v[j].z + v[j].w;
+        inc[j] = sv[j];
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int y = __shfl_up_sync(~0u, inc[j], o);
+          if (lane >= o) inc[j] += y;
+        }
+      }
+      int run = ctot[ch];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int q = (ch << 7) + (j << 5) + lane;
+        const int b0 = run + inc[j] - sv[j];
+        const int4 o4 = make_int4(b0, b0 + v[j].x, b0 + v[j].x + v[j].y, b0 + v[j].x + v[j].y + v[j].z);
+        if (q < nq4) {
+          bins4[q] = o4;   // exclusive prefix, in place (entries >= ncell: the total)
+          const int i = q << 2;
+          if (i + 4 <= ncell) {
+            pre4[q] = o4;
+          } else {
+            const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
+            for (int k = 0; i + k < ncell; ++k) pre[i + k] = oo[k];
+          }
+        }
+        run += __shfl_sync(~0u, inc[j], 31);
+      }
+    }
+    if (tid == 0) {
+      bins[ncell] = stot;
+      pre[ncell] = stot;
+    }
+    scan_sync<NTS>();
+    PGB_STAMP(5);
+    // particle -> cell (counting-sort order: particles of cell c are
+    // pre[c] .. pre[c+1]-1), in windows of slots staged in shared memory
+    // behind the prefix: mark the first slot of every cell starting in the
+    // window with the cell id, inclusive max-scan (carry in: the cell holding
+    // the window's first slot), 16-byte stores of the scanned slots
+    const int soff = ((nc4 + 4) & ~3) * 4;
+    unsigned short* scof = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(bins) + soff);
     int4* s4 = reinterpret_cast<int4*>(scof);
+    __shared__ int wcar[128];                     // per-chunk carries of one window
+    const int win = max(8, min(128 * 256, ((smem_bytes - soff) / 2) & ~7));   // slots per window (plans leave >= 8)
+    const int M8 = (M + 7) & ~7;
     auto max8 = [](const int4 w) {
       const int a = max(max(w.x & 0xffff, (int)((unsigned)w.x >> 16)), max(w.y & 0xffff, (int)((unsigned)w.y >> 16)));
       const int b = max(max(w.z & 0xffff, (int)((unsigned)w.z >> 16)), max(w.w & 0xffff, (int)((unsigned)w.w >> 16)));
       return max(a, b);
     };
-    for (int ch = warp; ch < nsch; ch += NW) {
-      const int q = (ch << 5) + lane;
-      int mx = q < ns4 ? max8(s4[q]) : 0;
+    for (int s0 = 0; s0 < M8; s0 += win) {
+      const int s1 = min(M8, s0 + win);
+      const int n4 = (s1 - s0) >> 3;               // int4 groups of 8 slots
+      for (int q = tid; q < n4; q += NTS) s4[q] = make_int4(0, 0, 0, 0);
+      // the cell holding slot s0: last c with bins[c] <= s0 (and a non-empty run)
+      int clo = 0;
+      if (s0 > 0) {
+        int lo = 0, hi = ncell - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (bins[mid] <= s0) lo = mid;
+          else hi = mid - 1;
+        }
+        clo = lo;   // bins is non-decreasing and bins[ncell] = M > s0: cell clo holds slot s0
+      }
+      scan_sync<NTS>();
+#pragma unroll 8
+      for (int c = tid; c < ncell; c += NTS) {
+        const int b = bins[c];
+        if (b >= s0 && b < s1 && b < bins[c + 1]) scof[b - s0] = (unsigned short)c;
+      }
+      scan_sync<NTS>();
+      // chunk maxima (256 slots = one warp layer of int4s per chunk)
+      const int nch = (n4 + 31) >> 5;
+      for (int ch = warp; ch < nch; ch += NS) {
+        const int q = (ch << 5) + lane;
+        int mx = q < n4 ? max8(s4[q]) : 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(~0u, mx, o));
-      if (lane == 0) bins[ch] = mx;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      int carry = 0;
-      for (int c0 = 0; c0 < nsch; c0 += 32) {
-        const int c = c0 + lane;
-        int m = c < nsch ? bins[c] : 0;
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(~0u, mx, o));
+        if (lane == 0) wcar[ch] = mx;
+      }
+      scan_sync<NTS>();
+      if (warp == 0) {
+        int carry = clo;
+        for (int c0 = 0; c0 < nch; c0 += 32) {
+          const int c = c0 + lane;
+          int m = c < nch ? wcar[c] : 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(~0u, m, o);
+            if (lane >= o) m = max(m, y);
+          }
+          const int up = __shfl_up_sync(~0u, m, 1);
+          const int ex = max(carry, lane ? up : 0);
+          if (c < nch) wcar[c] = ex;
+          carry = max(carry, __shfl_sync(~0u, m, 31));
+        }
+      }
+      scan_sync<NTS>();
+      int4* c4 = reinterpret_cast<int4*>(cof + s0);
+      for (int ch = warp; ch < nch; ch += NS) {
+        const int q = (ch << 5) + lane;
+        int4 w4 = make_int4(0, 0, 0, 0);
+        if (q < n4) w4 = s4[q];
+        int m = max8(w4);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(~0u, m, o);
           if (lane >= o) m = max(m, y);
         }
-        const int up = __shfl_up_sync(~0u, m, 1);
-        const int ex = max(carry, lane ? up : 0);
-        if (c < nsch) bins[c] = ex;
-        carry = max(carry, __shfl_sync(~0u, m, 31));
+        const int prev = __shfl_up_sync(~0u, m, 1);
+        int r = lane > 0 ? max(wcar[ch], prev) : wcar[ch];
+        int lo, hi, o0, o1, o2, o3;
+        lo = r = max(r, w4.x & 0xffff); hi = r = max(r, (int)((unsigned)w4.x >> 16)); o0 = lo | (hi << 16);
+        lo = r = max(r, w4.y & 0xffff); hi = r = max(r, (int)((unsigned)w4.y >> 16)); o1 = lo | (hi << 16);
+        lo = r = max(r, w4.z & 0xffff); hi = r = max(r, (int)((unsigned)w4.z >> 16)); o2 = lo | (hi << 16);
+        lo = r = max(r, w4.w & 0xffff); hi = r = max(r, (int)((unsigned)w4.w >> 16)); o3 = lo | (hi << 16);
+        if (q < n4) c4[q] = make_int4(o0, o1, o2, o3);
       }
-    }
-    __syncthreads();
-    int4* c4 = reinterpret_cast<int4*>(cof);
-    for (int ch = warp; ch < nsch; ch += NW) {
-      const int q = (ch << 5) + lane;
-      int4 w4 = make_int4(0, 0, 0, 0);
-      if (q < ns4) w4 = s4[q];
-      int m = max8(w4);
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(~0u, m, o);
-        if (lane >= o) m = max(m, y);
-      }
-      const int prev = __shfl_up_sync(~0u, m, 1);
-      int r = lane > 0 ? max(bins[ch], prev) : bins[ch];
-      int lo, hi, o0, o1, o2, o3;
-      lo = r = max(r, w4.x & 0xffff); hi = r = max(r, (int)((unsigned)w4.x >> 16)); o0 = lo | (hi << 16);
-      lo = r = max(r, w4.y & 0xffff); hi = r = max(r, (int)((unsigned)w4.y >> 16)); o1 = lo | (hi << 16);
-      lo = r = max(r, w4.z & 0xffff); hi = r = max(r, (int)((unsigned)w4.z >> 16)); o2 = lo | (hi << 16);
-      lo = r = max(r, w4.w & 0xffff); hi = r = max(r, (int)((unsigned)w4.w >> 16)); o3 = lo | (hi << 16);
-      if (q < ns4) c4[q] = make_int4(o0, o1, o2, o3);
-    }
-  } else {
-    for (int c = tid; c < ncell; c += NT) {
-      const int j1 = bins[c + 1];
-      for (int j = bins[c]; j < j1; ++j) cof[j] = (unsigned short)c;
+      if (s1 < M8) scan_sync<NTS>();
     }
   }
+  __syncthreads();   // the maximum-diameter warp joins
+  PGB_STAMP(6);
   if (tid == 0) {
-    pre[ncell] = wsum[0];
     PairHdr hd = shd;
     hd.cmax = scm;
     P.hdr[pl] = hd;
@@ -557,18 +577,22 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     __threadfence();
     st_release(P.pair_ready + pl, 1);
   }
+  PGB_STAMP(7);
 }
 
 // Standalone prologue (sample_particles path): one CTA per pair + kFieldBlocks
 // per flow field.
 __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(const BandParams P) {
   extern __shared__ int bins[];
+  PGB_STAMP(0);
   if (blockIdx.x >= P.pairs) {
     const int fb = blockIdx.x - P.pairs;
     field_bound_chunk<kPrologueThreads>(P, fb / kFieldBlocks, fb % kFieldBlocks);
+    PGB_STAMP(12);
     return;
   }
   pair_prologue<kPrologueThreads>(P, blockIdx.x, bins, P.pro_smem);
+  PGB_STAMP(12);
 }
 
 // ----------------------------------------------------------------------------
@@ -1431,6 +1455,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
   // the prologue borrows the accumulator region (>= its histogram, see make_band_plan)
   const int acc_bytes = P.pro_smem;
+  PGB_STAMP(0);
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)
     for (int e = tid; e < P.zero_head_n; e += kBandBlock) P.zero_head[e] = make_int4(0, 0, 0, 0);
   // One ticket sequence: [0, npro) prologue items (the pairs, then the
@@ -1445,6 +1470,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
     __syncthreads();
     first = sh->ticket0;
     __syncthreads();
+    PGB_STAMP(1);
     if (first >= P.npro) break;
     const int w = (int)first;
     if (w < P.pairs) {
@@ -1460,11 +1486,19 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
   // dynamic schedule: the staging warp takes the ticket of item k+1 and
   // prepares it (parameters + particle segments) while the workers splat item k
+  PGB_STAMP(8);
   if (stager) stage_next(P, sh, 0, first);
   __syncthreads();
+  PGB_STAMP(9);
+#ifdef PGB_TRACE
+  int nitems = 0;
+#endif
   for (int buf = 0;; buf ^= 1) {
     const int kind = sh->ic[buf].kind;
     if (kind == kItemEnd) break;
+#ifdef PGB_TRACE
+    ++nitems;
+#endif
     if (stager) {
       stage_next(P, sh, buf ^ 1, -1);
       __syncthreads();   // particles done
@@ -1488,11 +1522,21 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
       }
     }
     __syncthreads();   // particles done (stager: next item staged)
+#ifdef PGB_TRACE
+    if (nitems == 1) PGB_STAMP(10);
+#endif
     const float inv_scale = 1.0f / scale;
     band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
     band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
     __syncthreads();   // accumulators zeroed
+#ifdef PGB_TRACE
+    if (nitems == 1) PGB_STAMP(11);
+#endif
   }
+  PGB_STAMP(12);
+#ifdef PGB_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 2048) g_trace[blockIdx.x * kTraceSlots + 13] = nitems;
+#endif
 }
 
 
@@ -1500,6 +1544,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
 // the band kernel renders (positions = anchor + fraction).
 __global__ void sample_band_kernel(const BandParams P, pgb_particle_out O) {
   const int pl = blockIdx.x;
+  PGB_STAMP(9);
   const PairHdr hd = P.hdr[pl];
   const int ncell = 1 << (P.sy + P.sx);
   const int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
@@ -1537,6 +1582,7 @@ __global__ void sample_band_kernel(const BandParams P, pgb_particle_out O) {
     if (O.visible1) O.visible1[o] = pt.vis1 ? 1 : 0;
     if (O.visible2) O.visible2[o] = pt.vis2 ? 1 : 0;
   }
+  PGB_STAMP(10);
 }
 
 }  // namespace pgb

@@ -469,6 +469,10 @@ void cell_bits(int H, int W, int& sy, int& sx) {
     if (sx >= sy) --sx;
     else --sy;
   }
+  if (const char* e = std::getenv("PGB_CELL_BITS")) {   // timing experiments only (the oracle does not follow)
+    int a = 0, b = 0;
+    if (std::sscanf(e, "%d,%d", &a, &b) == 2 && a >= 0 && b >= 0 && a + b <= kMaxCellBits) { sy = a; sx = b; }
+  }
 }
 
 // Accumulator bytes per CTA such that two band CTAs fit on one SM: half the
@@ -1217,6 +1221,33 @@ int pgb_probe_ex2_dev(int blocks, int iters, float* sink, void* stream) {
     PGB_CK(cudaGetLastError());
   });
 }
+
+#ifdef PGB_TRACE
+// Timing probes of the last band launch (debug builds only): n u64 words.
+int pgb_trace_read(unsigned long long* out, int n) {
+  return guarded([&] {
+    PGB_CK(cudaDeviceSynchronize());
+    PGB_CK(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * (size_t)n));
+  });
+}
+// Peek at the probes while a kernel may still run (non-blocking stream copy).
+int pgb_trace_peek(unsigned long long* out, int n) {
+  return guarded([&] {
+    cudaStream_t s;
+    PGB_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    PGB_CK(cudaMemcpyFromSymbolAsync(out, g_trace, sizeof(unsigned long long) * (size_t)n, 0,
+                                     cudaMemcpyDeviceToHost, s));
+    PGB_CK(cudaStreamSynchronize(s));
+    PGB_CK(cudaStreamDestroy(s));
+  });
+}
+int pgb_trace_clear(void) {
+  return guarded([&] {
+    static unsigned long long zeros[2048 * kTraceSlots];
+    PGB_CK(cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros)));
+  });
+}
+#endif
 
 int pgb_overflow_count(void) {
   int v = -1;
