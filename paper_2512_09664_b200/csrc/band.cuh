@@ -63,6 +63,9 @@ constexpr int kBandWarps = kBandThreads / 32;
 constexpr int kBandBlock = kBandThreads + 32;   // + one staging warp
 constexpr int kMaxCellBits = 14;
 constexpr int kMaxUnpredWM = 12;   // largest unpredicated (separable) splat window
+constexpr int kSortClasses = 5;    // sorted splat window classes: 4, 6, 8, 10, 12
+constexpr int kSortMinW = 7;       // items whose window bound reaches this use the sorted splat
+constexpr int kVarSorted = 100;    // ItemCfg::var of the sorted splat
 
 struct __align__(16) PairHdr {
   double ppp;      // realised seeding density
@@ -85,6 +88,7 @@ struct BandParams {
   long long split_base, total_items;
   int split_s;
   int pad_rows;                // zero rows after the frame-2 accumulator (unpredicated splat windows)
+  int rec_bytes;               // SortShared region ahead of the accumulators (sorted splat), else 0
   int pro_smem;                // shared bytes the pair prologue may use (prologue kernel / band accumulators)
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
   int n, pairs;
@@ -1222,6 +1226,8 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   // stress test (scripts/stress.py); correlated particles use the dynamic loops
   const int wm = (P.psf == kPsfPoint && ic.sep && ic.wt <= kMaxUnpredWM && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
   ic.var = (P.psf == kPsfPoint ? 16 * ic.sep : 0) + wm;
+  // large separable windows: bank-sorted splat (plans with a record region)
+  if (P.rec_bytes && wm >= kSortMinW) ic.var = kVarSorted;
 }
 
 // Warp 0: next item's parameters + particle segments (one per cell row of the
@@ -1445,11 +1451,286 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
   }
 }
 
+
+// ----------------------------------------------------------------------------
+// Bank-sorted splat for large windows (C3: d up to 4 px, 12 x 12 windows).
+// With one particle-frame per lane, the 32 lanes of a shared-memory atomic hit
+// random banks (measured 3.7 wavefronts per ATOMS at C3: the shared-atomic
+// pipe, not the SFU, bounded the kernel). Here the workers first turn their
+// particle-frames into splat records (window origin, extents, Gaussian
+// coefficients), counting-sort them by (window class, accumulator bank of the
+// window origin), then splat in rounds where lane l takes record r + l*R of
+// the class (R = ceil(n / 32)): lanes of one round sit in different banks,
+// and every slot (i, j) of the round shifts all lanes by the same i*AS + j,
+// so each ATOMS is (nearly) conflict-free. The class bounds the unpredicated
+// window (4, 6, 8, 10, 12) instead of the pair's maximum. Same per-slot values
+// as splat_sep_u (bit-identical images).
+// ----------------------------------------------------------------------------
+
+struct __align__(16) SplatRec {
+  int base;        // accumulator offset of the window origin (frame 2: + TH * AS)
+  int nrnc;        // rows | cols << 16 inside the tile
+  float dx0, dy0, A, C, Ls, pad;
+};
+
+struct __align__(16) SortBuf {
+  SplatRec rec[2 * kBandThreads];            // record of (thread, frame), unsorted
+  unsigned short idx[2 * kBandThreads];      // sorted order -> record
+  int cnt[kSortClasses * 32];                // (class, bank) counts
+  int cls_start[kSortClasses + 1];           // class starts in sorted order
+  int cls_round[kSortClasses + 1];           // prefix of rounds, largest class first
+  int next_round;                            // dynamic round counter (work stealing)
+};
+
+// Two buffers: chunk k is generated into buf k&1 while chunk k-1 is splatted.
+struct __align__(16) SortShared {
+  SortBuf b[2];
+};
+
+// Record of one separable particle-frame; returns its sort key or -1 (no pixel
+// of the tile in the window).
+__device__ __forceinline__ int make_rec(int f_off, int AS, int ax, int ay, float fx, float fy, float amp,
+                                        float sx, float sy, int h, int r0, int r1, int c0, int c1, int shift,
+                                        SplatRec& r) {
+  const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
+  int rlo, clo, nr, nc;
+  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return -1;
+  r.base = f_off + (rlo - r0) * AS + (clo - c0);
+  r.nrnc = nr | (nc << 16);
+  r.dx0 = (float)(clo - ax) - fx;
+  r.dy0 = (float)(rlo - ay) - fy;
+  const float isx = rcp_approx(sx), isy = rcp_approx(sy);
+  r.A = (0.5f * kLog2e) * isx * isx;
+  r.C = (0.5f * kLog2e) * isy * isy;
+  r.Ls = lg2_approx(amp) + (float)shift;
+  r.pad = 0.f;
+  const int w = max(nr, nc);
+  const int cls = w <= 4 ? 0 : min(kSortClasses - 1, (w - 3) >> 1);   // 5-6: 1, 7-8: 2, 9-10: 3, 11-12: 4
+  return cls * 32 + (r.base & 31);
+}
+
+// One record, unpredicated WM x WM window (slots outside the record's window
+// add exactly 0; pad rows behind the frame-2 accumulator absorb the overhang).
+template <int WM>
+__device__ __forceinline__ void splat_rec(int* __restrict__ acc, int AS, const SplatRec& r) {
+  const int nr = r.nrnc & 0xffff, nc = r.nrnc >> 16;
+  int* base = acc + r.base;
+  float X[WM];
+#pragma unroll
+  for (int j = 0; j < WM; ++j) {
+    const float dx = r.dx0 + (float)j;
+    const float xv = ex2_approx(fmaf(-r.A * dx, dx, r.Ls));
+    X[j] = j < nc ? xv : 0.f;
+  }
+  if constexpr (WM <= 8) {
+    float Y[WM];
+#pragma unroll
+    for (int i = 0; i < WM; ++i) {
+      const float dy = r.dy0 + (float)i;
+      const float yv = ex2_approx(-r.C * dy * dy);
+      Y[i] = i < nr ? yv : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < WM; ++i) {
+      int* row = base + i * AS;
+#pragma unroll
+      for (int j = 0; j < WM; ++j)
+        atomicAdd(row + j, __float_as_int(fmaf(X[j], Y[i], 12582912.0f)) - 0x4B400000);
+    }
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < WM; ++i) {
+      const float dy = r.dy0 + (float)i;
+      const float yv = ex2_approx(-r.C * dy * dy);
+      const float Y = i < nr ? yv : 0.f;
+      int* row = base + i * AS;
+#pragma unroll
+      for (int j = 0; j < WM; ++j)
+        atomicAdd(row + j, __float_as_int(fmaf(X[j], Y, 12582912.0f)) - 0x4B400000);
+    }
+  }
+}
+
+// Worker warps, sorted splat. Per chunk k of NTW particle slots:
+//   G(k): regenerate, write records into buffer k&1, count (class, bank) keys
+//   S(k-1): splat the previous chunk's rounds (buffer (k-1)&1), work-stealing
+//   barrier A; every warp scans the counts (redundantly: no serial step),
+//   scatters its own records' sorted positions; warp 0 publishes the class
+//   layout; barrier B.
+// Two named barriers per chunk; generation of one chunk overlaps the splat of
+// the previous one across warps. Workers' named barrier BAR.
+template <int PSF, int NTW = kBandThreads, int BAR = 1>
+__device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandShared* sh, SortShared* ss,
+                                                      int buf, long long item, int* acc0) {
+  constexpr int NWW = NTW / 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const ItemCfg& ic = sh->ic[buf];
+  const int pl = ic.pl;
+  const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
+  const int h = ic.h, shift = ic.shift;
+  const PairHdr& hd = ic.hd;
+  const int AS = P.AS, f2off = P.TH * P.AS;
+  const float2* flow = P.flows + (size_t)ic.field * P.field_elems;
+  const unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
+  const RngKey key = band_key(P, pl);
+  int next_row = ic.cy0;
+  int pend = 0;   // chunks generated but not yet splatted (0 or 1), in buffer pbuf
+  int pbuf = 0;
+  // splat the rounds of buffer b (all workers, dynamic rounds)
+  auto splat_chunk = [&](SortBuf& B) {
+    const int nrounds = B.cls_round[kSortClasses];
+    for (int rr = warp; rr < nrounds;) {
+      int t = 0;
+      while (rr >= B.cls_round[t + 1]) ++t;
+      const int c = kSortClasses - 1 - t;
+      const int R = B.cls_round[t + 1] - B.cls_round[t];
+      const int cs = B.cls_start[c];
+      const int k = (rr - B.cls_round[t]) + lane * R;
+      int nxt = 0;
+      if (lane == 0) nxt = atomicAdd(&B.next_round, 1);
+      if (k < B.cls_start[c + 1] - cs) {
+        const SplatRec r = B.rec[B.idx[cs + k]];
+        switch (c) {   // warp-uniform
+          case 0: splat_rec<4>(acc0, AS, r); break;
+          case 1: splat_rec<6>(acc0, AS, r); break;
+          case 2: splat_rec<8>(acc0, AS, r); break;
+          case 3: splat_rec<10>(acc0, AS, r); break;
+          default: splat_rec<12>(acc0, AS, r); break;
+        }
+      }
+      rr = __shfl_sync(~0u, nxt, 0);
+    }
+  };
+  for (;;) {
+    const int nseg = sh->nseg[buf];
+    const int N = sh->seg_off[buf][nseg];
+    const int* soff = sh->seg_off[buf];
+    const int* sst = sh->seg_start[buf];
+    const int sst0 = sst[0];
+    auto locate = [&](int q) {
+      q = min(q, N - 1);
+      if (nseg == 1) return sst0 + q;
+      int sg = 0;
+      {
+        int hi = nseg - 1;
+        while (sg < hi) {
+          const int mid = (sg + hi + 1) >> 1;
+          if (soff[mid] <= q) sg = mid;
+          else hi = mid - 1;
+        }
+      }
+      return sst[sg] + (q - soff[sg]);
+    };
+    int gA = 0, cA = 0;
+    uint4 aA = make_uint4(0, 0, 0, 0);
+    if (N > 0) {
+      gA = locate(tid);
+      cA = __ldcg(cof + gA);
+      aA = draw_a(P.g, key, gA);
+    }
+    for (int qb = 0; qb < N; qb += NTW) {
+      SortBuf& G = ss->b[pbuf ^ 1];   // this chunk
+      const int qa = qb + tid;
+      const int giA = gA, ccA = cA;
+      const uint4 a = aA;
+      const bool more = qb + NTW < N;
+      if (more) {
+        gA = locate(qa + NTW);
+        cA = __ldcg(cof + gA);
+      }
+      PFrames A;
+      const bool ok = qa < N;
+      int k1 = -1, k2 = -1, rk1 = 0, rk2 = 0;
+      band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
+        if (ok && F.on1) {
+          SplatRec r;
+          k1 = make_rec(0, AS, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, h, r0, r1, c0, c1, shift, r);
+          if (k1 >= 0) {
+            G.rec[2 * tid] = r;
+            rk1 = atomicAdd(&G.cnt[k1], 1);
+          }
+        }
+        if (more) aA = draw_a(P.g, key, gA);
+      });
+      if (ok && A.on2) {
+        SplatRec r;
+        k2 = make_rec(f2off, AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, h, r0, r1, c0, c1, shift, r);
+        if (k2 >= 0) {
+          G.rec[2 * tid + 1] = r;
+          rk2 = atomicAdd(&G.cnt[k2], 1);
+        }
+      }
+      if (pend) splat_chunk(ss->b[pbuf]);   // the previous chunk, while others generate
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // A: counts final
+      {
+        // (class, bank) starts: every warp scans the counts itself
+        int st[kSortClasses], tots[kSortClasses];
+        int base = 0;
+#pragma unroll
+        for (int c = 0; c < kSortClasses; ++c) {
+          const int v = G.cnt[c * 32 + lane];
+          int x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(~0u, x, o);
+            if (lane >= o) x += y;
+          }
+          st[c] = base + x - v;
+          tots[c] = __shfl_sync(~0u, x, 31);
+          base += tots[c];
+        }
+        int s1 = 0, s2 = 0;
+#pragma unroll
+        for (int c = 0; c < kSortClasses; ++c) {
+          const int a1 = __shfl_sync(~0u, st[c], k1 & 31);
+          const int a2 = __shfl_sync(~0u, st[c], k2 & 31);
+          if ((k1 >> 5) == c) s1 = a1;
+          if ((k2 >> 5) == c) s2 = a2;
+        }
+        if (k1 >= 0) G.idx[s1 + rk1] = (unsigned short)(2 * tid);
+        if (k2 >= 0) G.idx[s2 + rk2] = (unsigned short)(2 * tid + 1);
+        SortBuf& Z = ss->b[pbuf];        // splatted above: reset its counts for chunk k+1
+        for (int e = tid; e < kSortClasses * 32; e += NTW) Z.cnt[e] = 0;
+        if (tid == 0) {
+          int b0 = 0, rounds = 0;
+#pragma unroll
+          for (int c = 0; c < kSortClasses; ++c) {
+            G.cls_start[c] = b0;
+            b0 += tots[c];
+          }
+          G.cls_start[kSortClasses] = b0;
+#pragma unroll
+          for (int t = 0; t < kSortClasses; ++t) {
+            G.cls_round[t] = rounds;
+            rounds += (tots[kSortClasses - 1 - t] + 31) >> 5;
+          }
+          G.cls_round[kSortClasses] = rounds;
+          G.next_round = NWW;
+        }
+      }
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // B: sorted order published
+      pbuf ^= 1;
+      pend = 1;
+    }
+    if (sh->rows_left[buf] <= 0) break;
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
+    next_row += kMaxSeg;
+    if (warp == 0) item_stage(P, item, sh, buf, next_row);
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
+  }
+  if (pend) {
+    splat_chunk(ss->b[pbuf]);
+    // leave both count buffers zeroed for the next item (buffer pbuf^1 was reset above)
+    for (int e = tid; e < kSortClasses * 32; e += NTW) ss->b[pbuf].cnt[e] = 0;
+  }
+}
+
 template <int PSF>
 __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
-  int* acc0 = reinterpret_cast<int*>(smem_raw + sizeof(BandShared));
+  SortShared* ss = reinterpret_cast<SortShared*>(smem_raw + sizeof(BandShared));   // when rec_bytes > 0
+  int* acc0 = reinterpret_cast<int*>(smem_raw + sizeof(BandShared) + P.rec_bytes);
   int* acc1 = acc0 + P.TH * P.AS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
@@ -1474,7 +1755,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
     if (first >= P.npro) break;
     const int w = (int)first;
     if (w < P.pairs) {
-      pair_prologue<kBandBlock>(P, w, acc0, acc_bytes);
+      pair_prologue<kBandBlock>(P, w, reinterpret_cast<int*>(ss), acc_bytes);
     } else {
       const int fc = w - P.pairs;
       field_bound_chunk<kBandBlock>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
@@ -1484,6 +1765,8 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   // both frame accumulators + the zero padding behind them
   for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 8) / 4; e += kBandBlock)
     reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+  if (P.rec_bytes)
+    for (int e = tid; e < 2 * kSortClasses * 32; e += kBandBlock) ss->b[e & 1].cnt[e >> 1] = 0;
   // dynamic schedule: the staging warp takes the ticket of item k+1 and
   // prepares it (parameters + particle segments) while the workers splat item k
   PGB_STAMP(8);
@@ -1514,6 +1797,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
       band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1);
     } else {
       switch (ic.var) {
+        case kVarSorted: band_particles_sorted<PSF>(P, sh, ss, buf, item, acc0); break;
 #define PGB_V(S, W) case 16 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
         PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6) PGB_V(1, 7)
         PGB_V(1, 8) PGB_V(1, 9) PGB_V(1, 10) PGB_V(1, 11) PGB_V(1, 12)

@@ -453,7 +453,7 @@ int guarded(F&& f) {
 // Band generator (band.cuh): plan + launch
 // ----------------------------------------------------------------------------
 struct BandPlan {
-  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx, pad_rows;
+  int TH, TW, AS, tiles_y, tiles_x, tiles, sy, sx, pad_rows, rec_bytes;
   size_t smem;
 };
 
@@ -505,12 +505,32 @@ size_t band_acc_budget() {
   return v;
 }
 
-BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0) {
+// Window bound of the generator's point PSF (item_setup, per pair <= this):
+// floor(2 R_max) + 1 for the largest sigma, at most the patch side.
+int window_bound(const pgb_config* c, int halo) {
+  int wt = 2 * halo + 1;
+  if (c->psf == PGB_PSF_POINT && !(c->f2_sigma_std > 0.0))
+    wt = std::min(wt, (int)std::floor(2.0 * (double)kTightR * c->d_hi / c->sigma_ratio) + 1);
+  return wt;
+}
+
+// Large separable windows splat through bank-sorted records (SortShared ahead
+// of the accumulators); the decision is per plan, the variant per item.
+bool sorted_splat(const pgb_config* c, int halo) {
+  const bool sep = c->rho_lo == 0.0 && c->rho_hi == 0.0 && !(c->f2_rho_std > 0.0);
+  const int wt = window_bound(c, halo);
+  return c->psf == PGB_PSF_POINT && sep && wt >= kSortMinW && wt <= kMaxUnpredWM &&
+         !std::getenv("PGB_NO_SORT");
+}
+
+BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0, bool sorted = false) {
   BandPlan p{};
   cell_bits(H, W, p.sy, p.sx);
   // zero rows behind the accumulators for unpredicated splat windows (<= 7 wide)
   p.pad_rows = std::min(kMaxUnpredWM - 1, 2 * halo);
-  const size_t budget_all = (acc_budget ? acc_budget : band_acc_budget()) / 4;   // int32: two frames + padding
+  p.rec_bytes = sorted ? (int)((sizeof(SortShared) + 15) & ~(size_t)15) : 0;
+  if (sorted) p.pad_rows = kMaxUnpredWM - 1;   // window classes round up (up to 12 rows)
+  const size_t budget_all = ((acc_budget ? acc_budget : band_acc_budget()) - p.rec_bytes) / 4;   // int32: two frames + padding
   auto th_cap = [&](int AS) -> size_t {
     const size_t pad = (size_t)p.pad_rows * AS + 8;
     return budget_all > pad ? (budget_all - pad) / (2 * (size_t)AS) : 0;
@@ -551,7 +571,7 @@ BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0) {
   // histogram (2^(sy+sx) + 4 ints): small tiles get at least that much
   const size_t acc_bytes = ((size_t)(2 * p.TH + p.pad_rows) * p.AS + 8) * 4;
   const size_t hist_bytes = ((size_t)(1 << (p.sy + p.sx)) + 8) * 4;
-  p.smem = sizeof(BandShared) + std::max(acc_bytes, hist_bytes);
+  p.smem = sizeof(BandShared) + std::max(p.rec_bytes + acc_bytes, hist_bytes);
   PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
   return p;
 }
@@ -591,7 +611,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
                    bool standalone) {
   P.H = cfg->height;
   P.W = cfg->width;
-  P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS; P.pad_rows = bp.pad_rows;
+  P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS; P.pad_rows = bp.pad_rows; P.rec_bytes = bp.rec_bytes;
   P.tiles_y = bp.tiles_y; P.tiles_x = bp.tiles_x; P.tiles = bp.tiles;
   P.sy = bp.sy; P.sx = bp.sx;
   P.n = cfg->n_capacity;
@@ -720,7 +740,7 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
               "pair range exceeds the flow window (num_fields * pairs_per_field)");
   if (pairs == 0) return;
   const int halo = patch_side_exact(cfg->d_hi, cfg->patch_multiplier) / 2;
-  const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo);
+  const BandPlan bp = make_band_plan(cfg->height, cfg->width, halo, 0, sorted_splat(cfg, halo));
   BandParams P{};
   band_prologue(P, bp, cfg, batch, pair_base, pairs, flows, num_fields, pairs_per_field, stats, stream, false);
   P.out_mode = out_mode;
@@ -1223,6 +1243,13 @@ int pgb_probe_ex2_dev(int blocks, int iters, float* sink, void* stream) {
 }
 
 #ifdef PGB_TRACE
+int pgb_probe_atoms_dev(int blocks, int iters, int mode, int* sink, void* stream) {
+  return guarded([&] {
+    atoms_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters, mode);
+    PGB_CK(cudaGetLastError());
+  });
+}
+
 // Timing probes of the last band launch (debug builds only): n u64 words.
 int pgb_trace_read(unsigned long long* out, int n) {
   return guarded([&] {
