@@ -91,6 +91,7 @@ struct BandParams {
   int rec_bytes;               // SortShared region ahead of the accumulators (sorted splat), else 0
   int pro_smem;                // shared bytes the pair prologue may use (prologue kernel / band accumulators)
   int sy, sx;                  // seeding cells: 2^sy rows x 2^sx columns
+  double inv_ch, inv_cw;       // 2^sy / H, 2^sx / W (cells per pixel)
   int n, pairs;
   long long pair_base;
   uint32_t batch_lo;
@@ -107,7 +108,7 @@ struct BandParams {
   PairHdr* hdr;                // [pairs]
   int* pair_ready;             // [pairs] prologue done (in-kernel prologue), else null
   int* fb_done;                // [num_fields] finished bound chunks, else null
-  long long npro;              // prologue tickets (pairs + flow-bound chunks) ahead of the band items
+  long long npro;              // prologue tickets (flow-bound chunks, then pairs) ahead of the band items
   int4* zero_head;             // the other control head: zeroed here for the next launch (or null)
   int zero_head_n;
   int field_lo, field_cnt;     // flow fields read by this pair range
@@ -271,14 +272,36 @@ __device__ __forceinline__ void field_bound_chunk(const BandParams& P, int f, in
   const int tid = threadIdx.x, lane = tid & 31;
   const float2* fl = P.flows + (size_t)f * P.field_elems;
   float mu = 0.f, mv = 0.f;
-  const long long stride = (long long)kFieldBlocks * NT;
-#pragma unroll 4
-  for (long long e = (long long)part * NT + tid; e < P.field_elems; e += stride) {
-    const float2 v = __ldg(fl + e);
+  auto take = [&](const float2 v) {
     const float au = fabsf(v.x), av = fabsf(v.y);
     mu = au <= 3.0e38f ? fmaxf(mu, au) : INFINITY;
     mv = av <= 3.0e38f ? fmaxf(mv, av) : INFINITY;
+  };
+  // the chunk is a contiguous range of the field read as 16-byte pairs of
+  // nodes, eight loads in flight per thread (the bound gates the first band
+  // items: latency, not bandwidth, matters)
+  const long long n = P.field_elems;
+  const long long per = ((n + kFieldBlocks - 1) / kFieldBlocks + 1) & ~1LL;
+  const long long lo = min(n, (long long)part * per), hi = min(n, lo + per);
+  const float4* f4 = reinterpret_cast<const float4*>(fl + lo);   // lo even
+  const bool vec = (reinterpret_cast<uintptr_t>(fl) & 15) == 0;
+  const long long n4 = vec ? (hi - lo) >> 1 : 0;
+  if (!vec)
+    for (long long e = lo + tid; e < hi; e += NT) take(__ldg(fl + e));
+  for (long long q0 = 0; q0 < n4; q0 += 8LL * NT) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long q = q0 + (long long)k * NT + tid;
+      v[k] = q < n4 ? __ldg(f4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      take(make_float2(v[k].x, v[k].y));
+      take(make_float2(v[k].z, v[k].w));
+    }
   }
+  if (vec && ((hi - lo) & 1) && tid == 0) take(__ldg(fl + hi - 1));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mu = fmaxf(mu, __shfl_xor_sync(~0u, mu, o));
@@ -363,6 +386,14 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
   const int M = (int)mm;
   int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
   unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
+  // particle -> cell slots staged in shared memory behind the prefix, in
+  // windows of `win` slots (one window: marked during the prefix pass)
+  const int soff = ((nc4 + 4) & ~3) * 4;
+  unsigned short* scof = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(bins) + soff);
+  int4* s4 = reinterpret_cast<int4*>(scof);
+  const int win = max(8, min(128 * 256, ((smem_bytes - soff) / 2) & ~7));   // slots per window (plans leave >= 8)
+  const int M8 = (M + 7) & ~7;
+  const bool one_win = M8 <= win;
   if (warp == NS) {
     if (lane == 0) {
       PairHdr hd;
@@ -377,6 +408,8 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     int4* bins4 = reinterpret_cast<int4*>(bins);
     const int nq4 = nc4 >> 2;                    // int4 groups of cells
     for (int i = tid; i < nq4; i += NTS) bins4[i] = make_int4(0, 0, 0, 0);
+    if (one_win)
+      for (int q = tid; q < (M8 >> 3); q += NTS) s4[q] = make_int4(0, 0, 0, 0);
     scan_sync<NTS>();
     // cell histogram of M iid labels (4 labels per Philox call, two calls in flight)
     const int nq = (M + 3) >> 2;
@@ -392,9 +425,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
       }
     }
     scan_sync<NTS>();
-#ifdef PGB_TRACE
-    if (tid == 32) trace_stamp(15);
-#endif
     PGB_STAMP(3);
     // Cell counts -> exclusive prefix (in place + global) and the maximum cell
     // count. Warps own 512-cell chunks (four 128-cell layers, lanes reading
@@ -470,6 +500,13 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
             const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
             for (int k = 0; i + k < ncell; ++k) pre[i + k] = oo[k];
           }
+          if (one_win) {
+            // mark the first slot of every non-empty cell with the cell id
+            if (v[j].x) scof[o4.x] = (unsigned short)i;
+            if (v[j].y) scof[o4.y] = (unsigned short)(i + 1);
+            if (v[j].z) scof[o4.z] = (unsigned short)(i + 2);
+            if (v[j].w) scof[o4.w] = (unsigned short)(i + 3);
+          }
         }
         run += __shfl_sync(~0u, inc[j], 31);
       }
@@ -481,16 +518,10 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     scan_sync<NTS>();
     PGB_STAMP(5);
     // particle -> cell (counting-sort order: particles of cell c are
-    // pre[c] .. pre[c+1]-1), in windows of slots staged in shared memory
-    // behind the prefix: mark the first slot of every cell starting in the
-    // window with the cell id, inclusive max-scan (carry in: the cell holding
-    // the window's first slot), 16-byte stores of the scanned slots
-    const int soff = ((nc4 + 4) & ~3) * 4;
-    unsigned short* scof = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(bins) + soff);
-    int4* s4 = reinterpret_cast<int4*>(scof);
+    // pre[c] .. pre[c+1]-1), per window of slots: mark the first slot of every
+    // cell starting in the window with the cell id, inclusive max-scan (carry
+    // in: the cell holding the window's first slot), 16-byte stores
     __shared__ int wcar[128];                     // per-chunk carries of one window
-    const int win = max(8, min(128 * 256, ((smem_bytes - soff) / 2) & ~7));   // slots per window (plans leave >= 8)
-    const int M8 = (M + 7) & ~7;
     auto max8 = [](const int4 w) {
       const int a = max(max(w.x & 0xffff, (int)((unsigned)w.x >> 16)), max(w.y & 0xffff, (int)((unsigned)w.y >> 16)));
       const int b = max(max(w.z & 0xffff, (int)((unsigned)w.z >> 16)), max(w.w & 0xffff, (int)((unsigned)w.w >> 16)));
@@ -499,7 +530,8 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     for (int s0 = 0; s0 < M8; s0 += win) {
       const int s1 = min(M8, s0 + win);
       const int n4 = (s1 - s0) >> 3;               // int4 groups of 8 slots
-      for (int q = tid; q < n4; q += NTS) s4[q] = make_int4(0, 0, 0, 0);
+      if (!one_win)
+        for (int q = tid; q < n4; q += NTS) s4[q] = make_int4(0, 0, 0, 0);
       // the cell holding slot s0: last c with bins[c] <= s0 (and a non-empty run)
       int clo = 0;
       if (s0 > 0) {
@@ -511,13 +543,15 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
         }
         clo = lo;   // bins is non-decreasing and bins[ncell] = M > s0: cell clo holds slot s0
       }
-      scan_sync<NTS>();
+      if (!one_win) {
+        scan_sync<NTS>();
 #pragma unroll 8
-      for (int c = tid; c < ncell; c += NTS) {
-        const int b = bins[c];
-        if (b >= s0 && b < s1 && b < bins[c + 1]) scof[b - s0] = (unsigned short)c;
+        for (int c = tid; c < ncell; c += NTS) {
+          const int b = bins[c];
+          if (b >= s0 && b < s1 && b < bins[c + 1]) scof[b - s0] = (unsigned short)c;
+        }
+        scan_sync<NTS>();
       }
-      scan_sync<NTS>();
       // chunk maxima (256 slots = one warp layer of int4s per chunk)
       const int nch = (n4 + 31) >> 5;
       for (int ch = warp; ch < nch; ch += NS) {
@@ -1145,20 +1179,32 @@ __device__ __forceinline__ void band_store(const BandParams& P, int* acc, int pl
 }
 
 
-// Range of seeding cells [lo, hi] whose span [k*s, (k+1)*s) meets [a, b).
-__device__ __forceinline__ void cell_range(double a, double b, double s, int n, int& lo, int& hi) {
-  const double fa = floor(fmax(a, 0.0) / s);
-  const double fb = floor(fmin(b, (double)n * s) / s);
+// Range of seeding cells [lo, hi] whose span [k*s, (k+1)*s) meets [a, b)
+// (inv = 1/s; the callers' bounds carry >= 1/2 px of slack, far above the
+// rounding of a*inv, so no division is needed on the staging path).
+__device__ __forceinline__ void cell_range(double a, double b, double inv, int n, int& lo, int& hi) {
+  const double fa = floor(fmax(a, 0.0) * inv);
+  const double fb = floor(fmin(b * inv, (double)n));
   lo = (int)fmin(fa, (double)(n - 1));
   hi = (int)fmin(fmax(fb, 0.0), (double)(n - 1));
 }
 
+// Fixed-point shift without a division: the largest e <= kAccShift with
+// cnt * (amp 2^e + 1/2) <= 2^31 (the contributions of `cnt` particles of
+// amplitude <= amp, each rounded up by at most 1/2, fit an int32).
+__device__ __forceinline__ int shift_for_fast(int cnt, float amp) {
+  const double ca = (double)cnt * (double)amp;
+  int e = min(kAccShift, 31 - ilogb(ca));
+  while (e > 0 && dadd(ldexp(ca, e), 0.5 * (double)cnt) > 2147483648.0) --e;
+  return e;
+}
+
 // Item parameters (lane 0 of warp 0): tile, the cells whose particles can reach
 // it, the fixed-point shift and the window bound.
+__device__ __forceinline__ void item_finish(const BandParams& P, ItemCfg& ic);
+
 __device__ __forceinline__ void item_setup(const BandParams& P, long long item, ItemCfg& ic) {
   const GenCfg& g = P.g;
-  const int CY = 1 << P.sy, CX = 1 << P.sx;
-  const double ch = (double)g.H / (double)CY, cw = (double)g.W / (double)CX;
   long long ti = item;
   int sub = 0, nsub = 1;
   if (item >= P.split_base) {
@@ -1194,6 +1240,15 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
 #pragma unroll
     for (int k = 0; k < (int)(sizeof(PairHdr) / 16); ++k) dst[k] = __ldcg(src + k);
   }
+  item_finish(P, ic);
+}
+
+// Item parameters from the tile, the pair header (ic.hd) and the field bound:
+// the cells whose particles can reach the tile, the fixed-point shift and the
+// window bound / particle-loop variant.
+__device__ __forceinline__ void item_finish(const BandParams& P, ItemCfg& ic) {
+  const GenCfg& g = P.g;
+  const int CY = 1 << P.sy, CX = 1 << P.sx;
   const int h = ic.hd.side >> 1;
   ic.h = h;
   const float2 fb = __ldcg(P.fbound + ic.field);
@@ -1202,14 +1257,15 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
   const double vy = (double)fb.y * (1.0 + 1e-6) + 1e-6;
   const double vx = (double)fb.x * (1.0 + 1e-6) + 1e-6;
-  cell_range((double)ic.r0 - h - 1.5 - vy, (double)ic.r1 + h + 0.5 + vy, ch, CY, ic.cy0, ic.cy1);
-  cell_range((double)ic.c0 - h - 1.5 - vx, (double)ic.c1 + h + 0.5 + vx, cw, CX, ic.cx0, ic.cx1);
+  cell_range((double)ic.r0 - h - 1.5 - vy, (double)ic.r1 + h + 0.5 + vy, P.inv_ch, CY, ic.cy0, ic.cy1);
+  cell_range((double)ic.c0 - h - 1.5 - vx, (double)ic.c1 + h + 0.5 + vx, P.inv_cw, CX, ic.cx0, ic.cx1);
   // fixed-point shift: contributions per pixel <= cmax * (cells one pixel's
-  // source box can meet), amplitude <= amp_bound
-  const double by = floor((2.0 * h + 3.0 + 2.0 * vy) / ch) + 2.0;
-  const double bx = floor((2.0 * h + 3.0 + 2.0 * vx) / cw) + 2.0;
+  // source box can meet), amplitude <= amp_bound (the 1e-9 keeps the floor
+  // of an exact quotient from rounding down)
+  const double by = floor((2.0 * h + 3.0 + 2.0 * vy) * P.inv_ch + 1e-9) + 2.0;
+  const double bx = floor((2.0 * h + 3.0 + 2.0 * vx) * P.inv_cw + 1e-9) + 2.0;
   const double cov = fmin((double)ic.hd.M, (double)ic.hd.cmax * fmin(by, (double)CY) * fmin(bx, (double)CX));
-  ic.shift = shift_for(max(1, (int)cov), P.amp_bound);
+  ic.shift = shift_for_fast(max(1, (int)cov), P.amp_bound);
   // window side bound: floor(2 R_max) + 1 columns/rows, R_max from the largest
   // sigma (frame-2 sigma jitter is unbounded -> patch side)
   int wt = 2 * h + 1;
@@ -1240,6 +1296,7 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
   const ItemCfg& ic = sh->ic[b];
   const int CX = 1 << P.sx;
   const int* pre = P.prefix + (size_t)ic.pl * pre_stride((1 << P.sy) * CX);
+  auto ldp = [&](size_t i) { return __ldcg(pre + i); };
   const bool full = ic.cx0 == 0 && ic.cx1 == CX - 1;
   const int y0 = row_lo < 0 ? ic.cy0 : row_lo;
   const int nrows = ic.cy1 - y0 + 1;
@@ -1250,12 +1307,12 @@ __device__ __forceinline__ void item_stage(const BandParams& P, long long item, 
     int st = 0, len = 0;
     if (sidx < nseg) {
       if (full) {
-        st = __ldcg(pre + ((size_t)ic.cy0 << P.sx));
-        len = __ldcg(pre + ((size_t)(ic.cy1 + 1) << P.sx)) - st;
+        st = ldp((size_t)ic.cy0 << P.sx);
+        len = ldp((size_t)(ic.cy1 + 1) << P.sx) - st;
       } else {
         const int cy = y0 + sidx;
-        st = __ldcg(pre + ((size_t)cy << P.sx) + ic.cx0);
-        len = __ldcg(pre + ((size_t)cy << P.sx) + ic.cx1 + 1) - st;
+        st = ldp(((size_t)cy << P.sx) + ic.cx0);
+        len = ldp(((size_t)cy << P.sx) + ic.cx1 + 1) - st;
       }
     }
     int x = len;
@@ -1725,6 +1782,35 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
   }
 }
 
+// Workers: particles of the staged item `buf`, then the fused epilogue; two
+// block barriers (the staging warp meets them).
+template <int PSF>
+__device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh, SortShared* ss, int buf,
+                                            int* acc0, int* acc1) {
+  const ItemCfg& ic = sh->ic[buf];
+  const long long item = ic.item;
+  const int pl = ic.pl;
+  const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
+  const float scale = (float)(1 << ic.shift);
+  if constexpr (PSF == kPsfErf) {
+    band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1);
+  } else {
+    switch (ic.var) {
+      case kVarSorted: band_particles_sorted<PSF>(P, sh, ss, buf, item, acc0); break;
+#define PGB_V(S, W) case 16 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
+      PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6) PGB_V(1, 7)
+      PGB_V(1, 8) PGB_V(1, 9) PGB_V(1, 10) PGB_V(1, 11) PGB_V(1, 12)
+#undef PGB_V
+      default: band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1); break;
+    }
+  }
+  __syncthreads();   // particles done (stager: next item staged)
+  const float inv_scale = 1.0f / scale;
+  band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
+  band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
+  __syncthreads();   // accumulators zeroed
+}
+
 template <int PSF>
 __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1734,39 +1820,44 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   int* acc1 = acc0 + P.TH * P.AS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool stager = warp == kBandWarps;   // the extra warp stages items, workers splat + store
-  // the prologue borrows the accumulator region (>= its histogram, see make_band_plan)
+  // the prologue borrows the record + accumulator region (>= its histogram, see make_band_plan)
   const int acc_bytes = P.pro_smem;
+  int* bins = reinterpret_cast<int*>(ss);
+  auto zero_acc = [&]() {
+    // both frame accumulators + the zero padding behind them (the prologue
+    // borrowed them), sorted-splat counts
+    for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 8) / 4; e += kBandBlock)
+      reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
+    if (P.rec_bytes)
+      for (int e = tid; e < 2 * kSortClasses * 32; e += kBandBlock) ss->b[e & 1].cnt[e >> 1] = 0;
+  };
   PGB_STAMP(0);
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)
     for (int e = tid; e < P.zero_head_n; e += kBandBlock) P.zero_head[e] = make_int4(0, 0, 0, 0);
-  // One ticket sequence: [0, npro) prologue items (the pairs, then the
-  // flow-bound chunks), then the band items. Band items wait on prologue
-  // flags only, and every prologue ticket precedes every band ticket, so each
-  // wait targets work already taken by a running CTA that waits on nothing:
+  // One ticket sequence: [0, npro) prologue items (the flow-bound chunks,
+  // then the pairs), then the band items. Band items wait on prologue flags
+  // only, and every prologue ticket precedes every band ticket, so each wait
+  // targets work already taken by a running CTA that waits on nothing:
   // forward progress without co-residency (MPS limits, green contexts, a
   // concurrent kernel holding SMs, any grid size).
+  const int nfc = P.field_cnt * kFieldBlocks;
   long long first;
   for (;;) {
     if (tid == 0) sh->ticket0 = atomicAdd(P.ticket, 1);
     __syncthreads();
     first = sh->ticket0;
     __syncthreads();
-    PGB_STAMP(1);
     if (first >= P.npro) break;
     const int w = (int)first;
-    if (w < P.pairs) {
-      pair_prologue<kBandBlock>(P, w, reinterpret_cast<int*>(ss), acc_bytes);
+    if (w < nfc) {
+      field_bound_chunk<kBandBlock>(P, P.field_lo + w / kFieldBlocks, w % kFieldBlocks);
+      PGB_STAMP(1);
     } else {
-      const int fc = w - P.pairs;
-      field_bound_chunk<kBandBlock>(P, P.field_lo + fc / kFieldBlocks, fc % kFieldBlocks);
+      pair_prologue<kBandBlock>(P, w - nfc, bins, acc_bytes);
     }
     __syncthreads();
   }
-  // both frame accumulators + the zero padding behind them
-  for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 8) / 4; e += kBandBlock)
-    reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
-  if (P.rec_bytes)
-    for (int e = tid; e < 2 * kSortClasses * 32; e += kBandBlock) ss->b[e & 1].cnt[e >> 1] = 0;
+  zero_acc();
   // dynamic schedule: the staging warp takes the ticket of item k+1 and
   // prepares it (parameters + particle segments) while the workers splat item k
   PGB_STAMP(8);
@@ -1788,34 +1879,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
       __syncthreads();   // store done
       continue;
     }
-    const ItemCfg& ic = sh->ic[buf];
-    const long long item = ic.item;
-    const int pl = ic.pl;
-    const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
-    const float scale = (float)(1 << ic.shift);
-    if constexpr (PSF == kPsfErf) {
-      band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1);
-    } else {
-      switch (ic.var) {
-        case kVarSorted: band_particles_sorted<PSF>(P, sh, ss, buf, item, acc0); break;
-#define PGB_V(S, W) case 16 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
-        PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6) PGB_V(1, 7)
-        PGB_V(1, 8) PGB_V(1, 9) PGB_V(1, 10) PGB_V(1, 11) PGB_V(1, 12)
-#undef PGB_V
-        default: band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1); break;
-      }
-    }
-    __syncthreads();   // particles done (stager: next item staged)
-#ifdef PGB_TRACE
-    if (nitems == 1) PGB_STAMP(10);
-#endif
-    const float inv_scale = 1.0f / scale;
-    band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
-    band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
-    __syncthreads();   // accumulators zeroed
-#ifdef PGB_TRACE
-    if (nitems == 1) PGB_STAMP(11);
-#endif
+    render_item<PSF>(P, sh, ss, buf, acc0, acc1);
   }
   PGB_STAMP(12);
 #ifdef PGB_TRACE

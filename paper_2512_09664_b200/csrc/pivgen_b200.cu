@@ -614,6 +614,8 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   P.TH = bp.TH; P.TW = bp.TW; P.AS = bp.AS; P.pad_rows = bp.pad_rows; P.rec_bytes = bp.rec_bytes;
   P.tiles_y = bp.tiles_y; P.tiles_x = bp.tiles_x; P.tiles = bp.tiles;
   P.sy = bp.sy; P.sx = bp.sx;
+  P.inv_ch = (double)(1 << bp.sy) / (double)cfg->height;
+  P.inv_cw = (double)(1 << bp.sx) / (double)cfg->width;
   P.n = cfg->n_capacity;
   P.pairs = pairs;
   P.pair_base = pair_base;

@@ -57,8 +57,15 @@ def main():
             ts.append((a, b))
         torch.cuda.synchronize()
         fl = sum(a.elapsed_time(b) for a, b in ts) / n * 1e3
+        import time
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(n):
+            step(300 + k)
+        host = (time.perf_counter() - t0) / n * 1e6
+        torch.cuda.synchronize()
         print(f"{name} B={B:5d}  back-to-back {b2b:8.1f} us  flushed {fl:8.1f} us  "
-              f"({fl / B:.3f} us/pair)", flush=True)
+              f"({fl / B:.3f} us/pair)  host enqueue {host:6.1f} us/call", flush=True)
         del img1, img2
 
 
