@@ -158,14 +158,19 @@ MAX_CELL_BITS = 14
 LN2 = 0.6931471805599453
 
 
+FULL_WIDTH_MAX = 256
+
+
 def cell_bits(height: int, width: int):
-    """csrc/pivgen_b200.cu cell_bits: ~2-row x 4-column cells, at most 2^14 cells."""
+    """csrc/pivgen_b200.cu cell_bits: ~2-row x 4-column cells, at most 2^14
+    cells; images up to FULL_WIDTH_MAX wide are rendered in full-width tiles
+    and seeded in full-width cell rows (sx = 0)."""
     def bits(n, px):
         s = 0
         while (px << (s + 1)) <= n:
             s += 1
         return s
-    sy, sx = bits(height, 2), bits(width, 4)
+    sy, sx = bits(height, 2), (0 if width <= FULL_WIDTH_MAX else bits(width, 4))
     while sy + sx > MAX_CELL_BITS:
         if sx >= sy:
             sx -= 1

@@ -458,13 +458,18 @@ struct BandPlan {
 };
 
 // Seeding cells ~2 rows x 4 columns: largest s with px * 2^s <= n, total <= 2^14 cells.
+constexpr int kFullWidthMax = 256;   // images this wide: full-width tiles, full-width cell rows
+
 void cell_bits(int H, int W, int& sy, int& sx) {
-  // ~2-row x 4-column cells: full-width tiles enumerate whole cell rows, so
-  // shorter cells trim the regenerated margin (measured -2.5% at c2; 1-row
-  // cells cost more in the prologue scan than they save)
+  // ~2-row x 4-column cells: the tiles of an item enumerate the cells within
+  // reach, so short cells trim the regenerated margin (measured -2.5% at c2;
+  // 1-row cells cost more in the prologue scan than they save). Images up to
+  // kFullWidthMax wide are rendered in full-width tiles, which enumerate whole
+  // cell rows: no column cells (a 64x smaller prologue histogram and scan at
+  // 256 x 256). Mirrored by oracle/generate.py cell_bits.
   auto bits = [](int n, long long px) { int s = 0; while ((px << (s + 1)) <= n) ++s; return s; };
   sy = bits(H, 2);
-  sx = bits(W, 4);
+  sx = W <= kFullWidthMax ? 0 : bits(W, 4);
   while (sy + sx > kMaxCellBits) {
     if (sx >= sy) --sx;
     else --sy;
@@ -538,7 +543,7 @@ BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0, bool sort
   const double m = halo + 4.0;                             // typical reach beyond the tile
   int bestTW = 0, bestTH = 0;
   double best = 1e30;
-  for (int tw = 4; ; tw *= 2) {
+  for (int tw = p.sx == 0 ? W : 4; ; tw *= 2) {   // no column cells: full-width tiles only
     const int TW = std::min(tw, (W + 3) / 4 * 4);
     const int AS = TW;
     int THmax = (int)std::min<size_t>((size_t)H, th_cap(AS));
