@@ -68,7 +68,7 @@ struct GenCfg {
   uint64_t hide_thr;         // visible iff word >= hide_thr  (exactly U >= p)
   float z_lo, z_span;
   float f2_sigma_std, f2_rho_std, f2_i0_std;
-  float dz0, shape, q, w;
+  float dz0, shape, q, w, inv_dz0sq;
   int laser;
   int need_b, need_perturb;
 };
@@ -207,10 +207,25 @@ __device__ __forceinline__ void advect_anchor(uint32_t X, int a, float d, int& a
 }
 
 __device__ __forceinline__ float laser_profile(const GenCfg& g, float z) {
-  // I0(z) = q exp(-(1/sqrt(2 pi)) |2 z^2 / dZ0^2|^s)
-  const float t = 2.0f * z * z / (g.dz0 * g.dz0);
-  const float p = t > 0.f ? powf(t, g.shape) : 0.f;
-  return g.q * expf(-0.3989422804014327f * p);
+  // I0(z) = q exp(-(1/sqrt(2 pi)) |2 z^2 / dZ0^2|^s).
+  // MUFU lg2/ex2 instead of powf/expf (measured 11% of C4's instructions):
+  // amplitude relative error ~1e-6 (tests: rtol 2e-5 vs the float64 oracle);
+  // the common shapes 1 and 2 are exact products. Warp-uniform branches.
+  float lg, e2;
+  const float t = 2.0f * z * z * g.inv_dz0sq;
+  float p;
+  if (g.shape == 2.0f) {
+    p = t * t;
+  } else if (g.shape == 1.0f) {
+    p = t;
+  } else {
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(t));
+    float ep;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ep) : "f"(g.shape * lg));
+    p = t > 0.f ? ep : 0.f;
+  }
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(-0.3989422804014327f * kLog2e * p));
+  return g.q * e2;
 }
 
 // Oracle mode: float64 positions from the reference; anchor = floor(x + 1/2)

@@ -402,6 +402,7 @@ GenCfg gen_cfg_from(const pgb_config* c) {
   g.f2_rho_std = (float)c->f2_rho_std;
   g.f2_i0_std = (float)c->f2_i0_std;
   g.dz0 = (float)c->laser_dz0;
+  g.inv_dz0sq = c->laser_dz0 > 0.0 ? (float)(1.0 / (c->laser_dz0 * c->laser_dz0)) : 0.f;
   g.shape = (float)c->laser_shape;
   g.q = (float)c->laser_q;
   g.w = (float)c->laser_w;
