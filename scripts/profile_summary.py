@@ -25,7 +25,8 @@ def band_ranges():
     marks = [("prologue", "// Per-pair prologue"), ("splat", "// Tight window of one particle-frame"),
              ("store", "// Epilogue: one output quad"), ("stage", "// Range of seeding cells"),
              ("gen", "// One regenerated particle"), ("loop", "// Worker warps: regenerate"),
-             ("kernel", "__global__ void PGB_BAND_BOUNDS band_kernel"),
+             ("sorted", "// Bank-sorted splat for large windows"),
+             ("kernel", "// Workers: particles of the staged item"),
              ("end", "// Particle arrays of the generator")]
     pos = []
     for name, m in marks:
