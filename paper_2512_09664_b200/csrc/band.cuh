@@ -1283,7 +1283,9 @@ __device__ __forceinline__ void item_finish(const BandParams& P, ItemCfg& ic) {
   const int wm = (P.psf == kPsfPoint && ic.sep && ic.wt <= kMaxUnpredWM && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
   ic.var = (P.psf == kPsfPoint ? 16 * ic.sep : 0) + wm;
   // large separable windows: bank-sorted splat (plans with a record region)
-  if (P.rec_bytes && wm >= kSortMinW) ic.var = kVarSorted;
+  // (records need no padding rows: make_rec keeps windows inside the frame)
+  if (P.rec_bytes && P.psf == kPsfPoint && ic.sep && ic.wt >= kSortMinW && ic.wt <= kMaxUnpredWM)
+    ic.var = kVarSorted;
 }
 
 // Warp 0: next item's parameters + particle segments (one per cell row of the
@@ -1521,7 +1523,7 @@ __device__ __forceinline__ void band_particles(const BandParams& P, BandShared* 
 // and every slot (i, j) of the round shifts all lanes by the same i*AS + j,
 // so each ATOMS is (nearly) conflict-free. The class bounds the unpredicated
 // window (4, 6, 8, 10, 12) instead of the pair's maximum. Same per-slot values
-// as splat_sep_u (bit-identical images).
+// as splat_sep_u.
 // ----------------------------------------------------------------------------
 
 struct __align__(16) SplatRec {
@@ -1530,30 +1532,33 @@ struct __align__(16) SplatRec {
   float dx0, dy0, A, C, Ls, pad;
 };
 
-struct __align__(16) SortBuf {
+struct __align__(16) SortShared {
   SplatRec rec[2 * kBandThreads];            // record of (thread, frame), unsorted
   unsigned short idx[2 * kBandThreads];      // sorted order -> record
   int cnt[kSortClasses * 32];                // (class, bank) counts
+  int start[kSortClasses * 32];              // (class, bank) exclusive starts
   int cls_start[kSortClasses + 1];           // class starts in sorted order
-  int cls_round[kSortClasses + 1];           // prefix of rounds, largest class first
-  int next_round;                            // dynamic round counter (work stealing)
-};
-
-// Two buffers: chunk k is generated into buf k&1 while chunk k-1 is splatted.
-struct __align__(16) SortShared {
-  SortBuf b[2];
+  int cls_round[kSortClasses + 1];           // prefix of rounds per class
 };
 
 // Record of one separable particle-frame; returns its sort key or -1 (no pixel
-// of the tile in the window).
-__device__ __forceinline__ int make_rec(int f_off, int AS, int ax, int ay, float fx, float fy, float amp,
-                                        float sx, float sy, int h, int r0, int r1, int c0, int c1, int shift,
-                                        SplatRec& r) {
+// of the tile in the window). The class bounds the unpredicated WM x WM
+// window; a window that would run past the frame's TH accumulator rows starts
+// higher instead (its rows above the particle's window get Y = 0), so the
+// sorted path needs no padding rows behind the accumulators.
+__device__ __forceinline__ int make_rec(int f_off, int AS, int TH, int ax, int ay, float fx, float fy,
+                                        float amp, float sx, float sy, int h, int r0, int r1, int c0, int c1,
+                                        int shift, SplatRec& r) {
   const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
   int rlo, clo, nr, nc;
   if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return -1;
+  const int w = max(nr, nc);
+  const int cls = w <= 4 ? 0 : min(kSortClasses - 1, (w - 3) >> 1);   // 5-6: 1, 7-8: 2, 9-10: 3, 11-12: 4
+  const int top = r0 + TH - (4 + 2 * cls);   // last origin row whose window stays in the frame
+  const int off = (rlo > top && top >= r0) ? rlo - top : 0;
+  rlo -= off;
   r.base = f_off + (rlo - r0) * AS + (clo - c0);
-  r.nrnc = nr | (nc << 16);
+  r.nrnc = off | ((off + nr) << 8) | (nc << 16);
   r.dx0 = (float)(clo - ax) - fx;
   r.dy0 = (float)(rlo - ay) - fy;
   const float isx = rcp_approx(sx), isy = rcp_approx(sy);
@@ -1561,16 +1566,15 @@ __device__ __forceinline__ int make_rec(int f_off, int AS, int ax, int ay, float
   r.C = (0.5f * kLog2e) * isy * isy;
   r.Ls = lg2_approx(amp) + (float)shift;
   r.pad = 0.f;
-  const int w = max(nr, nc);
-  const int cls = w <= 4 ? 0 : min(kSortClasses - 1, (w - 3) >> 1);   // 5-6: 1, 7-8: 2, 9-10: 3, 11-12: 4
   return cls * 32 + (r.base & 31);
 }
 
 // One record, unpredicated WM x WM window (slots outside the record's window
-// add exactly 0; pad rows behind the frame-2 accumulator absorb the overhang).
+// add exactly 0; rows [rlo, rhi) of the window carry the particle, columns
+// past the tile's last row spill into the accumulator's slack words).
 template <int WM>
 __device__ __forceinline__ void splat_rec(int* __restrict__ acc, int AS, const SplatRec& r) {
-  const int nr = r.nrnc & 0xffff, nc = r.nrnc >> 16;
+  const int rlo = r.nrnc & 0xff, rhi = (r.nrnc >> 8) & 0xff, nc = r.nrnc >> 16;
   int* base = acc + r.base;
   float X[WM];
 #pragma unroll
@@ -1585,7 +1589,7 @@ __device__ __forceinline__ void splat_rec(int* __restrict__ acc, int AS, const S
     for (int i = 0; i < WM; ++i) {
       const float dy = r.dy0 + (float)i;
       const float yv = ex2_approx(-r.C * dy * dy);
-      Y[i] = i < nr ? yv : 0.f;
+      Y[i] = (i >= rlo && i < rhi) ? yv : 0.f;
     }
 #pragma unroll
     for (int i = 0; i < WM; ++i) {
@@ -1599,7 +1603,7 @@ __device__ __forceinline__ void splat_rec(int* __restrict__ acc, int AS, const S
     for (int i = 0; i < WM; ++i) {
       const float dy = r.dy0 + (float)i;
       const float yv = ex2_approx(-r.C * dy * dy);
-      const float Y = i < nr ? yv : 0.f;
+      const float Y = (i >= rlo && i < rhi) ? yv : 0.f;
       int* row = base + i * AS;
 #pragma unroll
       for (int j = 0; j < WM; ++j)
@@ -1608,14 +1612,12 @@ __device__ __forceinline__ void splat_rec(int* __restrict__ acc, int AS, const S
   }
 }
 
-// Worker warps, sorted splat. Per chunk k of NTW particle slots:
-//   G(k): regenerate, write records into buffer k&1, count (class, bank) keys
-//   S(k-1): splat the previous chunk's rounds (buffer (k-1)&1), work-stealing
-//   barrier A; every warp scans the counts (redundantly: no serial step),
-//   scatters its own records' sorted positions; warp 0 publishes the class
-//   layout; barrier B.
-// Two named barriers per chunk; generation of one chunk overlaps the splat of
-// the previous one across warps. Workers' named barrier BAR.
+// Worker warps, sorted splat: per chunk of NTW particle slots, (1) regenerate
+// and write records + count keys, (2) warp 0 scans the counts, (3) scatter the
+// sorted order, (4) splat rounds (warp w takes rounds w, w + 8, ...). Workers'
+// named barrier BAR. (Measured against a double-buffered variant that overlaps
+// the generation of chunk k with the splat of chunk k-1: that one needs twice
+// the record space, i.e. shorter tiles, and was slower.)
 template <int PSF, int NTW = kBandThreads, int BAR = 1>
 __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandShared* sh, SortShared* ss,
                                                       int buf, long long item, int* acc0) {
@@ -1631,33 +1633,6 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
   const unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
   const RngKey key = band_key(P, pl);
   int next_row = ic.cy0;
-  int pend = 0;   // chunks generated but not yet splatted (0 or 1), in buffer pbuf
-  int pbuf = 0;
-  // splat the rounds of buffer b (all workers, dynamic rounds)
-  auto splat_chunk = [&](SortBuf& B) {
-    const int nrounds = B.cls_round[kSortClasses];
-    for (int rr = warp; rr < nrounds;) {
-      int t = 0;
-      while (rr >= B.cls_round[t + 1]) ++t;
-      const int c = kSortClasses - 1 - t;
-      const int R = B.cls_round[t + 1] - B.cls_round[t];
-      const int cs = B.cls_start[c];
-      const int k = (rr - B.cls_round[t]) + lane * R;
-      int nxt = 0;
-      if (lane == 0) nxt = atomicAdd(&B.next_round, 1);
-      if (k < B.cls_start[c + 1] - cs) {
-        const SplatRec r = B.rec[B.idx[cs + k]];
-        switch (c) {   // warp-uniform
-          case 0: splat_rec<4>(acc0, AS, r); break;
-          case 1: splat_rec<6>(acc0, AS, r); break;
-          case 2: splat_rec<8>(acc0, AS, r); break;
-          case 3: splat_rec<10>(acc0, AS, r); break;
-          default: splat_rec<12>(acc0, AS, r); break;
-        }
-      }
-      rr = __shfl_sync(~0u, nxt, 0);
-    }
-  };
   for (;;) {
     const int nseg = sh->nseg[buf];
     const int N = sh->seg_off[buf][nseg];
@@ -1686,7 +1661,6 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
       aA = draw_a(P.g, key, gA);
     }
     for (int qb = 0; qb < N; qb += NTW) {
-      SortBuf& G = ss->b[pbuf ^ 1];   // this chunk
       const int qa = qb + tid;
       const int giA = gA, ccA = cA;
       const uint4 a = aA;
@@ -1701,84 +1675,79 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
       band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
         if (ok && F.on1) {
           SplatRec r;
-          k1 = make_rec(0, AS, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, h, r0, r1, c0, c1, shift, r);
+          k1 = make_rec(0, AS, P.TH, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, h, r0, r1, c0, c1, shift, r);
           if (k1 >= 0) {
-            G.rec[2 * tid] = r;
-            rk1 = atomicAdd(&G.cnt[k1], 1);
+            ss->rec[2 * tid] = r;
+            rk1 = atomicAdd(&ss->cnt[k1], 1);
           }
         }
         if (more) aA = draw_a(P.g, key, gA);
       });
       if (ok && A.on2) {
         SplatRec r;
-        k2 = make_rec(f2off, AS, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, h, r0, r1, c0, c1, shift, r);
+        k2 = make_rec(f2off, AS, P.TH, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, h, r0, r1, c0, c1, shift, r);
         if (k2 >= 0) {
-          G.rec[2 * tid + 1] = r;
-          rk2 = atomicAdd(&G.cnt[k2], 1);
+          ss->rec[2 * tid + 1] = r;
+          rk2 = atomicAdd(&ss->cnt[k2], 1);
         }
       }
-      if (pend) splat_chunk(ss->b[pbuf]);   // the previous chunk, while others generate
-      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // A: counts final
-      {
-        // (class, bank) starts: every warp scans the counts itself
-        int st[kSortClasses], tots[kSortClasses];
-        int base = 0;
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
+      if (warp == 0) {
+        // (class, bank) counts -> starts; class starts and rounds; reset counts
+        int base = 0, rounds = 0;
 #pragma unroll
         for (int c = 0; c < kSortClasses; ++c) {
-          const int v = G.cnt[c * 32 + lane];
+          const int v = ss->cnt[c * 32 + lane];
           int x = v;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(~0u, x, o);
             if (lane >= o) x += y;
           }
-          st[c] = base + x - v;
-          tots[c] = __shfl_sync(~0u, x, 31);
-          base += tots[c];
-        }
-        int s1 = 0, s2 = 0;
-#pragma unroll
-        for (int c = 0; c < kSortClasses; ++c) {
-          const int a1 = __shfl_sync(~0u, st[c], k1 & 31);
-          const int a2 = __shfl_sync(~0u, st[c], k2 & 31);
-          if ((k1 >> 5) == c) s1 = a1;
-          if ((k2 >> 5) == c) s2 = a2;
-        }
-        if (k1 >= 0) G.idx[s1 + rk1] = (unsigned short)(2 * tid);
-        if (k2 >= 0) G.idx[s2 + rk2] = (unsigned short)(2 * tid + 1);
-        SortBuf& Z = ss->b[pbuf];        // splatted above: reset its counts for chunk k+1
-        for (int e = tid; e < kSortClasses * 32; e += NTW) Z.cnt[e] = 0;
-        if (tid == 0) {
-          int b0 = 0, rounds = 0;
-#pragma unroll
-          for (int c = 0; c < kSortClasses; ++c) {
-            G.cls_start[c] = b0;
-            b0 += tots[c];
+          ss->start[c * 32 + lane] = base + x - v;
+          ss->cnt[c * 32 + lane] = 0;
+          const int tot = __shfl_sync(~0u, x, 31);
+          if (lane == 0) {
+            ss->cls_start[c] = base;
+            ss->cls_round[c] = rounds;
           }
-          G.cls_start[kSortClasses] = b0;
-#pragma unroll
-          for (int t = 0; t < kSortClasses; ++t) {
-            G.cls_round[t] = rounds;
-            rounds += (tots[kSortClasses - 1 - t] + 31) >> 5;
-          }
-          G.cls_round[kSortClasses] = rounds;
-          G.next_round = NWW;
+          base += tot;
+          rounds += (tot + 31) >> 5;
+        }
+        if (lane == 0) {
+          ss->cls_start[kSortClasses] = base;
+          ss->cls_round[kSortClasses] = rounds;
         }
       }
-      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // B: sorted order published
-      pbuf ^= 1;
-      pend = 1;
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
+      if (k1 >= 0) ss->idx[ss->start[k1] + rk1] = (unsigned short)(2 * tid);
+      if (k2 >= 0) ss->idx[ss->start[k2] + rk2] = (unsigned short)(2 * tid + 1);
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
+      const int nrounds = ss->cls_round[kSortClasses];
+      for (int rr = warp; rr < nrounds; rr += NWW) {
+        int c = 0;
+        while (rr >= ss->cls_round[c + 1]) ++c;
+        const int R = ss->cls_round[c + 1] - ss->cls_round[c];
+        const int cs = ss->cls_start[c];
+        const int k = (rr - ss->cls_round[c]) + lane * R;
+        if (k < ss->cls_start[c + 1] - cs) {
+          const SplatRec r = ss->rec[ss->idx[cs + k]];
+          switch (c) {   // warp-uniform
+            case 0: splat_rec<4>(acc0, AS, r); break;
+            case 1: splat_rec<6>(acc0, AS, r); break;
+            case 2: splat_rec<8>(acc0, AS, r); break;
+            case 3: splat_rec<10>(acc0, AS, r); break;
+            default: splat_rec<12>(acc0, AS, r); break;
+          }
+        }
+      }
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
     }
     if (sh->rows_left[buf] <= 0) break;
     asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
     next_row += kMaxSeg;
     if (warp == 0) item_stage(P, item, sh, buf, next_row);
     asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
-  }
-  if (pend) {
-    splat_chunk(ss->b[pbuf]);
-    // leave both count buffers zeroed for the next item (buffer pbuf^1 was reset above)
-    for (int e = tid; e < kSortClasses * 32; e += NTW) ss->b[pbuf].cnt[e] = 0;
   }
 }
 
@@ -1826,10 +1795,10 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   auto zero_acc = [&]() {
     // both frame accumulators + the zero padding behind them (the prologue
     // borrowed them), sorted-splat counts
-    for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 8) / 4; e += kBandBlock)
+    for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 16) / 4; e += kBandBlock)
       reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
     if (P.rec_bytes)
-      for (int e = tid; e < 2 * kSortClasses * 32; e += kBandBlock) ss->b[e & 1].cnt[e >> 1] = 0;
+      for (int e = tid; e < kSortClasses * 32; e += kBandBlock) ss->cnt[e] = 0;
   };
   PGB_STAMP(0);
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)

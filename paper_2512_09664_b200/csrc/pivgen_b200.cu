@@ -535,10 +535,10 @@ BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0, bool sort
   // zero rows behind the accumulators for unpredicated splat windows (<= 7 wide)
   p.pad_rows = std::min(kMaxUnpredWM - 1, 2 * halo);
   p.rec_bytes = sorted ? (int)((sizeof(SortShared) + 15) & ~(size_t)15) : 0;
-  if (sorted) p.pad_rows = kMaxUnpredWM - 1;   // window classes round up (up to 12 rows)
+  if (sorted) p.pad_rows = 0;   // records start high enough to stay in the frame (make_rec)
   const size_t budget_all = ((acc_budget ? acc_budget : band_acc_budget()) - p.rec_bytes) / 4;   // int32: two frames + padding
   auto th_cap = [&](int AS) -> size_t {
-    const size_t pad = (size_t)p.pad_rows * AS + 8;
+    const size_t pad = (size_t)p.pad_rows * AS + 16;
     return budget_all > pad ? (budget_all - pad) / (2 * (size_t)AS) : 0;
   };
   const double m = halo + 4.0;                             // typical reach beyond the tile
@@ -575,7 +575,10 @@ BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0, bool sort
   p.tiles = p.tiles_y * p.tiles_x;
   // the in-kernel pair prologue borrows the accumulator region for its cell
   // histogram (2^(sy+sx) + 4 ints): small tiles get at least that much
-  const size_t acc_bytes = ((size_t)(2 * p.TH + p.pad_rows) * p.AS + 8) * 4;
+  // records need TH >= 12 rows to start inside the frame; shorter tiles
+  // (images under 12 rows) keep padding rows
+  if (sorted && p.TH < kMaxUnpredWM) p.pad_rows = kMaxUnpredWM - p.TH;
+  const size_t acc_bytes = ((size_t)(2 * p.TH + p.pad_rows) * p.AS + 16) * 4;
   const size_t hist_bytes = ((size_t)(1 << (p.sy + p.sx)) + 8) * 4;
   p.smem = sizeof(BandShared) + std::max(p.rec_bytes + acc_bytes, hist_bytes);
   PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
@@ -779,6 +782,11 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.split_base = R * (F >= ctas ? (long long)ctas : G);
   P.split_s = sp;
   P.total_items = P.split_base + rem * sp;
+  if (std::getenv("PGB_VERBOSE"))
+    std::fprintf(stderr, "pgb band plan: %dx%d tiles of %dx%d (AS %d, pad %d), cells 2^%d x 2^%d, smem %zu "
+                 "(records %d), grid %lld, items %lld (split %d)\n",
+                 bp.tiles_y, bp.tiles_x, bp.TH, bp.TW, bp.AS, bp.pad_rows, bp.sy, bp.sx, bp.smem, bp.rec_bytes,
+                 G, P.total_items, sp);
   fn<<<(int)G, kBandBlock, bp.smem, stream>>>(P);
   g_launches.fetch_add(1);
 }

@@ -51,8 +51,8 @@ def main():
     for k in range(5):
         step(k)
     torch.cuda.synchronize()
-    flush.zero_()
     lib.pgb_trace_clear()
+    flush.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     step(9)
