@@ -411,19 +411,28 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     if (one_win)
       for (int q = tid; q < (M8 >> 3); q += NTS) s4[q] = make_int4(0, 0, 0, 0);
     scan_sync<NTS>();
-    // cell histogram of M iid labels (4 labels per Philox call, two calls in flight)
+    // cell histogram of M iid labels (4 labels per Philox call; up to four
+    // calls in flight per thread when M is large)
     const int nq = (M + 3) >> 2;
-    for (int q = tid; q < nq; q += 2 * NTS) {
-      const int q2 = q + NTS;
+    auto labels = [&](int q) {
       const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
-      const uint4 b = philox_rk(make_uint4((uint32_t)q2, key.pair, key.batch, kTagCell), g.rk);
-      const uint32_t ws[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      const uint32_t ws[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int idx = k < 4 ? 4 * q + k : 4 * q2 + (k - 4);
-        if (idx < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
-      }
+      for (int k = 0; k < 4; ++k)
+        if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+    };
+    int q = tid;
+    for (; q + 3 * NTS < nq; q += 4 * NTS) {
+      const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
+      const uint4 b = philox_rk(make_uint4((uint32_t)(q + NTS), key.pair, key.batch, kTagCell), g.rk);
+      const uint4 c = philox_rk(make_uint4((uint32_t)(q + 2 * NTS), key.pair, key.batch, kTagCell), g.rk);
+      const uint4 d = philox_rk(make_uint4((uint32_t)(q + 3 * NTS), key.pair, key.batch, kTagCell), g.rk);
+      const uint32_t ws[16] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k)   // full groups: 4 (q + 3 NTS) + 3 < 4 nq ... only the last may be partial
+        if (4 * (q + (k >> 2) * NTS) + (k & 3) < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
     }
+    for (; q < nq; q += NTS) labels(q);
     scan_sync<NTS>();
     PGB_STAMP(3);
     // Cell counts -> exclusive prefix (in place + global) and the maximum cell
@@ -544,11 +553,22 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
         clo = lo;   // bins is non-decreasing and bins[ncell] = M > s0: cell clo holds slot s0
       }
       if (!one_win) {
+        // cells starting inside the window: (clo, chi], chi = last c with bins[c] < s1
+        int chi = ncell - 1;
+        if (s1 < M) {
+          int lo = clo, hi = ncell - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (bins[mid] < s1) lo = mid;
+            else hi = mid - 1;
+          }
+          chi = lo;
+        }
         scan_sync<NTS>();
-#pragma unroll 8
-        for (int c = tid; c < ncell; c += NTS) {
+#pragma unroll 4
+        for (int c = clo + tid; c <= chi; c += NTS) {
           const int b = bins[c];
-          if (b >= s0 && b < s1 && b < bins[c + 1]) scof[b - s0] = (unsigned short)c;
+          if (b >= s0 && b < bins[c + 1]) scof[b - s0] = (unsigned short)c;
         }
         scan_sync<NTS>();
       }
