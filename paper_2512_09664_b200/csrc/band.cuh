@@ -65,6 +65,8 @@ constexpr int kMaxCellBits = 14;
 constexpr int kMaxUnpredWM = 12;   // largest unpredicated (separable) splat window
 constexpr int kSortClasses = 5;    // sorted splat window classes: 4, 6, 8, 10, 12
 constexpr int kSortMinW = 7;       // items whose window bound reaches this use the sorted splat
+constexpr int kLaneWM = kSortMinW - 1;   // largest per-lane unpredicated window (code size: the
+                                         // kernel holds one unrolled particle loop per window)
 constexpr int kVarSorted = 100;    // ItemCfg::var of the sorted splat
 
 struct __align__(16) PairHdr {
@@ -1300,7 +1302,9 @@ __device__ __forceinline__ void item_finish(const BandParams& P, ItemCfg& ic) {
   // unpredicated windows for uncorrelated particles only: the correlated
   // variant (splat_point_u) showed tiling-dependent 1-ulp differences in the
   // stress test (scripts/stress.py); correlated particles use the dynamic loops
-  const int wm = (P.psf == kPsfPoint && ic.sep && ic.wt <= kMaxUnpredWM && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
+  // (per-lane unpredicated windows up to kLaneWM; larger separable windows
+  // take the bank-sorted splat, or the dynamic loops when PGB_NO_SORT)
+  const int wm = (P.psf == kPsfPoint && ic.sep && ic.wt <= kLaneWM && ic.wt - 1 <= P.pad_rows) ? ic.wt : 0;
   ic.var = (P.psf == kPsfPoint ? 16 * ic.sep : 0) + wm;
   // large separable windows: bank-sorted splat (plans with a record region)
   // (records need no padding rows: make_rec keeps windows inside the frame)
@@ -1787,8 +1791,7 @@ __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh,
     switch (ic.var) {
       case kVarSorted: band_particles_sorted<PSF>(P, sh, ss, buf, item, acc0); break;
 #define PGB_V(S, W) case 16 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
-      PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6) PGB_V(1, 7)
-      PGB_V(1, 8) PGB_V(1, 9) PGB_V(1, 10) PGB_V(1, 11) PGB_V(1, 12)
+      PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6)
 #undef PGB_V
       default: band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1); break;
     }
