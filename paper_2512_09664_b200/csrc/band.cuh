@@ -1560,7 +1560,6 @@ struct __align__(16) SortShared {
   SplatRec rec[2 * kBandThreads];            // record of (thread, frame), unsorted
   unsigned short idx[2 * kBandThreads];      // sorted order -> record
   int cnt[kSortClasses * 32];                // (class, bank) counts
-  int start[kSortClasses * 32];              // (class, bank) exclusive starts
   int cls_start[kSortClasses + 1];           // class starts in sorted order
   int cls_round[kSortClasses + 1];           // prefix of rounds per class
 };
@@ -1715,10 +1714,12 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
           rk2 = atomicAdd(&ss->cnt[k2], 1);
         }
       }
-      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
-      if (warp == 0) {
-        // (class, bank) counts -> starts; class starts and rounds; reset counts
-        int base = 0, rounds = 0;
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // counts final
+      {
+        // (class, bank) starts: every warp scans the counts itself (no serial
+        // step), then scatters its own records' sorted positions
+        int st[kSortClasses], tots[kSortClasses];
+        int base = 0;
 #pragma unroll
         for (int c = 0; c < kSortClasses; ++c) {
           const int v = ss->cnt[c * 32 + lane];
@@ -1728,25 +1729,35 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
             const int y = __shfl_up_sync(~0u, x, o);
             if (lane >= o) x += y;
           }
-          ss->start[c * 32 + lane] = base + x - v;
-          ss->cnt[c * 32 + lane] = 0;
-          const int tot = __shfl_sync(~0u, x, 31);
-          if (lane == 0) {
-            ss->cls_start[c] = base;
-            ss->cls_round[c] = rounds;
-          }
-          base += tot;
-          rounds += (tot + 31) >> 5;
+          st[c] = base + x - v;
+          tots[c] = __shfl_sync(~0u, x, 31);
+          base += tots[c];
         }
-        if (lane == 0) {
-          ss->cls_start[kSortClasses] = base;
+        int s1 = 0, s2 = 0;
+#pragma unroll
+        for (int c = 0; c < kSortClasses; ++c) {
+          const int a1 = __shfl_sync(~0u, st[c], k1 & 31);
+          const int a2 = __shfl_sync(~0u, st[c], k2 & 31);
+          if ((k1 >> 5) == c) s1 = a1;
+          if ((k2 >> 5) == c) s2 = a2;
+        }
+        if (k1 >= 0) ss->idx[s1 + rk1] = (unsigned short)(2 * tid);
+        if (k2 >= 0) ss->idx[s2 + rk2] = (unsigned short)(2 * tid + 1);
+        if (tid == 0) {
+          int b0 = 0, rounds = 0;
+#pragma unroll
+          for (int c = 0; c < kSortClasses; ++c) {
+            ss->cls_start[c] = b0;
+            ss->cls_round[c] = rounds;
+            b0 += tots[c];
+            rounds += (tots[c] + 31) >> 5;
+          }
+          ss->cls_start[kSortClasses] = b0;
           ss->cls_round[kSortClasses] = rounds;
         }
       }
-      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
-      if (k1 >= 0) ss->idx[ss->start[k1] + rk1] = (unsigned short)(2 * tid);
-      if (k2 >= 0) ss->idx[ss->start[k2] + rk2] = (unsigned short)(2 * tid + 1);
-      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // sorted order published
+      for (int e = tid; e < kSortClasses * 32; e += NTW) ss->cnt[e] = 0;   // every warp has read them
       const int nrounds = ss->cls_round[kSortClasses];
       for (int rr = warp; rr < nrounds; rr += NWW) {
         int c = 0;
