@@ -538,10 +538,14 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
       const int b = max(max(w.z & 0xffff, (int)((unsigned)w.z >> 16)), max(w.w & 0xffff, (int)((unsigned)w.w >> 16)));
       return max(a, b);
     };
+    // dense cells (>= 2 particles per cell on average, e.g. C3's 6.4): every
+    // cell writes its run into the window directly (no scans); sparse cells
+    // (C2's 0.5) mark run starts and max-scan
+    const bool dense = !one_win && M >= 2 * ncell;
     for (int s0 = 0; s0 < M8; s0 += win) {
       const int s1 = min(M8, s0 + win);
       const int n4 = (s1 - s0) >> 3;               // int4 groups of 8 slots
-      if (!one_win)
+      if (!one_win && !dense)
         for (int q = tid; q < n4; q += NTS) s4[q] = make_int4(0, 0, 0, 0);
       // the cell holding slot s0: last c with bins[c] <= s0 (and a non-empty run)
       int clo = 0;
@@ -553,6 +557,36 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
           else hi = mid - 1;
         }
         clo = lo;   // bins is non-decreasing and bins[ncell] = M > s0: cell clo holds slot s0
+      }
+      if (dense) {
+        int chi = ncell - 1;   // last cell with a slot in the window
+        if (s1 < M) {
+          int lo = clo, hi = ncell - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (bins[mid] < s1) lo = mid;
+            else hi = mid - 1;
+          }
+          chi = lo;
+        }
+        for (int cb = clo + warp * 32; cb <= chi; cb += NTS) {   // warp-uniform trip count
+          const int c = cb + lane;
+          int j0 = 0, n = 0;
+          if (c <= chi) {
+            j0 = max(bins[c], s0);
+            n = min(bins[c + 1], s1) - j0;
+          }
+          const int nmax = __reduce_max_sync(~0u, n);
+          for (int k = 0; k < nmax; ++k)
+            if (k < n) scof[j0 + k - s0] = (unsigned short)c;
+        }
+        if (tid < 8 && M + tid < s1) scof[M + tid - s0] = 0;   // padding slots of the last window
+        scan_sync<NTS>();
+        const int4* src = reinterpret_cast<const int4*>(scof);
+        int4* dst = reinterpret_cast<int4*>(cof + s0);
+        for (int q = tid; q < n4; q += NTS) dst[q] = src[q];
+        if (s1 < M8) scan_sync<NTS>();
+        continue;
       }
       if (!one_win) {
         // cells starting inside the window: (clo, chi], chi = last c with bins[c] < s1
