@@ -424,15 +424,16 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
         if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
     };
     int q = tid;
-    for (; q + 3 * NTS < nq; q += 4 * NTS) {
+    // full groups (the last call, q = nq - 1, may hold labels >= M: left to
+    // the checked tail loop), unconditional atomics
+    for (; q + 3 * NTS < nq - 1; q += 4 * NTS) {
       const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
       const uint4 b = philox_rk(make_uint4((uint32_t)(q + NTS), key.pair, key.batch, kTagCell), g.rk);
       const uint4 c = philox_rk(make_uint4((uint32_t)(q + 2 * NTS), key.pair, key.batch, kTagCell), g.rk);
       const uint4 d = philox_rk(make_uint4((uint32_t)(q + 3 * NTS), key.pair, key.batch, kTagCell), g.rk);
       const uint32_t ws[16] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
 #pragma unroll
-      for (int k = 0; k < 16; ++k)   // full groups: 4 (q + 3 NTS) + 3 < 4 nq ... only the last may be partial
-        if (4 * (q + (k >> 2) * NTS) + (k & 3) < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+      for (int k = 0; k < 16; ++k) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
     }
     for (; q < nq; q += NTS) labels(q);
     scan_sync<NTS>();
