@@ -1591,9 +1591,11 @@ struct __align__(16) SplatRec {
   float dx0, dy0, A, C, Ls, pad;
 };
 
+constexpr int kSortPPT = 2;        // particles per worker thread per sorted chunk
+
 struct __align__(16) SortShared {
-  SplatRec rec[2 * kBandThreads];            // record of (thread, frame), unsorted
-  unsigned short idx[2 * kBandThreads];      // sorted order -> record
+  SplatRec rec[2 * kSortPPT * kBandThreads];          // record of (thread, particle, frame), unsorted
+  unsigned short idx[2 * kSortPPT * kBandThreads];    // sorted order -> record
   int cnt[kSortClasses * 32];                // (class, bank) counts
   int cls_start[kSortClasses + 1];           // class starts in sorted order
   int cls_round[kSortClasses + 1];           // prefix of rounds per class
@@ -1718,36 +1720,44 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
       cA = __ldcg(cof + gA);
       aA = draw_a(P.g, key, gA);
     }
-    for (int qb = 0; qb < N; qb += NTW) {
-      const int qa = qb + tid;
-      const int giA = gA, ccA = cA;
-      const uint4 a = aA;
-      const bool more = qb + NTW < N;
-      if (more) {
-        gA = locate(qa + NTW);
-        cA = __ldcg(cof + gA);
-      }
-      PFrames A;
-      const bool ok = qa < N;
-      int k1 = -1, k2 = -1, rk1 = 0, rk2 = 0;
-      band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
-        if (ok && F.on1) {
+    for (int qc = 0; qc < N; qc += kSortPPT * NTW) {
+      int kk[2 * kSortPPT], rk[2 * kSortPPT];
+#pragma unroll
+      for (int p = 0; p < kSortPPT; ++p) {
+        const int qb = qc + p * NTW;
+        const int qa = qb + tid;
+        const int giA = gA, ccA = cA;
+        const uint4 a = aA;
+        const bool more = qb + NTW < N;
+        if (more) {
+          gA = locate(qa + NTW);
+          cA = __ldcg(cof + gA);
+        }
+        PFrames A;
+        const bool ok = qa < N;
+        int k1 = -1, k2 = -1, rk1 = 0, rk2 = 0;
+        const int slot = 2 * (p * NTW + tid);
+        band_gen(P, key, hd, flow, giA, ccA, a, h, r0, r1, c0, c1, A, [&](const PFrames& F) {
+          if (ok && F.on1) {
+            SplatRec r;
+            k1 = make_rec(0, AS, P.TH, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, h, r0, r1, c0, c1, shift, r);
+            if (k1 >= 0) {
+              ss->rec[slot] = r;
+              rk1 = atomicAdd(&ss->cnt[k1], 1);
+            }
+          }
+          if (more) aA = draw_a(P.g, key, gA);
+        });
+        if (ok && A.on2) {
           SplatRec r;
-          k1 = make_rec(0, AS, P.TH, F.ax1, F.ay1, F.fx1, F.fy1, F.amp1, F.sig, F.sig, h, r0, r1, c0, c1, shift, r);
-          if (k1 >= 0) {
-            ss->rec[2 * tid] = r;
-            rk1 = atomicAdd(&ss->cnt[k1], 1);
+          k2 = make_rec(f2off, AS, P.TH, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, h, r0, r1, c0, c1, shift, r);
+          if (k2 >= 0) {
+            ss->rec[slot + 1] = r;
+            rk2 = atomicAdd(&ss->cnt[k2], 1);
           }
         }
-        if (more) aA = draw_a(P.g, key, gA);
-      });
-      if (ok && A.on2) {
-        SplatRec r;
-        k2 = make_rec(f2off, AS, P.TH, A.ax2, A.ay2, A.fx2, A.fy2, A.amp2, A.sx2, A.sy2, h, r0, r1, c0, c1, shift, r);
-        if (k2 >= 0) {
-          ss->rec[2 * tid + 1] = r;
-          rk2 = atomicAdd(&ss->cnt[k2], 1);
-        }
+        kk[2 * p] = k1; rk[2 * p] = rk1;
+        kk[2 * p + 1] = k2; rk[2 * p + 1] = rk2;
       }
       asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // counts final
       {
@@ -1768,16 +1778,16 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
           tots[c] = __shfl_sync(~0u, x, 31);
           base += tots[c];
         }
-        int s1 = 0, s2 = 0;
 #pragma unroll
-        for (int c = 0; c < kSortClasses; ++c) {
-          const int a1 = __shfl_sync(~0u, st[c], k1 & 31);
-          const int a2 = __shfl_sync(~0u, st[c], k2 & 31);
-          if ((k1 >> 5) == c) s1 = a1;
-          if ((k2 >> 5) == c) s2 = a2;
+        for (int e = 0; e < 2 * kSortPPT; ++e) {
+          int sv = 0;
+#pragma unroll
+          for (int c = 0; c < kSortClasses; ++c) {
+            const int a1 = __shfl_sync(~0u, st[c], kk[e] & 31);
+            if ((kk[e] >> 5) == c) sv = a1;
+          }
+          if (kk[e] >= 0) ss->idx[sv + rk[e]] = (unsigned short)(2 * ((e >> 1) * NTW + tid) + (e & 1));
         }
-        if (k1 >= 0) ss->idx[s1 + rk1] = (unsigned short)(2 * tid);
-        if (k2 >= 0) ss->idx[s2 + rk2] = (unsigned short)(2 * tid + 1);
         if (tid == 0) {
           int b0 = 0, rounds = 0;
 #pragma unroll
