@@ -1803,13 +1803,22 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
       }
       asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTW) : "memory");   // sorted order published
       for (int e = tid; e < kSortClasses * 32; e += NTW) ss->cnt[e] = 0;   // every warp has read them
-      const int nrounds = ss->cls_round[kSortClasses];
+      // class layout in registers (the round -> class search is per round)
+      int cr[kSortClasses + 1];
+#pragma unroll
+      for (int c = 0; c <= kSortClasses; ++c) cr[c] = ss->cls_round[c];
+      const int nrounds = cr[kSortClasses];
       for (int rr = warp; rr < nrounds; rr += NWW) {
         int c = 0;
-        while (rr >= ss->cls_round[c + 1]) ++c;
-        const int R = ss->cls_round[c + 1] - ss->cls_round[c];
+#pragma unroll
+        for (int t = 1; t < kSortClasses; ++t) c += rr >= cr[t];
+        int c0 = cr[0], c1 = cr[1];
+#pragma unroll
+        for (int t = 1; t < kSortClasses; ++t)
+          if (c == t) { c0 = cr[t]; c1 = cr[t + 1]; }
+        const int R = c1 - c0;
         const int cs = ss->cls_start[c];
-        const int k = (rr - ss->cls_round[c]) + lane * R;
+        const int k = (rr - c0) + lane * R;
         if (k < ss->cls_start[c + 1] - cs) {
           const SplatRec r = ss->rec[ss->idx[cs + k]];
           switch (c) {   // warp-uniform
