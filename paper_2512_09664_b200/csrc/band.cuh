@@ -1842,7 +1842,7 @@ __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandS
 
 // Workers: particles of the staged item `buf`, then the fused epilogue; two
 // block barriers (the staging warp meets them).
-template <int PSF>
+template <int PSF, int SORT>
 __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh, SortShared* ss, int buf,
                                             int* acc0, int* acc1) {
   const ItemCfg& ic = sh->ic[buf];
@@ -1854,7 +1854,9 @@ __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh,
     band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1);
   } else {
     switch (ic.var) {
-      case kVarSorted: band_particles_sorted<PSF>(P, sh, ss, buf, item, acc0); break;
+      case kVarSorted:
+        if constexpr (SORT != 0) band_particles_sorted<PSF>(P, sh, ss, buf, item, acc0);
+        break;
 #define PGB_V(S, W) case 16 * S + W: band_particles<PSF, S, W>(P, sh, buf, item, acc0, acc1); break;
       PGB_V(1, 1) PGB_V(1, 2) PGB_V(1, 3) PGB_V(1, 4) PGB_V(1, 5) PGB_V(1, 6)
 #undef PGB_V
@@ -1868,7 +1870,10 @@ __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh,
   __syncthreads();   // accumulators zeroed
 }
 
-template <int PSF>
+// SORT = 1: the instantiation for plans with a record region (large windows);
+// a separate kernel so the sorted splat's registers do not weigh on the
+// small-window particle loop.
+template <int PSF, int SORT = 0>
 __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
@@ -1936,7 +1941,7 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
       __syncthreads();   // store done
       continue;
     }
-    render_item<PSF>(P, sh, ss, buf, acc0, acc1);
+    render_item<PSF, SORT>(P, sh, ss, buf, acc0, acc1);
   }
   PGB_STAMP(12);
 #ifdef PGB_TRACE
