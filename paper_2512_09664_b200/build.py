@@ -52,7 +52,7 @@ def check_band_kernel_frame(ptxas_log: str, limit: int = 256) -> None:
 
     cur = None
     for line in ptxas_log.splitlines():
-        m = re.search(r"Function properties for (_ZN3pgb1\d?band_kernel\S*)", line)
+        m = re.search(r"Function properties for (_ZN3pgb1\d?band_(?:sorted_)?kernel\S*)", line)
         if m:
             cur = m.group(1)
             continue

@@ -1870,11 +1870,11 @@ __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh,
   __syncthreads();   // accumulators zeroed
 }
 
-// SORT = 1: the instantiation for plans with a record region (large windows);
-// a separate kernel so the sorted splat's registers do not weigh on the
+// SORT = 1: the body for plans with a record region (large windows), in a
+// separate kernel so the sorted splat's registers do not weigh on the
 // small-window particle loop.
-template <int PSF, int SORT = 0>
-__global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
+template <int PSF, int SORT>
+__device__ __forceinline__ void band_body(const BandParams& P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BandShared* sh = reinterpret_cast<BandShared*>(smem_raw);
   SortShared* ss = reinterpret_cast<SortShared*>(smem_raw + sizeof(BandShared));   // when rec_bytes > 0
@@ -1949,6 +1949,18 @@ __global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
 #endif
 }
 
+
+template <int PSF>
+__global__ void PGB_BAND_BOUNDS band_kernel(const BandParams P) {
+  band_body<PSF, 0>(P);
+}
+
+// Large windows (a separate kernel: its chunk state costs registers, 96 with
+// a few spills at 2 CTAs x 9 warps per SM -- five warps of one SM sub-
+// partition share 16 K registers, so 104 would drop it to one CTA per SM).
+__global__ void PGB_BAND_BOUNDS band_sorted_kernel(const BandParams P) {
+  band_body<kPsfPoint, 1>(P);
+}
 
 // Particle arrays of the generator (one block per pair): exactly the particles
 // the band kernel renders (positions = anchor + fraction).

@@ -118,7 +118,6 @@ __global__ void hiding_kernel(int n, uint32_t k0, uint32_t k1, uint32_t gpair, u
 
 template __global__ void inject_render_kernel<kPsfPoint>(const FusedParams);
 template __global__ void band_kernel<kPsfPoint>(const BandParams);
-template __global__ void band_kernel<kPsfPoint, 1>(const BandParams);
 template __global__ void band_kernel<kPsfErf>(const BandParams);
 template __global__ void inject_render_kernel<kPsfErf>(const FusedParams);
 
@@ -499,7 +498,7 @@ size_t band_acc_budget() {
   if (it != cache.end()) return it->second;
   const bool ok = cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess &&
                   cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) == cudaSuccess &&
-                  cudaFuncGetAttributes(&fa, (const void*)band_kernel<kPsfPoint, 1>) == cudaSuccess &&
+                  cudaFuncGetAttributes(&fa, (const void*)band_sorted_kernel) == cudaSuccess &&
                   cudaFuncGetAttributes(&fe, (const void*)band_kernel<kPsfErf>) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
@@ -762,7 +761,7 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.out[1] = img2;
   P.pro_smem = (int)(bp.smem - sizeof(BandShared));
   BandFn fn = cfg->psf == PGB_PSF_ERF ? band_kernel<kPsfErf>
-             : bp.rec_bytes ? band_kernel<kPsfPoint, 1> : band_kernel<kPsfPoint>;
+             : bp.rec_bytes ? band_sorted_kernel : band_kernel<kPsfPoint>;
   const int ctas = band_resident_ctas(fn, bp.smem);
   // whole rounds of (pair, tile) items over the resident CTAs, then the
   // remaining tiles split into row parts (>= 8 rows) spread over the grid
