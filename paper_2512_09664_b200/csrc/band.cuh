@@ -110,7 +110,14 @@ struct BandParams {
   PairHdr* hdr;                // [pairs]
   int* pair_ready;             // [pairs] prologue done (in-kernel prologue), else null
   int* fb_done;                // [num_fields] finished bound chunks, else null
-  long long npro;              // prologue tickets (flow-bound chunks, then pairs) ahead of the band items
+  long long npro;              // prologue tickets ahead of the band items: flow-bound chunks, histogram
+                               // parts (pro_parts > 1), pair prologues, particle -> cell windows (fill_wins)
+  int pro_parts;               // histogram parts per pair on other CTAs (1: the prologue draws all labels)
+  int* part_counts;            // [pairs][pro_parts][2^(sy+sx)] partial cell histograms (pro_parts > 1)
+  int* part_done;              // [pairs] finished histogram parts
+  int fill_win, fill_wins;     // particle -> cell windows per pair on other CTAs (0: the prologue fills)
+  int* pre_ready;              // [pairs] header + prefix published (fill windows wait on it)
+  int* fill_done;              // [pairs] finished particle -> cell windows
   int4* zero_head;             // the other control head: zeroed here for the next launch (or null)
   int zero_head_n;
   int field_lo, field_cnt;     // flow fields read by this pair range
@@ -362,6 +369,179 @@ __device__ __forceinline__ void pair_max_diameter(const GenCfg& g, const RngKey&
 // Latency-bound (one pair per CTA at the start of every launch), so the last
 // warp draws the maximum diameter (a serial float64 chain) while the others
 // histogram and scan, synchronised by a named barrier of their own.
+// Cell histogram of labels 4q .. 4q+3 (< M) for Philox calls q in
+// [q_lo, q_hi) (4 labels per call; up to four calls in flight per thread), by
+// the NTS scan threads, with shared-memory atomics into bins.
+template <int NTS>
+__device__ __forceinline__ void hist_labels(const GenCfg& g, const RngKey& key, int M, int L, int* bins,
+                                            int q_lo, int q_hi) {
+  const int tid = threadIdx.x;
+  auto labels = [&](int q) {
+    const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
+    const uint32_t ws[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+  };
+  const int nq = (M + 3) >> 2;   // the last call, q = nq - 1, may hold labels >= M
+  const int q_full = min(q_hi, nq - 1);
+  int q = q_lo + tid;
+  // full groups, unconditional atomics
+  for (; q + 3 * NTS < q_full; q += 4 * NTS) {
+    const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
+    const uint4 b = philox_rk(make_uint4((uint32_t)(q + NTS), key.pair, key.batch, kTagCell), g.rk);
+    const uint4 c = philox_rk(make_uint4((uint32_t)(q + 2 * NTS), key.pair, key.batch, kTagCell), g.rk);
+    const uint4 d = philox_rk(make_uint4((uint32_t)(q + 3 * NTS), key.pair, key.batch, kTagCell), g.rk);
+    const uint32_t ws[16] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+  }
+  for (; q < q_hi; q += NTS) labels(q);
+}
+
+// Particle -> cell (counting-sort order: particles of cell c are
+// pre[c] .. pre[c+1]-1) for slots [s_lo, s_hi) in windows of `win` slots
+// staged in shared memory behind the prefix (bins); the NTS scan threads.
+// one_win: the slots were zeroed and the run starts marked during the prefix
+// pass (the whole pair in one window).
+template <int NTS>
+__device__ __forceinline__ void fill_slots(const int* bins, int ncell, int M, int s_lo, int s_hi, int win,
+                                           bool one_win, unsigned short* scof, unsigned short* cof) {
+  constexpr int NS = NTS / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int4* s4 = reinterpret_cast<int4*>(scof);
+  const int M8 = s_hi;
+  // particle -> cell (counting-sort order: particles of cell c are
+  // pre[c] .. pre[c+1]-1), per window of slots: mark the first slot of every
+  // cell starting in the window with the cell id, inclusive max-scan (carry
+  // in: the cell holding the window's first slot), 16-byte stores
+  __shared__ int wcar[128];                     // per-chunk carries of one window
+  auto max8 = [](const int4 w) {
+    const int a = max(max(w.x & 0xffff, (int)((unsigned)w.x >> 16)), max(w.y & 0xffff, (int)((unsigned)w.y >> 16)));
+    const int b = max(max(w.z & 0xffff, (int)((unsigned)w.z >> 16)), max(w.w & 0xffff, (int)((unsigned)w.w >> 16)));
+    return max(a, b);
+  };
+  // dense cells (>= 2 particles per cell on average, e.g. C3's 6.4): every
+  // cell writes its run into the window directly (no scans); sparse cells
+  // (C2's 0.5) mark run starts and max-scan
+  const bool dense = !one_win && M >= 2 * ncell;
+  for (int s0 = s_lo; s0 < M8; s0 += win) {
+    const int s1 = min(M8, s0 + win);
+    const int n4 = (s1 - s0) >> 3;               // int4 groups of 8 slots
+    if (!one_win && !dense)
+      for (int q = tid; q < n4; q += NTS) s4[q] = make_int4(0, 0, 0, 0);
+    // the cell holding slot s0: last c with bins[c] <= s0 (and a non-empty run)
+    int clo = 0;
+    if (s0 > 0) {
+      int lo = 0, hi = ncell - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (bins[mid] <= s0) lo = mid;
+        else hi = mid - 1;
+      }
+      clo = lo;   // bins is non-decreasing and bins[ncell] = M > s0: cell clo holds slot s0
+    }
+    if (dense) {
+      int chi = ncell - 1;   // last cell with a slot in the window
+      if (s1 < M) {
+        int lo = clo, hi = ncell - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (bins[mid] < s1) lo = mid;
+          else hi = mid - 1;
+        }
+        chi = lo;
+      }
+      for (int cb = clo + warp * 32; cb <= chi; cb += NTS) {   // warp-uniform trip count
+        const int c = cb + lane;
+        int j0 = 0, n = 0;
+        if (c <= chi) {
+          j0 = max(bins[c], s0);
+          n = min(bins[c + 1], s1) - j0;
+        }
+        const int nmax = __reduce_max_sync(~0u, n);
+        for (int k = 0; k < nmax; ++k)
+          if (k < n) scof[j0 + k - s0] = (unsigned short)c;
+      }
+      if (tid < 8 && M + tid < s1) scof[M + tid - s0] = 0;   // padding slots of the last window
+      scan_sync<NTS>();
+      const int4* src = reinterpret_cast<const int4*>(scof);
+      int4* dst = reinterpret_cast<int4*>(cof + s0);
+      for (int q = tid; q < n4; q += NTS) dst[q] = src[q];
+      if (s1 < M8) scan_sync<NTS>();
+      continue;
+    }
+    if (!one_win) {
+      // cells starting inside the window: (clo, chi], chi = last c with bins[c] < s1
+      int chi = ncell - 1;
+      if (s1 < M) {
+        int lo = clo, hi = ncell - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (bins[mid] < s1) lo = mid;
+          else hi = mid - 1;
+        }
+        chi = lo;
+      }
+      scan_sync<NTS>();
+#pragma unroll 4
+      for (int c = clo + tid; c <= chi; c += NTS) {
+        const int b = bins[c];
+        if (b >= s0 && b < bins[c + 1]) scof[b - s0] = (unsigned short)c;
+      }
+      scan_sync<NTS>();
+    }
+    // chunk maxima (256 slots = one warp layer of int4s per chunk)
+    const int nch = (n4 + 31) >> 5;
+    for (int ch = warp; ch < nch; ch += NS) {
+      const int q = (ch << 5) + lane;
+      int mx = q < n4 ? max8(s4[q]) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(~0u, mx, o));
+      if (lane == 0) wcar[ch] = mx;
+    }
+    scan_sync<NTS>();
+    if (warp == 0) {
+      int carry = clo;
+      for (int c0 = 0; c0 < nch; c0 += 32) {
+        const int c = c0 + lane;
+        int m = c < nch ? wcar[c] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(~0u, m, o);
+          if (lane >= o) m = max(m, y);
+        }
+        const int up = __shfl_up_sync(~0u, m, 1);
+        const int ex = max(carry, lane ? up : 0);
+        if (c < nch) wcar[c] = ex;
+        carry = max(carry, __shfl_sync(~0u, m, 31));
+      }
+    }
+    scan_sync<NTS>();
+    int4* c4 = reinterpret_cast<int4*>(cof + s0);
+    for (int ch = warp; ch < nch; ch += NS) {
+      const int q = (ch << 5) + lane;
+      int4 w4 = make_int4(0, 0, 0, 0);
+      if (q < n4) w4 = s4[q];
+      int m = max8(w4);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(~0u, m, o);
+        if (lane >= o) m = max(m, y);
+      }
+      const int prev = __shfl_up_sync(~0u, m, 1);
+      int r = lane > 0 ? max(wcar[ch], prev) : wcar[ch];
+      int lo, hi, o0, o1, o2, o3;
+      lo = r = max(r, w4.x & 0xffff); hi = r = max(r, (int)((unsigned)w4.x >> 16)); o0 = lo | (hi << 16);
+      lo = r = max(r, w4.y & 0xffff); hi = r = max(r, (int)((unsigned)w4.y >> 16)); o1 = lo | (hi << 16);
+      lo = r = max(r, w4.z & 0xffff); hi = r = max(r, (int)((unsigned)w4.z >> 16)); o2 = lo | (hi << 16);
+      lo = r = max(r, w4.w & 0xffff); hi = r = max(r, (int)((unsigned)w4.w >> 16)); o3 = lo | (hi << 16);
+      if (q < n4) c4[q] = make_int4(o0, o1, o2, o3);
+    }
+    if (s1 < M8) scan_sync<NTS>();
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* bins, int smem_bytes) {
   constexpr int NW = NT / 32;
@@ -413,29 +593,26 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     if (one_win)
       for (int q = tid; q < (M8 >> 3); q += NTS) s4[q] = make_int4(0, 0, 0, 0);
     scan_sync<NTS>();
-    // cell histogram of M iid labels (4 labels per Philox call; up to four
-    // calls in flight per thread when M is large)
-    const int nq = (M + 3) >> 2;
-    auto labels = [&](int q) {
-      const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
-      const uint32_t ws[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
-    };
-    int q = tid;
-    // full groups (the last call, q = nq - 1, may hold labels >= M: left to
-    // the checked tail loop), unconditional atomics
-    for (; q + 3 * NTS < nq - 1; q += 4 * NTS) {
-      const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
-      const uint4 b = philox_rk(make_uint4((uint32_t)(q + NTS), key.pair, key.batch, kTagCell), g.rk);
-      const uint4 c = philox_rk(make_uint4((uint32_t)(q + 2 * NTS), key.pair, key.batch, kTagCell), g.rk);
-      const uint4 d = philox_rk(make_uint4((uint32_t)(q + 3 * NTS), key.pair, key.batch, kTagCell), g.rk);
-      const uint32_t ws[16] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
-#pragma unroll
-      for (int k = 0; k < 16; ++k) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
+    if (P.pro_parts > 1) {
+      // the histogram was drawn in parts by other CTAs (earlier tickets): sum them
+      if (tid == 0) {
+        int ns = 32;
+        while (ld_acquire_b(P.part_done + pl) < P.pro_parts) { __nanosleep(ns); ns = min(ns * 2, 256); }
+      }
+      scan_sync<NTS>();
+      const int4* pc = reinterpret_cast<const int4*>(P.part_counts + (size_t)pl * P.pro_parts * ncell);
+      for (int i = tid; i < nq4; i += NTS) {
+        int4 t = make_int4(0, 0, 0, 0);
+        for (int k = 0; k < P.pro_parts; ++k) {
+          const int4 v = __ldcg(pc + (size_t)k * (ncell >> 2) + i);
+          t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+        }
+        bins4[i] = t;
+      }
+    } else {
+      hist_labels<NTS>(g, key, M, L, bins, 0, (M + 3) >> 2);
     }
-    for (; q < nq; q += NTS) labels(q);
+
     scan_sync<NTS>();
     PGB_STAMP(3);
     // Cell counts -> exclusive prefix (in place + global) and the maximum cell
@@ -529,135 +706,7 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     }
     scan_sync<NTS>();
     PGB_STAMP(5);
-    // particle -> cell (counting-sort order: particles of cell c are
-    // pre[c] .. pre[c+1]-1), per window of slots: mark the first slot of every
-    // cell starting in the window with the cell id, inclusive max-scan (carry
-    // in: the cell holding the window's first slot), 16-byte stores
-    __shared__ int wcar[128];                     // per-chunk carries of one window
-    auto max8 = [](const int4 w) {
-      const int a = max(max(w.x & 0xffff, (int)((unsigned)w.x >> 16)), max(w.y & 0xffff, (int)((unsigned)w.y >> 16)));
-      const int b = max(max(w.z & 0xffff, (int)((unsigned)w.z >> 16)), max(w.w & 0xffff, (int)((unsigned)w.w >> 16)));
-      return max(a, b);
-    };
-    // dense cells (>= 2 particles per cell on average, e.g. C3's 6.4): every
-    // cell writes its run into the window directly (no scans); sparse cells
-    // (C2's 0.5) mark run starts and max-scan
-    const bool dense = !one_win && M >= 2 * ncell;
-    for (int s0 = 0; s0 < M8; s0 += win) {
-      const int s1 = min(M8, s0 + win);
-      const int n4 = (s1 - s0) >> 3;               // int4 groups of 8 slots
-      if (!one_win && !dense)
-        for (int q = tid; q < n4; q += NTS) s4[q] = make_int4(0, 0, 0, 0);
-      // the cell holding slot s0: last c with bins[c] <= s0 (and a non-empty run)
-      int clo = 0;
-      if (s0 > 0) {
-        int lo = 0, hi = ncell - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (bins[mid] <= s0) lo = mid;
-          else hi = mid - 1;
-        }
-        clo = lo;   // bins is non-decreasing and bins[ncell] = M > s0: cell clo holds slot s0
-      }
-      if (dense) {
-        int chi = ncell - 1;   // last cell with a slot in the window
-        if (s1 < M) {
-          int lo = clo, hi = ncell - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (bins[mid] < s1) lo = mid;
-            else hi = mid - 1;
-          }
-          chi = lo;
-        }
-        for (int cb = clo + warp * 32; cb <= chi; cb += NTS) {   // warp-uniform trip count
-          const int c = cb + lane;
-          int j0 = 0, n = 0;
-          if (c <= chi) {
-            j0 = max(bins[c], s0);
-            n = min(bins[c + 1], s1) - j0;
-          }
-          const int nmax = __reduce_max_sync(~0u, n);
-          for (int k = 0; k < nmax; ++k)
-            if (k < n) scof[j0 + k - s0] = (unsigned short)c;
-        }
-        if (tid < 8 && M + tid < s1) scof[M + tid - s0] = 0;   // padding slots of the last window
-        scan_sync<NTS>();
-        const int4* src = reinterpret_cast<const int4*>(scof);
-        int4* dst = reinterpret_cast<int4*>(cof + s0);
-        for (int q = tid; q < n4; q += NTS) dst[q] = src[q];
-        if (s1 < M8) scan_sync<NTS>();
-        continue;
-      }
-      if (!one_win) {
-        // cells starting inside the window: (clo, chi], chi = last c with bins[c] < s1
-        int chi = ncell - 1;
-        if (s1 < M) {
-          int lo = clo, hi = ncell - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (bins[mid] < s1) lo = mid;
-            else hi = mid - 1;
-          }
-          chi = lo;
-        }
-        scan_sync<NTS>();
-#pragma unroll 4
-        for (int c = clo + tid; c <= chi; c += NTS) {
-          const int b = bins[c];
-          if (b >= s0 && b < bins[c + 1]) scof[b - s0] = (unsigned short)c;
-        }
-        scan_sync<NTS>();
-      }
-      // chunk maxima (256 slots = one warp layer of int4s per chunk)
-      const int nch = (n4 + 31) >> 5;
-      for (int ch = warp; ch < nch; ch += NS) {
-        const int q = (ch << 5) + lane;
-        int mx = q < n4 ? max8(s4[q]) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(~0u, mx, o));
-        if (lane == 0) wcar[ch] = mx;
-      }
-      scan_sync<NTS>();
-      if (warp == 0) {
-        int carry = clo;
-        for (int c0 = 0; c0 < nch; c0 += 32) {
-          const int c = c0 + lane;
-          int m = c < nch ? wcar[c] : 0;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(~0u, m, o);
-            if (lane >= o) m = max(m, y);
-          }
-          const int up = __shfl_up_sync(~0u, m, 1);
-          const int ex = max(carry, lane ? up : 0);
-          if (c < nch) wcar[c] = ex;
-          carry = max(carry, __shfl_sync(~0u, m, 31));
-        }
-      }
-      scan_sync<NTS>();
-      int4* c4 = reinterpret_cast<int4*>(cof + s0);
-      for (int ch = warp; ch < nch; ch += NS) {
-        const int q = (ch << 5) + lane;
-        int4 w4 = make_int4(0, 0, 0, 0);
-        if (q < n4) w4 = s4[q];
-        int m = max8(w4);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(~0u, m, o);
-          if (lane >= o) m = max(m, y);
-        }
-        const int prev = __shfl_up_sync(~0u, m, 1);
-        int r = lane > 0 ? max(wcar[ch], prev) : wcar[ch];
-        int lo, hi, o0, o1, o2, o3;
-        lo = r = max(r, w4.x & 0xffff); hi = r = max(r, (int)((unsigned)w4.x >> 16)); o0 = lo | (hi << 16);
-        lo = r = max(r, w4.y & 0xffff); hi = r = max(r, (int)((unsigned)w4.y >> 16)); o1 = lo | (hi << 16);
-        lo = r = max(r, w4.z & 0xffff); hi = r = max(r, (int)((unsigned)w4.z >> 16)); o2 = lo | (hi << 16);
-        lo = r = max(r, w4.w & 0xffff); hi = r = max(r, (int)((unsigned)w4.w >> 16)); o3 = lo | (hi << 16);
-        if (q < n4) c4[q] = make_int4(o0, o1, o2, o3);
-      }
-      if (s1 < M8) scan_sync<NTS>();
-    }
+    if (P.fill_wins == 0) fill_slots<NTS>(bins, ncell, M, 0, M8, win, one_win, scof, cof);
   }
   __syncthreads();   // the maximum-diameter warp joins
   PGB_STAMP(6);
@@ -670,9 +719,77 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
   __syncthreads();
   if (tid == 0 && P.pair_ready) {
     __threadfence();
-    st_release(P.pair_ready + pl, 1);
+    // particle -> cell windows on other CTAs: they release the pair
+    st_release(P.fill_wins ? P.pre_ready + pl : P.pair_ready + pl, 1);
   }
   PGB_STAMP(7);
+}
+
+// Histogram part k of pair pl (pro_parts > 1; whole block, the scan warps
+// draw): labels of Philox calls [k nq / K, (k+1) nq / K) into shared memory,
+// then to part_counts; part_done[pl] counts the finished parts.
+template <int NT>
+__device__ __forceinline__ void pair_hist_part(const BandParams& P, int pl, int k, int* bins) {
+  constexpr int NTS = (NT / 32 - 1) * 32;
+  const int tid = threadIdx.x;
+  const int L = P.sy + P.sx, ncell = 1 << L;
+  const RngKey key = band_key(P, pl);
+  const GenCfg& g = P.g;
+  const uint4 w0 = philox_rk(make_uint4(0u, key.pair, key.batch, kTagPair), g.rk);
+  const double ppp = lerp_exact(g.ppp_lo, g.ppp_hi, u53_to_unit(w0.x, w0.y));
+  double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
+  mm = fmin(fmax(mm, 0.0), (double)P.n);
+  const int M = (int)mm;
+  const int nq = (M + 3) >> 2;
+  const int K = P.pro_parts;
+  int4* bins4 = reinterpret_cast<int4*>(bins);
+  for (int i = tid; i < (ncell >> 2); i += NT) bins4[i] = make_int4(0, 0, 0, 0);
+  __syncthreads();
+  if (tid < NTS) hist_labels<NTS>(g, key, M, L, bins, (int)((long long)nq * k / K), (int)((long long)nq * (k + 1) / K));
+  __syncthreads();
+  int4* dst = reinterpret_cast<int4*>(P.part_counts + ((size_t)pl * K + k) * ncell);
+  for (int i = tid; i < (ncell >> 2); i += NT) dst[i] = bins4[i];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(P.part_done + pl, 1);
+  }
+}
+
+// Particle -> cell window w of pair pl (fill_wins > 0; whole block, the scan
+// warps fill): waits for the pair's prefix, stages it in shared memory, fills
+// the window; the last window of the pair releases it.
+template <int NT>
+__device__ __forceinline__ void pair_fill_window(const BandParams& P, int pl, int w, int* bins) {
+  constexpr int NTS = (NT / 32 - 1) * 32;
+  __shared__ int sM;
+  const int tid = threadIdx.x;
+  const int L = P.sy + P.sx, ncell = 1 << L, nc4 = ncell < 4 ? 4 : ncell;
+  if (tid == 0) {
+    int ns = 32;
+    while (ld_acquire_b(P.pre_ready + pl) == 0) { __nanosleep(ns); ns = min(ns * 2, 256); }
+    sM = __ldcg(&P.hdr[pl].M);
+  }
+  __syncthreads();
+  const int M = sM, M8 = (M + 7) & ~7;
+  const int s0 = w * P.fill_win, s1 = min(M8, s0 + P.fill_win);
+  if (s0 < s1) {
+    const int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
+    for (int i = tid; i <= ncell; i += NT) bins[i] = __ldcg(pre + i);
+    __syncthreads();
+    const int soff = ((nc4 + 4) & ~3) * 4;
+    unsigned short* scof = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(bins) + soff);
+    unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
+    if (tid < NTS) fill_slots<NTS>(bins, ncell, M, s0, s1, P.fill_win, false, scof, cof);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(P.fill_done + pl, 1) == P.fill_wins - 1) {
+      __threadfence();
+      st_release(P.pair_ready + pl, 1);
+    }
+  }
 }
 
 // Standalone prologue (sample_particles path): one CTA per pair + kFieldBlocks
@@ -1897,11 +2014,12 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)
     for (int e = tid; e < P.zero_head_n; e += kBandBlock) P.zero_head[e] = make_int4(0, 0, 0, 0);
   // One ticket sequence: [0, npro) prologue items (the flow-bound chunks,
-  // then the pairs), then the band items. Band items wait on prologue flags
-  // only, and every prologue ticket precedes every band ticket, so each wait
-  // targets work already taken by a running CTA that waits on nothing:
-  // forward progress without co-residency (MPS limits, green contexts, a
-  // concurrent kernel holding SMs, any grid size).
+  // histogram parts, pair prologues, particle -> cell windows), then the band
+  // items. Every ticket waits only on earlier tickets (a prologue on its
+  // histogram parts, a window on its pair's prefix, band items on pair and
+  // field flags), each taken by a running CTA: forward progress without
+  // co-residency (MPS limits, green contexts, a concurrent kernel holding SMs,
+  // any grid size).
   const int nfc = P.field_cnt * kFieldBlocks;
   long long first;
   for (;;) {
@@ -1910,12 +2028,18 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
     first = sh->ticket0;
     __syncthreads();
     if (first >= P.npro) break;
-    const int w = (int)first;
+    int w = (int)first;
+    const int nparts = P.pro_parts > 1 ? P.pairs * P.pro_parts : 0;
     if (w < nfc) {
       field_bound_chunk<kBandBlock>(P, P.field_lo + w / kFieldBlocks, w % kFieldBlocks);
       PGB_STAMP(1);
+    } else if ((w -= nfc) < nparts) {
+      pair_hist_part<kBandBlock>(P, w / P.pro_parts, w % P.pro_parts, bins);
+    } else if ((w -= nparts) < P.pairs) {
+      pair_prologue<kBandBlock>(P, w, bins, acc_bytes);
     } else {
-      pair_prologue<kBandBlock>(P, w - nfc, bins, acc_bytes);
+      w -= P.pairs;
+      pair_fill_window<kBandBlock>(P, w / P.fill_wins, w % P.fill_wins, bins);
     }
     __syncthreads();
   }

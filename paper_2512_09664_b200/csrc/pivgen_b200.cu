@@ -646,7 +646,25 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   const int ncell = 1 << (bp.sy + bp.sx);
   const size_t hdr_bytes = (size_t)pairs * sizeof(PairHdr);
   const size_t fb_bytes = (size_t)num_fields * sizeof(float2);
-  const size_t flag_bytes = ((size_t)pairs + num_fields) * sizeof(int);
+  const size_t flag_bytes = ((size_t)4 * pairs + num_fields) * sizeof(int);   // ready, fb_done, part/pre/fill
+  // Large pairs split their prologue over several CTAs (the tickets ahead of
+  // the band items): histogram parts (>= 4096 Philox calls each, <= 4 per
+  // pair) and particle -> cell windows (the shared-memory window of the band
+  // kernel's prologue scratch). One window / one part: the prologue does it all.
+  int parts = 1, fill_win = 0, fill_wins = 0;
+  if (!standalone) {
+    const long long nq = ((long long)cfg->n_capacity + 3) / 4;
+    parts = (int)std::max<long long>(1, std::min<long long>(4, nq / 4096));
+    const long long soff = ((long long)((std::max(ncell, 4) + 4) & ~3)) * 4;
+    const long long pro_smem = (long long)bp.smem - (long long)sizeof(BandShared);
+    const long long win = std::max<long long>(8, std::min<long long>(128 * 256, ((pro_smem - soff) / 2) & ~7LL));
+    const long long m8 = ((long long)cfg->n_capacity + 7) & ~7LL;
+    if (m8 > win) {
+      fill_win = (int)win;
+      fill_wins = (int)((m8 + win - 1) / win);
+    }
+  }
+  const size_t part_bytes = parts > 1 ? (size_t)pairs * parts * ncell * sizeof(int) : 0;
   const size_t pre_bytes = (size_t)pairs * pre_stride(ncell) * sizeof(int);
   const size_t cof_bytes = (size_t)pairs * cof_stride(cfg->n_capacity) * sizeof(unsigned short);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
@@ -654,7 +672,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   // [ticket | field bounds | ready flags] are zeroed per launch (two heads),
   // then the pair tables [headers | prefixes | particle -> cell arrays]
   const size_t head = up(256 + up(fb_bytes) + up(flag_bytes));
-  const size_t table_bytes = up(hdr_bytes) + up(pre_bytes) + up(cof_bytes);
+  const size_t table_bytes = up(hdr_bytes) + up(pre_bytes) + up(cof_bytes) + up(part_bytes);
   char* base = static_cast<char*>(ensure(w.band, w.band_bytes, 2 * head + table_bytes, &w.band_gen));
   if (w.head_gen != w.band_gen || head != w.head_bytes) {
     // new allocation (even at the same address) or a different head layout:
@@ -667,6 +685,10 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   P.hdr = reinterpret_cast<PairHdr*>(tables);
   P.prefix = reinterpret_cast<int*>(tables + up(hdr_bytes));
   P.cell_of = reinterpret_cast<unsigned short*>(tables + up(hdr_bytes) + up(pre_bytes));
+  P.part_counts = parts > 1 ? reinterpret_cast<int*>(tables + up(hdr_bytes) + up(pre_bytes) + up(cof_bytes)) : nullptr;
+  P.pro_parts = parts;
+  P.fill_win = fill_win;
+  P.fill_wins = fill_wins;
   // bounds only for the fields this pair range reads
   const int f_lo = (int)(pair_base / pairs_per_field);
   const int f_hi = (int)((pair_base + pairs - 1) / pairs_per_field);
@@ -686,7 +708,11 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
     int* flags = reinterpret_cast<int*>(b + 256 + up(fb_bytes));
     P.pair_ready = flags;
     P.fb_done = flags + pairs;
-    P.npro = (long long)pairs + (long long)P.field_cnt * kFieldBlocks;
+    P.part_done = flags + pairs + num_fields;
+    P.pre_ready = P.part_done + pairs;
+    P.fill_done = P.pre_ready + pairs;
+    P.npro = (long long)P.field_cnt * kFieldBlocks + (parts > 1 ? (long long)pairs * parts : 0) +
+             (long long)pairs + (long long)pairs * fill_wins;
     return;
   }
   // standalone prologue kernel: head 0, no readiness flags
