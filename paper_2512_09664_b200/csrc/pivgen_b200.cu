@@ -811,9 +811,9 @@ void generate_dev_impl(const pgb_config* cfg, uint64_t batch, int64_t pair_base,
   P.total_items = P.split_base + rem * sp;
   if (std::getenv("PGB_VERBOSE"))
     std::fprintf(stderr, "pgb band plan: %dx%d tiles of %dx%d (AS %d, pad %d), cells 2^%d x 2^%d, smem %zu "
-                 "(records %d), grid %lld, items %lld (split %d)\n",
+                 "(records %d), grid %lld, items %lld (split %d), prologue parts %d, cell windows %d\n",
                  bp.tiles_y, bp.tiles_x, bp.TH, bp.TW, bp.AS, bp.pad_rows, bp.sy, bp.sx, bp.smem, bp.rec_bytes,
-                 G, P.total_items, sp);
+                 G, P.total_items, sp, P.pro_parts, P.fill_wins);
   fn<<<(int)G, kBandBlock, bp.smem, stream>>>(P);
   g_launches.fetch_add(1);
 }

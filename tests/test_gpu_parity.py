@@ -434,6 +434,46 @@ def test_schedule_and_store_paths_bit_identical(pg, env, sep, hw, monkeypatch):
             np.testing.assert_array_equal(got[f], ref[b][f], err_msg=f"{env} batch {b} frame {f + 1}")
 
 
+@pytest.mark.parametrize("env", [{}, {"PGB_GRID": "1"}, {"PGB_GRID": "5"}, {"PGB_TILE": "64,128"}])
+def test_split_prologue_dense_pairs(pg, env, monkeypatch):
+    """Dense pairs split their prologue over CTAs (histogram parts and
+    particle -> cell windows as their own tickets; 512^2 at ppp <= 0.25: four
+    parts, three windows). Pair 0 matches the oracle render of the oracle
+    particles (whose positions follow the cell histogram and counting-sort
+    order exactly), and every grid / tiling gives the same bits: each ticket
+    waits only on earlier tickets."""
+    import torch
+
+    from paper_2512_09664_b200 import _lib
+    from paper_2512_09664_b200.particles import native_config
+
+    H, W, B = 512, 512, 3
+    cfg = _gen_cfg(pg, image_height=H, image_width=W, batch_size=B, seeding_density_range=(0.2, 0.25),
+                   diameter_range=(1.0, 4.0), rho_range=(0.0, 0.0), frame2_sigma_std=0.0,
+                   frame2_intensity_std=0.0, frame2_rho_std=0.0, hide_probability=0.0)
+    flow = pg.from_function(vortex_fn(H, W), H, W)
+    flows = flow.to_device().unsqueeze(0)
+    stream = torch.cuda.current_stream()
+
+    def run():
+        img = [torch.empty((B, H, W), dtype=torch.float32, device="cuda") for _ in range(2)]
+        _lib.call("pgb_generate_batch_dev", native_config(cfg), 5, 0, B, flows.data_ptr(), 1, B, _lib.OUT_RAW,
+                  img[0].data_ptr(), img[1].data_ptr(), None, None, stream.cuda_stream)
+        return [i.cpu().numpy() for i in img]
+
+    want = run()
+    o = og.sample_pair(_oracle_cfg(cfg), 5, 0, flow.interleaved())
+    for f in (1, 2):
+        ref = orr.splat(o[f"pos{f}"], o[f"i0_{f}"], o[f"sx_{f}"], o[f"sy_{f}"], o[f"rho_{f}"], o[f"on{f}"],
+                        o["side"], H, W)
+        _assert_close(want[f - 1][0], ref, what=f"split prologue frame {f}")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = run()
+    for f in range(2):
+        np.testing.assert_array_equal(got[f], want[f], err_msg=f"{env} frame {f + 1}")
+
+
 def test_match_histogram_kernel_bit_exact(pg):
     """CUDA histogram specification (csrc/histmatch.cuh) vs the reference's own
     outputs (golden) and the oracle: single images, one batched launch over a
