@@ -654,14 +654,16 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   int parts = 1, fill_win = 0, fill_wins = 0;
   if (!standalone) {
     const long long nq = ((long long)cfg->n_capacity + 3) / 4;
-    parts = (int)std::max<long long>(1, std::min<long long>(4, nq / 4096));
+    const long long kparts = std::getenv("PGB_PRO_PARTS") ? std::atoll(std::getenv("PGB_PRO_PARTS")) : 4;
+    parts = (int)std::max<long long>(1, std::min<long long>(kparts, nq / 4096));
     const long long soff = ((long long)((std::max(ncell, 4) + 4) & ~3)) * 4;
     const long long pro_smem = (long long)bp.smem - (long long)sizeof(BandShared);
     const long long win = std::max<long long>(8, std::min<long long>(128 * 256, ((pro_smem - soff) / 2) & ~7LL));
     const long long m8 = ((long long)cfg->n_capacity + 7) & ~7LL;
     if (m8 > win) {
-      fill_win = (int)win;
-      fill_wins = (int)((m8 + win - 1) / win);
+      const long long cap = std::getenv("PGB_FILL_WIN") ? std::atoll(std::getenv("PGB_FILL_WIN")) : win;
+      fill_win = (int)std::max<long long>(256, std::min(win, cap) & ~255LL);
+      fill_wins = (int)((m8 + fill_win - 1) / fill_win);
     }
   }
   const size_t part_bytes = parts > 1 ? (size_t)pairs * parts * ncell * sizeof(int) : 0;
