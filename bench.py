@@ -358,7 +358,8 @@ def run_ours(args):
     cfg = make_cfg(pg, name, global_batch)
     lib = _lib.load()
     ncfg = native_config(cfg)
-    kernel_label = "pgb::band_kernel<PSF> (screen-tile items, in-kernel prologue tickets; one launch per batch)"
+    kernel_label = ("pgb::band_sorted_kernel (screen-tile items, bank-sorted splat records)" if name == "c3" else
+                    "pgb::band_kernel<PSF> (screen-tile items, in-kernel prologue tickets; one launch per batch)")
     field = pg.from_function(vortex(H, W) if CONFIGS[name][5] == "vortex" else uniform, H, W)
     flows = field.to_device(dev).unsqueeze(0).contiguous()
     u16 = False

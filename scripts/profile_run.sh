@@ -13,7 +13,7 @@ mkdir -p gpurun_out
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --config $cfg"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${tag}_launches.csv $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:band_kernel -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"band_(sorted_)?kernel" -s 3 -c 1 \
   -o gpurun_out/${tag}_full -f $B > /dev/null 2>&1
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active
 M=$M,sm__inst_executed.sum,sm__inst_executed.avg.per_cycle_active

@@ -14,6 +14,11 @@ import subprocess
 import sys
 
 rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
+
+
+def is_band(name):
+    """The generator kernels: band_kernel<PSF> and band_sorted_kernel (not sample_band_kernel)."""
+    return "band_kernel" in name and "sample_band" not in name or "band_sorted_kernel" in name
 cfgname = sys.argv[4] if len(sys.argv) > 4 else "c2"
 pipes_csv = sys.argv[5] if len(sys.argv) > 5 else None
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -47,8 +52,8 @@ with open(prefix + "_launches.txt", "w") if rows else open(os.devnull, "w") as f
     fh.write(f"# command: python bench.py --steps 5 --warmup 3 --no-cpu-baseline --config {cfgname}\n")
     for r in rows:
         fh.write(f"{r['ID']:>4s}  {r['Kernel Name'][:70]:70s}  {float(r['Metric Value'])/1000:9.2f} us\n")
-    band = [float(r["Metric Value"]) for r in rows if "band_kernel" in r["Kernel Name"]]
-    other = [float(r["Metric Value"]) for r in rows if "band_kernel" not in r["Kernel Name"]]
+    band = [float(r["Metric Value"]) for r in rows if is_band(r["Kernel Name"])]
+    other = [float(r["Metric Value"]) for r in rows if not is_band(r["Kernel Name"])]
     if band:
         fh.write(f"# band_kernel launches: {len(band)}, mean {sum(band)/len(band)/1000:.2f} us; "
                  f"other kernels (bench L2 flush): {len(other)}\n")
@@ -73,7 +78,7 @@ def pipes_section(path, alg_bytes):
     out = ["\n# pipes / shared atomics / DRAM per band-kernel launch (ncu --metrics, scripts/profile_run.sh)\n"]
     flush_bytes = 256 * 1024 * 1024
     for i, L in enumerate(launches):
-        if "band_kernel" not in L["name"]:
+        if not is_band(L["name"]):
             continue
         m = L["m"]
         nxt = launches[i + 1]["m"] if i + 1 < len(launches) else {}
@@ -130,7 +135,7 @@ phases = subprocess.run([sys.executable, os.path.join(root, "scripts", "ncu_line
                          band_ranges()],
                         capture_output=True, text=True).stdout
 with open(prefix + "_band_kernel.txt", "w") as fh:
-    fh.write("# ncu --set full --clock-control none --import-source on -k regex:band_kernel -s 3 -c 1\n")
+    fh.write("# ncu --set full --clock-control none --import-source on -k regex:'band_(sorted_)?kernel' -s 3 -c 1\n")
     fh.write(f"#   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --config {cfgname}\n")
     fh.write(f"duration_us                {dur_ns/1000:.2f}\n")
     fh.write(f"dram_bytes_read            {dram_r:.0f}\n")
@@ -158,7 +163,7 @@ with open(prefix + "_band_kernel.txt", "w") as fh:
 
 tp = os.path.join(root, "profiles", "traffic.json")
 tj = json.load(open(tp)) if os.path.exists(tp) else {}
-tj[cfgname] = {"kernel": "pgb::band_kernel<0>", "dram_bytes_per_launch": dram_r + dram_w,
+tj[cfgname] = {"kernel": "pgb::band_sorted_kernel" if cfgname == "c3" else "pgb::band_kernel<0>", "dram_bytes_per_launch": dram_r + dram_w,
             "dram_read": dram_r, "dram_write": dram_w, "duration_us_ncu": dur_ns / 1000,
             "source": os.path.basename(prefix) + "_band_kernel.txt"}
 json.dump(tj, open(tp, "w"), indent=1)
