@@ -579,7 +579,8 @@ BandPlan make_band_plan(int H, int W, int halo, size_t acc_budget = 0, bool sort
   // (images under 12 rows) keep padding rows
   if (sorted && p.TH < kMaxUnpredWM) p.pad_rows = kMaxUnpredWM - p.TH;
   const size_t acc_bytes = ((size_t)(2 * p.TH + p.pad_rows) * p.AS + 16) * 4;
-  const size_t hist_bytes = ((size_t)(1 << (p.sy + p.sx)) + 8) * 4;
+  // (plus 16 KB: particle -> cell windows of >= 8 k slots)
+  const size_t hist_bytes = ((size_t)(1 << (p.sy + p.sx)) + 8) * 4 + 16384;
   p.smem = sizeof(BandShared) + std::max(p.rec_bytes + acc_bytes, hist_bytes);
   PGB_REQUIRE(p.smem <= kSmemMax, "band plan does not fit in shared memory");
   return p;
@@ -662,7 +663,7 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
     const long long m8 = ((long long)cfg->n_capacity + 7) & ~7LL;
     if (m8 > win) {
       const long long cap = std::getenv("PGB_FILL_WIN") ? std::atoll(std::getenv("PGB_FILL_WIN")) : win;
-      fill_win = (int)std::max<long long>(256, std::min(win, cap) & ~255LL);
+      fill_win = (int)std::max<long long>(8, std::min(win, cap) & ~7LL);   // never above the window space
       fill_wins = (int)((m8 + fill_win - 1) / fill_win);
     }
   }
