@@ -238,3 +238,41 @@ def test_device_evaluated_flow_function(pg):
     for (h1, h2), (d1, d2) in zip(out["h"], out["d"]):
         np.testing.assert_array_equal(h1, d1)            # frame 1 does not depend on the flow
         assert float(np.abs(h2 - d2).max()) <= 1e-5      # float32-rounding differences of the field
+
+
+def test_graph_captured_flow_function(pg):
+    """register_flow_function(..., device=True, graph=True): the evaluation is
+    captured once as a CUDA graph and replayed; every replay gives the eager
+    field bit for bit, a Sampler over it gives the eager Sampler's images, and
+    a function that cannot be captured (a host sync inside) falls back to
+    eager evaluation."""
+    import torch
+
+    H, W, B = 96, 128, 4
+
+    def dev_fn(x, y):
+        return 0.5 + 0.01 * torch.sin(0.05 * x) * y, -0.25 + 0.002 * x
+
+    eager = pg.from_function_device(dev_fn, H, W)
+    for _ in range(3):
+        g = pg.from_function_device(dev_fn, H, W, graph=True)
+        np.testing.assert_array_equal(g.u, eager.u)
+        np.testing.assert_array_equal(g.v, eager.v)
+
+    def syncing_fn(x, y):
+        s = float(x.max().item())          # a host sync: not capturable
+        return 0.0 * x + 1.0 / s, 0.0 * y
+
+    a = pg.from_function_device(syncing_fn, H, W, graph=True)
+    np.testing.assert_allclose(a.u, 1.0 / (W - 1), rtol=1e-6)
+    out = {}
+    for name, graph in (("e", False), ("g", True)):
+        pg.register_flow_function("gflow_" + name, dev_fn, device=True, graph=graph)
+        cfg = pg.GeneratorConfig(image_height=H, image_width=W, batch_size=B, seed=6,
+                                 flow_sources=(pg.FlowSource(function="gflow_" + name),))
+        with pg.make_sampler(cfg, max_batches=3) as s:
+            out[name] = [(b.images1.cpu().numpy(), b.images2.cpu().numpy()) for b in s]
+        pg.unregister_flow_function("gflow_" + name)
+    for (e1, e2), (g1, g2) in zip(out["e"], out["g"]):
+        np.testing.assert_array_equal(e1, g1)
+        np.testing.assert_array_equal(e2, g2)
