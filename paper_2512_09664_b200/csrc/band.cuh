@@ -829,6 +829,7 @@ enum { kItemBand = 0, kItemEnd = 2 };
 struct __align__(16) BandShared {
   int wsum[kBandWarps];
   long long ticket0;                 // prologue / first band ticket of this CTA
+  long long ticket_next;             // the following ticket, taken while a prologue item runs
 
   int nseg[kStageSlots];             // segments of the staged pass
   int rows_left[kStageSlots];        // cell rows not yet staged (rare multi-pass items)
@@ -2022,12 +2023,15 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
   // any grid size).
   const int nfc = P.field_cnt * kFieldBlocks;
   long long first;
+  if (tid == 0) sh->ticket0 = atomicAdd(P.ticket, 1);
+  __syncthreads();
+  first = sh->ticket0;
   for (;;) {
-    if (tid == 0) sh->ticket0 = atomicAdd(P.ticket, 1);
-    __syncthreads();
-    first = sh->ticket0;
-    __syncthreads();
     if (first >= P.npro) break;
+    // take the following ticket now (its atomic round trip overlaps this item;
+    // it is later than `first`, and every item waits only on earlier tickets,
+    // so the smallest unfinished ticket is always some CTA's current item)
+    if (tid == 0) sh->ticket_next = atomicAdd(P.ticket, 1);
     int w = (int)first;
     const int nparts = P.pro_parts > 1 ? P.pairs * P.pro_parts : 0;
     if (w < nfc) {
@@ -2041,6 +2045,8 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
       w -= P.pairs;
       pair_fill_window<kBandBlock>(P, w / P.fill_wins, w % P.fill_wins, bins);
     }
+    __syncthreads();
+    first = sh->ticket_next;
     __syncthreads();
   }
   zero_acc();
