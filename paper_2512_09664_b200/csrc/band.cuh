@@ -967,50 +967,10 @@ __device__ __forceinline__ void splat_erf(int* __restrict__ acc, int AS, int ax,
   }
 }
 
-// Uncorrelated point PSF (rho == 0): value * 2^s = X_j * Y_i with
-// X_j = exp2(Ls - A dx_j^2), Y_i = exp2(-C dy_i^2): 2 WM exponentials per
-// particle-frame, one multiply per pixel.
-template <int WM>
-__device__ __forceinline__ void splat_point_sep(int* __restrict__ acc, int AS, int ax, int ay,
-                                                float fx, float fy, float amp, float sx, float sy, int h,
-                                                int r0, int r1, int c0, int c1, int shift) {
-  const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
-  int rlo, clo, nr, nc;
-  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return;
-  nr = min(nr, WM);
-  nc = min(nc, WM);
-  const float dx0 = (float)(clo - ax) - fx;
-  const float dy0 = (float)(rlo - ay) - fy;
-  int* base = acc + (rlo - r0) * AS + (clo - c0);
-  const float isx = rcp_approx(sx), isy = rcp_approx(sy);
-  const float A = (0.5f * kLog2e) * isx * isx;
-  const float C = (0.5f * kLog2e) * isy * isy;
-  const float Ls = lg2_approx(amp) + (float)shift;
-  float X[WM], Y[WM];
-#pragma unroll
-  for (int j = 0; j < WM; ++j) {
-    const float dx = dx0 + (float)j;
-    X[j] = ex2_approx(fmaf(-A * dx, dx, Ls));
-    const float dy = dy0 + (float)j;
-    Y[j] = ex2_approx(-C * dy * dy);
-  }
-#pragma unroll
-  for (int i = 0; i < WM; ++i) {
-    if (i < nr) {
-      int* row = base + i * AS;
-#pragma unroll
-      for (int j = 0; j < WM; ++j)
-        if (j < nc) atomicAdd(row + j, round_small(X[j] * Y[i]));
-    }
-  }
-}
-
-
-// Unpredicated point-PSF windows (WM = compile-time window bound: 1..13
-// separable, 1..7 correlated).
+// Unpredicated separable point-PSF windows (WM = compile-time window bound,
+// 1..kLaneWM; uncorrelated particles, one particle-frame per lane).
 // Every particle-frame adds all WM x WM slots; slots outside its clipped
-// window add exactly 0 (their factor is 0, resp. their exponent -inf), so no
-// per-slot branch is needed. Slots past the tile's last row / column land on
+// window add exactly 0 (their factor is 0), so no per-slot branch is needed. Slots past the tile's last row / column land on
 // the next row or on the zero padding after the frame-2 accumulator
 // (pad_rows >= WM - 1 rows), always with value 0.
 template <int WM>
@@ -1064,44 +1024,8 @@ __device__ __forceinline__ void splat_sep_u(int* __restrict__ acc, int AS, int a
   }
 }
 
-template <int WM>
-__device__ __forceinline__ void splat_point_u(int* __restrict__ acc, int AS, int ax, int ay, float fx,
-                                              float fy, float amp, float sx, float sy, float rho, int h,
-                                              int r0, int r1, int c0, int c1, int shift) {
-  const float R = __fmul_rn(fmaxf(sx, sy), kTightR);
-  int rlo, clo, nr, nc;
-  if (!tile_window(ax, ay, fx, fy, R, h, r0, r1, c0, c1, rlo, clo, nr, nc)) return;
-  const float dx0 = (float)(clo - ax) - fx;
-  const float dy0 = (float)(rlo - ay) - fy;
-  int* base = acc + (rlo - r0) * AS + (clo - c0);
-  const float isx = rcp_approx(sx), isy = rcp_approx(sy);
-  const float iq = rcp_approx(1.0f - rho * rho);
-  const float A = (0.5f * kLog2e) * iq * isx * isx;
-  const float C = (0.5f * kLog2e) * iq * isy * isy;
-  const float B = -kLog2e * rho * iq * isx * isy;
-  const float Ls = lg2_approx(amp) + (float)shift;
-  float ct[WM], bx[WM];
-#pragma unroll
-  for (int j = 0; j < WM; ++j) {
-    const float dx = dx0 + (float)j;
-    const float cv = fmaf(-A * dx, dx, Ls);
-    ct[j] = j < nc ? cv : -INFINITY;
-    bx[j] = B * dx;
-  }
-#pragma unroll
-  for (int i = 0; i < WM; ++i) {
-    const float dy = dy0 + (float)i;
-    const float rv = -C * dy * dy;
-    const float rt = i < nr ? rv : -INFINITY;
-    int* row = base + i * AS;
-#pragma unroll
-    for (int j = 0; j < WM; ++j)
-      atomicAdd(row + j, round_small(ex2_approx(fmaf(-bx[j], dy, ct[j] + rt))));
-  }
-}
-
 // One particle-frame, variant fixed per item: SEP (rho == 0 everywhere),
-// WM (1..7 unpredicated windows; 0 = dynamic loops).
+// WM (1..kLaneWM unpredicated separable windows; 0 = dynamic loops).
 template <int PSF, int SEP, int WM>
 __device__ __forceinline__ void splat_v(int* acc, int AS, int ax, int ay, float fx, float fy, float amp,
                                         float sx, float sy, float rho, int h, int r0, int r1, int c0,
@@ -1110,48 +1034,10 @@ __device__ __forceinline__ void splat_v(int* acc, int AS, int ax, int ay, float 
     splat_erf(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, scale);
   } else if constexpr (WM == 0) {
     splat_point<0>(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, shift);
-  } else if constexpr (SEP != 0) {
-    splat_sep_u<WM>(acc, AS, ax, ay, fx, fy, amp, sx, sy, h, r0, r1, c0, c1, shift);
   } else {
-    splat_point_u<WM>(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, shift);
+    static_assert(SEP != 0, "unpredicated windows are instantiated for uncorrelated particles only");
+    splat_sep_u<WM>(acc, AS, ax, ay, fx, fy, amp, sx, sy, h, r0, r1, c0, c1, shift);
   }
-}
-
-template <int PSF>
-__device__ __forceinline__ void splat_dispatch_b(int wt, int sep, int* acc, int AS, int ax, int ay,
-                                                 float fx, float fy, float amp, float sx, float sy,
-                                                 float rho, int h, int r0, int r1, int c0, int c1,
-                                                 int shift, float scale) {
-  if (PSF == kPsfErf) {
-    splat_erf(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, scale);
-    return;
-  }
-  if (sep) {
-#define PGB_SS(WW) splat_point_sep<WW>(acc, AS, ax, ay, fx, fy, amp, sx, sy, h, r0, r1, c0, c1, shift)
-    switch (wt) {   // warp-uniform (per item)
-      case 1: PGB_SS(1); return;
-      case 2: PGB_SS(2); return;
-      case 3: PGB_SS(3); return;
-      case 4: PGB_SS(4); return;
-      case 5: PGB_SS(5); return;
-      case 6: PGB_SS(6); return;
-      case 7: PGB_SS(7); return;
-      default: break;
-    }
-#undef PGB_SS
-  }
-#define PGB_SP(WW) splat_point<WW>(acc, AS, ax, ay, fx, fy, amp, sx, sy, rho, h, r0, r1, c0, c1, shift)
-  switch (wt) {   // warp-uniform (per item)
-    case 1: PGB_SP(1); return;
-    case 2: PGB_SP(2); return;
-    case 3: PGB_SP(3); return;
-    case 4: PGB_SP(4); return;
-    case 5: PGB_SP(5); return;
-    case 6: PGB_SP(6); return;
-    case 7: PGB_SP(7); return;
-    default: PGB_SP(0); return;
-  }
-#undef PGB_SP
 }
 
 // Epilogue: one output quad (4 pixels) of frame f. (float)a is exact below
