@@ -1676,12 +1676,13 @@ __device__ __forceinline__ void splat_rec(int* __restrict__ acc, int AS, const S
   }
 }
 
-// Worker warps, sorted splat: per chunk of NTW particle slots, (1) regenerate
-// and write records + count keys, (2) warp 0 scans the counts, (3) scatter the
-// sorted order, (4) splat rounds (warp w takes rounds w, w + 8, ...). Workers'
-// named barrier BAR. (Measured against a double-buffered variant that overlaps
-// the generation of chunk k with the splat of chunk k-1: that one needs twice
-// the record space, i.e. shorter tiles, and was slower.)
+// Worker warps, sorted splat: per chunk (kSortPPT particles per worker
+// thread), (1) regenerate and write records + count keys, (2) every warp
+// scans the counts and scatters its records' sorted positions, (3) splat
+// rounds, smallest class first (warp w takes rounds w, w + 8, ...). Three
+// named barriers (BAR) per chunk. (Measured against a double-buffered variant
+// that overlaps the generation of chunk k with the splat of chunk k-1: that
+// one needs twice the record space, i.e. shorter tiles, and was slower.)
 template <int PSF, int NTW = kBandThreads, int BAR = 1>
 __device__ __forceinline__ void band_particles_sorted(const BandParams& P, BandShared* sh, SortShared* ss,
                                                       int buf, long long item, int* acc0) {
