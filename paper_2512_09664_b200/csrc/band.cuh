@@ -424,7 +424,7 @@ __device__ __forceinline__ void fill_slots(const int* bins, int ncell, int M, in
   // dense cells (>= 2 particles per cell on average, e.g. C3's 6.4): every
   // cell writes its run into the window directly (no scans); sparse cells
   // (C2's 0.5) mark run starts and max-scan
-  const bool dense = !one_win && M >= 2 * ncell;
+  const bool dense = M >= 2 * ncell;
   for (int s0 = s_lo; s0 < M8; s0 += win) {
     const int s1 = min(M8, s0 + win);
     const int n4 = (s1 - s0) >> 3;               // int4 groups of 8 slots
@@ -575,7 +575,10 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
   int4* s4 = reinterpret_cast<int4*>(scof);
   const int win = max(8, min(128 * 256, ((smem_bytes - soff) / 2) & ~7));   // slots per window (plans leave >= 8)
   const int M8 = (M + 7) & ~7;
-  const bool one_win = M8 <= win;
+  // one window, sparse cells: run starts marked during the prefix pass, then
+  // a max-scan; dense cells (>= 2 particles per cell: C2's 128 full-width cell
+  // rows hold ~31 each) write their runs directly (fill_slots)
+  const bool one_win = M8 <= win && M < 2 * ncell;
   if (warp == NS) {
     if (lane == 0) {
       PairHdr hd;
