@@ -376,13 +376,6 @@ template <int NTS>
 __device__ __forceinline__ void hist_labels(const GenCfg& g, const RngKey& key, int M, int L, int* bins,
                                             int q_lo, int q_hi) {
   const int tid = threadIdx.x;
-  auto labels = [&](int q) {
-    const uint4 a = philox_rk(make_uint4((uint32_t)q, key.pair, key.batch, kTagCell), g.rk);
-    const uint32_t ws[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (4 * q + k < M) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
-  };
   const int nq = (M + 3) >> 2;   // the last call, q = nq - 1, may hold labels >= M
   const int q_full = min(q_hi, nq - 1);
   int q = q_lo + tid;
@@ -396,7 +389,22 @@ __device__ __forceinline__ void hist_labels(const GenCfg& g, const RngKey& key, 
 #pragma unroll
     for (int k = 0; k < 16; ++k) atomicAdd(&bins[L ? (ws[k] >> (32 - L)) : 0], 1);
   }
-  for (; q < q_hi; q += NTS) labels(q);
+  // the rest (< 4 calls per thread, up to the partial last call): one group,
+  // its calls in flight together, checked atomics
+  if (q < q_hi) {
+    uint4 w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = philox_rk(make_uint4((uint32_t)(q + k * NTS), key.pair, key.batch, kTagCell), g.rk);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int qk = q + k * NTS;
+      const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (qk < q_hi && 4 * qk + e < M) atomicAdd(&bins[L ? (ws[e] >> (32 - L)) : 0], 1);
+    }
+  }
 }
 
 // Particle -> cell (counting-sort order: particles of cell c are
@@ -566,6 +574,7 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
   double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
   mm = fmin(fmax(mm, 0.0), (double)P.n);
   const int M = (int)mm;
+  PGB_STAMP(11);
   int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
   unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
   // particle -> cell slots staged in shared memory behind the prefix, in
@@ -596,6 +605,7 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     if (one_win)
       for (int q = tid; q < (M8 >> 3); q += NTS) s4[q] = make_int4(0, 0, 0, 0);
     scan_sync<NTS>();
+    PGB_STAMP(10);
     if (P.pro_parts > 1) {
       // the histogram was drawn in parts by other CTAs (earlier tickets): sum them
       if (tid == 0) {
@@ -823,6 +833,7 @@ struct ItemCfg {
   int cy0, cy1, cx0, cx1;
   int h, wt, shift, field, sep;
   int var;                 // particle-loop variant: 16 * sep + WM (0 = dynamic windows)
+  float2 fb;               // the field's displacement bound (max |u|, max |v|)
   int kind;                // kItemBand or kItemEnd
   long long item;          // band item index
   PairHdr hd;
@@ -1293,16 +1304,27 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
   ic.c1 = min(ic.c0 + P.TW, g.W);
   ic.field = (int)((P.pair_base + pl) / P.pairs_per_field);
   if (P.pair_ready) {
-    // produced inside this launch by other CTAs (earlier tickets)
+    // produced inside this launch by other CTAs (earlier tickets); both flags
+    // polled together (one L2 round trip when they are already set)
     int ns = 32;
-    while (ld_acquire_b(P.pair_ready + pl) == 0) { __nanosleep(ns); ns = min(ns * 2, 256); }
-    while (ld_acquire_b(P.fb_done + ic.field) < kFieldBlocks) { __nanosleep(ns); ns = min(ns * 2, 256); }
+    for (;;) {
+      const int a = ld_acquire_b(P.pair_ready + pl);
+      const int b = ld_acquire_b(P.fb_done + ic.field);
+      if (a != 0 && b >= kFieldBlocks) break;
+      __nanosleep(ns);
+      ns = min(ns * 2, 256);
+    }
   }
   {
+    // header and field bound loaded together
     const int4* src = reinterpret_cast<const int4*>(P.hdr + pl);
+    int4 t[sizeof(PairHdr) / 16];
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(PairHdr) / 16); ++k) t[k] = __ldcg(src + k);
+    ic.fb = __ldcg(P.fbound + ic.field);
     int4* dst = reinterpret_cast<int4*>(&ic.hd);
 #pragma unroll
-    for (int k = 0; k < (int)(sizeof(PairHdr) / 16); ++k) dst[k] = __ldcg(src + k);
+    for (int k = 0; k < (int)(sizeof(PairHdr) / 16); ++k) dst[k] = t[k];
   }
   item_finish(P, ic);
 }
@@ -1315,7 +1337,7 @@ __device__ __forceinline__ void item_finish(const BandParams& P, ItemCfg& ic) {
   const int CY = 1 << P.sy, CX = 1 << P.sx;
   const int h = ic.hd.side >> 1;
   ic.h = h;
-  const float2 fb = __ldcg(P.fbound + ic.field);
+  const float2 fb = ic.fb;
   // frame-1 positions that can reach the tile in either frame: anchors within
   // h of the tile (frame 1), or within h + 1 + max|v| (frame 2: the anchor
   // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
@@ -1894,12 +1916,12 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
   const int acc_bytes = P.pro_smem;
   int* bins = reinterpret_cast<int*>(ss);
   auto zero_acc = [&]() {
-    // both frame accumulators + the zero padding behind them (the prologue
-    // borrowed them), sorted-splat counts
-    for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 16) / 4; e += kBandBlock)
+    // (workers) both frame accumulators + the zero padding behind them (the
+    // prologue borrowed them), sorted-splat counts
+    for (int e = tid; e < ((2 * P.TH + P.pad_rows) * P.AS + 16) / 4; e += kBandThreads)
       reinterpret_cast<int4*>(acc0)[e] = make_int4(0, 0, 0, 0);
     if (P.rec_bytes)
-      for (int e = tid; e < kSortClasses * 32; e += kBandBlock) ss->cnt[e] = 0;
+      for (int e = tid; e < kSortClasses * 32; e += kBandThreads) ss->cnt[e] = 0;
   };
   PGB_STAMP(0);
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)
@@ -1939,11 +1961,12 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
     first = sh->ticket_next;
     __syncthreads();
   }
-  zero_acc();
   // dynamic schedule: the staging warp takes the ticket of item k+1 and
-  // prepares it (parameters + particle segments) while the workers splat item k
+  // prepares it (parameters + particle segments) while the workers splat item
+  // k; the first item is staged while the workers zero the accumulators
   PGB_STAMP(8);
   if (stager) stage_next(P, sh, 0, first);
+  else zero_acc();
   __syncthreads();
   PGB_STAMP(9);
 #ifdef PGB_TRACE

@@ -23,7 +23,7 @@ from paper_2512_09664_b200.particles import native_config  # noqa: E402
 
 SLOTS = 16
 NAMES = ["entry", "field_chunk_done", "pro_start", "pro_hist", "pro_sums", "pro_prefix", "pro_maxscan",
-         "pro_released", "pro_loop_done", "item1_staged", "owned_staged", "owned_done", "exit", "(items)", "pro_f64_chain",
+         "pro_released", "pro_loop_done", "item1_staged", "pro_zeroed", "pro_M", "exit", "(items)", "pro_f64_chain",
          "owned_fb_ok"]
 
 
