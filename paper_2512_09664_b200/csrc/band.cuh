@@ -35,7 +35,7 @@ namespace pgb {
 // Timing probes (build with -DPGB_TRACE only; scripts/trace.py reads them):
 // globaltimer stamps per CTA, slot = blockIdx.x * kTraceSlots + event.
 #ifdef PGB_TRACE
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 40;   // 0-15 events, 16 + 3k.. item k phases (k < 8)
 __device__ unsigned long long g_trace[2048 * kTraceSlots];
 __device__ __forceinline__ void trace_stamp(int ev) {
   unsigned long long t;
@@ -43,6 +43,13 @@ __device__ __forceinline__ void trace_stamp(int ev) {
   if (blockIdx.x < 2048) g_trace[blockIdx.x * kTraceSlots + ev] = t;
 }
 #define PGB_STAMP(ev) do { if (threadIdx.x == 0) trace_stamp(ev); } while (0)
+// first-item stamps (stager lane 0): a shared flag, not a read-back of
+// g_trace (a global load would add an L2 round trip to the stamped interval)
+__shared__ int g_trace_first;
+__shared__ int g_trace_item;   // items rendered so far (worker thread 0)
+__device__ __forceinline__ void trace_item(int phase) {
+  if (threadIdx.x == 0 && g_trace_item < 8) trace_stamp(16 + 3 * g_trace_item + phase);
+}
 #else
 #define PGB_STAMP(ev) do { } while (0)
 #endif
@@ -574,7 +581,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
   double mm = rint(dmul(dmul(ppp, (double)g.H), (double)g.W));
   mm = fmin(fmax(mm, 0.0), (double)P.n);
   const int M = (int)mm;
-  PGB_STAMP(11);
   int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
   unsigned short* cof = P.cell_of + (size_t)pl * cof_stride(P.n);
   // particle -> cell slots staged in shared memory behind the prefix, in
@@ -605,7 +611,6 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     if (one_win)
       for (int q = tid; q < (M8 >> 3); q += NTS) s4[q] = make_int4(0, 0, 0, 0);
     scan_sync<NTS>();
-    PGB_STAMP(10);
     if (P.pro_parts > 1) {
       // the histogram was drawn in parts by other CTAs (earlier tickets): sum them
       if (tid == 0) {
@@ -1256,22 +1261,39 @@ __device__ __forceinline__ void band_store(const BandParams& P, int* acc, int pl
 
 // Range of seeding cells [lo, hi] whose span [k*s, (k+1)*s) meets [a, b)
 // (inv = 1/s; the callers' bounds carry >= 1/2 px of slack, far above the
-// rounding of a*inv, so no division is needed on the staging path).
-__device__ __forceinline__ void cell_range(double a, double b, double inv, int n, int& lo, int& hi) {
-  const double fa = floor(fmax(a, 0.0) * inv);
-  const double fb = floor(fmin(b * inv, (double)n));
-  lo = (int)fmin(fa, (double)(n - 1));
-  hi = (int)fmin(fmax(fb, 0.0), (double)(n - 1));
+// float rounding of a*inv (< 1e-3 px for frames below 2^13 px), so no
+// division and no FP64 on the staging path: FP64 made the first item's
+// parameters a ~1 us dependent chain at every launch start).
+__device__ __forceinline__ void cell_range(float a, float b, float inv, int n, int& lo, int& hi) {
+  const float fa = floorf(fmaxf(a, 0.f) * inv);
+  const float fb = floorf(fminf(b * inv, (float)n));
+  lo = (int)fminf(fa, (float)(n - 1));
+  hi = (int)fminf(fmaxf(fb, 0.f), (float)(n - 1));
 }
 
 // Fixed-point shift without a division: the largest e <= kAccShift with
 // cnt * (amp 2^e + 1/2) <= 2^31 (the contributions of `cnt` particles of
-// amplitude <= amp, each rounded up by at most 1/2, fit an int32).
+// amplitude <= amp, each rounded up by at most 1/2, fit an int32). Float
+// arithmetic rounded upwards (products and sums, plus a 2^-20 margin): it
+// may give one bit less than the exact bound at the boundary, never more.
 __device__ __forceinline__ int shift_for_fast(int cnt, float amp) {
-  const double ca = (double)cnt * (double)amp;
-  int e = min(kAccShift, 31 - ilogb(ca));
-  while (e > 0 && dadd(ldexp(ca, e), 0.5 * (double)cnt) > 2147483648.0) --e;
+  const float ca = __fmul_ru(__fmul_ru(__int2float_ru(cnt), amp), 1.f + 0x1p-20f);
+  if (!(ca > 0.f)) return kAccShift;
+  int e = min(kAccShift, 31 - ilogbf(ca));
+  while (e > 0 && __fadd_ru(ldexpf(ca, e), __fmul_ru(0.5f, __int2float_ru(cnt))) > 2147483648.f) --e;
   return e;
+}
+
+// The parameters only the staging path reads, loaded once by the stager's
+// lane 0 at kernel entry (overlapping the first ticket's atomic): otherwise
+// their constant-cache misses are serial latency in the first item's staging.
+__device__ __forceinline__ void touch_stage_params(const BandParams& P) {
+  asm volatile("" ::"l"(P.split_base), "r"(P.split_s), "r"(P.tiles), "r"(P.tiles_x), "r"(P.TH), "r"(P.TW),
+               "r"(P.sy), "r"(P.sx), "d"(P.inv_ch), "d"(P.inv_cw), "f"(P.amp_bound), "r"(P.pairs_per_field),
+               "l"(P.pair_base), "l"(P.hdr), "l"(P.fbound), "l"(P.pair_ready));
+  asm volatile("" ::"l"(P.fb_done), "l"(P.prefix), "f"(P.g.f2_sigma_std), "d"(P.g.d_hi), "f"(P.g.inv_ratio),
+               "f"(P.g.rho_lo), "f"(P.g.rho_span), "f"(P.g.f2_rho_std), "r"(P.psf), "r"(P.rec_bytes),
+               "r"(P.pad_rows), "l"(P.total_items), "l"(P.npro), "r"(P.g.H));
 }
 
 // Item parameters (lane 0 of warp 0): tile, the cells whose particles can reach
@@ -1315,6 +1337,9 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
       ns = min(ns * 2, 256);
     }
   }
+#ifdef PGB_TRACE
+  if (g_trace_first == 0) trace_stamp(10);
+#endif
   {
     // header and field bound loaded together
     const int4* src = reinterpret_cast<const int4*>(P.hdr + pl);
@@ -1326,7 +1351,17 @@ __device__ __forceinline__ void item_setup(const BandParams& P, long long item, 
 #pragma unroll
     for (int k = 0; k < (int)(sizeof(PairHdr) / 16); ++k) dst[k] = t[k];
   }
+#ifdef PGB_TRACE
+  // (conditioned on the loaded data so the stamp waits for the loads)
+  if (g_trace_first == 0 && ic.hd.M >= -1 && ic.fb.x > -1.f) trace_stamp(11);
+#endif
   item_finish(P, ic);
+#ifdef PGB_TRACE
+  if (g_trace_first == 0 && ic.shift >= 0 && ic.cy1 >= -1 && ic.cx1 >= -1 && ic.var >= 0) {
+    trace_stamp(15);
+    g_trace_first = 1;
+  }
+#endif
 }
 
 // Item parameters from the tile, the pair header (ic.hd) and the field bound:
@@ -1341,16 +1376,17 @@ __device__ __forceinline__ void item_finish(const BandParams& P, ItemCfg& ic) {
   // frame-1 positions that can reach the tile in either frame: anchors within
   // h of the tile (frame 1), or within h + 1 + max|v| (frame 2: the anchor
   // moves by floor(f + v + 1/2), |f| <= 1/2); slack covers float rounding.
-  const double vy = (double)fb.y * (1.0 + 1e-6) + 1e-6;
-  const double vx = (double)fb.x * (1.0 + 1e-6) + 1e-6;
-  cell_range((double)ic.r0 - h - 1.5 - vy, (double)ic.r1 + h + 0.5 + vy, P.inv_ch, CY, ic.cy0, ic.cy1);
-  cell_range((double)ic.c0 - h - 1.5 - vx, (double)ic.c1 + h + 0.5 + vx, P.inv_cw, CX, ic.cx0, ic.cx1);
+  const float vy = __fmaf_ru(fb.y, 1.f + 1e-6f, 1e-6f);
+  const float vx = __fmaf_ru(fb.x, 1.f + 1e-6f, 1e-6f);
+  const float inv_ch = (float)P.inv_ch, inv_cw = (float)P.inv_cw;
+  cell_range((float)(ic.r0 - h) - 1.5f - vy, (float)(ic.r1 + h) + 0.5f + vy, inv_ch, CY, ic.cy0, ic.cy1);
+  cell_range((float)(ic.c0 - h) - 1.5f - vx, (float)(ic.c1 + h) + 0.5f + vx, inv_cw, CX, ic.cx0, ic.cx1);
   // fixed-point shift: contributions per pixel <= cmax * (cells one pixel's
-  // source box can meet), amplitude <= amp_bound (the 1e-9 keeps the floor
-  // of an exact quotient from rounding down)
-  const double by = floor((2.0 * h + 3.0 + 2.0 * vy) * P.inv_ch + 1e-9) + 2.0;
-  const double bx = floor((2.0 * h + 3.0 + 2.0 * vx) * P.inv_cw + 1e-9) + 2.0;
-  const double cov = fmin((double)ic.hd.M, (double)ic.hd.cmax * fmin(by, (double)CY) * fmin(bx, (double)CX));
+  // source box can meet), amplitude <= amp_bound (the 1e-4 keeps the floor
+  // of an exact quotient from rounding down; a larger bound is only safer)
+  const int by = (int)floorf(__fmaf_ru(2.f * vy + (float)(2 * h + 3), inv_ch, 1e-4f)) + 2;
+  const int bx = (int)floorf(__fmaf_ru(2.f * vx + (float)(2 * h + 3), inv_cw, 1e-4f)) + 2;
+  const long long cov = min((long long)ic.hd.M, (long long)ic.hd.cmax * min(by, CY) * min(bx, CX));
   ic.shift = shift_for_fast(max(1, (int)cov), P.amp_bound);
   // window side bound: floor(2 R_max) + 1 columns/rows, R_max from the largest
   // sigma (frame-2 sigma jitter is unbounded -> patch side)
@@ -1893,11 +1929,21 @@ __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh,
       default: band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1); break;
     }
   }
+#ifdef PGB_TRACE
+  trace_item(0);
+#endif
   __syncthreads();   // particles done (stager: next item staged)
+#ifdef PGB_TRACE
+  trace_item(1);
+#endif
   const float inv_scale = 1.0f / scale;
   band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
   band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
   __syncthreads();   // accumulators zeroed
+#ifdef PGB_TRACE
+  trace_item(2);
+  if (threadIdx.x == 0) ++g_trace_item;
+#endif
 }
 
 // SORT = 1: the body for plans with a record region (large windows), in a
@@ -1924,6 +1970,14 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
       for (int e = tid; e < kSortClasses * 32; e += kBandThreads) ss->cnt[e] = 0;
   };
   PGB_STAMP(0);
+#ifdef PGB_TRACE
+  if (tid == 0) {
+    g_trace_first = 0, g_trace_item = 0;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (blockIdx.x < 2048) g_trace[blockIdx.x * kTraceSlots + 39] = smid + 1;
+  }
+#endif
   if (blockIdx.x == gridDim.x - 1 && P.zero_head)
     for (int e = tid; e < P.zero_head_n; e += kBandBlock) P.zero_head[e] = make_int4(0, 0, 0, 0);
   // One ticket sequence: [0, npro) prologue items (the flow-bound chunks,
@@ -1936,6 +1990,7 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
   const int nfc = P.field_cnt * kFieldBlocks;
   long long first;
   if (tid == 0) sh->ticket0 = atomicAdd(P.ticket, 1);
+  if (tid == kBandThreads) touch_stage_params(P);
   __syncthreads();
   first = sh->ticket0;
   for (;;) {

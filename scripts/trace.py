@@ -21,10 +21,10 @@ import paper_2512_09664_b200 as pg  # noqa: E402
 from paper_2512_09664_b200 import _lib  # noqa: E402
 from paper_2512_09664_b200.particles import native_config  # noqa: E402
 
-SLOTS = 16
+SLOTS = 40
 NAMES = ["entry", "field_chunk_done", "pro_start", "pro_hist", "pro_sums", "pro_prefix", "pro_maxscan",
-         "pro_released", "pro_loop_done", "item1_staged", "pro_zeroed", "pro_M", "exit", "(items)", "pro_f64_chain",
-         "owned_fb_ok"]
+         "pro_released", "pro_loop_done", "item1_staged", "stage_polled", "stage_loaded", "exit", "(items)", "pro_f64_chain",
+         "stage_finished"]
 
 
 def main():
@@ -51,8 +51,22 @@ def main():
     for k in range(5):
         step(k)
     torch.cuda.synchronize()
+    if os.environ.get("TRACE_NOFLUSH"):
+        step(8)   # the previous launch leaves code, flow and tables in L2
+        torch.cuda.synchronize()
+    else:
+        flush.zero_()
+        if os.environ.get("TRACE_CODEWARM"):
+            # one single-pair launch after the flush: kernel code back in L2
+            _lib.check(lib.pgb_generate_batch_dev(ncfg, 7, 0, 1, flows.data_ptr(), 1, B, _lib.OUT_F32,
+                                                  img1.data_ptr(), img2.data_ptr(), None, None,
+                                                  stream.cuda_stream))
+            torch.cuda.synchronize()
+        if os.environ.get("TRACE_IDLE"):
+            # idle gap after the flush (no launch): does the L2 drain its dirty lines?
+            torch.cuda._sleep(int(os.environ["TRACE_IDLE"]))
+            torch.cuda.synchronize()
     lib.pgb_trace_clear()
-    flush.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     step(9)
@@ -77,6 +91,40 @@ def main():
               f"max {r.max():7.2f} us")
     items = t[:, 13]
     print(f"  items per CTA: min {items.min()} med {np.median(items)} max {items.max()}")
+    # per-item phases (worker thread 0): own particles done, all particles
+    # done (barrier), store done
+    for k in range(8):
+        c = t[:, 16 + 3 * k:19 + 3 * k]
+        ok = c[:, 2] > 0
+        if not ok.any():
+            break
+        c = (c[ok] - t0) / 1e3
+        print(f"  item {k}: n={ok.sum():4d}  splat_end med {np.median(c[:, 0]):6.2f}  barrier med "
+              f"{np.median(c[:, 1]):6.2f}  store_end med {np.median(c[:, 2]):6.2f} (min {c[:, 2].min():6.2f} max "
+              f"{c[:, 2].max():6.2f})  bar-wait med {np.median(c[:, 1] - c[:, 0]):5.2f}  store med "
+              f"{np.median(c[:, 2] - c[:, 1]):5.2f} us")
+    # SM co-residents (slot 39 = smid + 1): how much of a CTA's store phases
+    # overlap its neighbour's store phases
+    sm = t[:, 39] - 1
+    ov, tot = 0.0, 0.0
+    for s_ in np.unique(sm):
+        idx = np.where(sm == s_)[0]
+        if len(idx) != 2:
+            continue
+        ph = []
+        for i in idx:
+            iv = []
+            for k in range(8):
+                a, b = t[i, 17 + 3 * k], t[i, 18 + 3 * k]
+                if b > 0:
+                    iv.append((a, b))
+            ph.append(iv)
+        for a, b in ph[0]:
+            tot += b - a
+            for c, d in ph[1]:
+                ov += max(0, min(b, d) - max(a, c))
+    if tot > 0:
+        print(f"  store phases of SM co-residents overlapping: {100 * ov / tot:.0f} %")
     pro = (t[:, 2] > 0) & (t[:, 7] > 0)
     if pro.any():
         d = (t[pro][:, 3:8] - t[pro][:, 2:7]) / 1e3
