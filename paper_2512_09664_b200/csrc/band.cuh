@@ -1225,23 +1225,31 @@ __device__ __forceinline__ void band_store_scalar(const BandParams& P, int* __re
   }
 }
 
+// Full-width tiles are stored by the whole block (the staging warp joins: it
+// has staged the next item by then); other tiles by the worker warps.
+__device__ __forceinline__ bool store_is_lin(const BandParams& P, int c0, int nc) {
+  return ((nc & 3) == 0) && ((P.W & 3) == 0) && c0 == 0 && nc == P.W && P.AS == P.W;
+}
+
 __device__ __forceinline__ void band_store(const BandParams& P, int* acc, int pl, int f, int r0, int nr, int c0, int nc,
                            float inv_scale) {
   const bool vec = ((nc & 3) == 0) && ((P.W & 3) == 0) && ((c0 & 3) == 0);
   const bool noise = P.noise_std > 0.f;
-  if (vec && c0 == 0 && nc == P.W && P.AS == P.W) {
+  if (store_is_lin(P, c0, nc)) {
+    const int t = threadIdx.x, nt = kBandBlock;
     switch (P.out_mode) {
-      case kOutRaw: band_store_lin<kOutRaw, false>(P, acc, pl, f, r0, nr, inv_scale); return;
+      case kOutRaw: band_store_lin<kOutRaw, false>(P, acc, pl, f, r0, nr, inv_scale, t, nt); return;
       case kOutF32:
-        if (noise) band_store_lin<kOutF32, true>(P, acc, pl, f, r0, nr, inv_scale);
-        else band_store_lin<kOutF32, false>(P, acc, pl, f, r0, nr, inv_scale);
+        if (noise) band_store_lin<kOutF32, true>(P, acc, pl, f, r0, nr, inv_scale, t, nt);
+        else band_store_lin<kOutF32, false>(P, acc, pl, f, r0, nr, inv_scale, t, nt);
         return;
       default:
-        if (noise) band_store_lin<kOutU16, true>(P, acc, pl, f, r0, nr, inv_scale);
-        else band_store_lin<kOutU16, false>(P, acc, pl, f, r0, nr, inv_scale);
+        if (noise) band_store_lin<kOutU16, true>(P, acc, pl, f, r0, nr, inv_scale, t, nt);
+        else band_store_lin<kOutU16, false>(P, acc, pl, f, r0, nr, inv_scale, t, nt);
         return;
     }
   }
+  if (threadIdx.x >= kBandThreads) return;
   if (vec) {
     switch (P.out_mode) {
       case kOutRaw: band_store_vec<kOutRaw, false>(P, acc, pl, f, r0, nr, c0, nc, inv_scale); return;
@@ -1913,10 +1921,10 @@ __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh,
                                             int* acc0, int* acc1) {
   const ItemCfg& ic = sh->ic[buf];
   const long long item = ic.item;
-  const int pl = ic.pl;
-  const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
-  const float scale = (float)(1 << ic.shift);
-  if constexpr (PSF == kPsfErf) {
+  if (threadIdx.x >= kBandThreads) {
+    // staging warp: the next item, then the store of this one (below)
+    stage_next(P, sh, buf ^ 1, -1);
+  } else if constexpr (PSF == kPsfErf) {
     band_particles<PSF, 0, 0>(P, sh, buf, item, acc0, acc1);
   } else {
     switch (ic.var) {
@@ -1936,7 +1944,9 @@ __device__ __forceinline__ void render_item(const BandParams& P, BandShared* sh,
 #ifdef PGB_TRACE
   trace_item(1);
 #endif
-  const float inv_scale = 1.0f / scale;
+  const int pl = ic.pl;
+  const int r0 = ic.r0, r1 = ic.r1, c0 = ic.c0, c1 = ic.c1;
+  const float inv_scale = 1.0f / (float)(1 << ic.shift);
   band_store(P, acc0, pl, 0, r0, r1 - r0, c0, c1 - c0, inv_scale);
   band_store(P, acc1, pl, 1, r0, r1 - r0, c0, c1 - c0, inv_scale);
   __syncthreads();   // accumulators zeroed
@@ -2033,12 +2043,6 @@ __device__ __forceinline__ void band_body(const BandParams& P) {
 #ifdef PGB_TRACE
     ++nitems;
 #endif
-    if (stager) {
-      stage_next(P, sh, buf ^ 1, -1);
-      __syncthreads();   // particles done
-      __syncthreads();   // store done
-      continue;
-    }
     render_item<PSF, SORT>(P, sh, ss, buf, acc0, acc1);
   }
   PGB_STAMP(12);
