@@ -618,14 +618,28 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
         while (ld_acquire_b(P.part_done + pl) < P.pro_parts) { __nanosleep(ns); ns = min(ns * 2, 256); }
       }
       scan_sync<NTS>();
+      // (all loads of four rows x up to four parts in flight: a dependent
+      // loop over parts was one L2 round trip per row, ~10 us at C3)
       const int4* pc = reinterpret_cast<const int4*>(P.part_counts + (size_t)pl * P.pro_parts * ncell);
-      for (int i = tid; i < nq4; i += NTS) {
-        int4 t = make_int4(0, 0, 0, 0);
-        for (int k = 0; k < P.pro_parts; ++k) {
-          const int4 v = __ldcg(pc + (size_t)k * (ncell >> 2) + i);
-          t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+      const int K = P.pro_parts;
+      for (int i0 = tid; i0 < nq4; i0 += 4 * NTS) {
+        int4 v[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int i = i0 + j * NTS;
+            v[j][k] = (i < nq4 && k < K) ? __ldcg(pc + (size_t)k * (ncell >> 2) + i) : make_int4(0, 0, 0, 0);
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + j * NTS;
+          const int4 t = make_int4(v[j][0].x + v[j][1].x + v[j][2].x + v[j][3].x,
+                                   v[j][0].y + v[j][1].y + v[j][2].y + v[j][3].y,
+                                   v[j][0].z + v[j][1].z + v[j][2].z + v[j][3].z,
+                                   v[j][0].w + v[j][1].w + v[j][2].w + v[j][3].w);
+          if (i < nq4) bins4[i] = t;
         }
-        bins4[i] = t;
       }
     } else {
       hist_labels<NTS>(g, key, M, L, bins, 0, (M + 3) >> 2);
@@ -792,8 +806,19 @@ __device__ __forceinline__ void pair_fill_window(const BandParams& P, int pl, in
   const int M = sM, M8 = (M + 7) & ~7;
   const int s0 = w * P.fill_win, s1 = min(M8, s0 + P.fill_win);
   if (s0 < s1) {
+    // the prefix row (ncell + 4 ints, 16-byte aligned) as int4s, eight loads
+    // in flight per thread (one dependent L2 round trip per int was ~10 us
+    // of the C3 start-up chain)
     const int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
-    for (int i = tid; i <= ncell; i += NT) bins[i] = __ldcg(pre + i);
+    if ((ncell & 3) == 0) {
+      const int4* pre4 = reinterpret_cast<const int4*>(pre);
+      int4* b4 = reinterpret_cast<int4*>(bins);
+      const int n4 = (int)(pre_stride(ncell) >> 2);
+#pragma unroll 8
+      for (int i = tid; i < n4; i += NT) b4[i] = __ldcg(pre4 + i);
+    } else {
+      for (int i = tid; i <= ncell; i += NT) bins[i] = __ldcg(pre + i);
+    }
     __syncthreads();
     const int soff = ((nc4 + 4) & ~3) * 4;
     unsigned short* scof = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(bins) + soff);

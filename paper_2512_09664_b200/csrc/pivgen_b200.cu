@@ -656,7 +656,8 @@ void band_prologue(BandParams& P, const BandPlan& bp, const pgb_config* cfg, uin
   if (!standalone) {
     const long long nq = ((long long)cfg->n_capacity + 3) / 4;
     const long long kparts = std::getenv("PGB_PRO_PARTS") ? std::atoll(std::getenv("PGB_PRO_PARTS")) : 4;
-    parts = (int)std::max<long long>(1, std::min<long long>(kparts, nq / 4096));
+    // (<= 4: the prologue sums the parts with all four loads in flight)
+    parts = (int)std::max<long long>(1, std::min<long long>(std::min(kparts, 4LL), nq / 4096));
     const long long soff = ((long long)((std::max(ncell, 4) + 4) & ~3)) * 4;
     const long long pro_smem = (long long)bp.smem - (long long)sizeof(BandShared);
     const long long win = std::max<long long>(8, std::min<long long>(128 * 256, ((pro_smem - soff) / 2) & ~7LL));
