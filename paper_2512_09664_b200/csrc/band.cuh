@@ -35,7 +35,7 @@ namespace pgb {
 // Timing probes (build with -DPGB_TRACE only; scripts/trace.py reads them):
 // globaltimer stamps per CTA, slot = blockIdx.x * kTraceSlots + event.
 #ifdef PGB_TRACE
-constexpr int kTraceSlots = 40;   // 0-15 events, 16 + 3k.. item k phases (k < 8)
+constexpr int kTraceSlots = 40;   // 0-15 events, 16 + 3k.. item k phases (k < 6), 34-38 part/window events, 39 smid
 __device__ unsigned long long g_trace[2048 * kTraceSlots];
 __device__ __forceinline__ void trace_stamp(int ev) {
   unsigned long long t;
@@ -48,7 +48,7 @@ __device__ __forceinline__ void trace_stamp(int ev) {
 __shared__ int g_trace_first;
 __shared__ int g_trace_item;   // items rendered so far (worker thread 0)
 __device__ __forceinline__ void trace_item(int phase) {
-  if (threadIdx.x == 0 && g_trace_item < 8) trace_stamp(16 + 3 * g_trace_item + phase);
+  if (threadIdx.x == 0 && g_trace_item < 6) trace_stamp(16 + 3 * g_trace_item + phase);
 }
 #else
 #define PGB_STAMP(ev) do { } while (0)
@@ -775,10 +775,12 @@ __device__ __forceinline__ void pair_hist_part(const BandParams& P, int pl, int 
   const int nq = (M + 3) >> 2;
   const int K = P.pro_parts;
   int4* bins4 = reinterpret_cast<int4*>(bins);
+  PGB_STAMP(34);
   for (int i = tid; i < (ncell >> 2); i += NT) bins4[i] = make_int4(0, 0, 0, 0);
   __syncthreads();
   if (tid < NTS) hist_labels<NTS>(g, key, M, L, bins, (int)((long long)nq * k / K), (int)((long long)nq * (k + 1) / K));
   __syncthreads();
+  PGB_STAMP(35);
   int4* dst = reinterpret_cast<int4*>(P.part_counts + ((size_t)pl * K + k) * ncell);
   for (int i = tid; i < (ncell >> 2); i += NT) dst[i] = bins4[i];
   __syncthreads();
@@ -786,6 +788,7 @@ __device__ __forceinline__ void pair_hist_part(const BandParams& P, int pl, int 
     __threadfence();
     atomicAdd(P.part_done + pl, 1);
   }
+  PGB_STAMP(36);
 }
 
 // Particle -> cell window w of pair pl (fill_wins > 0; whole block, the scan
@@ -803,6 +806,7 @@ __device__ __forceinline__ void pair_fill_window(const BandParams& P, int pl, in
     sM = __ldcg(&P.hdr[pl].M);
   }
   __syncthreads();
+  PGB_STAMP(37);
   const int M = sM, M8 = (M + 7) & ~7;
   const int s0 = w * P.fill_win, s1 = min(M8, s0 + P.fill_win);
   if (s0 < s1) {
@@ -811,11 +815,25 @@ __device__ __forceinline__ void pair_fill_window(const BandParams& P, int pl, in
     // of the C3 start-up chain)
     const int* pre = P.prefix + (size_t)pl * pre_stride(ncell);
     if ((ncell & 3) == 0) {
+      // loads first, then the shared stores: interleaved, the compiler cannot
+      // move a load above the previous (possibly aliasing) store, and every
+      // row costs a full L2 round trip (measured 9 us per C3 window)
       const int4* pre4 = reinterpret_cast<const int4*>(pre);
       int4* b4 = reinterpret_cast<int4*>(bins);
       const int n4 = (int)(pre_stride(ncell) >> 2);
-#pragma unroll 8
-      for (int i = tid; i < n4; i += NT) b4[i] = __ldcg(pre4 + i);
+      for (int i0 = tid; i0 < n4; i0 += 8 * NT) {
+        int4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = i0 + j * NT;
+          v[j] = i < n4 ? __ldcg(pre4 + i) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = i0 + j * NT;
+          if (i < n4) b4[i] = v[j];
+        }
+      }
     } else {
       for (int i = tid; i <= ncell; i += NT) bins[i] = __ldcg(pre + i);
     }
@@ -833,6 +851,7 @@ __device__ __forceinline__ void pair_fill_window(const BandParams& P, int pl, in
       st_release(P.pair_ready + pl, 1);
     }
   }
+  PGB_STAMP(38);
 }
 
 // Standalone prologue (sample_particles path): one CTA per pair + kFieldBlocks

@@ -6,7 +6,8 @@
 Events (globaltimer ns, relative to the earliest kernel-entry stamp):
  0 entry, 1 first ticket, 2-7 pair prologue (start, histogram, chunk sums,
  prefix+marks, max-scan, released), 8 prologue loop done, 9 first item staged,
- 10 first item particles done, 11 first item stored, 12 exit, 13 items.
+ 10 first item particles done, 11 first item stored, 12 exit, 13 items,
+34-38 histogram part / cell window events (last one per CTA).
 """
 import ctypes
 import os
@@ -25,6 +26,7 @@ SLOTS = 40
 NAMES = ["entry", "field_chunk_done", "pro_start", "pro_hist", "pro_sums", "pro_prefix", "pro_maxscan",
          "pro_released", "pro_loop_done", "item1_staged", "stage_polled", "stage_loaded", "exit", "(items)", "pro_f64_chain",
          "stage_finished"]
+EXTRA = {34: "part_start", 35: "part_labels", 36: "part_published", 37: "window_go", 38: "window_done"}
 
 
 def main():
@@ -89,11 +91,18 @@ def main():
         r = (col[ok] - t0) / 1e3
         print(f"  {ev:2d} {nm:16s} n={ok.sum():4d}  min {r.min():7.2f}  med {np.median(r):7.2f}  "
               f"max {r.max():7.2f} us")
+    for ev, nm in EXTRA.items():
+        col = t[:, ev]
+        ok = col > 0
+        if ok.any():
+            r = (col[ok] - t0) / 1e3
+            print(f"  {ev:2d} {nm:16s} n={ok.sum():4d}  min {r.min():7.2f}  med {np.median(r):7.2f}  "
+                  f"max {r.max():7.2f} us")
     items = t[:, 13]
     print(f"  items per CTA: min {items.min()} med {np.median(items)} max {items.max()}")
     # per-item phases (worker thread 0): own particles done, all particles
     # done (barrier), store done
-    for k in range(8):
+    for k in range(6):
         c = t[:, 16 + 3 * k:19 + 3 * k]
         ok = c[:, 2] > 0
         if not ok.any():
@@ -114,7 +123,7 @@ def main():
         ph = []
         for i in idx:
             iv = []
-            for k in range(8):
+            for k in range(6):
                 a, b = t[i, 17 + 3 * k], t[i, 18 + 3 * k]
                 if b > 0:
                     iv.append((a, b))
