@@ -747,12 +747,12 @@ __device__ __forceinline__ void pair_prologue(const BandParams& P, int pl, int* 
     hd.cmax = scm;
     P.hdr[pl] = hd;
     write_stats(P, pl, hd);
-  }
-  __syncthreads();
-  if (tid == 0 && P.pair_ready) {
-    __threadfence();
-    // particle -> cell windows on other CTAs: they release the pair
-    st_release(P.fill_wins ? P.pre_ready + pl : P.pair_ready + pl, 1);
+    // The block's prefix / particle -> cell writes are ordered before this
+    // thread by the barrier above, its own header write by program order; a
+    // release store is cumulative over both (the bar.sync + st.release.gpu
+    // publish pattern), so no separate fence. Particle -> cell windows on
+    // other CTAs release the pair when there are any.
+    if (P.pair_ready) st_release(P.fill_wins ? P.pre_ready + pl : P.pair_ready + pl, 1);
   }
   PGB_STAMP(7);
 }
